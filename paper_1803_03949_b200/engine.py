@@ -1,0 +1,229 @@
+"""Frame-by-frame reconstruction driver (mirror of reference pkg/src/voxmesh/engine.py).
+
+``Engine.fuse_frame`` is ONE C-ABI call (``vm_fuse_frame``): depth upload,
+then the whole per-frame kernel sequence on the device (collect -> integrate
+-> scope/halo -> retype(+refine) -> place -> triangulate -> GC -> normals), and
+a D2H read of the StatsRow counters.  The non-timing StatsRow columns match
+the reference exactly; ``fusion_ms`` / ``meshing_ms`` are device times (CUDA
+events) of the same two segments the reference times on the host.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import time
+from dataclasses import dataclass, replace
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .errors import ConsistencyError
+from .fusion import Intrinsics, Pose
+from .mesher import STRATEGIES
+from .refine import REGULAR_TYPES, RefineParams
+from .store import CompactMesh, SpatialStore
+
+
+@dataclass
+class RunConfig:
+    cube_size: float = 0.03
+    trunc: Optional[float] = None        # defaults to 3 * cube_size
+    epsilon: float = 0.1
+    refine: bool = False
+    strategy: str = "claim"
+    baseline: bool = False
+    max_range: float = 5.0
+    frustum_only: bool = False
+    workers: int = 0                     # accepted for API parity; the GPU ignores it
+    seed: int = 0
+    weight_cap: int = 128
+    max_vertices: Optional[int] = None
+    table_size: int = 1 << 20
+    # device arena capacity hints (0 = defaults; arenas grow on demand)
+    block_capacity: int = 0
+    vertex_capacity: int = 0
+    triangle_capacity: int = 0
+
+    def resolved(self) -> "RunConfig":
+        cfg = replace(self)
+        if cfg.trunc is None:
+            cfg.trunc = 3.0 * cfg.cube_size
+        if cfg.trunc < cfg.cube_size:
+            raise ValueError("truncation band must be at least one cube")
+        if cfg.workers <= 0:
+            cfg.workers = os.cpu_count() or 1
+        if cfg.strategy not in STRATEGIES:
+            raise ValueError(f"unknown strategy {cfg.strategy!r}")
+        return cfg
+
+    def to_dict(self) -> dict:
+        return {k: getattr(self, k) for k in (
+            "cube_size", "trunc", "epsilon", "refine", "strategy", "baseline", "max_range",
+            "frustum_only", "workers", "seed", "weight_cap")}
+
+
+@dataclass
+class StatsRow:
+    frame: int
+    blocks_active: int
+    vertices_live: int
+    triangles_live: int
+    vertices_allocated_total: int
+    vertices_recycled_total: int
+    irregular_cube_count: int
+    fusion_ms: float
+    meshing_ms: float
+    compact_ms: float
+
+    FIELDS = ("frame", "blocks_active", "vertices_live", "triangles_live",
+              "vertices_allocated_total", "vertices_recycled_total",
+              "irregular_cube_count", "fusion_ms", "meshing_ms", "compact_ms")
+
+
+@dataclass
+class AuditReport:
+    vertices_live: int
+    triangles_live: int
+    refcount_mismatches: int
+    duplicate_handles: int
+    zero_ref_live: int
+    conservation_ok: bool
+
+    @property
+    def ok(self) -> bool:
+        return (self.refcount_mismatches == 0 and self.duplicate_handles == 0
+                and self.zero_ref_live == 0 and self.conservation_ok)
+
+
+_REGULAR_MASK = np.zeros(256, dtype=bool)
+_REGULAR_MASK[list(REGULAR_TYPES)] = True
+
+
+def _is_device_tensor(x) -> bool:
+    return hasattr(x, "data_ptr") and getattr(x, "is_cuda", False)
+
+
+class Engine:
+    def __init__(self, config: RunConfig, intrinsics: Intrinsics, audit_every_frame: bool = False):
+        self.config = config.resolved()
+        self.intrinsics = intrinsics
+        c = self.config
+        self.store = SpatialStore(c.cube_size, table_size=c.table_size,
+                                  max_vertices=c.max_vertices, initial_blocks=c.block_capacity,
+                                  initial_vertices=c.vertex_capacity,
+                                  initial_triangles=c.triangle_capacity)
+        self.frame_index = 0
+        self.stats: list[StatsRow] = []
+        self.device_stats: list[dict] = []
+        self.audit_every_frame = audit_every_frame
+        self._intr_c = _lib.intr_c(intrinsics)
+        self._fcfg = _lib.FrameConfig(float(c.trunc), float(c.max_range), float(c.epsilon),
+                                      int(c.weight_cap), int(bool(c.refine)),
+                                      int(bool(c.frustum_only)), _lib.STRATEGY_CODES[c.strategy], 0)
+        self._collected_n = 0
+        self._collected_cache = None
+
+    # -- per-frame pipeline ---------------------------------------------------
+    def _depth_args(self, depth):
+        if _is_device_tensor(depth):
+            import torch
+            if depth.dtype != torch.float64 or not depth.is_contiguous() or depth.dim() != 2:
+                raise ValueError("device depth must be a contiguous 2-D float64 CUDA tensor")
+            return C.c_void_p(depth.data_ptr()), depth.shape[0], depth.shape[1], 1, None
+        d = np.ascontiguousarray(np.asarray(depth, dtype=np.float64))
+        if d.ndim != 2:
+            raise ValueError("depth must be a 2-D array")
+        return _lib.ptr(d), d.shape[0], d.shape[1], 0, d
+
+    def fuse_frame(self, depth, pose: Pose) -> StatsRow:
+        ptr, h, w, on_dev, keep = self._depth_args(depth)
+        st = _lib.Stats()
+        self.store._touch()
+        _lib.check(_lib.load().vm_fuse_frame(self.store._h, ptr, h, w, on_dev,
+                                              C.byref(self._intr_c), C.byref(_lib.pose_c(pose)),
+                                              C.byref(self._fcfg), self.frame_index, C.byref(st)))
+        del keep
+        return self._record(st)
+
+    def fuse_frame_enqueue(self, depth, pose: Pose):
+        """Split form for device timing: enqueue only (see vm_fuse_frame_enqueue)."""
+        ptr, h, w, on_dev, keep = self._depth_args(depth)
+        self.store._touch()
+        _lib.check(_lib.load().vm_fuse_frame_enqueue(self.store._h, ptr, h, w, on_dev,
+                                                      C.byref(self._intr_c),
+                                                      C.byref(_lib.pose_c(pose)),
+                                                      C.byref(self._fcfg), self.frame_index))
+        return keep
+
+    def fuse_frame_finish(self) -> StatsRow:
+        st = _lib.Stats()
+        _lib.check(_lib.load().vm_fuse_frame_finish(self.store._h, C.byref(st)))
+        return self._record(st)
+
+    def _record(self, st) -> StatsRow:
+        d = st.as_dict()
+        self.device_stats.append(d)
+        self._collected_n = d["collected_blocks"]
+        self._collected_cache = None
+        row = StatsRow(frame=self.frame_index, blocks_active=d["blocks_active"],
+                       vertices_live=d["vertices_live"], triangles_live=d["triangles_live"],
+                       vertices_allocated_total=d["vertices_allocated_total"],
+                       vertices_recycled_total=d["vertices_recycled_total"],
+                       irregular_cube_count=d["irregular_cube_count"],
+                       fusion_ms=d["fusion_ms"], meshing_ms=d["meshing_ms"], compact_ms=0.0)
+        self.stats.append(row)
+        self.frame_index += 1
+        if self.audit_every_frame:
+            report = self.audit()
+            if not report.ok:
+                raise ConsistencyError(f"frame {row.frame} audit failed: {report}")
+        return row
+
+    @property
+    def last_collected(self) -> list:
+        if self._collected_cache is None:
+            n = self._collected_n
+            out = np.zeros((n, 3), np.int32)
+            if n:
+                _lib.check(_lib.load().vm_get_collected(self.store._h, _lib.ptr(out), n))
+            self._collected_cache = sorted((int(a), int(b), int(c)) for a, b, c in out)
+        return self._collected_cache
+
+    # -- derived quantities -----------------------------------------------------
+    def irregular_cube_count(self) -> int:
+        """engine.py:169-176 as a full device scan."""
+        return self.store.irregular_cube_count()
+
+    def compact(self) -> CompactMesh:
+        t0 = time.perf_counter()
+        mesh = self.store.compact_mesh(self.frame_index)
+        if self.stats:
+            self.stats[-1].compact_ms = (time.perf_counter() - t0) * 1e3
+        return mesh
+
+    def audit(self) -> AuditReport:
+        """engine.py:187-230 as device reductions."""
+        a = _lib.AuditC()
+        _lib.check(_lib.load().vm_audit(self.store._h, C.byref(a)))
+        return AuditReport(vertices_live=int(a.vertices_live), triangles_live=int(a.triangles_live),
+                           refcount_mismatches=int(a.refcount_mismatches),
+                           duplicate_handles=int(a.duplicate_handles),
+                           zero_ref_live=int(a.zero_ref_live),
+                           conservation_ok=bool(a.conservation_ok))
+
+    def set_profiling(self, on: bool = True) -> None:
+        _lib.check(_lib.load().vm_set_profiling(self.store._h, int(bool(on))))
+
+    def phase_times(self) -> dict:
+        """Per-kernel device ms of the last frame (requires set_profiling)."""
+        ms = np.zeros(12)
+        _lib.check(_lib.load().vm_phase_times(self.store._h, _lib.ptr(ms), 12))
+        return dict(zip(PHASES, (float(v) for v in ms)))
+
+    def set_stream(self, stream_handle: int) -> None:
+        _lib.check(_lib.load().vm_set_stream(self.store._h, C.c_void_p(stream_handle or None)))
+
+
+PHASES = ("depth_stats", "collect", "init_blocks", "integrate", "scope_halo", "retype", "place",
+          "tri_release", "tri_alloc", "gc", "normals", "fallback")

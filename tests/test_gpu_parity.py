@@ -1,0 +1,189 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's own
+golden fixtures and against the CPU oracle on identical inputs.
+
+Bit-exact: block sets, TSDF and weights, cube types, triangle topology (compact
+indices), vertex positions and ages, StatsRow non-timing columns.  Normals are
+also expected bit-exact (the fallback reproduces the reference's summation
+order); the written tolerance is 1e-12 (unit vectors).
+"""
+import numpy as np
+import pytest
+
+from conftest import ENGINE_SCENES, FIELD_SCENES, cfg_from_golden, load_golden
+
+pytestmark = pytest.mark.gpu
+
+NORMAL_ATOL = 1e-12
+
+
+def _engine_from_golden(g, **over):
+    from paper_1803_03949_b200 import Engine, Intrinsics, RunConfig
+    cfg = cfg_from_golden(g)
+    cfg.update(over)
+    i6 = g["intr6"]
+    intr = Intrinsics(float(i6[0]), float(i6[1]), float(i6[2]), float(i6[3]), int(i6[4]), int(i6[5]))
+    return Engine(RunConfig(**cfg), intr)
+
+
+def _pose(g, i):
+    from paper_1803_03949_b200 import Pose
+    return Pose(g["rot"][i], g["trans"][i])
+
+
+def _stats_tuple(row):
+    return (row.frame, row.blocks_active, row.vertices_live, row.triangles_live,
+            row.vertices_allocated_total, row.vertices_recycled_total, row.irregular_cube_count)
+
+
+def _check_blocks(store, g):
+    blocks = list(store.blocks())
+    coords = np.array([b.coord for b in blocks], np.int32).reshape(-1, 3)
+    assert np.array_equal(coords, g["coords"])
+    for k in ("tsdf", "weight", "type_prev", "type_curr"):
+        got = np.stack([getattr(b, k) for b in blocks]) if blocks else np.zeros((0,))
+        assert np.array_equal(got, g[k]), k
+    # slot occupancy pattern (handles differ: GPU allocation order is free)
+    ev = np.stack([b.edge_vertex for b in blocks])
+    tr = np.stack([b.triangles for b in blocks])
+    assert np.array_equal(ev >= 0, g["edge_vertex"] >= 0)
+    assert np.array_equal(tr >= 0, g["triangles"] >= 0)
+
+
+def _check_mesh(mesh, g):
+    assert np.array_equal(mesh.indices, g["m_indices"])
+    assert np.array_equal(mesh.positions, g["m_positions"])
+    assert np.array_equal(mesh.ages, g["m_ages"])
+    assert np.allclose(mesh.normals, g["m_normals"], rtol=0, atol=NORMAL_ATOL)
+
+
+@pytest.mark.parametrize("name", ENGINE_SCENES)
+@pytest.mark.parametrize("strategy", ["claim", "partition"])
+def test_engine_matches_reference_golden(name, strategy):
+    g = load_golden(name)
+    eng = _engine_from_golden(g, strategy=strategy)
+    for i in range(len(g["depth"])):
+        row = eng.fuse_frame(g["depth"][i], _pose(g, i))
+        assert _stats_tuple(row) == tuple(g["stats"][i]), (name, i)
+        assert eng.audit().ok
+    assert eng.irregular_cube_count() == int(g["stats"][-1][6])
+    assert sorted(eng.last_collected) == sorted(map(tuple, g["last_collected"].tolist()))
+    _check_blocks(eng.store, g)
+    _check_mesh(eng.compact(), g)
+    a = eng.audit()
+    assert [a.vertices_live, a.triangles_live, a.refcount_mismatches, a.duplicate_handles,
+            a.zero_ref_live, int(a.conservation_ok)] == list(g["audit"])
+    c = eng.store._counters()
+    # arena accounting that the reference pins (VertexPool.count/free/recycled/events)
+    assert c["vertex_count"] == g["counters"][2]
+    assert c["vertex_free"] == g["counters"][3]
+    assert c["vertex_recycled_total"] == g["counters"][4]
+    assert c["vertex_allocation_events"] == g["counters"][5]
+    assert c["triangle_count"] - c["triangle_free"] == g["counters"][6] - g["counters"][7]
+
+
+@pytest.mark.parametrize("name", ENGINE_SCENES)
+def test_engine_resume_after_arena_growth(name):
+    """Tiny initial arenas force every capacity guard to trip and the frame to
+    resume after growth; results must be unchanged."""
+    g = load_golden(name)
+    eng = _engine_from_golden(g, block_capacity=4, vertex_capacity=16, triangle_capacity=16)
+    resumes = 0
+    for i in range(len(g["depth"])):
+        row = eng.fuse_frame(g["depth"][i], _pose(g, i))
+        resumes += eng.device_stats[-1]["resumes"]
+        assert _stats_tuple(row) == tuple(g["stats"][i]), (name, i)
+    assert resumes > 0
+    _check_mesh(eng.compact(), g)
+
+
+@pytest.mark.parametrize("name", FIELD_SCENES)
+@pytest.mark.parametrize("strategy", ["serial", "claim", "partition"])
+def test_extract_fields_match_reference(name, strategy):
+    from paper_1803_03949_b200 import RefineParams, SpatialStore
+    from paper_1803_03949_b200.mesher import extract_frame
+    g = load_golden(name)
+    cfg = cfg_from_golden(g)
+    st = SpatialStore(cfg["cube_size"])
+    coords = [tuple(c) for c in g["in_coords"].tolist()]
+    st.set_block_samples(coords, g["in_tsdf"], g["in_weight"])
+    scope = [(c, None) for c in sorted(coords)]
+    rp = RefineParams(epsilon=cfg["epsilon"], enabled=cfg["refine"])
+    r1 = extract_frame(st, scope, 0, strategy=strategy, refine_params=rp, halo=sorted(coords))
+    st.set_block_samples(coords, g["in_tsdf2"], None)
+    r2 = extract_frame(st, scope, 1, strategy=strategy, refine_params=rp, halo=sorted(coords))
+    assert [r1["refined"], r1["freed"], r2["refined"], r2["freed"]] == list(g["extract_out"])
+    _check_blocks(st, g)
+    _check_mesh(st.compact_mesh(2), g)
+
+
+def _run_oracle_and_gpu(spec, cfg, frames, strategy="claim", rng=None):
+    from oracle.oracle import OracleEngine
+    from paper_1803_03949_b200 import Engine, RunConfig
+    from paper_1803_03949_b200.synth import camera_pose, render_depth
+    intr = spec.intrinsics()
+    eng = Engine(RunConfig(strategy=strategy, **cfg), intr)
+    ora = OracleEngine(cfg, (intr.fx, intr.fy, intr.cx, intr.cy, intr.width, intr.height))
+    for i in range(frames):
+        pose = camera_pose(spec, i)
+        d = render_depth(spec, pose, rng)
+        row = eng.fuse_frame(d, pose)
+        ref = ora.fuse_frame(d, pose.rotation, pose.translation)
+        assert _stats_tuple(row) == tuple(ref[k] for k in (
+            "frame", "blocks_active", "vertices_live", "triangles_live",
+            "vertices_allocated_total", "vertices_recycled_total", "irregular_cube_count")), i
+    return eng, ora
+
+
+def _compare_final(eng, ora):
+    m = eng.compact()
+    pos, nrm, ages, idx = ora.compact()
+    assert np.array_equal(m.indices, idx)
+    assert np.array_equal(m.positions, pos)
+    assert np.array_equal(m.ages, ages)
+    assert np.allclose(m.normals, nrm, rtol=0, atol=NORMAL_ATOL)
+    snap = ora.store.snapshot_blocks()
+    blocks = list(eng.store.blocks())
+    assert np.array_equal(np.array([b.coord for b in blocks], np.int32), snap["coords"])
+    assert np.array_equal(np.stack([b.tsdf for b in blocks]), snap["tsdf"])
+    assert np.array_equal(np.stack([b.type_curr for b in blocks]), snap["type_curr"])
+
+
+def test_c1_sphere_box_prefix_matches_oracle():
+    """BASELINE config C1 (sphere+box, 320x240, 8 mm), first 4 frames."""
+    from paper_1803_03949_b200.synth import config_spec
+    spec, cfg = config_spec("C1")
+    eng, ora = _run_oracle_and_gpu(spec, cfg, 4)
+    _compare_final(eng, ora)
+
+
+def test_c3_refine_room_prefix_matches_oracle():
+    """C3-style refine run at reduced resolution (160x120, 8 mm), 6 frames."""
+    from paper_1803_03949_b200.synth import config_spec
+    spec, cfg = config_spec("C3")
+    spec.width, spec.height, spec.fx, spec.fy = 160, 120, 131.25, 131.25
+    eng, ora = _run_oracle_and_gpu(spec, cfg, 6)
+    _compare_final(eng, ora)
+
+
+def test_noisy_partition_matches_oracle():
+    from paper_1803_03949_b200.synth import SceneSpec
+    spec = SceneSpec(scene="room", room_size=(2.0, 2.0, 1.4), orbit_radius=0.3, look="outward",
+                     elevation_amp_deg=30.0, angular_step_deg=20.0, frames=8, width=96, height=72,
+                     fx=70.0, fy=70.0, noise_sigma=0.003)
+    eng, ora = _run_oracle_and_gpu(spec, dict(cube_size=0.02, refine=True), 8,
+                                   strategy="partition", rng=np.random.default_rng(5))
+    _compare_final(eng, ora)
+
+
+def test_run_to_run_and_strategy_determinism():
+    from paper_1803_03949_b200.synth import SceneSpec
+    spec = SceneSpec(scene="sphere", sphere_radius=0.3, orbit_radius=0.9, elevation_amp_deg=60.0,
+                     angular_step_deg=18.0, frames=6, width=96, height=72, fx=80.0, fy=80.0)
+    meshes = []
+    for strategy in ("serial", "claim", "partition", "claim"):
+        eng, _ = _run_oracle_and_gpu(spec, dict(cube_size=0.025), 6, strategy=strategy)
+        meshes.append(eng.compact())
+    for m in meshes[1:]:
+        assert np.array_equal(m.positions, meshes[0].positions)
+        assert np.array_equal(m.indices, meshes[0].indices)
+        assert np.array_equal(m.normals, meshes[0].normals)
