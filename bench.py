@@ -1,0 +1,355 @@
+#!/usr/bin/env python
+"""Benchmark: depth frames/sec of integrate + incremental mesh update (+GC) on
+BASELINE.json configs[1] = C2 (synthetic room, 300-frame trajectory, 640x480,
+8 mm voxels), one step = one depth frame through ``Engine.fuse_frame``.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
+
+Arms
+* default: the B200 path.  ``value`` = K / sum of per-frame device times
+  (CUDA events on the engine's stream = torch's current stream; depth already
+  in HBM; L2 flushed with a 256 MiB write between frames, outside the events).
+  ``e2e`` = the same frames through the public API with pinned host depth
+  (H2D every frame) and the StatsRow D2H, wall clock.  ``roofline`` = the
+  dominant kernel's algorithmic bytes / its mean event-timed duration against
+  MEASURED_PEAKS.json hbm_gbs.  ``cpu_baseline`` = the CPU oracle port
+  (oracle/, serial C restatement of the reference) on a bounded prefix.
+* --impl reference: the reference CPU algorithm (the oracle port; the
+  reference itself is pure Python and cannot travel) on the same frames.
+Multi-GPU (torchrun): independent replicas per rank (weak scaling), device
+time = max over ranks; see DESIGN.md section 6.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "depth frames/sec (integrate+mesh) at 640x480, 8mm voxels; % of HBM roofline"
+FLUSH_BYTES = 256 << 20
+
+# Algorithmic bytes per unit (device layout):
+# tsdf f64 (8) + weight i32 (4) per sample; types 2 x u8; edge slots 3 x i32;
+# triangle slots 5 x i32; vertex = pos 24 + normal 24 + refcount 4 + birth 4 +
+# alive 1; triangle = 3 x i32 + alive 1.
+SAMPLE = 12
+BLOCK_BYTES = 512 * (8 + 4 + 1 + 1 + 12 + 20)
+
+
+def phase_bytes(ds: dict, h: int, w: int) -> dict:
+    """Algorithmic (compulsory) bytes per kernel for one frame's unit counts."""
+    depth = h * w * 8
+    coll, new, scope, halo = ds["collected_blocks"], ds["new_blocks"], ds["scope_blocks"], ds["halo_blocks"]
+    return {
+        "depth_stats": depth,
+        "collect": depth + coll * 16 + new * 28,
+        "init_blocks": new * BLOCK_BYTES,
+        "integrate": coll * 512 * SAMPLE * 2 + min(coll * 512, h * w) * 8,
+        "scope_halo": coll * 27 * 4 + halo * 8,
+        "retype": scope * (729 * SAMPLE + 512 + 1024 + 64),
+        "place": scope * (729 * 8 + 64 + 512) + ds["edge_placements"] * (4 + 24)
+        + ds["new_vertices"] * (4 + 4 + 1 + 24 + 4),
+        "tri_release": scope * (64 + 1024) + ds["changed_cubes"] * 20
+        + ds["triangles_freed"] * (12 + 1 + 4 + 3 * 4),
+        "tri_alloc": scope * (64 + 1024) + ds["changed_cubes"] * 20
+        + ds["triangles_allocated"] * (3 * 4 + 12 + 1 + 3 * 4),
+        "gc": halo * 512 * 12 + ds["normals_computed"] * 4 + ds["vertices_freed"] * (4 + 1 + 4),
+        "normals": halo * 1331 * SAMPLE + ds["normals_computed"] * (4 + 24),
+        "fallback": ds["fallback_normals"] * (12 + 24 * 4),
+    }
+
+
+# ---------------------------------------------------------------- helpers
+def measured_peak_gbs():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+        except Exception:
+            pass
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[2:6]) if v == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def make_frames(spec, nframes, device):
+    from paper_1803_03949_b200.synth import camera_pose, render_depth, render_depth_torch
+    poses = [camera_pose(spec, i) for i in range(nframes)]
+    if device is not None:
+        depths = [render_depth_torch(spec, p, device=device) for p in poses]
+    else:
+        depths = [render_depth(spec, p) for p in poses]
+    return poses, depths
+
+
+def oracle_run(spec, cfg, depths_host, poses, budget_s, warmup=0):
+    """Time the CPU oracle (serial C port of the reference) frame by frame."""
+    from oracle.oracle import OracleEngine
+    intr = spec.intrinsics()
+    eng = OracleEngine(cfg, (intr.fx, intr.fy, intr.cx, intr.cy, intr.width, intr.height))
+    for i in range(min(warmup, len(depths_host))):
+        eng.fuse_frame(depths_host[i], poses[i].rotation, poses[i].translation)
+    t_total, n = 0.0, 0
+    for i in range(warmup, len(depths_host)):
+        t0 = time.perf_counter()
+        eng.fuse_frame(depths_host[i], poses[i].rotation, poses[i].translation)
+        t_total += time.perf_counter() - t0
+        n += 1
+        if t_total > budget_s:
+            break
+    return n, t_total
+
+
+# ---------------------------------------------------------------- arms
+def run_reference(args, spec, cfg, rank, world):
+    import torch
+    if rank != 0:
+        return
+    nframes = args.warmup + args.steps
+    dev = "cuda" if torch.cuda.is_available() else None
+    poses, depths = make_frames(spec, nframes, dev)
+    host = [d.cpu().numpy() if dev else d for d in depths]
+    n, t = oracle_run(spec, cfg, host, poses, budget_s=args.ref_budget, warmup=args.warmup)
+    v = n / t if t > 0 else 0.0
+    sample = (f"{args.config} frames {args.warmup}..{args.warmup + n - 1} after {args.warmup} "
+              f"untimed warm-up frames (time cap {args.ref_budget:.0f} s)")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "frames/s", "n_gpus": world,
+            "steps": n, "warmup": args.warmup, "ms_per_step": 1e3 * t / max(n, 1),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (sphere-traced analytic scene)", "config": workload(args, spec, cfg),
+            "cpu_baseline": {"value": v, "unit": "frames/s", "cores": 1, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload(args, spec, cfg):
+    return {"workload": f"{args.config}: BASELINE.json configs[1] synthetic room 4x4x2.5 m, "
+                        f"{spec.width}x{spec.height} depth, {cfg['cube_size'] * 1e3:.0f} mm voxels, "
+                        "integrate + incremental mesh update + GC",
+            "frames": args.warmup + args.steps, "width": spec.width, "height": spec.height,
+            "cube_size_m": cfg["cube_size"], "trunc_m": cfg["trunc"],
+            "refine": bool(cfg.get("refine", False)), "strategy": args.strategy,
+            "l2": "flushed between frames (256 MiB write, outside the timed events)",
+            "parallelism": f"replicas x{args.gpus}" if args.gpus > 1 else "single GPU"}
+
+
+def run_gpu(args, spec, cfg, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_1803_03949_b200 import Engine, RunConfig
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    nframes = args.warmup + args.steps
+    poses, depths = make_frames(spec, nframes, dev)
+    torch.cuda.synchronize()
+    # a dedicated (non-default) stream: the engine's kernels and the timing
+    # events must share it (torch's default stream has handle 0)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+
+    # sizing pass: learn the arena sizes the capacity guards ask for, so no
+    # frame in the timed region has to grow an arena and resume
+    probe = Engine(RunConfig(strategy=args.strategy, **cfg), spec.intrinsics())
+    for i in range(nframes):
+        probe.fuse_frame(depths[i], poses[i])
+    c = probe.store._counters()
+    ds = probe.device_stats
+    caps = dict(block_capacity=c["block_count"] + 64,
+                vertex_capacity=c["vertex_count"] + max(d["edge_placements"] for d in ds) + 4096,
+                triangle_capacity=c["triangle_count"] + 5 * max(d["changed_cubes"] for d in ds) + 8192)
+    del probe
+
+    eng = Engine(RunConfig(strategy=args.strategy, **cfg, **caps), spec.intrinsics())
+    eng.set_stream(stream.cuda_stream)
+    eng.set_profiling(True)
+    flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
+    for i in range(args.warmup):
+        eng.fuse_frame(depths[i], poses[i])
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    phase_ms = []
+    resumes = 0
+    with ClockSampler(local_rank) as clocks:
+        for k in range(args.steps):
+            i = args.warmup + k
+            flush.zero_()
+            starts[k].record(stream)
+            eng.fuse_frame_enqueue(depths[i], poses[i])
+            ends[k].record(stream)
+            eng.fuse_frame_finish()
+            resumes += eng.device_stats[-1]["resumes"]
+            phase_ms.append(eng.phase_times())
+        torch.cuda.synchronize()
+    frame_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    dev_s = sum(frame_ms) / 1e3
+    if world > 1:
+        t = torch.tensor([dev_s], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_s = float(t.item())
+    value = world * args.steps / dev_s
+    stats = eng.device_stats[args.warmup:]
+
+    # roofline: dominant kernel (largest share of the timed frames)
+    names = list(phase_ms[0].keys())
+    tot = {n: sum(p[n] for p in phase_ms) for n in names}
+    dom = max(names, key=lambda n: tot[n])
+    bytes_dom = sum(phase_bytes(s, spec.height, spec.width)[dom] for s in stats)
+    achieved = bytes_dom / (tot[dom] / 1e3) / 1e9
+    peak, peak_kind = measured_peak_gbs()
+    frame_bytes = sum(sum(phase_bytes(s, spec.height, spec.width).values()) for s in stats)
+
+    # e2e: public API, pinned host depth, H2D + StatsRow D2H per frame, wall clock
+    host = [torch.empty(d.shape, dtype=torch.float64, pin_memory=True) for d in depths]
+    for hd, d in zip(host, depths):
+        hd.copy_(d)
+    host_np = [h.numpy() for h in host]
+    e2 = Engine(RunConfig(strategy=args.strategy, **cfg, **caps), spec.intrinsics())
+    for i in range(args.warmup):
+        e2.fuse_frame(host_np[i], poses[i])
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        e2.fuse_frame(host_np[args.warmup + k], poses[args.warmup + k])
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    # parity spot check of the timed engine vs the e2e engine (same frames)
+    same = eng.stats[-1].vertices_live == e2.stats[-1].vertices_live
+
+    if rank != 0:
+        return
+    cpu = None
+    if not args.no_cpu_baseline:
+        hn = [d.cpu().numpy() for d in depths]
+        n, t = oracle_run(spec, cfg, hn, poses, budget_s=args.cpu_budget)
+        cpu = {"value": n / t, "unit": "frames/s", "cores": 1, "kind": "port",
+               "sample": f"{args.config} frames 0..{n - 1} through the CPU oracle (serial C "
+                         f"restatement of the reference, oracle/), {t:.1f} s"}
+    launches_per_frame = 12 if args.strategy != "partition" else 19
+    clk = clocks.summary()
+    line = {
+        "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * dev_s / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (sphere-traced analytic room, GPU-rendered f64 depth)",
+        "config": workload(args, spec, cfg),
+        "roofline": {"bound": "hbm", "kernel": f"k_{dom}", "achieved": achieved, "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "kernel_share": tot[dom] / sum(tot.values()),
+                     "frame_alg_bytes": frame_bytes / args.steps,
+                     "frame_achieved_gbs": frame_bytes / dev_s / 1e9 / world,
+                     "frame_frac": frame_bytes / dev_s / 1e9 / world / peak},
+        "phase_ms_mean": {n: tot[n] / args.steps for n in names},
+        "cpu_baseline": cpu,
+        "e2e": {"value": world * args.steps / e2e_s, "unit": "frames/s",
+                "h2d_bytes_per_step": spec.width * spec.height * 8 + 256,
+                "d2h_bytes_per_step": 512},
+        "gpu_launches": launches_per_frame * args.steps,
+        "resumes_in_timed_region": resumes,
+        "clocks": clk,
+        "final_state": {"blocks": stats[-1]["blocks_active"], "vertices": stats[-1]["vertices_live"],
+                        "triangles": stats[-1]["triangles_live"], "e2e_state_match": bool(same)},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=295)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--strategy", default="claim")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--ref-budget", type=float, default=150.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    from paper_1803_03949_b200.synth import config_spec
+    spec, cfg = config_spec(args.config)
+    spec.frames = args.warmup + args.steps
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if world > 1 and args.impl != "reference":
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl")
+    try:
+        if args.impl == "reference":
+            run_reference(args, spec, cfg, rank, world)
+        else:
+            run_gpu(args, spec, cfg, rank, world, local_rank)
+    finally:
+        if world > 1 and args.impl != "reference":
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
