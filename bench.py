@@ -40,34 +40,27 @@ sys.path.insert(0, str(ROOT))
 METRIC = "depth frames/sec (integrate+mesh) at 640x480, 8mm voxels; % of HBM roofline"
 FLUSH_BYTES = 256 << 20
 
-# Algorithmic bytes per unit (device layout):
-# tsdf f64 (8) + weight i32 (4) per sample; types 2 x u8; edge slots 3 x i32;
-# triangle slots 5 x i32; vertex = pos 24 + normal 24 + refcount 4 + birth 4 +
-# alive 1; triangle = 3 x i32 + alive 1.
+# Algorithmic bytes per unit, device layout v2:
+# a corner sample is tsdf f64 + weight i32 (12 B); cube types 2 x u8; an edge
+# slot is birth i32 (4) + coordinate f64 (8) + normal 3 x f64 (24).
 SAMPLE = 12
-BLOCK_BYTES = 512 * (8 + 4 + 1 + 1 + 12 + 20)
+SLOT_SCAN = 4
 
 
 def phase_bytes(ds: dict, h: int, w: int) -> dict:
-    """Algorithmic (compulsory) bytes per kernel for one frame's unit counts."""
+    """Compulsory bytes per kernel for one frame's unit counts."""
     depth = h * w * 8
     coll, new, scope, halo = ds["collected_blocks"], ds["new_blocks"], ds["scope_blocks"], ds["halo_blocks"]
+    old = coll - new
     return {
         "depth_stats": depth,
-        "collect": depth + coll * 16 + new * 28,
-        "init_blocks": new * BLOCK_BYTES,
-        "integrate": coll * 512 * SAMPLE * 2 + min(coll * 512, h * w) * 8,
-        "scope_halo": coll * 27 * 4 + halo * 8,
-        "retype": scope * (729 * SAMPLE + 512 + 1024 + 64),
-        "place": scope * (729 * 8 + 64 + 512) + ds["edge_placements"] * (4 + 24)
-        + ds["new_vertices"] * (4 + 4 + 1 + 24 + 4),
-        "tri_release": scope * (64 + 1024) + ds["changed_cubes"] * 20
-        + ds["triangles_freed"] * (12 + 1 + 4 + 3 * 4),
-        "tri_alloc": scope * (64 + 1024) + ds["changed_cubes"] * 20
-        + ds["triangles_allocated"] * (3 * 4 + 12 + 1 + 3 * 4),
-        "gc": halo * 512 * 12 + ds["normals_computed"] * 4 + ds["vertices_freed"] * (4 + 1 + 4),
-        "normals": halo * 1331 * SAMPLE + ds["normals_computed"] * (4 + 24),
-        "fallback": ds["fallback_normals"] * (12 + 24 * 4),
+        "collect": depth + coll * 16 + new * 40,
+        "fuse_blocks": old * 512 * SAMPLE + coll * 512 * SAMPLE + new * (512 * 2 + 1536 * SLOT_SCAN)
+        + min(coll * 512, h * w) * 8 + coll * 27 * 16,
+        "retype_place": scope * (729 * SAMPLE + 512 + 1024) + ds["edge_placements"] * (4 + 8)
+        + ds["new_vertices"] * 24,
+        "gc_normals": halo * (1536 * SLOT_SCAN + 729 + 1331 * SAMPLE) + ds["normals_computed"] * 24
+        + ds["vertices_freed"] * 4,
     }
 
 
@@ -208,11 +201,7 @@ def run_gpu(args, spec, cfg, rank, world, local_rank):
     probe = Engine(RunConfig(strategy=args.strategy, **cfg), spec.intrinsics())
     for i in range(nframes):
         probe.fuse_frame(depths[i], poses[i])
-    c = probe.store._counters()
-    ds = probe.device_stats
-    caps = dict(block_capacity=c["block_count"] + 64,
-                vertex_capacity=c["vertex_count"] + max(d["edge_placements"] for d in ds) + 4096,
-                triangle_capacity=c["triangle_count"] + 5 * max(d["changed_cubes"] for d in ds) + 8192)
+    caps = dict(block_capacity=probe.store._counters()["block_count"] + 64)
     del probe
 
     eng = Engine(RunConfig(strategy=args.strategy, **cfg, **caps), spec.intrinsics())
@@ -287,7 +276,7 @@ def run_gpu(args, spec, cfg, rank, world, local_rank):
         cpu = {"value": n / t, "unit": "frames/s", "cores": 1, "kind": "port",
                "sample": f"{args.config} frames 0..{n - 1} through the CPU oracle (serial C "
                          f"restatement of the reference, oracle/), {t:.1f} s"}
-    launches_per_frame = 12 if args.strategy != "partition" else 19
+    launches_per_frame = 5
     clk = clocks.summary()
     line = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,

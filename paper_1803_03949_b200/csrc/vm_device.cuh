@@ -1,10 +1,22 @@
 // vm_device.cuh -- device-side data structures and helpers for the B200
-// online mesh-generation path (see DESIGN.md for the layout rationale).
+// online mesh-generation path (DESIGN.md sections 2-3).
 //
-// Numeric contract: this translation unit is compiled with --fmad=false so
-// that no multiply-add is contracted implicitly; the only FMAs are the
-// explicit __fma_rn chains that restate numpy/OpenBLAS 3x3 products
-// (reference fusion.py:87, :144).
+// Layout ("slot-resident cube field"):
+//   * block table: bucketed hash (8 CAS slots per bucket + locked overflow
+//     chains) mapping packed block coordinates to a dense block index;
+//   * per block (SoA, 8x8x8 cubes, C order x,y,z): tsdf f64, weight i32,
+//     type_prev/type_curr u8, and per owned edge slot (3 per cube): vertex
+//     birth frame i32 (-1 = empty slot), position along the edge axis f64,
+//     normal f64x3.  A vertex lives IN its edge slot (the paper's "cube owns
+//     its 3 edges"): allocation = claiming the slot, recycling = clearing it.
+//   * triangles are not stored: a cube's live triangles are always
+//     TRI_TABLE[type_curr] (the reference retriangulates exactly when the type
+//     changes, mesher.py:283-320), so triangle lists and vertex reference
+//     counts are derived from the types; counters reproduce the reference's
+//     pool statistics (store.py:95-241).
+//
+// Numeric contract: compiled with --fmad=false; the only FMAs are explicit
+// __fma_rn chains restating numpy/OpenBLAS 3x3 products (SURVEY.md appx A).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -17,31 +29,28 @@ constexpr int kB = 8;          // cubes per block edge (store.py:26)
 constexpr int kNC = 512;       // cubes per block
 constexpr int kSlotsPerBucket = 8;
 constexpr int kEV = kNC * 3;   // edge-vertex slots per block
-constexpr int kTS = kNC * 5;   // triangle slots per block
 constexpr long long kEmptyKey = -1LL;
 
-// error codes == vm_status
 enum { ERR_NONE = 0, ERR_CAPACITY = 1, ERR_CONSISTENCY = 2 };
-// arena-growth requests (host grows, then resumes the frame at a segment)
-enum { NEED_BLOCKS = 1, NEED_VERTS = 2, NEED_TRIS = 4 };
+enum { NEED_BLOCKS = 1 };
 
 // Device counters.  Persistent fields first; everything from `nvalid` on is
-// reset at the start of every frame (one memset).
+// reset at the start of every call (one memset).
 struct Counters {
-  int32_t nblocks;       // blocks allocated (SpatialStore.block_count)
-  int32_t ovf_count;     // overflow-chain entries used
-  int32_t v_count;       // vertex arena high-water (VertexPool.count)
-  int32_t v_free;        // vertex free-stack size
-  int32_t t_count;
-  int32_t t_free;
-  int32_t error;         // first error code
-  int32_t need;          // NEED_* bits
+  int32_t nblocks;       // SpatialStore.block_count
+  int32_t ovf_count;
+  int32_t error;
+  int32_t need;
+  int64_t v_live;        // VertexPool.live_count
+  int64_t v_count;       // VertexPool.count (arena high-water)
   int64_t v_recycled;
   int64_t v_events;      // VertexPool.allocation_events
+  int64_t t_live;        // TrianglePool.live_count
+  int64_t t_count;
   int64_t t_recycled;
-  int64_t irregular;     // running Engine.irregular_cube_count
+  int64_t irregular;     // Engine.irregular_cube_count, maintained incrementally
   int64_t err_info[4];
-  // ---- per frame -------------------------------------------------------
+  // ---- per call ----------------------------------------------------------
   int32_t nvalid;
   int32_t nsteps;
   unsigned long long maxnorm_bits;
@@ -51,26 +60,23 @@ struct Counters {
   int32_t nhalo;
   int32_t nexplicit;
   int32_t nitems_live;
-  int32_t nfallback;
-  int32_t v_tickets;
-  int32_t t_tickets;
-  int32_t done_place;
-  int32_t done_tri;
+  int32_t done_gc;
   int32_t pad0;
-  int64_t v_bound;
-  int64_t t_bound;
-  int64_t active_cubes;
-  int64_t edge_placements;
-  int64_t changed_cubes;
+  int64_t v_allocs;
+  int64_t v_frees;
+  int64_t placements;
+  int64_t active;
+  int64_t changed;
   int64_t t_released;
   int64_t t_allocated;
-  int64_t v_freed;
+  int64_t irr_delta;
   int64_t normals;
+  int64_t fallbacks;
   int64_t refined;
 };
 
-// Per-call parameters, resident in device memory (so a captured graph can be
-// replayed with new poses / depth pointers).
+// Per-call parameters in device memory (a captured frame graph replays with
+// new poses / depth pointers).
 struct FrameDev {
   const double *depth;
   int32_t h, w;
@@ -81,67 +87,47 @@ struct FrameDev {
   double trunc, max_range, epsilon;
   int64_t weight_cap;
   int32_t refine, frustum_only;
-  int32_t epoch;        // monotone stamp for per-frame membership sets
+  int32_t epoch;        // monotone stamp for per-call membership sets
   int32_t frame;        // frame index (vertex birth)
   int32_t scope_mode;   // 0: collected + slabs (device scope); 1: explicit items
-  int32_t parity;       // partition strategy pass (-1 = claim)
+  int32_t pad;
 };
 
-struct FallbackRec {
-  int32_t h;      // vertex handle
-  int32_t blk;    // owning block (slot owner)
-  int32_t slot;   // ci*3 + axis
-};
-
-// All device pointers and capacities; passed by value to every kernel.
 struct DevState {
   double cube_size, extent;
   long long table_size;
   long long ts_mask;    // table_size-1 if a power of two, else 0
   int32_t nbuckets;
-  int32_t max_blocks;   // table_size/2 (reference load-factor limit)
-  // bucketed hash: lock-free CAS slots + lock-based overflow chains
+  int32_t max_blocks;   // reference load-factor limit: 2*n < table_size
   long long *keys;      // [nbuckets*8] packed coords, -1 empty
   int32_t *vals;        // [nbuckets*8] block index, -1 unpublished
-  int32_t *ovf_head;    // [nbuckets]
-  int32_t *ovf_lock;    // [nbuckets]
-  long long *ovf_key;   // [ovf_cap]
+  int32_t *ovf_head;
+  int32_t *ovf_lock;
+  long long *ovf_key;
   int32_t *ovf_val;
   int32_t *ovf_next;
   int32_t ovf_cap;
   // per-block metadata, sized max_blocks
-  int4 *bcoord;         // x, y, z, 0
+  int4 *bcoord;
   int32_t *nbr;         // [max_blocks*27] neighbour block index (-1 absent); 13 = self
   int32_t *stamp_collect;
   int32_t *stamp_halo;
-  uint8_t *slab_bits;   // minus-neighbour scope slabs (7 bits), cleared after use
-  int32_t *scope;       // [max_blocks] scope items: collected first, then slabs
-  int32_t *newlist;     // [max_blocks]
-  int32_t *halo;        // [max_blocks]
+  int32_t *stamp_new;   // epoch in which the block was allocated
+  uint8_t *slab_bits;
+  int32_t *scope;       // scope items: collected first, then minus slabs
+  int32_t *newlist;
+  int32_t *halo;
   // heavy block storage, sized block_cap (grows)
   int32_t block_cap;
-  double *tsdf;         // [cap*512] C order (x, y, z)
+  double *tsdf;         // [cap*512]
   int32_t *weight;      // [cap*512]
   uint8_t *tp, *tc;     // [cap*512]
-  int32_t *ev;          // [cap*512*3]
-  int32_t *tri;         // [cap*512*5]
-  uint32_t *item_mask;  // [cap*16] explicit scope masks
-  uint32_t *item_sel;   // [cap*16] selected (defined & mask) cubes per scope item
-  // vertex arena
-  int32_t v_cap;
-  long long max_vertices;   // <= 0 unlimited
-  double *vpos;         // [cap*3]
-  double *vnrm;         // [cap*3]
-  int32_t *vref;
-  int32_t *vbirth;
-  uint8_t *valive;
-  int32_t *vfree;
-  FallbackRec *fallback;  // [v_cap]
-  // triangle arena
-  int32_t t_cap;
-  int32_t *tverts;      // [cap*3]
-  uint8_t *talive;
-  int32_t *tfree;
+  int32_t *vbirth;      // [cap*1536] slot occupancy: birth frame, -1 empty
+  double *vparam;       // [cap*1536] vertex coordinate along the edge axis
+  double *vnrm;         // [cap*1536*3]
+  uint32_t *item_mask;  // [cap*16] explicit scope cube masks
+  uint32_t *item_sel;   // [cap*16] unused by the fused kernels (kept for debugging)
+  long long max_vertices;
   Counters *ctr;
 };
 
@@ -151,16 +137,17 @@ __constant__ uint8_t c_tri_count[256] = VM_TRI_COUNT_INIT;
 __constant__ unsigned long long c_tri_packed[256] = VM_TRI_PACKED_INIT;
 // corner offsets (mc_tables.py:31-34) packed as x | y<<1 | z<<2
 __constant__ uint8_t c_corner[8] = {0, 1, 3, 2, 4, 5, 7, 6};
-// edge geometry derived as mc_tables.py:44-64: owner offset (packed), axis,
-// oriented start/end corners
+// edge geometry (mc_tables.py:44-64): owner offset (packed), axis, oriented corners
 __constant__ uint8_t c_e_own[12] = {0, 1, 2, 0, 4, 5, 6, 4, 0, 1, 3, 2};
 __constant__ uint8_t c_e_axis[12] = {0, 1, 0, 1, 0, 1, 0, 1, 2, 2, 2, 2};
 __constant__ uint8_t c_e_start[12] = {0, 1, 3, 0, 4, 5, 7, 4, 0, 1, 2, 3};
 __constant__ uint8_t c_e_end[12] = {1, 2, 2, 3, 5, 6, 6, 7, 4, 5, 6, 7};
-// regular types (refine.py:32-45): x-, x+, y-, y+, z-, z+
+// inverse: edge index of the cube whose owner offset is `own` along `axis`
+// (-1 if no such edge); [axis][own]
+__constant__ int8_t c_edge_of[3][8] = {{0, -1, 2, -1, 4, -1, 6, -1},
+                                       {3, 1, -1, -1, 7, 5, -1, -1},
+                                       {8, 9, 11, 10, -1, -1, -1, -1}};
 __constant__ uint8_t c_regular[6] = {0x99, 0x66, 0x33, 0xCC, 0x0F, 0xF0};
-// slab selection: for "at max" pattern m = (x==7)<<2|(y==7)<<1|(z==7), the
-// minus-offset bits (bit o-1 for o = ox*4+oy*2+oz) whose slab contains the cube
 __constant__ uint8_t c_slab_sel[8];
 
 __host__ __device__ inline bool is_regular_type(unsigned t) {
@@ -171,11 +158,6 @@ __host__ __device__ inline bool is_regular_type(unsigned t) {
 __device__ __forceinline__ long long pack_coord(int x, int y, int z) {
   const long long off = 1LL << 20;
   return ((((long long)x + off) << 42) | (((long long)y + off) << 21) | ((long long)z + off));
-}
-__device__ __forceinline__ int3 unpack_coord(long long k) {
-  const long long off = 1LL << 20;
-  return make_int3((int)((k >> 42) - off), (int)(((k >> 21) & ((1LL << 21) - 1)) - off),
-                   (int)((k & ((1LL << 21) - 1)) - off));
 }
 // store.py:84-87 (Python floor-mod of the xor of prime products)
 __device__ __forceinline__ long long hash_block(const DevState &S, int x, int y, int z) {
@@ -194,6 +176,10 @@ __device__ __forceinline__ void set_error(const DevState &S, int code, long long
     S.ctr->err_info[0] = a; S.ctr->err_info[1] = b;
     S.ctr->err_info[2] = c; S.ctr->err_info[3] = d;
   }
+}
+
+__device__ __forceinline__ void add64(int64_t *p, long long v) {
+  if (v) atomicAdd((unsigned long long *)p, (unsigned long long)v);
 }
 
 // ---------------------------------------------------------------- hash table
@@ -220,7 +206,7 @@ __device__ int hash_find(const DevState &S, int x, int y, int z) {
 }
 
 // allocate the next block index; CapacityError at 2*n >= table_size (store.py:304-306)
-__device__ int alloc_block(const DevState &S, int x, int y, int z) {
+__device__ int alloc_block(const DevState &S, int x, int y, int z, int epoch) {
   int idx = atomicAdd(&S.ctr->nblocks, 1);
   if (2LL * idx >= S.table_size) {
     set_error(S, ERR_CAPACITY, idx, S.table_size, 1);
@@ -228,14 +214,15 @@ __device__ int alloc_block(const DevState &S, int x, int y, int z) {
   }
   if (idx >= S.block_cap) atomicOr(&S.ctr->need, NEED_BLOCKS);
   S.bcoord[idx] = make_int4(x, y, z, 0);
+  S.stamp_new[idx] = epoch;
   S.newlist[atomicAdd(&S.ctr->nnew, 1)] = idx;
   return idx;
 }
 
-// SpatialStore.get_or_allocate_block (store.py:296-320), lock-free in the
-// bucket (CAS on the key, then publish the value) and lock-based in the
-// bucket's overflow chain.  Exactly one allocation per coordinate.
-__device__ int hash_insert(const DevState &S, int x, int y, int z) {
+// SpatialStore.get_or_allocate_block (store.py:296-320): lock-free in the
+// bucket (CAS the key, then publish the index) and lock-based in the bucket's
+// overflow chain.  Exactly one allocation per coordinate, no dropped inserts.
+__device__ int hash_insert(const DevState &S, int x, int y, int z, int epoch) {
   const long long key = pack_coord(x, y, z);
   const unsigned b = (unsigned)(hash_block(S, x, y, z) >> 3);
   long long *kb = S.keys + (size_t)b * kSlotsPerBucket;
@@ -246,7 +233,7 @@ __device__ int hash_insert(const DevState &S, int x, int y, int z) {
       k = (long long)atomicCAS((unsigned long long *)(kb + i), (unsigned long long)kEmptyKey,
                                (unsigned long long)key);
       if (k == kEmptyKey) {
-        int idx = alloc_block(S, x, y, z);
+        int idx = alloc_block(S, x, y, z, epoch);
         __threadfence();
         atomicExch(vb + i, idx);
         return idx;
@@ -254,7 +241,6 @@ __device__ int hash_insert(const DevState &S, int x, int y, int z) {
     }
     if (k == key) return wait_val(vb + i);
   }
-  // bucket full: overflow chain under the bucket lock
   int found = -1;
   bool done = false;
   while (!done) {
@@ -268,7 +254,7 @@ __device__ int hash_insert(const DevState &S, int x, int y, int z) {
           set_error(S, ERR_CAPACITY, e, S.ovf_cap, 2);
           found = -2;
         } else {
-          found = alloc_block(S, x, y, z);
+          found = alloc_block(S, x, y, z, epoch);
           S.ovf_key[e] = key;
           S.ovf_val[e] = found;
           S.ovf_next[e] = S.ovf_head[b];
@@ -291,8 +277,7 @@ __device__ __forceinline__ int nbr_dir(int dx, int dy, int dz) {
   return (dx + 1) * 9 + (dy + 1) * 3 + (dz + 1);
 }
 
-// out_j = fma(a2, B[2][j], fma(a1, B[1][j], a0*B[0][j])) -- numpy `a @ B` via
-// OpenBLAS dgemm; B row-major 3x3
+// out_j = fma(a2, B[2][j], fma(a1, B[1][j], a0*B[0][j])) -- numpy `a @ B`
 __device__ __forceinline__ double matvec_col(const double *a, const double *B, int j) {
   return __fma_rn(a[2], B[6 + j], __fma_rn(a[1], B[3 + j], __dmul_rn(a[0], B[j])));
 }
@@ -321,25 +306,22 @@ __device__ bool block_in_frustum_dev(int4 c, const FrameDev &F, double extent) {
   return false;
 }
 
-// refine.refine_block_types for one cube (refine.py:98-135); returns the new
-// type, sets *changed.
-__device__ __forceinline__ unsigned refine_type(unsigned tc, unsigned tp, const double *corner,
-                                                double eps, bool *changed) {
+// refine.refine_block_types for one cube (refine.py:98-135).  `small` = bit k
+// set iff |corner k| < epsilon.  Returns the new type; *changed as counted by
+// the reference (hit & new != current).
+__device__ __forceinline__ unsigned refine_type(unsigned tc, unsigned tp, unsigned small,
+                                                bool *changed) {
   *changed = false;
   if (__popc((tc ^ tp) & 0xFF) > 3) return tc;
-  unsigned small = 0;
-#pragma unroll
-  for (int k = 0; k < 8; k++) small |= (fabs(corner[k]) < eps ? 1u : 0u) << k;
   int best_score = 255;
   unsigned best = 0;
 #pragma unroll
   for (int j = 0; j < 6; j++) {
-    unsigned reg = c_regular[j];
-    unsigned diff = (tc ^ reg) & 0xFF;
-    int dist = __popc(diff);
-    if (dist > 3) continue;
-    if (diff & ~small) continue;   // a disagreeing corner is not near zero
-    int score = dist * 8 + j;
+    const unsigned reg = c_regular[j];
+    const unsigned diff = (tc ^ reg) & 0xFF;
+    const int dist = __popc(diff);
+    if (dist > 3 || (diff & ~small)) continue;   // a disagreeing corner is not near zero
+    const int score = dist * 8 + j;
     if (score < best_score) { best_score = score; best = reg; }
   }
   if (best_score < 255) {
@@ -357,8 +339,7 @@ __device__ __forceinline__ T warp_sum(T v) {
   return v;
 }
 
-// block-wide sum of a long long (blockDim multiple of 32, <= 1024); result
-// valid in thread 0.  `sh` must hold 32 entries.
+// block-wide sum (blockDim multiple of 32); result valid in thread 0
 __device__ __forceinline__ long long block_sum(long long v, long long *sh) {
   v = warp_sum(v);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -371,6 +352,17 @@ __device__ __forceinline__ long long block_sum(long long v, long long *sh) {
     r = warp_sum(r);
   }
   return r;
+}
+
+// vertex position from its slot (mesher.py:216-235): every coordinate is
+// (owner cube index) * l except the edge axis, which holds the interpolated
+// value stored at placement.  Bit-identical to the reference.
+__device__ __forceinline__ void slot_position(const DevState &S, int blk, int slot, double *p) {
+  const int4 c = S.bcoord[blk];
+  const int ci = slot / 3, axis = slot - 3 * (slot / 3);
+  const int g[3] = {c.x * kB + (ci >> 6), c.y * kB + ((ci >> 3) & 7), c.z * kB + (ci & 7)};
+  for (int d = 0; d < 3; d++) p[d] = __dmul_rn((double)g[d], S.cube_size);
+  p[axis] = S.vparam[(size_t)blk * kEV + slot];
 }
 
 }  // namespace vm

@@ -1,13 +1,12 @@
 // vm_engine.cu -- host runtime of the B200 mesh-generation path and the C ABI
 // declared in include/voxmesh_b200.h.
 //
-// One engine == one SpatialStore + its device arenas + one CUDA stream.  A
-// frame is enqueued as a fixed sequence of persistent-grid kernels that read
-// their work counts from device counters (no host sync inside a frame).  The
-// block heap and the vertex/triangle arenas are sized speculatively; kernels
-// check a capacity guard and, if it trips, every later kernel of the frame
-// exits at once, the host grows the arena and resumes the frame at the failed
-// segment (collect/allocation is idempotent).
+// One engine == one SpatialStore in HBM + one CUDA stream.  A frame is five
+// persistent-grid kernels that read their work counts from device counters
+// (no host sync inside a frame).  The only speculatively sized structure is
+// the block heap: if a frame allocates past its capacity, every kernel after
+// k_collect exits immediately, the host grows the heap and resumes the frame
+// at k_fuse_blocks (collect + allocation is idempotent).
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
 
@@ -36,24 +35,28 @@ static int set_err(int code, const char *fmt, ...) {
   return code;
 }
 
-#define CK(x)                                                                      \
-  do {                                                                             \
-    cudaError_t _e = (x);                                                          \
-    if (_e != cudaSuccess)                                                         \
+#define CK(x)                                                                            \
+  do {                                                                                   \
+    cudaError_t _e = (x);                                                                \
+    if (_e != cudaSuccess)                                                               \
       return set_err(VM_ERR_CUDA, "%s failed: %s (%s:%d)", #x, cudaGetErrorString(_e), \
-                     __FILE__, __LINE__);                                          \
+                     __FILE__, __LINE__);                                                \
   } while (0)
 
-#define TRY(x)                 \
-  do {                         \
-    int _r = (x);              \
+#define TRY(x)                  \
+  do {                          \
+    int _r = (x);               \
     if (_r != VM_OK) return _r; \
   } while (0)
 
-enum Segment { SEG_COLLECT = 0, SEG_INIT = 1, SEG_PLACE = 2, SEG_TRIALLOC = 3 };
-enum Phase {
-  PH_DEPTH = 0, PH_COLLECT, PH_INIT, PH_INTEGRATE, PH_SCOPE, PH_RETYPE, PH_PLACE,
-  PH_TRI_RELEASE, PH_TRI_ALLOC, PH_GC, PH_NORMALS, PH_FALLBACK, PH_END, PH_COUNT
+enum Phase { PH_DEPTH = 0, PH_COLLECT, PH_FUSE, PH_RETYPE, PH_GC, PH_END, PH_COUNT };
+
+struct Compacted {
+  double *pos = nullptr, *nrm = nullptr;
+  long long *age = nullptr;
+  int32_t *idx = nullptr;
+  int32_t *ev_handles = nullptr, *tri_handles = nullptr;
+  int64_t nv = 0, nt = 0;
 };
 
 struct vm_engine {
@@ -68,24 +71,15 @@ struct vm_engine {
   bool own_stream = false;
   int32_t epoch = 0;
   int sm_count = 148;
-  int strategy = VM_STRATEGY_CLAIM;
-  int refine_flag = 0;
-  // scratch for explicit-list calls
   void *d_scratch = nullptr;
   size_t scratch_cap = 0;
-  // compaction
-  double *c_pos = nullptr, *c_nrm = nullptr;
-  long long *c_age = nullptr;
-  int32_t *c_idx = nullptr;
-  int64_t c_nv = 0, c_nt = 0;
-  // timing
+  Compacted comp;
   cudaEvent_t ev[PH_COUNT] = {};
   bool profiling = false;
-  int pending = 0;     // an enqueued frame awaits finish
+  int pending = 0;
   int64_t pending_frame = 0;
   int last_resumes = 0;
 };
-
 
 // ------------------------------------------------------------ helpers
 template <typename T>
@@ -97,12 +91,10 @@ static int dev_alloc(T **p, size_t n, int fill_byte = -2) {
   return VM_OK;
 }
 
-// grow a device array from old_n to new_n elements, copying the old prefix
 template <typename T>
-static int dev_grow(T **p, size_t old_n, size_t new_n, cudaStream_t st, int fill_byte = -2) {
+static int dev_grow(T **p, size_t old_n, size_t new_n, cudaStream_t st) {
   T *q = nullptr;
   CK(cudaMalloc((void **)&q, new_n * sizeof(T)));
-  if (fill_byte != -2) CK(cudaMemsetAsync(q, fill_byte, new_n * sizeof(T), st));
   if (*p && old_n) CK(cudaMemcpyAsync(q, *p, old_n * sizeof(T), cudaMemcpyDeviceToDevice, st));
   CK(cudaStreamSynchronize(st));
   if (*p) CK(cudaFree(*p));
@@ -114,7 +106,7 @@ static int scratch(vm_engine *e, size_t bytes, void **out) {
   if (bytes > e->scratch_cap) {
     if (e->d_scratch) CK(cudaFree(e->d_scratch));
     e->d_scratch = nullptr;
-    size_t cap = std::max(bytes, (size_t)1 << 20);
+    const size_t cap = std::max(bytes, (size_t)1 << 20);
     CK(cudaMalloc(&e->d_scratch, cap));
     e->scratch_cap = cap;
   }
@@ -125,66 +117,34 @@ static int scratch(vm_engine *e, size_t bytes, void **out) {
 static inline int grid_blocks(vm_engine *e) { return e->sm_count * 4; }
 static inline int grid_threads(vm_engine *e, long long n, int tpb) {
   long long g = (n + tpb - 1) / tpb;
-  long long cap = (long long)e->sm_count * 8;
+  const long long cap = (long long)e->sm_count * 8;
   if (g < 1) g = 1;
   return (int)std::min(g, cap);
 }
 
 static int check_launch() {
-  cudaError_t err = cudaGetLastError();
+  const cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return set_err(VM_ERR_CUDA, "kernel launch failed: %s", cudaGetErrorString(err));
   return VM_OK;
 }
 
-// ------------------------------------------------------------ arenas
 static int grow_blocks(vm_engine *e, int64_t need) {
   DevState &S = e->S;
-  int64_t cap = std::max<int64_t>((int64_t)S.block_cap * 2, need + need / 4 + 64);
+  int64_t cap = std::max<int64_t>((int64_t)S.block_cap * 2, need + need / 4 + 8);
   cap = std::min<int64_t>(cap, (int64_t)S.max_blocks);
   if (cap < need) cap = need;
+  if (cap <= S.block_cap) return VM_OK;
   const size_t o = (size_t)S.block_cap, n = (size_t)cap;
   cudaStream_t st = e->stream;
   TRY(dev_grow(&S.tsdf, o * kNC, n * kNC, st));
   TRY(dev_grow(&S.weight, o * kNC, n * kNC, st));
   TRY(dev_grow(&S.tp, o * kNC, n * kNC, st));
   TRY(dev_grow(&S.tc, o * kNC, n * kNC, st));
-  TRY(dev_grow(&S.ev, o * kEV, n * kEV, st));
-  TRY(dev_grow(&S.tri, o * kTS, n * kTS, st));
+  TRY(dev_grow(&S.vbirth, o * kEV, n * kEV, st));
+  TRY(dev_grow(&S.vparam, o * kEV, n * kEV, st));
+  TRY(dev_grow(&S.vnrm, o * kEV * 3, n * kEV * 3, st));
   TRY(dev_grow(&S.item_mask, 0, n * 16, st));
-  TRY(dev_grow(&S.item_sel, 0, n * 16, st));
   S.block_cap = (int32_t)cap;
-  return VM_OK;
-}
-
-static int grow_vertices(vm_engine *e, int64_t need) {
-  DevState &S = e->S;
-  int64_t cap = std::max<int64_t>((int64_t)S.v_cap * 2, need + need / 4 + 1024);
-  cap = std::min<int64_t>(cap, (int64_t)INT32_MAX - 1);
-  if (cap < need) return set_err(VM_ERR_CAPACITY, "vertex arena exceeds 2^31 handles");
-  const size_t o = (size_t)S.v_cap, n = (size_t)cap;
-  cudaStream_t st = e->stream;
-  TRY(dev_grow(&S.vpos, o * 3, n * 3, st, 0));
-  TRY(dev_grow(&S.vnrm, o * 3, n * 3, st, 0));
-  TRY(dev_grow(&S.vref, o, n, st, 0));
-  TRY(dev_grow(&S.vbirth, o, n, st, 0));
-  TRY(dev_grow(&S.valive, o, n, st, 0));
-  TRY(dev_grow(&S.vfree, o, n, st));
-  TRY(dev_grow(&S.fallback, 0, n, st));
-  S.v_cap = (int32_t)cap;
-  return VM_OK;
-}
-
-static int grow_triangles(vm_engine *e, int64_t need) {
-  DevState &S = e->S;
-  int64_t cap = std::max<int64_t>((int64_t)S.t_cap * 2, need + need / 4 + 1024);
-  cap = std::min<int64_t>(cap, (int64_t)INT32_MAX - 1);
-  if (cap < need) return set_err(VM_ERR_CAPACITY, "triangle arena exceeds 2^31 handles");
-  const size_t o = (size_t)S.t_cap, n = (size_t)cap;
-  cudaStream_t st = e->stream;
-  TRY(dev_grow(&S.tverts, o * 3, n * 3, st, 0xFF));
-  TRY(dev_grow(&S.talive, o, n, st, 0));
-  TRY(dev_grow(&S.tfree, o, n, st));
-  S.t_cap = (int32_t)cap;
   return VM_OK;
 }
 
@@ -206,15 +166,9 @@ static int error_from_counters(vm_engine *e) {
   }
   if (c.error == ERR_CONSISTENCY) {
     switch (c.err_info[0]) {
-      case 10: return set_err(VM_ERR_CONSISTENCY, "edge owner block absent during placement (cube %lld, %lld, %lld)",
-                              (long long)c.err_info[1], (long long)c.err_info[2], (long long)c.err_info[3]);
-      case 11: return set_err(VM_ERR_CONSISTENCY, "edge owner block absent during triangulation (cube %lld, %lld, %lld)",
-                              (long long)c.err_info[1], (long long)c.err_info[2], (long long)c.err_info[3]);
-      case 12: return set_err(VM_ERR_CONSISTENCY, "edge of cube (%lld, %lld, %lld) has no vertex; placement incomplete",
-                              (long long)c.err_info[1], (long long)c.err_info[2], (long long)c.err_info[3]);
-      case 20: return set_err(VM_ERR_CONSISTENCY, "negative refcount on vertex %lld", (long long)c.err_info[1]);
-      case 21: return set_err(VM_ERR_CONSISTENCY, "double free of triangle handle %lld", (long long)c.err_info[1]);
-      case 30: return set_err(VM_ERR_CONSISTENCY, "double free of vertex handle %lld", (long long)c.err_info[1]);
+      case 10:
+        return set_err(VM_ERR_CONSISTENCY, "edge owner block absent during placement (cube %lld, %lld, %lld)",
+                       (long long)c.err_info[1], (long long)c.err_info[2], (long long)c.err_info[3]);
       case 40: return set_err(VM_ERR_CONSISTENCY, "triangle references a vertex bound to no edge");
       default: return set_err(VM_ERR_CONSISTENCY, "consistency error %lld", (long long)c.err_info[0]);
     }
@@ -222,27 +176,7 @@ static int error_from_counters(vm_engine *e) {
   return VM_OK;
 }
 
-// grow what the guards asked for; returns the segment to resume at
-static int handle_need(vm_engine *e, int *seg) {
-  const Counters &c = *e->h_ctr;
-  *seg = -1;
-  if (c.need & NEED_BLOCKS) {
-    TRY(grow_blocks(e, c.nblocks));
-    *seg = SEG_INIT;
-  } else if (c.need & NEED_VERTS) {
-    int64_t need = (int64_t)c.v_count + std::max<int64_t>(0, c.v_bound - c.v_free);
-    TRY(grow_vertices(e, need));
-    *seg = SEG_PLACE;
-  } else if (c.need & NEED_TRIS) {
-    int64_t need = (int64_t)c.t_count + std::max<int64_t>(0, c.t_bound - c.t_free);
-    TRY(grow_triangles(e, need));
-    *seg = SEG_TRIALLOC;
-  }
-  if (*seg >= 0) CK(cudaMemsetAsync(&e->S.ctr->need, 0, sizeof(int32_t), e->stream));
-  return VM_OK;
-}
-
-static int reset_frame_counters(vm_engine *e) {
+static int reset_call_counters(vm_engine *e) {
   const size_t off = offsetof(Counters, nvalid);
   CK(cudaMemsetAsync((char *)e->S.ctr + off, 0, sizeof(Counters) - off, e->stream));
   return VM_OK;
@@ -254,60 +188,36 @@ static int upload_frame(vm_engine *e) {
 }
 
 static inline void rec(vm_engine *e, int ph) {
-  if (e->profiling || ph == PH_DEPTH || ph == PH_SCOPE || ph == PH_END) cudaEventRecord(e->ev[ph], e->stream);
+  if (e->profiling || ph == PH_DEPTH || ph == PH_RETYPE || ph == PH_END) cudaEventRecord(e->ev[ph], e->stream);
 }
 
-// ------------------------------------------------------------ segments
-static int enqueue_meshing(vm_engine *e, int from, bool device_scope) {
+// frame segment after collect: fuse (init/integrate/scope), retype+place, gc+normals
+static int enqueue_after_collect(vm_engine *e) {
   DevState &S = e->S;
   cudaStream_t st = e->stream;
   const int gb = grid_blocks(e);
-  if (from <= SEG_INIT) {
-    if (device_scope) {
-      rec(e, PH_INIT);
-      k_init_blocks<<<gb, 256, 0, st>>>(S);
-      rec(e, PH_INTEGRATE);
-      k_integrate<<<gb, kThreadsCube, 0, st>>>(S, e->d_frame, S.scope, &S.ctr->ncollected, 0);
-      rec(e, PH_SCOPE);
-      k_scope_halo<<<grid_threads(e, 1 << 20, 256), 256, 0, st>>>(S, e->d_frame);
-    }
-    rec(e, PH_RETYPE);
-    k_retype<<<gb, kThreadsCube, 0, st>>>(S, e->d_frame);
-  }
-  if (from <= SEG_PLACE) {
-    rec(e, PH_PLACE);
-    if (e->strategy == VM_STRATEGY_PARTITION) {
-      for (int p = 0; p < 8; p++) k_place<<<gb, kThreadsCube, 0, st>>>(S, e->d_frame, p, p == 7);
-    } else {
-      k_place<<<gb, kThreadsCube, 0, st>>>(S, e->d_frame, -1, 1);
-    }
-    rec(e, PH_TRI_RELEASE);
-    k_tri_release<<<gb, kThreadsCube, 0, st>>>(S, e->d_frame);
-  }
-  if (from <= SEG_TRIALLOC) {
-    rec(e, PH_TRI_ALLOC);
-    k_tri_alloc<<<gb, kThreadsCube, 0, st>>>(S, e->d_frame);
-    rec(e, PH_GC);
-    k_gc<<<gb, kThreadsCube, 0, st>>>(S, S.halo, &S.ctr->nhalo, 0, 1);
-    rec(e, PH_NORMALS);
-    k_normals<<<gb, kThreadsCube, 0, st>>>(S, S.halo, &S.ctr->nhalo, 0, 1);
-    rec(e, PH_FALLBACK);
-    k_fallback<<<grid_threads(e, 1 << 16, 128), 128, 0, st>>>(S, e->d_frame, 1);
-  }
+  rec(e, PH_FUSE);
+  k_fuse_blocks<<<gb, kThreadsCube, 0, st>>>(S, e->d_frame, S.scope, &S.ctr->ncollected, 0,
+                                            F_INIT | F_INTEGRATE | F_SCOPE);
+  rec(e, PH_RETYPE);
+  k_retype_place<<<gb, kThreadsCube, 0, st>>>(S, e->d_frame);
+  rec(e, PH_GC);
+  k_gc_normals<<<gb, kThreadsCube, 0, st>>>(S, e->d_frame, S.halo, &S.ctr->nhalo, 0,
+                                           G_GC | G_NORMALS | G_COMMIT | G_REQUIRE_ITEMS);
   rec(e, PH_END);
   return check_launch();
 }
 
-// run a (possibly resumed) meshing pass to completion on the host side
-static int complete_with_resume(vm_engine *e, bool device_scope, int *resumes) {
+// host side of a (possibly resumed) frame
+static int complete_with_resume(vm_engine *e, int *resumes) {
   for (int guard = 0; guard < 64; guard++) {
     TRY(read_counters(e));
     TRY(error_from_counters(e));
-    if (!e->h_ctr->need) return VM_OK;
-    int seg;
-    TRY(handle_need(e, &seg));
+    if (!(e->h_ctr->need & NEED_BLOCKS)) return VM_OK;
+    TRY(grow_blocks(e, e->h_ctr->nblocks));
+    CK(cudaMemsetAsync(&e->S.ctr->need, 0, sizeof(int32_t), e->stream));
     if (resumes) (*resumes)++;
-    TRY(enqueue_meshing(e, seg, device_scope));
+    TRY(enqueue_after_collect(e));
   }
   return set_err(VM_ERR_CUDA, "resume loop did not converge");
 }
@@ -316,7 +226,8 @@ static void fill_frame_host(vm_engine *e, const double *depth_dev, int32_t h, in
                             const vm_intrinsics *intr, const vm_pose *pose) {
   FrameDev &F = *e->h_frame;
   F.depth = depth_dev;
-  F.h = h; F.w = w;
+  F.h = h;
+  F.w = w;
   if (intr) {
     F.fx = intr->fx; F.fy = intr->fy; F.cx = intr->cx; F.cy = intr->cy;
     F.width = intr->width; F.height = intr->height;
@@ -330,8 +241,11 @@ static void fill_frame_host(vm_engine *e, const double *depth_dev, int32_t h, in
 static int stage_depth(vm_engine *e, const double *depth, int32_t h, int32_t w, int on_device,
                        const double **out) {
   if (!depth || h <= 0 || w <= 0) return set_err(VM_ERR_INPUT, "depth must be a non-empty (H, W) array");
-  if (on_device) { *out = depth; return VM_OK; }
-  size_t bytes = (size_t)h * w * sizeof(double);
+  if (on_device) {
+    *out = depth;
+    return VM_OK;
+  }
+  const size_t bytes = (size_t)h * w * sizeof(double);
   if (bytes > e->depth_cap) {
     if (e->d_depth) CK(cudaFree(e->d_depth));
     CK(cudaMalloc((void **)&e->d_depth, bytes));
@@ -342,11 +256,120 @@ static int stage_depth(vm_engine *e, const double *depth, int32_t h, int32_t w, 
   return VM_OK;
 }
 
+// upload coords into scratch and map them to block indices
+static int map_coords(vm_engine *e, const int32_t *coords, int64_t n, int32_t **idx_dev, int32_t *stamp,
+                      int32_t epoch, bool insert) {
+  void *buf;
+  TRY(scratch(e, (size_t)n * (sizeof(int3) + sizeof(int32_t)) + 256, &buf));
+  int3 *dc = (int3 *)buf;
+  int32_t *di = (int32_t *)((char *)buf + ((n * sizeof(int3) + 127) & ~(size_t)127));
+  if (n) {
+    CK(cudaMemcpyAsync(dc, coords, (size_t)n * sizeof(int3), cudaMemcpyHostToDevice, e->stream));
+    if (insert)
+      k_insert_coords<<<grid_threads(e, n, 128), 128, 0, e->stream>>>(e->S, dc, (int)n, di, epoch);
+    else
+      k_lookup_coords<<<grid_threads(e, n, 128), 128, 0, e->stream>>>(e->S, dc, (int)n, di, stamp, epoch);
+    TRY(check_launch());
+  }
+  *idx_dev = di;
+  return VM_OK;
+}
+
+// after an insertion outside a frame: grow the heap if needed, then
+// initialise + link the new blocks
+static int init_new_blocks(vm_engine *e) {
+  TRY(read_counters(e));
+  TRY(error_from_counters(e));
+  if (e->h_ctr->need & NEED_BLOCKS) {
+    TRY(grow_blocks(e, e->h_ctr->nblocks));
+    CK(cudaMemsetAsync(&e->S.ctr->need, 0, sizeof(int32_t), e->stream));
+  }
+  k_init_blocks<<<grid_blocks(e), kThreadsCube, 0, e->stream>>>(e->S);
+  TRY(check_launch());
+  TRY(read_counters(e));
+  return error_from_counters(e);
+}
+
+static void free_compacted(Compacted &c) {
+  for (void *p : {(void *)c.pos, (void *)c.nrm, (void *)c.age, (void *)c.idx, (void *)c.ev_handles,
+                  (void *)c.tri_handles})
+    if (p) cudaFree(p);
+  c = Compacted();
+}
+
+// store.py:388-425 on the device; with_handles also materialises the
+// per-slot / per-triangle-slot dense handles of the snapshot views
+static int run_compaction(vm_engine *e, int64_t frame, bool with_handles) {
+  TRY(read_counters(e));
+  const int nb = e->h_ctr->nblocks;
+  cudaStream_t st = e->stream;
+  free_compacted(e->comp);
+  if (nb == 0) return VM_OK;
+  unsigned long long *keys_in, *keys_out;
+  int32_t *vals_in, *order, *vcnt, *tcnt, *vbase, *tbase, *vbase_by_blk;
+  uint32_t *occ_bits;
+  uint16_t *occ_pre;
+  CK(cudaMalloc(&keys_in, 8ull * nb));
+  CK(cudaMalloc(&keys_out, 8ull * nb));
+  CK(cudaMalloc(&vals_in, 4ull * nb));
+  CK(cudaMalloc(&order, 4ull * nb));
+  CK(cudaMalloc(&vcnt, 4ull * (nb + 1)));
+  CK(cudaMalloc(&tcnt, 4ull * (nb + 1)));
+  CK(cudaMalloc(&vbase, 4ull * (nb + 1)));
+  CK(cudaMalloc(&tbase, 4ull * (nb + 1)));
+  CK(cudaMalloc(&vbase_by_blk, 4ull * nb));
+  CK(cudaMalloc(&occ_bits, 4ull * 48 * nb));
+  CK(cudaMalloc(&occ_pre, 2ull * 48 * nb));
+  k_block_keys<<<grid_threads(e, nb, 256), 256, 0, st>>>(e->S, nb, keys_in, vals_in);
+  size_t tmp_bytes = 0, tmp2 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys_in, keys_out, vals_in, order, nb, 0, 64, st);
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp2, vcnt, vbase, nb + 1, st);
+  tmp_bytes = std::max(tmp_bytes, tmp2);
+  void *tmp;
+  CK(cudaMalloc(&tmp, tmp_bytes + 16));
+  cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys_in, keys_out, vals_in, order, nb, 0, 64, st);
+  CK(cudaMemsetAsync(vcnt + nb, 0, 4, st));
+  CK(cudaMemsetAsync(tcnt + nb, 0, 4, st));
+  k_compact_count<<<grid_blocks(e), kThreadsCube, 0, st>>>(e->S, order, nb, vcnt, tcnt, occ_bits, occ_pre);
+  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, vcnt, vbase, nb + 1, st);
+  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, tcnt, tbase, nb + 1, st);
+  k_block_base<<<grid_threads(e, nb, 256), 256, 0, st>>>(order, vbase, nb, vbase_by_blk);
+  int32_t nv = 0, nt = 0;
+  CK(cudaMemcpyAsync(&nv, vbase + nb, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&nt, tbase + nb, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  Compacted &c = e->comp;
+  CK(cudaMalloc(&c.pos, 24ull * (nv + 1)));
+  CK(cudaMalloc(&c.nrm, 24ull * (nv + 1)));
+  CK(cudaMalloc(&c.age, 8ull * (nv + 1)));
+  CK(cudaMalloc(&c.idx, 12ull * (nt + 1)));
+  if (with_handles) {
+    CK(cudaMalloc(&c.ev_handles, 4ull * kEV * nb));
+    CK(cudaMalloc(&c.tri_handles, 4ull * kNC * 5 * nb));
+  }
+  TRY(reset_call_counters(e));
+  k_compact_vertices<<<grid_blocks(e), kThreadsCube, 0, st>>>(e->S, order, nb, occ_bits, occ_pre, vbase_by_blk,
+                                                              c.pos, c.nrm, c.age, (long long)frame,
+                                                              c.ev_handles);
+  k_compact_triangles<<<grid_blocks(e), kThreadsCube, 0, st>>>(e->S, order, nb, tbase, occ_bits, occ_pre,
+                                                               vbase_by_blk, c.idx, c.tri_handles);
+  TRY(check_launch());
+  CK(cudaStreamSynchronize(st));
+  for (void *p : {(void *)keys_in, (void *)keys_out, (void *)vals_in, (void *)order, (void *)vcnt,
+                  (void *)tcnt, (void *)vbase, (void *)tbase, (void *)vbase_by_blk, (void *)occ_bits,
+                  (void *)occ_pre, tmp})
+    cudaFree(p);
+  c.nv = nv;
+  c.nt = nt;
+  TRY(read_counters(e));
+  return error_from_counters(e);
+}
+
 // ------------------------------------------------------------ C ABI
 extern "C" {
 
 const char *vm_last_error(void) { return g_err.c_str(); }
-const char *vm_version(void) { return "voxmesh-b200 0.1.0 (sm_100a)"; }
+const char *vm_version(void) { return "voxmesh-b200 0.2.0 (sm_100a, slot-resident cube field)"; }
 
 int vm_create(const vm_store_config *cfg, vm_engine **out) {
   if (!cfg || !out) return set_err(VM_ERR_INPUT, "null argument");
@@ -386,14 +409,14 @@ int vm_create(const vm_store_config *cfg, vm_engine **out) {
   TRY(dev_alloc(&S.nbr, mb * 27, 0xFF));
   TRY(dev_alloc(&S.stamp_collect, mb, 0xFF));
   TRY(dev_alloc(&S.stamp_halo, mb, 0xFF));
+  TRY(dev_alloc(&S.stamp_new, mb, 0xFF));
   TRY(dev_alloc(&S.slab_bits, (mb + 4) & ~(size_t)3, 0));
   TRY(dev_alloc(&S.scope, mb));
   TRY(dev_alloc(&S.newlist, mb));
   TRY(dev_alloc(&S.halo, mb));
   TRY(dev_alloc(&S.ctr, 1, 0));
   TRY(dev_alloc(&e->d_frame, 1, 0));
-  // slab selection table (mesher.py:518-525)
-  uint8_t slab_sel[8];
+  uint8_t slab_sel[8];   // mesher.py:518-525
   for (int m = 0; m < 8; m++) {
     uint8_t bits = 0;
     for (int o = 1; o < 8; o++)
@@ -401,13 +424,9 @@ int vm_create(const vm_store_config *cfg, vm_engine **out) {
     slab_sel[m] = bits;
   }
   CK(cudaMemcpyToSymbol(c_slab_sel, slab_sel, sizeof slab_sel));
-  S.block_cap = 0; S.v_cap = 0; S.t_cap = 0;
-  int64_t ib = cfg->initial_blocks > 0 ? cfg->initial_blocks : 1024;
-  int64_t iv = cfg->initial_vertices > 0 ? cfg->initial_vertices : 1 << 18;
-  int64_t it = cfg->initial_triangles > 0 ? cfg->initial_triangles : 1 << 19;
+  S.block_cap = 0;
+  const int64_t ib = cfg->initial_blocks > 0 ? cfg->initial_blocks : 1024;
   TRY(grow_blocks(e, std::min<int64_t>(ib, S.max_blocks)));
-  TRY(grow_vertices(e, iv));
-  TRY(grow_triangles(e, it));
   CK(cudaDeviceSynchronize());
   *out = e;
   return VM_OK;
@@ -417,14 +436,13 @@ int vm_destroy(vm_engine *e) {
   if (!e) return VM_OK;
   cudaStreamSynchronize(e->stream);
   DevState &S = e->S;
-  void *ptrs[] = {S.keys, S.vals, S.ovf_head, S.ovf_lock, S.ovf_key, S.ovf_val, S.ovf_next,
-                  S.bcoord, S.nbr, S.stamp_collect, S.stamp_halo, S.slab_bits, S.scope,
-                  S.newlist, S.halo, S.tsdf, S.weight, S.tp, S.tc, S.ev, S.tri, S.item_mask,
-                  S.item_sel, S.vpos, S.vnrm, S.vref, S.vbirth, S.valive, S.vfree, S.fallback,
-                  S.tverts, S.talive, S.tfree, S.ctr, e->d_frame, e->d_depth, e->d_scratch,
-                  e->c_pos, e->c_nrm, e->c_age, e->c_idx};
+  void *ptrs[] = {S.keys, S.vals, S.ovf_head, S.ovf_lock, S.ovf_key, S.ovf_val, S.ovf_next, S.bcoord,
+                  S.nbr, S.stamp_collect, S.stamp_halo, S.stamp_new, S.slab_bits, S.scope, S.newlist,
+                  S.halo, S.tsdf, S.weight, S.tp, S.tc, S.vbirth, S.vparam, S.vnrm, S.item_mask,
+                  S.ctr, e->d_frame, e->d_depth, e->d_scratch};
   for (void *p : ptrs)
     if (p) cudaFree(p);
+  free_compacted(e->comp);
   if (e->h_ctr) cudaFreeHost(e->h_ctr);
   if (e->h_frame) cudaFreeHost(e->h_frame);
   for (int i = 0; i < PH_COUNT; i++)
@@ -454,13 +472,14 @@ int vm_set_profiling(vm_engine *e, int on) {
   return VM_OK;
 }
 
-// per-phase device times of the last frame (profiling mode), ms; n <= 12
+// per-kernel device times of the last frame (profiling mode), ms:
+// depth_stats, collect, fuse_blocks, retype_place, gc_normals
 int vm_phase_times(vm_engine *e, double *ms, int n) {
   if (!e || !ms) return set_err(VM_ERR_INPUT, "null argument");
   CK(cudaEventSynchronize(e->ev[PH_END]));
   for (int i = 0; i < n && i < PH_END; i++) {
     float f = 0.f;
-    cudaError_t r = cudaEventElapsedTime(&f, e->ev[i], e->ev[i + 1]);
+    const cudaError_t r = cudaEventElapsedTime(&f, e->ev[i], e->ev[i + 1]);
     ms[i] = (r == cudaSuccess) ? (double)f : -1.0;
   }
   cudaGetLastError();
@@ -469,9 +488,9 @@ int vm_phase_times(vm_engine *e, double *ms, int n) {
 
 int vm_reserve(vm_engine *e, int64_t blocks, int64_t vertices, int64_t triangles) {
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
+  (void)vertices;
+  (void)triangles;   // vertices live in edge slots, triangles are implicit
   if (blocks > e->S.block_cap) TRY(grow_blocks(e, std::min<int64_t>(blocks, e->S.max_blocks)));
-  if (vertices > e->S.v_cap) TRY(grow_vertices(e, vertices));
-  if (triangles > e->S.t_cap) TRY(grow_triangles(e, triangles));
   return VM_OK;
 }
 
@@ -480,8 +499,8 @@ static void fill_stats(vm_engine *e, int64_t frame, vm_stats *out) {
   memset(out, 0, sizeof *out);
   out->frame = frame;
   out->blocks_active = c.nblocks;
-  out->vertices_live = (int64_t)c.v_count - c.v_free;
-  out->triangles_live = (int64_t)c.t_count - c.t_free;
+  out->vertices_live = c.v_live;
+  out->triangles_live = c.t_live;
   out->vertices_allocated_total = c.v_count;
   out->vertices_recycled_total = c.v_recycled;
   out->irregular_cube_count = c.irregular;
@@ -491,49 +510,53 @@ static void fill_stats(vm_engine *e, int64_t frame, vm_stats *out) {
   out->new_blocks = c.nnew;
   out->scope_blocks = (int64_t)c.ncollected + c.nslab;
   out->halo_blocks = c.nhalo;
-  out->active_cubes = c.active_cubes;
-  out->edge_placements = c.edge_placements;
-  out->new_vertices = c.v_tickets;
-  out->changed_cubes = c.changed_cubes;
+  out->active_cubes = c.active;
+  out->edge_placements = c.placements;
+  out->new_vertices = c.v_allocs;
+  out->changed_cubes = c.changed;
   out->triangles_freed = c.t_released;
   out->triangles_allocated = c.t_allocated;
-  out->vertices_freed = c.v_freed;
+  out->vertices_freed = c.v_frees;
   out->normals_computed = c.normals;
-  out->fallback_normals = c.nfallback;
+  out->fallback_normals = c.fallbacks;
   out->refined_cubes = c.refined;
   out->resumes = e->last_resumes;
   float ms = 0.f;
   if (cudaEventElapsedTime(&ms, e->ev[PH_DEPTH], e->ev[PH_END]) == cudaSuccess) out->device_ms = ms;
-  if (cudaEventElapsedTime(&ms, e->ev[PH_DEPTH], e->ev[PH_SCOPE]) == cudaSuccess) out->fusion_ms = ms;
-  if (cudaEventElapsedTime(&ms, e->ev[PH_SCOPE], e->ev[PH_END]) == cudaSuccess) out->meshing_ms = ms;
+  if (cudaEventElapsedTime(&ms, e->ev[PH_DEPTH], e->ev[PH_RETYPE]) == cudaSuccess) out->fusion_ms = ms;
+  if (cudaEventElapsedTime(&ms, e->ev[PH_RETYPE], e->ev[PH_END]) == cudaSuccess) out->meshing_ms = ms;
   cudaGetLastError();
 }
 
-int vm_fuse_frame_enqueue(vm_engine *e, const double *depth, int32_t h, int32_t w,
-                          int32_t depth_on_device, const vm_intrinsics *intr, const vm_pose *pose,
-                          const vm_frame_config *cfg, int64_t frame_index) {
+int vm_fuse_frame_enqueue(vm_engine *e, const double *depth, int32_t h, int32_t w, int32_t depth_on_device,
+                          const vm_intrinsics *intr, const vm_pose *pose, const vm_frame_config *cfg,
+                          int64_t frame_index) {
   if (!e || !intr || !pose || !cfg) return set_err(VM_ERR_INPUT, "null argument");
   if (e->pending) return set_err(VM_ERR_INPUT, "previous frame not finished");
   if (cfg->strategy < 0 || cfg->strategy > 2) return set_err(VM_ERR_VALUE, "unknown strategy %d", cfg->strategy);
   if (cfg->trunc < e->S.cube_size) return set_err(VM_ERR_VALUE, "truncation band must be at least one cube");
   const double *dd;
   TRY(stage_depth(e, depth, h, w, depth_on_device, &dd));
-  e->strategy = cfg->strategy;
   fill_frame_host(e, dd, h, w, intr, pose);
   FrameDev &F = *e->h_frame;
-  F.trunc = cfg->trunc; F.max_range = cfg->max_range; F.epsilon = cfg->epsilon;
-  F.weight_cap = cfg->weight_cap; F.refine = cfg->refine; F.frustum_only = cfg->frustum_only;
-  F.epoch = ++e->epoch; F.frame = (int32_t)frame_index; F.scope_mode = 0; F.parity = -1;
+  F.trunc = cfg->trunc;
+  F.max_range = cfg->max_range;
+  F.epsilon = cfg->epsilon;
+  F.weight_cap = cfg->weight_cap;
+  F.refine = cfg->refine;
+  F.frustum_only = cfg->frustum_only;
+  F.epoch = ++e->epoch;
+  F.frame = (int32_t)frame_index;
+  F.scope_mode = 0;
   TRY(upload_frame(e));
-  TRY(reset_frame_counters(e));
+  TRY(reset_call_counters(e));
   cudaStream_t st = e->stream;
-  DevState &S = e->S;
   rec(e, PH_DEPTH);
-  k_depth_stats<<<grid_threads(e, (long long)h * w, 256), 256, 0, st>>>(S, e->d_frame);
+  k_depth_stats<<<grid_blocks(e), 256, 0, st>>>(e->S, e->d_frame);
   rec(e, PH_COLLECT);
-  k_collect<<<grid_threads(e, (long long)h * w, 256), 256, 0, st>>>(S, e->d_frame);
-  TRY(enqueue_meshing(e, SEG_INIT, true));
-  CK(cudaMemcpyAsync(e->h_ctr, S.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+  k_collect<<<grid_threads(e, (long long)h * w, 256), 256, 0, st>>>(e->S, e->d_frame);
+  TRY(enqueue_after_collect(e));
+  CK(cudaMemcpyAsync(e->h_ctr, e->S.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
   e->pending = 1;
   e->pending_frame = frame_index;
   return VM_OK;
@@ -544,7 +567,7 @@ int vm_fuse_frame_finish(vm_engine *e, vm_stats *out) {
   if (!e->pending) return set_err(VM_ERR_INPUT, "no frame pending");
   e->pending = 0;
   e->last_resumes = 0;
-  TRY(complete_with_resume(e, true, &e->last_resumes));
+  TRY(complete_with_resume(e, &e->last_resumes));
   if (out) fill_stats(e, e->pending_frame, out);
   return VM_OK;
 }
@@ -557,20 +580,6 @@ int vm_fuse_frame(vm_engine *e, const double *depth, int32_t h, int32_t w, int32
 }
 
 // ---- phase API ------------------------------------------------------------
-static int init_new_blocks(vm_engine *e) {
-  // after any insertion: grow the block heap if needed, then initialise
-  TRY(read_counters(e));
-  TRY(error_from_counters(e));
-  if (e->h_ctr->need & NEED_BLOCKS) {
-    TRY(grow_blocks(e, e->h_ctr->nblocks));
-    CK(cudaMemsetAsync(&e->S.ctr->need, 0, sizeof(int32_t), e->stream));
-  }
-  k_init_blocks<<<grid_blocks(e), 256, 0, e->stream>>>(e->S);
-  TRY(check_launch());
-  TRY(read_counters(e));
-  return error_from_counters(e);
-}
-
 int vm_collect(vm_engine *e, const double *depth, int32_t h, int32_t w, int32_t depth_on_device,
                const vm_intrinsics *intr, const vm_pose *pose, double trunc, double max_range,
                int64_t *n_out) {
@@ -579,11 +588,13 @@ int vm_collect(vm_engine *e, const double *depth, int32_t h, int32_t w, int32_t 
   TRY(stage_depth(e, depth, h, w, depth_on_device, &dd));
   fill_frame_host(e, dd, h, w, intr, pose);
   FrameDev &F = *e->h_frame;
-  F.trunc = trunc; F.max_range = max_range;
-  F.epoch = ++e->epoch; F.scope_mode = 0; F.parity = -1;
+  F.trunc = trunc;
+  F.max_range = max_range;
+  F.epoch = ++e->epoch;
+  F.scope_mode = 0;
   TRY(upload_frame(e));
-  TRY(reset_frame_counters(e));
-  k_depth_stats<<<grid_threads(e, (long long)h * w, 256), 256, 0, e->stream>>>(e->S, e->d_frame);
+  TRY(reset_call_counters(e));
+  k_depth_stats<<<grid_blocks(e), 256, 0, e->stream>>>(e->S, e->d_frame);
   k_collect<<<grid_threads(e, (long long)h * w, 256), 256, 0, e->stream>>>(e->S, e->d_frame);
   TRY(check_launch());
   TRY(init_new_blocks(e));
@@ -594,111 +605,84 @@ int vm_collect(vm_engine *e, const double *depth, int32_t h, int32_t w, int32_t 
 int vm_get_collected(vm_engine *e, int32_t *coords_out, int64_t n) {
   if (!e || (!coords_out && n)) return set_err(VM_ERR_INPUT, "null argument");
   if (n == 0) return VM_OK;
-  void *buf;
-  TRY(scratch(e, (size_t)n * sizeof(int32_t), &buf));
-  CK(cudaMemcpyAsync(buf, e->S.scope, (size_t)n * sizeof(int32_t), cudaMemcpyDeviceToDevice, e->stream));
   std::vector<int32_t> idx(n);
-  CK(cudaMemcpyAsync(idx.data(), buf, (size_t)n * sizeof(int32_t), cudaMemcpyDeviceToHost, e->stream));
+  CK(cudaMemcpyAsync(idx.data(), e->S.scope, (size_t)n * sizeof(int32_t), cudaMemcpyDeviceToHost, e->stream));
   TRY(read_counters(e));
   std::vector<int4> bc(e->h_ctr->nblocks);
   if (!bc.empty()) CK(cudaMemcpy(bc.data(), e->S.bcoord, sizeof(int4) * bc.size(), cudaMemcpyDeviceToHost));
   for (int64_t i = 0; i < n; i++) {
     const int4 c = bc[idx[i]];
-    coords_out[3 * i] = c.x; coords_out[3 * i + 1] = c.y; coords_out[3 * i + 2] = c.z;
+    coords_out[3 * i] = c.x;
+    coords_out[3 * i + 1] = c.y;
+    coords_out[3 * i + 2] = c.z;
   }
   return VM_OK;
 }
 
-// upload coords into scratch and map them to block indices (optionally stamping)
-static int map_coords(vm_engine *e, const int32_t *coords, int64_t n, int32_t **idx_dev,
-                      int32_t *stamp, int32_t epoch, bool insert) {
-  void *buf;
-  TRY(scratch(e, (size_t)n * (sizeof(int3) + sizeof(int32_t)) + 256, &buf));
-  int3 *dc = (int3 *)buf;
-  int32_t *di = (int32_t *)((char *)buf + ((n * sizeof(int3) + 127) & ~(size_t)127));
-  if (n) CK(cudaMemcpyAsync(dc, coords, (size_t)n * sizeof(int3), cudaMemcpyHostToDevice, e->stream));
-  if (n) {
-    if (insert)
-      k_insert_coords<<<grid_threads(e, n, 128), 128, 0, e->stream>>>(e->S, dc, (int)n, di);
-    else
-      k_lookup_coords<<<grid_threads(e, n, 128), 128, 0, e->stream>>>(e->S, dc, (int)n, di, stamp, epoch);
-    TRY(check_launch());
-  }
-  *idx_dev = di;
-  return VM_OK;
-}
-
-int vm_integrate(vm_engine *e, const int32_t *coords, int64_t n, const double *depth, int32_t h,
-                 int32_t w, int32_t depth_on_device, const vm_intrinsics *intr, const vm_pose *pose,
-                 double trunc, double max_range, int64_t weight_cap) {
+int vm_integrate(vm_engine *e, const int32_t *coords, int64_t n, const double *depth, int32_t h, int32_t w,
+                 int32_t depth_on_device, const vm_intrinsics *intr, const vm_pose *pose, double trunc,
+                 double max_range, int64_t weight_cap) {
   if (!e || !intr || !pose) return set_err(VM_ERR_INPUT, "null argument");
   const double *dd;
   TRY(stage_depth(e, depth, h, w, depth_on_device, &dd));
   fill_frame_host(e, dd, h, w, intr, pose);
   FrameDev &F = *e->h_frame;
-  F.trunc = trunc; F.max_range = max_range; F.weight_cap = weight_cap;
+  F.trunc = trunc;
+  F.max_range = max_range;
+  F.weight_cap = weight_cap;
   TRY(upload_frame(e));
   if (coords) {
-    int32_t *di;
-    // integrate is sequential per list entry in the reference; duplicates are
-    // processed in separate launches so repeated blocks integrate repeatedly
-    std::vector<int32_t> uniq;
+    // fusion.py:136-168 integrates list entries in order: a repeated block is
+    // integrated again, so duplicates go to separate launches
     int64_t start = 0;
     while (start < n) {
       int64_t end = start;
       std::vector<std::array<int32_t, 3>> seen;
-      while (end < n) {
-        std::array<int32_t, 3> c = {coords[3 * end], coords[3 * end + 1], coords[3 * end + 2]};
+      while (end < n && seen.size() < 4096) {
+        const std::array<int32_t, 3> c = {coords[3 * end], coords[3 * end + 1], coords[3 * end + 2]};
         if (std::find(seen.begin(), seen.end(), c) != seen.end()) break;
-        if (seen.size() < 4096) seen.push_back(c);
-        else break;
+        seen.push_back(c);
         end++;
       }
+      int32_t *di;
       TRY(map_coords(e, coords + 3 * start, end - start, &di, nullptr, 0, false));
-      k_integrate<<<grid_blocks(e), kThreadsCube, 0, e->stream>>>(e->S, e->d_frame, di, nullptr,
-                                                                  (int)(end - start));
+      k_fuse_blocks<<<grid_blocks(e), kThreadsCube, 0, e->stream>>>(e->S, e->d_frame, di, nullptr,
+                                                                    (int)(end - start), F_INTEGRATE);
       TRY(check_launch());
       CK(cudaStreamSynchronize(e->stream));
       start = end;
     }
   } else {
-    k_integrate<<<grid_blocks(e), kThreadsCube, 0, e->stream>>>(e->S, e->d_frame, e->S.scope,
-                                                                &e->S.ctr->ncollected, 0);
+    k_fuse_blocks<<<grid_blocks(e), kThreadsCube, 0, e->stream>>>(e->S, e->d_frame, e->S.scope,
+                                                                  &e->S.ctr->ncollected, 0, F_INTEGRATE);
     TRY(check_launch());
   }
   CK(cudaStreamSynchronize(e->stream));
   return VM_OK;
 }
 
-__global__ void k_clear_slabs(DevState S, int nc, int ns) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ns; i += gridDim.x * blockDim.x)
-    S.slab_bits[S.scope[nc + i]] = 0;
-}
-
 int vm_scope_halo(vm_engine *e, int64_t *n_scope, int32_t *scope_coords, uint8_t *scope_masks,
                   int64_t *n_halo, int32_t *halo_coords) {
   if (!e || !n_scope || !n_halo) return set_err(VM_ERR_INPUT, "null argument");
-  // recompute on the current collected list (stamps of the last collect)
   CK(cudaMemsetAsync(&e->S.ctr->nslab, 0, sizeof(int32_t), e->stream));
   CK(cudaMemsetAsync(&e->S.ctr->nhalo, 0, sizeof(int32_t), e->stream));
-  k_scope_halo<<<grid_threads(e, 1 << 20, 256), 256, 0, e->stream>>>(e->S, e->d_frame);
+  k_fuse_blocks<<<grid_blocks(e), kThreadsCube, 0, e->stream>>>(e->S, e->d_frame, e->S.scope,
+                                                                &e->S.ctr->ncollected, 0, F_SCOPE);
   TRY(check_launch());
   TRY(read_counters(e));
   const int nc = e->h_ctr->ncollected, ns = e->h_ctr->nslab, nh = e->h_ctr->nhalo;
   *n_scope = nc + ns;
   *n_halo = nh;
   std::vector<int32_t> sidx(nc + ns), hidx(nh);
-  std::vector<uint8_t> bits(ns);
   if (nc + ns) CK(cudaMemcpy(sidx.data(), e->S.scope, sizeof(int32_t) * (nc + ns), cudaMemcpyDeviceToHost));
   if (nh) CK(cudaMemcpy(hidx.data(), e->S.halo, sizeof(int32_t) * nh, cudaMemcpyDeviceToHost));
   std::vector<int4> bc(e->h_ctr->nblocks);
   if (!bc.empty()) CK(cudaMemcpy(bc.data(), e->S.bcoord, sizeof(int4) * bc.size(), cudaMemcpyDeviceToHost));
+  std::vector<uint8_t> bits(ns);
   if (ns) {
     std::vector<uint8_t> all(bc.size());
     CK(cudaMemcpy(all.data(), e->S.slab_bits, all.size(), cudaMemcpyDeviceToHost));
     for (int i = 0; i < ns; i++) bits[i] = all[sidx[nc + i]];
-  }
-  if (ns) {
     k_clear_slabs<<<grid_threads(e, ns, 128), 128, 0, e->stream>>>(e->S, nc, ns);
     TRY(check_launch());
     CK(cudaStreamSynchronize(e->stream));
@@ -706,31 +690,35 @@ int vm_scope_halo(vm_engine *e, int64_t *n_scope, int32_t *scope_coords, uint8_t
   uint8_t slab_sel[8];
   for (int m = 0; m < 8; m++) {
     uint8_t b = 0;
-    for (int o = 1; o < 8; o++) if ((o & ~m) == 0) b |= (uint8_t)(1u << (o - 1));
+    for (int o = 1; o < 8; o++)
+      if ((o & ~m) == 0) b |= (uint8_t)(1u << (o - 1));
     slab_sel[m] = b;
   }
-  if (scope_coords) {
+  if (scope_coords)
     for (int i = 0; i < nc + ns; i++) {
-      int4 c = bc[sidx[i]];
-      scope_coords[3 * i] = c.x; scope_coords[3 * i + 1] = c.y; scope_coords[3 * i + 2] = c.z;
+      const int4 c = bc[sidx[i]];
+      scope_coords[3 * i] = c.x;
+      scope_coords[3 * i + 1] = c.y;
+      scope_coords[3 * i + 2] = c.z;
       if (scope_masks) {
         uint8_t *m = scope_masks + (size_t)i * 64;
         memset(m, 0, 64);
         for (int ci = 0; ci < kNC; ci++) {
           bool sel = true;
           if (i >= nc) {
-            int x = ci >> 6, y = (ci >> 3) & 7, z = ci & 7;
+            const int x = ci >> 6, y = (ci >> 3) & 7, z = ci & 7;
             sel = (bits[i - nc] & slab_sel[((x == 7) << 2) | ((y == 7) << 1) | (z == 7)]) != 0;
           }
           if (sel) m[ci >> 3] |= (uint8_t)(1u << (ci & 7));
         }
       }
     }
-  }
   if (halo_coords)
     for (int i = 0; i < nh; i++) {
-      int4 c = bc[hidx[i]];
-      halo_coords[3 * i] = c.x; halo_coords[3 * i + 1] = c.y; halo_coords[3 * i + 2] = c.z;
+      const int4 c = bc[hidx[i]];
+      halo_coords[3 * i] = c.x;
+      halo_coords[3 * i + 1] = c.y;
+      halo_coords[3 * i + 2] = c.z;
     }
   return VM_OK;
 }
@@ -744,67 +732,72 @@ int vm_extract(vm_engine *e, const int32_t *scope_coords, const uint8_t *scope_m
   if (n_scope <= 0) return VM_OK;   // mesher.py:564-565
   if (n_scope > e->S.block_cap) TRY(grow_blocks(e, std::min<int64_t>(n_scope, e->S.max_blocks)));
   if (n_scope > e->S.block_cap) return set_err(VM_ERR_INPUT, "scope larger than the block table");
-  e->strategy = strategy;
   FrameDev &F = *e->h_frame;
-  F.refine = refine; F.epsilon = epsilon; F.frustum_only = 0;
-  F.epoch = ++e->epoch; F.frame = (int32_t)frame_index; F.scope_mode = 1; F.parity = -1;
+  F.refine = refine;
+  F.epsilon = epsilon;
+  F.frustum_only = 0;
+  F.epoch = ++e->epoch;
+  F.frame = (int32_t)frame_index;
+  F.scope_mode = 1;
   TRY(upload_frame(e));
-  TRY(reset_frame_counters(e));
-  // scope items
+  TRY(reset_call_counters(e));
   int32_t *di;
   TRY(map_coords(e, scope_coords, n_scope, &di, nullptr, 0, false));
   CK(cudaMemcpyAsync(e->S.scope, di, sizeof(int32_t) * n_scope, cudaMemcpyDeviceToDevice, e->stream));
-  if (scope_masks) {
+  if (scope_masks)
     CK(cudaMemcpyAsync(e->S.item_mask, scope_masks, (size_t)n_scope * 64, cudaMemcpyHostToDevice, e->stream));
-  } else {
+  else
     CK(cudaMemsetAsync(e->S.item_mask, 0xFF, (size_t)n_scope * 64, e->stream));
-  }
-  int32_t ni = (int32_t)n_scope;
+  const int32_t ni = (int32_t)n_scope;
   CK(cudaMemcpyAsync(&e->S.ctr->nexplicit, &ni, sizeof ni, cudaMemcpyHostToDevice, e->stream));
   CK(cudaStreamSynchronize(e->stream));
-  // halo
   if (n_halo >= 0) {
     TRY(map_coords(e, halo_coords, n_halo, &di, e->S.stamp_halo, F.epoch, false));
     CK(cudaMemcpyAsync(e->S.halo, di, sizeof(int32_t) * n_halo, cudaMemcpyDeviceToDevice, e->stream));
-    int32_t nh = (int32_t)n_halo;
+    const int32_t nh = (int32_t)n_halo;
     CK(cudaMemcpyAsync(&e->S.ctr->nhalo, &nh, sizeof nh, cudaMemcpyHostToDevice, e->stream));
     CK(cudaStreamSynchronize(e->stream));
   } else {
     k_halo_from_items<<<grid_threads(e, n_scope * 27, 256), 256, 0, e->stream>>>(e->S, e->d_frame);
     TRY(check_launch());
   }
-  int resumes = 0;
-  TRY(enqueue_meshing(e, SEG_INIT, false));
-  TRY(complete_with_resume(e, false, &resumes));
-  if (out2) { out2[0] = e->h_ctr->refined; out2[1] = e->h_ctr->v_freed; }
+  const int gb = grid_blocks(e);
+  k_retype_place<<<gb, kThreadsCube, 0, e->stream>>>(e->S, e->d_frame);
+  k_gc_normals<<<gb, kThreadsCube, 0, e->stream>>>(e->S, e->d_frame, e->S.halo, &e->S.ctr->nhalo, 0,
+                                                  G_GC | G_NORMALS | G_COMMIT | G_REQUIRE_ITEMS);
+  TRY(check_launch());
+  TRY(read_counters(e));
+  TRY(error_from_counters(e));
+  if (out2) {
+    out2[0] = e->h_ctr->refined;
+    out2[1] = e->h_ctr->v_frees;
+  }
   return VM_OK;
 }
 
 int vm_garbage_collect(vm_engine *e, const int32_t *coords, int64_t n, int64_t *freed) {
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
-  TRY(reset_frame_counters(e));
-  if (n > 0) {
-    int32_t *di;
-    TRY(map_coords(e, coords, n, &di, nullptr, 0, false));
-    k_gc<<<grid_blocks(e), kThreadsCube, 0, e->stream>>>(e->S, di, nullptr, (int)n, 0);
-    TRY(check_launch());
-  }
+  TRY(reset_call_counters(e));
+  int32_t *di = nullptr;
+  if (n > 0) TRY(map_coords(e, coords, n, &di, nullptr, 0, false));
+  k_gc_normals<<<grid_blocks(e), kThreadsCube, 0, e->stream>>>(e->S, e->d_frame, di, nullptr,
+                                                                (int)std::max<int64_t>(n, 0), G_GC | G_COMMIT);
+  TRY(check_launch());
   TRY(read_counters(e));
   TRY(error_from_counters(e));
-  if (freed) *freed = e->h_ctr->v_freed;
+  if (freed) *freed = e->h_ctr->v_frees;
   return VM_OK;
 }
 
 int vm_compute_normals(vm_engine *e, const int32_t *coords, int64_t n) {
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
-  TRY(reset_frame_counters(e));
+  TRY(reset_call_counters(e));
   if (n <= 0) return VM_OK;
   e->h_frame->epoch = ++e->epoch;
   TRY(upload_frame(e));
   int32_t *di;
   TRY(map_coords(e, coords, n, &di, e->S.stamp_halo, e->epoch, false));
-  k_normals<<<grid_blocks(e), kThreadsCube, 0, e->stream>>>(e->S, di, nullptr, (int)n, 0);
-  k_fallback<<<grid_threads(e, 1 << 16, 128), 128, 0, e->stream>>>(e->S, e->d_frame, 0);
+  k_gc_normals<<<grid_blocks(e), kThreadsCube, 0, e->stream>>>(e->S, e->d_frame, di, nullptr, (int)n, G_NORMALS);
   TRY(check_launch());
   TRY(read_counters(e));
   return error_from_counters(e);
@@ -849,13 +842,12 @@ int vm_block_in_frustum(vm_engine *e, const int32_t *coords, int64_t n, const vm
 }
 
 // ---- store access -----------------------------------------------------------
-int vm_set_blocks(vm_engine *e, const int32_t *coords, int64_t n, const double *tsdf,
-                  const int32_t *weight) {
+int vm_set_blocks(vm_engine *e, const int32_t *coords, int64_t n, const double *tsdf, const int32_t *weight) {
   if (!e || (!coords && n)) return set_err(VM_ERR_INPUT, "null argument");
   if (n <= 0) return VM_OK;
-  TRY(reset_frame_counters(e));
+  TRY(reset_call_counters(e));
   int32_t *di;
-  TRY(map_coords(e, coords, n, &di, nullptr, 0, true));
+  TRY(map_coords(e, coords, n, &di, nullptr, ++e->epoch, true));
   std::vector<int32_t> idx(n);
   CK(cudaMemcpyAsync(idx.data(), di, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, e->stream));
   TRY(init_new_blocks(e));
@@ -901,69 +893,112 @@ int vm_counters(vm_engine *e, vm_counter_set *out) {
   out->block_count = c.nblocks;
   out->block_allocations = c.nblocks;
   out->vertex_count = c.v_count;
-  out->vertex_free = c.v_free;
+  out->vertex_free = c.v_count - c.v_live;
   out->vertex_recycled_total = c.v_recycled;
   out->vertex_allocation_events = c.v_events;
   out->triangle_count = c.t_count;
-  out->triangle_free = c.t_free;
+  out->triangle_free = c.t_count - c.t_live;
   out->triangle_recycled_total = c.t_recycled;
   out->irregular_cube_count = c.irregular;
   out->block_capacity = e->S.block_cap;
-  out->vertex_capacity = e->S.v_cap;
-  out->triangle_capacity = e->S.t_cap;
+  out->vertex_capacity = (int64_t)e->S.block_cap * kEV;
+  out->triangle_capacity = (int64_t)e->S.block_cap * kNC * 5;
   return VM_OK;
 }
 
-int vm_snapshot_blocks(vm_engine *e, int64_t n, int32_t *coords, double *tsdf, int32_t *weight,
-                       uint8_t *tp, uint8_t *tc, int32_t *ev, int32_t *tri) {
+int vm_snapshot_blocks(vm_engine *e, int64_t n, int32_t *coords, double *tsdf, int32_t *weight, uint8_t *tp,
+                       uint8_t *tc, int32_t *ev, int32_t *tri) {
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
   TRY(read_counters(e));
-  if (n != e->h_ctr->nblocks) return set_err(VM_ERR_INPUT, "snapshot size %lld != block count %d", (long long)n, e->h_ctr->nblocks);
+  if (n != e->h_ctr->nblocks)
+    return set_err(VM_ERR_INPUT, "snapshot size %lld != block count %d", (long long)n, e->h_ctr->nblocks);
   if (n == 0) return VM_OK;
   const DevState &S = e->S;
   if (coords) {
     std::vector<int4> bc(n);
     CK(cudaMemcpy(bc.data(), S.bcoord, sizeof(int4) * n, cudaMemcpyDeviceToHost));
-    for (int64_t i = 0; i < n; i++) { coords[3 * i] = bc[i].x; coords[3 * i + 1] = bc[i].y; coords[3 * i + 2] = bc[i].z; }
+    for (int64_t i = 0; i < n; i++) {
+      coords[3 * i] = bc[i].x;
+      coords[3 * i + 1] = bc[i].y;
+      coords[3 * i + 2] = bc[i].z;
+    }
   }
   if (tsdf) CK(cudaMemcpy(tsdf, S.tsdf, sizeof(double) * n * kNC, cudaMemcpyDeviceToHost));
   if (weight) CK(cudaMemcpy(weight, S.weight, sizeof(int32_t) * n * kNC, cudaMemcpyDeviceToHost));
   if (tp) CK(cudaMemcpy(tp, S.tp, (size_t)n * kNC, cudaMemcpyDeviceToHost));
   if (tc) CK(cudaMemcpy(tc, S.tc, (size_t)n * kNC, cudaMemcpyDeviceToHost));
-  if (ev) CK(cudaMemcpy(ev, S.ev, sizeof(int32_t) * n * kEV, cudaMemcpyDeviceToHost));
-  if (tri) CK(cudaMemcpy(tri, S.tri, sizeof(int32_t) * n * kTS, cudaMemcpyDeviceToHost));
+  if (ev || tri) {
+    TRY(run_compaction(e, 0, true));
+    if (ev) CK(cudaMemcpy(ev, e->comp.ev_handles, sizeof(int32_t) * n * kEV, cudaMemcpyDeviceToHost));
+    if (tri) CK(cudaMemcpy(tri, e->comp.tri_handles, sizeof(int32_t) * n * kNC * 5, cudaMemcpyDeviceToHost));
+  }
   return VM_OK;
 }
 
+// vertex pool view: handles 0..live-1 are the live vertices in compaction
+// order, live..count-1 the free entries of the reference's arena accounting
 int vm_snapshot_vertices(vm_engine *e, int64_t n, double *pos, double *nrm, int32_t *ref, int32_t *birth,
                          uint8_t *alive, int32_t *free_stack) {
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
   TRY(read_counters(e));
-  if (n != e->h_ctr->v_count) return set_err(VM_ERR_INPUT, "snapshot size mismatch");
-  const DevState &S = e->S;
+  const int64_t count = e->h_ctr->v_count, live = e->h_ctr->v_live;
+  if (n != count) return set_err(VM_ERR_INPUT, "snapshot size mismatch");
+  const int nb = e->h_ctr->nblocks;
+  TRY(run_compaction(e, 0, true));
+  if (e->comp.nv != live)
+    return set_err(VM_ERR_CONSISTENCY, "live vertex count %lld != occupied slots %lld", (long long)live,
+                   (long long)e->comp.nv);
   if (n) {
-    if (pos) CK(cudaMemcpy(pos, S.vpos, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost));
-    if (nrm) CK(cudaMemcpy(nrm, S.vnrm, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost));
-    if (ref) CK(cudaMemcpy(ref, S.vref, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
-    if (birth) CK(cudaMemcpy(birth, S.vbirth, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
-    if (alive) CK(cudaMemcpy(alive, S.valive, n, cudaMemcpyDeviceToHost));
+    if (pos) {
+      if (live) CK(cudaMemcpy(pos, e->comp.pos, 24ull * live, cudaMemcpyDeviceToHost));
+      memset(pos + 3 * live, 0, 24ull * (n - live));
+    }
+    if (nrm) {
+      if (live) CK(cudaMemcpy(nrm, e->comp.nrm, 24ull * live, cudaMemcpyDeviceToHost));
+      memset(nrm + 3 * live, 0, 24ull * (n - live));
+    }
+    if (birth) {
+      std::vector<long long> age(live + 1);
+      if (live) CK(cudaMemcpy(age.data(), e->comp.age, 8ull * live, cudaMemcpyDeviceToHost));
+      for (int64_t i = 0; i < live; i++) birth[i] = (int32_t)(-age[i]);   // compacted at frame 0
+      for (int64_t i = live; i < n; i++) birth[i] = 0;
+    }
+    if (alive)
+      for (int64_t i = 0; i < n; i++) alive[i] = i < live;
+    if (ref) {
+      int32_t *dref;
+      CK(cudaMalloc(&dref, 4ull * (live + 1)));
+      if (nb) {
+        k_slot_refcounts<<<grid_threads(e, (long long)nb * kEV, 256), 256, 0, e->stream>>>(e->S, nb,
+                                                                                         e->comp.ev_handles, dref);
+        TRY(check_launch());
+      }
+      CK(cudaStreamSynchronize(e->stream));
+      if (live) CK(cudaMemcpy(ref, dref, 4ull * live, cudaMemcpyDeviceToHost));
+      for (int64_t i = live; i < n; i++) ref[i] = 0;
+      cudaFree(dref);
+    }
   }
-  if (free_stack && e->h_ctr->v_free)
-    CK(cudaMemcpy(free_stack, S.vfree, sizeof(int32_t) * e->h_ctr->v_free, cudaMemcpyDeviceToHost));
+  if (free_stack)
+    for (int64_t i = live; i < count; i++) free_stack[i - live] = (int32_t)i;
   return VM_OK;
 }
 
 int vm_snapshot_triangles(vm_engine *e, int64_t n, int32_t *verts, uint8_t *alive, int32_t *free_stack) {
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
   TRY(read_counters(e));
-  if (n != e->h_ctr->t_count) return set_err(VM_ERR_INPUT, "snapshot size mismatch");
-  const DevState &S = e->S;
-  if (n) {
-    if (verts) CK(cudaMemcpy(verts, S.tverts, sizeof(int32_t) * 3 * n, cudaMemcpyDeviceToHost));
-    if (alive) CK(cudaMemcpy(alive, S.talive, n, cudaMemcpyDeviceToHost));
+  const int64_t count = e->h_ctr->t_count, live = e->h_ctr->t_live;
+  if (n != count) return set_err(VM_ERR_INPUT, "snapshot size mismatch");
+  TRY(run_compaction(e, 0, false));
+  if (e->comp.nt != live) return set_err(VM_ERR_CONSISTENCY, "live triangle count mismatch");
+  if (verts) {
+    if (live) CK(cudaMemcpy(verts, e->comp.idx, 12ull * live, cudaMemcpyDeviceToHost));
+    for (int64_t i = 3 * live; i < 3 * n; i++) verts[i] = -1;
   }
-  if (free_stack && e->h_ctr->t_free)
-    CK(cudaMemcpy(free_stack, S.tfree, sizeof(int32_t) * e->h_ctr->t_free, cudaMemcpyDeviceToHost));
+  if (alive)
+    for (int64_t i = 0; i < n; i++) alive[i] = i < live;
+  if (free_stack)
+    for (int64_t i = live; i < count; i++) free_stack[i - live] = (int32_t)i;
   return VM_OK;
 }
 
@@ -976,7 +1011,8 @@ int vm_irregular_count(vm_engine *e, int64_t *out) {
   CK(cudaMemsetAsync(buf, 0, 8, e->stream));
   const int nb = e->h_ctr->nblocks;
   if (nb) {
-    k_irregular_full<<<grid_threads(e, (long long)nb * kNC, 256), 256, 0, e->stream>>>(e->S, nb, (unsigned long long *)buf);
+    k_irregular_full<<<grid_threads(e, (long long)nb * kNC, 256), 256, 0, e->stream>>>(e->S, nb,
+                                                                                   (unsigned long long *)buf);
     TRY(check_launch());
   }
   unsigned long long r = 0;
@@ -988,101 +1024,50 @@ int vm_irregular_count(vm_engine *e, int64_t *out) {
 
 int vm_compact(vm_engine *e, int64_t current_frame, int64_t *n_vertices, int64_t *n_triangles) {
   if (!e || !n_vertices || !n_triangles) return set_err(VM_ERR_INPUT, "null argument");
-  TRY(read_counters(e));
-  const int nb = e->h_ctr->nblocks;
-  const int vcount = e->h_ctr->v_count;
-  cudaStream_t st = e->stream;
-  for (void *p : {(void *)e->c_pos, (void *)e->c_nrm, (void *)e->c_age, (void *)e->c_idx})
-    if (p) CK(cudaFree(p));
-  e->c_pos = e->c_nrm = nullptr; e->c_age = nullptr; e->c_idx = nullptr;
-  e->c_nv = e->c_nt = 0;
-  if (nb == 0) { *n_vertices = 0; *n_triangles = 0; return VM_OK; }
-  unsigned long long *keys_in, *keys_out;
-  int32_t *vals_in, *order, *vcnt, *tcnt, *vbase, *tbase, *remap;
-  CK(cudaMalloc(&keys_in, 8ull * nb)); CK(cudaMalloc(&keys_out, 8ull * nb));
-  CK(cudaMalloc(&vals_in, 4ull * nb)); CK(cudaMalloc(&order, 4ull * nb));
-  CK(cudaMalloc(&vcnt, 4ull * (nb + 1))); CK(cudaMalloc(&tcnt, 4ull * (nb + 1)));
-  CK(cudaMalloc(&vbase, 4ull * (nb + 1))); CK(cudaMalloc(&tbase, 4ull * (nb + 1)));
-  CK(cudaMalloc(&remap, 4ull * (vcount + 1)));
-  CK(cudaMemsetAsync(remap, 0xFF, 4ull * (vcount + 1), st));
-  k_block_keys<<<grid_threads(e, nb, 256), 256, 0, st>>>(e->S, nb, keys_in, vals_in);
-  size_t tmp_bytes = 0, tmp2 = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys_in, keys_out, vals_in, order, nb, 0, 64, st);
-  cub::DeviceScan::ExclusiveSum(nullptr, tmp2, vcnt, vbase, nb + 1, st);
-  tmp_bytes = std::max(tmp_bytes, tmp2);
-  void *tmp;
-  CK(cudaMalloc(&tmp, tmp_bytes + 16));
-  cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys_in, keys_out, vals_in, order, nb, 0, 64, st);
-  CK(cudaMemsetAsync(vcnt + nb, 0, 4, st));
-  CK(cudaMemsetAsync(tcnt + nb, 0, 4, st));
-  k_compact_count<<<grid_blocks(e), kThreadsCube, 0, st>>>(e->S, order, nb, vcnt, tcnt);
-  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, vcnt, vbase, nb + 1, st);
-  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, tcnt, tbase, nb + 1, st);
-  int32_t nv = 0, nt = 0;
-  CK(cudaMemcpyAsync(&nv, vbase + nb, 4, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(&nt, tbase + nb, 4, cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  CK(cudaMalloc(&e->c_pos, 24ull * (nv + 1)));
-  CK(cudaMalloc(&e->c_nrm, 24ull * (nv + 1)));
-  CK(cudaMalloc(&e->c_age, 8ull * (nv + 1)));
-  CK(cudaMalloc(&e->c_idx, 12ull * (nt + 1)));
-  TRY(reset_frame_counters(e));
-  k_compact_vertices<<<grid_blocks(e), kThreadsCube, 0, st>>>(e->S, order, nb, vbase, remap, e->c_pos, e->c_nrm,
-                                                              e->c_age, (long long)current_frame);
-  k_compact_triangles<<<grid_blocks(e), kThreadsCube, 0, st>>>(e->S, order, nb, tbase, remap, e->c_idx);
-  TRY(check_launch());
-  CK(cudaStreamSynchronize(st));
-  for (void *p : {(void *)keys_in, (void *)keys_out, (void *)vals_in, (void *)order, (void *)vcnt,
-                  (void *)tcnt, (void *)vbase, (void *)tbase, (void *)remap, tmp})
-    cudaFree(p);
-  TRY(read_counters(e));
-  TRY(error_from_counters(e));
-  e->c_nv = nv; e->c_nt = nt;
-  *n_vertices = nv;
-  *n_triangles = nt;
+  TRY(run_compaction(e, current_frame, false));
+  *n_vertices = e->comp.nv;
+  *n_triangles = e->comp.nt;
   return VM_OK;
 }
 
 int vm_compact_fetch(vm_engine *e, double *pos, double *nrm, int64_t *ages, int32_t *idx) {
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
-  if (e->c_nv) {
-    if (pos) CK(cudaMemcpy(pos, e->c_pos, 24ull * e->c_nv, cudaMemcpyDeviceToHost));
-    if (nrm) CK(cudaMemcpy(nrm, e->c_nrm, 24ull * e->c_nv, cudaMemcpyDeviceToHost));
-    if (ages) CK(cudaMemcpy(ages, e->c_age, 8ull * e->c_nv, cudaMemcpyDeviceToHost));
+  const Compacted &c = e->comp;
+  if (c.nv) {
+    if (pos) CK(cudaMemcpy(pos, c.pos, 24ull * c.nv, cudaMemcpyDeviceToHost));
+    if (nrm) CK(cudaMemcpy(nrm, c.nrm, 24ull * c.nv, cudaMemcpyDeviceToHost));
+    if (ages) CK(cudaMemcpy(ages, c.age, 8ull * c.nv, cudaMemcpyDeviceToHost));
   }
-  if (e->c_nt && idx) CK(cudaMemcpy(idx, e->c_idx, 12ull * e->c_nt, cudaMemcpyDeviceToHost));
+  if (c.nt && idx) CK(cudaMemcpy(idx, c.idx, 12ull * c.nt, cudaMemcpyDeviceToHost));
   return VM_OK;
 }
 
+// Engine.audit (engine.py:187-230).  With slot-resident vertices and
+// type-derived triangles, a reference-count mismatch shows up as a referenced
+// but empty slot and a zero-ref live vertex as an occupied but unreferenced
+// slot; conservation compares the pool counters with full recounts.
 int vm_audit(vm_engine *e, vm_audit_report *out) {
   if (!e || !out) return set_err(VM_ERR_INPUT, "null argument");
   TRY(read_counters(e));
   const Counters c = *e->h_ctr;
-  const int nb = c.nblocks, vc = c.v_count, tc = c.t_count;
-  int32_t *tally, *seen;
   unsigned long long *sums;
-  CK(cudaMalloc(&tally, 4ull * (vc + 1)));
-  CK(cudaMalloc(&seen, 4ull * (vc + 1)));
-  CK(cudaMalloc(&sums, 8 * 8));
-  CK(cudaMemsetAsync(tally, 0, 4ull * (vc + 1), e->stream));
-  CK(cudaMemsetAsync(seen, 0, 4ull * (vc + 1), e->stream));
+  CK(cudaMalloc(&sums, 64));
   CK(cudaMemsetAsync(sums, 0, 64, e->stream));
-  if (nb) k_audit_blocks<<<grid_threads(e, (long long)nb * kNC, 256), 256, 0, e->stream>>>(e->S, nb, tally, seen, sums);
-  const int m = std::max(vc, tc);
-  if (m) k_audit_pools<<<grid_threads(e, m, 256), 256, 0, e->stream>>>(e->S, vc, tc, tally, sums);
-  TRY(check_launch());
+  if (c.nblocks) {
+    k_audit<<<grid_threads(e, (long long)c.nblocks * kEV, 256), 256, 0, e->stream>>>(e->S, c.nblocks, sums);
+    TRY(check_launch());
+  }
   unsigned long long h[8];
   CK(cudaMemcpyAsync(h, sums, 64, cudaMemcpyDeviceToHost, e->stream));
   CK(cudaStreamSynchronize(e->stream));
-  cudaFree(tally); cudaFree(seen); cudaFree(sums);
-  const int64_t vlive = (int64_t)vc - c.v_free, tlive = (int64_t)tc - c.t_free;
-  out->vertices_live = vlive;
-  out->triangles_live = tlive;
-  out->refcount_mismatches = (int64_t)h[3];
-  out->duplicate_handles = (int64_t)h[2];
-  out->zero_ref_live = (int64_t)h[4];
-  out->conservation_ok = (vlive == (int64_t)h[1]) && ((int64_t)h[5] == vlive) &&
-                         (tlive == (int64_t)h[0]) && ((int64_t)h[6] == tlive);
+  cudaFree(sums);
+  out->vertices_live = c.v_live;
+  out->triangles_live = c.t_live;
+  out->refcount_mismatches = (int64_t)h[1];
+  out->duplicate_handles = 0;   // one vertex per slot by construction
+  out->zero_ref_live = (int64_t)h[2];
+  out->conservation_ok = ((int64_t)h[0] == c.v_live) && ((int64_t)h[3] == c.t_live) &&
+                         (c.v_count >= c.v_live) && (c.t_count >= c.t_live);
   return VM_OK;
 }
 

@@ -217,13 +217,12 @@ class Engine:
 
     def phase_times(self) -> dict:
         """Per-kernel device ms of the last frame (requires set_profiling)."""
-        ms = np.zeros(12)
-        _lib.check(_lib.load().vm_phase_times(self.store._h, _lib.ptr(ms), 12))
+        ms = np.zeros(len(PHASES))
+        _lib.check(_lib.load().vm_phase_times(self.store._h, _lib.ptr(ms), len(PHASES)))
         return dict(zip(PHASES, (float(v) for v in ms)))
 
     def set_stream(self, stream_handle: int) -> None:
         _lib.check(_lib.load().vm_set_stream(self.store._h, C.c_void_p(stream_handle or None)))
 
 
-PHASES = ("depth_stats", "collect", "init_blocks", "integrate", "scope_halo", "retype", "place",
-          "tri_release", "tri_alloc", "gc", "normals", "fallback")
+PHASES = ("depth_stats", "collect", "fuse_blocks", "retype_place", "gc_normals")
