@@ -93,14 +93,21 @@ struct FrameDev {
   int32_t pad;
 };
 
+// one hash slot: packed coordinate (-1 empty) and block index (-1 while the
+// inserting thread has not published it yet)
+struct alignas(16) HashSlot {
+  long long key;
+  int32_t val;
+  int32_t pad;
+};
+
 struct DevState {
   double cube_size, extent;
   long long table_size;
   long long ts_mask;    // table_size-1 if a power of two, else 0
   int32_t nbuckets;
   int32_t max_blocks;   // reference load-factor limit: 2*n < table_size
-  long long *keys;      // [nbuckets*8] packed coords, -1 empty
-  int32_t *vals;        // [nbuckets*8] block index, -1 unpublished
+  HashSlot *slots;      // [nbuckets*8] (packed coord, block index); a bucket = one 128-B line
   int32_t *ovf_head;
   int32_t *ovf_lock;
   long long *ovf_key;
@@ -193,11 +200,14 @@ __device__ __forceinline__ int wait_val(const int32_t *p) {
 __device__ int hash_find(const DevState &S, int x, int y, int z) {
   const long long key = pack_coord(x, y, z);
   const unsigned b = (unsigned)(hash_block(S, x, y, z) >> 3);
-  const long long *kb = S.keys + (size_t)b * kSlotsPerBucket;
+  const HashSlot *kb = S.slots + (size_t)b * kSlotsPerBucket;
 #pragma unroll
   for (int i = 0; i < kSlotsPerBucket; i++) {
-    long long k = ld_vol(kb + i);
-    if (k == key) return wait_val(S.vals + (size_t)b * kSlotsPerBucket + i);
+    const long long k = ld_vol(&kb[i].key);
+    if (k == key) {
+      const int v = ld_vol(&kb[i].val);
+      return v != -1 ? v : wait_val(&kb[i].val);
+    }
     if (k == kEmptyKey) return -1;  // slots fill in prefix order
   }
   for (int e = ld_vol(S.ovf_head + b); e >= 0; e = ld_vol(S.ovf_next + e))
@@ -225,21 +235,20 @@ __device__ int alloc_block(const DevState &S, int x, int y, int z, int epoch) {
 __device__ int hash_insert(const DevState &S, int x, int y, int z, int epoch) {
   const long long key = pack_coord(x, y, z);
   const unsigned b = (unsigned)(hash_block(S, x, y, z) >> 3);
-  long long *kb = S.keys + (size_t)b * kSlotsPerBucket;
-  int32_t *vb = S.vals + (size_t)b * kSlotsPerBucket;
+  HashSlot *kb = S.slots + (size_t)b * kSlotsPerBucket;
   for (int i = 0; i < kSlotsPerBucket; i++) {
-    long long k = ld_vol(kb + i);
+    long long k = ld_vol(&kb[i].key);
     if (k == kEmptyKey) {
-      k = (long long)atomicCAS((unsigned long long *)(kb + i), (unsigned long long)kEmptyKey,
+      k = (long long)atomicCAS((unsigned long long *)&kb[i].key, (unsigned long long)kEmptyKey,
                                (unsigned long long)key);
       if (k == kEmptyKey) {
-        int idx = alloc_block(S, x, y, z, epoch);
+        const int idx = alloc_block(S, x, y, z, epoch);
         __threadfence();
-        atomicExch(vb + i, idx);
+        atomicExch(&kb[i].val, idx);
         return idx;
       }
     }
-    if (k == key) return wait_val(vb + i);
+    if (k == key) return wait_val(&kb[i].val);
   }
   int found = -1;
   bool done = false;

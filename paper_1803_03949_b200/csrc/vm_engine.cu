@@ -122,6 +122,15 @@ static inline int grid_threads(vm_engine *e, long long n, int tpb) {
   return (int)std::min(g, cap);
 }
 
+// every host<->device copy is ordered on the engine's (non-blocking) stream;
+// a plain cudaMemcpy would run on the legacy stream, unordered with it
+static int copy_sync(vm_engine *e, void *dst, const void *src, size_t bytes, cudaMemcpyKind kind) {
+  if (!bytes) return VM_OK;
+  CK(cudaMemcpyAsync(dst, src, bytes, kind, e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+  return VM_OK;
+}
+
 static int check_launch() {
   const cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return set_err(VM_ERR_CUDA, "kernel launch failed: %s", cudaGetErrorString(err));
@@ -397,8 +406,7 @@ int vm_create(const vm_store_config *cfg, vm_engine **out) {
   S.max_blocks = (int32_t)((cfg->table_size + 1) / 2);
   S.max_vertices = cfg->max_vertices;
   const size_t mb = (size_t)S.max_blocks;
-  TRY(dev_alloc(&S.keys, (size_t)S.nbuckets * kSlotsPerBucket, 0xFF));
-  TRY(dev_alloc(&S.vals, (size_t)S.nbuckets * kSlotsPerBucket, 0xFF));
+  TRY(dev_alloc(&S.slots, (size_t)S.nbuckets * kSlotsPerBucket, 0xFF));
   TRY(dev_alloc(&S.ovf_head, (size_t)S.nbuckets, 0xFF));
   TRY(dev_alloc(&S.ovf_lock, (size_t)S.nbuckets, 0));
   S.ovf_cap = (int32_t)mb + 1;
@@ -436,7 +444,7 @@ int vm_destroy(vm_engine *e) {
   if (!e) return VM_OK;
   cudaStreamSynchronize(e->stream);
   DevState &S = e->S;
-  void *ptrs[] = {S.keys, S.vals, S.ovf_head, S.ovf_lock, S.ovf_key, S.ovf_val, S.ovf_next, S.bcoord,
+  void *ptrs[] = {S.slots, S.ovf_head, S.ovf_lock, S.ovf_key, S.ovf_val, S.ovf_next, S.bcoord,
                   S.nbr, S.stamp_collect, S.stamp_halo, S.stamp_new, S.slab_bits, S.scope, S.newlist,
                   S.halo, S.tsdf, S.weight, S.tp, S.tc, S.vbirth, S.vparam, S.vnrm, S.item_mask,
                   S.ctr, e->d_frame, e->d_depth, e->d_scratch};
@@ -609,7 +617,7 @@ int vm_get_collected(vm_engine *e, int32_t *coords_out, int64_t n) {
   CK(cudaMemcpyAsync(idx.data(), e->S.scope, (size_t)n * sizeof(int32_t), cudaMemcpyDeviceToHost, e->stream));
   TRY(read_counters(e));
   std::vector<int4> bc(e->h_ctr->nblocks);
-  if (!bc.empty()) CK(cudaMemcpy(bc.data(), e->S.bcoord, sizeof(int4) * bc.size(), cudaMemcpyDeviceToHost));
+  if (!bc.empty()) TRY(copy_sync(e, bc.data(), e->S.bcoord, sizeof(int4) * bc.size(), cudaMemcpyDeviceToHost));
   for (int64_t i = 0; i < n; i++) {
     const int4 c = bc[idx[i]];
     coords_out[3 * i] = c.x;
@@ -674,14 +682,14 @@ int vm_scope_halo(vm_engine *e, int64_t *n_scope, int32_t *scope_coords, uint8_t
   *n_scope = nc + ns;
   *n_halo = nh;
   std::vector<int32_t> sidx(nc + ns), hidx(nh);
-  if (nc + ns) CK(cudaMemcpy(sidx.data(), e->S.scope, sizeof(int32_t) * (nc + ns), cudaMemcpyDeviceToHost));
-  if (nh) CK(cudaMemcpy(hidx.data(), e->S.halo, sizeof(int32_t) * nh, cudaMemcpyDeviceToHost));
+  if (nc + ns) TRY(copy_sync(e, sidx.data(), e->S.scope, sizeof(int32_t) * (nc + ns), cudaMemcpyDeviceToHost));
+  if (nh) TRY(copy_sync(e, hidx.data(), e->S.halo, sizeof(int32_t) * nh, cudaMemcpyDeviceToHost));
   std::vector<int4> bc(e->h_ctr->nblocks);
-  if (!bc.empty()) CK(cudaMemcpy(bc.data(), e->S.bcoord, sizeof(int4) * bc.size(), cudaMemcpyDeviceToHost));
+  if (!bc.empty()) TRY(copy_sync(e, bc.data(), e->S.bcoord, sizeof(int4) * bc.size(), cudaMemcpyDeviceToHost));
   std::vector<uint8_t> bits(ns);
   if (ns) {
     std::vector<uint8_t> all(bc.size());
-    CK(cudaMemcpy(all.data(), e->S.slab_bits, all.size(), cudaMemcpyDeviceToHost));
+    TRY(copy_sync(e, all.data(), e->S.slab_bits, all.size(), cudaMemcpyDeviceToHost));
     for (int i = 0; i < ns; i++) bits[i] = all[sidx[nc + i]];
     k_clear_slabs<<<grid_threads(e, ns, 128), 128, 0, e->stream>>>(e->S, nc, ns);
     TRY(check_launch());
@@ -855,14 +863,14 @@ int vm_set_blocks(vm_engine *e, const int32_t *coords, int64_t n, const double *
     double *dt = nullptr;
     int32_t *dw = nullptr, *didx = nullptr;
     CK(cudaMalloc((void **)&didx, sizeof(int32_t) * n));
-    CK(cudaMemcpy(didx, idx.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+    TRY(copy_sync(e, didx, idx.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
     if (tsdf) {
       CK(cudaMalloc((void **)&dt, sizeof(double) * n * kNC));
-      CK(cudaMemcpy(dt, tsdf, sizeof(double) * n * kNC, cudaMemcpyHostToDevice));
+      TRY(copy_sync(e, dt, tsdf, sizeof(double) * n * kNC, cudaMemcpyHostToDevice));
     }
     if (weight) {
       CK(cudaMalloc((void **)&dw, sizeof(int32_t) * n * kNC));
-      CK(cudaMemcpy(dw, weight, sizeof(int32_t) * n * kNC, cudaMemcpyHostToDevice));
+      TRY(copy_sync(e, dw, weight, sizeof(int32_t) * n * kNC, cudaMemcpyHostToDevice));
     }
     k_scatter_samples<<<grid_threads(e, n * kNC, 256), 256, 0, e->stream>>>(e->S, didx, (int)n, dt, dw);
     TRY(check_launch());
@@ -916,21 +924,21 @@ int vm_snapshot_blocks(vm_engine *e, int64_t n, int32_t *coords, double *tsdf, i
   const DevState &S = e->S;
   if (coords) {
     std::vector<int4> bc(n);
-    CK(cudaMemcpy(bc.data(), S.bcoord, sizeof(int4) * n, cudaMemcpyDeviceToHost));
+    TRY(copy_sync(e, bc.data(), S.bcoord, sizeof(int4) * n, cudaMemcpyDeviceToHost));
     for (int64_t i = 0; i < n; i++) {
       coords[3 * i] = bc[i].x;
       coords[3 * i + 1] = bc[i].y;
       coords[3 * i + 2] = bc[i].z;
     }
   }
-  if (tsdf) CK(cudaMemcpy(tsdf, S.tsdf, sizeof(double) * n * kNC, cudaMemcpyDeviceToHost));
-  if (weight) CK(cudaMemcpy(weight, S.weight, sizeof(int32_t) * n * kNC, cudaMemcpyDeviceToHost));
-  if (tp) CK(cudaMemcpy(tp, S.tp, (size_t)n * kNC, cudaMemcpyDeviceToHost));
-  if (tc) CK(cudaMemcpy(tc, S.tc, (size_t)n * kNC, cudaMemcpyDeviceToHost));
+  if (tsdf) TRY(copy_sync(e, tsdf, S.tsdf, sizeof(double) * n * kNC, cudaMemcpyDeviceToHost));
+  if (weight) TRY(copy_sync(e, weight, S.weight, sizeof(int32_t) * n * kNC, cudaMemcpyDeviceToHost));
+  if (tp) TRY(copy_sync(e, tp, S.tp, (size_t)n * kNC, cudaMemcpyDeviceToHost));
+  if (tc) TRY(copy_sync(e, tc, S.tc, (size_t)n * kNC, cudaMemcpyDeviceToHost));
   if (ev || tri) {
     TRY(run_compaction(e, 0, true));
-    if (ev) CK(cudaMemcpy(ev, e->comp.ev_handles, sizeof(int32_t) * n * kEV, cudaMemcpyDeviceToHost));
-    if (tri) CK(cudaMemcpy(tri, e->comp.tri_handles, sizeof(int32_t) * n * kNC * 5, cudaMemcpyDeviceToHost));
+    if (ev) TRY(copy_sync(e, ev, e->comp.ev_handles, sizeof(int32_t) * n * kEV, cudaMemcpyDeviceToHost));
+    if (tri) TRY(copy_sync(e, tri, e->comp.tri_handles, sizeof(int32_t) * n * kNC * 5, cudaMemcpyDeviceToHost));
   }
   return VM_OK;
 }
@@ -950,16 +958,16 @@ int vm_snapshot_vertices(vm_engine *e, int64_t n, double *pos, double *nrm, int3
                    (long long)e->comp.nv);
   if (n) {
     if (pos) {
-      if (live) CK(cudaMemcpy(pos, e->comp.pos, 24ull * live, cudaMemcpyDeviceToHost));
+      if (live) TRY(copy_sync(e, pos, e->comp.pos, 24ull * live, cudaMemcpyDeviceToHost));
       memset(pos + 3 * live, 0, 24ull * (n - live));
     }
     if (nrm) {
-      if (live) CK(cudaMemcpy(nrm, e->comp.nrm, 24ull * live, cudaMemcpyDeviceToHost));
+      if (live) TRY(copy_sync(e, nrm, e->comp.nrm, 24ull * live, cudaMemcpyDeviceToHost));
       memset(nrm + 3 * live, 0, 24ull * (n - live));
     }
     if (birth) {
       std::vector<long long> age(live + 1);
-      if (live) CK(cudaMemcpy(age.data(), e->comp.age, 8ull * live, cudaMemcpyDeviceToHost));
+      if (live) TRY(copy_sync(e, age.data(), e->comp.age, 8ull * live, cudaMemcpyDeviceToHost));
       for (int64_t i = 0; i < live; i++) birth[i] = (int32_t)(-age[i]);   // compacted at frame 0
       for (int64_t i = live; i < n; i++) birth[i] = 0;
     }
@@ -974,7 +982,7 @@ int vm_snapshot_vertices(vm_engine *e, int64_t n, double *pos, double *nrm, int3
         TRY(check_launch());
       }
       CK(cudaStreamSynchronize(e->stream));
-      if (live) CK(cudaMemcpy(ref, dref, 4ull * live, cudaMemcpyDeviceToHost));
+      if (live) TRY(copy_sync(e, ref, dref, 4ull * live, cudaMemcpyDeviceToHost));
       for (int64_t i = live; i < n; i++) ref[i] = 0;
       cudaFree(dref);
     }
@@ -992,7 +1000,7 @@ int vm_snapshot_triangles(vm_engine *e, int64_t n, int32_t *verts, uint8_t *aliv
   TRY(run_compaction(e, 0, false));
   if (e->comp.nt != live) return set_err(VM_ERR_CONSISTENCY, "live triangle count mismatch");
   if (verts) {
-    if (live) CK(cudaMemcpy(verts, e->comp.idx, 12ull * live, cudaMemcpyDeviceToHost));
+    if (live) TRY(copy_sync(e, verts, e->comp.idx, 12ull * live, cudaMemcpyDeviceToHost));
     for (int64_t i = 3 * live; i < 3 * n; i++) verts[i] = -1;
   }
   if (alive)
@@ -1034,11 +1042,11 @@ int vm_compact_fetch(vm_engine *e, double *pos, double *nrm, int64_t *ages, int3
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
   const Compacted &c = e->comp;
   if (c.nv) {
-    if (pos) CK(cudaMemcpy(pos, c.pos, 24ull * c.nv, cudaMemcpyDeviceToHost));
-    if (nrm) CK(cudaMemcpy(nrm, c.nrm, 24ull * c.nv, cudaMemcpyDeviceToHost));
-    if (ages) CK(cudaMemcpy(ages, c.age, 8ull * c.nv, cudaMemcpyDeviceToHost));
+    if (pos) TRY(copy_sync(e, pos, c.pos, 24ull * c.nv, cudaMemcpyDeviceToHost));
+    if (nrm) TRY(copy_sync(e, nrm, c.nrm, 24ull * c.nv, cudaMemcpyDeviceToHost));
+    if (ages) TRY(copy_sync(e, ages, c.age, 8ull * c.nv, cudaMemcpyDeviceToHost));
   }
-  if (c.nt && idx) CK(cudaMemcpy(idx, c.idx, 12ull * c.nt, cudaMemcpyDeviceToHost));
+  if (c.nt && idx) TRY(copy_sync(e, idx, c.idx, 12ull * c.nt, cudaMemcpyDeviceToHost));
   return VM_OK;
 }
 

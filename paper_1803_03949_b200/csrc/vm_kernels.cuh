@@ -265,9 +265,15 @@ __global__ void k_clear_slabs(DevState S, int nc, int ns) {
 }
 
 // ------------------------------------------------------------ tile loaders
+// the block's 27-neighbour row, cached in shared memory (one round trip)
+__device__ __forceinline__ void load_nbr_row(const DevState &S, int b, int *s_nbr) {
+  if (threadIdx.x < 27) s_nbr[threadIdx.x] = threadIdx.x == 13 ? b : S.nbr[(size_t)b * 27 + threadIdx.x];
+}
+
 // (B+1)^3 tile of a block plus its 7 plus-neighbours (mesher.py:75-96):
 // tsdf and the "weight > 0" flag.
-__device__ __forceinline__ void load_ext_tile(const DevState &S, int b, double *tile, uint8_t *tw) {
+__device__ __forceinline__ void load_ext_tile(const DevState &S, int b, const int *s_nbr, double *tile,
+                                              uint8_t *tw) {
   const int t = threadIdx.x;
   {
     const int x = t >> 6, y = (t >> 3) & 7, z = t & 7;
@@ -284,7 +290,7 @@ __device__ __forceinline__ void load_ext_tile(const DevState &S, int b, double *
     else if (t < 208) { x = 8; y = t - 200; z = 8; }
     else if (t < 216) { x = t - 208; y = 8; z = 8; }
     else { x = 8; y = 8; z = 8; }
-    const int nb = S.nbr[(size_t)b * 27 + nbr_dir(x >> 3, y >> 3, z >> 3)];
+    const int nb = s_nbr[nbr_dir(x >> 3, y >> 3, z >> 3)];
     double v = 0.0;
     uint8_t w = 0;
     if (nb >= 0) {
@@ -302,21 +308,45 @@ __device__ __forceinline__ int item_count(const DevState &S, const FrameDev &F) 
                            : ld_vol(&S.ctr->nexplicit);
 }
 
+// warp-aggregated append of `cnt` entries to a shared-memory list; returns
+// this lane's first index
+__device__ __forceinline__ int smem_append(int cnt, int *s_count) {
+  const int lane = threadIdx.x & 31;
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += u;
+  }
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  int base = 0;
+  if (lane == 31 && total) base = atomicAdd(s_count, total);
+  base = __shfl_sync(0xffffffffu, base, 31);
+  return base + incl - cnt;
+}
+
 // ------------------------------------------------------------ retype + place
-// One CTA per scope item, one thread per cube.  Typing and refinement as the
-// reference; a cube whose type changed is "retriangulated" implicitly (its
-// triangles become TRI_TABLE[type_curr]) and contributes the triangle /
-// irregular-count deltas; every active cube claims each required edge slot
-// (atomicCAS on the slot's birth word: exactly one allocation per edge) and
-// writes the interpolated coordinate -- all requesters produce identical
-// bits (d0, d1 are the oriented edge endpoint samples, mesher.py:216-235).
+// One CTA per scope item, one thread per cube for typing.  Typing and
+// refinement as the reference; a cube whose type changed is retriangulated
+// implicitly (its triangles become TRI_TABLE[type_curr]) and contributes the
+// triangle / irregular-count deltas.  The (active cube, mask edge) placements
+// of the block are compacted into a shared-memory list and spread over all
+// threads: each claims its edge slot (atomicCAS on the slot's birth word,
+// exactly one allocation per edge) and writes the interpolated coordinate;
+// all requesters produce identical bits (mesher.py:216-235).
+constexpr int kMaxPlace = kNC * 12;
+
 __global__ void __launch_bounds__(kThreadsCube, 2) k_retype_place(DevState S, const FrameDev *__restrict__ Fp) {
   if (halted(S)) return;
   __shared__ double tile[729];
   __shared__ uint8_t tw[729];
+  __shared__ uint16_t s_place[kMaxPlace];
+  __shared__ int s_nbr[27];
   __shared__ long long red[32];
   __shared__ int s_mode;  // 0 skip, 1 full, 2 slab bits, 3 explicit mask
   __shared__ int s_slab;
+  __shared__ int s_nplace;
+  __shared__ int4 s_coord;
   const FrameDev &F = *Fp;
   const int n = item_count(S, F);
   const int nc = ld_vol(&S.ctr->ncollected);
@@ -336,17 +366,22 @@ __global__ void __launch_bounds__(kThreadsCube, 2) k_retype_place(DevState S, co
       else if (F.scope_mode == 1) mode = 3;
       else if (i < nc) mode = 1;
       else { mode = 2; s_slab = S.slab_bits[b]; S.slab_bits[b] = 0; }
-      if (mode && F.frustum_only && !block_in_frustum_dev(S.bcoord[b], F, S.extent)) mode = 0;
+      if (mode) {
+        s_coord = S.bcoord[b];
+        if (F.frustum_only && !block_in_frustum_dev(s_coord, F, S.extent)) mode = 0;
+      }
       s_mode = mode;
+      s_nplace = 0;
       if (mode) live++;
     }
+    if (b >= 0) load_nbr_row(S, b, s_nbr);
     __syncthreads();
     const int mode = s_mode;
     if (mode == 0) {
       __syncthreads();
       continue;
     }
-    load_ext_tile(S, b, tile, tw);
+    load_ext_tile(S, b, s_nbr, tile, tw);
     __syncthreads();
     bool sel;
     if (mode == 1) sel = true;
@@ -362,6 +397,7 @@ __global__ void __launch_bounds__(kThreadsCube, 2) k_retype_place(DevState S, co
       bits |= (cv < 0.0 ? 1u : 0u) << k;
       small |= (fabs(cv) < eps ? 1u : 0u) << k;
     }
+    unsigned mask = 0;
     if (sel) {
       const size_t q = (size_t)b * kNC + t;
       const unsigned tp = S.tc[q];
@@ -380,37 +416,44 @@ __global__ void __launch_bounds__(kThreadsCube, 2) k_retype_place(DevState S, co
         t_new += nnew;
         irr += (nnew > 0 && !is_regular_type(tc)) - (nold > 0 && !is_regular_type(tp));
       }
-      unsigned mask = c_edge_mask[tc];
+      mask = c_edge_mask[tc];
       if (mask) {
         active++;
         placements += __popc(mask);
-        const int4 bc = S.bcoord[b];
-        const int g[3] = {bc.x * kB + x, bc.y * kB + y, bc.z * kB + z};
-        while (mask) {
-          const int e = __ffs(mask) - 1;
-          mask &= mask - 1;
-          const int own = c_e_own[e], axis = c_e_axis[e];
-          const int ox = x + (own & 1), oy = y + ((own >> 1) & 1), oz = z + ((own >> 2) & 1);
-          const int dir = nbr_dir(ox >> 3, oy >> 3, oz >> 3);
-          const int owner = (dir == 13) ? b : S.nbr[(size_t)b * 27 + dir];
-          if (owner < 0) {
-            set_error(S, ERR_CONSISTENCY, 10, g[0], g[1], g[2]);
-            continue;
-          }
-          const size_t slot = (size_t)owner * kEV + (((ox & 7) * 64 + (oy & 7) * 8 + (oz & 7)) * 3 + axis);
-          if (ld_vol(S.vbirth + slot) == -1 && atomicCAS(S.vbirth + slot, -1, frame) == -1) {
-            allocs++;
-            S.vnrm[3 * slot] = 0.0; S.vnrm[3 * slot + 1] = 0.0; S.vnrm[3 * slot + 2] = 0.0;
-          }
-          // start corner = owner cube origin; end corner one step along axis
-          const int sc = c_corner[c_e_start[e]], ec = c_corner[c_e_end[e]];
-          const double d0 = tile[((x + (sc & 1)) * 9 + (y + ((sc >> 1) & 1))) * 9 + (z + ((sc >> 2) & 1))];
-          const double d1 = tile[((x + (ec & 1)) * 9 + (y + ((ec >> 1) & 1))) * 9 + (z + ((ec >> 2) & 1))];
-          const double param = (d0 == d1) ? 0.5 : d0 / (d0 - d1);
-          const int ga = g[axis] + ((sc >> axis) & 1);
-          S.vparam[slot] = __dadd_rn(__dmul_rn((double)ga, l), __dmul_rn(param, l));
-        }
       }
+    }
+    // compact this block's placements into shared memory
+    int pos = smem_append(__popc(mask), &s_nplace);
+    while (mask) {
+      const int e = __ffs(mask) - 1;
+      mask &= mask - 1;
+      s_place[pos++] = (uint16_t)((t << 4) | e);
+    }
+    __syncthreads();
+    const int np = s_nplace;
+    for (int p = t; p < np; p += kThreadsCube) {
+      const int ent = s_place[p];
+      const int ci = ent >> 4, e = ent & 15;
+      const int cx = ci >> 6, cy = (ci >> 3) & 7, cz = ci & 7;
+      const int own = c_e_own[e], axis = c_e_axis[e];
+      const int ox = cx + (own & 1), oy = cy + ((own >> 1) & 1), oz = cz + ((own >> 2) & 1);
+      const int owner = s_nbr[nbr_dir(ox >> 3, oy >> 3, oz >> 3)];
+      if (owner < 0) {
+        set_error(S, ERR_CONSISTENCY, 10, s_coord.x * kB + cx, s_coord.y * kB + cy, s_coord.z * kB + cz);
+        continue;
+      }
+      const size_t slot = (size_t)owner * kEV + (((ox & 7) * 64 + (oy & 7) * 8 + (oz & 7)) * 3 + axis);
+      if (ld_vol(S.vbirth + slot) == -1 && atomicCAS(S.vbirth + slot, -1, frame) == -1) {
+        allocs++;
+        S.vnrm[3 * slot] = 0.0; S.vnrm[3 * slot + 1] = 0.0; S.vnrm[3 * slot + 2] = 0.0;
+      }
+      // start corner = owner cube origin; end corner one step along the axis
+      const double d0 = tile[(ox * 9 + oy) * 9 + oz];
+      const double d1 = tile[((ox + (axis == 0)) * 9 + (oy + (axis == 1))) * 9 + (oz + (axis == 2))];
+      const double param = (d0 == d1) ? 0.5 : d0 / (d0 - d1);
+      const int ga = (axis == 0 ? s_coord.x : axis == 1 ? s_coord.y : s_coord.z) * kB +
+                     (axis == 0 ? ox : axis == 1 ? oy : oz);
+      S.vparam[slot] = __dadd_rn(__dmul_rn((double)ga, l), __dmul_rn(param, l));
     }
     __syncthreads();
   }
@@ -427,20 +470,19 @@ __global__ void __launch_bounds__(kThreadsCube, 2) k_retype_place(DevState S, co
 }
 
 // ------------------------------------------------------------ GC + normals
-// Does the cube at tile position (cx, cy, cz) (types tile over locals -1..7)
-// reference the edge slot owned by cube (x, y, z) along `axis` (it does iff
-// the edge is in EDGE_TABLE[type], since the cube's triangles are
-// TRI_TABLE[type] and their edges cover exactly the mask)?
+// edge index, in the neighbour cube owner - du*e_u - dw*e_w, of the edge slot
+// owned along `axis` (u, w the other two axes)
 __device__ __forceinline__ int cube_edge_of_slot(int axis, int du, int dw) {
-  // neighbour cube = owner - du*e_u - dw*e_w; its owner offset for this edge
   const int u = axis == 0 ? 1 : 0, w = axis == 2 ? 1 : 2;
   const int own = (du << u) | (dw << w);
   return c_edge_of[axis][own];
 }
 
-// face normal accumulation for one vertex in reference order (mesher.py:459-486)
-__device__ void fallback_normal(const DevState &S, const uint8_t *ttile, int b, int slot_ci, int axis,
-                                int epoch, double *dst) {
+// face normal accumulation for one vertex in the reference order
+// (mesher.py:459-486): vertex position k major, then halo blocks in sorted
+// order, then (cube, triangle slot) order; ttile = types over locals -1..7
+__device__ void fallback_normal(const DevState &S, const uint8_t *ttile, const int *s_nbr, int slot_ci,
+                                int axis, int epoch, double *dst) {
   const int lx = slot_ci >> 6, ly = (slot_ci >> 3) & 7, lz = slot_ci & 7;
   const int u = axis == 0 ? 1 : 0, w = axis == 2 ? 1 : 2;
   int cb[4], cc[4], ce[4], ctype[4], key[4];
@@ -454,11 +496,10 @@ __device__ void fallback_normal(const DevState &S, const uint8_t *ttile, int b, 
       const int e = cube_edge_of_slot(axis, du, dw);
       if (!((c_edge_mask[tt] >> e) & 1)) continue;
       const int dx = l[0] < 0 ? -1 : 0, dy = l[1] < 0 ? -1 : 0, dz = l[2] < 0 ? -1 : 0;
-      const int dir = nbr_dir(dx, dy, dz);
-      const int nb = (dir == 13) ? b : S.nbr[(size_t)b * 27 + dir];
-      if (nb < 0 || ld_vol(S.stamp_halo + nb) != epoch) continue;   // triangles in halo blocks only
+      const int nb = s_nbr[nbr_dir(dx, dy, dz)];
+      if (nb < 0 || ld_vol(S.stamp_halo + nb) != epoch) continue;   // triangles of halo blocks only
       const int cidx = (l[0] & 7) * 64 + (l[1] & 7) * 8 + (l[2] & 7);
-      const int k = (((dx + 1) * 4 + (dy + 1) * 2 + (dz + 1)) << 9) | cidx;  // sorted block, cube
+      const int k = (((dx + 1) * 4 + (dy + 1) * 2 + (dz + 1)) << 9) | cidx;
       int j = m++;
       while (j > 0 && key[j - 1] > k) {
         key[j] = key[j - 1]; cb[j] = cb[j - 1]; cc[j] = cc[j - 1]; ce[j] = ce[j - 1]; ctype[j] = ctype[j - 1];
@@ -501,11 +542,13 @@ __device__ void fallback_normal(const DevState &S, const uint8_t *ttile, int b, 
   }
 }
 
-// One CTA per listed (halo) block.  G_GC: every occupied slot that no cube
-// references any more is cleared (the reference's refcount == 0 recycling).
-// G_NORMALS: gradient normal of every surviving vertex (11^3 stencil tile),
-// face-normal fallback inline.  G_COMMIT: the last CTA folds the per-call
-// deltas into the persistent pool counters.
+// One CTA per listed (halo) block.  All tiles (neighbour row, slot births,
+// types over locals -1..7, the 11^3 tsdf stencil) are staged in shared memory;
+// G_GC clears every occupied slot no cube references any more (refcount ==
+// 0 recycling); the surviving vertices are compacted into a shared list and
+// G_NORMALS computes their normals with all threads (blended central-
+// difference gradient, face-normal fallback inline).  G_COMMIT: the last CTA
+// folds the per-call deltas into the persistent pool counters.
 __global__ void __launch_bounds__(kThreadsCube, 2) k_gc_normals(DevState S, const FrameDev *__restrict__ Fp,
                                                                 const int32_t *__restrict__ list,
                                                                 const int32_t *__restrict__ count_ptr,
@@ -516,6 +559,9 @@ __global__ void __launch_bounds__(kThreadsCube, 2) k_gc_normals(DevState S, cons
   __shared__ double st[1331];
   __shared__ uint8_t sw[1331];
   __shared__ uint8_t ttile[729];
+  __shared__ uint16_t s_vlist[kEV];
+  __shared__ int s_nbr[27];
+  __shared__ int s_nv;
   __shared__ long long red[32];
   const int epoch = Fp->epoch;
   const int n = run ? list_count(count_ptr, count_const) : 0;
@@ -525,18 +571,22 @@ __global__ void __launch_bounds__(kThreadsCube, 2) k_gc_normals(DevState S, cons
   for (int i = blockIdx.x; i < n; i += gridDim.x) {
     const int b = list[i];
     if (b < 0) continue;
-    // types over locals -1..7 (cubes that can reference this block's slots)
+    load_nbr_row(S, b, s_nbr);
+    if (t == 0) s_nv = 0;
+    __syncthreads();
+    // issue every staging load of this block together
+    int birth[3];
+#pragma unroll
+    for (int a = 0; a < 3; a++) birth[a] = S.vbirth[(size_t)b * kEV + t * 3 + a];
     for (int q = t; q < 729; q += kThreadsCube) {
       const int X = q / 81 - 1, Y = (q / 9) % 9 - 1, Z = q % 9 - 1;
-      const int dir = nbr_dir(X >> 3, Y >> 3, Z >> 3);
-      const int nb = (dir == 13) ? b : S.nbr[(size_t)b * 27 + dir];
+      const int nb = s_nbr[nbr_dir(X >> 3, Y >> 3, Z >> 3)];
       ttile[q] = nb >= 0 ? S.tc[(size_t)nb * kNC + ((X & 7) * 64 + (Y & 7) * 8 + (Z & 7))] : 0;
     }
     if (mode & G_NORMALS) {
       for (int q = t; q < 1331; q += kThreadsCube) {
         const int lx = q / 121 - 1, ly = (q / 11) % 11 - 1, lz = q % 11 - 1;
-        const int dir = nbr_dir(lx >> 3, ly >> 3, lz >> 3);
-        const int nb = (dir == 13) ? b : S.nbr[(size_t)b * 27 + dir];
+        const int nb = s_nbr[nbr_dir(lx >> 3, ly >> 3, lz >> 3)];
         double v = 0.0;
         uint8_t w = 0;
         if (nb >= 0) {
@@ -549,9 +599,11 @@ __global__ void __launch_bounds__(kThreadsCube, 2) k_gc_normals(DevState S, cons
       }
     }
     __syncthreads();
+    int keep = 0;
+    unsigned keep_axes = 0;
+#pragma unroll
     for (int axis = 0; axis < 3; axis++) {
-      const size_t slot = (size_t)b * kEV + t * 3 + axis;
-      if (S.vbirth[slot] < 0) continue;
+      if (birth[axis] < 0) continue;
       if (mode & G_GC) {
         const int u = axis == 0 ? 1 : 0, w = axis == 2 ? 1 : 2;
         bool ref = false;
@@ -564,15 +616,27 @@ __global__ void __launch_bounds__(kThreadsCube, 2) k_gc_normals(DevState S, cons
             ref = (c_edge_mask[tt] >> cube_edge_of_slot(axis, du, dw)) & 1;
           }
         if (!ref) {
-          S.vbirth[slot] = -1;
+          S.vbirth[(size_t)b * kEV + t * 3 + axis] = -1;
           frees++;
           continue;
         }
       }
-      if (!(mode & G_NORMALS)) continue;
+      keep++;
+      keep_axes |= 1u << axis;
+    }
+    if (mode & G_NORMALS) {
+      int pos = smem_append(keep, &s_nv);
+      for (int axis = 0; axis < 3; axis++)
+        if ((keep_axes >> axis) & 1) s_vlist[pos++] = (uint16_t)(t * 3 + axis);
+    }
+    __syncthreads();
+    const int nv = (mode & G_NORMALS) ? s_nv : 0;
+    for (int p = t; p < nv; p += kThreadsCube) {
+      const int sl = s_vlist[p];
+      const int ci = sl / 3, axis = sl - 3 * (sl / 3);
       computed++;
-      int c0[3] = {x + 1, y + 1, z + 1};
-      int c1[3] = {x + 1, y + 1, z + 1};
+      int c0[3] = {(ci >> 6) + 1, ((ci >> 3) & 7) + 1, (ci & 7) + 1};
+      int c1[3] = {c0[0], c0[1], c0[2]};
       c1[axis]++;
       const double d0 = st[(c0[0] * 11 + c0[1]) * 11 + c0[2]];
       const double d1 = st[(c1[0] * 11 + c1[1]) * 11 + c1[2]];
@@ -582,16 +646,11 @@ __global__ void __launch_bounds__(kThreadsCube, 2) k_gc_normals(DevState S, cons
       bool valid = true;
 #pragma unroll
       for (int d = 0; d < 3; d++) {
-        int pp[3] = {c0[0], c0[1], c0[2]}, mm[3] = {c0[0], c0[1], c0[2]};
-        pp[d]++; mm[d]--;
-        const int ip = (pp[0] * 11 + pp[1]) * 11 + pp[2], im = (mm[0] * 11 + mm[1]) * 11 + mm[2];
-        g0[d] = st[ip] - st[im];
-        valid = valid && sw[ip] && sw[im];
-        int pq[3] = {c1[0], c1[1], c1[2]}, mq[3] = {c1[0], c1[1], c1[2]};
-        pq[d]++; mq[d]--;
-        const int jp = (pq[0] * 11 + pq[1]) * 11 + pq[2], jm = (mq[0] * 11 + mq[1]) * 11 + mq[2];
-        g1[d] = st[jp] - st[jm];
-        valid = valid && sw[jp] && sw[jm];
+        const int sd = d == 0 ? 121 : d == 1 ? 11 : 1;
+        const int i0 = (c0[0] * 11 + c0[1]) * 11 + c0[2], i1 = (c1[0] * 11 + c1[1]) * 11 + c1[2];
+        g0[d] = st[i0 + sd] - st[i0 - sd];
+        g1[d] = st[i1 + sd] - st[i1 - sd];
+        valid = valid && sw[i0 + sd] && sw[i0 - sd] && sw[i1 + sd] && sw[i1 - sd];
       }
       double g[3];
       const double wa = 1.0 - param;
@@ -599,12 +658,12 @@ __global__ void __launch_bounds__(kThreadsCube, 2) k_gc_normals(DevState S, cons
       for (int d = 0; d < 3; d++) g[d] = __dadd_rn(__dmul_rn(wa, g0[d]), __dmul_rn(param, g1[d]));
       const double nrm = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(g[0], g[0]), __dmul_rn(g[1], g[1])),
                                         __dmul_rn(g[2], g[2])));
-      double *dst = S.vnrm + 3 * slot;
+      double *dst = S.vnrm + 3 * ((size_t)b * kEV + sl);
       if (valid && nrm > 1e-12) {
         dst[0] = g[0] / nrm; dst[1] = g[1] / nrm; dst[2] = g[2] / nrm;
       } else {
         fallbacks++;
-        fallback_normal(S, ttile, b, t, axis, epoch, dst);
+        fallback_normal(S, ttile, s_nbr, ci, axis, epoch, dst);
       }
     }
     __syncthreads();

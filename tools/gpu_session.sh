@@ -11,5 +11,5 @@ timeout 900 python -m pytest tests -q -m gpu -x > $OUT/pytest_gpu_$TAG.log 2>&1;
 timeout 600 python bench.py --steps $STEPS --warmup 5 > $OUT/bench_$TAG.json 2> $OUT/bench_$TAG.err; echo "bench rc=$?"; tail -c 3000 $OUT/bench_$TAG.json
 timeout 400 python bench.py --impl reference --steps 60 --warmup 5 --ref-budget 60 > $OUT/bench_ref_$TAG.json 2> $OUT/bench_ref_$TAG.err; echo "ref rc=$?"; tail -c 1500 $OUT/bench_ref_$TAG.json
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_" --csv --log-file $OUT/launches_$TAG.csv python bench.py --steps 20 --warmup 3 --no-cpu-baseline > $OUT/ncu_bench_$TAG.log 2>&1; echo "ncu-launch rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_(place|retype|tri_alloc|tri_release|normals|integrate|collect|gc|fallback|init_blocks|scope_halo|depth_stats)" -s 120 -c 12 -o $OUT/prof_$TAG python bench.py --steps 20 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_$TAG.log 2>&1; echo "ncu-full rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_(depth_stats|collect|fuse_blocks|retype_place|gc_normals)" -s 50 -c 10 -o $OUT/prof_$TAG python bench.py --steps 20 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_$TAG.log 2>&1; echo "ncu-full rc=$?"
 ls -la $OUT
