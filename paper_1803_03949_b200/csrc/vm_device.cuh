@@ -98,7 +98,7 @@ struct FrameDev {
 struct alignas(16) HashSlot {
   long long key;
   int32_t val;
-  int32_t pad;
+  int32_t pad;    // epoch in which the block was last collected
 };
 
 struct DevState {
@@ -113,6 +113,7 @@ struct DevState {
   long long *ovf_key;
   int32_t *ovf_val;
   int32_t *ovf_next;
+  int32_t *ovf_stamp;   // "collected" epoch of chain entries
   int32_t ovf_cap;
   // per-block metadata, sized max_blocks
   int4 *bcoord;
@@ -196,6 +197,35 @@ __device__ __forceinline__ int wait_val(const int32_t *p) {
   return v;
 }
 
+// A probe result: block index (-1 absent, -2 capacity error), the slot's
+// "collected" epoch stamp as read, and where that stamp lives.
+struct HashRef {
+  int idx;
+  int stamp;
+  int32_t *stamp_ptr;
+};
+
+// get_block with the slot's stamp: every bucket slot is one 16-byte load
+// (key, index, stamp), so a probe is a single round trip in the common case
+__device__ HashRef hash_find_ref(const DevState &S, int x, int y, int z) {
+  const long long key = pack_coord(x, y, z);
+  const unsigned b = (unsigned)(hash_block(S, x, y, z) >> 3);
+  HashSlot *kb = S.slots + (size_t)b * kSlotsPerBucket;
+#pragma unroll
+  for (int i = 0; i < kSlotsPerBucket; i++) {
+    const int4 v = __ldcg(reinterpret_cast<const int4 *>(kb + i));
+    const long long k = (long long)(((unsigned long long)(unsigned)v.y << 32) | (unsigned)v.x);
+    if (k == key) {
+      const int idx = v.z != -1 ? v.z : wait_val(&kb[i].val);
+      return {idx, v.w, &kb[i].pad};
+    }
+    if (k == kEmptyKey) return {-1, -1, nullptr};   // slots fill in prefix order
+  }
+  for (int e = ld_vol(S.ovf_head + b); e >= 0; e = ld_vol(S.ovf_next + e))
+    if (ld_vol(S.ovf_key + e) == key) return {ld_vol(S.ovf_val + e), ld_vol(S.ovf_stamp + e), S.ovf_stamp + e};
+  return {-1, -1, nullptr};
+}
+
 // SpatialStore.get_block (store.py:280-294)
 __device__ int hash_find(const DevState &S, int x, int y, int z) {
   const long long key = pack_coord(x, y, z);
@@ -232,7 +262,11 @@ __device__ int alloc_block(const DevState &S, int x, int y, int z, int epoch) {
 // SpatialStore.get_or_allocate_block (store.py:296-320): lock-free in the
 // bucket (CAS the key, then publish the index) and lock-based in the bucket's
 // overflow chain.  Exactly one allocation per coordinate, no dropped inserts.
+__device__ HashRef hash_insert_ref(const DevState &S, int x, int y, int z, int epoch);
 __device__ int hash_insert(const DevState &S, int x, int y, int z, int epoch) {
+  return hash_insert_ref(S, x, y, z, epoch).idx;
+}
+__device__ HashRef hash_insert_ref(const DevState &S, int x, int y, int z, int epoch) {
   const long long key = pack_coord(x, y, z);
   const unsigned b = (unsigned)(hash_block(S, x, y, z) >> 3);
   HashSlot *kb = S.slots + (size_t)b * kSlotsPerBucket;
@@ -245,18 +279,19 @@ __device__ int hash_insert(const DevState &S, int x, int y, int z, int epoch) {
         const int idx = alloc_block(S, x, y, z, epoch);
         __threadfence();
         atomicExch(&kb[i].val, idx);
-        return idx;
+        return {idx, ld_vol(&kb[i].pad), &kb[i].pad};
       }
     }
-    if (k == key) return wait_val(&kb[i].val);
+    if (k == key) return {wait_val(&kb[i].val), ld_vol(&kb[i].pad), &kb[i].pad};
   }
+  int32_t *sp = nullptr;
   int found = -1;
   bool done = false;
   while (!done) {
     if (atomicCAS(S.ovf_lock + b, 0, 1) == 0) {
       __threadfence();
       for (int e = ld_vol(S.ovf_head + b); e >= 0; e = ld_vol(S.ovf_next + e))
-        if (ld_vol(S.ovf_key + e) == key) { found = ld_vol(S.ovf_val + e); break; }
+        if (ld_vol(S.ovf_key + e) == key) { found = ld_vol(S.ovf_val + e); sp = S.ovf_stamp + e; break; }
       if (found == -1) {
         int e = atomicAdd(&S.ctr->ovf_count, 1);
         if (e >= S.ovf_cap) {
@@ -266,6 +301,8 @@ __device__ int hash_insert(const DevState &S, int x, int y, int z, int epoch) {
           found = alloc_block(S, x, y, z, epoch);
           S.ovf_key[e] = key;
           S.ovf_val[e] = found;
+          S.ovf_stamp[e] = -1;
+          sp = S.ovf_stamp + e;
           S.ovf_next[e] = S.ovf_head[b];
           __threadfence();
           atomicExch(S.ovf_head + b, e);
@@ -278,7 +315,7 @@ __device__ int hash_insert(const DevState &S, int x, int y, int z, int epoch) {
       __nanosleep(64);
     }
   }
-  return found;
+  return {found, sp ? ld_vol(sp) : -1, sp};
 }
 
 // ---------------------------------------------------------------- misc
@@ -361,6 +398,26 @@ __device__ __forceinline__ long long block_sum(long long v, long long *sh) {
     r = warp_sum(r);
   }
   return r;
+}
+
+// Block-wide sums of N counters in one pass (one barrier pair), then one
+// atomicAdd per counter: thread k < N adds vals[k] to dst[k] (null = skip).
+// `sh` must hold 32 * N entries.
+template <int N>
+__device__ __forceinline__ void block_add_counters(long long (&vals)[N], long long *sh, int64_t *const (&dst)[N]) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int k = 0; k < N; k++) vals[k] = warp_sum(vals[k]);
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < N; k++) sh[k * 32 + wid] = vals[k];
+  __syncthreads();
+  if (threadIdx.x < N) {
+    long long r = 0;
+    for (int w = 0; w < nw; w++) r += sh[threadIdx.x * 32 + w];
+    if (r && dst[threadIdx.x]) atomicAdd((unsigned long long *)dst[threadIdx.x], (unsigned long long)r);
+  }
 }
 
 // vertex position from its slot (mesher.py:216-235): every coordinate is

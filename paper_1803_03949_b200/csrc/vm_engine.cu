@@ -63,8 +63,7 @@ struct vm_engine {
   vm_store_config cfg{};
   DevState S{};
   Counters *h_ctr = nullptr;   // pinned mirror
-  FrameDev *d_frame = nullptr;
-  FrameDev *h_frame = nullptr; // pinned
+  FrameDev *h_frame = nullptr; // pinned; passed by value to every kernel
   double *d_depth = nullptr;
   size_t depth_cap = 0;
   cudaStream_t stream = nullptr;
@@ -191,11 +190,6 @@ static int reset_call_counters(vm_engine *e) {
   return VM_OK;
 }
 
-static int upload_frame(vm_engine *e) {
-  CK(cudaMemcpyAsync(e->d_frame, e->h_frame, sizeof(FrameDev), cudaMemcpyHostToDevice, e->stream));
-  return VM_OK;
-}
-
 static inline void rec(vm_engine *e, int ph) {
   if (e->profiling || ph == PH_DEPTH || ph == PH_RETYPE || ph == PH_END) cudaEventRecord(e->ev[ph], e->stream);
 }
@@ -206,12 +200,12 @@ static int enqueue_after_collect(vm_engine *e) {
   cudaStream_t st = e->stream;
   const int gb = grid_blocks(e);
   rec(e, PH_FUSE);
-  k_fuse_blocks<<<gb, kThreadsCube, 0, st>>>(S, e->d_frame, S.scope, &S.ctr->ncollected, 0,
+  k_fuse_blocks<<<gb, kThreadsCube, 0, st>>>(S, *e->h_frame, S.scope, &S.ctr->ncollected, 0,
                                             F_INIT | F_INTEGRATE | F_SCOPE);
   rec(e, PH_RETYPE);
-  k_retype_place<<<gb, kThreadsCube, 0, st>>>(S, e->d_frame);
+  k_retype_place<<<gb, kThreadsCube, kRetypeSmem, st>>>(S, *e->h_frame);
   rec(e, PH_GC);
-  k_gc_normals<<<gb, kThreadsCube, 0, st>>>(S, e->d_frame, S.halo, &S.ctr->nhalo, 0,
+  k_gc_normals<<<gb, kThreadsCube, kGcSmem, st>>>(S, *e->h_frame, S.halo, &S.ctr->nhalo, 0,
                                            G_GC | G_NORMALS | G_COMMIT | G_REQUIRE_ITEMS);
   rec(e, PH_END);
   return check_launch();
@@ -413,6 +407,7 @@ int vm_create(const vm_store_config *cfg, vm_engine **out) {
   TRY(dev_alloc(&S.ovf_key, (size_t)S.ovf_cap));
   TRY(dev_alloc(&S.ovf_val, (size_t)S.ovf_cap));
   TRY(dev_alloc(&S.ovf_next, (size_t)S.ovf_cap));
+  TRY(dev_alloc(&S.ovf_stamp, (size_t)S.ovf_cap, 0xFF));
   TRY(dev_alloc(&S.bcoord, mb));
   TRY(dev_alloc(&S.nbr, mb * 27, 0xFF));
   TRY(dev_alloc(&S.stamp_collect, mb, 0xFF));
@@ -423,7 +418,6 @@ int vm_create(const vm_store_config *cfg, vm_engine **out) {
   TRY(dev_alloc(&S.newlist, mb));
   TRY(dev_alloc(&S.halo, mb));
   TRY(dev_alloc(&S.ctr, 1, 0));
-  TRY(dev_alloc(&e->d_frame, 1, 0));
   uint8_t slab_sel[8];   // mesher.py:518-525
   for (int m = 0; m < 8; m++) {
     uint8_t bits = 0;
@@ -432,6 +426,8 @@ int vm_create(const vm_store_config *cfg, vm_engine **out) {
     slab_sel[m] = bits;
   }
   CK(cudaMemcpyToSymbol(c_slab_sel, slab_sel, sizeof slab_sel));
+  CK(cudaFuncSetAttribute(k_retype_place, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRetypeSmem));
+  CK(cudaFuncSetAttribute(k_gc_normals, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGcSmem));
   S.block_cap = 0;
   const int64_t ib = cfg->initial_blocks > 0 ? cfg->initial_blocks : 1024;
   TRY(grow_blocks(e, std::min<int64_t>(ib, S.max_blocks)));
@@ -444,10 +440,10 @@ int vm_destroy(vm_engine *e) {
   if (!e) return VM_OK;
   cudaStreamSynchronize(e->stream);
   DevState &S = e->S;
-  void *ptrs[] = {S.slots, S.ovf_head, S.ovf_lock, S.ovf_key, S.ovf_val, S.ovf_next, S.bcoord,
+  void *ptrs[] = {S.slots, S.ovf_head, S.ovf_lock, S.ovf_key, S.ovf_val, S.ovf_next, S.ovf_stamp, S.bcoord,
                   S.nbr, S.stamp_collect, S.stamp_halo, S.stamp_new, S.slab_bits, S.scope, S.newlist,
                   S.halo, S.tsdf, S.weight, S.tp, S.tc, S.vbirth, S.vparam, S.vnrm, S.item_mask,
-                  S.ctr, e->d_frame, e->d_depth, e->d_scratch};
+                  S.ctr, e->d_depth, e->d_scratch};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   free_compacted(e->comp);
@@ -556,13 +552,12 @@ int vm_fuse_frame_enqueue(vm_engine *e, const double *depth, int32_t h, int32_t 
   F.epoch = ++e->epoch;
   F.frame = (int32_t)frame_index;
   F.scope_mode = 0;
-  TRY(upload_frame(e));
   TRY(reset_call_counters(e));
   cudaStream_t st = e->stream;
   rec(e, PH_DEPTH);
-  k_depth_stats<<<grid_blocks(e), 256, 0, st>>>(e->S, e->d_frame);
+  k_depth_stats<<<grid_blocks(e), 256, 0, st>>>(e->S, *e->h_frame);
   rec(e, PH_COLLECT);
-  k_collect<<<grid_threads(e, (long long)h * w, 256), 256, 0, st>>>(e->S, e->d_frame);
+  k_collect<<<grid_threads(e, (long long)h * w, 256), 256, 0, st>>>(e->S, *e->h_frame);
   TRY(enqueue_after_collect(e));
   CK(cudaMemcpyAsync(e->h_ctr, e->S.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
   e->pending = 1;
@@ -600,10 +595,9 @@ int vm_collect(vm_engine *e, const double *depth, int32_t h, int32_t w, int32_t 
   F.max_range = max_range;
   F.epoch = ++e->epoch;
   F.scope_mode = 0;
-  TRY(upload_frame(e));
   TRY(reset_call_counters(e));
-  k_depth_stats<<<grid_blocks(e), 256, 0, e->stream>>>(e->S, e->d_frame);
-  k_collect<<<grid_threads(e, (long long)h * w, 256), 256, 0, e->stream>>>(e->S, e->d_frame);
+  k_depth_stats<<<grid_blocks(e), 256, 0, e->stream>>>(e->S, *e->h_frame);
+  k_collect<<<grid_threads(e, (long long)h * w, 256), 256, 0, e->stream>>>(e->S, *e->h_frame);
   TRY(check_launch());
   TRY(init_new_blocks(e));
   if (n_out) *n_out = e->h_ctr->ncollected;
@@ -638,7 +632,6 @@ int vm_integrate(vm_engine *e, const int32_t *coords, int64_t n, const double *d
   F.trunc = trunc;
   F.max_range = max_range;
   F.weight_cap = weight_cap;
-  TRY(upload_frame(e));
   if (coords) {
     // fusion.py:136-168 integrates list entries in order: a repeated block is
     // integrated again, so duplicates go to separate launches
@@ -654,14 +647,14 @@ int vm_integrate(vm_engine *e, const int32_t *coords, int64_t n, const double *d
       }
       int32_t *di;
       TRY(map_coords(e, coords + 3 * start, end - start, &di, nullptr, 0, false));
-      k_fuse_blocks<<<grid_blocks(e), kThreadsCube, 0, e->stream>>>(e->S, e->d_frame, di, nullptr,
+      k_fuse_blocks<<<grid_blocks(e), kThreadsCube, 0, e->stream>>>(e->S, *e->h_frame, di, nullptr,
                                                                     (int)(end - start), F_INTEGRATE);
       TRY(check_launch());
       CK(cudaStreamSynchronize(e->stream));
       start = end;
     }
   } else {
-    k_fuse_blocks<<<grid_blocks(e), kThreadsCube, 0, e->stream>>>(e->S, e->d_frame, e->S.scope,
+    k_fuse_blocks<<<grid_blocks(e), kThreadsCube, 0, e->stream>>>(e->S, *e->h_frame, e->S.scope,
                                                                   &e->S.ctr->ncollected, 0, F_INTEGRATE);
     TRY(check_launch());
   }
@@ -674,7 +667,7 @@ int vm_scope_halo(vm_engine *e, int64_t *n_scope, int32_t *scope_coords, uint8_t
   if (!e || !n_scope || !n_halo) return set_err(VM_ERR_INPUT, "null argument");
   CK(cudaMemsetAsync(&e->S.ctr->nslab, 0, sizeof(int32_t), e->stream));
   CK(cudaMemsetAsync(&e->S.ctr->nhalo, 0, sizeof(int32_t), e->stream));
-  k_fuse_blocks<<<grid_blocks(e), kThreadsCube, 0, e->stream>>>(e->S, e->d_frame, e->S.scope,
+  k_fuse_blocks<<<grid_blocks(e), kThreadsCube, 0, e->stream>>>(e->S, *e->h_frame, e->S.scope,
                                                                 &e->S.ctr->ncollected, 0, F_SCOPE);
   TRY(check_launch());
   TRY(read_counters(e));
@@ -747,7 +740,6 @@ int vm_extract(vm_engine *e, const int32_t *scope_coords, const uint8_t *scope_m
   F.epoch = ++e->epoch;
   F.frame = (int32_t)frame_index;
   F.scope_mode = 1;
-  TRY(upload_frame(e));
   TRY(reset_call_counters(e));
   int32_t *di;
   TRY(map_coords(e, scope_coords, n_scope, &di, nullptr, 0, false));
@@ -766,12 +758,12 @@ int vm_extract(vm_engine *e, const int32_t *scope_coords, const uint8_t *scope_m
     CK(cudaMemcpyAsync(&e->S.ctr->nhalo, &nh, sizeof nh, cudaMemcpyHostToDevice, e->stream));
     CK(cudaStreamSynchronize(e->stream));
   } else {
-    k_halo_from_items<<<grid_threads(e, n_scope * 27, 256), 256, 0, e->stream>>>(e->S, e->d_frame);
+    k_halo_from_items<<<grid_threads(e, n_scope * 27, 256), 256, 0, e->stream>>>(e->S, *e->h_frame);
     TRY(check_launch());
   }
   const int gb = grid_blocks(e);
-  k_retype_place<<<gb, kThreadsCube, 0, e->stream>>>(e->S, e->d_frame);
-  k_gc_normals<<<gb, kThreadsCube, 0, e->stream>>>(e->S, e->d_frame, e->S.halo, &e->S.ctr->nhalo, 0,
+  k_retype_place<<<gb, kThreadsCube, kRetypeSmem, e->stream>>>(e->S, *e->h_frame);
+  k_gc_normals<<<gb, kThreadsCube, kGcSmem, e->stream>>>(e->S, *e->h_frame, e->S.halo, &e->S.ctr->nhalo, 0,
                                                   G_GC | G_NORMALS | G_COMMIT | G_REQUIRE_ITEMS);
   TRY(check_launch());
   TRY(read_counters(e));
@@ -788,7 +780,7 @@ int vm_garbage_collect(vm_engine *e, const int32_t *coords, int64_t n, int64_t *
   TRY(reset_call_counters(e));
   int32_t *di = nullptr;
   if (n > 0) TRY(map_coords(e, coords, n, &di, nullptr, 0, false));
-  k_gc_normals<<<grid_blocks(e), kThreadsCube, 0, e->stream>>>(e->S, e->d_frame, di, nullptr,
+  k_gc_normals<<<grid_blocks(e), kThreadsCube, kGcSmem, e->stream>>>(e->S, *e->h_frame, di, nullptr,
                                                                 (int)std::max<int64_t>(n, 0), G_GC | G_COMMIT);
   TRY(check_launch());
   TRY(read_counters(e));
@@ -802,10 +794,9 @@ int vm_compute_normals(vm_engine *e, const int32_t *coords, int64_t n) {
   TRY(reset_call_counters(e));
   if (n <= 0) return VM_OK;
   e->h_frame->epoch = ++e->epoch;
-  TRY(upload_frame(e));
   int32_t *di;
   TRY(map_coords(e, coords, n, &di, e->S.stamp_halo, e->epoch, false));
-  k_gc_normals<<<grid_blocks(e), kThreadsCube, 0, e->stream>>>(e->S, e->d_frame, di, nullptr, (int)n, G_NORMALS);
+  k_gc_normals<<<grid_blocks(e), kThreadsCube, kGcSmem, e->stream>>>(e->S, *e->h_frame, di, nullptr, (int)n, G_NORMALS);
   TRY(check_launch());
   TRY(read_counters(e));
   return error_from_counters(e);
@@ -836,12 +827,11 @@ int vm_block_in_frustum(vm_engine *e, const int32_t *coords, int64_t n, const vm
   if (!e || !coords || !pose || !intr || !out) return set_err(VM_ERR_INPUT, "null argument");
   if (n <= 0) return VM_OK;
   fill_frame_host(e, nullptr, 0, 0, intr, pose);
-  TRY(upload_frame(e));
   void *buf;
   const size_t o1 = ((size_t)n * sizeof(int3) + 255) & ~(size_t)255;
   TRY(scratch(e, o1 + n + 256, &buf));
   CK(cudaMemcpyAsync(buf, coords, (size_t)n * sizeof(int3), cudaMemcpyHostToDevice, e->stream));
-  k_frustum_eval<<<grid_threads(e, n, 128), 128, 0, e->stream>>>(e->S, e->d_frame, (int3 *)buf, (int)n,
+  k_frustum_eval<<<grid_threads(e, n, 128), 128, 0, e->stream>>>(e->S, *e->h_frame, (int3 *)buf, (int)n,
                                                                   (uint8_t *)buf + o1);
   TRY(check_launch());
   CK(cudaMemcpyAsync(out, (uint8_t *)buf + o1, n, cudaMemcpyDeviceToHost, e->stream));

@@ -15,6 +15,8 @@
 // Kernels after k_collect return at once if the block-heap guard tripped
 // (ctr->need) or an error was raised; the host grows the heap and resumes.
 #pragma once
+#include <cuda_pipeline.h>
+
 #include "vm_device.cuh"
 
 namespace vm {
@@ -24,8 +26,10 @@ constexpr int kThreadsCube = 512;   // one thread per cube of a block
 enum { F_INIT = 1, F_INTEGRATE = 2, F_SCOPE = 4 };
 enum { G_GC = 1, G_NORMALS = 2, G_COMMIT = 4, G_REQUIRE_ITEMS = 8 };
 
+// error and need are adjacent: one 8-byte load
 __device__ __forceinline__ bool halted(const DevState &S) {
-  return ld_vol(&S.ctr->need) != 0 || ld_vol(&S.ctr->error) != 0;
+  const int2 v = __ldcg(reinterpret_cast<const int2 *>(&S.ctr->error));
+  return (v.x | v.y) != 0;
 }
 
 __device__ __forceinline__ int list_count(const int32_t *count_ptr, int count_const) {
@@ -33,10 +37,9 @@ __device__ __forceinline__ int list_count(const int32_t *count_ptr, int count_co
 }
 
 // ------------------------------------------------------------ depth stats
-__global__ void __launch_bounds__(256) k_depth_stats(DevState S, const FrameDev *__restrict__ Fp) {
+__global__ void __launch_bounds__(256) k_depth_stats(DevState S, const FrameDev F) {
   __shared__ double smax[8];
   __shared__ int scnt[8];
-  const FrameDev &F = *Fp;
   const long long npix = (long long)F.h * F.w;
   double best = -1.0;
   int cnt = 0;
@@ -69,8 +72,7 @@ __global__ void __launch_bounds__(256) k_depth_stats(DevState S, const FrameDev 
 // One thread per pixel looping over the nsteps band samples.  Samples of a
 // warp falling in the same block are merged with __match_any_sync, so one
 // lane per distinct block probes the hash table.
-__global__ void __launch_bounds__(256) k_collect(DevState S, const FrameDev *__restrict__ Fp) {
-  const FrameDev &F = *Fp;
+__global__ void __launch_bounds__(256) k_collect(DevState S, const FrameDev F) {
   Counters *ctr = S.ctr;
   if (ld_vol(&ctr->nvalid) == 0) return;
   const double maxnorm = __longlong_as_double((long long)ld_vol(&ctr->maxnorm_bits));
@@ -111,11 +113,10 @@ __global__ void __launch_bounds__(256) k_collect(DevState S, const FrameDev *__r
       }
       const unsigned grp = __match_any_sync(0xffffffffu, key);
       if (key != kEmptyKey && lane == __ffs(grp) - 1) {
-        int idx = hash_find(S, c[0], c[1], c[2]);
-        if (idx == -1) idx = hash_insert(S, c[0], c[1], c[2], F.epoch);
-        if (idx >= 0 && ld_vol(S.stamp_collect + idx) != F.epoch &&
-            atomicExch(S.stamp_collect + idx, F.epoch) != F.epoch)
-          S.scope[atomicAdd(&ctr->ncollected, 1)] = idx;
+        HashRef r = hash_find_ref(S, c[0], c[1], c[2]);
+        if (r.idx == -1) r = hash_insert_ref(S, c[0], c[1], c[2], F.epoch);
+        if (r.idx >= 0 && r.stamp != F.epoch && atomicExch(r.stamp_ptr, F.epoch) != F.epoch)
+          S.scope[atomicAdd(&ctr->ncollected, 1)] = r.idx;
       }
     }
   }
@@ -178,14 +179,11 @@ __global__ void __launch_bounds__(kThreadsCube) k_init_blocks(DevState S) {
 //  F_SCOPE     27-neighbour halo marking and minus-slab scope marking
 //              (mesher.py:499-543), with hash lookups (links of blocks
 //              created in this launch are still being written).
-__global__ void __launch_bounds__(kThreadsCube) k_fuse_blocks(DevState S, const FrameDev *__restrict__ Fp,
+__global__ void __launch_bounds__(kThreadsCube) k_fuse_blocks(DevState S, const FrameDev F,
                                                               const int32_t *__restrict__ list,
                                                               const int32_t *__restrict__ count_ptr,
                                                               int count_const, int flags) {
   if (halted(S)) return;
-  __shared__ FrameDev F;
-  if (threadIdx.x == 0) F = *Fp;
-  __syncthreads();
   const int n = list_count(count_ptr, count_const);
   const int ci = threadIdx.x;
   const int lx = ci >> 6, ly = (ci >> 3) & 7, lz = ci & 7;
@@ -198,7 +196,12 @@ __global__ void __launch_bounds__(kThreadsCube) k_fuse_blocks(DevState S, const 
     if ((flags & (F_SCOPE | F_INIT)) && ci < 27) {
       const int t = ci;
       const int dx = t / 9 - 1, dy = (t / 3) % 3 - 1, dz = t % 3 - 1;
-      const int nb = (t == 13) ? b : hash_find(S, c.x + dx, c.y + dy, c.z + dz);
+      int nb = b, nb_collected = 1;
+      if (t != 13) {
+        const HashRef r = hash_find_ref(S, c.x + dx, c.y + dy, c.z + dz);
+        nb = r.idx;
+        nb_collected = r.stamp == F.epoch;
+      }
       if (fresh) {
         S.nbr[(size_t)b * 27 + t] = nb;
         if (nb >= 0 && t != 13) S.nbr[(size_t)nb * 27 + (26 - t)] = b;
@@ -207,7 +210,7 @@ __global__ void __launch_bounds__(kThreadsCube) k_fuse_blocks(DevState S, const 
         if (ld_vol(S.stamp_halo + nb) != F.epoch && atomicExch(S.stamp_halo + nb, F.epoch) != F.epoch)
           S.halo[atomicAdd(&S.ctr->nhalo, 1)] = nb;
         // minus neighbour n = c - o, o in {0,1}^3 \ 0, not itself collected
-        if (dx <= 0 && dy <= 0 && dz <= 0 && t != 13 && ld_vol(S.stamp_collect + nb) != F.epoch) {
+        if (dx <= 0 && dy <= 0 && dz <= 0 && t != 13 && !nb_collected) {
           const int o = (-dx) * 4 + (-dy) * 2 + (-dz);
           const unsigned sh = 8 * (nb & 3);
           const unsigned old = atomicOr((unsigned *)(S.slab_bits + (nb & ~3)), (1u << (o - 1)) << sh);
@@ -244,9 +247,9 @@ __global__ void __launch_bounds__(kThreadsCube) k_fuse_blocks(DevState S, const 
 }
 
 // halo of an explicit scope (extract_frame default, mesher.py:627-633)
-__global__ void k_halo_from_items(DevState S, const FrameDev *__restrict__ Fp) {
+__global__ void k_halo_from_items(DevState S, const FrameDev F) {
   if (halted(S)) return;
-  const int epoch = Fp->epoch;
+  const int epoch = F.epoch;
   const int ni = ld_vol(&S.ctr->nexplicit);
   for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < (long long)ni * 27;
        t += (long long)gridDim.x * blockDim.x) {
@@ -304,8 +307,9 @@ __device__ __forceinline__ void load_ext_tile(const DevState &S, int b, const in
 }
 
 __device__ __forceinline__ int item_count(const DevState &S, const FrameDev &F) {
-  return F.scope_mode == 0 ? ld_vol(&S.ctr->ncollected) + ld_vol(&S.ctr->nslab)
-                           : ld_vol(&S.ctr->nexplicit);
+  if (F.scope_mode != 0) return __ldcg(&S.ctr->nexplicit);
+  const int2 v = __ldcg(reinterpret_cast<const int2 *>(&S.ctr->ncollected));   // ncollected, nnew
+  return v.x + __ldcg(&S.ctr->nslab);
 }
 
 // warp-aggregated append of `cnt` entries to a shared-memory list; returns
@@ -326,28 +330,92 @@ __device__ __forceinline__ int smem_append(int cnt, int *s_count) {
 }
 
 // ------------------------------------------------------------ retype + place
-// One CTA per scope item, one thread per cube for typing.  Typing and
-// refinement as the reference; a cube whose type changed is retriangulated
-// implicitly (its triangles become TRI_TABLE[type_curr]) and contributes the
-// triangle / irregular-count deltas.  The (active cube, mask edge) placements
-// of the block are compacted into a shared-memory list and spread over all
-// threads: each claims its edge slot (atomicCAS on the slot's birth word,
-// exactly one allocation per edge) and writes the interpolated coordinate;
-// all requesters produce identical bits (mesher.py:216-235).
+// One CTA per scope item (persistent over the item list), one thread per cube
+// for typing.  Software-pipelined: while block i is typed and placed, the
+// neighbour row and the 9^3 tsdf/weight tile + type row of the CTA's next
+// block stream into the other shared-memory buffer with cp.async (LDGSTS).
+// Typing and refinement as the reference; a cube whose type changed is
+// retriangulated implicitly (its triangles become TRI_TABLE[type_curr]) and
+// contributes the triangle / irregular-count deltas.  The (active cube, mask
+// edge) placements are compacted in shared memory and spread over the CTA:
+// each claims its edge slot (atomicCAS on the slot's birth word -- exactly one
+// allocation per edge) and writes the interpolated coordinate; all requesters
+// produce identical bits (mesher.py:216-235).
 constexpr int kMaxPlace = kNC * 12;
 
-__global__ void __launch_bounds__(kThreadsCube, 2) k_retype_place(DevState S, const FrameDev *__restrict__ Fp) {
+struct RetypeBuf {
+  double tsdf[729];
+  int32_t w[729];
+  alignas(16) uint8_t tc[kNC];
+  int4 coord;
+  int nbr[27];
+  int b, mode, slab;
+};
+
+// stage A: resolve item i (scope index -> block, mode, coords, neighbour row)
+__device__ __forceinline__ void retype_resolve(const DevState &S, const FrameDev &F, int i, int nc,
+                                               RetypeBuf &B) {
+  const int t = threadIdx.x;
+  if (t < 32) {
+    const int b = S.scope[i];
+    if (t < 27) B.nbr[t] = (b < 0) ? -1 : (t == 13 ? b : S.nbr[(size_t)b * 27 + t]);
+    if (t == 27) {
+      int mode;
+      if (b < 0) mode = 0;
+      else if (F.scope_mode == 1) mode = 3;
+      else if (i < nc) mode = 1;
+      else { mode = 2; B.slab = S.slab_bits[b]; S.slab_bits[b] = 0; }
+      if (mode) {
+        B.coord = S.bcoord[b];
+        if (F.frustum_only && !block_in_frustum_dev(B.coord, F, S.extent)) mode = 0;
+      }
+      B.mode = mode;
+      B.b = b;
+    }
+  }
+}
+
+// stage B: issue the asynchronous copies of the item's tiles (needs B.nbr)
+__device__ __forceinline__ void retype_issue(const DevState &S, RetypeBuf &B) {
+  const int t = threadIdx.x;
+  if (B.mode == 0) return;
+  const int b = B.b;
+  {
+    const int x = t >> 6, y = (t >> 3) & 7, z = t & 7;
+    const int p = (x * 9 + y) * 9 + z;
+    __pipeline_memcpy_async(&B.tsdf[p], S.tsdf + (size_t)b * kNC + t, 8);
+    __pipeline_memcpy_async(&B.w[p], S.weight + (size_t)b * kNC + t, 4);
+  }
+  if (t < 32) __pipeline_memcpy_async(&B.tc[t * 16], S.tc + (size_t)b * kNC + t * 16, 16);
+  if (t < 217) {
+    int x, y, z;   // the 217 tile positions with max(x, y, z) == 8
+    if (t < 64) { x = 8; y = t >> 3; z = t & 7; }
+    else if (t < 128) { x = (t - 64) >> 3; y = 8; z = t & 7; }
+    else if (t < 192) { x = (t - 128) >> 3; y = t & 7; z = 8; }
+    else if (t < 200) { x = 8; y = 8; z = t - 192; }
+    else if (t < 208) { x = 8; y = t - 200; z = 8; }
+    else if (t < 216) { x = t - 208; y = 8; z = 8; }
+    else { x = 8; y = 8; z = 8; }
+    const int p = (x * 9 + y) * 9 + z;
+    const int nb = B.nbr[nbr_dir(x >> 3, y >> 3, z >> 3)];
+    if (nb >= 0) {
+      const size_t q = (size_t)nb * kNC + ((x & 7) * 64 + (y & 7) * 8 + (z & 7));
+      __pipeline_memcpy_async(&B.tsdf[p], S.tsdf + q, 8);
+      __pipeline_memcpy_async(&B.w[p], S.weight + q, 4);
+    } else {
+      B.tsdf[p] = 0.0;
+      B.w[p] = 0;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreadsCube, 2) k_retype_place(DevState S, const FrameDev F) {
   if (halted(S)) return;
-  __shared__ double tile[729];
-  __shared__ uint8_t tw[729];
-  __shared__ uint16_t s_place[kMaxPlace];
-  __shared__ int s_nbr[27];
-  __shared__ long long red[32];
-  __shared__ int s_mode;  // 0 skip, 1 full, 2 slab bits, 3 explicit mask
-  __shared__ int s_slab;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  RetypeBuf *bufs = reinterpret_cast<RetypeBuf *>(smem_raw);
+  uint16_t *s_place = reinterpret_cast<uint16_t *>(smem_raw + 2 * sizeof(RetypeBuf));
+  __shared__ long long red8[8 * 32];
   __shared__ int s_nplace;
-  __shared__ int4 s_coord;
-  const FrameDev &F = *Fp;
   const int n = item_count(S, F);
   const int nc = ld_vol(&S.ctr->ncollected);
   const int t = threadIdx.x;
@@ -358,55 +426,59 @@ __global__ void __launch_bounds__(kThreadsCube, 2) k_retype_place(DevState S, co
   const double eps = F.epsilon;
   long long allocs = 0, placements = 0, active = 0, changed = 0, t_rel = 0, t_new = 0, irr = 0,
             refined = 0, live = 0;
-  for (int i = blockIdx.x; i < n; i += gridDim.x) {
-    const int b = S.scope[i];
-    if (t == 0) {
-      int mode;
-      if (b < 0) mode = 0;
-      else if (F.scope_mode == 1) mode = 3;
-      else if (i < nc) mode = 1;
-      else { mode = 2; s_slab = S.slab_bits[b]; S.slab_bits[b] = 0; }
-      if (mode) {
-        s_coord = S.bcoord[b];
-        if (F.frustum_only && !block_in_frustum_dev(s_coord, F, S.extent)) mode = 0;
-      }
-      s_mode = mode;
-      s_nplace = 0;
-      if (mode) live++;
-    }
-    if (b >= 0) load_nbr_row(S, b, s_nbr);
+  int cur = 0;
+  if ((int)blockIdx.x < n) {
+    retype_resolve(S, F, blockIdx.x, nc, bufs[0]);
     __syncthreads();
-    const int mode = s_mode;
-    if (mode == 0) {
+    retype_issue(S, bufs[0]);
+    __pipeline_commit();
+  }
+  for (int i = blockIdx.x; i < n; i += gridDim.x, cur ^= 1) {
+    RetypeBuf &B = bufs[cur];
+    const int inext = i + gridDim.x;
+    if (inext < n) retype_resolve(S, F, inext, nc, bufs[cur ^ 1]);
+    if (t == 0) s_nplace = 0;
+    __syncthreads();
+    if (inext < n) {
+      retype_issue(S, bufs[cur ^ 1]);
+      __pipeline_commit();
+      __pipeline_wait_prior(1);
+    } else {
+      __pipeline_wait_prior(0);
+    }
+    __syncthreads();
+    const int mode = B.mode;
+    if (mode == 0) {   // uniform skip; the barrier orders reuse of this buffer
       __syncthreads();
       continue;
     }
-    load_ext_tile(S, b, s_nbr, tile, tw);
-    __syncthreads();
+    if (t == 0) live++;
+    const int b = B.b;
     bool sel;
     if (mode == 1) sel = true;
-    else if (mode == 2) sel = (s_slab & c_slab_sel[((x == 7) << 2) | ((y == 7) << 1) | (z == 7)]) != 0;
+    else if (mode == 2) sel = (B.slab & c_slab_sel[((x == 7) << 2) | ((y == 7) << 1) | (z == 7)]) != 0;
     else sel = (S.item_mask[(size_t)i * 16 + (t >> 5)] >> (t & 31)) & 1;
     unsigned bits = 0, small = 0;
+    const int base = (x * 9 + y) * 9 + z;
 #pragma unroll
     for (int k = 0; k < 8; k++) {
       const int o = c_corner[k];
-      const int e = ((x + (o & 1)) * 9 + (y + ((o >> 1) & 1))) * 9 + (z + ((o >> 2) & 1));
-      const double cv = tile[e];
-      sel = sel && tw[e];
+      const int e = base + (o & 1) * 81 + ((o >> 1) & 1) * 9 + ((o >> 2) & 1);
+      const double cv = B.tsdf[e];
+      sel = sel && (B.w[e] > 0);
       bits |= (cv < 0.0 ? 1u : 0u) << k;
       small |= (fabs(cv) < eps ? 1u : 0u) << k;
     }
     unsigned mask = 0;
     if (sel) {
-      const size_t q = (size_t)b * kNC + t;
-      const unsigned tp = S.tc[q];
+      const unsigned tp = B.tc[t];
       unsigned tc = bits;
       if (do_refine) {
         bool ch;
         tc = refine_type(bits, tp, small, &ch);
         refined += ch;
       }
+      const size_t q = (size_t)b * kNC + t;
       S.tp[q] = (uint8_t)tp;
       S.tc[q] = (uint8_t)tc;
       if (tc != tp) {
@@ -422,7 +494,6 @@ __global__ void __launch_bounds__(kThreadsCube, 2) k_retype_place(DevState S, co
         placements += __popc(mask);
       }
     }
-    // compact this block's placements into shared memory
     int pos = smem_append(__popc(mask), &s_nplace);
     while (mask) {
       const int e = __ffs(mask) - 1;
@@ -434,12 +505,13 @@ __global__ void __launch_bounds__(kThreadsCube, 2) k_retype_place(DevState S, co
     for (int p = t; p < np; p += kThreadsCube) {
       const int ent = s_place[p];
       const int ci = ent >> 4, e = ent & 15;
-      const int cx = ci >> 6, cy = (ci >> 3) & 7, cz = ci & 7;
       const int own = c_e_own[e], axis = c_e_axis[e];
-      const int ox = cx + (own & 1), oy = cy + ((own >> 1) & 1), oz = cz + ((own >> 2) & 1);
-      const int owner = s_nbr[nbr_dir(ox >> 3, oy >> 3, oz >> 3)];
+      const int ox = (ci >> 6) + (own & 1), oy = ((ci >> 3) & 7) + ((own >> 1) & 1),
+                oz = (ci & 7) + ((own >> 2) & 1);
+      const int owner = B.nbr[nbr_dir(ox >> 3, oy >> 3, oz >> 3)];
       if (owner < 0) {
-        set_error(S, ERR_CONSISTENCY, 10, s_coord.x * kB + cx, s_coord.y * kB + cy, s_coord.z * kB + cz);
+        set_error(S, ERR_CONSISTENCY, 10, B.coord.x * kB + (ci >> 6), B.coord.y * kB + ((ci >> 3) & 7),
+                  B.coord.z * kB + (ci & 7));
         continue;
       }
       const size_t slot = (size_t)owner * kEV + (((ox & 7) * 64 + (oy & 7) * 8 + (oz & 7)) * 3 + axis);
@@ -448,26 +520,24 @@ __global__ void __launch_bounds__(kThreadsCube, 2) k_retype_place(DevState S, co
         S.vnrm[3 * slot] = 0.0; S.vnrm[3 * slot + 1] = 0.0; S.vnrm[3 * slot + 2] = 0.0;
       }
       // start corner = owner cube origin; end corner one step along the axis
-      const double d0 = tile[(ox * 9 + oy) * 9 + oz];
-      const double d1 = tile[((ox + (axis == 0)) * 9 + (oy + (axis == 1))) * 9 + (oz + (axis == 2))];
+      const int p0 = (ox * 9 + oy) * 9 + oz;
+      const double d0 = B.tsdf[p0];
+      const double d1 = B.tsdf[p0 + (axis == 0 ? 81 : axis == 1 ? 9 : 1)];
       const double param = (d0 == d1) ? 0.5 : d0 / (d0 - d1);
-      const int ga = (axis == 0 ? s_coord.x : axis == 1 ? s_coord.y : s_coord.z) * kB +
-                     (axis == 0 ? ox : axis == 1 ? oy : oz);
+      const int ga = (axis == 0 ? B.coord.x * kB + ox : axis == 1 ? B.coord.y * kB + oy : B.coord.z * kB + oz);
       S.vparam[slot] = __dadd_rn(__dmul_rn((double)ga, l), __dmul_rn(param, l));
     }
-    __syncthreads();
+    __syncthreads();   // buffer `cur` is resolved into again two items later
   }
-  long long r;
-  r = block_sum(allocs, red);     if (t == 0) add64(&S.ctr->v_allocs, r);
-  r = block_sum(placements, red); if (t == 0) add64(&S.ctr->placements, r);
-  r = block_sum(active, red);     if (t == 0) add64(&S.ctr->active, r);
-  r = block_sum(changed, red);    if (t == 0) add64(&S.ctr->changed, r);
-  r = block_sum(t_rel, red);      if (t == 0) add64(&S.ctr->t_released, r);
-  r = block_sum(t_new, red);      if (t == 0) add64(&S.ctr->t_allocated, r);
-  r = block_sum(irr, red);        if (t == 0) add64(&S.ctr->irr_delta, r);
-  r = block_sum(refined, red);    if (t == 0) add64(&S.ctr->refined, r);
+  {
+    long long vals[8] = {allocs, placements, active, changed, t_rel, t_new, irr, refined};
+    int64_t *const dst[8] = {&S.ctr->v_allocs, &S.ctr->placements, &S.ctr->active, &S.ctr->changed,
+                             &S.ctr->t_released, &S.ctr->t_allocated, &S.ctr->irr_delta, &S.ctr->refined};
+    block_add_counters<8>(vals, red8, dst);
+  }
   if (t == 0 && live) atomicAdd(&S.ctr->nitems_live, (int)live);
 }
+constexpr size_t kRetypeSmem = 2 * sizeof(RetypeBuf) + kMaxPlace * sizeof(uint16_t);
 
 // ------------------------------------------------------------ GC + normals
 // edge index, in the neighbour cube owner - du*e_u - dw*e_w, of the edge slot
@@ -478,132 +548,218 @@ __device__ __forceinline__ int cube_edge_of_slot(int axis, int du, int dw) {
   return c_edge_of[axis][own];
 }
 
-// face normal accumulation for one vertex in the reference order
-// (mesher.py:459-486): vertex position k major, then halo blocks in sorted
-// order, then (cube, triangle slot) order; ttile = types over locals -1..7
-__device__ void fallback_normal(const DevState &S, const uint8_t *ttile, const int *s_nbr, int slot_ci,
-                                int axis, int epoch, double *dst) {
+// type of the cube at local (l0, l1, l2) in [-1, 7]^3 from the staged words
+// (each word is the aligned 4 bytes of tc holding the cube's type)
+__device__ __forceinline__ int staged_type(const uint32_t *ttw, int l0, int l1, int l2) {
+  return (ttw[((l0 + 1) * 9 + (l1 + 1)) * 9 + (l2 + 1)] >> (8 * (l2 & 3))) & 0xFF;
+}
+
+// Face-normal fallback for one vertex, computed by one warp (mesher.py:459-486).
+// Lane l handles candidate (incident cube j = l / 5, triangle slot s = l % 5);
+// the contributions are then summed by lane 0 in the reference's order:
+// vertex position k major, then halo blocks in sorted order, then cube, then
+// triangle slot -- so the result is bit-identical to np.add.at's.
+__device__ void fallback_normal_warp(const DevState &S, const uint32_t *ttw, const int *s_nbr, int4 bc,
+                                     int slot_ci, int axis, int epoch, double *dst) {
+  const int lane = threadIdx.x & 31;
   const int lx = slot_ci >> 6, ly = (slot_ci >> 3) & 7, lz = slot_ci & 7;
   const int u = axis == 0 ? 1 : 0, w = axis == 2 ? 1 : 2;
-  int cb[4], cc[4], ce[4], ctype[4], key[4];
-  int m = 0;
-  for (int du = 0; du < 2; du++)
-    for (int dw = 0; dw < 2; dw++) {
-      int l[3] = {lx, ly, lz};
-      l[u] -= du;
-      l[w] -= dw;
-      const int tt = ttile[((l[0] + 1) * 9 + (l[1] + 1)) * 9 + (l[2] + 1)];
-      const int e = cube_edge_of_slot(axis, du, dw);
-      if (!((c_edge_mask[tt] >> e) & 1)) continue;
-      const int dx = l[0] < 0 ? -1 : 0, dy = l[1] < 0 ? -1 : 0, dz = l[2] < 0 ? -1 : 0;
-      const int nb = s_nbr[nbr_dir(dx, dy, dz)];
-      if (nb < 0 || ld_vol(S.stamp_halo + nb) != epoch) continue;   // triangles of halo blocks only
-      const int cidx = (l[0] & 7) * 64 + (l[1] & 7) * 8 + (l[2] & 7);
-      const int k = (((dx + 1) * 4 + (dy + 1) * 2 + (dz + 1)) << 9) | cidx;
-      int j = m++;
-      while (j > 0 && key[j - 1] > k) {
-        key[j] = key[j - 1]; cb[j] = cb[j - 1]; cc[j] = cc[j - 1]; ce[j] = ce[j - 1]; ctype[j] = ctype[j - 1];
-        j--;
-      }
-      key[j] = k; cb[j] = nb; cc[j] = cidx; ce[j] = e; ctype[j] = tt;
+  // cube candidates j = 0..3: (du, dw) = (j >> 1, j & 1)
+  int cj = -1, ckey = 0x7fffffff, ctt = 0, ce = 0;
+  int cl[3] = {0, 0, 0};
+  if (lane < 4) {
+    const int du = lane >> 1, dw = lane & 1;
+    int l[3] = {lx, ly, lz};
+    l[u] -= du;
+    l[w] -= dw;
+    const int tt = staged_type(ttw, l[0], l[1], l[2]);
+    const int e = cube_edge_of_slot(axis, du, dw);
+    const int dx = l[0] < 0 ? -1 : 0, dy = l[1] < 0 ? -1 : 0, dz = l[2] < 0 ? -1 : 0;
+    const int nb = s_nbr[nbr_dir(dx, dy, dz)];
+    if (((c_edge_mask[tt] >> e) & 1) && nb >= 0 && ld_vol(S.stamp_halo + nb) == epoch) {
+      cj = lane;
+      ckey = (((dx + 1) * 4 + (dy + 1) * 2 + (dz + 1)) << 9) | ((l[0] & 7) * 64 + (l[1] & 7) * 8 + (l[2] & 7));
+      ctt = tt;
+      ce = e;
+      cl[0] = l[0]; cl[1] = l[1]; cl[2] = l[2];
     }
+  }
+  // rank of each cube candidate by (sorted block, cube) key
+  int rank = 0;
+#pragma unroll
+  for (int j = 0; j < 4; j++) {
+    const int kj = __shfl_sync(0xffffffffu, ckey, j);
+    rank += (kj < ckey);
+  }
+  // lane l: candidate cube j = l / 5, triangle slot s = l % 5
+  const int j = lane / 5, s = lane % 5;
+  const int jj = j < 4 ? j : 0;
+  const int my_valid = __shfl_sync(0xffffffffu, cj, jj) >= 0 && j < 4;
+  const int tt = __shfl_sync(0xffffffffu, ctt, jj);
+  const int e = __shfl_sync(0xffffffffu, ce, jj);
+  const int jrank = __shfl_sync(0xffffffffu, rank, jj);
+  const int c0 = __shfl_sync(0xffffffffu, cl[0], jj), c1 = __shfl_sync(0xffffffffu, cl[1], jj),
+            c2 = __shfl_sync(0xffffffffu, cl[2], jj);
+  int kpos = -1;
+  double fn[3] = {0.0, 0.0, 0.0};
+  if (my_valid && s < c_tri_count[tt]) {
+    const unsigned long long packed = c_tri_packed[tt];
+    for (int q = 0; q < 3; q++)
+      if ((int)((packed >> (4 * (3 * s + q))) & 0xF) == e) kpos = q;
+    if (kpos >= 0) {
+      double p[3][3];
+      for (int q = 0; q < 3; q++) {
+        const int eq = (int)((packed >> (4 * (3 * s + q))) & 0xF);
+        const int own = c_e_own[eq], ax = c_e_axis[eq];
+        const int ox = c0 + (own & 1), oy = c1 + ((own >> 1) & 1), oz = c2 + ((own >> 2) & 1);
+        const int ob = s_nbr[nbr_dir(ox < 0 ? -1 : ox >> 3, oy < 0 ? -1 : oy >> 3, oz < 0 ? -1 : oz >> 3)];
+        const int g[3] = {bc.x * kB + ox, bc.y * kB + oy, bc.z * kB + oz};
+        for (int d = 0; d < 3; d++) p[q][d] = __dmul_rn((double)g[d], S.cube_size);
+        p[q][ax] = S.vparam[(size_t)ob * kEV + ((ox & 7) * 64 + (oy & 7) * 8 + (oz & 7)) * 3 + ax];
+      }
+      const double a[3] = {p[1][0] - p[0][0], p[1][1] - p[0][1], p[1][2] - p[0][2]};
+      const double bb[3] = {p[2][0] - p[0][0], p[2][1] - p[0][1], p[2][2] - p[0][2]};
+      fn[0] = __dmul_rn(a[1], bb[2]) - __dmul_rn(a[2], bb[1]);
+      fn[1] = __dmul_rn(a[2], bb[0]) - __dmul_rn(a[0], bb[2]);
+      fn[2] = __dmul_rn(a[0], bb[1]) - __dmul_rn(a[1], bb[0]);
+    }
+  }
+  // ordered accumulation: k major, then cube rank, then triangle slot
+  int mykey = kpos >= 0 ? (kpos * 4 + jrank) * 5 + s : (1 << 20);
   double acc[3] = {0.0, 0.0, 0.0};
-  for (int k = 0; k < 3; k++)
-    for (int j = 0; j < m; j++) {
-      const unsigned long long packed = c_tri_packed[ctype[j]];
-      const int ntri = c_tri_count[ctype[j]];
-      for (int s = 0; s < ntri; s++) {
-        if ((int)((packed >> (4 * (3 * s + k))) & 0xF) != ce[j]) continue;
-        double p[3][3];
-        for (int q = 0; q < 3; q++) {
-          const int e = (int)((packed >> (4 * (3 * s + q))) & 0xF);
-          const int own = c_e_own[e];
-          const int cx = cc[j] >> 6, cy = (cc[j] >> 3) & 7, cz = cc[j] & 7;
-          const int ox = cx + (own & 1), oy = cy + ((own >> 1) & 1), oz = cz + ((own >> 2) & 1);
-          const int dir = nbr_dir(ox >> 3, oy >> 3, oz >> 3);
-          const int ob = (dir == 13) ? cb[j] : S.nbr[(size_t)cb[j] * 27 + dir];
-          slot_position(S, ob, ((ox & 7) * 64 + (oy & 7) * 8 + (oz & 7)) * 3 + c_e_axis[e], p[q]);
-        }
-        const double a[3] = {p[1][0] - p[0][0], p[1][1] - p[0][1], p[1][2] - p[0][2]};
-        const double bb[3] = {p[2][0] - p[0][0], p[2][1] - p[0][1], p[2][2] - p[0][2]};
-        acc[0] = __dadd_rn(acc[0], __dmul_rn(a[1], bb[2]) - __dmul_rn(a[2], bb[1]));
-        acc[1] = __dadd_rn(acc[1], __dmul_rn(a[2], bb[0]) - __dmul_rn(a[0], bb[2]));
-        acc[2] = __dadd_rn(acc[2], __dmul_rn(a[0], bb[1]) - __dmul_rn(a[1], bb[0]));
-      }
+  const int npend = __popc(__ballot_sync(0xffffffffu, kpos >= 0));
+  for (int it = 0; it < npend; it++) {
+    int best = mykey, bl = lane;   // pending lane with the smallest key
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const int ok = __shfl_xor_sync(0xffffffffu, best, o), ol = __shfl_xor_sync(0xffffffffu, bl, o);
+      if (ok < best || (ok == best && ol < bl)) { best = ok; bl = ol; }
     }
-  const double nrm = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(acc[0], acc[0]), __dmul_rn(acc[1], acc[1])),
-                                    __dmul_rn(acc[2], acc[2])));
-  if (nrm > 1e-20) {
-    dst[0] = (-1.0 * acc[0]) / nrm;
-    dst[1] = (-1.0 * acc[1]) / nrm;
-    dst[2] = (-1.0 * acc[2]) / nrm;
-  } else if (dst[0] == 0.0 && dst[1] == 0.0 && dst[2] == 0.0) {
-    dst[2] = 1.0;
+    acc[0] = __dadd_rn(acc[0], __shfl_sync(0xffffffffu, fn[0], bl));
+    acc[1] = __dadd_rn(acc[1], __shfl_sync(0xffffffffu, fn[1], bl));
+    acc[2] = __dadd_rn(acc[2], __shfl_sync(0xffffffffu, fn[2], bl));
+    if (lane == bl) mykey = 1 << 20;
+  }
+  if (lane == 0) {
+    const double nrm = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(acc[0], acc[0]), __dmul_rn(acc[1], acc[1])),
+                                      __dmul_rn(acc[2], acc[2])));
+    if (nrm > 1e-20) {
+      dst[0] = (-1.0 * acc[0]) / nrm;
+      dst[1] = (-1.0 * acc[1]) / nrm;
+      dst[2] = (-1.0 * acc[2]) / nrm;
+    } else if (dst[0] == 0.0 && dst[1] == 0.0 && dst[2] == 0.0) {
+      dst[2] = 1.0;
+    }
   }
 }
 
-// One CTA per listed (halo) block.  All tiles (neighbour row, slot births,
-// types over locals -1..7, the 11^3 tsdf stencil) are staged in shared memory;
-// G_GC clears every occupied slot no cube references any more (refcount ==
-// 0 recycling); the surviving vertices are compacted into a shared list and
-// G_NORMALS computes their normals with all threads (blended central-
-// difference gradient, face-normal fallback inline).  G_COMMIT: the last CTA
-// folds the per-call deltas into the persistent pool counters.
-__global__ void __launch_bounds__(kThreadsCube, 2) k_gc_normals(DevState S, const FrameDev *__restrict__ Fp,
+struct GcBuf {
+  double st[1331];       // tsdf over locals -1..9
+  int32_t sw[1331];      // weights over locals -1..9
+  alignas(16) int32_t birth[kEV];  // this block's slot birth words
+  uint32_t ttw[729];     // type words over cube locals -1..7
+  int4 coord;
+  int nbr[27];
+  int b;
+};
+
+__device__ __forceinline__ void gc_resolve(const DevState &S, const int32_t *list, int i, GcBuf &B) {
+  const int t = threadIdx.x;
+  if (t < 29) {
+    const int b = list[i];
+    if (t < 27) B.nbr[t] = (b < 0) ? -1 : (t == 13 ? b : S.nbr[(size_t)b * 27 + t]);
+    else if (t == 27) B.b = b;
+    else if (b >= 0) B.coord = S.bcoord[b];
+  }
+}
+
+__device__ __forceinline__ void gc_issue(const DevState &S, int mode, GcBuf &B) {
+  const int t = threadIdx.x;
+  const int b = B.b;
+  if (b < 0) return;
+  if (t < kEV / 4) __pipeline_memcpy_async(&B.birth[t * 4], S.vbirth + (size_t)b * kEV + t * 4, 16);
+  for (int q = t; q < 729; q += kThreadsCube) {
+    const int X = q / 81 - 1, Y = (q / 9) % 9 - 1, Z = q % 9 - 1;
+    const int nb = B.nbr[nbr_dir(X >> 3, Y >> 3, Z >> 3)];
+    if (nb >= 0) {
+      const size_t src = (size_t)nb * kNC + ((X & 7) * 64 + (Y & 7) * 8 + (Z & 7));
+      __pipeline_memcpy_async(&B.ttw[q], S.tc + (src & ~(size_t)3), 4);
+    } else {
+      B.ttw[q] = 0;
+    }
+  }
+  if (mode & G_NORMALS) {
+    for (int q = t; q < 1331; q += kThreadsCube) {
+      const int lx = q / 121 - 1, ly = (q / 11) % 11 - 1, lz = q % 11 - 1;
+      const int nb = B.nbr[nbr_dir(lx >> 3, ly >> 3, lz >> 3)];
+      if (nb >= 0) {
+        const size_t src = (size_t)nb * kNC + ((lx & 7) * 64 + (ly & 7) * 8 + (lz & 7));
+        __pipeline_memcpy_async(&B.st[q], S.tsdf + src, 8);
+        __pipeline_memcpy_async(&B.sw[q], S.weight + src, 4);
+      } else {
+        B.st[q] = 0.0;
+        B.sw[q] = 0;
+      }
+    }
+  }
+}
+
+// One CTA per listed (halo) block, persistent over the list and
+// software-pipelined like k_retype_place.  G_GC clears every occupied slot
+// that no cube references any more (the reference's refcount == 0 recycling);
+// the surviving vertices are compacted into a shared list and G_NORMALS gives
+// them the blended central-difference gradient normal (face-normal fallback
+// inline).  G_COMMIT: the last CTA folds the per-call deltas into the pool
+// counters.
+__global__ void __launch_bounds__(kThreadsCube, 2) k_gc_normals(DevState S, const FrameDev F,
                                                                 const int32_t *__restrict__ list,
                                                                 const int32_t *__restrict__ count_ptr,
                                                                 int count_const, int mode) {
   if (halted(S)) return;
   Counters *ctr = S.ctr;
   const bool run = !(mode & G_REQUIRE_ITEMS) || ld_vol(&ctr->nitems_live) > 0;
-  __shared__ double st[1331];
-  __shared__ uint8_t sw[1331];
-  __shared__ uint8_t ttile[729];
-  __shared__ uint16_t s_vlist[kEV];
-  __shared__ int s_nbr[27];
-  __shared__ int s_nv;
-  __shared__ long long red[32];
-  const int epoch = Fp->epoch;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  GcBuf *bufs = reinterpret_cast<GcBuf *>(smem_raw);
+  uint16_t *s_vlist = reinterpret_cast<uint16_t *>(smem_raw + 2 * sizeof(GcBuf));
+  uint16_t *s_fb = s_vlist + kEV;
+  __shared__ int s_nv, s_nfb;
+  __shared__ long long red[3 * 32];
+  const int epoch = F.epoch;
   const int n = run ? list_count(count_ptr, count_const) : 0;
   const int t = threadIdx.x;
   const int x = t >> 6, y = (t >> 3) & 7, z = t & 7;
   long long frees = 0, computed = 0, fallbacks = 0;
-  for (int i = blockIdx.x; i < n; i += gridDim.x) {
-    const int b = list[i];
-    if (b < 0) continue;
-    load_nbr_row(S, b, s_nbr);
-    if (t == 0) s_nv = 0;
+  int cur = 0;
+  if ((int)blockIdx.x < n) {
+    gc_resolve(S, list, blockIdx.x, bufs[0]);
     __syncthreads();
-    // issue every staging load of this block together
-    int birth[3];
-#pragma unroll
-    for (int a = 0; a < 3; a++) birth[a] = S.vbirth[(size_t)b * kEV + t * 3 + a];
-    for (int q = t; q < 729; q += kThreadsCube) {
-      const int X = q / 81 - 1, Y = (q / 9) % 9 - 1, Z = q % 9 - 1;
-      const int nb = s_nbr[nbr_dir(X >> 3, Y >> 3, Z >> 3)];
-      ttile[q] = nb >= 0 ? S.tc[(size_t)nb * kNC + ((X & 7) * 64 + (Y & 7) * 8 + (Z & 7))] : 0;
-    }
-    if (mode & G_NORMALS) {
-      for (int q = t; q < 1331; q += kThreadsCube) {
-        const int lx = q / 121 - 1, ly = (q / 11) % 11 - 1, lz = q % 11 - 1;
-        const int nb = s_nbr[nbr_dir(lx >> 3, ly >> 3, lz >> 3)];
-        double v = 0.0;
-        uint8_t w = 0;
-        if (nb >= 0) {
-          const size_t src = (size_t)nb * kNC + ((lx & 7) * 64 + (ly & 7) * 8 + (lz & 7));
-          v = S.tsdf[src];
-          w = S.weight[src] > 0;
-        }
-        st[q] = v;
-        sw[q] = w;
-      }
+    gc_issue(S, mode, bufs[0]);
+    __pipeline_commit();
+  }
+  for (int i = blockIdx.x; i < n; i += gridDim.x, cur ^= 1) {
+    GcBuf &B = bufs[cur];
+    const int inext = i + gridDim.x;
+    if (inext < n) gc_resolve(S, list, inext, bufs[cur ^ 1]);
+    if (t == 0) { s_nv = 0; s_nfb = 0; }
+    __syncthreads();
+    if (inext < n) {
+      gc_issue(S, mode, bufs[cur ^ 1]);
+      __pipeline_commit();
+      __pipeline_wait_prior(1);
+    } else {
+      __pipeline_wait_prior(0);
     }
     __syncthreads();
+    const int b = B.b;
+    if (b < 0) {
+      __syncthreads();
+      continue;
+    }
     int keep = 0;
     unsigned keep_axes = 0;
 #pragma unroll
     for (int axis = 0; axis < 3; axis++) {
-      if (birth[axis] < 0) continue;
+      if (B.birth[t * 3 + axis] < 0) continue;
       if (mode & G_GC) {
         const int u = axis == 0 ? 1 : 0, w = axis == 2 ? 1 : 2;
         bool ref = false;
@@ -612,8 +768,7 @@ __global__ void __launch_bounds__(kThreadsCube, 2) k_gc_normals(DevState S, cons
             int l[3] = {x, y, z};
             l[u] -= du;
             l[w] -= dw;
-            const int tt = ttile[((l[0] + 1) * 9 + (l[1] + 1)) * 9 + (l[2] + 1)];
-            ref = (c_edge_mask[tt] >> cube_edge_of_slot(axis, du, dw)) & 1;
+            ref = (c_edge_mask[staged_type(B.ttw, l[0], l[1], l[2])] >> cube_edge_of_slot(axis, du, dw)) & 1;
           }
         if (!ref) {
           S.vbirth[(size_t)b * kEV + t * 3 + axis] = -1;
@@ -635,11 +790,11 @@ __global__ void __launch_bounds__(kThreadsCube, 2) k_gc_normals(DevState S, cons
       const int sl = s_vlist[p];
       const int ci = sl / 3, axis = sl - 3 * (sl / 3);
       computed++;
-      int c0[3] = {(ci >> 6) + 1, ((ci >> 3) & 7) + 1, (ci & 7) + 1};
-      int c1[3] = {c0[0], c0[1], c0[2]};
-      c1[axis]++;
-      const double d0 = st[(c0[0] * 11 + c0[1]) * 11 + c0[2]];
-      const double d1 = st[(c1[0] * 11 + c1[1]) * 11 + c1[2]];
+      const int i0 = (((ci >> 6) + 1) * 11 + ((ci >> 3) & 7) + 1) * 11 + (ci & 7) + 1;
+      const int sa = axis == 0 ? 121 : axis == 1 ? 11 : 1;
+      const int i1 = i0 + sa;
+      const double d0 = B.st[i0];
+      const double d1 = B.st[i1];
       const double denom = d0 - d1;
       const double param = (denom != 0) ? d0 / denom : 0.5;
       double g0[3], g1[3];
@@ -647,10 +802,9 @@ __global__ void __launch_bounds__(kThreadsCube, 2) k_gc_normals(DevState S, cons
 #pragma unroll
       for (int d = 0; d < 3; d++) {
         const int sd = d == 0 ? 121 : d == 1 ? 11 : 1;
-        const int i0 = (c0[0] * 11 + c0[1]) * 11 + c0[2], i1 = (c1[0] * 11 + c1[1]) * 11 + c1[2];
-        g0[d] = st[i0 + sd] - st[i0 - sd];
-        g1[d] = st[i1 + sd] - st[i1 - sd];
-        valid = valid && sw[i0 + sd] && sw[i0 - sd] && sw[i1 + sd] && sw[i1 - sd];
+        g0[d] = B.st[i0 + sd] - B.st[i0 - sd];
+        g1[d] = B.st[i1 + sd] - B.st[i1 - sd];
+        valid = valid && B.sw[i0 + sd] > 0 && B.sw[i0 - sd] > 0 && B.sw[i1 + sd] > 0 && B.sw[i1 - sd] > 0;
       }
       double g[3];
       const double wa = 1.0 - param;
@@ -658,20 +812,28 @@ __global__ void __launch_bounds__(kThreadsCube, 2) k_gc_normals(DevState S, cons
       for (int d = 0; d < 3; d++) g[d] = __dadd_rn(__dmul_rn(wa, g0[d]), __dmul_rn(param, g1[d]));
       const double nrm = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(g[0], g[0]), __dmul_rn(g[1], g[1])),
                                         __dmul_rn(g[2], g[2])));
-      double *dst = S.vnrm + 3 * ((size_t)b * kEV + sl);
       if (valid && nrm > 1e-12) {
+        double *dst = S.vnrm + 3 * ((size_t)b * kEV + sl);
         dst[0] = g[0] / nrm; dst[1] = g[1] / nrm; dst[2] = g[2] / nrm;
       } else {
         fallbacks++;
-        fallback_normal(S, ttile, s_nbr, ci, axis, epoch, dst);
+        s_fb[atomicAdd(&s_nfb, 1)] = (uint16_t)sl;
       }
     }
     __syncthreads();
+    // face-normal fallback: one warp per vertex
+    const int nfb = s_nfb;
+    for (int f = t >> 5; f < nfb; f += kThreadsCube / 32) {
+      const int sl = s_fb[f];
+      fallback_normal_warp(S, B.ttw, B.nbr, B.coord, sl / 3, sl % 3, epoch, S.vnrm + 3 * ((size_t)b * kEV + sl));
+    }
+    __syncthreads();   // buffer `cur` is resolved into again two items later
   }
-  long long r;
-  r = block_sum(frees, red);     if (t == 0) add64(&ctr->v_frees, r);
-  r = block_sum(computed, red);  if (t == 0) add64(&ctr->normals, r);
-  r = block_sum(fallbacks, red); if (t == 0) add64(&ctr->fallbacks, r);
+  {
+    long long vals[3] = {frees, computed, fallbacks};
+    int64_t *const dst[3] = {&ctr->v_frees, &ctr->normals, &ctr->fallbacks};
+    block_add_counters<3>(vals, red, dst);
+  }
   if (t == 0 && (mode & G_COMMIT)) {
     __threadfence();
     if (atomicAdd(&ctr->done_gc, 1) == (int)gridDim.x - 1) {
@@ -693,6 +855,7 @@ __global__ void __launch_bounds__(kThreadsCube, 2) k_gc_normals(DevState S, cons
     }
   }
 }
+constexpr size_t kGcSmem = 2 * sizeof(GcBuf) + 2 * kEV * sizeof(uint16_t);
 
 // ------------------------------------------------------------ full scans
 __global__ void k_irregular_full(DevState S, int nblocks, unsigned long long *out) {
@@ -771,11 +934,11 @@ __global__ void k_refine_eval(const uint8_t *tc, const uint8_t *tp, const double
   }
 }
 
-__global__ void k_frustum_eval(DevState S, const FrameDev *__restrict__ Fp, const int3 *coords, int n,
+__global__ void k_frustum_eval(DevState S, const FrameDev F, const int3 *coords, int n,
                                uint8_t *out) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int3 c = coords[i];
-    out[i] = block_in_frustum_dev(make_int4(c.x, c.y, c.z, 0), *Fp, S.extent);
+    out[i] = block_in_frustum_dev(make_int4(c.x, c.y, c.z, 0), F, S.extent);
   }
 }
 
