@@ -59,8 +59,9 @@ def phase_bytes(ds: dict, h: int, w: int) -> dict:
         + min(coll * 512, h * w) * 8 + coll * 27 * 16,
         "retype_place": scope * (729 * SAMPLE + 512 + 1024) + ds["edge_placements"] * (4 + 8)
         + ds["new_vertices"] * 24,
-        "gc_normals": halo * (1536 * SLOT_SCAN + 729 + 1331 * SAMPLE) + ds["normals_computed"] * 24
+        "gc_normals": halo * (1536 * SLOT_SCAN + 729) + ds["normals_computed"] * (12 * SAMPLE + 24)
         + ds["vertices_freed"] * 4,
+        "fallback": ds["fallback_normals"] * (27 * 4 + 4 + 20 * 3 * 8 + 24),
     }
 
 
@@ -276,7 +277,7 @@ def run_gpu(args, spec, cfg, rank, world, local_rank):
         cpu = {"value": n / t, "unit": "frames/s", "cores": 1, "kind": "port",
                "sample": f"{args.config} frames 0..{n - 1} through the CPU oracle (serial C "
                          f"restatement of the reference, oracle/), {t:.1f} s"}
-    launches_per_frame = 5
+    launches_per_frame = 6
     clk = clocks.summary()
     line = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,

@@ -61,7 +61,7 @@ struct Counters {
   int32_t nexplicit;
   int32_t nitems_live;
   int32_t done_gc;
-  int32_t pad0;
+  int32_t nfallback;
   int64_t v_allocs;
   int64_t v_frees;
   int64_t placements;
@@ -134,7 +134,7 @@ struct DevState {
   double *vparam;       // [cap*1536] vertex coordinate along the edge axis
   double *vnrm;         // [cap*1536*3]
   uint32_t *item_mask;  // [cap*16] explicit scope cube masks
-  uint32_t *item_sel;   // [cap*16] unused by the fused kernels (kept for debugging)
+  int2 *fallback;       // [cap*1536] face-normal fallback worklist (block, slot)
   long long max_vertices;
   Counters *ctr;
 };

@@ -49,7 +49,7 @@ static int set_err(int code, const char *fmt, ...) {
     if (_r != VM_OK) return _r; \
   } while (0)
 
-enum Phase { PH_DEPTH = 0, PH_COLLECT, PH_FUSE, PH_RETYPE, PH_GC, PH_END, PH_COUNT };
+enum Phase { PH_DEPTH = 0, PH_COLLECT, PH_FUSE, PH_RETYPE, PH_GC, PH_FALLBACK, PH_END, PH_COUNT };
 
 struct Compacted {
   double *pos = nullptr, *nrm = nullptr;
@@ -70,6 +70,7 @@ struct vm_engine {
   bool own_stream = false;
   int32_t epoch = 0;
   int sm_count = 148;
+  int grid_retype = 296, grid_gc = 296, grid_fuse = 296;
   void *d_scratch = nullptr;
   size_t scratch_cap = 0;
   Compacted comp;
@@ -152,6 +153,7 @@ static int grow_blocks(vm_engine *e, int64_t need) {
   TRY(dev_grow(&S.vparam, o * kEV, n * kEV, st));
   TRY(dev_grow(&S.vnrm, o * kEV * 3, n * kEV * 3, st));
   TRY(dev_grow(&S.item_mask, 0, n * 16, st));
+  TRY(dev_grow(&S.fallback, 0, n * kEV, st));
   S.block_cap = (int32_t)cap;
   return VM_OK;
 }
@@ -200,13 +202,15 @@ static int enqueue_after_collect(vm_engine *e) {
   cudaStream_t st = e->stream;
   const int gb = grid_blocks(e);
   rec(e, PH_FUSE);
-  k_fuse_blocks<<<gb, kThreadsCube, 0, st>>>(S, *e->h_frame, S.scope, &S.ctr->ncollected, 0,
+  k_fuse_blocks<<<e->grid_fuse, kThreadsCube, 0, st>>>(S, *e->h_frame, S.scope, &S.ctr->ncollected, 0,
                                             F_INIT | F_INTEGRATE | F_SCOPE);
   rec(e, PH_RETYPE);
-  k_retype_place<<<gb, kThreadsCube, kRetypeSmem, st>>>(S, *e->h_frame);
+  k_retype_place<<<e->grid_retype, kNT, kRetypeSmem, st>>>(S, *e->h_frame);
   rec(e, PH_GC);
-  k_gc_normals<<<gb, kThreadsCube, kGcSmem, st>>>(S, *e->h_frame, S.halo, &S.ctr->nhalo, 0,
+  k_gc_normals<<<e->grid_gc, kGT, kGcSmem, st>>>(S, *e->h_frame, S.halo, &S.ctr->nhalo, 0,
                                            G_GC | G_NORMALS | G_COMMIT | G_REQUIRE_ITEMS);
+  rec(e, PH_FALLBACK);
+  k_fallback<<<e->sm_count * 4, kFT, 0, st>>>(S, *e->h_frame);
   rec(e, PH_END);
   return check_launch();
 }
@@ -368,6 +372,41 @@ static int run_compaction(vm_engine *e, int64_t frame, bool with_handles) {
   return error_from_counters(e);
 }
 
+// tile-source tables of the staged loaders (vm_kernels.cuh g_*_tab)
+static int upload_tile_tables() {
+  uint32_t ext[217];
+  for (int t = 0; t < 217; t++) {
+    int x, y, z;
+    if (t < 64) { x = 8; y = t >> 3; z = t & 7; }
+    else if (t < 128) { x = (t - 64) >> 3; y = 8; z = t & 7; }
+    else if (t < 192) { x = (t - 128) >> 3; y = t & 7; z = 8; }
+    else if (t < 200) { x = 8; y = 8; z = t - 192; }
+    else if (t < 208) { x = 8; y = t - 200; z = 8; }
+    else if (t < 216) { x = t - 208; y = 8; z = 8; }
+    else { x = 8; y = 8; z = 8; }
+    const uint32_t p = (x * 9 + y) * 9 + z;
+    const uint32_t dir = ((x >> 3) + 1) * 9 + ((y >> 3) + 1) * 3 + ((z >> 3) + 1);
+    const uint32_t src = (x & 7) * 64 + (y & 7) * 8 + (z & 7);
+    ext[t] = p | dir << 10 | src << 15;
+  }
+  auto dir_of = [](int l) { return l < 0 ? -1 : (l >> 3); };
+  uint16_t sten[1331], typ[729];
+  for (int q = 0; q < 1331; q++) {
+    const int lx = q / 121 - 1, ly = (q / 11) % 11 - 1, lz = q % 11 - 1;
+    const int dir = (dir_of(lx) + 1) * 9 + (dir_of(ly) + 1) * 3 + (dir_of(lz) + 1);
+    sten[q] = (uint16_t)(dir << 9 | ((lx & 7) * 64 + (ly & 7) * 8 + (lz & 7)));
+  }
+  for (int q = 0; q < 729; q++) {
+    const int X = q / 81 - 1, Y = (q / 9) % 9 - 1, Z = q % 9 - 1;
+    const int dir = (dir_of(X) + 1) * 9 + (dir_of(Y) + 1) * 3 + (dir_of(Z) + 1);
+    typ[q] = (uint16_t)(dir << 9 | ((X & 7) * 64 + (Y & 7) * 8 + (Z & 7)));
+  }
+  CK(cudaMemcpyToSymbol(g_ext_tab, ext, sizeof ext));
+  CK(cudaMemcpyToSymbol(g_sten_tab, sten, sizeof sten));
+  CK(cudaMemcpyToSymbol(g_type_tab, typ, sizeof typ));
+  return VM_OK;
+}
+
 // ------------------------------------------------------------ C ABI
 extern "C" {
 
@@ -426,8 +465,17 @@ int vm_create(const vm_store_config *cfg, vm_engine **out) {
     slab_sel[m] = bits;
   }
   CK(cudaMemcpyToSymbol(c_slab_sel, slab_sel, sizeof slab_sel));
-  CK(cudaFuncSetAttribute(k_retype_place, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRetypeSmem));
-  CK(cudaFuncSetAttribute(k_gc_normals, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGcSmem));
+  TRY(upload_tile_tables());
+  {
+    // persistent grids: exactly the number of co-resident CTAs
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_retype_place, kNT, kRetypeSmem));
+    e->grid_retype = std::max(1, occ) * e->sm_count;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gc_normals, kGT, kGcSmem));
+    e->grid_gc = std::max(1, occ) * e->sm_count;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fuse_blocks, kThreadsCube, 0));
+    e->grid_fuse = std::max(1, occ) * e->sm_count;
+  }
   S.block_cap = 0;
   const int64_t ib = cfg->initial_blocks > 0 ? cfg->initial_blocks : 1024;
   TRY(grow_blocks(e, std::min<int64_t>(ib, S.max_blocks)));
@@ -442,7 +490,7 @@ int vm_destroy(vm_engine *e) {
   DevState &S = e->S;
   void *ptrs[] = {S.slots, S.ovf_head, S.ovf_lock, S.ovf_key, S.ovf_val, S.ovf_next, S.ovf_stamp, S.bcoord,
                   S.nbr, S.stamp_collect, S.stamp_halo, S.stamp_new, S.slab_bits, S.scope, S.newlist,
-                  S.halo, S.tsdf, S.weight, S.tp, S.tc, S.vbirth, S.vparam, S.vnrm, S.item_mask,
+                  S.halo, S.tsdf, S.weight, S.tp, S.tc, S.vbirth, S.vparam, S.vnrm, S.item_mask, S.fallback,
                   S.ctr, e->d_depth, e->d_scratch};
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -762,9 +810,10 @@ int vm_extract(vm_engine *e, const int32_t *scope_coords, const uint8_t *scope_m
     TRY(check_launch());
   }
   const int gb = grid_blocks(e);
-  k_retype_place<<<gb, kThreadsCube, kRetypeSmem, e->stream>>>(e->S, *e->h_frame);
-  k_gc_normals<<<gb, kThreadsCube, kGcSmem, e->stream>>>(e->S, *e->h_frame, e->S.halo, &e->S.ctr->nhalo, 0,
+  k_retype_place<<<e->grid_retype, kNT, kRetypeSmem, e->stream>>>(e->S, *e->h_frame);
+  k_gc_normals<<<e->grid_gc, kGT, kGcSmem, e->stream>>>(e->S, *e->h_frame, e->S.halo, &e->S.ctr->nhalo, 0,
                                                   G_GC | G_NORMALS | G_COMMIT | G_REQUIRE_ITEMS);
+  k_fallback<<<e->sm_count * 4, kFT, 0, e->stream>>>(e->S, *e->h_frame);
   TRY(check_launch());
   TRY(read_counters(e));
   TRY(error_from_counters(e));
@@ -780,7 +829,7 @@ int vm_garbage_collect(vm_engine *e, const int32_t *coords, int64_t n, int64_t *
   TRY(reset_call_counters(e));
   int32_t *di = nullptr;
   if (n > 0) TRY(map_coords(e, coords, n, &di, nullptr, 0, false));
-  k_gc_normals<<<grid_blocks(e), kThreadsCube, kGcSmem, e->stream>>>(e->S, *e->h_frame, di, nullptr,
+  k_gc_normals<<<e->grid_gc, kGT, kGcSmem, e->stream>>>(e->S, *e->h_frame, di, nullptr,
                                                                 (int)std::max<int64_t>(n, 0), G_GC | G_COMMIT);
   TRY(check_launch());
   TRY(read_counters(e));
@@ -796,7 +845,8 @@ int vm_compute_normals(vm_engine *e, const int32_t *coords, int64_t n) {
   e->h_frame->epoch = ++e->epoch;
   int32_t *di;
   TRY(map_coords(e, coords, n, &di, e->S.stamp_halo, e->epoch, false));
-  k_gc_normals<<<grid_blocks(e), kThreadsCube, kGcSmem, e->stream>>>(e->S, *e->h_frame, di, nullptr, (int)n, G_NORMALS);
+  k_gc_normals<<<e->grid_gc, kGT, kGcSmem, e->stream>>>(e->S, *e->h_frame, di, nullptr, (int)n, G_NORMALS);
+  k_fallback<<<e->sm_count * 4, kFT, 0, e->stream>>>(e->S, *e->h_frame);
   TRY(check_launch());
   TRY(read_counters(e));
   return error_from_counters(e);

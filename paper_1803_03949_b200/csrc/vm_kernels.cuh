@@ -343,191 +343,234 @@ __device__ __forceinline__ int smem_append(int cnt, int *s_count) {
 // produce identical bits (mesher.py:216-235).
 constexpr int kMaxPlace = kNC * 12;
 
-struct RetypeBuf {
-  double tsdf[729];
-  int32_t w[729];
-  alignas(16) uint8_t tc[kNC];
+// Tile-source tables (filled by vm_create): for every staged tile position,
+// the neighbour direction (0..26) and the source cube index in that block,
+// so the loaders do no div/mod index arithmetic.
+__device__ uint32_t g_ext_tab[217];   // 9^3 tile position | dir << 10 | src << 15 (positions with a coord == 8)
+__device__ uint16_t g_sten_tab[1331]; // dir << 9 | src, 11^3 stencil over locals -1..9
+__device__ uint16_t g_type_tab[729];  // dir << 9 | src, 9^3 type tile over locals -1..7
+
+// Per-item "resolved" record (three in flight: computing, staged, resolving)
+struct Resolved {
   int4 coord;
   int nbr[27];
-  int b, mode, slab;
+  int b, mode, slab, item;   // mode: -1 past the end, 0 skip, 1 full, 2 slab bits, 3 explicit mask
 };
 
-// stage A: resolve item i (scope index -> block, mode, coords, neighbour row)
-__device__ __forceinline__ void retype_resolve(const DevState &S, const FrameDev &F, int i, int nc,
-                                               RetypeBuf &B) {
-  const int t = threadIdx.x;
-  if (t < 32) {
-    const int b = S.scope[i];
-    if (t < 27) B.nbr[t] = (b < 0) ? -1 : (t == 13 ? b : S.nbr[(size_t)b * 27 + t]);
-    if (t == 27) {
-      int mode;
-      if (b < 0) mode = 0;
-      else if (F.scope_mode == 1) mode = 3;
-      else if (i < nc) mode = 1;
-      else { mode = 2; B.slab = S.slab_bits[b]; S.slab_bits[b] = 0; }
-      if (mode) {
-        B.coord = S.bcoord[b];
-        if (F.frustum_only && !block_in_frustum_dev(B.coord, F, S.extent)) mode = 0;
-      }
-      B.mode = mode;
-      B.b = b;
-    }
+// registers warp 0 carries while the loads of a future item are in flight
+struct ResolveRegs {
+  int v;       // lanes 0..26: neighbour row entry; lane 27: slab bits
+  int4 coord;  // lane 28
+};
+
+__device__ __forceinline__ ResolveRegs resolve_load(const DevState &S, const FrameDev &F, int b, int item,
+                                                    int nc) {
+  const int lane = threadIdx.x;
+  ResolveRegs r;
+  r.v = -1;
+  r.coord = make_int4(0, 0, 0, 0);
+  if (b >= 0) {
+    if (lane < 27) r.v = lane == 13 ? b : __ldcg(S.nbr + (size_t)b * 27 + lane);
+    else if (lane == 27) r.v = (F.scope_mode == 0 && item >= nc) ? __ldcg(S.slab_bits + b) : 0;
+    else if (lane == 28) r.coord = __ldcg(S.bcoord + b);
+  }
+  return r;
+}
+
+__device__ __forceinline__ void resolve_store(const DevState &S, const FrameDev &F, const ResolveRegs &r,
+                                              int b, int item, int n, int nc, Resolved &R) {
+  const int lane = threadIdx.x;
+  if (lane < 27) R.nbr[lane] = r.v;
+  const int slab = __shfl_sync(0xffffffffu, r.v, 27);
+  int4 c;
+  c.x = __shfl_sync(0xffffffffu, r.coord.x, 28);
+  c.y = __shfl_sync(0xffffffffu, r.coord.y, 28);
+  c.z = __shfl_sync(0xffffffffu, r.coord.z, 28);
+  c.w = 0;
+  if (lane == 27) {
+    int mode;
+    if (item >= n) mode = -1;
+    else if (b < 0) mode = 0;
+    else if (F.scope_mode == 1) mode = 3;
+    else if (item < nc) mode = 1;
+    else { mode = 2; S.slab_bits[b] = 0; }   // slab consumed: clear for the next frame
+    if (mode > 0 && F.frustum_only && !block_in_frustum_dev(c, F, S.extent)) mode = 0;
+    R.mode = mode;
+    R.b = b;
+    R.slab = slab;
+    R.item = item;
+    R.coord = c;
   }
 }
 
-// stage B: issue the asynchronous copies of the item's tiles (needs B.nbr)
-__device__ __forceinline__ void retype_issue(const DevState &S, RetypeBuf &B) {
-  const int t = threadIdx.x;
-  if (B.mode == 0) return;
-  const int b = B.b;
-  {
-    const int x = t >> 6, y = (t >> 3) & 7, z = t & 7;
-    const int p = (x * 9 + y) * 9 + z;
-    __pipeline_memcpy_async(&B.tsdf[p], S.tsdf + (size_t)b * kNC + t, 8);
-    __pipeline_memcpy_async(&B.w[p], S.weight + (size_t)b * kNC + t, 4);
-  }
-  if (t < 32) __pipeline_memcpy_async(&B.tc[t * 16], S.tc + (size_t)b * kNC + t * 16, 16);
-  if (t < 217) {
-    int x, y, z;   // the 217 tile positions with max(x, y, z) == 8
-    if (t < 64) { x = 8; y = t >> 3; z = t & 7; }
-    else if (t < 128) { x = (t - 64) >> 3; y = 8; z = t & 7; }
-    else if (t < 192) { x = (t - 128) >> 3; y = t & 7; z = 8; }
-    else if (t < 200) { x = 8; y = 8; z = t - 192; }
-    else if (t < 208) { x = 8; y = t - 200; z = 8; }
-    else if (t < 216) { x = t - 208; y = 8; z = 8; }
-    else { x = 8; y = 8; z = 8; }
-    const int p = (x * 9 + y) * 9 + z;
-    const int nb = B.nbr[nbr_dir(x >> 3, y >> 3, z >> 3)];
-    if (nb >= 0) {
-      const size_t q = (size_t)nb * kNC + ((x & 7) * 64 + (y & 7) * 8 + (z & 7));
-      __pipeline_memcpy_async(&B.tsdf[p], S.tsdf + q, 8);
-      __pipeline_memcpy_async(&B.w[p], S.weight + q, 4);
-    } else {
-      B.tsdf[p] = 0.0;
-      B.w[p] = 0;
-    }
-  }
-}
+constexpr int kNT = 128;   // threads per CTA of the per-block meshing kernels (4 cubes each)
 
-__global__ void __launch_bounds__(kThreadsCube, 2) k_retype_place(DevState S, const FrameDev F) {
+// One CTA of 128 threads per scope item (persistent over the item list).
+// Small CTAs keep ~8 blocks in flight per SM so their serial phases (resolve,
+// staging, typing, placement) overlap across blocks.  Typing and refinement
+// as the reference; a cube whose type changed is retriangulated implicitly
+// (its triangles become TRI_TABLE[type_curr]) and contributes the triangle /
+// irregular-count deltas.  The (active cube, mask edge) placements are
+// compacted in shared memory and spread over the CTA: each claims its edge
+// slot (atomicCAS on the slot's birth word -- exactly one allocation per
+// edge) and writes the interpolated coordinate; all requesters produce
+// identical bits (mesher.py:216-235).
+__global__ void __launch_bounds__(kNT, 8) k_retype_place(DevState S, const FrameDev F) {
   if (halted(S)) return;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  RetypeBuf *bufs = reinterpret_cast<RetypeBuf *>(smem_raw);
-  uint16_t *s_place = reinterpret_cast<uint16_t *>(smem_raw + 2 * sizeof(RetypeBuf));
+  __shared__ double tile[729];
+  __shared__ uint8_t tw[729];
+  __shared__ __align__(16) uint8_t s_tc[kNC];
+  __shared__ uint16_t s_place[kMaxPlace];
+  __shared__ Resolved R;
   __shared__ long long red8[8 * 32];
   __shared__ int s_nplace;
   const int n = item_count(S, F);
-  const int nc = ld_vol(&S.ctr->ncollected);
+  const int nc = __ldcg(&S.ctr->ncollected);
   const int t = threadIdx.x;
-  const int x = t >> 6, y = (t >> 3) & 7, z = t & 7;
   const double l = S.cube_size;
   const int frame = F.frame;
   const int do_refine = F.refine;
   const double eps = F.epsilon;
   long long allocs = 0, placements = 0, active = 0, changed = 0, t_rel = 0, t_new = 0, irr = 0,
             refined = 0, live = 0;
-  int cur = 0;
-  if ((int)blockIdx.x < n) {
-    retype_resolve(S, F, blockIdx.x, nc, bufs[0]);
-    __syncthreads();
-    retype_issue(S, bufs[0]);
-    __pipeline_commit();
-  }
-  for (int i = blockIdx.x; i < n; i += gridDim.x, cur ^= 1) {
-    RetypeBuf &B = bufs[cur];
-    const int inext = i + gridDim.x;
-    if (inext < n) retype_resolve(S, F, inext, nc, bufs[cur ^ 1]);
+  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+    if (t < 32) {
+      const int b = __ldcg(S.scope + i);
+      const ResolveRegs rr = resolve_load(S, F, b, i, nc);
+      resolve_store(S, F, rr, b, i, n, nc, R);
+    }
     if (t == 0) s_nplace = 0;
     __syncthreads();
-    if (inext < n) {
-      retype_issue(S, bufs[cur ^ 1]);
-      __pipeline_commit();
-      __pipeline_wait_prior(1);
-    } else {
-      __pipeline_wait_prior(0);
-    }
-    __syncthreads();
-    const int mode = B.mode;
-    if (mode == 0) {   // uniform skip; the barrier orders reuse of this buffer
+    const int mode = R.mode;
+    if (mode <= 0) {
       __syncthreads();
       continue;
     }
+    const int b = R.b;
     if (t == 0) live++;
-    const int b = B.b;
-    bool sel;
-    if (mode == 1) sel = true;
-    else if (mode == 2) sel = (B.slab & c_slab_sel[((x == 7) << 2) | ((y == 7) << 1) | (z == 7)]) != 0;
-    else sel = (S.item_mask[(size_t)i * 16 + (t >> 5)] >> (t & 31)) & 1;
-    unsigned bits = 0, small = 0;
-    const int base = (x * 9 + y) * 9 + z;
+    // stage the (B+1)^3 tile (mesher.py:75-96) and the current types
+    {
+      // batched gathers: all loads in flight before any shared-memory store
+      double ov[kNC / kNT], xv[2];
+      int ow[kNC / kNT], xw[2], xp[2];
+      uint4 tcv = make_uint4(0, 0, 0, 0);
 #pragma unroll
-    for (int k = 0; k < 8; k++) {
-      const int o = c_corner[k];
-      const int e = base + (o & 1) * 81 + ((o >> 1) & 1) * 9 + ((o >> 2) & 1);
-      const double cv = B.tsdf[e];
-      sel = sel && (B.w[e] > 0);
-      bits |= (cv < 0.0 ? 1u : 0u) << k;
-      small |= (fabs(cv) < eps ? 1u : 0u) << k;
+      for (int j = 0; j < kNC / kNT; j++) {
+        ov[j] = S.tsdf[(size_t)b * kNC + t + j * kNT];
+        ow[j] = S.weight[(size_t)b * kNC + t + j * kNT];
+      }
+      if (t < 32) tcv = reinterpret_cast<const uint4 *>(S.tc + (size_t)b * kNC)[t];
+#pragma unroll
+      for (int j = 0; j < 2; j++) {
+        const int q = t + j * kNT;
+        xv[j] = 0.0;
+        xw[j] = 0;
+        xp[j] = -1;
+        if (q < 217) {
+          const uint32_t e = __ldg(&g_ext_tab[q]);
+          const int nb = R.nbr[(e >> 10) & 31];
+          xp[j] = e & 1023;
+          if (nb >= 0) {
+            const size_t src = (size_t)nb * kNC + (e >> 15);
+            xv[j] = S.tsdf[src];
+            xw[j] = S.weight[src];
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kNC / kNT; j++) {
+        const int c = t + j * kNT;
+        const int p = ((c >> 6) * 9 + ((c >> 3) & 7)) * 9 + (c & 7);
+        tile[p] = ov[j];
+        tw[p] = ow[j] > 0;
+      }
+      if (t < 32) reinterpret_cast<uint4 *>(s_tc)[t] = tcv;
+#pragma unroll
+      for (int j = 0; j < 2; j++)
+        if (xp[j] >= 0) {
+          tile[xp[j]] = xv[j];
+          tw[xp[j]] = xw[j] > 0;
+        }
     }
-    unsigned mask = 0;
-    if (sel) {
-      const unsigned tp = B.tc[t];
-      unsigned tc = bits;
-      if (do_refine) {
-        bool ch;
-        tc = refine_type(bits, tp, small, &ch);
-        refined += ch;
+    __syncthreads();
+#pragma unroll 1
+    for (int j = 0; j < kNC / kNT; j++) {
+      const int c = t + j * kNT;
+      const int x = c >> 6, y = (c >> 3) & 7, z = c & 7;
+      bool sel;
+      if (mode == 1) sel = true;
+      else if (mode == 2) sel = (R.slab & c_slab_sel[((x == 7) << 2) | ((y == 7) << 1) | (z == 7)]) != 0;
+      else sel = (S.item_mask[(size_t)R.item * 16 + (c >> 5)] >> (c & 31)) & 1;
+      unsigned bits = 0, small = 0;
+      const int base = (x * 9 + y) * 9 + z;
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        const int o = c_corner[k];
+        const int e = base + (o & 1) * 81 + ((o >> 1) & 1) * 9 + ((o >> 2) & 1);
+        const double cv = tile[e];
+        sel = sel && tw[e];
+        bits |= (cv < 0.0 ? 1u : 0u) << k;
+        small |= (fabs(cv) < eps ? 1u : 0u) << k;
       }
-      const size_t q = (size_t)b * kNC + t;
-      S.tp[q] = (uint8_t)tp;
-      S.tc[q] = (uint8_t)tc;
-      if (tc != tp) {
-        changed++;
-        const int nold = c_tri_count[tp], nnew = c_tri_count[tc];
-        t_rel += nold;
-        t_new += nnew;
-        irr += (nnew > 0 && !is_regular_type(tc)) - (nold > 0 && !is_regular_type(tp));
+      unsigned mask = 0;
+      if (sel) {
+        const unsigned tp = s_tc[c];
+        unsigned tc = bits;
+        if (do_refine) {
+          bool ch;
+          tc = refine_type(bits, tp, small, &ch);
+          refined += ch;
+        }
+        const size_t q = (size_t)b * kNC + c;
+        S.tp[q] = (uint8_t)tp;
+        S.tc[q] = (uint8_t)tc;
+        if (tc != tp) {
+          changed++;
+          const int nold = c_tri_count[tp], nnew = c_tri_count[tc];
+          t_rel += nold;
+          t_new += nnew;
+          irr += (nnew > 0 && !is_regular_type(tc)) - (nold > 0 && !is_regular_type(tp));
+        }
+        mask = c_edge_mask[tc];
+        if (mask) {
+          active++;
+          placements += __popc(mask);
+        }
       }
-      mask = c_edge_mask[tc];
-      if (mask) {
-        active++;
-        placements += __popc(mask);
+      int pos = smem_append(__popc(mask), &s_nplace);
+      while (mask) {
+        const int e = __ffs(mask) - 1;
+        mask &= mask - 1;
+        s_place[pos++] = (uint16_t)((c << 4) | e);
       }
-    }
-    int pos = smem_append(__popc(mask), &s_nplace);
-    while (mask) {
-      const int e = __ffs(mask) - 1;
-      mask &= mask - 1;
-      s_place[pos++] = (uint16_t)((t << 4) | e);
     }
     __syncthreads();
     const int np = s_nplace;
-    for (int p = t; p < np; p += kThreadsCube) {
+    for (int p = t; p < np; p += kNT) {
       const int ent = s_place[p];
       const int ci = ent >> 4, e = ent & 15;
       const int own = c_e_own[e], axis = c_e_axis[e];
-      const int ox = (ci >> 6) + (own & 1), oy = ((ci >> 3) & 7) + ((own >> 1) & 1),
-                oz = (ci & 7) + ((own >> 2) & 1);
-      const int owner = B.nbr[nbr_dir(ox >> 3, oy >> 3, oz >> 3)];
+      const int ox = (ci >> 6) + (own & 1), oy = ((ci >> 3) & 7) + ((own >> 1) & 1), oz = (ci & 7) + ((own >> 2) & 1);
+      const int owner = R.nbr[nbr_dir(ox >> 3, oy >> 3, oz >> 3)];
       if (owner < 0) {
-        set_error(S, ERR_CONSISTENCY, 10, B.coord.x * kB + (ci >> 6), B.coord.y * kB + ((ci >> 3) & 7),
-                  B.coord.z * kB + (ci & 7));
+        set_error(S, ERR_CONSISTENCY, 10, R.coord.x * kB + (ci >> 6), R.coord.y * kB + ((ci >> 3) & 7),
+                  R.coord.z * kB + (ci & 7));
         continue;
       }
       const size_t slot = (size_t)owner * kEV + (((ox & 7) * 64 + (oy & 7) * 8 + (oz & 7)) * 3 + axis);
-      if (ld_vol(S.vbirth + slot) == -1 && atomicCAS(S.vbirth + slot, -1, frame) == -1) {
+      // start corner = owner cube origin; end corner one step along the axis
+      const int p0 = (ox * 9 + oy) * 9 + oz;
+      const double d0 = tile[p0];
+      const double d1 = tile[p0 + (axis == 0 ? 81 : axis == 1 ? 9 : 1)];
+      const double param = (d0 == d1) ? 0.5 : d0 / (d0 - d1);
+      const int ga = (axis == 0 ? R.coord.x * kB + ox : axis == 1 ? R.coord.y * kB + oy : R.coord.z * kB + oz);
+      S.vparam[slot] = __dadd_rn(__dmul_rn((double)ga, l), __dmul_rn(param, l));
+      if (atomicCAS(S.vbirth + slot, -1, frame) == -1) {
         allocs++;
         S.vnrm[3 * slot] = 0.0; S.vnrm[3 * slot + 1] = 0.0; S.vnrm[3 * slot + 2] = 0.0;
       }
-      // start corner = owner cube origin; end corner one step along the axis
-      const int p0 = (ox * 9 + oy) * 9 + oz;
-      const double d0 = B.tsdf[p0];
-      const double d1 = B.tsdf[p0 + (axis == 0 ? 81 : axis == 1 ? 9 : 1)];
-      const double param = (d0 == d1) ? 0.5 : d0 / (d0 - d1);
-      const int ga = (axis == 0 ? B.coord.x * kB + ox : axis == 1 ? B.coord.y * kB + oy : B.coord.z * kB + oz);
-      S.vparam[slot] = __dadd_rn(__dmul_rn((double)ga, l), __dmul_rn(param, l));
     }
-    __syncthreads();   // buffer `cur` is resolved into again two items later
+    __syncthreads();   // R, tile and the placement list are rewritten by the next item
   }
   {
     long long vals[8] = {allocs, placements, active, changed, t_rel, t_new, irr, refined};
@@ -537,7 +580,9 @@ __global__ void __launch_bounds__(kThreadsCube, 2) k_retype_place(DevState S, co
   }
   if (t == 0 && live) atomicAdd(&S.ctr->nitems_live, (int)live);
 }
-constexpr size_t kRetypeSmem = 2 * sizeof(RetypeBuf) + kMaxPlace * sizeof(uint16_t);
+constexpr size_t kRetypeSmem = 0;
+
+
 
 // ------------------------------------------------------------ GC + normals
 // edge index, in the neighbour cube owner - du*e_u - dw*e_w, of the edge slot
@@ -559,7 +604,7 @@ __device__ __forceinline__ int staged_type(const uint32_t *ttw, int l0, int l1, 
 // the contributions are then summed by lane 0 in the reference's order:
 // vertex position k major, then halo blocks in sorted order, then cube, then
 // triangle slot -- so the result is bit-identical to np.add.at's.
-__device__ void fallback_normal_warp(const DevState &S, const uint32_t *ttw, const int *s_nbr, int4 bc,
+__device__ void fallback_normal_warp(const DevState &S, const uint8_t *ttile, const int *s_nbr, int4 bc,
                                      int slot_ci, int axis, int epoch, double *dst) {
   const int lane = threadIdx.x & 31;
   const int lx = slot_ci >> 6, ly = (slot_ci >> 3) & 7, lz = slot_ci & 7;
@@ -572,7 +617,7 @@ __device__ void fallback_normal_warp(const DevState &S, const uint32_t *ttw, con
     int l[3] = {lx, ly, lz};
     l[u] -= du;
     l[w] -= dw;
-    const int tt = staged_type(ttw, l[0], l[1], l[2]);
+    const int tt = ttile[((l[0] + 1) * 9 + (l[1] + 1)) * 9 + (l[2] + 1)];
     const int e = cube_edge_of_slot(axis, du, dw);
     const int dx = l[0] < 0 ? -1 : 0, dy = l[1] < 0 ? -1 : 0, dz = l[2] < 0 ? -1 : 0;
     const int nb = s_nbr[nbr_dir(dx, dy, dz)];
@@ -653,181 +698,201 @@ __device__ void fallback_normal_warp(const DevState &S, const uint32_t *ttw, con
   }
 }
 
-struct GcBuf {
-  double st[1331];       // tsdf over locals -1..9
-  int32_t sw[1331];      // weights over locals -1..9
-  alignas(16) int32_t birth[kEV];  // this block's slot birth words
-  uint32_t ttw[729];     // type words over cube locals -1..7
-  int4 coord;
-  int nbr[27];
-  int b;
-};
-
-__device__ __forceinline__ void gc_resolve(const DevState &S, const int32_t *list, int i, GcBuf &B) {
-  const int t = threadIdx.x;
-  if (t < 29) {
-    const int b = list[i];
-    if (t < 27) B.nbr[t] = (b < 0) ? -1 : (t == 13 ? b : S.nbr[(size_t)b * 27 + t]);
-    else if (t == 27) B.b = b;
-    else if (b >= 0) B.coord = S.bcoord[b];
+// Face-normal fallback worklist consumer: one warp per vertex; stages the
+// vertex's block neighbour row and the 9^3 type tile entries it needs through
+// shared memory, then runs the ordered warp accumulation.
+constexpr int kFT = 128;
+__global__ void __launch_bounds__(kFT) k_fallback(DevState S, const FrameDev F) {
+  if (halted(S)) return;
+  __shared__ int s_nbr[kFT / 32][27];
+  __shared__ uint8_t s_tt[kFT / 32][729];
+  __shared__ int4 s_coord[kFT / 32];
+  const int n = __ldcg(&S.ctr->nfallback);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int f = blockIdx.x * (kFT / 32) + w; f < n; f += gridDim.x * (kFT / 32)) {
+    const int2 rec = S.fallback[f];
+    const int b = rec.x, sl = rec.y;
+    if (lane < 27) s_nbr[w][lane] = lane == 13 ? b : __ldcg(S.nbr + (size_t)b * 27 + lane);
+    if (lane == 27) s_coord[w] = __ldcg(S.bcoord + b);
+    __syncwarp();
+    // only the types of the <= 4 cubes around the slot are read: stage those
+    const int ci = sl / 3, axis = sl % 3;
+    const int u = axis == 0 ? 1 : 0, ww = axis == 2 ? 1 : 2;
+    if (lane < 4) {
+      int l[3] = {ci >> 6, (ci >> 3) & 7, ci & 7};
+      l[u] -= lane >> 1;
+      l[ww] -= lane & 1;
+      const int nb = s_nbr[w][nbr_dir(l[0] >> 3, l[1] >> 3, l[2] >> 3)];
+      s_tt[w][((l[0] + 1) * 9 + (l[1] + 1)) * 9 + (l[2] + 1)] =
+          nb >= 0 ? S.tc[(size_t)nb * kNC + ((l[0] & 7) * 64 + (l[1] & 7) * 8 + (l[2] & 7))] : 0;
+    }
+    __syncwarp();
+    fallback_normal_warp(S, s_tt[w], s_nbr[w], s_coord[w], ci, axis, F.epoch, S.vnrm + 3 * ((size_t)b * kEV + sl));
+    __syncwarp();
   }
 }
 
-__device__ __forceinline__ void gc_issue(const DevState &S, int mode, GcBuf &B) {
-  const int t = threadIdx.x;
-  const int b = B.b;
-  if (b < 0) return;
-  if (t < kEV / 4) __pipeline_memcpy_async(&B.birth[t * 4], S.vbirth + (size_t)b * kEV + t * 4, 16);
-  for (int q = t; q < 729; q += kThreadsCube) {
-    const int X = q / 81 - 1, Y = (q / 9) % 9 - 1, Z = q % 9 - 1;
-    const int nb = B.nbr[nbr_dir(X >> 3, Y >> 3, Z >> 3)];
-    if (nb >= 0) {
-      const size_t src = (size_t)nb * kNC + ((X & 7) * 64 + (Y & 7) * 8 + (Z & 7));
-      __pipeline_memcpy_async(&B.ttw[q], S.tc + (src & ~(size_t)3), 4);
-    } else {
-      B.ttw[q] = 0;
-    }
-  }
-  if (mode & G_NORMALS) {
-    for (int q = t; q < 1331; q += kThreadsCube) {
-      const int lx = q / 121 - 1, ly = (q / 11) % 11 - 1, lz = q % 11 - 1;
-      const int nb = B.nbr[nbr_dir(lx >> 3, ly >> 3, lz >> 3)];
-      if (nb >= 0) {
-        const size_t src = (size_t)nb * kNC + ((lx & 7) * 64 + (ly & 7) * 8 + (lz & 7));
-        __pipeline_memcpy_async(&B.st[q], S.tsdf + src, 8);
-        __pipeline_memcpy_async(&B.sw[q], S.weight + src, 4);
-      } else {
-        B.st[q] = 0.0;
-        B.sw[q] = 0;
-      }
-    }
-  }
+constexpr int kGT = 64;   // threads per CTA of k_gc_normals
+
+// tsdf / weight sample at block-local corner (lx, ly, lz) in [-1, 9]^3
+__device__ __forceinline__ size_t sample_index(const int *s_nbr, int lx, int ly, int lz) {
+  const int nb = s_nbr[nbr_dir(lx >> 3, ly >> 3, lz >> 3)];
+  return nb < 0 ? ~(size_t)0 : (size_t)nb * kNC + ((lx & 7) * 64 + (ly & 7) * 8 + (lz & 7));
 }
 
-// One CTA per listed (halo) block, persistent over the list and
-// software-pipelined like k_retype_place.  G_GC clears every occupied slot
-// that no cube references any more (the reference's refcount == 0 recycling);
-// the surviving vertices are compacted into a shared list and G_NORMALS gives
-// them the blended central-difference gradient normal (face-normal fallback
-// inline).  G_COMMIT: the last CTA folds the per-call deltas into the pool
-// counters.
-__global__ void __launch_bounds__(kThreadsCube, 2) k_gc_normals(DevState S, const FrameDev F,
-                                                                const int32_t *__restrict__ list,
-                                                                const int32_t *__restrict__ count_ptr,
-                                                                int count_const, int mode) {
+// One CTA of 64 threads per listed (halo) block; small shared footprint so
+// every halo block of a frame is resident at once.  G_GC clears every
+// occupied slot that no cube references any more (the reference's refcount ==
+// 0 recycling: the 4 cubes around the edge are read from a staged 9^3 type
+// tile); the surviving vertices are compacted and G_NORMALS gathers each
+// vertex's 12-point stencil directly (mesher.py:400-439), the face-normal
+// fallback one warp per vertex.  G_COMMIT: the last CTA folds the per-call
+// deltas into the pool counters.
+__global__ void __launch_bounds__(kGT, 16) k_gc_normals(DevState S, const FrameDev F,
+                                                    const int32_t *__restrict__ list,
+                                                    const int32_t *__restrict__ count_ptr,
+                                                    int count_const, int mode) {
   if (halted(S)) return;
   Counters *ctr = S.ctr;
-  const bool run = !(mode & G_REQUIRE_ITEMS) || ld_vol(&ctr->nitems_live) > 0;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  GcBuf *bufs = reinterpret_cast<GcBuf *>(smem_raw);
-  uint16_t *s_vlist = reinterpret_cast<uint16_t *>(smem_raw + 2 * sizeof(GcBuf));
-  uint16_t *s_fb = s_vlist + kEV;
-  __shared__ int s_nv, s_nfb;
+  const bool run = !(mode & G_REQUIRE_ITEMS) || __ldcg(&ctr->nitems_live) > 0;
+  __shared__ uint8_t tt[729];        // type_curr over cube locals -1..7
+  __shared__ uint32_t occ[kEV / 32]; // slot occupancy bits
+  __shared__ uint16_t s_vlist[kEV];
+  __shared__ Resolved R;
+  __shared__ int s_nv;
   __shared__ long long red[3 * 32];
-  const int epoch = F.epoch;
-  const int n = run ? list_count(count_ptr, count_const) : 0;
-  const int t = threadIdx.x;
-  const int x = t >> 6, y = (t >> 3) & 7, z = t & 7;
+  const int n = run ? (count_ptr ? __ldcg(count_ptr) : count_const) : 0;
+  const int t = threadIdx.x, lane = t & 31;
+  FrameDev Fr = F;
+  Fr.scope_mode = 1;   // resolve as explicit items: no slab bits
+  Fr.frustum_only = 0;
   long long frees = 0, computed = 0, fallbacks = 0;
-  int cur = 0;
-  if ((int)blockIdx.x < n) {
-    gc_resolve(S, list, blockIdx.x, bufs[0]);
-    __syncthreads();
-    gc_issue(S, mode, bufs[0]);
-    __pipeline_commit();
-  }
-  for (int i = blockIdx.x; i < n; i += gridDim.x, cur ^= 1) {
-    GcBuf &B = bufs[cur];
-    const int inext = i + gridDim.x;
-    if (inext < n) gc_resolve(S, list, inext, bufs[cur ^ 1]);
-    if (t == 0) { s_nv = 0; s_nfb = 0; }
-    __syncthreads();
-    if (inext < n) {
-      gc_issue(S, mode, bufs[cur ^ 1]);
-      __pipeline_commit();
-      __pipeline_wait_prior(1);
-    } else {
-      __pipeline_wait_prior(0);
+  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+    if (t < 32) {
+      const int b = __ldcg(list + i);
+      const ResolveRegs rr = resolve_load(S, Fr, b, i, 0);
+      resolve_store(S, Fr, rr, b, i, n, 0, R);
     }
+    if (t == 0) s_nv = 0;
     __syncthreads();
-    const int b = B.b;
-    if (b < 0) {
+    if (R.mode <= 0) {
       __syncthreads();
       continue;
     }
-    int keep = 0;
-    unsigned keep_axes = 0;
+    const int b = R.b;
+    // stage slot occupancy and the type tile (batched: all loads in flight)
 #pragma unroll
-    for (int axis = 0; axis < 3; axis++) {
-      if (B.birth[t * 3 + axis] < 0) continue;
-      if (mode & G_GC) {
-        const int u = axis == 0 ? 1 : 0, w = axis == 2 ? 1 : 2;
-        bool ref = false;
-        for (int du = 0; du < 2 && !ref; du++)
-          for (int dw = 0; dw < 2 && !ref; dw++) {
-            int l[3] = {x, y, z};
-            l[u] -= du;
-            l[w] -= dw;
-            ref = (c_edge_mask[staged_type(B.ttw, l[0], l[1], l[2])] >> cube_edge_of_slot(axis, du, dw)) & 1;
-          }
-        if (!ref) {
-          S.vbirth[(size_t)b * kEV + t * 3 + axis] = -1;
-          frees++;
-          continue;
+    for (int j0 = 0; j0 < kEV / kGT; j0 += 8) {
+      int bv[8];
+#pragma unroll
+      for (int j = 0; j < 8; j++) bv[j] = S.vbirth[(size_t)b * kEV + (j0 + j) * kGT + t];
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        const unsigned ball = __ballot_sync(0xffffffffu, bv[j] >= 0);
+        if (lane == 0) occ[((j0 + j) * kGT + t) >> 5] = ball;
+      }
+    }
+    {
+      constexpr int kT = (729 + kGT - 1) / kGT;   // 12
+      uint8_t tv[kT];
+#pragma unroll
+      for (int j = 0; j < kT; j++) {
+        const int q = t + j * kGT;
+        tv[j] = 0;
+        if (q < 729) {
+          const int e = __ldg(&g_type_tab[q]);
+          const int nb = R.nbr[e >> 9];
+          if (nb >= 0) tv[j] = S.tc[(size_t)nb * kNC + (e & 511)];
         }
       }
-      keep++;
-      keep_axes |= 1u << axis;
+#pragma unroll
+      for (int j = 0; j < kT; j++)
+        if (t + j * kGT < 729) tt[t + j * kGT] = tv[j];
+    }
+    __syncthreads();
+    // GC: a slot survives iff a cube around its edge still has the edge in its mask
+#pragma unroll 1
+    for (int j = 0; j < kNC / kGT; j++) {
+      const int c = t + j * kGT;
+      const int x = c >> 6, y = (c >> 3) & 7, z = c & 7;
+      int keep = 0;
+      unsigned keep_axes = 0;
+      for (int axis = 0; axis < 3; axis++) {
+        const int sl = c * 3 + axis;
+        if (!((occ[sl >> 5] >> (sl & 31)) & 1)) continue;
+        if (mode & G_GC) {
+          const int u = axis == 0 ? 1 : 0, w = axis == 2 ? 1 : 2;
+          bool ref = false;
+          for (int du = 0; du < 2 && !ref; du++)
+            for (int dw = 0; dw < 2 && !ref; dw++) {
+              int l[3] = {x, y, z};
+              l[u] -= du;
+              l[w] -= dw;
+              ref = (c_edge_mask[tt[((l[0] + 1) * 9 + (l[1] + 1)) * 9 + (l[2] + 1)]] >>
+                     cube_edge_of_slot(axis, du, dw)) & 1;
+            }
+          if (!ref) {
+            S.vbirth[(size_t)b * kEV + sl] = -1;
+            frees++;
+            continue;
+          }
+        }
+        keep++;
+        keep_axes |= 1u << axis;
+      }
+      if (mode & G_NORMALS) {
+        int pos = smem_append(keep, &s_nv);
+        for (int axis = 0; axis < 3; axis++)
+          if ((keep_axes >> axis) & 1) s_vlist[pos++] = (uint16_t)(c * 3 + axis);
+      }
     }
     if (mode & G_NORMALS) {
-      int pos = smem_append(keep, &s_nv);
-      for (int axis = 0; axis < 3; axis++)
-        if ((keep_axes >> axis) & 1) s_vlist[pos++] = (uint16_t)(t * 3 + axis);
-    }
-    __syncthreads();
-    const int nv = (mode & G_NORMALS) ? s_nv : 0;
-    for (int p = t; p < nv; p += kThreadsCube) {
-      const int sl = s_vlist[p];
-      const int ci = sl / 3, axis = sl - 3 * (sl / 3);
-      computed++;
-      const int i0 = (((ci >> 6) + 1) * 11 + ((ci >> 3) & 7) + 1) * 11 + (ci & 7) + 1;
-      const int sa = axis == 0 ? 121 : axis == 1 ? 11 : 1;
-      const int i1 = i0 + sa;
-      const double d0 = B.st[i0];
-      const double d1 = B.st[i1];
-      const double denom = d0 - d1;
-      const double param = (denom != 0) ? d0 / denom : 0.5;
-      double g0[3], g1[3];
-      bool valid = true;
+      __syncthreads();
+      const int nv = s_nv;
+      for (int p = t; p < nv; p += kGT) {
+        const int sl = s_vlist[p];
+        const int ci = sl / 3, axis = sl - 3 * (sl / 3);
+        computed++;
+        const int c0[3] = {ci >> 6, (ci >> 3) & 7, ci & 7};
+        int c1[3] = {c0[0], c0[1], c0[2]};
+        c1[axis]++;
+        // the 12 stencil points: c0 +- e_d, c1 +- e_d (c0 + e_axis = c1, c1 - e_axis = c0)
+        double v0p[3], v0m[3], v1p[3], v1m[3];
+        bool valid = true;
 #pragma unroll
-      for (int d = 0; d < 3; d++) {
-        const int sd = d == 0 ? 121 : d == 1 ? 11 : 1;
-        g0[d] = B.st[i0 + sd] - B.st[i0 - sd];
-        g1[d] = B.st[i1 + sd] - B.st[i1 - sd];
-        valid = valid && B.sw[i0 + sd] > 0 && B.sw[i0 - sd] > 0 && B.sw[i1 + sd] > 0 && B.sw[i1 - sd] > 0;
-      }
-      double g[3];
-      const double wa = 1.0 - param;
+        for (int d = 0; d < 3; d++) {
+          const int dx = d == 0, dy = d == 1, dz = d == 2;
+          const size_t a = sample_index(R.nbr, c0[0] + dx, c0[1] + dy, c0[2] + dz);
+          const size_t bq = sample_index(R.nbr, c0[0] - dx, c0[1] - dy, c0[2] - dz);
+          const size_t cq = sample_index(R.nbr, c1[0] + dx, c1[1] + dy, c1[2] + dz);
+          const size_t dq = sample_index(R.nbr, c1[0] - dx, c1[1] - dy, c1[2] - dz);
+          v0p[d] = a != ~(size_t)0 ? S.tsdf[a] : 0.0;
+          v0m[d] = bq != ~(size_t)0 ? S.tsdf[bq] : 0.0;
+          v1p[d] = cq != ~(size_t)0 ? S.tsdf[cq] : 0.0;
+          v1m[d] = dq != ~(size_t)0 ? S.tsdf[dq] : 0.0;
+          valid = valid && a != ~(size_t)0 && S.weight[a] > 0 && bq != ~(size_t)0 && S.weight[bq] > 0 &&
+                  cq != ~(size_t)0 && S.weight[cq] > 0 && dq != ~(size_t)0 && S.weight[dq] > 0;
+        }
+        const double d0 = v1m[axis], d1 = v0p[axis];   // samples at c0 and c1
+        const double denom = d0 - d1;
+        const double param = (denom != 0) ? d0 / denom : 0.5;
+        double g[3];
+        const double wa = 1.0 - param;
 #pragma unroll
-      for (int d = 0; d < 3; d++) g[d] = __dadd_rn(__dmul_rn(wa, g0[d]), __dmul_rn(param, g1[d]));
-      const double nrm = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(g[0], g[0]), __dmul_rn(g[1], g[1])),
-                                        __dmul_rn(g[2], g[2])));
-      if (valid && nrm > 1e-12) {
-        double *dst = S.vnrm + 3 * ((size_t)b * kEV + sl);
-        dst[0] = g[0] / nrm; dst[1] = g[1] / nrm; dst[2] = g[2] / nrm;
-      } else {
-        fallbacks++;
-        s_fb[atomicAdd(&s_nfb, 1)] = (uint16_t)sl;
+        for (int d = 0; d < 3; d++)
+          g[d] = __dadd_rn(__dmul_rn(wa, v0p[d] - v0m[d]), __dmul_rn(param, v1p[d] - v1m[d]));
+        const double nrm = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(g[0], g[0]), __dmul_rn(g[1], g[1])),
+                                          __dmul_rn(g[2], g[2])));
+        if (valid && nrm > 1e-12) {
+          double *dst = S.vnrm + 3 * ((size_t)b * kEV + sl);
+          dst[0] = g[0] / nrm; dst[1] = g[1] / nrm; dst[2] = g[2] / nrm;
+        } else {
+          fallbacks++;   // face-normal fallback: deferred to k_fallback (global worklist)
+          S.fallback[atomicAdd(&ctr->nfallback, 1)] = make_int2(b, sl);
+        }
       }
     }
-    __syncthreads();
-    // face-normal fallback: one warp per vertex
-    const int nfb = s_nfb;
-    for (int f = t >> 5; f < nfb; f += kThreadsCube / 32) {
-      const int sl = s_fb[f];
-      fallback_normal_warp(S, B.ttw, B.nbr, B.coord, sl / 3, sl % 3, epoch, S.vnrm + 3 * ((size_t)b * kEV + sl));
-    }
-    __syncthreads();   // buffer `cur` is resolved into again two items later
+    __syncthreads();   // R and the tiles are rewritten by the next item
   }
   {
     long long vals[3] = {frees, computed, fallbacks};
@@ -855,7 +920,10 @@ __global__ void __launch_bounds__(kThreadsCube, 2) k_gc_normals(DevState S, cons
     }
   }
 }
-constexpr size_t kGcSmem = 2 * sizeof(GcBuf) + 2 * kEV * sizeof(uint16_t);
+constexpr size_t kGcSmem = 0;
+
+
+
 
 // ------------------------------------------------------------ full scans
 __global__ void k_irregular_full(DevState S, int nblocks, unsigned long long *out) {

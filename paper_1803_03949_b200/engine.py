@@ -225,4 +225,4 @@ class Engine:
         _lib.check(_lib.load().vm_set_stream(self.store._h, C.c_void_p(stream_handle or None)))
 
 
-PHASES = ("depth_stats", "collect", "fuse_blocks", "retype_place", "gc_normals")
+PHASES = ("depth_stats", "collect", "fuse_blocks", "retype_place", "gc_normals", "fallback")
