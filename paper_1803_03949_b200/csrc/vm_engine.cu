@@ -131,6 +131,23 @@ static int copy_sync(vm_engine *e, void *dst, const void *src, size_t bytes, cud
   return VM_OK;
 }
 
+// Programmatic Dependent Launch: the kernel's CTAs are scheduled while the
+// previous kernel of the frame drains; they wait in cudaGridDependencySynchronize()
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*kern)(KArgs...), int grid, int block, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 static int check_launch() {
   const cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return set_err(VM_ERR_CUDA, "kernel launch failed: %s", cudaGetErrorString(err));
@@ -193,7 +210,7 @@ static int reset_call_counters(vm_engine *e) {
 }
 
 static inline void rec(vm_engine *e, int ph) {
-  if (e->profiling || ph == PH_DEPTH || ph == PH_RETYPE || ph == PH_END) cudaEventRecord(e->ev[ph], e->stream);
+  if (e->profiling || ph == PH_DEPTH || ph == PH_END) cudaEventRecord(e->ev[ph], e->stream);
 }
 
 // frame segment after collect: fuse (init/integrate/scope), retype+place, gc+normals
@@ -201,16 +218,17 @@ static int enqueue_after_collect(vm_engine *e) {
   DevState &S = e->S;
   cudaStream_t st = e->stream;
   const int gb = grid_blocks(e);
+  const FrameDev F = *e->h_frame;
   rec(e, PH_FUSE);
-  k_fuse_blocks<<<e->grid_fuse, kThreadsCube, 0, st>>>(S, *e->h_frame, S.scope, &S.ctr->ncollected, 0,
-                                            F_INIT | F_INTEGRATE | F_SCOPE);
+  launch_pdl(k_fuse_blocks, e->grid_fuse, kFB, st, S, F, (const int32_t *)S.scope,
+             (const int32_t *)&S.ctr->ncollected, 0, (int)(F_INIT | F_INTEGRATE | F_SCOPE));
   rec(e, PH_RETYPE);
-  k_retype_place<<<e->grid_retype, kNT, kRetypeSmem, st>>>(S, *e->h_frame);
+  launch_pdl(k_retype_place, e->grid_retype, kNT, st, S, F);
   rec(e, PH_GC);
-  k_gc_normals<<<e->grid_gc, kGT, kGcSmem, st>>>(S, *e->h_frame, S.halo, &S.ctr->nhalo, 0,
-                                           G_GC | G_NORMALS | G_COMMIT | G_REQUIRE_ITEMS);
+  launch_pdl(k_gc_normals, e->grid_gc, kGT, st, S, F, (const int32_t *)S.halo, (const int32_t *)&S.ctr->nhalo,
+             0, (int)(G_GC | G_NORMALS | G_COMMIT | G_REQUIRE_ITEMS));
   rec(e, PH_FALLBACK);
-  k_fallback<<<e->sm_count * 4, kFT, 0, st>>>(S, *e->h_frame);
+  launch_pdl(k_fallback, e->sm_count * 4, kFT, st, S, F);
   rec(e, PH_END);
   return check_launch();
 }
@@ -473,7 +491,7 @@ int vm_create(const vm_store_config *cfg, vm_engine **out) {
     e->grid_retype = std::max(1, occ) * e->sm_count;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gc_normals, kGT, kGcSmem));
     e->grid_gc = std::max(1, occ) * e->sm_count;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fuse_blocks, kThreadsCube, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fuse_blocks, kFB, 0));
     e->grid_fuse = std::max(1, occ) * e->sm_count;
   }
   S.block_cap = 0;
@@ -575,8 +593,13 @@ static void fill_stats(vm_engine *e, int64_t frame, vm_stats *out) {
   out->resumes = e->last_resumes;
   float ms = 0.f;
   if (cudaEventElapsedTime(&ms, e->ev[PH_DEPTH], e->ev[PH_END]) == cudaSuccess) out->device_ms = ms;
-  if (cudaEventElapsedTime(&ms, e->ev[PH_DEPTH], e->ev[PH_RETYPE]) == cudaSuccess) out->fusion_ms = ms;
-  if (cudaEventElapsedTime(&ms, e->ev[PH_RETYPE], e->ev[PH_END]) == cudaSuccess) out->meshing_ms = ms;
+  if (e->profiling) {   // segment split needs the per-kernel events
+    if (cudaEventElapsedTime(&ms, e->ev[PH_DEPTH], e->ev[PH_RETYPE]) == cudaSuccess) out->fusion_ms = ms;
+    if (cudaEventElapsedTime(&ms, e->ev[PH_RETYPE], e->ev[PH_END]) == cudaSuccess) out->meshing_ms = ms;
+  } else {
+    out->fusion_ms = out->device_ms;   // whole frame; per-segment split with vm_set_profiling
+    out->meshing_ms = 0.0;
+  }
   cudaGetLastError();
 }
 
@@ -605,7 +628,7 @@ int vm_fuse_frame_enqueue(vm_engine *e, const double *depth, int32_t h, int32_t 
   rec(e, PH_DEPTH);
   k_depth_stats<<<grid_blocks(e), 256, 0, st>>>(e->S, *e->h_frame);
   rec(e, PH_COLLECT);
-  k_collect<<<grid_threads(e, (long long)h * w, 256), 256, 0, st>>>(e->S, *e->h_frame);
+  launch_pdl(k_collect, grid_threads(e, (long long)h * w, 256), 256, st, e->S, *e->h_frame);
   TRY(enqueue_after_collect(e));
   CK(cudaMemcpyAsync(e->h_ctr, e->S.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
   e->pending = 1;
@@ -695,14 +718,14 @@ int vm_integrate(vm_engine *e, const int32_t *coords, int64_t n, const double *d
       }
       int32_t *di;
       TRY(map_coords(e, coords + 3 * start, end - start, &di, nullptr, 0, false));
-      k_fuse_blocks<<<grid_blocks(e), kThreadsCube, 0, e->stream>>>(e->S, *e->h_frame, di, nullptr,
+      k_fuse_blocks<<<grid_blocks(e), kFB, 0, e->stream>>>(e->S, *e->h_frame, di, nullptr,
                                                                     (int)(end - start), F_INTEGRATE);
       TRY(check_launch());
       CK(cudaStreamSynchronize(e->stream));
       start = end;
     }
   } else {
-    k_fuse_blocks<<<grid_blocks(e), kThreadsCube, 0, e->stream>>>(e->S, *e->h_frame, e->S.scope,
+    k_fuse_blocks<<<grid_blocks(e), kFB, 0, e->stream>>>(e->S, *e->h_frame, e->S.scope,
                                                                   &e->S.ctr->ncollected, 0, F_INTEGRATE);
     TRY(check_launch());
   }
@@ -715,7 +738,7 @@ int vm_scope_halo(vm_engine *e, int64_t *n_scope, int32_t *scope_coords, uint8_t
   if (!e || !n_scope || !n_halo) return set_err(VM_ERR_INPUT, "null argument");
   CK(cudaMemsetAsync(&e->S.ctr->nslab, 0, sizeof(int32_t), e->stream));
   CK(cudaMemsetAsync(&e->S.ctr->nhalo, 0, sizeof(int32_t), e->stream));
-  k_fuse_blocks<<<grid_blocks(e), kThreadsCube, 0, e->stream>>>(e->S, *e->h_frame, e->S.scope,
+  k_fuse_blocks<<<grid_blocks(e), kFB, 0, e->stream>>>(e->S, *e->h_frame, e->S.scope,
                                                                 &e->S.ctr->ncollected, 0, F_SCOPE);
   TRY(check_launch());
   TRY(read_counters(e));

@@ -38,6 +38,7 @@ __device__ __forceinline__ int list_count(const int32_t *count_ptr, int count_co
 
 // ------------------------------------------------------------ depth stats
 __global__ void __launch_bounds__(256) k_depth_stats(DevState S, const FrameDev F) {
+  cudaGridDependencySynchronize();   // PDL: wait for the previous kernel of the frame
   __shared__ double smax[8];
   __shared__ int scnt[8];
   const long long npix = (long long)F.h * F.w;
@@ -73,6 +74,7 @@ __global__ void __launch_bounds__(256) k_depth_stats(DevState S, const FrameDev 
 // warp falling in the same block are merged with __match_any_sync, so one
 // lane per distinct block probes the hash table.
 __global__ void __launch_bounds__(256) k_collect(DevState S, const FrameDev F) {
+  cudaGridDependencySynchronize();   // PDL: wait for the previous kernel of the frame
   Counters *ctr = S.ctr;
   if (ld_vol(&ctr->nvalid) == 0) return;
   const double maxnorm = __longlong_as_double((long long)ld_vol(&ctr->maxnorm_bits));
@@ -179,22 +181,25 @@ __global__ void __launch_bounds__(kThreadsCube) k_init_blocks(DevState S) {
 //  F_SCOPE     27-neighbour halo marking and minus-slab scope marking
 //              (mesher.py:499-543), with hash lookups (links of blocks
 //              created in this launch are still being written).
-__global__ void __launch_bounds__(kThreadsCube) k_fuse_blocks(DevState S, const FrameDev F,
-                                                              const int32_t *__restrict__ list,
-                                                              const int32_t *__restrict__ count_ptr,
-                                                              int count_const, int flags) {
+constexpr int kFB = 128;   // threads per CTA of k_fuse_blocks (4 corners each)
+
+__global__ void __launch_bounds__(kFB) k_fuse_blocks(DevState S, const FrameDev F,
+                                                     const int32_t *__restrict__ list,
+                                                     const int32_t *__restrict__ count_ptr,
+                                                     int count_const, int flags) {
+  cudaGridDependencySynchronize();   // PDL: wait for the previous kernel of the frame
   if (halted(S)) return;
   const int n = list_count(count_ptr, count_const);
-  const int ci = threadIdx.x;
-  const int lx = ci >> 6, ly = (ci >> 3) & 7, lz = ci & 7;
+  const int t = threadIdx.x;
   for (int i = blockIdx.x; i < n; i += gridDim.x) {
-    const int b = list[i];
+    const int b = __ldcg(list + i);
     if (b < 0) continue;
-    const int4 c = S.bcoord[b];
-    const bool fresh = (flags & F_INIT) && S.stamp_new[b] == F.epoch;
-    if (fresh) init_block(S, b, ci);
-    if ((flags & (F_SCOPE | F_INIT)) && ci < 27) {
-      const int t = ci;
+    const int4 c = __ldcg(S.bcoord + b);
+    const bool fresh = (flags & F_INIT) && __ldcg(S.stamp_new + b) == F.epoch;
+    if (fresh)
+#pragma unroll
+      for (int j = 0; j < kNC / kFB; j++) init_block(S, b, t + j * kFB);
+    if ((flags & (F_SCOPE | F_INIT)) && t < 27) {
       const int dx = t / 9 - 1, dy = (t / 3) % 3 - 1, dz = t % 3 - 1;
       int nb = b, nb_collected = 1;
       if (t != 13) {
@@ -220,29 +225,47 @@ __global__ void __launch_bounds__(kThreadsCube) k_fuse_blocks(DevState S, const 
       }
     }
     if (!(flags & F_INTEGRATE)) continue;
-    double a[3];
-    a[0] = __dadd_rn(__dmul_rn((double)c.x, S.extent), __dmul_rn((double)lx, S.cube_size)) - F.t[0];
-    a[1] = __dadd_rn(__dmul_rn((double)c.y, S.extent), __dmul_rn((double)ly, S.cube_size)) - F.t[1];
-    a[2] = __dadd_rn(__dmul_rn((double)c.z, S.extent), __dmul_rn((double)lz, S.cube_size)) - F.t[2];
-    const double z = matvec_col(a, F.R, 2);
-    if (!(z > 0)) continue;
-    const double x = matvec_col(a, F.R, 0), y = matvec_col(a, F.R, 1);
-    const double u = rint(__dadd_rn(__dmul_rn(F.fx, x) / z, F.cx));
-    const double v = rint(__dadd_rn(__dmul_rn(F.fy, y) / z, F.cy));
-    if (!(u >= 0 && u < (double)F.w && v >= 0 && v < (double)F.h)) continue;
-    const double meas = F.depth[(long long)v * F.w + (long long)u];
-    if (!(meas > 0 && meas <= F.max_range)) continue;
-    const double sdf = meas - z;
-    if (!(sdf >= -F.trunc)) continue;
-    double dn = sdf / F.trunc;
-    dn = dn < -1.0 ? -1.0 : (dn > 1.0 ? 1.0 : dn);
-    const size_t q = (size_t)b * kNC + ci;
-    const int w_old = fresh ? 0 : S.weight[q];
-    const double t_old = fresh ? 0.0 : S.tsdf[q];
-    const double wo = (double)w_old;
-    S.tsdf[q] = __dadd_rn(__dmul_rn(wo, t_old), dn) / __dadd_rn(wo, 1.0);
-    const long long nw = (long long)w_old + 1;
-    S.weight[q] = (int)(nw < F.weight_cap ? nw : F.weight_cap);
+    // fusion.py:138-168, four corners per thread: projections, then gathers
+    const double bx = __dmul_rn((double)c.x, S.extent), by = __dmul_rn((double)c.y, S.extent),
+                 bz = __dmul_rn((double)c.z, S.extent);
+    double zc[kNC / kFB], meas[kNC / kFB];
+    bool ok[kNC / kFB];
+#pragma unroll
+    for (int j = 0; j < kNC / kFB; j++) {
+      const int ci = t + j * kFB;
+      double a[3];
+      a[0] = __dadd_rn(bx, __dmul_rn((double)(ci >> 6), S.cube_size)) - F.t[0];
+      a[1] = __dadd_rn(by, __dmul_rn((double)((ci >> 3) & 7), S.cube_size)) - F.t[1];
+      a[2] = __dadd_rn(bz, __dmul_rn((double)(ci & 7), S.cube_size)) - F.t[2];
+      const double z = matvec_col(a, F.R, 2);
+      zc[j] = z;
+      ok[j] = false;
+      meas[j] = 0.0;
+      if (!(z > 0)) continue;
+      const double x = matvec_col(a, F.R, 0), y = matvec_col(a, F.R, 1);
+      const double u = rint(__dadd_rn(__dmul_rn(F.fx, x) / z, F.cx));
+      const double v = rint(__dadd_rn(__dmul_rn(F.fy, y) / z, F.cy));
+      if (!(u >= 0 && u < (double)F.w && v >= 0 && v < (double)F.h)) continue;
+      ok[j] = true;
+      meas[j] = F.depth[(long long)v * F.w + (long long)u];
+    }
+#pragma unroll
+    for (int j = 0; j < kNC / kFB; j++) {
+      if (!ok[j]) continue;
+      const double m = meas[j];
+      if (!(m > 0 && m <= F.max_range)) continue;
+      const double sdf = m - zc[j];
+      if (!(sdf >= -F.trunc)) continue;
+      double dn = sdf / F.trunc;
+      dn = dn < -1.0 ? -1.0 : (dn > 1.0 ? 1.0 : dn);
+      const size_t q = (size_t)b * kNC + t + j * kFB;
+      const int w_old = fresh ? 0 : S.weight[q];
+      const double t_old = fresh ? 0.0 : S.tsdf[q];
+      const double wo = (double)w_old;
+      S.tsdf[q] = __dadd_rn(__dmul_rn(wo, t_old), dn) / __dadd_rn(wo, 1.0);
+      const long long nw = (long long)w_old + 1;
+      S.weight[q] = (int)(nw < F.weight_cap ? nw : F.weight_cap);
+    }
   }
 }
 
@@ -416,6 +439,7 @@ constexpr int kNT = 128;   // threads per CTA of the per-block meshing kernels (
 // edge) and writes the interpolated coordinate; all requesters produce
 // identical bits (mesher.py:216-235).
 __global__ void __launch_bounds__(kNT, 8) k_retype_place(DevState S, const FrameDev F) {
+  cudaGridDependencySynchronize();   // PDL: wait for the previous kernel of the frame
   if (halted(S)) return;
   __shared__ double tile[729];
   __shared__ uint8_t tw[729];
@@ -703,6 +727,7 @@ __device__ void fallback_normal_warp(const DevState &S, const uint8_t *ttile, co
 // shared memory, then runs the ordered warp accumulation.
 constexpr int kFT = 128;
 __global__ void __launch_bounds__(kFT) k_fallback(DevState S, const FrameDev F) {
+  cudaGridDependencySynchronize();   // PDL: wait for the previous kernel of the frame
   if (halted(S)) return;
   __shared__ int s_nbr[kFT / 32][27];
   __shared__ uint8_t s_tt[kFT / 32][729];
@@ -752,6 +777,7 @@ __global__ void __launch_bounds__(kGT, 16) k_gc_normals(DevState S, const FrameD
                                                     const int32_t *__restrict__ list,
                                                     const int32_t *__restrict__ count_ptr,
                                                     int count_const, int mode) {
+  cudaGridDependencySynchronize();   // PDL: wait for the previous kernel of the frame
   if (halted(S)) return;
   Counters *ctr = S.ctr;
   const bool run = !(mode & G_REQUIRE_ITEMS) || __ldcg(&ctr->nitems_live) > 0;
