@@ -122,8 +122,9 @@ class ClockSampler:
 
 
 def make_frames(spec, nframes, device):
-    from paper_1803_03949_b200.synth import camera_pose, render_depth, render_depth_torch
-    poses = [camera_pose(spec, i) for i in range(nframes)]
+    from paper_1803_03949_b200.synth import camera_pose, multiroom_pose, render_depth, render_depth_torch
+    pose_fn = multiroom_pose if spec.scene == "multiroom" else camera_pose
+    poses = [pose_fn(spec, i) for i in range(nframes)]
     if device is not None:
         depths = [render_depth_torch(spec, p, device=device) for p in poses]
     else:
@@ -172,10 +173,19 @@ def run_reference(args, spec, cfg, rank, world):
     print(json.dumps(line), flush=True)
 
 
+CONFIG_TEXT = {
+    "C1": "BASELINE.json configs[0] synthetic sphere+box scene",
+    "C2": "BASELINE.json configs[1] synthetic room 4x4x2.5 m, 300-frame trajectory",
+    "C3": "BASELINE.json configs[2] room with Hamming refinement every frame",
+    "C4": "BASELINE.json configs[3] fine resolution room, 40 mm band",
+    "C5": "BASELINE.json configs[4] 20x20 m multi-room scene",
+}
+
+
 def workload(args, spec, cfg):
-    return {"workload": f"{args.config}: BASELINE.json configs[1] synthetic room 4x4x2.5 m, "
+    return {"workload": f"{args.config}: {CONFIG_TEXT.get(args.config, args.config)}, "
                         f"{spec.width}x{spec.height} depth, {cfg['cube_size'] * 1e3:.0f} mm voxels, "
-                        "integrate + incremental mesh update + GC",
+                        "integrate + incremental mesh update (+refine) + GC",
             "frames": args.warmup + args.steps, "width": spec.width, "height": spec.height,
             "cube_size_m": cfg["cube_size"], "trunc_m": cfg["trunc"],
             "refine": bool(cfg.get("refine", False)), "strategy": args.strategy,
@@ -256,6 +266,10 @@ def run_gpu(args, spec, cfg, rank, world, local_rank):
     bytes_dom = sum(phase_bytes(s, spec.height, spec.width)[dom] for s in stats)
     achieved = bytes_dom / (tot[dom] / 1e3) / 1e9
     peak, peak_kind = measured_peak_gbs()
+    traffic = None   # dram read+write bytes per launch of that kernel, from the committed ncu capture
+    tp = ROOT / "profiles" / "ncu_traffic.json"
+    if tp.exists():
+        traffic = json.loads(tp.read_text()).get("dram_bytes_per_launch", {}).get(f"k_{dom}")
     frame_bytes = sum(sum(phase_bytes(s, spec.height, spec.width).values()) for s in stats)
 
     # e2e: public API, pinned host depth, H2D + StatsRow D2H per frame, wall clock
@@ -298,7 +312,7 @@ def run_gpu(args, spec, cfg, rank, world, local_rank):
         "config": workload(args, spec, cfg),
         "roofline": {"bound": "hbm", "kernel": f"k_{dom}", "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "kernel_share": tot[dom] / sum(tot.values()),
+                     "traffic": traffic, "alg_bytes_per_launch": bytes_dom / args.steps, "kernel_share": tot[dom] / sum(tot.values()),
                      "frame_alg_bytes": frame_bytes / args.steps,
                      "frame_achieved_gbs": frame_bytes / dev_s / 1e9 / world,
                      "frame_frac": frame_bytes / dev_s / 1e9 / world / peak},

@@ -241,12 +241,16 @@ def config_spec(name: str) -> tuple:
 
 
 def multiroom_pose(spec: SceneSpec, i: int) -> Pose:
-    """Lawn-mower trajectory at 1.4 m height through the 20x20 m multi-room (C5)."""
-    lane = (i // 100) % 8
-    s = (i % 100) / 99.0
-    y = -8.75 + 2.5 * lane
-    x = -9.0 + 18.0 * (s if lane % 2 == 0 else 1.0 - s)
-    ang = 2.0 * math.pi * (i / 37.0)
-    pos = np.array([x, y, -0.1])
-    fwd = np.array([math.cos(ang), math.sin(ang), -0.15])
+    """C5 trajectory: the camera visits the 16 rooms of the 20x20 m floor in a
+    serpentine order, 125 frames per room, circling 0.6 m around the room
+    centre at 1.4 m above the floor while panning (two turns per room)."""
+    room = (i // 125) % 16
+    row, col = room // 4, room % 4
+    if row % 2:
+        col = 3 - col
+    cx, cy = -7.5 + 5.0 * col, -7.5 + 5.0 * row
+    ph = 2.0 * math.pi * (i % 125) / 125.0
+    pos = np.array([cx + 0.6 * math.cos(ph), cy + 0.6 * math.sin(ph), -0.1])
+    ang = 2.0 * ph + 0.3
+    fwd = np.array([math.cos(ang), math.sin(ang), -0.2 + 0.15 * math.sin(3.0 * ph)])
     return static_pose(pos, pos + fwd)

@@ -123,7 +123,7 @@ def test_extract_fields_match_reference(name, strategy):
     _check_mesh(st.compact_mesh(2), g)
 
 
-def _run_oracle_and_gpu(spec, cfg, frames, strategy="claim", rng=None):
+def _run_oracle_and_gpu(spec, cfg, frames, strategy="claim", rng=None, pose_fn=None):
     from oracle.oracle import OracleEngine
     from paper_1803_03949_b200 import Engine, RunConfig
     from paper_1803_03949_b200.synth import camera_pose, render_depth
@@ -131,7 +131,7 @@ def _run_oracle_and_gpu(spec, cfg, frames, strategy="claim", rng=None):
     eng = Engine(RunConfig(strategy=strategy, **cfg), intr)
     ora = OracleEngine(cfg, (intr.fx, intr.fy, intr.cx, intr.cy, intr.width, intr.height))
     for i in range(frames):
-        pose = camera_pose(spec, i)
+        pose = (pose_fn or camera_pose)(spec, i)
         d = render_depth(spec, pose, rng)
         row = eng.fuse_frame(d, pose)
         ref = ora.fuse_frame(d, pose.rotation, pose.translation)
@@ -194,3 +194,22 @@ def test_run_to_run_and_strategy_determinism():
         assert np.array_equal(m.positions, meshes[0].positions)
         assert np.array_equal(m.indices, meshes[0].indices)
         assert np.array_equal(m.normals, meshes[0].normals)
+
+
+def test_c4_fine_resolution_prefix_matches_oracle():
+    """BASELINE config C4 (4 mm cubes, 40 mm band: 8 ray steps) at 320x240, 3 frames."""
+    from paper_1803_03949_b200.synth import config_spec
+    spec, cfg = config_spec("C4")
+    spec.width, spec.height, spec.fx, spec.fy = 320, 240, 262.5, 262.5
+    eng, ora = _run_oracle_and_gpu(spec, cfg, 3)
+    assert eng.device_stats[-1]["nsteps"] >= 8
+    _compare_final(eng, ora)
+
+
+def test_c5_multiroom_prefix_matches_oracle():
+    """BASELINE config C5 (20 x 20 m multi-room, table 2^21) at 320x240, 4 frames."""
+    from paper_1803_03949_b200.synth import config_spec, multiroom_pose
+    spec, cfg = config_spec("C5")
+    spec.width, spec.height, spec.fx, spec.fy = 320, 240, 262.5, 262.5
+    eng, ora = _run_oracle_and_gpu(spec, cfg, 4, pose_fn=multiroom_pose)
+    _compare_final(eng, ora)
