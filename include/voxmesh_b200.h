@@ -44,6 +44,14 @@ typedef struct {
   int64_t initial_blocks;    /* capacity hints for the device arenas (0 = default); */
   int64_t initial_vertices;  /* the arenas grow geometrically when a frame needs more */
   int64_t initial_triangles;
+  /* spatial partition across ranks; nranks <= 1: off.
+   * Blocks belong to hashed tiles of tile_blocks^3 blocks; each rank owns its
+   * tiles and also computes a 1-block margin around them, so every owned
+   * result is exact with no halo exchange.  Counters cover owned blocks. */
+  int32_t rank;
+  int32_t nranks;
+  int32_t tile_blocks;       /* power of two (default 8) */
+  int32_t reserved;
 } vm_store_config;
 
 /* Intrinsics (fusion.py:20-33) */
@@ -102,6 +110,20 @@ typedef struct {
   double fusion_ms;       /* collect + integrate (engine.py:127-132 split) */
   double meshing_ms;      /* scope .. normals (engine.py:134-144 split) */
 } vm_stats;
+
+/* Export the state of this engine's blocks (owned_only: the blocks this rank
+ * owns) as dense arrays; pass coords == NULL to query *n_out first.  Arrays:
+ * coords i32[n,3], tsdf f64[n,512], weight i32[n,512], type_prev/type_curr
+ * u8[n,512], slot birth i32[n,1536], slot coordinate f64[n,1536], slot
+ * normal f64[n,1536,3]. */
+int vm_export_blocks(vm_engine *e, int32_t owned_only, int64_t *n_out, int32_t *coords, double *tsdf,
+                     int32_t *weight, uint8_t *type_prev, uint8_t *type_curr, int32_t *birth,
+                     double *param, double *normal);
+/* Import block states exported by vm_export_blocks (allocating the blocks);
+ * used to merge the ranks of a partitioned reconstruction for compaction. */
+int vm_import_blocks(vm_engine *e, int64_t n, const int32_t *coords, const double *tsdf,
+                     const int32_t *weight, const uint8_t *type_prev, const uint8_t *type_curr,
+                     const int32_t *birth, const double *param, const double *normal);
 
 /* AuditReport (engine.py:89-101) */
 typedef struct {

@@ -23,7 +23,8 @@ STRATEGY_CODES = {"serial": 0, "claim": 1, "partition": 2}
 class StoreConfig(C.Structure):
     _fields_ = [("cube_size", C.c_double), ("table_size", C.c_int64), ("max_vertices", C.c_int64),
                 ("initial_blocks", C.c_int64), ("initial_vertices", C.c_int64),
-                ("initial_triangles", C.c_int64)]
+                ("initial_triangles", C.c_int64), ("rank", C.c_int32), ("nranks", C.c_int32),
+                ("tile_blocks", C.c_int32), ("reserved", C.c_int32)]
 
 
 class Intr(C.Structure):
@@ -119,6 +120,8 @@ _SIGS = {
     "vm_compact": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "vm_compact_fetch": (C.c_int, [C.c_void_p] + [C.c_void_p] * 4),
     "vm_audit": (C.c_int, [C.c_void_p, C.POINTER(AuditC)]),
+    "vm_export_blocks": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_int64)] + [C.c_void_p] * 8),
+    "vm_import_blocks": (C.c_int, [C.c_void_p, C.c_int64] + [C.c_void_p] * 8),
 }
 
 EXPORTED = tuple(_SIGS)

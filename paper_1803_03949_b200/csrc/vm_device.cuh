@@ -49,6 +49,7 @@ struct Counters {
   int64_t t_count;
   int64_t t_recycled;
   int64_t irregular;     // Engine.irregular_cube_count, maintained incrementally
+  int64_t nblocks_owned; // blocks this rank owns (== nblocks unless partitioned)
   int64_t err_info[4];
   // ---- per call ----------------------------------------------------------
   int32_t nvalid;
@@ -136,6 +137,10 @@ struct DevState {
   uint32_t *item_mask;  // [cap*16] explicit scope cube masks
   int2 *fallback;       // [cap*1536] face-normal fallback worklist (block, slot)
   long long max_vertices;
+  // spatial partition: blocks are owned by hashed tiles
+  // of 2^tile_shift blocks per axis; a rank also computes a 1-block margin
+  int32_t rank, nranks, tile_shift;
+  uint8_t *bowned;      // [max_blocks] block owned by this rank
   Counters *ctr;
 };
 
@@ -245,6 +250,28 @@ __device__ int hash_find(const DevState &S, int x, int y, int z) {
   return -1;
 }
 
+// ---------------------------------------------------------------- partition
+__device__ __forceinline__ int tile_owner(const DevState &S, int tx, int ty, int tz) {
+  long long h = ((long long)tx * 73856093LL) ^ ((long long)ty * 19349669LL) ^ ((long long)tz * 83492791LL);
+  long long m = h % S.nranks;
+  return (int)(m < 0 ? m + S.nranks : m);
+}
+__device__ __forceinline__ bool block_owned(const DevState &S, int x, int y, int z) {
+  return S.nranks <= 1 || tile_owner(S, x >> S.tile_shift, y >> S.tile_shift, z >> S.tile_shift) == S.rank;
+}
+// owned, or within one block of an owned tile (the margin this rank computes)
+__device__ __forceinline__ bool block_relevant(const DevState &S, int x, int y, int z) {
+  if (S.nranks <= 1) return true;
+  const int sh = S.tile_shift;
+  const int x0 = (x - 1) >> sh, x1 = (x + 1) >> sh, y0 = (y - 1) >> sh, y1 = (y + 1) >> sh;
+  const int z0 = (z - 1) >> sh, z1 = (z + 1) >> sh;
+  for (int tx = x0; tx <= x1; tx++)
+    for (int ty = y0; ty <= y1; ty++)
+      for (int tz = z0; tz <= z1; tz++)
+        if (tile_owner(S, tx, ty, tz) == S.rank) return true;
+  return false;
+}
+
 // allocate the next block index; CapacityError at 2*n >= table_size (store.py:304-306)
 __device__ int alloc_block(const DevState &S, int x, int y, int z, int epoch) {
   int idx = atomicAdd(&S.ctr->nblocks, 1);
@@ -255,6 +282,9 @@ __device__ int alloc_block(const DevState &S, int x, int y, int z, int epoch) {
   if (idx >= S.block_cap) atomicOr(&S.ctr->need, NEED_BLOCKS);
   S.bcoord[idx] = make_int4(x, y, z, 0);
   S.stamp_new[idx] = epoch;
+  const bool own = block_owned(S, x, y, z);
+  S.bowned[idx] = own;
+  if (own) atomicAdd((unsigned long long *)&S.ctr->nblocks_owned, 1ull);
   S.newlist[atomicAdd(&S.ctr->nnew, 1)] = idx;
   return idx;
 }

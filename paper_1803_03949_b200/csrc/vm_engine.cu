@@ -456,6 +456,15 @@ int vm_create(const vm_store_config *cfg, vm_engine **out) {
   S.nbuckets = (int32_t)((cfg->table_size + kSlotsPerBucket - 1) / kSlotsPerBucket);
   S.max_blocks = (int32_t)((cfg->table_size + 1) / 2);
   S.max_vertices = cfg->max_vertices;
+  S.rank = cfg->nranks > 1 ? cfg->rank : 0;
+  S.nranks = cfg->nranks > 1 ? cfg->nranks : 1;
+  {
+    const int tb = cfg->tile_blocks > 0 ? cfg->tile_blocks : 8;
+    if (tb & (tb - 1)) return set_err(VM_ERR_VALUE, "tile_blocks must be a power of two");
+    if (S.rank < 0 || S.rank >= S.nranks) return set_err(VM_ERR_VALUE, "rank out of range");
+    S.tile_shift = 0;
+    while ((1 << S.tile_shift) < tb) S.tile_shift++;
+  }
   const size_t mb = (size_t)S.max_blocks;
   TRY(dev_alloc(&S.slots, (size_t)S.nbuckets * kSlotsPerBucket, 0xFF));
   TRY(dev_alloc(&S.ovf_head, (size_t)S.nbuckets, 0xFF));
@@ -470,6 +479,7 @@ int vm_create(const vm_store_config *cfg, vm_engine **out) {
   TRY(dev_alloc(&S.stamp_collect, mb, 0xFF));
   TRY(dev_alloc(&S.stamp_halo, mb, 0xFF));
   TRY(dev_alloc(&S.stamp_new, mb, 0xFF));
+  TRY(dev_alloc(&S.bowned, mb, 0));
   TRY(dev_alloc(&S.slab_bits, (mb + 4) & ~(size_t)3, 0));
   TRY(dev_alloc(&S.scope, mb));
   TRY(dev_alloc(&S.newlist, mb));
@@ -507,7 +517,7 @@ int vm_destroy(vm_engine *e) {
   cudaStreamSynchronize(e->stream);
   DevState &S = e->S;
   void *ptrs[] = {S.slots, S.ovf_head, S.ovf_lock, S.ovf_key, S.ovf_val, S.ovf_next, S.ovf_stamp, S.bcoord,
-                  S.nbr, S.stamp_collect, S.stamp_halo, S.stamp_new, S.slab_bits, S.scope, S.newlist,
+                  S.nbr, S.stamp_collect, S.stamp_halo, S.stamp_new, S.bowned, S.slab_bits, S.scope, S.newlist,
                   S.halo, S.tsdf, S.weight, S.tp, S.tc, S.vbirth, S.vparam, S.vnrm, S.item_mask, S.fallback,
                   S.ctr, e->d_depth, e->d_scratch};
   for (void *p : ptrs)
@@ -568,7 +578,7 @@ static void fill_stats(vm_engine *e, int64_t frame, vm_stats *out) {
   const Counters &c = *e->h_ctr;
   memset(out, 0, sizeof *out);
   out->frame = frame;
-  out->blocks_active = c.nblocks;
+  out->blocks_active = c.nblocks_owned;
   out->vertices_live = c.v_live;
   out->triangles_live = c.t_live;
   out->vertices_allocated_total = c.v_count;
@@ -961,8 +971,8 @@ int vm_counters(vm_engine *e, vm_counter_set *out) {
   if (!e || !out) return set_err(VM_ERR_INPUT, "null argument");
   TRY(read_counters(e));
   const Counters &c = *e->h_ctr;
-  out->block_count = c.nblocks;
-  out->block_allocations = c.nblocks;
+  out->block_count = c.nblocks_owned;
+  out->block_allocations = c.nblocks_owned;
   out->vertex_count = c.v_count;
   out->vertex_free = c.v_count - c.v_live;
   out->vertex_recycled_total = c.v_recycled;
@@ -1110,6 +1120,61 @@ int vm_compact_fetch(vm_engine *e, double *pos, double *nrm, int64_t *ages, int3
     if (ages) TRY(copy_sync(e, ages, c.age, 8ull * c.nv, cudaMemcpyDeviceToHost));
   }
   if (c.nt && idx) TRY(copy_sync(e, idx, c.idx, 12ull * c.nt, cudaMemcpyDeviceToHost));
+  return VM_OK;
+}
+
+int vm_export_blocks(vm_engine *e, int32_t owned_only, int64_t *n_out, int32_t *coords, double *tsdf,
+                     int32_t *weight, uint8_t *tp, uint8_t *tc, int32_t *birth, double *param, double *normal) {
+  if (!e || !n_out) return set_err(VM_ERR_INPUT, "null argument");
+  TRY(read_counters(e));
+  const int nb = e->h_ctr->nblocks;
+  std::vector<uint8_t> own(nb);
+  if (nb) TRY(copy_sync(e, own.data(), e->S.bowned, nb, cudaMemcpyDeviceToHost));
+  std::vector<int> sel;
+  for (int i = 0; i < nb; i++)
+    if (!owned_only || own[i] || e->S.nranks <= 1) sel.push_back(i);
+  *n_out = (int64_t)sel.size();
+  if (!coords || sel.empty()) return VM_OK;
+  const DevState &S = e->S;
+  std::vector<int4> bc(nb);
+  TRY(copy_sync(e, bc.data(), S.bcoord, sizeof(int4) * nb, cudaMemcpyDeviceToHost));
+  for (size_t k = 0; k < sel.size(); k++) {
+    const int i = sel[k];
+    coords[3 * k] = bc[i].x; coords[3 * k + 1] = bc[i].y; coords[3 * k + 2] = bc[i].z;
+    if (tsdf) TRY(copy_sync(e, tsdf + k * kNC, S.tsdf + (size_t)i * kNC, 8 * kNC, cudaMemcpyDeviceToHost));
+    if (weight) TRY(copy_sync(e, weight + k * kNC, S.weight + (size_t)i * kNC, 4 * kNC, cudaMemcpyDeviceToHost));
+    if (tp) TRY(copy_sync(e, tp + k * kNC, S.tp + (size_t)i * kNC, kNC, cudaMemcpyDeviceToHost));
+    if (tc) TRY(copy_sync(e, tc + k * kNC, S.tc + (size_t)i * kNC, kNC, cudaMemcpyDeviceToHost));
+    if (birth) TRY(copy_sync(e, birth + k * kEV, S.vbirth + (size_t)i * kEV, 4 * kEV, cudaMemcpyDeviceToHost));
+    if (param) TRY(copy_sync(e, param + k * kEV, S.vparam + (size_t)i * kEV, 8 * kEV, cudaMemcpyDeviceToHost));
+    if (normal) TRY(copy_sync(e, normal + k * kEV * 3, S.vnrm + (size_t)i * kEV * 3, 24 * kEV, cudaMemcpyDeviceToHost));
+  }
+  return VM_OK;
+}
+
+int vm_import_blocks(vm_engine *e, int64_t n, const int32_t *coords, const double *tsdf, const int32_t *weight,
+                     const uint8_t *tp, const uint8_t *tc, const int32_t *birth, const double *param,
+                     const double *normal) {
+  if (!e || (n && !coords)) return set_err(VM_ERR_INPUT, "null argument");
+  if (n <= 0) return VM_OK;
+  TRY(reset_call_counters(e));
+  int32_t *di;
+  TRY(map_coords(e, coords, n, &di, nullptr, ++e->epoch, true));
+  std::vector<int32_t> idx(n);
+  TRY(copy_sync(e, idx.data(), di, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+  TRY(init_new_blocks(e));
+  const DevState &S = e->S;
+  for (int64_t k = 0; k < n; k++) {
+    const size_t i = (size_t)idx[k];
+    if (idx[k] < 0) return set_err(VM_ERR_CAPACITY, "import: block table full");
+    if (tsdf) TRY(copy_sync(e, S.tsdf + i * kNC, tsdf + k * kNC, 8 * kNC, cudaMemcpyHostToDevice));
+    if (weight) TRY(copy_sync(e, S.weight + i * kNC, weight + k * kNC, 4 * kNC, cudaMemcpyHostToDevice));
+    if (tp) TRY(copy_sync(e, S.tp + i * kNC, tp + k * kNC, kNC, cudaMemcpyHostToDevice));
+    if (tc) TRY(copy_sync(e, S.tc + i * kNC, tc + k * kNC, kNC, cudaMemcpyHostToDevice));
+    if (birth) TRY(copy_sync(e, S.vbirth + i * kEV, birth + k * kEV, 4 * kEV, cudaMemcpyHostToDevice));
+    if (param) TRY(copy_sync(e, S.vparam + i * kEV, param + k * kEV, 8 * kEV, cudaMemcpyHostToDevice));
+    if (normal) TRY(copy_sync(e, S.vnrm + i * kEV * 3, normal + k * kEV * 3, 24 * kEV, cudaMemcpyHostToDevice));
+  }
   return VM_OK;
 }
 

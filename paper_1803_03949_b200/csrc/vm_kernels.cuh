@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(256) k_collect(DevState S, const FrameDev F) {
         const double f = __dadd_rn(1.0, __dmul_rn(s, delta));
         for (int j = 0; j < 3; j++)
           c[j] = (int)floor(__dadd_rn(F.t[j], __dmul_rn(qs[j], f)) / S.extent);
-        key = pack_coord(c[0], c[1], c[2]);
+        if (block_relevant(S, c[0], c[1], c[2])) key = pack_coord(c[0], c[1], c[2]);
       }
       const unsigned grp = __match_any_sync(0xffffffffu, key);
       if (key != kEmptyKey && lane == __ffs(grp) - 1) {
@@ -378,6 +378,7 @@ struct Resolved {
   int4 coord;
   int nbr[27];
   int b, mode, slab, item;   // mode: -1 past the end, 0 skip, 1 full, 2 slab bits, 3 explicit mask
+  int owned;                 // counters only accumulate over blocks this rank owns
 };
 
 // registers warp 0 carries while the loads of a future item are in flight
@@ -423,6 +424,7 @@ __device__ __forceinline__ void resolve_store(const DevState &S, const FrameDev 
     R.slab = slab;
     R.item = item;
     R.coord = c;
+    R.owned = (b >= 0 && S.nranks > 1) ? __ldcg(S.bowned + b) : 1;
   }
 }
 
@@ -471,6 +473,7 @@ __global__ void __launch_bounds__(kNT, 8) k_retype_place(DevState S, const Frame
       continue;
     }
     const int b = R.b;
+    const int own = R.owned;
     if (t == 0) live++;
     // stage the (B+1)^3 tile (mesher.py:75-96) and the current types
     {
@@ -543,12 +546,12 @@ __global__ void __launch_bounds__(kNT, 8) k_retype_place(DevState S, const Frame
         if (do_refine) {
           bool ch;
           tc = refine_type(bits, tp, small, &ch);
-          refined += ch;
+          refined += ch && own;
         }
         const size_t q = (size_t)b * kNC + c;
         S.tp[q] = (uint8_t)tp;
         S.tc[q] = (uint8_t)tc;
-        if (tc != tp) {
+        if (tc != tp && own) {
           changed++;
           const int nold = c_tri_count[tp], nnew = c_tri_count[tc];
           t_rel += nold;
@@ -556,7 +559,7 @@ __global__ void __launch_bounds__(kNT, 8) k_retype_place(DevState S, const Frame
           irr += (nnew > 0 && !is_regular_type(tc)) - (nold > 0 && !is_regular_type(tp));
         }
         mask = c_edge_mask[tc];
-        if (mask) {
+        if (mask && own) {
           active++;
           placements += __popc(mask);
         }
@@ -590,7 +593,7 @@ __global__ void __launch_bounds__(kNT, 8) k_retype_place(DevState S, const Frame
       const int ga = (axis == 0 ? R.coord.x * kB + ox : axis == 1 ? R.coord.y * kB + oy : R.coord.z * kB + oz);
       S.vparam[slot] = __dadd_rn(__dmul_rn((double)ga, l), __dmul_rn(param, l));
       if (atomicCAS(S.vbirth + slot, -1, frame) == -1) {
-        allocs++;
+        allocs += (S.nranks <= 1 || S.bowned[owner]);   // counted by the slot's owning rank
         S.vnrm[3 * slot] = 0.0; S.vnrm[3 * slot + 1] = 0.0; S.vnrm[3 * slot + 2] = 0.0;
       }
     }
@@ -859,7 +862,7 @@ __global__ void __launch_bounds__(kGT, 16) k_gc_normals(DevState S, const FrameD
             }
           if (!ref) {
             S.vbirth[(size_t)b * kEV + sl] = -1;
-            frees++;
+            frees += R.owned;
             continue;
           }
         }
@@ -878,7 +881,7 @@ __global__ void __launch_bounds__(kGT, 16) k_gc_normals(DevState S, const FrameD
       for (int p = t; p < nv; p += kGT) {
         const int sl = s_vlist[p];
         const int ci = sl / 3, axis = sl - 3 * (sl / 3);
-        computed++;
+        computed += R.owned;
         const int c0[3] = {ci >> 6, (ci >> 3) & 7, ci & 7};
         int c1[3] = {c0[0], c0[1], c0[2]};
         c1[axis]++;
@@ -913,7 +916,7 @@ __global__ void __launch_bounds__(kGT, 16) k_gc_normals(DevState S, const FrameD
           double *dst = S.vnrm + 3 * ((size_t)b * kEV + sl);
           dst[0] = g[0] / nrm; dst[1] = g[1] / nrm; dst[2] = g[2] / nrm;
         } else {
-          fallbacks++;   // face-normal fallback: deferred to k_fallback (global worklist)
+          fallbacks += R.owned;   // face-normal fallback: deferred to k_fallback (global worklist)
           S.fallback[atomicAdd(&ctr->nfallback, 1)] = make_int2(b, sl);
         }
       }
@@ -957,7 +960,7 @@ __global__ void k_irregular_full(DevState S, int nblocks, unsigned long long *ou
   for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < (long long)nblocks * kNC;
        q += (long long)gridDim.x * blockDim.x) {
     const unsigned tc = S.tc[q];
-    cnt += c_tri_count[tc] > 0 && !is_regular_type(tc);
+    cnt += c_tri_count[tc] > 0 && !is_regular_type(tc) && (S.nranks <= 1 || S.bowned[q / kNC]);
   }
   cnt = warp_sum(cnt);
   if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(out, (unsigned long long)cnt);

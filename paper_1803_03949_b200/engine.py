@@ -44,6 +44,10 @@ class RunConfig:
     block_capacity: int = 0
     vertex_capacity: int = 0
     triangle_capacity: int = 0
+    # spatial partition: this engine computes rank's tiles
+    rank: int = 0
+    nranks: int = 1
+    tile_blocks: int = 8
 
     def resolved(self) -> "RunConfig":
         cfg = replace(self)
@@ -112,7 +116,8 @@ class Engine:
         self.store = SpatialStore(c.cube_size, table_size=c.table_size,
                                   max_vertices=c.max_vertices, initial_blocks=c.block_capacity,
                                   initial_vertices=c.vertex_capacity,
-                                  initial_triangles=c.triangle_capacity)
+                                  initial_triangles=c.triangle_capacity, rank=c.rank,
+                                  nranks=c.nranks, tile_blocks=c.tile_blocks)
         self.frame_index = 0
         self.stats: list[StatsRow] = []
         self.device_stats: list[dict] = []
