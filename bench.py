@@ -16,8 +16,12 @@ Arms
   (oracle/, serial C restatement of the reference) on a bounded prefix.
 * --impl reference: the reference CPU algorithm (the oracle port; the
   reference itself is pure Python and cannot travel) on the same frames.
-Multi-GPU (torchrun): independent replicas per rank (weak scaling), device
-time = max over ranks; see DESIGN.md section 6.
+Multi-GPU (torchrun, NCCL): default ``--mode partition`` -- one reconstruction
+spatially partitioned across the ranks (hashed tiles of --tile-blocks^3
+blocks), every rank fed the same frame; strong scaling,
+value = K / sum over frames of the max-over-ranks frame device time; the
+per-frame global StatsRow is one NCCL int64 all-reduce (inside e2e).
+``--mode replicas``: independent replicas (weak scaling).
 """
 from __future__ import annotations
 
@@ -190,13 +194,19 @@ def workload(args, spec, cfg):
             "cube_size_m": cfg["cube_size"], "trunc_m": cfg["trunc"],
             "refine": bool(cfg.get("refine", False)), "strategy": args.strategy,
             "l2": "flushed between frames (256 MiB write, outside the timed events)",
-            "parallelism": f"replicas x{args.gpus}" if args.gpus > 1 else "single GPU"}
+            "parallelism": (f"spatial partition x{args.gpus} (tiles of {args.tile_blocks}^3 blocks)"
+                            if args.gpus > 1 and args.mode == "partition" else
+                            f"replicas x{args.gpus}" if args.gpus > 1 else "single GPU")}
 
 
 def run_gpu(args, spec, cfg, rank, world, local_rank):
     import torch
     import torch.distributed as dist
     from paper_1803_03949_b200 import Engine, RunConfig
+    from paper_1803_03949_b200.partition import PartitionedEngine
+    part = world > 1 and args.mode == "partition"
+    ekw = dict(rank=rank, nranks=world, tile_blocks=args.tile_blocks) if part else {}
+    local_rank %= torch.cuda.device_count()   # (several ranks may share a GPU in tests)
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     nframes = args.warmup + args.steps
@@ -209,7 +219,7 @@ def run_gpu(args, spec, cfg, rank, world, local_rank):
 
     # sizing pass: learn the arena sizes the capacity guards ask for, so no
     # frame in the timed region has to grow an arena and resume
-    probe = Engine(RunConfig(strategy=args.strategy, **cfg), spec.intrinsics())
+    probe = Engine(RunConfig(strategy=args.strategy, **cfg, **ekw), spec.intrinsics())
     for i in range(nframes):
         probe.fuse_frame(depths[i], poses[i])
     caps = dict(block_capacity=probe.store._counters()["block_count"] + 64)
@@ -220,7 +230,7 @@ def run_gpu(args, spec, cfg, rank, world, local_rank):
     def timed_pass(profiling: bool):
         """warmup + steps frames on a fresh engine, each step timed with CUDA
         events on the engine's stream, L2 flushed between steps"""
-        eng = Engine(RunConfig(strategy=args.strategy, **cfg, **caps), spec.intrinsics())
+        eng = Engine(RunConfig(strategy=args.strategy, **cfg, **caps, **ekw), spec.intrinsics())
         eng.set_stream(stream.cuda_stream)
         eng.set_profiling(profiling)
         for i in range(args.warmup):
@@ -251,12 +261,20 @@ def run_gpu(args, spec, cfg, rank, world, local_rank):
     # second pass on a fresh engine (same frames, same state evolution) with an
     # event before every kernel: per-kernel durations for the roofline
     _, prof_frame_ms, phase_ms, _ = timed_pass(True)
-    dev_s = sum(frame_ms) / 1e3
-    if world > 1:
-        t = torch.tensor([dev_s], device=dev, dtype=torch.float64)
+    local_s = sum(frame_ms) / 1e3
+    if part:
+        # frames are processed jointly: a frame ends when its slowest rank ends
+        t = torch.tensor(frame_ms, device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dev_s = float(t.item())
-    value = world * args.steps / dev_s
+        dev_s = float(t.sum().item()) / 1e3
+        value = args.steps / dev_s
+    else:
+        dev_s = local_s
+        if world > 1:
+            t = torch.tensor([dev_s], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dev_s = float(t.item())
+        value = world * args.steps / dev_s
     stats = eng.device_stats[args.warmup:]
 
     # roofline: dominant kernel (largest share of the timed frames)
@@ -277,10 +295,16 @@ def run_gpu(args, spec, cfg, rank, world, local_rank):
     for hd, d in zip(host, depths):
         hd.copy_(d)
     host_np = [h.numpy() for h in host]
-    e2 = Engine(RunConfig(strategy=args.strategy, **cfg, **caps), spec.intrinsics())
+    if part:   # global StatsRow every frame: one NCCL all-reduce of the rank counters
+        e2 = PartitionedEngine(RunConfig(strategy=args.strategy, **cfg, **caps), spec.intrinsics(),
+                               tile_blocks=args.tile_blocks, device=dev)
+    else:
+        e2 = Engine(RunConfig(strategy=args.strategy, **cfg, **caps), spec.intrinsics())
     for i in range(args.warmup):
         e2.fuse_frame(host_np[i], poses[i])
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     t0 = time.perf_counter()
     for k in range(args.steps):
         e2.fuse_frame(host_np[args.warmup + k], poses[args.warmup + k])
@@ -291,7 +315,9 @@ def run_gpu(args, spec, cfg, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     # parity spot check of the timed engine vs the e2e engine (same frames)
-    same = eng.stats[-1].vertices_live == e2.stats[-1].vertices_live
+    e2_local = e2.engine if part else e2
+    same = eng.stats[-1].vertices_live == e2_local.stats[-1].vertices_live
+    glob = e2.stats[-1]
 
     if rank != 0:
         return
@@ -307,26 +333,26 @@ def run_gpu(args, spec, cfg, rank, world, local_rank):
     line = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * dev_s / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong" if part else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (sphere-traced analytic room, GPU-rendered f64 depth)",
         "config": workload(args, spec, cfg),
         "roofline": {"bound": "hbm", "kernel": f"k_{dom}", "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "alg_bytes_per_launch": bytes_dom / args.steps, "kernel_share": tot[dom] / sum(tot.values()),
                      "frame_alg_bytes": frame_bytes / args.steps,
-                     "frame_achieved_gbs": frame_bytes / dev_s / 1e9 / world,
-                     "frame_frac": frame_bytes / dev_s / 1e9 / world / peak},
+                     "frame_achieved_gbs": frame_bytes / local_s / 1e9,
+                     "frame_frac": frame_bytes / local_s / 1e9 / peak},
         "phase_ms_mean": {n: tot[n] / args.steps for n in names},
         "profiled_pass_ms_per_step": sum(prof_frame_ms) / args.steps,
         "cpu_baseline": cpu,
-        "e2e": {"value": world * args.steps / e2e_s, "unit": "frames/s",
+        "e2e": {"value": (1 if part else world) * args.steps / e2e_s, "unit": "frames/s",
                 "h2d_bytes_per_step": spec.width * spec.height * 8 + 256,
                 "d2h_bytes_per_step": 512},
-        "gpu_launches": launches_per_frame * args.steps,
+        "gpu_launches": launches_per_frame * args.steps * world,
         "resumes_in_timed_region": resumes,
         "clocks": clk,
-        "final_state": {"blocks": stats[-1]["blocks_active"], "vertices": stats[-1]["vertices_live"],
-                        "triangles": stats[-1]["triangles_live"], "e2e_state_match": bool(same)},
+        "final_state": {"blocks": glob.blocks_active, "vertices": glob.vertices_live,
+                        "triangles": glob.triangles_live, "e2e_state_match": bool(same)},
     }
     print(json.dumps(line), flush=True)
 
@@ -339,6 +365,9 @@ def main():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--strategy", default="claim")
+    ap.add_argument("--mode", default="partition", choices=["partition", "replicas"])
+    ap.add_argument("--tile-blocks", type=int, default=8)
+    ap.add_argument("--backend", default="nccl", help="gloo only to test N>1 on a single GPU")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--ref-budget", type=float, default=150.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -354,8 +383,8 @@ def main():
     if world > 1 and args.impl != "reference":
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(local_rank % torch.cuda.device_count())
+        dist.init_process_group(args.backend)
     try:
         if args.impl == "reference":
             run_reference(args, spec, cfg, rank, world)
