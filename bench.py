@@ -276,6 +276,7 @@ def run_gpu(args, spec, cfg, rank, world, local_rank):
             dev_s = float(t.item())
         value = world * args.steps / dev_s
     stats = eng.device_stats[args.warmup:]
+    launches = sum(s["kernel_launches"] for s in stats)   # our kernels in the timed region
 
     # roofline: dominant kernel (largest share of the timed frames)
     names = list(phase_ms[0].keys())
@@ -328,7 +329,6 @@ def run_gpu(args, spec, cfg, rank, world, local_rank):
         cpu = {"value": n / t, "unit": "frames/s", "cores": 1, "kind": "port",
                "sample": f"{args.config} frames 0..{n - 1} through the CPU oracle (serial C "
                          f"restatement of the reference, oracle/), {t:.1f} s"}
-    launches_per_frame = 6
     clk = clocks.summary()
     line = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
@@ -348,7 +348,7 @@ def run_gpu(args, spec, cfg, rank, world, local_rank):
         "e2e": {"value": (1 if part else world) * args.steps / e2e_s, "unit": "frames/s",
                 "h2d_bytes_per_step": spec.width * spec.height * 8 + 256,
                 "d2h_bytes_per_step": 512},
-        "gpu_launches": launches_per_frame * args.steps * world,
+        "gpu_launches": launches * world,
         "resumes_in_timed_region": resumes,
         "clocks": clk,
         "final_state": {"blocks": glob.blocks_active, "vertices": glob.vertices_live,

@@ -106,6 +106,7 @@ typedef struct {
   int64_t fallback_normals;
   int64_t refined_cubes;
   int64_t resumes;        /* arena growths that required a resume this frame */
+  int64_t kernel_launches;/* kernels this library launched for the frame */
   double device_ms;       /* device time of the frame (CUDA events) */
   double fusion_ms;       /* collect + integrate (engine.py:127-132 split) */
   double meshing_ms;      /* scope .. normals (engine.py:134-144 split) */

@@ -91,7 +91,7 @@ struct FrameDev {
   int32_t epoch;        // monotone stamp for per-call membership sets
   int32_t frame;        // frame index (vertex birth)
   int32_t scope_mode;   // 0: collected + slabs (device scope); 1: explicit items
-  int32_t pad;
+  int32_t nsteps_fixed; // > 0: band step count fixed by the intrinsics (k_depth_stats skipped)
 };
 
 // one hash slot: packed coordinate (-1 empty) and block index (-1 while the
@@ -443,11 +443,13 @@ __device__ __forceinline__ void block_add_counters(long long (&vals)[N], long lo
 #pragma unroll
     for (int k = 0; k < N; k++) sh[k * 32 + wid] = vals[k];
   __syncthreads();
-  if (threadIdx.x < N) {
-    long long r = 0;
-    for (int w = 0; w < nw; w++) r += sh[threadIdx.x * 32 + w];
-    if (r && dst[threadIdx.x]) atomicAdd((unsigned long long *)dst[threadIdx.x], (unsigned long long)r);
-  }
+#pragma unroll
+  for (int k = 0; k < N; k++)   // static indices: dst stays in registers
+    if (threadIdx.x == k) {
+      long long r = 0;
+      for (int w = 0; w < nw; w++) r += sh[k * 32 + w];
+      if (r && dst[k]) atomicAdd((unsigned long long *)dst[k], (unsigned long long)r);
+    }
 }
 
 // vertex position from its slot (mesher.py:216-235): every coordinate is

@@ -79,6 +79,11 @@ struct vm_engine {
   int pending = 0;
   int64_t pending_frame = 0;
   int last_resumes = 0;
+  int frame_launches = 0;   // kernels launched by the pending / last frame
+  // ray-norm bounds over the image, cached per (h, w, fx, fy, cx, cy)
+  double norm_key[6] = {0, 0, 0, 0, 0, 0};
+  double norm_lo = 0.0, norm_hi = 0.0;
+  bool norm_valid = false;
 };
 
 // ------------------------------------------------------------ helpers
@@ -243,6 +248,7 @@ static int complete_with_resume(vm_engine *e, int *resumes) {
     CK(cudaMemsetAsync(&e->S.ctr->need, 0, sizeof(int32_t), e->stream));
     if (resumes) (*resumes)++;
     TRY(enqueue_after_collect(e));
+    e->frame_launches += 4;
   }
   return set_err(VM_ERR_CUDA, "resume loop did not converge");
 }
@@ -601,6 +607,7 @@ static void fill_stats(vm_engine *e, int64_t frame, vm_stats *out) {
   out->fallback_normals = c.fallbacks;
   out->refined_cubes = c.refined;
   out->resumes = e->last_resumes;
+  out->kernel_launches = e->frame_launches;
   float ms = 0.f;
   if (cudaEventElapsedTime(&ms, e->ev[PH_DEPTH], e->ev[PH_END]) == cudaSuccess) out->device_ms = ms;
   if (e->profiling) {   // segment split needs the per-kernel events
@@ -611,6 +618,38 @@ static void fill_stats(vm_engine *e, int64_t frame, vm_stats *out) {
     out->meshing_ms = 0.0;
   }
   cudaGetLastError();
+}
+
+// band step count for a max ray norm, exactly as k_collect computes it (fusion.py:90-94)
+static int nsteps_for(double maxnorm, double trunc, double extent) {
+  const double band = (2.0 * trunc) * maxnorm;
+  int n = (int)std::ceil(band / (extent * 0.5)) + 1;
+  return n < 2 ? 2 : n;
+}
+
+// The step count is a monotone function of the max norm over the valid pixels,
+// which lies within [min, max] of the norm over the whole image: when both
+// bounds give the same count, the frame's count is known without reading the
+// depth and k_depth_stats is skipped.  Returns 0 when it is data dependent.
+static int fixed_nsteps(vm_engine *e, int32_t h, int32_t w, double trunc) {
+  FrameDev &F = *e->h_frame;
+  const double key[6] = {(double)h, (double)w, F.fx, F.fy, F.cx, F.cy};
+  if (!e->norm_valid || memcmp(key, e->norm_key, sizeof key) != 0) {
+    unsigned long long *d;
+    if (scratch(e, 2 * sizeof(unsigned long long), (void **)&d) != VM_OK) return 0;
+    const unsigned long long init[2] = {~0ull, 0ull};
+    unsigned long long res[2];
+    if (cudaMemcpyAsync(d, init, sizeof init, cudaMemcpyHostToDevice, e->stream) != cudaSuccess) return 0;
+    k_norm_bounds<<<grid_threads(e, (long long)h * w, 256), 256, 0, e->stream>>>(F, d);
+    if (cudaMemcpyAsync(res, d, sizeof res, cudaMemcpyDeviceToHost, e->stream) != cudaSuccess) return 0;
+    if (cudaStreamSynchronize(e->stream) != cudaSuccess) return 0;
+    memcpy(&e->norm_lo, &res[0], sizeof(double));
+    memcpy(&e->norm_hi, &res[1], sizeof(double));
+    memcpy(e->norm_key, key, sizeof key);
+    e->norm_valid = true;
+  }
+  const int lo = nsteps_for(e->norm_lo, trunc, e->S.extent), hi = nsteps_for(e->norm_hi, trunc, e->S.extent);
+  return lo == hi ? lo : 0;
 }
 
 int vm_fuse_frame_enqueue(vm_engine *e, const double *depth, int32_t h, int32_t w, int32_t depth_on_device,
@@ -633,10 +672,15 @@ int vm_fuse_frame_enqueue(vm_engine *e, const double *depth, int32_t h, int32_t 
   F.epoch = ++e->epoch;
   F.frame = (int32_t)frame_index;
   F.scope_mode = 0;
+  F.nsteps_fixed = fixed_nsteps(e, h, w, cfg->trunc);
   TRY(reset_call_counters(e));
   cudaStream_t st = e->stream;
   rec(e, PH_DEPTH);
-  k_depth_stats<<<grid_blocks(e), 256, 0, st>>>(e->S, *e->h_frame);
+  e->frame_launches = 5;   // collect, fuse, retype, gc, fallback (+ depth stats)
+  if (F.nsteps_fixed <= 0) {
+    k_depth_stats<<<grid_blocks(e), 256, 0, st>>>(e->S, *e->h_frame);
+    e->frame_launches++;
+  }
   rec(e, PH_COLLECT);
   launch_pdl(k_collect, grid_threads(e, (long long)h * w, 256), 256, st, e->S, *e->h_frame);
   TRY(enqueue_after_collect(e));
@@ -676,6 +720,7 @@ int vm_collect(vm_engine *e, const double *depth, int32_t h, int32_t w, int32_t 
   F.max_range = max_range;
   F.epoch = ++e->epoch;
   F.scope_mode = 0;
+  F.nsteps_fixed = 0;   // the phase API always runs the depth reduction
   TRY(reset_call_counters(e));
   k_depth_stats<<<grid_blocks(e), 256, 0, e->stream>>>(e->S, *e->h_frame);
   k_collect<<<grid_threads(e, (long long)h * w, 256), 256, 0, e->stream>>>(e->S, *e->h_frame);

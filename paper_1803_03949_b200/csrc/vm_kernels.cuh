@@ -69,39 +69,69 @@ __global__ void __launch_bounds__(256) k_depth_stats(DevState S, const FrameDev 
   }
 }
 
+// ------------------------------------------------------------ norm bounds
+// min / max ray norm over every pixel of an (h, w) image (positive doubles
+// order as their bit patterns).  The band step count is monotone in the max
+// norm over the VALID pixels, which lies between the two, so when both bounds
+// give the same count the frame needs no depth reduction (fusion.py:88-94).
+__global__ void k_norm_bounds(const FrameDev F, unsigned long long *out) {
+  const long long npix = (long long)F.h * F.w;
+  unsigned long long lo = ~0ull, hi = 0;
+  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < npix;
+       p += (long long)gridDim.x * blockDim.x) {
+    const int v = (int)(p / F.w), u = (int)(p - (long long)v * F.w);
+    const double rx = ((double)u - F.cx) / F.fx, ry = ((double)v - F.cy) / F.fy;
+    const unsigned long long b = (unsigned long long)__double_as_longlong(
+        sqrt(__dadd_rn(__dadd_rn(__dmul_rn(rx, rx), __dmul_rn(ry, ry)), 1.0)));
+    lo = b < lo ? b : lo;
+    hi = b > hi ? b : hi;
+  }
+  atomicMin(out, lo);
+  atomicMax(out + 1, hi);
+}
+
 // ------------------------------------------------------------ collect
 // One thread per pixel looping over the nsteps band samples.  Samples of a
 // warp falling in the same block are merged with __match_any_sync, so one
-// lane per distinct block probes the hash table.
+// lane per distinct block probes the hash table.  A warp covers an 8x4 pixel
+// tile (blocks project to compact image regions, so fewer distinct blocks per
+// warp than a 32-pixel row).
 __global__ void __launch_bounds__(256) k_collect(DevState S, const FrameDev F) {
   cudaGridDependencySynchronize();   // PDL: wait for the previous kernel of the frame
   Counters *ctr = S.ctr;
-  if (ld_vol(&ctr->nvalid) == 0) return;
-  const double maxnorm = __longlong_as_double((long long)ld_vol(&ctr->maxnorm_bits));
-  const double half_block = S.extent * 0.5;
-  const double band = __dmul_rn(__dmul_rn(2.0, F.trunc), maxnorm);
-  int nsteps = (int)ceil(band / half_block) + 1;
-  if (nsteps < 2) nsteps = 2;
-  if (blockIdx.x == 0 && threadIdx.x == 0) ctr->nsteps = nsteps;
+  int nsteps = F.nsteps_fixed;
+  if (nsteps <= 0) {
+    if (ld_vol(&ctr->nvalid) == 0) return;
+    const double maxnorm = __longlong_as_double((long long)ld_vol(&ctr->maxnorm_bits));
+    const double half_block = S.extent * 0.5;
+    const double band = __dmul_rn(__dmul_rn(2.0, F.trunc), maxnorm);
+    nsteps = (int)ceil(band / half_block) + 1;
+    if (nsteps < 2) nsteps = 2;
+  }
   const double step = 2.0 / (double)(nsteps - 1);
-  const long long npix = (long long)F.h * F.w;
   const int lane = threadIdx.x & 31;
-  const long long wstride = (long long)gridDim.x * blockDim.x;
-  for (long long base = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < npix;
-       base += wstride) {
-    const long long p = base + lane;
+  // warp tiles of 8x4 pixels, row-major over the tile grid
+  const int tiles_x = (F.w + 7) >> 3, tiles_y = (F.h + 3) >> 2;
+  const long long ntiles = (long long)tiles_x * tiles_y;
+  const long long wstride = (long long)gridDim.x * (blockDim.x >> 5);
+  int nvalid = 0;
+  for (long long tile = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); tile < ntiles;
+       tile += wstride) {
+    const int ty = (int)(tile / tiles_x), tx = (int)(tile - (long long)ty * tiles_x);
+    const int u = tx * 8 + (lane & 7), v = ty * 4 + (lane >> 3);
     double d = 0.0, qs[3] = {0, 0, 0};
     bool valid = false;
-    if (p < npix) {
-      d = F.depth[p];
+    if (u < F.w && v < F.h) {
+      d = F.depth[(long long)v * F.w + u];
       valid = d > 0 && d <= F.max_range;
     }
     if (valid) {
-      const int v = (int)(p / F.w), u = (int)(p - (long long)v * F.w);
+      nvalid++;
       const double rx = ((double)u - F.cx) / F.fx, ry = ((double)v - F.cy) / F.fy;
       const double pc[3] = {__dmul_rn(rx, d), __dmul_rn(ry, d), __dmul_rn(1.0, d)};
       for (int j = 0; j < 3; j++) qs[j] = matvec_row(pc, F.R, j);   // pts_cam @ R.T
     }
+    if (!__any_sync(0xffffffffu, valid)) continue;
     const double delta = valid ? F.trunc / d : 0.0;
     for (int i = 0; i < nsteps; i++) {
       long long key = kEmptyKey;
@@ -122,6 +152,16 @@ __global__ void __launch_bounds__(256) k_collect(DevState S, const FrameDev F) {
       }
     }
   }
+  if (F.nsteps_fixed > 0) {   // valid-pixel count (k_depth_stats did not run): one atomic per CTA
+    __shared__ int s_valid;
+    if (threadIdx.x == 0) s_valid = 0;
+    __syncthreads();
+    nvalid = warp_sum(nvalid);
+    if (lane == 0 && nvalid) atomicAdd(&s_valid, nvalid);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_valid) atomicAdd(&ctr->nvalid, s_valid);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) ctr->nsteps = nsteps;
 }
 
 // ------------------------------------------------------------ explicit lists
@@ -183,39 +223,78 @@ __global__ void __launch_bounds__(kThreadsCube) k_init_blocks(DevState S) {
 //              created in this launch are still being written).
 constexpr int kFB = 128;   // threads per CTA of k_fuse_blocks (4 corners each)
 
-__global__ void __launch_bounds__(kFB) k_fuse_blocks(DevState S, const FrameDev F,
+__global__ void __launch_bounds__(kFB, 6) k_fuse_blocks(DevState S, const FrameDev F,
                                                      const int32_t *__restrict__ list,
                                                      const int32_t *__restrict__ count_ptr,
                                                      int count_const, int flags) {
   cudaGridDependencySynchronize();   // PDL: wait for the previous kernel of the frame
-  if (halted(S)) return;
-  const int n = list_count(count_ptr, count_const);
+  const bool stop = halted(S);
+  const int n = list_count(count_ptr, count_const);   // issued together with the halt check
+  if (stop) return;
   const int t = threadIdx.x;
+  // neighbour probe of this thread: 7 lanes of each warp, directions 0..26
+  const int pl = t & 31, pdir = (t >> 5) * 7 + pl;
+  const bool prober = pl < 7 && pdir < 27;
   for (int i = blockIdx.x; i < n; i += gridDim.x) {
     const int b = __ldcg(list + i);
     if (b < 0) continue;
     const int4 c = __ldcg(S.bcoord + b);
     const bool fresh = (flags & F_INIT) && __ldcg(S.stamp_new + b) == F.epoch;
+    // fusion.py:138-168, four corners per thread.  The old state of the corners
+    // is requested first, so its round trip overlaps the projections and the
+    // depth gathers.
+    double t_old[kNC / kFB], zc[kNC / kFB], meas[kNC / kFB];
+    int w_old[kNC / kFB];
+    bool ok[kNC / kFB];
+    if (flags & F_INTEGRATE) {
+#pragma unroll
+      for (int j = 0; j < kNC / kFB; j++) {
+        const size_t q = (size_t)b * kNC + t + j * kFB;
+        t_old[j] = fresh ? 0.0 : S.tsdf[q];
+        w_old[j] = fresh ? 0 : S.weight[q];
+      }
+      const double bx = __dmul_rn((double)c.x, S.extent), by = __dmul_rn((double)c.y, S.extent),
+                   bz = __dmul_rn((double)c.z, S.extent);
+#pragma unroll
+      for (int j = 0; j < kNC / kFB; j++) {
+        const int ci = t + j * kFB;
+        double a[3];
+        a[0] = __dadd_rn(bx, __dmul_rn((double)(ci >> 6), S.cube_size)) - F.t[0];
+        a[1] = __dadd_rn(by, __dmul_rn((double)((ci >> 3) & 7), S.cube_size)) - F.t[1];
+        a[2] = __dadd_rn(bz, __dmul_rn((double)(ci & 7), S.cube_size)) - F.t[2];
+        const double z = matvec_col(a, F.R, 2);
+        zc[j] = z;
+        ok[j] = false;
+        meas[j] = 0.0;
+        if (!(z > 0)) continue;
+        const double x = matvec_col(a, F.R, 0), y = matvec_col(a, F.R, 1);
+        const double u = rint(__dadd_rn(__dmul_rn(F.fx, x) / z, F.cx));
+        const double v = rint(__dadd_rn(__dmul_rn(F.fy, y) / z, F.cy));
+        if (!(u >= 0 && u < (double)F.w && v >= 0 && v < (double)F.h)) continue;
+        ok[j] = true;
+        meas[j] = F.depth[(long long)v * F.w + (long long)u];
+      }
+    }
     if (fresh)
 #pragma unroll
       for (int j = 0; j < kNC / kFB; j++) init_block(S, b, t + j * kFB);
-    if ((flags & (F_SCOPE | F_INIT)) && t < 27) {
-      const int dx = t / 9 - 1, dy = (t / 3) % 3 - 1, dz = t % 3 - 1;
+    if ((flags & (F_SCOPE | F_INIT)) && prober) {
+      const int dx = pdir / 9 - 1, dy = (pdir / 3) % 3 - 1, dz = pdir % 3 - 1;
       int nb = b, nb_collected = 1;
-      if (t != 13) {
+      if (pdir != 13) {
         const HashRef r = hash_find_ref(S, c.x + dx, c.y + dy, c.z + dz);
         nb = r.idx;
         nb_collected = r.stamp == F.epoch;
       }
       if (fresh) {
-        S.nbr[(size_t)b * 27 + t] = nb;
-        if (nb >= 0 && t != 13) S.nbr[(size_t)nb * 27 + (26 - t)] = b;
+        S.nbr[(size_t)b * 27 + pdir] = nb;
+        if (nb >= 0 && pdir != 13) S.nbr[(size_t)nb * 27 + (26 - pdir)] = b;
       }
       if ((flags & F_SCOPE) && nb >= 0) {
         if (ld_vol(S.stamp_halo + nb) != F.epoch && atomicExch(S.stamp_halo + nb, F.epoch) != F.epoch)
           S.halo[atomicAdd(&S.ctr->nhalo, 1)] = nb;
         // minus neighbour n = c - o, o in {0,1}^3 \ 0, not itself collected
-        if (dx <= 0 && dy <= 0 && dz <= 0 && t != 13 && !nb_collected) {
+        if (dx <= 0 && dy <= 0 && dz <= 0 && pdir != 13 && !nb_collected) {
           const int o = (-dx) * 4 + (-dy) * 2 + (-dz);
           const unsigned sh = 8 * (nb & 3);
           const unsigned old = atomicOr((unsigned *)(S.slab_bits + (nb & ~3)), (1u << (o - 1)) << sh);
@@ -225,30 +304,6 @@ __global__ void __launch_bounds__(kFB) k_fuse_blocks(DevState S, const FrameDev 
       }
     }
     if (!(flags & F_INTEGRATE)) continue;
-    // fusion.py:138-168, four corners per thread: projections, then gathers
-    const double bx = __dmul_rn((double)c.x, S.extent), by = __dmul_rn((double)c.y, S.extent),
-                 bz = __dmul_rn((double)c.z, S.extent);
-    double zc[kNC / kFB], meas[kNC / kFB];
-    bool ok[kNC / kFB];
-#pragma unroll
-    for (int j = 0; j < kNC / kFB; j++) {
-      const int ci = t + j * kFB;
-      double a[3];
-      a[0] = __dadd_rn(bx, __dmul_rn((double)(ci >> 6), S.cube_size)) - F.t[0];
-      a[1] = __dadd_rn(by, __dmul_rn((double)((ci >> 3) & 7), S.cube_size)) - F.t[1];
-      a[2] = __dadd_rn(bz, __dmul_rn((double)(ci & 7), S.cube_size)) - F.t[2];
-      const double z = matvec_col(a, F.R, 2);
-      zc[j] = z;
-      ok[j] = false;
-      meas[j] = 0.0;
-      if (!(z > 0)) continue;
-      const double x = matvec_col(a, F.R, 0), y = matvec_col(a, F.R, 1);
-      const double u = rint(__dadd_rn(__dmul_rn(F.fx, x) / z, F.cx));
-      const double v = rint(__dadd_rn(__dmul_rn(F.fy, y) / z, F.cy));
-      if (!(u >= 0 && u < (double)F.w && v >= 0 && v < (double)F.h)) continue;
-      ok[j] = true;
-      meas[j] = F.depth[(long long)v * F.w + (long long)u];
-    }
 #pragma unroll
     for (int j = 0; j < kNC / kFB; j++) {
       if (!ok[j]) continue;
@@ -259,11 +314,9 @@ __global__ void __launch_bounds__(kFB) k_fuse_blocks(DevState S, const FrameDev 
       double dn = sdf / F.trunc;
       dn = dn < -1.0 ? -1.0 : (dn > 1.0 ? 1.0 : dn);
       const size_t q = (size_t)b * kNC + t + j * kFB;
-      const int w_old = fresh ? 0 : S.weight[q];
-      const double t_old = fresh ? 0.0 : S.tsdf[q];
-      const double wo = (double)w_old;
-      S.tsdf[q] = __dadd_rn(__dmul_rn(wo, t_old), dn) / __dadd_rn(wo, 1.0);
-      const long long nw = (long long)w_old + 1;
+      const double wo = (double)w_old[j];
+      S.tsdf[q] = __dadd_rn(__dmul_rn(wo, t_old[j]), dn) / __dadd_rn(wo, 1.0);
+      const long long nw = (long long)w_old[j] + 1;
       S.weight[q] = (int)(nw < F.weight_cap ? nw : F.weight_cap);
     }
   }
@@ -846,20 +899,21 @@ __global__ void __launch_bounds__(kGT, 16) k_gc_normals(DevState S, const FrameD
       const int x = c >> 6, y = (c >> 3) & 7, z = c & 7;
       int keep = 0;
       unsigned keep_axes = 0;
+#pragma unroll
       for (int axis = 0; axis < 3; axis++) {
         const int sl = c * 3 + axis;
         if (!((occ[sl >> 5] >> (sl & 31)) & 1)) continue;
         if (mode & G_GC) {
-          const int u = axis == 0 ? 1 : 0, w = axis == 2 ? 1 : 2;
+          // the 4 cubes around the edge: offsets -du along u, -dw along w
+          // (u, w = the two axes other than `axis`); tile strides 81, 9, 1
+          const int su = axis == 0 ? 9 : 81, sw = axis == 2 ? 9 : 1;
+          const int p0 = ((x + 1) * 9 + (y + 1)) * 9 + (z + 1);
           bool ref = false;
-          for (int du = 0; du < 2 && !ref; du++)
-            for (int dw = 0; dw < 2 && !ref; dw++) {
-              int l[3] = {x, y, z};
-              l[u] -= du;
-              l[w] -= dw;
-              ref = (c_edge_mask[tt[((l[0] + 1) * 9 + (l[1] + 1)) * 9 + (l[2] + 1)]] >>
-                     cube_edge_of_slot(axis, du, dw)) & 1;
-            }
+#pragma unroll
+          for (int j = 0; j < 4; j++) {
+            const int du = j >> 1, dw = j & 1;
+            ref = ref || ((c_edge_mask[tt[p0 - du * su - dw * sw]] >> cube_edge_of_slot(axis, du, dw)) & 1);
+          }
           if (!ref) {
             S.vbirth[(size_t)b * kEV + sl] = -1;
             frees += R.owned;
@@ -882,27 +936,35 @@ __global__ void __launch_bounds__(kGT, 16) k_gc_normals(DevState S, const FrameD
         const int sl = s_vlist[p];
         const int ci = sl / 3, axis = sl - 3 * (sl / 3);
         computed += R.owned;
-        const int c0[3] = {ci >> 6, (ci >> 3) & 7, ci & 7};
-        int c1[3] = {c0[0], c0[1], c0[2]};
-        c1[axis]++;
-        // the 12 stencil points: c0 +- e_d, c1 +- e_d (c0 + e_axis = c1, c1 - e_axis = c0)
+        const int x0 = ci >> 6, y0 = (ci >> 3) & 7, z0 = ci & 7;
+        const int x1 = x0 + (axis == 0), y1 = y0 + (axis == 1), z1 = z0 + (axis == 2);
+        // the 12 stencil points: c0 +- e_d, c1 +- e_d (c0 + e_axis = c1, c1 - e_axis = c0);
+        // all 24 loads are issued before any is used (absent neighbours read a
+        // dummy in-bounds sample and are masked out)
         double v0p[3], v0m[3], v1p[3], v1m[3];
-        bool valid = true;
+        int w0p[3], w0m[3], w1p[3], w1m[3];
+        bool inb = true;
+        const size_t dummy = (size_t)b * kNC;
 #pragma unroll
         for (int d = 0; d < 3; d++) {
           const int dx = d == 0, dy = d == 1, dz = d == 2;
-          const size_t a = sample_index(R.nbr, c0[0] + dx, c0[1] + dy, c0[2] + dz);
-          const size_t bq = sample_index(R.nbr, c0[0] - dx, c0[1] - dy, c0[2] - dz);
-          const size_t cq = sample_index(R.nbr, c1[0] + dx, c1[1] + dy, c1[2] + dz);
-          const size_t dq = sample_index(R.nbr, c1[0] - dx, c1[1] - dy, c1[2] - dz);
-          v0p[d] = a != ~(size_t)0 ? S.tsdf[a] : 0.0;
-          v0m[d] = bq != ~(size_t)0 ? S.tsdf[bq] : 0.0;
-          v1p[d] = cq != ~(size_t)0 ? S.tsdf[cq] : 0.0;
-          v1m[d] = dq != ~(size_t)0 ? S.tsdf[dq] : 0.0;
-          valid = valid && a != ~(size_t)0 && S.weight[a] > 0 && bq != ~(size_t)0 && S.weight[bq] > 0 &&
-                  cq != ~(size_t)0 && S.weight[cq] > 0 && dq != ~(size_t)0 && S.weight[dq] > 0;
+          size_t a = sample_index(R.nbr, x0 + dx, y0 + dy, z0 + dz);
+          size_t bq = sample_index(R.nbr, x0 - dx, y0 - dy, z0 - dz);
+          size_t cq = sample_index(R.nbr, x1 + dx, y1 + dy, z1 + dz);
+          size_t dq = sample_index(R.nbr, x1 - dx, y1 - dy, z1 - dz);
+          inb = inb && a != ~(size_t)0 && bq != ~(size_t)0 && cq != ~(size_t)0 && dq != ~(size_t)0;
+          a = a == ~(size_t)0 ? dummy : a;
+          bq = bq == ~(size_t)0 ? dummy : bq;
+          cq = cq == ~(size_t)0 ? dummy : cq;
+          dq = dq == ~(size_t)0 ? dummy : dq;
+          v0p[d] = S.tsdf[a]; v0m[d] = S.tsdf[bq]; v1p[d] = S.tsdf[cq]; v1m[d] = S.tsdf[dq];
+          w0p[d] = S.weight[a]; w0m[d] = S.weight[bq]; w1p[d] = S.weight[cq]; w1m[d] = S.weight[dq];
         }
-        const double d0 = v1m[axis], d1 = v0p[axis];   // samples at c0 and c1
+        bool valid = inb;   // (an invalid stencil's gradient is never used)
+#pragma unroll
+        for (int d = 0; d < 3; d++) valid = valid && w0p[d] > 0 && w0m[d] > 0 && w1p[d] > 0 && w1m[d] > 0;
+        const double d0 = axis == 0 ? v1m[0] : axis == 1 ? v1m[1] : v1m[2];   // samples at c0 and c1
+        const double d1 = axis == 0 ? v0p[0] : axis == 1 ? v0p[1] : v0p[2];
         const double denom = d0 - d1;
         const double param = (denom != 0) ? d0 / denom : 0.5;
         double g[3];
