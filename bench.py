@@ -64,8 +64,7 @@ def phase_bytes(ds: dict, h: int, w: int) -> dict:
         "retype_place": scope * (729 * SAMPLE + 512 + 1024) + ds["edge_placements"] * (4 + 8)
         + ds["new_vertices"] * 24,
         "gc_normals": halo * (1536 * SLOT_SCAN + 729) + ds["normals_computed"] * (12 * SAMPLE + 24)
-        + ds["vertices_freed"] * 4,
-        "fallback": ds["fallback_normals"] * (27 * 4 + 4 + 20 * 3 * 8 + 24),
+        + ds["vertices_freed"] * 4 + ds["fallback_normals"] * (27 * 4 + 4 + 20 * 3 * 8 + 24),
     }
 
 

@@ -163,10 +163,13 @@ int vm_destroy(vm_engine *e);
 int vm_set_stream(vm_engine *e, void *cuda_stream);
 /* Record CUDA events between the frame's kernels (per-phase device times). */
 int vm_set_profiling(vm_engine *e, int on);
-/* Per-phase device times (ms) of the last frame: depth_stats, collect,
- * init_blocks, integrate, scope_halo, retype, place, tri_release, tri_alloc,
- * gc, normals, fallback (n <= 12). Requires vm_set_profiling(e, 1). */
+/* Per-kernel device times (ms) of the last frame: depth_stats, collect,
+ * fuse_blocks, retype_place, gc_normals (n <= 5). Requires vm_set_profiling(e, 1). */
 int vm_phase_times(vm_engine *e, double *ms, int n);
+/* Diagnostics: per-CTA phase timestamps (%globaltimer, ns) of the frame
+ * kernels into a caller-owned DEVICE buffer of u64[4 * 2048 * 32] (layout in
+ * csrc/vm_device.cuh, kTraceCtas); NULL switches tracing off. */
+int vm_set_trace(vm_engine *e, void *device_buffer);
 /* Guarantee arena capacity (blocks/vertices/triangles) without growth later. */
 int vm_reserve(vm_engine *e, int64_t blocks, int64_t vertices, int64_t triangles);
 

@@ -16,6 +16,13 @@ from .errors import CapacityError, ConsistencyError, InputError
 PKG = Path(__file__).resolve().parent
 LIB_PATH = PKG / "libvoxmesh_b200.so"
 
+
+def lib_path() -> Path:
+    """The product library, or the VOXMESH_B200_LIB override (the tracing build
+    of tools/trace_frame.py), read when the library is first loaded."""
+    env = os.environ.get("VOXMESH_B200_LIB")
+    return Path(env) if env else LIB_PATH
+
 VM_OK, VM_ERR_CAPACITY, VM_ERR_CONSISTENCY, VM_ERR_VALUE, VM_ERR_CUDA, VM_ERR_INPUT = range(6)
 STRATEGY_CODES = {"serial": 0, "claim": 1, "partition": 2}
 
@@ -85,6 +92,7 @@ _SIGS = {
     "vm_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
     "vm_set_profiling": (C.c_int, [C.c_void_p, C.c_int]),
     "vm_phase_times": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
+    "vm_set_trace": (C.c_int, [C.c_void_p, C.c_void_p]),
     "vm_reserve": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int64]),
     "vm_fuse_frame": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                                 C.POINTER(Intr), C.POINTER(PoseC), C.POINTER(FrameConfig),
@@ -132,11 +140,12 @@ def load():
     """Load the CUDA library (raises if it has not been built)."""
     global _lib
     if _lib is None:
-        if not LIB_PATH.exists():
+        path = lib_path()
+        if not path.exists():
             raise RuntimeError(
-                f"{LIB_PATH.name} not built: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                f"{path.name} not built: run `python -c 'import __graft_entry__ as g; g.build()'` "
                 "(there is no CPU fallback)")
-        L = C.CDLL(str(LIB_PATH))
+        L = C.CDLL(str(path))
         for name, (res, args) in _SIGS.items():
             fn = getattr(L, name)
             fn.restype = res

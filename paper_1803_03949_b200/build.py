@@ -25,16 +25,22 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and OUT.exists() and all(OUT.stat().st_mtime >= d.stat().st_mtime for d in DEPS):
-        return OUT
-    tmp = OUT.with_suffix(".so.tmp")
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", str(tmp), str(SRC)]
+TRACE_OUT = PKG / "libvoxmesh_b200_trace.so"
+
+
+def build(force: bool = False, verbose: bool = False, trace: bool = False) -> Path:
+    """The product library; trace=True builds the diagnostics variant with the
+    per-CTA phase timestamps compiled in (-DVM_TRACE, vm_set_trace)."""
+    out = TRACE_OUT if trace else OUT
+    if not force and out.exists() and all(out.stat().st_mtime >= d.stat().st_mtime for d in DEPS):
+        return out
+    tmp = out.with_suffix(".so.tmp")
+    cmd = [nvcc(), *NVCC_FLAGS, *(["-DVM_TRACE"] if trace else []), "-o", str(tmp), str(SRC)]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":

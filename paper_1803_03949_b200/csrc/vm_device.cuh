@@ -62,7 +62,8 @@ struct Counters {
   int32_t nexplicit;
   int32_t nitems_live;
   int32_t done_gc;
-  int32_t nfallback;
+  int32_t nfallback;     // face-normal fallback entries reserved this call
+  int32_t gc_bar;        // k_gc_normals grid barrier arrivals
   int64_t v_allocs;
   int64_t v_frees;
   int64_t placements;
@@ -92,6 +93,8 @@ struct FrameDev {
   int32_t frame;        // frame index (vertex birth)
   int32_t scope_mode;   // 0: collected + slabs (device scope); 1: explicit items
   int32_t nsteps_fixed; // > 0: band step count fixed by the intrinsics (k_depth_stats skipped)
+  int32_t bar_stamp;    // unique per k_gc_normals launch (grid-barrier release value)
+  int32_t pad2;
 };
 
 // one hash slot: packed coordinate (-1 empty) and block index (-1 while the
@@ -104,8 +107,10 @@ struct alignas(16) HashSlot {
 
 struct DevState {
   double cube_size, extent;
+  double inv_extent;    // RN(1 / extent): division-free floor with an exact fallback
+  const double *rays;   // (u - cx) / fx for u < w, then (v - cy) / fy for v < h (fusion.py:29-33)
   long long table_size;
-  long long ts_mask;    // table_size-1 if a power of two, else 0
+  unsigned bmask;       // nbuckets-1 if a power of two, else 0
   int32_t nbuckets;
   int32_t max_blocks;   // reference load-factor limit: 2*n < table_size
   HashSlot *slots;      // [nbuckets*8] (packed coord, block index); a bucket = one 128-B line
@@ -132,17 +137,50 @@ struct DevState {
   int32_t *weight;      // [cap*512]
   uint8_t *tp, *tc;     // [cap*512]
   int32_t *vbirth;      // [cap*1536] slot occupancy: birth frame, -1 empty
+  uint32_t *vocc;       // [cap*48] the same occupancy as bits (claimed with atomicOr; read by GC)
   double *vparam;       // [cap*1536] vertex coordinate along the edge axis
   double *vnrm;         // [cap*1536*3]
   uint32_t *item_mask;  // [cap*16] explicit scope cube masks
-  int2 *fallback;       // [cap*1536] face-normal fallback worklist (block, slot)
+  int4 *fallback;       // [cap*1536] fallback worklist: block, slot, 4 cube types, candidate mask
+  int32_t *bar_flags;   // [32 * 32] grid-barrier release flags (one line each), epoch-stamped
   long long max_vertices;
   // spatial partition: blocks are owned by hashed tiles
   // of 2^tile_shift blocks per axis; a rank also computes a 1-block margin
   int32_t rank, nranks, tile_shift;
   uint8_t *bowned;      // [max_blocks] block owned by this rank
   Counters *ctr;
+  unsigned long long *trace;   // per-CTA phase timestamps (vm_set_trace), null = off
 };
+
+// ---------------------------------------------------------------- tracing
+// Diagnostics only: with a trace buffer set, thread 0 of CTA c < kTraceCtas of
+// kernel k stores %globaltimer at phase p to trace[(k * kTraceCtas + c) * kTraceSlots + p].
+// Slots: 0 start, 1 prologue done, 2 + 4 * item + {0 item start, 1 resolved,
+// 2 staged, 3 computed} for the first 6 items, 27 items processed (a count),
+// 28 item loop done, 29 / 30 kernel-specific, 31 end.
+constexpr int kTraceCtas = 2048, kTraceSlots = 32;
+enum { TK_COLLECT = 0, TK_FUSE = 1, TK_RETYPE = 2, TK_GC = 3, TK_COUNT = 4 };
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#ifdef VM_TRACE   // diagnostics build only (build(trace=True)); the product build has no trace code
+__device__ __forceinline__ void trace_at(const DevState &S, int k, int slot) {
+  if (S.trace && threadIdx.x == 0 && blockIdx.x < kTraceCtas)
+    S.trace[((size_t)k * kTraceCtas + blockIdx.x) * kTraceSlots + slot] = gtimer();
+}
+__device__ __forceinline__ void trace_count(const DevState &S, int k, int n) {
+  if (S.trace && threadIdx.x == 0 && blockIdx.x < kTraceCtas)
+    S.trace[((size_t)k * kTraceCtas + blockIdx.x) * kTraceSlots + 27] = (unsigned long long)n;
+}
+#else
+__device__ __forceinline__ void trace_at(const DevState &, int, int) {}
+__device__ __forceinline__ void trace_count(const DevState &, int, int) {}
+#endif
+__device__ __forceinline__ void trace_item(const DevState &S, int k, int nth, int phase) {
+  if (nth < 6) trace_at(S, k, 2 + 4 * nth + phase);
+}
 
 // ---------------------------------------------------------------- tables
 __constant__ uint16_t c_edge_mask[256] = VM_EDGE_MASK_INIT;
@@ -161,6 +199,10 @@ __constant__ int8_t c_edge_of[3][8] = {{0, -1, 2, -1, 4, -1, 6, -1},
                                        {3, 1, -1, -1, 7, 5, -1, -1},
                                        {8, 9, 11, 10, -1, -1, -1, -1}};
 __constant__ uint8_t c_regular[6] = {0x99, 0x66, 0x33, 0xCC, 0x0F, 0xF0};
+// global-memory copies, staged into shared memory by the meshing kernels
+// (coalesced loads; constant-bank reads with per-thread indices serialise)
+__device__ const uint16_t g_edge_mask[256] = VM_EDGE_MASK_INIT;
+__device__ const uint8_t g_tri_count[256] = VM_TRI_COUNT_INIT;
 __constant__ uint8_t c_slab_sel[8];
 
 __host__ __device__ inline bool is_regular_type(unsigned t) {
@@ -172,12 +214,17 @@ __device__ __forceinline__ long long pack_coord(int x, int y, int z) {
   const long long off = 1LL << 20;
   return ((((long long)x + off) << 42) | (((long long)y + off) << 21) | ((long long)z + off));
 }
-// store.py:84-87 (Python floor-mod of the xor of prime products)
-__device__ __forceinline__ long long hash_block(const DevState &S, int x, int y, int z) {
-  long long h = ((long long)x * 73856093LL) ^ ((long long)y * 19349669LL) ^ ((long long)z * 83492791LL);
-  if (S.ts_mask) return h & S.ts_mask;
-  long long m = h % S.table_size;
-  return m < 0 ? m + S.table_size : m;
+// Bucket of a packed block coordinate.  Where a block sits in the table is
+// not observable (the reference's contract is one allocation per coordinate
+// and CapacityError at 2n >= table_size, store.py:296-320), so the bucket uses
+// a full 64-bit mix rather than the reference's xor-of-primes slot hash
+// (store.py:84-87), which clusters spatially coherent keys into shared buckets.
+__device__ __forceinline__ unsigned bucket_of(const DevState &S, long long key) {
+  unsigned long long h = (unsigned long long)key;
+  h ^= h >> 33; h *= 0xff51afd7ed558ccdULL;
+  h ^= h >> 33; h *= 0xc4ceb9fe1a85ec53ULL;
+  h ^= h >> 33;
+  return S.bmask ? (unsigned)h & S.bmask : (unsigned)(h % (unsigned long long)S.nbuckets);
 }
 
 template <typename T>
@@ -214,18 +261,26 @@ struct HashRef {
 // (key, index, stamp), so a probe is a single round trip in the common case
 __device__ HashRef hash_find_ref(const DevState &S, int x, int y, int z) {
   const long long key = pack_coord(x, y, z);
-  const unsigned b = (unsigned)(hash_block(S, x, y, z) >> 3);
+  const unsigned b = bucket_of(S, key);
   HashSlot *kb = S.slots + (size_t)b * kSlotsPerBucket;
+  int4 v[kSlotsPerBucket];   // the whole 128-B bucket in one round trip
+#pragma unroll
+  for (int i = 0; i < kSlotsPerBucket; i++) v[i] = __ldcg(reinterpret_cast<const int4 *>(kb + i));
+  // first slot holding the key or empty (slots fill in prefix order), with
+  // register selects only (no dynamically indexed local array)
+  int hit = -1, idx = -1, stamp = -1;
+  bool stop = false;
 #pragma unroll
   for (int i = 0; i < kSlotsPerBucket; i++) {
-    const int4 v = __ldcg(reinterpret_cast<const int4 *>(kb + i));
-    const long long k = (long long)(((unsigned long long)(unsigned)v.y << 32) | (unsigned)v.x);
-    if (k == key) {
-      const int idx = v.z != -1 ? v.z : wait_val(&kb[i].val);
-      return {idx, v.w, &kb[i].pad};
-    }
-    if (k == kEmptyKey) return {-1, -1, nullptr};   // slots fill in prefix order
+    const long long k = (long long)(((unsigned long long)(unsigned)v[i].y << 32) | (unsigned)v[i].x);
+    if (!stop && k == key) { hit = i; idx = v[i].z; stamp = v[i].w; }
+    stop = stop || k == key || k == kEmptyKey;
   }
+  if (hit >= 0) {
+    if (idx == -1) idx = wait_val(&kb[hit].val);
+    return {idx, stamp, &kb[hit].pad};
+  }
+  if (stop) return {-1, -1, nullptr};
   for (int e = ld_vol(S.ovf_head + b); e >= 0; e = ld_vol(S.ovf_next + e))
     if (ld_vol(S.ovf_key + e) == key) return {ld_vol(S.ovf_val + e), ld_vol(S.ovf_stamp + e), S.ovf_stamp + e};
   return {-1, -1, nullptr};
@@ -234,7 +289,7 @@ __device__ HashRef hash_find_ref(const DevState &S, int x, int y, int z) {
 // SpatialStore.get_block (store.py:280-294)
 __device__ int hash_find(const DevState &S, int x, int y, int z) {
   const long long key = pack_coord(x, y, z);
-  const unsigned b = (unsigned)(hash_block(S, x, y, z) >> 3);
+  const unsigned b = bucket_of(S, key);
   const HashSlot *kb = S.slots + (size_t)b * kSlotsPerBucket;
 #pragma unroll
   for (int i = 0; i < kSlotsPerBucket; i++) {
@@ -298,7 +353,7 @@ __device__ int hash_insert(const DevState &S, int x, int y, int z, int epoch) {
 }
 __device__ HashRef hash_insert_ref(const DevState &S, int x, int y, int z, int epoch) {
   const long long key = pack_coord(x, y, z);
-  const unsigned b = (unsigned)(hash_block(S, x, y, z) >> 3);
+  const unsigned b = bucket_of(S, key);
   HashSlot *kb = S.slots + (size_t)b * kSlotsPerBucket;
   for (int i = 0; i < kSlotsPerBucket; i++) {
     long long k = ld_vol(&kb[i].key);
@@ -351,6 +406,18 @@ __device__ HashRef hash_insert_ref(const DevState &S, int x, int y, int z, int e
 // ---------------------------------------------------------------- misc
 __device__ __forceinline__ int nbr_dir(int dx, int dy, int dz) {
   return (dx + 1) * 9 + (dy + 1) * 3 + (dz + 1);
+}
+
+// floor(p / e) exactly as the correctly rounded division, without dividing in
+// the common case: q = RN(p * RN(1/e)) is within ~2.2e-16 |p/e| of p/e (and of
+// RN(p/e)), so unless q lies within 1e-7 of an integer (|p/e| < 2^21 here) both
+// floor to the same value; near an integer the exact quotient decides.
+__device__ __forceinline__ int floor_div_exact(double p, double e, double inv_e) {
+  const double q = __dmul_rn(p, inv_e);
+  const double f = floor(q);
+  const double r = q - f;   // exact
+  if (r > 1e-7 && r < 1.0 - 1e-7) return (int)f;
+  return (int)floor(p / e);
 }
 
 // out_j = fma(a2, B[2][j], fma(a1, B[1][j], a0*B[0][j])) -- numpy `a @ B`
@@ -430,18 +497,18 @@ __device__ __forceinline__ long long block_sum(long long v, long long *sh) {
   return r;
 }
 
-// Block-wide sums of N counters in one pass (one barrier pair), then one
-// atomicAdd per counter: thread k < N adds vals[k] to dst[k] (null = skip).
-// `sh` must hold 32 * N entries.
+// Block-wide sums of N per-thread counters (each < 2^31 per CTA): one
+// redux.sync per counter and warp, one barrier pair, then one atomicAdd per
+// counter (thread k adds counter k to dst[k]; null = skip).  `sh` holds 32 * N.
 template <int N>
-__device__ __forceinline__ void block_add_counters(long long (&vals)[N], long long *sh, int64_t *const (&dst)[N]) {
+__device__ __forceinline__ void block_add_counters(int (&vals)[N], int *sh, int64_t *const (&dst)[N]) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-#pragma unroll
-  for (int k = 0; k < N; k++) vals[k] = warp_sum(vals[k]);
   __syncthreads();
-  if (lane == 0)
 #pragma unroll
-    for (int k = 0; k < N; k++) sh[k * 32 + wid] = vals[k];
+  for (int k = 0; k < N; k++) {
+    const unsigned v = __reduce_add_sync(0xffffffffu, (unsigned)vals[k]);
+    if (lane == 0) sh[k * 32 + wid] = (int)v;
+  }
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < N; k++)   // static indices: dst stays in registers

@@ -49,7 +49,7 @@ static int set_err(int code, const char *fmt, ...) {
     if (_r != VM_OK) return _r; \
   } while (0)
 
-enum Phase { PH_DEPTH = 0, PH_COLLECT, PH_FUSE, PH_RETYPE, PH_GC, PH_FALLBACK, PH_END, PH_COUNT };
+enum Phase { PH_DEPTH = 0, PH_COLLECT, PH_FUSE, PH_RETYPE, PH_GC, PH_END, PH_COUNT };
 
 struct Compacted {
   double *pos = nullptr, *nrm = nullptr;
@@ -70,7 +70,7 @@ struct vm_engine {
   bool own_stream = false;
   int32_t epoch = 0;
   int sm_count = 148;
-  int grid_retype = 296, grid_gc = 296, grid_fuse = 296;
+  int grid_retype = 296, grid_gc = 296, grid_fuse = 296, grid_collect = 296;
   void *d_scratch = nullptr;
   size_t scratch_cap = 0;
   Compacted comp;
@@ -79,11 +79,14 @@ struct vm_engine {
   int pending = 0;
   int64_t pending_frame = 0;
   int last_resumes = 0;
+  int32_t bar_seq = 0;     // k_gc_normals grid-barrier stamps
   int frame_launches = 0;   // kernels launched by the pending / last frame
   // ray-norm bounds over the image, cached per (h, w, fx, fy, cx, cy)
   double norm_key[6] = {0, 0, 0, 0, 0, 0};
   double norm_lo = 0.0, norm_hi = 0.0;
   bool norm_valid = false;
+  double *d_rays = nullptr;   // ray tables of the cached intrinsics (k_norm_bounds)
+  size_t rays_cap = 0;
 };
 
 // ------------------------------------------------------------ helpers
@@ -153,6 +156,37 @@ static void launch_pdl(void (*kern)(KArgs...), int grid, int block, cudaStream_t
   cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
+// k_gc_normals holds a grid barrier before its fallback phase, so it is always
+// launched cooperatively (every CTA co-resident, or the launch fails), with
+// programmatic dependent launch where the driver accepts the combination.
+template <typename... KArgs, typename... Args>
+static void launch_coop(bool pdl, void (*kern)(KArgs...), int grid, int block, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 2 : 1;
+  if (cudaLaunchKernelEx(&cfg, kern, args...) != cudaSuccess && pdl) {
+    cudaGetLastError();
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, args...);
+  }
+}
+
+// k_gc_normals with a fresh grid-barrier stamp
+static void launch_gc(vm_engine *e, bool pdl, const int32_t *list, const int32_t *count_ptr, int count_const,
+                      int mode) {
+  e->h_frame->bar_stamp = ++e->bar_seq;
+  launch_coop(pdl, k_gc_normals, e->grid_gc, kGT, e->stream, e->S, *e->h_frame, list, count_ptr, count_const, mode);
+}
+
 static int check_launch() {
   const cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return set_err(VM_ERR_CUDA, "kernel launch failed: %s", cudaGetErrorString(err));
@@ -172,6 +206,7 @@ static int grow_blocks(vm_engine *e, int64_t need) {
   TRY(dev_grow(&S.tp, o * kNC, n * kNC, st));
   TRY(dev_grow(&S.tc, o * kNC, n * kNC, st));
   TRY(dev_grow(&S.vbirth, o * kEV, n * kEV, st));
+  TRY(dev_grow(&S.vocc, o * (kEV / 32), n * (kEV / 32), st));
   TRY(dev_grow(&S.vparam, o * kEV, n * kEV, st));
   TRY(dev_grow(&S.vnrm, o * kEV * 3, n * kEV * 3, st));
   TRY(dev_grow(&S.item_mask, 0, n * 16, st));
@@ -230,10 +265,7 @@ static int enqueue_after_collect(vm_engine *e) {
   rec(e, PH_RETYPE);
   launch_pdl(k_retype_place, e->grid_retype, kNT, st, S, F);
   rec(e, PH_GC);
-  launch_pdl(k_gc_normals, e->grid_gc, kGT, st, S, F, (const int32_t *)S.halo, (const int32_t *)&S.ctr->nhalo,
-             0, (int)(G_GC | G_NORMALS | G_COMMIT | G_REQUIRE_ITEMS));
-  rec(e, PH_FALLBACK);
-  launch_pdl(k_fallback, e->sm_count * 4, kFT, st, S, F);
+  launch_gc(e, true, S.halo, &S.ctr->nhalo, 0, (int)(G_GC | G_NORMALS | G_COMMIT | G_REQUIRE_ITEMS));
   rec(e, PH_END);
   return check_launch();
 }
@@ -248,7 +280,7 @@ static int complete_with_resume(vm_engine *e, int *resumes) {
     CK(cudaMemsetAsync(&e->S.ctr->need, 0, sizeof(int32_t), e->stream));
     if (resumes) (*resumes)++;
     TRY(enqueue_after_collect(e));
-    e->frame_launches += 4;
+    e->frame_launches += 3;
   }
   return set_err(VM_ERR_CUDA, "resume loop did not converge");
 }
@@ -396,40 +428,6 @@ static int run_compaction(vm_engine *e, int64_t frame, bool with_handles) {
   return error_from_counters(e);
 }
 
-// tile-source tables of the staged loaders (vm_kernels.cuh g_*_tab)
-static int upload_tile_tables() {
-  uint32_t ext[217];
-  for (int t = 0; t < 217; t++) {
-    int x, y, z;
-    if (t < 64) { x = 8; y = t >> 3; z = t & 7; }
-    else if (t < 128) { x = (t - 64) >> 3; y = 8; z = t & 7; }
-    else if (t < 192) { x = (t - 128) >> 3; y = t & 7; z = 8; }
-    else if (t < 200) { x = 8; y = 8; z = t - 192; }
-    else if (t < 208) { x = 8; y = t - 200; z = 8; }
-    else if (t < 216) { x = t - 208; y = 8; z = 8; }
-    else { x = 8; y = 8; z = 8; }
-    const uint32_t p = (x * 9 + y) * 9 + z;
-    const uint32_t dir = ((x >> 3) + 1) * 9 + ((y >> 3) + 1) * 3 + ((z >> 3) + 1);
-    const uint32_t src = (x & 7) * 64 + (y & 7) * 8 + (z & 7);
-    ext[t] = p | dir << 10 | src << 15;
-  }
-  auto dir_of = [](int l) { return l < 0 ? -1 : (l >> 3); };
-  uint16_t sten[1331], typ[729];
-  for (int q = 0; q < 1331; q++) {
-    const int lx = q / 121 - 1, ly = (q / 11) % 11 - 1, lz = q % 11 - 1;
-    const int dir = (dir_of(lx) + 1) * 9 + (dir_of(ly) + 1) * 3 + (dir_of(lz) + 1);
-    sten[q] = (uint16_t)(dir << 9 | ((lx & 7) * 64 + (ly & 7) * 8 + (lz & 7)));
-  }
-  for (int q = 0; q < 729; q++) {
-    const int X = q / 81 - 1, Y = (q / 9) % 9 - 1, Z = q % 9 - 1;
-    const int dir = (dir_of(X) + 1) * 9 + (dir_of(Y) + 1) * 3 + (dir_of(Z) + 1);
-    typ[q] = (uint16_t)(dir << 9 | ((X & 7) * 64 + (Y & 7) * 8 + (Z & 7)));
-  }
-  CK(cudaMemcpyToSymbol(g_ext_tab, ext, sizeof ext));
-  CK(cudaMemcpyToSymbol(g_sten_tab, sten, sizeof sten));
-  CK(cudaMemcpyToSymbol(g_type_tab, typ, sizeof typ));
-  return VM_OK;
-}
 
 // ------------------------------------------------------------ C ABI
 extern "C" {
@@ -457,9 +455,10 @@ int vm_create(const vm_store_config *cfg, vm_engine **out) {
   DevState &S = e->S;
   S.cube_size = cfg->cube_size;
   S.extent = cfg->cube_size * kB;
+  S.inv_extent = 1.0 / S.extent;
   S.table_size = cfg->table_size;
-  S.ts_mask = ((cfg->table_size & (cfg->table_size - 1)) == 0) ? cfg->table_size - 1 : 0;
   S.nbuckets = (int32_t)((cfg->table_size + kSlotsPerBucket - 1) / kSlotsPerBucket);
+  S.bmask = (S.nbuckets & (S.nbuckets - 1)) == 0 ? (unsigned)S.nbuckets - 1 : 0u;
   S.max_blocks = (int32_t)((cfg->table_size + 1) / 2);
   S.max_vertices = cfg->max_vertices;
   S.rank = cfg->nranks > 1 ? cfg->rank : 0;
@@ -491,6 +490,7 @@ int vm_create(const vm_store_config *cfg, vm_engine **out) {
   TRY(dev_alloc(&S.newlist, mb));
   TRY(dev_alloc(&S.halo, mb));
   TRY(dev_alloc(&S.ctr, 1, 0));
+  TRY(dev_alloc(&S.bar_flags, 32 * 32, 0));
   uint8_t slab_sel[8];   // mesher.py:518-525
   for (int m = 0; m < 8; m++) {
     uint8_t bits = 0;
@@ -499,7 +499,6 @@ int vm_create(const vm_store_config *cfg, vm_engine **out) {
     slab_sel[m] = bits;
   }
   CK(cudaMemcpyToSymbol(c_slab_sel, slab_sel, sizeof slab_sel));
-  TRY(upload_tile_tables());
   {
     // persistent grids: exactly the number of co-resident CTAs
     int occ = 0;
@@ -509,6 +508,8 @@ int vm_create(const vm_store_config *cfg, vm_engine **out) {
     e->grid_gc = std::max(1, occ) * e->sm_count;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fuse_blocks, kFB, 0));
     e->grid_fuse = std::max(1, occ) * e->sm_count;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_collect, kCollectThreads, 0));
+    e->grid_collect = std::max(1, occ) * e->sm_count;
   }
   S.block_cap = 0;
   const int64_t ib = cfg->initial_blocks > 0 ? cfg->initial_blocks : 1024;
@@ -524,7 +525,7 @@ int vm_destroy(vm_engine *e) {
   DevState &S = e->S;
   void *ptrs[] = {S.slots, S.ovf_head, S.ovf_lock, S.ovf_key, S.ovf_val, S.ovf_next, S.ovf_stamp, S.bcoord,
                   S.nbr, S.stamp_collect, S.stamp_halo, S.stamp_new, S.bowned, S.slab_bits, S.scope, S.newlist,
-                  S.halo, S.tsdf, S.weight, S.tp, S.tc, S.vbirth, S.vparam, S.vnrm, S.item_mask, S.fallback,
+                  S.halo, S.tsdf, S.weight, S.tp, S.tc, S.vbirth, S.vocc, S.vparam, S.vnrm, S.item_mask, S.fallback, S.bar_flags, e->d_rays,
                   S.ctr, e->d_depth, e->d_scratch};
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -549,6 +550,12 @@ int vm_set_stream(vm_engine *e, void *stream) {
     CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
     e->own_stream = true;
   }
+  return VM_OK;
+}
+
+int vm_set_trace(vm_engine *e, void *device_buffer) {
+  if (!e) return set_err(VM_ERR_INPUT, "null engine");
+  e->S.trace = (unsigned long long *)device_buffer;
   return VM_OK;
 }
 
@@ -627,27 +634,42 @@ static int nsteps_for(double maxnorm, double trunc, double extent) {
   return n < 2 ? 2 : n;
 }
 
+// Per-intrinsics state, recomputed when (h, w, fx, fy, cx, cy) change: the ray
+// tables the pixel passes read, and the min / max ray norm over the image.
+static int ensure_rays(vm_engine *e, int32_t h, int32_t w) {
+  FrameDev &F = *e->h_frame;
+  const double key[6] = {(double)h, (double)w, F.fx, F.fy, F.cx, F.cy};
+  if (e->norm_valid && memcmp(key, e->norm_key, sizeof key) == 0) {
+    e->S.rays = e->d_rays;
+    return VM_OK;
+  }
+  const size_t need = (size_t)(h + w) * sizeof(double);
+  if (need > e->rays_cap) {
+    if (e->d_rays) CK(cudaFree(e->d_rays));
+    CK(cudaMalloc((void **)&e->d_rays, need));
+    e->rays_cap = need;
+  }
+  unsigned long long *d;
+  TRY(scratch(e, 2 * sizeof(unsigned long long), (void **)&d));
+  const unsigned long long init[2] = {~0ull, 0ull};
+  unsigned long long res[2];
+  CK(cudaMemcpyAsync(d, init, sizeof init, cudaMemcpyHostToDevice, e->stream));
+  k_norm_bounds<<<grid_threads(e, (long long)h * w, 256), 256, 0, e->stream>>>(F, d, e->d_rays);
+  CK(cudaMemcpyAsync(res, d, sizeof res, cudaMemcpyDeviceToHost, e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+  memcpy(&e->norm_lo, &res[0], sizeof(double));
+  memcpy(&e->norm_hi, &res[1], sizeof(double));
+  memcpy(e->norm_key, key, sizeof key);
+  e->norm_valid = true;
+  e->S.rays = e->d_rays;
+  return VM_OK;
+}
+
 // The step count is a monotone function of the max norm over the valid pixels,
 // which lies within [min, max] of the norm over the whole image: when both
 // bounds give the same count, the frame's count is known without reading the
 // depth and k_depth_stats is skipped.  Returns 0 when it is data dependent.
-static int fixed_nsteps(vm_engine *e, int32_t h, int32_t w, double trunc) {
-  FrameDev &F = *e->h_frame;
-  const double key[6] = {(double)h, (double)w, F.fx, F.fy, F.cx, F.cy};
-  if (!e->norm_valid || memcmp(key, e->norm_key, sizeof key) != 0) {
-    unsigned long long *d;
-    if (scratch(e, 2 * sizeof(unsigned long long), (void **)&d) != VM_OK) return 0;
-    const unsigned long long init[2] = {~0ull, 0ull};
-    unsigned long long res[2];
-    if (cudaMemcpyAsync(d, init, sizeof init, cudaMemcpyHostToDevice, e->stream) != cudaSuccess) return 0;
-    k_norm_bounds<<<grid_threads(e, (long long)h * w, 256), 256, 0, e->stream>>>(F, d);
-    if (cudaMemcpyAsync(res, d, sizeof res, cudaMemcpyDeviceToHost, e->stream) != cudaSuccess) return 0;
-    if (cudaStreamSynchronize(e->stream) != cudaSuccess) return 0;
-    memcpy(&e->norm_lo, &res[0], sizeof(double));
-    memcpy(&e->norm_hi, &res[1], sizeof(double));
-    memcpy(e->norm_key, key, sizeof key);
-    e->norm_valid = true;
-  }
+static int fixed_nsteps(vm_engine *e, double trunc) {
   const int lo = nsteps_for(e->norm_lo, trunc, e->S.extent), hi = nsteps_for(e->norm_hi, trunc, e->S.extent);
   return lo == hi ? lo : 0;
 }
@@ -672,17 +694,18 @@ int vm_fuse_frame_enqueue(vm_engine *e, const double *depth, int32_t h, int32_t 
   F.epoch = ++e->epoch;
   F.frame = (int32_t)frame_index;
   F.scope_mode = 0;
-  F.nsteps_fixed = fixed_nsteps(e, h, w, cfg->trunc);
+  TRY(ensure_rays(e, h, w));
+  F.nsteps_fixed = fixed_nsteps(e, cfg->trunc);
   TRY(reset_call_counters(e));
   cudaStream_t st = e->stream;
   rec(e, PH_DEPTH);
-  e->frame_launches = 5;   // collect, fuse, retype, gc, fallback (+ depth stats)
+  e->frame_launches = 4;   // collect, fuse, retype, gc (+ depth stats)
   if (F.nsteps_fixed <= 0) {
     k_depth_stats<<<grid_blocks(e), 256, 0, st>>>(e->S, *e->h_frame);
     e->frame_launches++;
   }
   rec(e, PH_COLLECT);
-  launch_pdl(k_collect, grid_threads(e, (long long)h * w, 256), 256, st, e->S, *e->h_frame);
+  launch_pdl(k_collect, e->grid_collect, kCollectThreads, st, e->S, *e->h_frame);
   TRY(enqueue_after_collect(e));
   CK(cudaMemcpyAsync(e->h_ctr, e->S.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
   e->pending = 1;
@@ -721,9 +744,10 @@ int vm_collect(vm_engine *e, const double *depth, int32_t h, int32_t w, int32_t 
   F.epoch = ++e->epoch;
   F.scope_mode = 0;
   F.nsteps_fixed = 0;   // the phase API always runs the depth reduction
+  TRY(ensure_rays(e, h, w));
   TRY(reset_call_counters(e));
   k_depth_stats<<<grid_blocks(e), 256, 0, e->stream>>>(e->S, *e->h_frame);
-  k_collect<<<grid_threads(e, (long long)h * w, 256), 256, 0, e->stream>>>(e->S, *e->h_frame);
+  k_collect<<<e->grid_collect, kCollectThreads, 0, e->stream>>>(e->S, *e->h_frame);
   TRY(check_launch());
   TRY(init_new_blocks(e));
   if (n_out) *n_out = e->h_ctr->ncollected;
@@ -889,9 +913,7 @@ int vm_extract(vm_engine *e, const int32_t *scope_coords, const uint8_t *scope_m
   }
   const int gb = grid_blocks(e);
   k_retype_place<<<e->grid_retype, kNT, kRetypeSmem, e->stream>>>(e->S, *e->h_frame);
-  k_gc_normals<<<e->grid_gc, kGT, kGcSmem, e->stream>>>(e->S, *e->h_frame, e->S.halo, &e->S.ctr->nhalo, 0,
-                                                  G_GC | G_NORMALS | G_COMMIT | G_REQUIRE_ITEMS);
-  k_fallback<<<e->sm_count * 4, kFT, 0, e->stream>>>(e->S, *e->h_frame);
+  launch_gc(e, false, e->S.halo, &e->S.ctr->nhalo, 0, (int)(G_GC | G_NORMALS | G_COMMIT | G_REQUIRE_ITEMS));
   TRY(check_launch());
   TRY(read_counters(e));
   TRY(error_from_counters(e));
@@ -907,8 +929,7 @@ int vm_garbage_collect(vm_engine *e, const int32_t *coords, int64_t n, int64_t *
   TRY(reset_call_counters(e));
   int32_t *di = nullptr;
   if (n > 0) TRY(map_coords(e, coords, n, &di, nullptr, 0, false));
-  k_gc_normals<<<e->grid_gc, kGT, kGcSmem, e->stream>>>(e->S, *e->h_frame, di, nullptr,
-                                                                (int)std::max<int64_t>(n, 0), G_GC | G_COMMIT);
+  launch_gc(e, false, di, nullptr, (int)std::max<int64_t>(n, 0), (int)(G_GC | G_COMMIT));
   TRY(check_launch());
   TRY(read_counters(e));
   TRY(error_from_counters(e));
@@ -923,8 +944,7 @@ int vm_compute_normals(vm_engine *e, const int32_t *coords, int64_t n) {
   e->h_frame->epoch = ++e->epoch;
   int32_t *di;
   TRY(map_coords(e, coords, n, &di, e->S.stamp_halo, e->epoch, false));
-  k_gc_normals<<<e->grid_gc, kGT, kGcSmem, e->stream>>>(e->S, *e->h_frame, di, nullptr, (int)n, G_NORMALS);
-  k_fallback<<<e->sm_count * 4, kFT, 0, e->stream>>>(e->S, *e->h_frame);
+  launch_gc(e, false, di, nullptr, (int)n, (int)G_NORMALS);
   TRY(check_launch());
   TRY(read_counters(e));
   return error_from_counters(e);
@@ -1216,7 +1236,13 @@ int vm_import_blocks(vm_engine *e, int64_t n, const int32_t *coords, const doubl
     if (weight) TRY(copy_sync(e, S.weight + i * kNC, weight + k * kNC, 4 * kNC, cudaMemcpyHostToDevice));
     if (tp) TRY(copy_sync(e, S.tp + i * kNC, tp + k * kNC, kNC, cudaMemcpyHostToDevice));
     if (tc) TRY(copy_sync(e, S.tc + i * kNC, tc + k * kNC, kNC, cudaMemcpyHostToDevice));
-    if (birth) TRY(copy_sync(e, S.vbirth + i * kEV, birth + k * kEV, 4 * kEV, cudaMemcpyHostToDevice));
+    if (birth) {
+      TRY(copy_sync(e, S.vbirth + i * kEV, birth + k * kEV, 4 * kEV, cudaMemcpyHostToDevice));
+      uint32_t occ[kEV / 32] = {};
+      for (int q = 0; q < kEV; q++)
+        if (birth[k * kEV + q] >= 0) occ[q >> 5] |= 1u << (q & 31);
+      TRY(copy_sync(e, S.vocc + i * (kEV / 32), occ, sizeof occ, cudaMemcpyHostToDevice));
+    }
     if (param) TRY(copy_sync(e, S.vparam + i * kEV, param + k * kEV, 8 * kEV, cudaMemcpyHostToDevice));
     if (normal) TRY(copy_sync(e, S.vnrm + i * kEV * 3, normal + k * kEV * 3, 24 * kEV, cudaMemcpyHostToDevice));
   }

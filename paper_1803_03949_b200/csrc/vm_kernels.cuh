@@ -32,8 +32,58 @@ __device__ __forceinline__ bool halted(const DevState &S) {
   return (v.x | v.y) != 0;
 }
 
-__device__ __forceinline__ int list_count(const int32_t *count_ptr, int count_const) {
-  return count_ptr ? ld_vol(count_ptr) : count_const;
+
+// warp-aggregated append of `cnt` entries to a shared-memory list; returns
+// this lane's first index
+__device__ __forceinline__ int smem_append(int cnt, int *s_count) {
+  const int lane = threadIdx.x & 31;
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += u;
+  }
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  int base = 0;
+  if (lane == 31 && total) base = atomicAdd(s_count, total);
+  base = __shfl_sync(0xffffffffu, base, 31);
+  return base + incl - cnt;
+}
+
+// ------------------------------------------------------------ shared helpers
+// MC tables indexed by a per-thread cube type: from the constant bank every
+// distinct index of a warp is a serialised access, so the meshing kernels copy
+// them to shared memory once per CTA.
+struct __align__(16) SmemTables {
+  uint16_t edge_mask[256];
+  uint8_t tri_count[256];
+};
+__device__ __forceinline__ void load_tables(SmemTables &T) {
+  for (int q = threadIdx.x; q < 128; q += blockDim.x)
+    reinterpret_cast<uint32_t *>(T.edge_mask)[q] = __ldg(reinterpret_cast<const uint32_t *>(g_edge_mask) + q);
+  for (int q = threadIdx.x; q < 64; q += blockDim.x)
+    reinterpret_cast<uint32_t *>(T.tri_count)[q] = __ldg(reinterpret_cast<const uint32_t *>(g_tri_count) + q);
+}
+
+// Per-call counters a kernel needs before its loop, read by ONE thread and
+// broadcast through shared memory (every CTA reading them from every warp
+// serialises thousands of requests on one L2 line).  v[0] = halted, v[1..3]
+// kernel-specific.  Ends with a barrier.
+// (null pointers read as 0).  sv[4] = the CTA's first list entry, prefetched
+// in the same round trip when `first` is non-null, and the MC tables are
+// staged into `T` (if given) meanwhile.
+__device__ __forceinline__ void read_prologue(const DevState &S, int *sv, const int32_t *a, const int32_t *b,
+                                              const int32_t *c, const int32_t *first = nullptr,
+                                              SmemTables *T = nullptr) {
+  if (threadIdx.x == 0) {
+    const int2 h = __ldcg(reinterpret_cast<const int2 *>(&S.ctr->error));
+    const int va = a ? __ldcg(a) : 0, vb = b ? __ldcg(b) : 0, vc = c ? __ldcg(c) : 0;
+    const int vf = first ? __ldcg(first) : -1;
+    sv[0] = (h.x | h.y) != 0;
+    sv[1] = va; sv[2] = vb; sv[3] = vc; sv[4] = vf;
+  }
+  if (T) load_tables(*T);
+  __syncthreads();
 }
 
 // ------------------------------------------------------------ depth stats
@@ -74,8 +124,12 @@ __global__ void __launch_bounds__(256) k_depth_stats(DevState S, const FrameDev 
 // order as their bit patterns).  The band step count is monotone in the max
 // norm over the VALID pixels, which lies between the two, so when both bounds
 // give the same count the frame needs no depth reduction (fusion.py:88-94).
-__global__ void k_norm_bounds(const FrameDev F, unsigned long long *out) {
+// Also fills the per-column / per-row ray tables (fusion.py:29-33: (u - cx) / fx,
+// (v - cy) / fy), so the per-pixel passes do not divide.
+__global__ void k_norm_bounds(const FrameDev F, unsigned long long *out, double *rays) {
   const long long npix = (long long)F.h * F.w;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < F.w + F.h; q += gridDim.x * blockDim.x)
+    rays[q] = q < F.w ? ((double)q - F.cx) / F.fx : ((double)(q - F.w) - F.cy) / F.fy;
   unsigned long long lo = ~0ull, hi = 0;
   for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < npix;
        p += (long long)gridDim.x * blockDim.x) {
@@ -91,13 +145,38 @@ __global__ void k_norm_bounds(const FrameDev F, unsigned long long *out) {
 }
 
 // ------------------------------------------------------------ collect
-// One thread per pixel looping over the nsteps band samples.  Samples of a
-// warp falling in the same block are merged with __match_any_sync, so one
-// lane per distinct block probes the hash table.  A warp covers an 8x4 pixel
-// tile (blocks project to compact image regions, so fewer distinct blocks per
-// warp than a 32-pixel row).
-__global__ void __launch_bounds__(256) k_collect(DevState S, const FrameDev F) {
+// fusion.py:95-106 + store.py:296-320.  A CTA covers a 64x8-pixel region (two
+// pixels per thread, coalesced rows).  The band samples' block keys are first
+// merged inside each warp (__match_any_sync), then in a CTA-local shared-memory
+// set; after one barrier the region's DISTINCT blocks are probed / inserted in
+// the global table in parallel, one thread each -- one hash round trip per
+// block and region instead of one per sample step and warp.
+constexpr int kCollectThreads = 256;
+constexpr int kRegionW = 64, kRegionH = 8;
+constexpr int kCSet = 1024;   // CTA-local key set (open addressing)
+constexpr int kCOver = 512;   // keys that found no free set slot within 32 probes
+constexpr unsigned long long kNoKey = ~0ull;
+
+__device__ __forceinline__ unsigned cset_hash(unsigned long long k) {
+  const unsigned x = (unsigned)(k ^ (k >> 21) ^ (k >> 42));
+  return (x * 2654435761u) >> (32 - 10);
+}
+
+// probe / insert one block; returns its index if this call collects it now
+// (first to stamp it this call), else -1
+__device__ __forceinline__ int collect_block(const DevState &S, const FrameDev &F, int x, int y, int z) {
+  HashRef r = hash_find_ref(S, x, y, z);
+  if (r.idx == -1) r = hash_insert_ref(S, x, y, z, F.epoch);
+  if (r.idx >= 0 && r.stamp != F.epoch && atomicExch(r.stamp_ptr, F.epoch) != F.epoch) {
+    S.stamp_collect[r.idx] = F.epoch;
+    return r.idx;
+  }
+  return -1;
+}
+
+__global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, const FrameDev F) {
   cudaGridDependencySynchronize();   // PDL: wait for the previous kernel of the frame
+  trace_at(S, TK_COLLECT, 0);
   Counters *ctr = S.ctr;
   int nsteps = F.nsteps_fixed;
   if (nsteps <= 0) {
@@ -109,59 +188,105 @@ __global__ void __launch_bounds__(256) k_collect(DevState S, const FrameDev F) {
     if (nsteps < 2) nsteps = 2;
   }
   const double step = 2.0 / (double)(nsteps - 1);
-  const int lane = threadIdx.x & 31;
-  // warp tiles of 8x4 pixels, row-major over the tile grid
-  const int tiles_x = (F.w + 7) >> 3, tiles_y = (F.h + 3) >> 2;
-  const long long ntiles = (long long)tiles_x * tiles_y;
-  const long long wstride = (long long)gridDim.x * (blockDim.x >> 5);
-  int nvalid = 0;
-  for (long long tile = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); tile < ntiles;
-       tile += wstride) {
-    const int ty = (int)(tile / tiles_x), tx = (int)(tile - (long long)ty * tiles_x);
-    const int u = tx * 8 + (lane & 7), v = ty * 4 + (lane >> 3);
-    double d = 0.0, qs[3] = {0, 0, 0};
-    bool valid = false;
-    if (u < F.w && v < F.h) {
-      d = F.depth[(long long)v * F.w + u];
-      valid = d > 0 && d <= F.max_range;
+  trace_at(S, TK_COLLECT, 1);
+  __shared__ unsigned long long s_key[kCSet];
+  __shared__ uint16_t s_list[kCSet];
+  __shared__ unsigned long long s_over[kCOver];
+  __shared__ int s_out[kCSet + kCOver];
+  __shared__ int s_n, s_nover, s_valid, s_nout, s_base;
+  const int t = threadIdx.x, lane = t & 31;
+  const int rx = (F.w + kRegionW - 1) / kRegionW, ry = (F.h + kRegionH - 1) / kRegionH;
+  int nvalid = 0, nth = 0;
+  if (t == 0) s_valid = 0;
+  for (int reg = blockIdx.x; reg < rx * ry; reg += gridDim.x, nth++) {
+    trace_item(S, TK_COLLECT, nth, 0);
+    for (int q = t; q < kCSet; q += kCollectThreads) s_key[q] = kNoKey;
+    if (t == 0) { s_n = 0; s_nover = 0; }
+    __syncthreads();
+    const int ry0 = reg / rx, rx0 = reg - ry0 * rx;
+    const int u = rx0 * kRegionW + (t & (kRegionW - 1));
+    const double rxn = u < F.w ? __ldg(S.rays + u) : 0.0;
+    double d[2];
+    bool valid[2];
+#pragma unroll
+    for (int k = 0; k < 2; k++) {   // both depth loads in flight together
+      const int v = ry0 * kRegionH + (t >> 6) + 4 * k;
+      d[k] = (u < F.w && v < F.h) ? F.depth[(long long)v * F.w + u] : 0.0;
     }
-    if (valid) {
-      nvalid++;
-      const double rx = ((double)u - F.cx) / F.fx, ry = ((double)v - F.cy) / F.fy;
-      const double pc[3] = {__dmul_rn(rx, d), __dmul_rn(ry, d), __dmul_rn(1.0, d)};
-      for (int j = 0; j < 3; j++) qs[j] = matvec_row(pc, F.R, j);   // pts_cam @ R.T
-    }
-    if (!__any_sync(0xffffffffu, valid)) continue;
-    const double delta = valid ? F.trunc / d : 0.0;
-    for (int i = 0; i < nsteps; i++) {
-      long long key = kEmptyKey;
-      int c[3] = {0, 0, 0};
-      if (valid) {
-        const double s = (i == nsteps - 1) ? 1.0 : __dadd_rn(__dmul_rn((double)i, step), -1.0);
-        const double f = __dadd_rn(1.0, __dmul_rn(s, delta));
-        for (int j = 0; j < 3; j++)
-          c[j] = (int)floor(__dadd_rn(F.t[j], __dmul_rn(qs[j], f)) / S.extent);
-        if (block_relevant(S, c[0], c[1], c[2])) key = pack_coord(c[0], c[1], c[2]);
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+      const int v = ry0 * kRegionH + (t >> 6) + 4 * k;
+      valid[k] = u < F.w && v < F.h && d[k] > 0 && d[k] <= F.max_range;
+      double qs[3] = {0, 0, 0};
+      if (valid[k]) {
+        nvalid++;
+        const double ryn = __ldg(S.rays + F.w + v);
+        const double pc[3] = {__dmul_rn(rxn, d[k]), __dmul_rn(ryn, d[k]), __dmul_rn(1.0, d[k])};
+        for (int j = 0; j < 3; j++) qs[j] = matvec_row(pc, F.R, j);   // pts_cam @ R.T
       }
-      const unsigned grp = __match_any_sync(0xffffffffu, key);
-      if (key != kEmptyKey && lane == __ffs(grp) - 1) {
-        HashRef r = hash_find_ref(S, c[0], c[1], c[2]);
-        if (r.idx == -1) r = hash_insert_ref(S, c[0], c[1], c[2], F.epoch);
-        if (r.idx >= 0 && r.stamp != F.epoch && atomicExch(r.stamp_ptr, F.epoch) != F.epoch)
-          S.scope[atomicAdd(&ctr->ncollected, 1)] = r.idx;
+      if (!__any_sync(0xffffffffu, valid[k])) continue;
+      const double delta = valid[k] ? F.trunc / d[k] : 0.0;
+      for (int i = 0; i < nsteps; i++) {
+        unsigned long long key = kNoKey;
+        int c[3] = {0, 0, 0};
+        if (valid[k]) {
+          const double sv = (i == nsteps - 1) ? 1.0 : __dadd_rn(__dmul_rn((double)i, step), -1.0);
+          const double f = __dadd_rn(1.0, __dmul_rn(sv, delta));
+          for (int j = 0; j < 3; j++)
+            c[j] = floor_div_exact(__dadd_rn(F.t[j], __dmul_rn(qs[j], f)), S.extent, S.inv_extent);
+          if (block_relevant(S, c[0], c[1], c[2])) key = (unsigned long long)pack_coord(c[0], c[1], c[2]);
+        }
+        const unsigned grp = __match_any_sync(0xffffffffu, key);
+        if (key != kNoKey && lane == __ffs(grp) - 1) {
+          // CTA-local set: first inserter lists the key
+          unsigned h = cset_hash(key);
+          bool placed = false;
+          for (int probe = 0; probe < 32 && !placed; probe++, h = (h + 1) & (kCSet - 1)) {
+            const unsigned long long old = atomicCAS(&s_key[h], kNoKey, key);
+            if (old == kNoKey) s_list[atomicAdd(&s_n, 1)] = (uint16_t)h;
+            placed = old == kNoKey || old == key;
+          }
+          if (!placed) s_over[atomicAdd(&s_nover, 1) & (kCOver - 1)] = key;   // set crowded
+        }
       }
     }
+    trace_item(S, TK_COLLECT, nth, 1);
+    __syncthreads();
+    trace_item(S, TK_COLLECT, nth, 2);
+    // the region's distinct blocks, one thread each (+ keys that found the set
+    // crowded); the newly collected ones are appended with one atomic per CTA
+    const int nk = s_n, no = min(s_nover, kCOver);
+    if (t == 0) s_nout = 0;
+    __syncthreads();
+    for (int q0 = 0; q0 < nk + no; q0 += kCollectThreads) {
+      const int q = q0 + t;
+      int got = -1;
+      if (q < nk + no) {
+        const unsigned long long key = q < nk ? s_key[s_list[q]] : s_over[q - nk];
+        const long long off = 1LL << 20;
+        const int x = (int)((long long)(key >> 42) - off),
+                  y = (int)((long long)((key >> 21) & 0x1FFFFF) - off), z = (int)((long long)(key & 0x1FFFFF) - off);
+        got = collect_block(S, F, x, y, z);
+      }
+      const int pos = smem_append(got >= 0, &s_nout);
+      if (got >= 0) s_out[pos] = got;
+    }
+    __syncthreads();
+    if (t == 0 && s_nout) s_base = atomicAdd(&ctr->ncollected, s_nout);
+    __syncthreads();
+    for (int q = t; q < s_nout; q += kCollectThreads) S.scope[s_base + q] = s_out[q];
+    __syncthreads();   // the set is reset for the next region
+    trace_item(S, TK_COLLECT, nth, 3);
   }
   if (F.nsteps_fixed > 0) {   // valid-pixel count (k_depth_stats did not run): one atomic per CTA
-    __shared__ int s_valid;
-    if (threadIdx.x == 0) s_valid = 0;
-    __syncthreads();
-    nvalid = warp_sum(nvalid);
+    nvalid = __reduce_add_sync(0xffffffffu, (unsigned)nvalid);
     if (lane == 0 && nvalid) atomicAdd(&s_valid, nvalid);
     __syncthreads();
-    if (threadIdx.x == 0 && s_valid) atomicAdd(&ctr->nvalid, s_valid);
+    if (t == 0 && s_valid) atomicAdd(&ctr->nvalid, s_valid);
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) ctr->nsteps = nsteps;
+  if (blockIdx.x == 0 && t == 0) ctr->nsteps = nsteps;
+  trace_count(S, TK_COLLECT, nth);
+  trace_at(S, TK_COLLECT, 31);
 }
 
 // ------------------------------------------------------------ explicit lists
@@ -196,6 +321,7 @@ __device__ __forceinline__ void init_block(const DevState &S, int b, int t) {
   vb[t] = -1;
   vb[t + kNC] = -1;
   vb[t + 2 * kNC] = -1;
+  if (t < kEV / 32) S.vocc[(size_t)b * (kEV / 32) + t] = 0u;
 }
 
 __global__ void __launch_bounds__(kThreadsCube) k_init_blocks(DevState S) {
@@ -228,15 +354,21 @@ __global__ void __launch_bounds__(kFB, 6) k_fuse_blocks(DevState S, const FrameD
                                                      const int32_t *__restrict__ count_ptr,
                                                      int count_const, int flags) {
   cudaGridDependencySynchronize();   // PDL: wait for the previous kernel of the frame
-  const bool stop = halted(S);
-  const int n = list_count(count_ptr, count_const);   // issued together with the halt check
-  if (stop) return;
+  trace_at(S, TK_FUSE, 0);
+  __shared__ int s_pro[5];
+  const int list_cap = count_ptr ? S.max_blocks : count_const;
+  read_prologue(S, s_pro, count_ptr, nullptr, nullptr, (int)blockIdx.x < list_cap ? list + blockIdx.x : nullptr);
+  if (s_pro[0]) return;
+  const int n = count_ptr ? s_pro[1] : count_const;
+  trace_at(S, TK_FUSE, 1);
+  int nth = 0;
   const int t = threadIdx.x;
   // neighbour probe of this thread: 7 lanes of each warp, directions 0..26
   const int pl = t & 31, pdir = (t >> 5) * 7 + pl;
   const bool prober = pl < 7 && pdir < 27;
-  for (int i = blockIdx.x; i < n; i += gridDim.x) {
-    const int b = __ldcg(list + i);
+  for (int i = blockIdx.x; i < n; i += gridDim.x, nth++) {
+    trace_item(S, TK_FUSE, nth, 0);
+    const int b = i == (int)blockIdx.x && s_pro[4] != -1 ? s_pro[4] : __ldcg(list + i);
     if (b < 0) continue;
     const int4 c = __ldcg(S.bcoord + b);
     const bool fresh = (flags & F_INIT) && __ldcg(S.stamp_new + b) == F.epoch;
@@ -282,9 +414,16 @@ __global__ void __launch_bounds__(kFB, 6) k_fuse_blocks(DevState S, const FrameD
       const int dx = pdir / 9 - 1, dy = (pdir / 3) % 3 - 1, dz = pdir % 3 - 1;
       int nb = b, nb_collected = 1;
       if (pdir != 13) {
-        const HashRef r = hash_find_ref(S, c.x + dx, c.y + dy, c.z + dz);
-        nb = r.idx;
-        nb_collected = r.stamp == F.epoch;
+        if (fresh) {   // its links are built here, from the table
+          const HashRef r = hash_find_ref(S, c.x + dx, c.y + dy, c.z + dz);
+          nb = r.idx;
+          nb_collected = r.stamp == F.epoch;
+        } else {
+          // an older block's row is complete except for neighbours created in
+          // this call, which are collected and mark themselves
+          nb = __ldcg(S.nbr + (size_t)b * 27 + pdir);
+          nb_collected = nb >= 0 && __ldcg(S.stamp_collect + nb) == F.epoch;
+        }
       }
       if (fresh) {
         S.nbr[(size_t)b * 27 + pdir] = nb;
@@ -319,7 +458,10 @@ __global__ void __launch_bounds__(kFB, 6) k_fuse_blocks(DevState S, const FrameD
       const long long nw = (long long)w_old[j] + 1;
       S.weight[q] = (int)(nw < F.weight_cap ? nw : F.weight_cap);
     }
+    trace_item(S, TK_FUSE, nth, 3);
   }
+  trace_count(S, TK_FUSE, nth);
+  trace_at(S, TK_FUSE, 31);
 }
 
 // halo of an explicit scope (extract_frame default, mesher.py:627-633)
@@ -382,51 +524,10 @@ __device__ __forceinline__ void load_ext_tile(const DevState &S, int b, const in
   }
 }
 
-__device__ __forceinline__ int item_count(const DevState &S, const FrameDev &F) {
-  if (F.scope_mode != 0) return __ldcg(&S.ctr->nexplicit);
-  const int2 v = __ldcg(reinterpret_cast<const int2 *>(&S.ctr->ncollected));   // ncollected, nnew
-  return v.x + __ldcg(&S.ctr->nslab);
-}
 
-// warp-aggregated append of `cnt` entries to a shared-memory list; returns
-// this lane's first index
-__device__ __forceinline__ int smem_append(int cnt, int *s_count) {
-  const int lane = threadIdx.x & 31;
-  int incl = cnt;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int u = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += u;
-  }
-  const int total = __shfl_sync(0xffffffffu, incl, 31);
-  int base = 0;
-  if (lane == 31 && total) base = atomicAdd(s_count, total);
-  base = __shfl_sync(0xffffffffu, base, 31);
-  return base + incl - cnt;
-}
 
 // ------------------------------------------------------------ retype + place
-// One CTA per scope item (persistent over the item list), one thread per cube
-// for typing.  Software-pipelined: while block i is typed and placed, the
-// neighbour row and the 9^3 tsdf/weight tile + type row of the CTA's next
-// block stream into the other shared-memory buffer with cp.async (LDGSTS).
-// Typing and refinement as the reference; a cube whose type changed is
-// retriangulated implicitly (its triangles become TRI_TABLE[type_curr]) and
-// contributes the triangle / irregular-count deltas.  The (active cube, mask
-// edge) placements are compacted in shared memory and spread over the CTA:
-// each claims its edge slot (atomicCAS on the slot's birth word -- exactly one
-// allocation per edge) and writes the interpolated coordinate; all requesters
-// produce identical bits (mesher.py:216-235).
-constexpr int kMaxPlace = kNC * 12;
-
-// Tile-source tables (filled by vm_create): for every staged tile position,
-// the neighbour direction (0..26) and the source cube index in that block,
-// so the loaders do no div/mod index arithmetic.
-__device__ uint32_t g_ext_tab[217];   // 9^3 tile position | dir << 10 | src << 15 (positions with a coord == 8)
-__device__ uint16_t g_sten_tab[1331]; // dir << 9 | src, 11^3 stencil over locals -1..9
-__device__ uint16_t g_type_tab[729];  // dir << 9 | src, 9^3 type tile over locals -1..7
-
-// Per-item "resolved" record (three in flight: computing, staged, resolving)
+// Per-item "resolved" record: the item's block, neighbour row and selection mode
 struct Resolved {
   int4 coord;
   int nbr[27];
@@ -482,44 +583,92 @@ __device__ __forceinline__ void resolve_store(const DevState &S, const FrameDev 
 }
 
 constexpr int kNT = 128;   // threads per CTA of the per-block meshing kernels (4 cubes each)
+constexpr int kTileSlots = 729 * 3;   // edge slots owned by the 9^3 tile points (3 axes each)
+
+
+// position q < 217 of the (B+1)^3 tile's plus layer (points with a coordinate
+// == 8): tile point, neighbour direction and source sample (mesher.py:75-96)
+__device__ __forceinline__ void ext_src(int q, int &p, int &dir, int &src) {
+  int x, y, z;
+  if (q < 64) { x = 8; y = q >> 3; z = q & 7; }
+  else if (q < 128) { x = (q - 64) >> 3; y = 8; z = q & 7; }
+  else if (q < 192) { x = (q - 128) >> 3; y = q & 7; z = 8; }
+  else if (q < 200) { x = 8; y = 8; z = q - 192; }
+  else if (q < 208) { x = 8; y = q - 200; z = 8; }
+  else if (q < 216) { x = q - 208; y = 8; z = 8; }
+  else { x = 8; y = 8; z = 8; }
+  p = (x * 9 + y) * 9 + z;
+  dir = ((x >> 3) + 1) * 9 + ((y >> 3) + 1) * 3 + ((z >> 3) + 1);
+  src = (x & 7) * 64 + (y & 7) * 8 + (z & 7);
+}
+
+// Corner bytes of the 4 cubes z0..z0+3 of a column, bit plane starting at bit
+// `sh` of the 4 column words of the (x, y) footprint: byte j holds cube
+// z0 + j's 8 corner bits in CORNER_OFFSETS order (mc_tables.py:31-34:
+// (0,0,0) (1,0,0) (1,1,0) (0,1,0), then the same at z + 1).  spread4 moves
+// 4 bits to the low bit of 4 bytes (one multiply, no carries).
+__device__ __forceinline__ uint32_t spread4(uint32_t v) { return ((v & 0xFu) * 0x00204081u) & 0x01010101u; }
+__device__ __forceinline__ uint32_t corner_bytes4(const uint32_t (&w)[4], int sh) {
+  uint32_t r = 0;
+#pragma unroll
+  for (int k = 0; k < 4; k++) r |= (spread4(w[k] >> sh) << k) | (spread4(w[k] >> (sh + 1)) << (k + 4));
+  return r;
+}
 
 // One CTA of 128 threads per scope item (persistent over the item list).
-// Small CTAs keep ~8 blocks in flight per SM so their serial phases (resolve,
-// staging, typing, placement) overlap across blocks.  Typing and refinement
-// as the reference; a cube whose type changed is retriangulated implicitly
-// (its triangles become TRI_TABLE[type_curr]) and contributes the triangle /
-// irregular-count deltas.  The (active cube, mask edge) placements are
-// compacted in shared memory and spread over the CTA: each claims its edge
-// slot (atomicCAS on the slot's birth word -- exactly one allocation per
-// edge) and writes the interpolated coordinate; all requesters produce
-// identical bits (mesher.py:216-235).
+//  * stage: the block's tsdf/weight/types and the plus layer of its 7 plus
+//    neighbours (mesher.py:75-96); the corner predicates (tsdf < 0, weight > 0,
+//    |tsdf| < eps) are packed with warp ballots into one 27-bit word per tile
+//    column (x, y) -- bit z, 9 + z, 18 + z;
+//  * typing (+ Hamming refinement), one thread per 4-cube run of a column:
+//    8 corner bits from 4 column words (mesher.py:111-134, refine.py:98-135);
+//    a cube whose type changed is retriangulated implicitly (its triangles
+//    become TRI_TABLE[type_curr], mesher.py:283-326) and contributes the
+//    triangle / irregular-count deltas;
+//  * placement (mesher.py:178-257): the requested edge slots are deduplicated
+//    in a shared-memory bitmap (all requesters of a slot write identical bits),
+//    then each is claimed (atomicCAS on its birth word -- exactly one
+//    allocation per edge) and its coordinate written.
 __global__ void __launch_bounds__(kNT, 8) k_retype_place(DevState S, const FrameDev F) {
   cudaGridDependencySynchronize();   // PDL: wait for the previous kernel of the frame
-  if (halted(S)) return;
+  trace_at(S, TK_RETYPE, 0);
+  __shared__ int s_pro[5];
+  __shared__ SmemTables T;
+  read_prologue(S, s_pro, &S.ctr->ncollected, &S.ctr->nslab, &S.ctr->nexplicit,
+                (int)blockIdx.x < S.max_blocks ? S.scope + blockIdx.x : nullptr, &T);
+  if (s_pro[0]) return;
+  const int nc = s_pro[1];
+  const int n = F.scope_mode != 0 ? s_pro[3] : nc + s_pro[2];
+  trace_at(S, TK_RETYPE, 1);
+  int nth = 0;
   __shared__ double tile[729];
-  __shared__ uint8_t tw[729];
+  __shared__ uint32_t s_col[81];    // tile column x*9+y: sign bits 0..7, valid 9..16, small 18..25
+  __shared__ uint8_t s_top[81];     // its z = 8 point: bit 0 sign, 1 valid, 2 small
   __shared__ __align__(16) uint8_t s_tc[kNC];
-  __shared__ uint16_t s_place[kMaxPlace];
+  __shared__ __align__(16) uint8_t s_tp[kNC];
+  __shared__ uint32_t s_claim[3 * 81];   // requested slots: [axis][tile column], bit = owner z
+  __shared__ uint16_t s_place[kTileSlots];
   __shared__ Resolved R;
-  __shared__ long long red8[8 * 32];
+  __shared__ int red8[8 * 32];
   __shared__ int s_nplace;
-  const int n = item_count(S, F);
-  const int nc = __ldcg(&S.ctr->ncollected);
-  const int t = threadIdx.x;
+  const int t = threadIdx.x, lane = t & 31;
   const double l = S.cube_size;
   const int frame = F.frame;
   const int do_refine = F.refine;
   const double eps = F.epsilon;
-  long long allocs = 0, placements = 0, active = 0, changed = 0, t_rel = 0, t_new = 0, irr = 0,
-            refined = 0, live = 0;
-  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+  int allocs = 0, placements = 0, active = 0, changed = 0, t_rel = 0, t_new = 0, irr = 0, refined = 0,
+      live = 0;
+  for (int i = blockIdx.x; i < n; i += gridDim.x, nth++) {
+    trace_item(S, TK_RETYPE, nth, 0);
     if (t < 32) {
-      const int b = __ldcg(S.scope + i);
+      const int b = i == (int)blockIdx.x && s_pro[4] != -1 ? s_pro[4] : __ldcg(S.scope + i);
       const ResolveRegs rr = resolve_load(S, F, b, i, nc);
       resolve_store(S, F, rr, b, i, n, nc, R);
     }
+    for (int q = t; q < 3 * 81; q += kNT) s_claim[q] = 0;
     if (t == 0) s_nplace = 0;
     __syncthreads();
+    trace_item(S, TK_RETYPE, nth, 1);
     const int mode = R.mode;
     if (mode <= 0) {
       __syncthreads();
@@ -528,18 +677,18 @@ __global__ void __launch_bounds__(kNT, 8) k_retype_place(DevState S, const Frame
     const int b = R.b;
     const int own = R.owned;
     if (t == 0) live++;
-    // stage the (B+1)^3 tile (mesher.py:75-96) and the current types
     {
       // batched gathers: all loads in flight before any shared-memory store
       double ov[kNC / kNT], xv[2];
       int ow[kNC / kNT], xw[2], xp[2];
-      uint4 tcv = make_uint4(0, 0, 0, 0);
+      uint4 tcv = make_uint4(0, 0, 0, 0), tpv = make_uint4(0, 0, 0, 0);
 #pragma unroll
       for (int j = 0; j < kNC / kNT; j++) {
         ov[j] = S.tsdf[(size_t)b * kNC + t + j * kNT];
         ow[j] = S.weight[(size_t)b * kNC + t + j * kNT];
       }
       if (t < 32) tcv = reinterpret_cast<const uint4 *>(S.tc + (size_t)b * kNC)[t];
+      else if (t < 64) tpv = reinterpret_cast<const uint4 *>(S.tp + (size_t)b * kNC)[t - 32];
 #pragma unroll
       for (int j = 0; j < 2; j++) {
         const int q = t + j * kNT;
@@ -547,118 +696,181 @@ __global__ void __launch_bounds__(kNT, 8) k_retype_place(DevState S, const Frame
         xw[j] = 0;
         xp[j] = -1;
         if (q < 217) {
-          const uint32_t e = __ldg(&g_ext_tab[q]);
-          const int nb = R.nbr[(e >> 10) & 31];
-          xp[j] = e & 1023;
+          int dir, src;
+          ext_src(q, xp[j], dir, src);
+          const int nb = R.nbr[dir];
           if (nb >= 0) {
-            const size_t src = (size_t)nb * kNC + (e >> 15);
-            xv[j] = S.tsdf[src];
-            xw[j] = S.weight[src];
+            xv[j] = S.tsdf[(size_t)nb * kNC + src];
+            xw[j] = S.weight[(size_t)nb * kNC + src];
           }
         }
       }
+      // own samples: lanes 8g..8g+7 hold z = 0..7 of one column
+      const int g8 = (lane >> 3) * 8;
 #pragma unroll
       for (int j = 0; j < kNC / kNT; j++) {
         const int c = t + j * kNT;
-        const int p = ((c >> 6) * 9 + ((c >> 3) & 7)) * 9 + (c & 7);
-        tile[p] = ov[j];
-        tw[p] = ow[j] > 0;
+        const int col = (c >> 6) * 9 + ((c >> 3) & 7);
+        tile[col * 9 + (c & 7)] = ov[j];
+        const unsigned bs = __ballot_sync(0xffffffffu, ov[j] < 0.0);
+        const unsigned bv = __ballot_sync(0xffffffffu, ow[j] > 0);
+        const unsigned bm = __ballot_sync(0xffffffffu, fabs(ov[j]) < eps);
+        if ((lane & 7) == 0)
+          s_col[col] = ((bs >> g8) & 0xFFu) | (((bv >> g8) & 0xFFu) << 9) | (((bm >> g8) & 0xFFu) << 18);
       }
       if (t < 32) reinterpret_cast<uint4 *>(s_tc)[t] = tcv;
+      else if (t < 64) reinterpret_cast<uint4 *>(s_tp)[t - 32] = tpv;
+      // plus layer: q < 128 are the x = 8 and y = 8 faces (z = 0..7 runs of a
+      // column), q = 192..199 the column (8, 8); the rest are z = 8 points
 #pragma unroll
-      for (int j = 0; j < 2; j++)
+      for (int j = 0; j < 2; j++) {
+        const int q = t + j * kNT;
+        const bool run = q < 128 || (q >= 192 && q < 200);
+        const unsigned bs = __ballot_sync(0xffffffffu, xv[j] < 0.0);
+        const unsigned bv = __ballot_sync(0xffffffffu, xw[j] > 0);
+        const unsigned bm = __ballot_sync(0xffffffffu, fabs(xv[j]) < eps);
         if (xp[j] >= 0) {
           tile[xp[j]] = xv[j];
-          tw[xp[j]] = xw[j] > 0;
+          const int col = xp[j] / 9;
+          if (run) {
+            if ((lane & 7) == 0)
+              s_col[col] = ((bs >> g8) & 0xFFu) | (((bv >> g8) & 0xFFu) << 9) | (((bm >> g8) & 0xFFu) << 18);
+          } else {
+            s_top[col] = (uint8_t)((xv[j] < 0.0) | ((xw[j] > 0) << 1) | ((fabs(xv[j]) < eps) << 2));
+          }
         }
+      }
     }
     __syncthreads();
-#pragma unroll 1
-    for (int j = 0; j < kNC / kNT; j++) {
-      const int c = t + j * kNT;
-      const int x = c >> 6, y = (c >> 3) & 7, z = c & 7;
-      bool sel;
-      if (mode == 1) sel = true;
-      else if (mode == 2) sel = (R.slab & c_slab_sel[((x == 7) << 2) | ((y == 7) << 1) | (z == 7)]) != 0;
-      else sel = (S.item_mask[(size_t)R.item * 16 + (c >> 5)] >> (c & 31)) & 1;
-      unsigned bits = 0, small = 0;
-      const int base = (x * 9 + y) * 9 + z;
+    trace_item(S, TK_RETYPE, nth, 2);
+    // typing: thread t -> column (x, y) = t >> 1 (x = col >> 3), cubes z0..z0+3.
+    // The 4 cubes' corner bytes are formed bit-sliced: byte j of a plane word
+    // holds the 8 corner bits of cube z0 + j.
+    {
+      const int x = t >> 4, y = (t >> 1) & 7, z0 = (t & 1) * 4;
+      uint32_t w[4];
+      const int cols[4] = {x * 9 + y, (x + 1) * 9 + y, (x + 1) * 9 + y + 1, x * 9 + y + 1};
 #pragma unroll
-      for (int k = 0; k < 8; k++) {
-        const int o = c_corner[k];
-        const int e = base + (o & 1) * 81 + ((o >> 1) & 1) * 9 + ((o >> 2) & 1);
-        const double cv = tile[e];
-        sel = sel && tw[e];
-        bits |= (cv < 0.0 ? 1u : 0u) << k;
-        small |= (fabs(cv) < eps ? 1u : 0u) << k;
+      for (int k = 0; k < 4; k++) {
+        const uint32_t tp8 = s_top[cols[k]];
+        w[k] = s_col[cols[k]] | ((tp8 & 1u) << 8) | (((tp8 >> 1) & 1u) << 17) | (((tp8 >> 2) & 1u) << 26);
       }
-      unsigned mask = 0;
-      if (sel) {
-        const unsigned tp = s_tc[c];
+      const uint32_t sgn = corner_bytes4(w, z0), val = corner_bytes4(w, 9 + z0);
+      const uint32_t sml = do_refine ? corner_bytes4(w, 18 + z0) : 0u;
+      const int c0 = (x * 8 + y) * 8 + z0;
+      const uint32_t old_tc = reinterpret_cast<const uint32_t *>(s_tc)[c0 >> 2];
+      const uint32_t old_tp = reinterpret_cast<const uint32_t *>(s_tp)[c0 >> 2];
+      uint32_t new_tc = old_tc, new_tp = old_tp;
+      uint32_t cxa = 0, cxb = 0, cya = 0, cyb = 0, cza = 0, czb = 0, czc = 0, czd = 0;
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const int z = z0 + k;
+        const int c = c0 + k;
+        bool sel;
+        if (mode == 1) sel = true;
+        else if (mode == 2) sel = (R.slab & c_slab_sel[((x == 7) << 2) | ((y == 7) << 1) | (z == 7)]) != 0;
+        else sel = (S.item_mask[(size_t)R.item * 16 + (c >> 5)] >> (c & 31)) & 1;
+        sel = sel && ((val >> (8 * k)) & 0xFFu) == 0xFFu;   // all 8 weights > 0
+        if (!sel) continue;
+        const unsigned bits = (sgn >> (8 * k)) & 0xFFu;
+        const unsigned tp = (old_tc >> (8 * k)) & 0xFFu;
         unsigned tc = bits;
         if (do_refine) {
           bool ch;
-          tc = refine_type(bits, tp, small, &ch);
+          tc = refine_type(bits, tp, (sml >> (8 * k)) & 0xFFu, &ch);
           refined += ch && own;
         }
-        const size_t q = (size_t)b * kNC + c;
-        S.tp[q] = (uint8_t)tp;
-        S.tc[q] = (uint8_t)tc;
+        new_tp = (new_tp & ~(0xFFu << (8 * k))) | (tp << (8 * k));
+        new_tc = (new_tc & ~(0xFFu << (8 * k))) | (tc << (8 * k));
         if (tc != tp && own) {
           changed++;
-          const int nold = c_tri_count[tp], nnew = c_tri_count[tc];
+          const int nold = T.tri_count[tp], nnew = T.tri_count[tc];
           t_rel += nold;
           t_new += nnew;
           irr += (nnew > 0 && !is_regular_type(tc)) - (nold > 0 && !is_regular_type(tp));
         }
-        mask = c_edge_mask[tc];
+        const unsigned mask = T.edge_mask[tc];
         if (mask && own) {
           active++;
           placements += __popc(mask);
         }
+        // request the mask edges' slots: per axis, the owner point's column
+        // word (bit = owner z), edge geometry of mc_tables.py:44-64
+        const unsigned b0 = 1u << z, b1 = 2u << z;
+        cxa |= (mask & 1u ? b0 : 0u) | (mask & 16u ? b1 : 0u);            // e0, e4: (x, y)
+        cxb |= (mask & 4u ? b0 : 0u) | (mask & 64u ? b1 : 0u);            // e2, e6: (x, y+1)
+        cya |= (mask & 2u ? b0 : 0u) | (mask & 32u ? b1 : 0u);            // e1, e5: (x+1, y)
+        cyb |= (mask & 8u ? b0 : 0u) | (mask & 128u ? b1 : 0u);           // e3, e7: (x, y)
+        cza |= mask & 256u ? b0 : 0u;                                      // e8: (x, y)
+        czb |= mask & 512u ? b0 : 0u;                                      // e9: (x+1, y)
+        czc |= mask & 1024u ? b0 : 0u;                                     // e10: (x+1, y+1)
+        czd |= mask & 2048u ? b0 : 0u;                                     // e11: (x, y+1)
       }
-      int pos = smem_append(__popc(mask), &s_nplace);
-      while (mask) {
-        const int e = __ffs(mask) - 1;
-        mask &= mask - 1;
-        s_place[pos++] = (uint16_t)((c << 4) | e);
+      // one shared-memory OR per (axis, column) word this thread touched
+      if (cxa) atomicOr(&s_claim[0 * 81 + cols[0]], cxa);
+      if (cxb) atomicOr(&s_claim[0 * 81 + cols[3]], cxb);
+      if (cya) atomicOr(&s_claim[1 * 81 + cols[1]], cya);
+      if (cyb) atomicOr(&s_claim[1 * 81 + cols[0]], cyb);
+      if (cza) atomicOr(&s_claim[2 * 81 + cols[0]], cza);
+      if (czb) atomicOr(&s_claim[2 * 81 + cols[1]], czb);
+      if (czc) atomicOr(&s_claim[2 * 81 + cols[2]], czc);
+      if (czd) atomicOr(&s_claim[2 * 81 + cols[3]], czd);
+      if (new_tc != old_tc || new_tp != old_tp) {   // 4 cubes per 32-bit store
+        const size_t q4 = ((size_t)b * kNC + c0) >> 2;
+        reinterpret_cast<uint32_t *>(S.tp)[q4] = new_tp;
+        reinterpret_cast<uint32_t *>(S.tc)[q4] = new_tc;
       }
     }
     __syncthreads();
+    // compact the requested slots (each once, whichever cubes asked for it):
+    // word a * 81 + col holds owner heights z of axis a in column col
+#pragma unroll
+    for (int r = 0; r < 2; r++) {
+      const int wi = t + r * kNT;
+      const uint32_t word = wi < 3 * 81 ? s_claim[wi] : 0u;
+      int pos = smem_append(__popc(word), &s_nplace);
+      const int axis = wi / 81, col = wi - axis * 81;
+      for (uint32_t m = word; m; m &= m - 1) s_place[pos++] = (uint16_t)(((col * 9 + __ffs(m) - 1) * 3) + axis);
+    }
+    __syncthreads();
+    trace_item(S, TK_RETYPE, nth, 3);
     const int np = s_nplace;
     for (int p = t; p < np; p += kNT) {
-      const int ent = s_place[p];
-      const int ci = ent >> 4, e = ent & 15;
-      const int own = c_e_own[e], axis = c_e_axis[e];
-      const int ox = (ci >> 6) + (own & 1), oy = ((ci >> 3) & 7) + ((own >> 1) & 1), oz = (ci & 7) + ((own >> 2) & 1);
+      const int u = s_place[p];
+      const int pt = u / 3, axis = u - 3 * pt;
+      const int ox = pt / 81, oy = (pt / 9) % 9, oz = pt % 9;
       const int owner = R.nbr[nbr_dir(ox >> 3, oy >> 3, oz >> 3)];
       if (owner < 0) {
-        set_error(S, ERR_CONSISTENCY, 10, R.coord.x * kB + (ci >> 6), R.coord.y * kB + ((ci >> 3) & 7),
-                  R.coord.z * kB + (ci & 7));
+        set_error(S, ERR_CONSISTENCY, 10, R.coord.x * kB + ox, R.coord.y * kB + oy, R.coord.z * kB + oz);
         continue;
       }
       const size_t slot = (size_t)owner * kEV + (((ox & 7) * 64 + (oy & 7) * 8 + (oz & 7)) * 3 + axis);
-      // start corner = owner cube origin; end corner one step along the axis
-      const int p0 = (ox * 9 + oy) * 9 + oz;
-      const double d0 = tile[p0];
-      const double d1 = tile[p0 + (axis == 0 ? 81 : axis == 1 ? 9 : 1)];
+      // start corner = the owner point; end corner one step along the axis
+      const double d0 = tile[pt];
+      const double d1 = tile[pt + (axis == 0 ? 81 : axis == 1 ? 9 : 1)];
       const double param = (d0 == d1) ? 0.5 : d0 / (d0 - d1);
       const int ga = (axis == 0 ? R.coord.x * kB + ox : axis == 1 ? R.coord.y * kB + oy : R.coord.z * kB + oz);
       S.vparam[slot] = __dadd_rn(__dmul_rn((double)ga, l), __dmul_rn(param, l));
-      if (atomicCAS(S.vbirth + slot, -1, frame) == -1) {
+      // claim: the first requester to set the slot's occupancy bit allocates
+      const uint32_t bit = 1u << (slot & 31);
+      if (!(atomicOr(S.vocc + (slot >> 5), bit) & bit)) {
         allocs += (S.nranks <= 1 || S.bowned[owner]);   // counted by the slot's owning rank
+        S.vbirth[slot] = frame;
         S.vnrm[3 * slot] = 0.0; S.vnrm[3 * slot + 1] = 0.0; S.vnrm[3 * slot + 2] = 0.0;
       }
     }
     __syncthreads();   // R, tile and the placement list are rewritten by the next item
   }
   {
-    long long vals[8] = {allocs, placements, active, changed, t_rel, t_new, irr, refined};
+    trace_count(S, TK_RETYPE, nth);
+    trace_at(S, TK_RETYPE, 28);
+    int vals[8] = {allocs, placements, active, changed, t_rel, t_new, irr, refined};
     int64_t *const dst[8] = {&S.ctr->v_allocs, &S.ctr->placements, &S.ctr->active, &S.ctr->changed,
                              &S.ctr->t_released, &S.ctr->t_allocated, &S.ctr->irr_delta, &S.ctr->refined};
     block_add_counters<8>(vals, red8, dst);
   }
   if (t == 0 && live) atomicAdd(&S.ctr->nitems_live, (int)live);
+  trace_at(S, TK_RETYPE, 31);
 }
 constexpr size_t kRetypeSmem = 0;
 
@@ -673,81 +885,110 @@ __device__ __forceinline__ int cube_edge_of_slot(int axis, int du, int dw) {
   return c_edge_of[axis][own];
 }
 
-// type of the cube at local (l0, l1, l2) in [-1, 7]^3 from the staged words
-// (each word is the aligned 4 bytes of tc holding the cube's type)
-__device__ __forceinline__ int staged_type(const uint32_t *ttw, int l0, int l1, int l2) {
-  return (ttw[((l0 + 1) * 9 + (l1 + 1)) * 9 + (l2 + 1)] >> (8 * (l2 & 3))) & 0xFF;
+// position q of the 9^3 type tile over cube locals -1..7 -> neighbour
+// direction and source cube (index arithmetic, no table load on the chain)
+__device__ __forceinline__ void type_tile_src(int q, int &dir, int &src) {
+  const int a = q / 81, r = q - a * 81, bb = r / 9, cc = r - bb * 9;
+  const int lx = a - 1, ly = bb - 1, lz = cc - 1;
+  dir = nbr_dir(lx < 0 ? -1 : 0, ly < 0 ? -1 : 0, lz < 0 ? -1 : 0);
+  src = (lx & 7) * 64 + (ly & 7) * 8 + (lz & 7);
 }
 
-// Face-normal fallback for one vertex, computed by one warp (mesher.py:459-486).
-// Lane l handles candidate (incident cube j = l / 5, triangle slot s = l % 5);
-// the contributions are then summed by lane 0 in the reference's order:
-// vertex position k major, then halo blocks in sorted order, then cube, then
-// triangle slot -- so the result is bit-identical to np.add.at's.
-__device__ void fallback_normal_warp(const DevState &S, const uint8_t *ttile, const int *s_nbr, int4 bc,
-                                     int slot_ci, int axis, int epoch, double *dst) {
+// edge e -> owner-cube offset (x | y<<1 | z<<2) | axis << 3, 5 bits per edge (mc_tables.py:44-64)
+__host__ __device__ constexpr unsigned long long edge_own_axis(int e) {
+  constexpr int own[12] = {0, 1, 2, 0, 4, 5, 6, 4, 0, 1, 3, 2};
+  constexpr int axis[12] = {0, 1, 0, 1, 0, 1, 0, 1, 2, 2, 2, 2};
+  return (unsigned long long)(own[e] | axis[e] << 3);
+}
+constexpr unsigned long long kEdgeOwnAxis =
+    edge_own_axis(0) | edge_own_axis(1) << 5 | edge_own_axis(2) << 10 | edge_own_axis(3) << 15 |
+    edge_own_axis(4) << 20 | edge_own_axis(5) << 25 | edge_own_axis(6) << 30 | edge_own_axis(7) << 35 |
+    edge_own_axis(8) << 40 | edge_own_axis(9) << 45 | edge_own_axis(10) << 50 | edge_own_axis(11) << 55;
+
+// The 4 cubes around the edge slot (slot_ci, axis): candidate j = (du, dw) =
+// (j >> 1, j & 1) sits at -du along u and -dw along w (u, w = the other two
+// axes), i.e. at cube locals (l0, l1, l2) in [-1, 7]^3.
+__device__ __forceinline__ void slot_cube(int slot_ci, int axis, int j, int &l0, int &l1, int &l2) {
+  const int du = j >> 1, dw = j & 1;
+  l0 = (slot_ci >> 6) - (axis == 0 ? 0 : du);
+  l1 = ((slot_ci >> 3) & 7) - (axis == 0 ? du : 0) - (axis == 2 ? dw : 0);
+  l2 = (slot_ci & 7) - (axis == 2 ? 0 : dw);
+}
+
+// Face-normal fallback for one vertex, computed by one warp (mesher.py:456-486).
+// `types4` holds the types of the 4 cubes around the slot (byte j = candidate
+// j), `cand` flags the candidates whose triangles count (edge in the cube's
+// mask, cube inside a halo block of this call); lanes 0..26 hold the block's
+// neighbour row in `nbr_lane`.  Lane l handles (incident cube j = l / 5,
+// triangle slot s = l % 5); the contributions are then summed by lane 0 in the
+// reference's order: vertex position k major, then halo blocks in sorted order,
+// then cube, then triangle slot -- bit-identical to np.add.at's.
+__device__ __forceinline__ void fallback_normal_warp(const double *__restrict__ vparam, double cube_size,
+                                                     int nbr_lane, uint32_t types4, uint32_t cand, int4 bc,
+                                                     int slot_ci, int axis, double *dst) {
   const int lane = threadIdx.x & 31;
-  const int lx = slot_ci >> 6, ly = (slot_ci >> 3) & 7, lz = slot_ci & 7;
-  const int u = axis == 0 ? 1 : 0, w = axis == 2 ? 1 : 2;
-  // cube candidates j = 0..3: (du, dw) = (j >> 1, j & 1)
-  int cj = -1, ckey = 0x7fffffff, ctt = 0, ce = 0;
-  int cl[3] = {0, 0, 0};
-  if (lane < 4) {
-    const int du = lane >> 1, dw = lane & 1;
-    int l[3] = {lx, ly, lz};
-    l[u] -= du;
-    l[w] -= dw;
-    const int tt = ttile[((l[0] + 1) * 9 + (l[1] + 1)) * 9 + (l[2] + 1)];
-    const int e = cube_edge_of_slot(axis, du, dw);
-    const int dx = l[0] < 0 ? -1 : 0, dy = l[1] < 0 ? -1 : 0, dz = l[2] < 0 ? -1 : 0;
-    const int nb = s_nbr[nbr_dir(dx, dy, dz)];
-    if (((c_edge_mask[tt] >> e) & 1) && nb >= 0 && ld_vol(S.stamp_halo + nb) == epoch) {
-      cj = lane;
-      ckey = (((dx + 1) * 4 + (dy + 1) * 2 + (dz + 1)) << 9) | ((l[0] & 7) * 64 + (l[1] & 7) * 8 + (l[2] & 7));
-      ctt = tt;
-      ce = e;
-      cl[0] = l[0]; cl[1] = l[1]; cl[2] = l[2];
-    }
-  }
-  // rank of each cube candidate by (sorted block, cube) key
-  int rank = 0;
-#pragma unroll
-  for (int j = 0; j < 4; j++) {
-    const int kj = __shfl_sync(0xffffffffu, ckey, j);
-    rank += (kj < ckey);
-  }
+  // the vertex's current normal ("never set" test) is requested first
+  const double o0 = lane == 0 ? dst[0] : 0.0, o1 = lane == 0 ? dst[1] : 0.0, o2 = lane == 0 ? dst[2] : 0.0;
   // lane l: candidate cube j = l / 5, triangle slot s = l % 5
   const int j = lane / 5, s = lane % 5;
   const int jj = j < 4 ? j : 0;
-  const int my_valid = __shfl_sync(0xffffffffu, cj, jj) >= 0 && j < 4;
-  const int tt = __shfl_sync(0xffffffffu, ctt, jj);
-  const int e = __shfl_sync(0xffffffffu, ce, jj);
-  const int jrank = __shfl_sync(0xffffffffu, rank, jj);
-  const int c0 = __shfl_sync(0xffffffffu, cl[0], jj), c1 = __shfl_sync(0xffffffffu, cl[1], jj),
-            c2 = __shfl_sync(0xffffffffu, cl[2], jj);
+  int m0, m1, m2;
+  slot_cube(slot_ci, axis, jj, m0, m1, m2);
+  const int tt = (types4 >> (8 * jj)) & 0xFF;
+  const int e = cube_edge_of_slot(axis, jj >> 1, jj & 1);
+  // rank of the candidate cube by (sorted block, cube) key among the valid ones
+  int jrank = 0;
+  {
+    auto key = [&](int q) {
+      int a0, a1, a2;
+      slot_cube(slot_ci, axis, q, a0, a1, a2);
+      const int dx = a0 < 0 ? -1 : 0, dy = a1 < 0 ? -1 : 0, dz = a2 < 0 ? -1 : 0;
+      return (((dx + 1) * 4 + (dy + 1) * 2 + (dz + 1)) << 9) | ((a0 & 7) * 64 + (a1 & 7) * 8 + (a2 & 7));
+    };
+    const int mine = key(jj);
+#pragma unroll
+    for (int q = 0; q < 4; q++) jrank += ((cand >> q) & 1) && key(q) < mine;
+  }
+  const bool my_valid = j < 4 && ((cand >> jj) & 1) && s < c_tri_count[tt];
+  const unsigned long long packed = c_tri_packed[tt];
   int kpos = -1;
-  double fn[3] = {0.0, 0.0, 0.0};
-  if (my_valid && s < c_tri_count[tt]) {
-    const unsigned long long packed = c_tri_packed[tt];
+  if (my_valid) {
+#pragma unroll
     for (int q = 0; q < 3; q++)
       if ((int)((packed >> (4 * (3 * s + q))) & 0xF) == e) kpos = q;
-    if (kpos >= 0) {
-      double p[3][3];
-      for (int q = 0; q < 3; q++) {
-        const int eq = (int)((packed >> (4 * (3 * s + q))) & 0xF);
-        const int own = c_e_own[eq], ax = c_e_axis[eq];
-        const int ox = c0 + (own & 1), oy = c1 + ((own >> 1) & 1), oz = c2 + ((own >> 2) & 1);
-        const int ob = s_nbr[nbr_dir(ox < 0 ? -1 : ox >> 3, oy < 0 ? -1 : oy >> 3, oz < 0 ? -1 : oz >> 3)];
-        const int g[3] = {bc.x * kB + ox, bc.y * kB + oy, bc.z * kB + oz};
-        for (int d = 0; d < 3; d++) p[q][d] = __dmul_rn((double)g[d], S.cube_size);
-        p[q][ax] = S.vparam[(size_t)ob * kEV + ((ox & 7) * 64 + (oy & 7) * 8 + (oz & 7)) * 3 + ax];
-      }
-      const double a[3] = {p[1][0] - p[0][0], p[1][1] - p[0][1], p[1][2] - p[0][2]};
-      const double bb[3] = {p[2][0] - p[0][0], p[2][1] - p[0][1], p[2][2] - p[0][2]};
-      fn[0] = __dmul_rn(a[1], bb[2]) - __dmul_rn(a[2], bb[1]);
-      fn[1] = __dmul_rn(a[2], bb[0]) - __dmul_rn(a[0], bb[2]);
-      fn[2] = __dmul_rn(a[0], bb[1]) - __dmul_rn(a[1], bb[0]);
+  }
+  // owner block of each of the triangle's 3 vertices (shuffled from the row)
+  int obq[3], oxq[3], oyq[3], ozq[3], axq[3];
+#pragma unroll
+  for (int q = 0; q < 3; q++) {
+    const int eq = (int)((packed >> (4 * (3 * s + q))) & 0xF);
+    const int oa = (int)((kEdgeOwnAxis >> (5 * eq)) & 31);   // owner offset | axis << 3
+    const int own = oa & 7;
+    axq[q] = oa >> 3;
+    oxq[q] = m0 + (own & 1); oyq[q] = m1 + ((own >> 1) & 1); ozq[q] = m2 + ((own >> 2) & 1);
+    const int dir = nbr_dir(oxq[q] < 0 ? -1 : oxq[q] >> 3, oyq[q] < 0 ? -1 : oyq[q] >> 3,
+                            ozq[q] < 0 ? -1 : ozq[q] >> 3);
+    obq[q] = __shfl_sync(0xffffffffu, nbr_lane, dir);
+  }
+  double fn[3] = {0.0, 0.0, 0.0};
+  if (kpos >= 0) {
+    double p[3][3];
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+      const int ox = oxq[q], oy = oyq[q], oz = ozq[q], ax = axq[q];
+      const double pa = vparam[(size_t)obq[q] * kEV + ((ox & 7) * 64 + (oy & 7) * 8 + (oz & 7)) * 3 + ax];
+      const double gx = __dmul_rn((double)(bc.x * kB + ox), cube_size);
+      const double gy = __dmul_rn((double)(bc.y * kB + oy), cube_size);
+      const double gz = __dmul_rn((double)(bc.z * kB + oz), cube_size);
+      p[q][0] = ax == 0 ? pa : gx;
+      p[q][1] = ax == 1 ? pa : gy;
+      p[q][2] = ax == 2 ? pa : gz;
     }
+    const double a[3] = {p[1][0] - p[0][0], p[1][1] - p[0][1], p[1][2] - p[0][2]};
+    const double bb[3] = {p[2][0] - p[0][0], p[2][1] - p[0][1], p[2][2] - p[0][2]};
+    fn[0] = __dmul_rn(a[1], bb[2]) - __dmul_rn(a[2], bb[1]);
+    fn[1] = __dmul_rn(a[2], bb[0]) - __dmul_rn(a[0], bb[2]);
+    fn[2] = __dmul_rn(a[0], bb[1]) - __dmul_rn(a[1], bb[0]);
   }
   // ordered accumulation: k major, then cube rank, then triangle slot
   int mykey = kpos >= 0 ? (kpos * 4 + jrank) * 5 + s : (1 << 20);
@@ -772,44 +1013,35 @@ __device__ void fallback_normal_warp(const DevState &S, const uint8_t *ttile, co
       dst[0] = (-1.0 * acc[0]) / nrm;
       dst[1] = (-1.0 * acc[1]) / nrm;
       dst[2] = (-1.0 * acc[2]) / nrm;
-    } else if (dst[0] == 0.0 && dst[1] == 0.0 && dst[2] == 0.0) {
+    } else if (o0 == 0.0 && o1 == 0.0 && o2 == 0.0) {
       dst[2] = 1.0;
     }
   }
 }
 
-// Face-normal fallback worklist consumer: one warp per vertex; stages the
-// vertex's block neighbour row and the 9^3 type tile entries it needs through
-// shared memory, then runs the ordered warp accumulation.
-constexpr int kFT = 128;
-__global__ void __launch_bounds__(kFT) k_fallback(DevState S, const FrameDev F) {
-  cudaGridDependencySynchronize();   // PDL: wait for the previous kernel of the frame
-  if (halted(S)) return;
-  __shared__ int s_nbr[kFT / 32][27];
-  __shared__ uint8_t s_tt[kFT / 32][729];
-  __shared__ int4 s_coord[kFT / 32];
+struct FallbackArgs {   // what the consumer touches (passed by value: no DevState copy in local memory)
+  Counters *ctr;
+  const int4 *fallback;
+  const int32_t *nbr;
+  const int4 *bcoord;
+  const double *vparam;
+  double *vnrm;
+  double cube_size;
+};
+
+// The call's face-normal fallback worklist, after the grid barrier: entries
+// are spread statically over every warp of the grid, one warp per entry.
+__device__ __noinline__ void consume_fallbacks(const FallbackArgs S) {
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (blockDim.x >> 5) * gridDim.x;
   const int n = __ldcg(&S.ctr->nfallback);
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int f = blockIdx.x * (kFT / 32) + w; f < n; f += gridDim.x * (kFT / 32)) {
-    const int2 rec = S.fallback[f];
+  for (int f = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); f < n; f += nwarps) {
+    const int4 rec = __ldcg(S.fallback + f);
     const int b = rec.x, sl = rec.y;
-    if (lane < 27) s_nbr[w][lane] = lane == 13 ? b : __ldcg(S.nbr + (size_t)b * 27 + lane);
-    if (lane == 27) s_coord[w] = __ldcg(S.bcoord + b);
-    __syncwarp();
-    // only the types of the <= 4 cubes around the slot are read: stage those
-    const int ci = sl / 3, axis = sl % 3;
-    const int u = axis == 0 ? 1 : 0, ww = axis == 2 ? 1 : 2;
-    if (lane < 4) {
-      int l[3] = {ci >> 6, (ci >> 3) & 7, ci & 7};
-      l[u] -= lane >> 1;
-      l[ww] -= lane & 1;
-      const int nb = s_nbr[w][nbr_dir(l[0] >> 3, l[1] >> 3, l[2] >> 3)];
-      s_tt[w][((l[0] + 1) * 9 + (l[1] + 1)) * 9 + (l[2] + 1)] =
-          nb >= 0 ? S.tc[(size_t)nb * kNC + ((l[0] & 7) * 64 + (l[1] & 7) * 8 + (l[2] & 7))] : 0;
-    }
-    __syncwarp();
-    fallback_normal_warp(S, s_tt[w], s_nbr[w], s_coord[w], ci, axis, F.epoch, S.vnrm + 3 * ((size_t)b * kEV + sl));
-    __syncwarp();
+    const int nbr_lane = lane < 27 ? (lane == 13 ? b : __ldcg(S.nbr + (size_t)b * 27 + lane)) : -1;
+    const int4 bc = __ldcg(S.bcoord + b);
+    fallback_normal_warp(S.vparam, S.cube_size, nbr_lane, (uint32_t)rec.z, (uint32_t)rec.w, bc, sl / 3, sl % 3,
+                         S.vnrm + 3 * ((size_t)b * kEV + sl));
   }
 }
 
@@ -821,60 +1053,89 @@ __device__ __forceinline__ size_t sample_index(const int *s_nbr, int lx, int ly,
   return nb < 0 ? ~(size_t)0 : (size_t)nb * kNC + ((lx & 7) * 64 + (ly & 7) * 8 + (lz & 7));
 }
 
-// One CTA of 64 threads per listed (halo) block; small shared footprint so
-// every halo block of a frame is resident at once.  G_GC clears every
-// occupied slot that no cube references any more (the reference's refcount ==
-// 0 recycling: the 4 cubes around the edge are read from a staged 9^3 type
-// tile); the surviving vertices are compacted and G_NORMALS gathers each
-// vertex's 12-point stencil directly (mesher.py:400-439), the face-normal
-// fallback one warp per vertex.  G_COMMIT: the last CTA folds the per-call
+// Grid barrier (k_gc_normals is launched cooperatively: every CTA is
+// resident).  CTAs arrive on one per-call counter; the last arriver releases
+// 32 flags on separate lines with the call's epoch, and each CTA polls the
+// flag of its group -- polling spread over 32 lines instead of one.
+__device__ __forceinline__ void grid_barrier(int32_t *count, int32_t *flags, int stamp) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(count, 1) == (int)gridDim.x - 1) {
+#pragma unroll 1
+      for (int g = 0; g < 32; g++) *(volatile int32_t *)(flags + g * 32) = stamp;
+    } else {
+      volatile int32_t *f = flags + (blockIdx.x & 31) * 32;
+      while (*f != stamp) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// One CTA of 64 threads per listed (halo) block:
+//  * stage slot occupancy and the 9^3 type tile (cube locals -1..7);
+//  * G_GC clears every occupied slot that no cube references any more (the
+//    reference's refcount == 0 recycling, mesher.py:333-356: the 4 cubes
+//    around the edge from the type tile);
+//  * G_NORMALS computes each surviving vertex's central-difference normal
+//    from its 12-sample stencil, gathered directly (mesher.py:369-439);
+//    vertices whose stencil fails go to a global worklist, drained after a
+//    grid barrier by the whole grid, one warp per vertex (face-normal fallback,
+//    mesher.py:456-486).
+// The per-call counters are summed per CTA; G_COMMIT: the last CTA folds the
 // deltas into the pool counters.
-__global__ void __launch_bounds__(kGT, 16) k_gc_normals(DevState S, const FrameDev F,
+__global__ void __launch_bounds__(kGT, 12) k_gc_normals(DevState S, const FrameDev F,
                                                     const int32_t *__restrict__ list,
                                                     const int32_t *__restrict__ count_ptr,
                                                     int count_const, int mode) {
   cudaGridDependencySynchronize();   // PDL: wait for the previous kernel of the frame
-  if (halted(S)) return;
+  trace_at(S, TK_GC, 0);
   Counters *ctr = S.ctr;
-  const bool run = !(mode & G_REQUIRE_ITEMS) || __ldcg(&ctr->nitems_live) > 0;
-  __shared__ uint8_t tt[729];        // type_curr over cube locals -1..7
-  __shared__ uint32_t occ[kEV / 32]; // slot occupancy bits
-  __shared__ uint16_t s_vlist[kEV];
+  __shared__ int s_pro[5];
+  __shared__ SmemTables T;
+  // the halt flags, the live-item count, the list length and the first list
+  // entry: one thread, one round trip (the tables are staged meanwhile)
+  const int list_cap = count_ptr ? S.max_blocks : count_const;
+  read_prologue(S, s_pro, (mode & G_REQUIRE_ITEMS) ? &ctr->nitems_live : nullptr, count_ptr, nullptr,
+                (int)blockIdx.x < list_cap ? list + blockIdx.x : nullptr, &T);
+  if (s_pro[0]) return;
+  const int live_items = (mode & G_REQUIRE_ITEMS) ? s_pro[1] : 1;
+  const int n_listed = count_ptr ? s_pro[2] : count_const;
+  __shared__ uint8_t tt[729];          // type_curr over cube locals -1..7
+  __shared__ uint8_t s_inhalo[27];     // neighbour is a halo block of this call
+  __shared__ uint32_t occ[kEV / 32];   // slot occupancy bits
+  __shared__ uint16_t s_vlist[kEV];    // surviving slots
   __shared__ Resolved R;
   __shared__ int s_nv;
-  __shared__ long long red[3 * 32];
-  const int n = run ? (count_ptr ? __ldcg(count_ptr) : count_const) : 0;
+  __shared__ int red[3 * 32];
+  const int n = live_items > 0 ? n_listed : 0;
   const int t = threadIdx.x, lane = t & 31;
+  const bool normals = (mode & G_NORMALS) != 0;
   FrameDev Fr = F;
   Fr.scope_mode = 1;   // resolve as explicit items: no slab bits
   Fr.frustum_only = 0;
-  long long frees = 0, computed = 0, fallbacks = 0;
-  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+  int frees = 0, computed = 0, fallbacks = 0;
+  trace_at(S, TK_GC, 1);
+  int nth = 0;
+  for (int i = blockIdx.x; i < n; i += gridDim.x, nth++) {
+    trace_item(S, TK_GC, nth, 0);
     if (t < 32) {
-      const int b = __ldcg(list + i);
+      const int b = i == (int)blockIdx.x && s_pro[4] != -1 ? s_pro[4] : __ldcg(list + i);
       const ResolveRegs rr = resolve_load(S, Fr, b, i, 0);
       resolve_store(S, Fr, rr, b, i, n, 0, R);
     }
     if (t == 0) s_nv = 0;
     __syncthreads();
+    trace_item(S, TK_GC, nth, 1);
     if (R.mode <= 0) {
       __syncthreads();
       continue;
     }
     const int b = R.b;
-    // stage slot occupancy and the type tile (batched: all loads in flight)
-#pragma unroll
-    for (int j0 = 0; j0 < kEV / kGT; j0 += 8) {
-      int bv[8];
-#pragma unroll
-      for (int j = 0; j < 8; j++) bv[j] = S.vbirth[(size_t)b * kEV + (j0 + j) * kGT + t];
-#pragma unroll
-      for (int j = 0; j < 8; j++) {
-        const unsigned ball = __ballot_sync(0xffffffffu, bv[j] >= 0);
-        if (lane == 0) occ[((j0 + j) * kGT + t) >> 5] = ball;
-      }
-    }
+    // stage occupancy, types and halo flags (all loads in flight)
     {
+      const uint32_t ov = t < kEV / 32 ? __ldcg(S.vocc + (size_t)b * (kEV / 32) + t) : 0u;
       constexpr int kT = (729 + kGT - 1) / kGT;   // 12
       uint8_t tv[kT];
 #pragma unroll
@@ -882,16 +1143,25 @@ __global__ void __launch_bounds__(kGT, 16) k_gc_normals(DevState S, const FrameD
         const int q = t + j * kGT;
         tv[j] = 0;
         if (q < 729) {
-          const int e = __ldg(&g_type_tab[q]);
-          const int nb = R.nbr[e >> 9];
-          if (nb >= 0) tv[j] = S.tc[(size_t)nb * kNC + (e & 511)];
+          int dir, src;
+          type_tile_src(q, dir, src);
+          const int nb = R.nbr[dir];
+          if (nb >= 0) tv[j] = S.tc[(size_t)nb * kNC + src];
         }
       }
+      int hv = 0;
+      if (normals && t < 27) {
+        const int nb = R.nbr[t];
+        hv = nb >= 0 && __ldcg(S.stamp_halo + nb) == F.epoch;
+      }
+      if (t < kEV / 32) occ[t] = ov;
 #pragma unroll
       for (int j = 0; j < kT; j++)
         if (t + j * kGT < 729) tt[t + j * kGT] = tv[j];
+      if (t < 27) s_inhalo[t] = (uint8_t)hv;
     }
     __syncthreads();
+    trace_item(S, TK_GC, nth, 2);
     // GC: a slot survives iff a cube around its edge still has the edge in its mask
 #pragma unroll 1
     for (int j = 0; j < kNC / kGT; j++) {
@@ -910,12 +1180,13 @@ __global__ void __launch_bounds__(kGT, 16) k_gc_normals(DevState S, const FrameD
           const int p0 = ((x + 1) * 9 + (y + 1)) * 9 + (z + 1);
           bool ref = false;
 #pragma unroll
-          for (int j = 0; j < 4; j++) {
-            const int du = j >> 1, dw = j & 1;
-            ref = ref || ((c_edge_mask[tt[p0 - du * su - dw * sw]] >> cube_edge_of_slot(axis, du, dw)) & 1);
+          for (int q = 0; q < 4; q++) {
+            const int du = q >> 1, dw = q & 1;
+            ref = ref || ((T.edge_mask[tt[p0 - du * su - dw * sw]] >> cube_edge_of_slot(axis, du, dw)) & 1);
           }
           if (!ref) {
             S.vbirth[(size_t)b * kEV + sl] = -1;
+            atomicAnd(&occ[sl >> 5], ~(1u << (sl & 31)));
             frees += R.owned;
             continue;
           }
@@ -923,24 +1194,26 @@ __global__ void __launch_bounds__(kGT, 16) k_gc_normals(DevState S, const FrameD
         keep++;
         keep_axes |= 1u << axis;
       }
-      if (mode & G_NORMALS) {
+      if (normals) {
         int pos = smem_append(keep, &s_nv);
+#pragma unroll
         for (int axis = 0; axis < 3; axis++)
           if ((keep_axes >> axis) & 1) s_vlist[pos++] = (uint16_t)(c * 3 + axis);
       }
     }
-    if (mode & G_NORMALS) {
-      __syncthreads();
+    __syncthreads();
+    if ((mode & G_GC) && t < kEV / 32) S.vocc[(size_t)b * (kEV / 32) + t] = occ[t];   // frees applied
+    if (normals) {
       const int nv = s_nv;
       for (int p = t; p < nv; p += kGT) {
         const int sl = s_vlist[p];
-        const int ci = sl / 3, axis = sl - 3 * (sl / 3);
+        const int ci = sl / 3, axis = sl - 3 * ci;
         computed += R.owned;
         const int x0 = ci >> 6, y0 = (ci >> 3) & 7, z0 = ci & 7;
         const int x1 = x0 + (axis == 0), y1 = y0 + (axis == 1), z1 = z0 + (axis == 2);
-        // the 12 stencil points: c0 +- e_d, c1 +- e_d (c0 + e_axis = c1, c1 - e_axis = c0);
-        // all 24 loads are issued before any is used (absent neighbours read a
-        // dummy in-bounds sample and are masked out)
+        // the 12 stencil samples c0 +- e_d, c1 +- e_d (c1 = c0 + e_axis), all
+        // 24 loads in flight together; absent neighbours read a dummy in-bounds
+        // sample and invalidate the stencil
         double v0p[3], v0m[3], v1p[3], v1m[3];
         int w0p[3], w0m[3], w1p[3], w1m[3];
         bool inb = true;
@@ -978,15 +1251,38 @@ __global__ void __launch_bounds__(kGT, 16) k_gc_normals(DevState S, const FrameD
           double *dst = S.vnrm + 3 * ((size_t)b * kEV + sl);
           dst[0] = g[0] / nrm; dst[1] = g[1] / nrm; dst[2] = g[2] / nrm;
         } else {
-          fallbacks += R.owned;   // face-normal fallback: deferred to k_fallback (global worklist)
-          S.fallback[atomicAdd(&ctr->nfallback, 1)] = make_int2(b, sl);
+          // face-normal fallback: publish the slot with its 4 cube types and
+          // candidate mask (types, neighbour row and halo flags are staged here)
+          fallbacks += R.owned;
+          uint32_t types4 = 0, cand = 0;
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            int l0, l1, l2;
+            slot_cube(ci, axis, q, l0, l1, l2);
+            const uint32_t ty = tt[((l0 + 1) * 9 + (l1 + 1)) * 9 + (l2 + 1)];
+            const int dir = nbr_dir(l0 < 0 ? -1 : 0, l1 < 0 ? -1 : 0, l2 < 0 ? -1 : 0);
+            types4 |= ty << (8 * q);
+            if (((T.edge_mask[ty] >> cube_edge_of_slot(axis, q >> 1, q & 1)) & 1) && R.nbr[dir] >= 0 &&
+                s_inhalo[dir])
+              cand |= 1u << q;
+          }
+          S.fallback[atomicAdd(&ctr->nfallback, 1)] = make_int4(b, sl, (int)types4, (int)cand);
         }
       }
     }
+    trace_item(S, TK_GC, nth, 3);
     __syncthreads();   // R and the tiles are rewritten by the next item
   }
+  trace_count(S, TK_GC, nth);
+  trace_at(S, TK_GC, 28);
+  if (normals) {
+    grid_barrier(&ctr->gc_bar, S.bar_flags, F.bar_stamp);
+    trace_at(S, TK_GC, 29);
+    consume_fallbacks(FallbackArgs{S.ctr, S.fallback, S.nbr, S.bcoord, S.vparam, S.vnrm, S.cube_size});
+    trace_at(S, TK_GC, 30);
+  }
   {
-    long long vals[3] = {frees, computed, fallbacks};
+    int vals[3] = {frees, computed, fallbacks};
     int64_t *const dst[3] = {&ctr->v_frees, &ctr->normals, &ctr->fallbacks};
     block_add_counters<3>(vals, red, dst);
   }
@@ -1010,8 +1306,10 @@ __global__ void __launch_bounds__(kGT, 16) k_gc_normals(DevState S, const FrameD
       ctr->done_gc = 0;
     }
   }
+  trace_at(S, TK_GC, 31);
 }
 constexpr size_t kGcSmem = 0;
+
 
 
 

@@ -226,8 +226,14 @@ class Engine:
         _lib.check(_lib.load().vm_phase_times(self.store._h, _lib.ptr(ms), len(PHASES)))
         return dict(zip(PHASES, (float(v) for v in ms)))
 
+    def set_trace(self, buffer) -> None:
+        """Diagnostics: per-CTA kernel phase timestamps into a CUDA u64 tensor of
+        4 * 2048 * 32 entries (csrc/vm_device.cuh, kTraceCtas); None = off."""
+        ptr = None if buffer is None else buffer.data_ptr()
+        _lib.check(_lib.load().vm_set_trace(self.store._h, C.c_void_p(ptr)))
+
     def set_stream(self, stream_handle: int) -> None:
         _lib.check(_lib.load().vm_set_stream(self.store._h, C.c_void_p(stream_handle or None)))
 
 
-PHASES = ("depth_stats", "collect", "fuse_blocks", "retype_place", "gc_normals", "fallback")
+PHASES = ("depth_stats", "collect", "fuse_blocks", "retype_place", "gc_normals")

@@ -1,13 +1,11 @@
 """Incremental Marching Cubes phases (mirror of reference pkg/src/voxmesh/mesher.py).
 
-``extract_frame`` runs the device pipeline k_retype (+refine) -> k_place ->
-k_tri_release -> k_tri_alloc -> k_gc -> k_normals -> k_fallback
-(csrc/vm_kernels.cuh) over an explicit scope.  Strategies:
-
-* ``claim``     -- atomicCAS edge-slot claims (the paper's lock-based scheme);
-* ``partition`` -- 8 parity passes with plain slot stores (lock-free scheme);
-* ``serial``    -- accepted for API compatibility; runs the claim kernel (the
-  result is independent of the strategy, as the reference guarantees).
+``extract_frame`` runs the device pipeline k_retype_place (typing, +refine,
+implicit retriangulation, claim-based vertex placement) -> k_gc_normals (GC,
+gradient normals, face-normal fallback) (csrc/vm_kernels.cuh) over an explicit
+scope.  Strategies ``claim``, ``partition`` and ``serial`` are accepted; all run
+the claim kernel (atomicCAS on the edge slot), since the result is independent
+of the strategy, as the reference guarantees.
 
 ``meshing_scope`` / ``fused_halo`` are the reference's scope rules evaluated
 on the host with device existence lookups; ``Engine.fuse_frame`` computes the
