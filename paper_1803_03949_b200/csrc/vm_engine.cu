@@ -156,35 +156,15 @@ static void launch_pdl(void (*kern)(KArgs...), int grid, int block, cudaStream_t
   cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
-// k_gc_normals holds a grid barrier before its fallback phase, so it is always
-// launched cooperatively (every CTA co-resident, or the launch fails), with
-// programmatic dependent launch where the driver accepts the combination.
-template <typename... KArgs, typename... Args>
-static void launch_coop(bool pdl, void (*kern)(KArgs...), int grid, int block, cudaStream_t st, Args... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(block);
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 2 : 1;
-  if (cudaLaunchKernelEx(&cfg, kern, args...) != cudaSuccess && pdl) {
-    cudaGetLastError();
-    cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, kern, args...);
-  }
-}
-
-// k_gc_normals with a fresh grid-barrier stamp
+// k_gc_normals with a fresh grid-barrier stamp; its grid is the occupancy
+// limit, so every CTA is resident once the previous kernel drains
 static void launch_gc(vm_engine *e, bool pdl, const int32_t *list, const int32_t *count_ptr, int count_const,
                       int mode) {
   e->h_frame->bar_stamp = ++e->bar_seq;
-  launch_coop(pdl, k_gc_normals, e->grid_gc, kGT, e->stream, e->S, *e->h_frame, list, count_ptr, count_const, mode);
+  if (pdl)
+    launch_pdl(k_gc_normals, e->grid_gc, kGT, e->stream, e->S, *e->h_frame, list, count_ptr, count_const, mode);
+  else
+    k_gc_normals<<<e->grid_gc, kGT, 0, e->stream>>>(e->S, *e->h_frame, list, count_ptr, count_const, mode);
 }
 
 static int check_launch() {
@@ -237,6 +217,7 @@ static int error_from_counters(vm_engine *e) {
         return set_err(VM_ERR_CONSISTENCY, "edge owner block absent during placement (cube %lld, %lld, %lld)",
                        (long long)c.err_info[1], (long long)c.err_info[2], (long long)c.err_info[3]);
       case 40: return set_err(VM_ERR_CONSISTENCY, "triangle references a vertex bound to no edge");
+      case 50: return set_err(VM_ERR_CUDA, "k_gc_normals grid barrier timed out (CTAs not co-resident)");
       default: return set_err(VM_ERR_CONSISTENCY, "consistency error %lld", (long long)c.err_info[0]);
     }
   }

@@ -582,7 +582,7 @@ __device__ __forceinline__ void resolve_store(const DevState &S, const FrameDev 
   }
 }
 
-constexpr int kNT = 128;   // threads per CTA of the per-block meshing kernels (4 cubes each)
+constexpr int kNT = 64;   // threads per CTA of k_retype_place (one tile column each)
 constexpr int kTileSlots = 729 * 3;   // edge slots owned by the 9^3 tile points (3 axes each)
 
 
@@ -629,7 +629,7 @@ __device__ __forceinline__ uint32_t corner_bytes4(const uint32_t (&w)[4], int sh
 //    in a shared-memory bitmap (all requesters of a slot write identical bits),
 //    then each is claimed (atomicCAS on its birth word -- exactly one
 //    allocation per edge) and its coordinate written.
-__global__ void __launch_bounds__(kNT, 8) k_retype_place(DevState S, const FrameDev F) {
+__global__ void __launch_bounds__(kNT, 14) k_retype_place(DevState S, const FrameDev F) {
   cudaGridDependencySynchronize();   // PDL: wait for the previous kernel of the frame
   trace_at(S, TK_RETYPE, 0);
   __shared__ int s_pro[5];
@@ -679,18 +679,19 @@ __global__ void __launch_bounds__(kNT, 8) k_retype_place(DevState S, const Frame
     if (t == 0) live++;
     {
       // batched gathers: all loads in flight before any shared-memory store
-      double ov[kNC / kNT], xv[2];
-      int ow[kNC / kNT], xw[2], xp[2];
-      uint4 tcv = make_uint4(0, 0, 0, 0), tpv = make_uint4(0, 0, 0, 0);
+      constexpr int kOwn = kNC / kNT, kExt = (217 + kNT - 1) / kNT;
+      double ov[kOwn], xv[kExt];
+      int ow[kOwn], xw[kExt], xp[kExt];
+      uint4 tcv = make_uint4(0, 0, 0, 0);
 #pragma unroll
-      for (int j = 0; j < kNC / kNT; j++) {
+      for (int j = 0; j < kOwn; j++) {
         ov[j] = S.tsdf[(size_t)b * kNC + t + j * kNT];
         ow[j] = S.weight[(size_t)b * kNC + t + j * kNT];
       }
-      if (t < 32) tcv = reinterpret_cast<const uint4 *>(S.tc + (size_t)b * kNC)[t];
-      else if (t < 64) tpv = reinterpret_cast<const uint4 *>(S.tp + (size_t)b * kNC)[t - 32];
+      tcv = t < 32 ? reinterpret_cast<const uint4 *>(S.tc + (size_t)b * kNC)[t]
+                   : reinterpret_cast<const uint4 *>(S.tp + (size_t)b * kNC)[t - 32];
 #pragma unroll
-      for (int j = 0; j < 2; j++) {
+      for (int j = 0; j < kExt; j++) {
         const int q = t + j * kNT;
         xv[j] = 0.0;
         xw[j] = 0;
@@ -708,7 +709,7 @@ __global__ void __launch_bounds__(kNT, 8) k_retype_place(DevState S, const Frame
       // own samples: lanes 8g..8g+7 hold z = 0..7 of one column
       const int g8 = (lane >> 3) * 8;
 #pragma unroll
-      for (int j = 0; j < kNC / kNT; j++) {
+      for (int j = 0; j < kOwn; j++) {
         const int c = t + j * kNT;
         const int col = (c >> 6) * 9 + ((c >> 3) & 7);
         tile[col * 9 + (c & 7)] = ov[j];
@@ -718,12 +719,11 @@ __global__ void __launch_bounds__(kNT, 8) k_retype_place(DevState S, const Frame
         if ((lane & 7) == 0)
           s_col[col] = ((bs >> g8) & 0xFFu) | (((bv >> g8) & 0xFFu) << 9) | (((bm >> g8) & 0xFFu) << 18);
       }
-      if (t < 32) reinterpret_cast<uint4 *>(s_tc)[t] = tcv;
-      else if (t < 64) reinterpret_cast<uint4 *>(s_tp)[t - 32] = tpv;
+      reinterpret_cast<uint4 *>(t < 32 ? s_tc : s_tp)[t & 31] = tcv;
       // plus layer: q < 128 are the x = 8 and y = 8 faces (z = 0..7 runs of a
       // column), q = 192..199 the column (8, 8); the rest are z = 8 points
 #pragma unroll
-      for (int j = 0; j < 2; j++) {
+      for (int j = 0; j < kExt; j++) {
         const int q = t + j * kNT;
         const bool run = q < 128 || (q >= 192 && q < 200);
         const unsigned bs = __ballot_sync(0xffffffffu, xv[j] < 0.0);
@@ -743,11 +743,11 @@ __global__ void __launch_bounds__(kNT, 8) k_retype_place(DevState S, const Frame
     }
     __syncthreads();
     trace_item(S, TK_RETYPE, nth, 2);
-    // typing: thread t -> column (x, y) = t >> 1 (x = col >> 3), cubes z0..z0+3.
-    // The 4 cubes' corner bytes are formed bit-sliced: byte j of a plane word
-    // holds the 8 corner bits of cube z0 + j.
+    // typing: thread t -> tile column (x, y) = (t >> 3, t & 7), its 8 cubes.
+    // The corner bytes of 4 cubes at a time are formed bit-sliced: byte j of a
+    // plane word holds the 8 corner bits of cube z0 + j.
     {
-      const int x = t >> 4, y = (t >> 1) & 7, z0 = (t & 1) * 4;
+      const int x = t >> 3, y = t & 7;
       uint32_t w[4];
       const int cols[4] = {x * 9 + y, (x + 1) * 9 + y, (x + 1) * 9 + y + 1, x * 9 + y + 1};
 #pragma unroll
@@ -755,56 +755,65 @@ __global__ void __launch_bounds__(kNT, 8) k_retype_place(DevState S, const Frame
         const uint32_t tp8 = s_top[cols[k]];
         w[k] = s_col[cols[k]] | ((tp8 & 1u) << 8) | (((tp8 >> 1) & 1u) << 17) | (((tp8 >> 2) & 1u) << 26);
       }
-      const uint32_t sgn = corner_bytes4(w, z0), val = corner_bytes4(w, 9 + z0);
-      const uint32_t sml = do_refine ? corner_bytes4(w, 18 + z0) : 0u;
-      const int c0 = (x * 8 + y) * 8 + z0;
-      const uint32_t old_tc = reinterpret_cast<const uint32_t *>(s_tc)[c0 >> 2];
-      const uint32_t old_tp = reinterpret_cast<const uint32_t *>(s_tp)[c0 >> 2];
-      uint32_t new_tc = old_tc, new_tp = old_tp;
       uint32_t cxa = 0, cxb = 0, cya = 0, cyb = 0, cza = 0, czb = 0, czc = 0, czd = 0;
 #pragma unroll
-      for (int k = 0; k < 4; k++) {
-        const int z = z0 + k;
-        const int c = c0 + k;
-        bool sel;
-        if (mode == 1) sel = true;
-        else if (mode == 2) sel = (R.slab & c_slab_sel[((x == 7) << 2) | ((y == 7) << 1) | (z == 7)]) != 0;
-        else sel = (S.item_mask[(size_t)R.item * 16 + (c >> 5)] >> (c & 31)) & 1;
-        sel = sel && ((val >> (8 * k)) & 0xFFu) == 0xFFu;   // all 8 weights > 0
-        if (!sel) continue;
-        const unsigned bits = (sgn >> (8 * k)) & 0xFFu;
-        const unsigned tp = (old_tc >> (8 * k)) & 0xFFu;
-        unsigned tc = bits;
-        if (do_refine) {
-          bool ch;
-          tc = refine_type(bits, tp, (sml >> (8 * k)) & 0xFFu, &ch);
-          refined += ch && own;
+      for (int half = 0; half < 2; half++) {
+        const int z0 = 4 * half;
+        const uint32_t sgn = corner_bytes4(w, z0), val = corner_bytes4(w, 9 + z0);
+        const uint32_t sml = do_refine ? corner_bytes4(w, 18 + z0) : 0u;
+        const int c0 = (x * 8 + y) * 8 + z0;
+        const uint32_t old_tc = reinterpret_cast<const uint32_t *>(s_tc)[c0 >> 2];
+        const uint32_t old_tp = reinterpret_cast<const uint32_t *>(s_tp)[c0 >> 2];
+        uint32_t new_tc = old_tc, new_tp = old_tp;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+          const int z = z0 + k;
+          const int c = c0 + k;
+          bool sel;
+          if (mode == 1) sel = true;
+          else if (mode == 2) sel = (R.slab & c_slab_sel[((x == 7) << 2) | ((y == 7) << 1) | (z == 7)]) != 0;
+          else sel = (S.item_mask[(size_t)R.item * 16 + (c >> 5)] >> (c & 31)) & 1;
+          sel = sel && ((val >> (8 * k)) & 0xFFu) == 0xFFu;   // all 8 weights > 0
+          if (!sel) continue;
+          const unsigned bits = (sgn >> (8 * k)) & 0xFFu;
+          const unsigned tp = (old_tc >> (8 * k)) & 0xFFu;
+          unsigned tc = bits;
+          if (do_refine) {
+            bool ch;
+            tc = refine_type(bits, tp, (sml >> (8 * k)) & 0xFFu, &ch);
+            refined += ch && own;
+          }
+          new_tp = (new_tp & ~(0xFFu << (8 * k))) | (tp << (8 * k));
+          new_tc = (new_tc & ~(0xFFu << (8 * k))) | (tc << (8 * k));
+          if (tc != tp && own) {
+            changed++;
+            const int nold = T.tri_count[tp], nnew = T.tri_count[tc];
+            t_rel += nold;
+            t_new += nnew;
+            irr += (nnew > 0 && !is_regular_type(tc)) - (nold > 0 && !is_regular_type(tp));
+          }
+          const unsigned mask = T.edge_mask[tc];
+          if (mask && own) {
+            active++;
+            placements += __popc(mask);
+          }
+          // request the mask edges' slots: per axis, the owner point's column
+          // word (bit = owner z), edge geometry of mc_tables.py:44-64
+          const unsigned b0 = 1u << z, b1 = 2u << z;
+          cxa |= (mask & 1u ? b0 : 0u) | (mask & 16u ? b1 : 0u);            // e0, e4: (x, y)
+          cxb |= (mask & 4u ? b0 : 0u) | (mask & 64u ? b1 : 0u);            // e2, e6: (x, y+1)
+          cya |= (mask & 2u ? b0 : 0u) | (mask & 32u ? b1 : 0u);            // e1, e5: (x+1, y)
+          cyb |= (mask & 8u ? b0 : 0u) | (mask & 128u ? b1 : 0u);           // e3, e7: (x, y)
+          cza |= mask & 256u ? b0 : 0u;                                      // e8: (x, y)
+          czb |= mask & 512u ? b0 : 0u;                                      // e9: (x+1, y)
+          czc |= mask & 1024u ? b0 : 0u;                                     // e10: (x+1, y+1)
+          czd |= mask & 2048u ? b0 : 0u;                                     // e11: (x, y+1)
         }
-        new_tp = (new_tp & ~(0xFFu << (8 * k))) | (tp << (8 * k));
-        new_tc = (new_tc & ~(0xFFu << (8 * k))) | (tc << (8 * k));
-        if (tc != tp && own) {
-          changed++;
-          const int nold = T.tri_count[tp], nnew = T.tri_count[tc];
-          t_rel += nold;
-          t_new += nnew;
-          irr += (nnew > 0 && !is_regular_type(tc)) - (nold > 0 && !is_regular_type(tp));
+        if (new_tc != old_tc || new_tp != old_tp) {   // 4 cubes per 32-bit store
+          const size_t q4 = ((size_t)b * kNC + c0) >> 2;
+          reinterpret_cast<uint32_t *>(S.tp)[q4] = new_tp;
+          reinterpret_cast<uint32_t *>(S.tc)[q4] = new_tc;
         }
-        const unsigned mask = T.edge_mask[tc];
-        if (mask && own) {
-          active++;
-          placements += __popc(mask);
-        }
-        // request the mask edges' slots: per axis, the owner point's column
-        // word (bit = owner z), edge geometry of mc_tables.py:44-64
-        const unsigned b0 = 1u << z, b1 = 2u << z;
-        cxa |= (mask & 1u ? b0 : 0u) | (mask & 16u ? b1 : 0u);            // e0, e4: (x, y)
-        cxb |= (mask & 4u ? b0 : 0u) | (mask & 64u ? b1 : 0u);            // e2, e6: (x, y+1)
-        cya |= (mask & 2u ? b0 : 0u) | (mask & 32u ? b1 : 0u);            // e1, e5: (x+1, y)
-        cyb |= (mask & 8u ? b0 : 0u) | (mask & 128u ? b1 : 0u);           // e3, e7: (x, y)
-        cza |= mask & 256u ? b0 : 0u;                                      // e8: (x, y)
-        czb |= mask & 512u ? b0 : 0u;                                      // e9: (x+1, y)
-        czc |= mask & 1024u ? b0 : 0u;                                     // e10: (x+1, y+1)
-        czd |= mask & 2048u ? b0 : 0u;                                     // e11: (x, y+1)
       }
       // one shared-memory OR per (axis, column) word this thread touched
       if (cxa) atomicOr(&s_claim[0 * 81 + cols[0]], cxa);
@@ -815,17 +824,12 @@ __global__ void __launch_bounds__(kNT, 8) k_retype_place(DevState S, const Frame
       if (czb) atomicOr(&s_claim[2 * 81 + cols[1]], czb);
       if (czc) atomicOr(&s_claim[2 * 81 + cols[2]], czc);
       if (czd) atomicOr(&s_claim[2 * 81 + cols[3]], czd);
-      if (new_tc != old_tc || new_tp != old_tp) {   // 4 cubes per 32-bit store
-        const size_t q4 = ((size_t)b * kNC + c0) >> 2;
-        reinterpret_cast<uint32_t *>(S.tp)[q4] = new_tp;
-        reinterpret_cast<uint32_t *>(S.tc)[q4] = new_tc;
-      }
     }
     __syncthreads();
     // compact the requested slots (each once, whichever cubes asked for it):
     // word a * 81 + col holds owner heights z of axis a in column col
 #pragma unroll
-    for (int r = 0; r < 2; r++) {
+    for (int r = 0; r < (3 * 81 + kNT - 1) / kNT; r++) {
       const int wi = t + r * kNT;
       const uint32_t word = wi < 3 * 81 ? s_claim[wi] : 0u;
       int pos = smem_append(__popc(word), &s_nplace);
@@ -834,29 +838,45 @@ __global__ void __launch_bounds__(kNT, 8) k_retype_place(DevState S, const Frame
     }
     __syncthreads();
     trace_item(S, TK_RETYPE, nth, 3);
+    // placement, 4 slots per thread in flight: coordinate store and claim
+    // (the first requester to set the slot's occupancy bit allocates)
     const int np = s_nplace;
-    for (int p = t; p < np; p += kNT) {
-      const int u = s_place[p];
-      const int pt = u / 3, axis = u - 3 * pt;
-      const int ox = pt / 81, oy = (pt / 9) % 9, oz = pt % 9;
-      const int owner = R.nbr[nbr_dir(ox >> 3, oy >> 3, oz >> 3)];
-      if (owner < 0) {
-        set_error(S, ERR_CONSISTENCY, 10, R.coord.x * kB + ox, R.coord.y * kB + oy, R.coord.z * kB + oz);
-        continue;
+    for (int p0 = 0; p0 < np; p0 += 4 * kNT) {
+      size_t slot[4];
+      uint32_t bit[4], old[4];
+      int owner[4];
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        const int p = p0 + j * kNT + t;
+        owner[j] = -1;
+        old[j] = ~0u;
+        bit[j] = 0;
+        slot[j] = 0;
+        if (p >= np) continue;
+        const int u = s_place[p];
+        const int pt = u / 3, axis = u - 3 * pt;
+        const int ox = pt / 81, oy = (pt / 9) % 9, oz = pt % 9;
+        owner[j] = R.nbr[nbr_dir(ox >> 3, oy >> 3, oz >> 3)];
+        if (owner[j] < 0) {
+          set_error(S, ERR_CONSISTENCY, 10, R.coord.x * kB + ox, R.coord.y * kB + oy, R.coord.z * kB + oz);
+          continue;
+        }
+        slot[j] = (size_t)owner[j] * kEV + (((ox & 7) * 64 + (oy & 7) * 8 + (oz & 7)) * 3 + axis);
+        // start corner = the owner point; end corner one step along the axis
+        const double d0 = tile[pt];
+        const double d1 = tile[pt + (axis == 0 ? 81 : axis == 1 ? 9 : 1)];
+        const double param = (d0 == d1) ? 0.5 : d0 / (d0 - d1);
+        const int ga = (axis == 0 ? R.coord.x * kB + ox : axis == 1 ? R.coord.y * kB + oy : R.coord.z * kB + oz);
+        S.vparam[slot[j]] = __dadd_rn(__dmul_rn((double)ga, l), __dmul_rn(param, l));
+        bit[j] = 1u << (slot[j] & 31);
+        old[j] = atomicOr(S.vocc + (slot[j] >> 5), bit[j]);
       }
-      const size_t slot = (size_t)owner * kEV + (((ox & 7) * 64 + (oy & 7) * 8 + (oz & 7)) * 3 + axis);
-      // start corner = the owner point; end corner one step along the axis
-      const double d0 = tile[pt];
-      const double d1 = tile[pt + (axis == 0 ? 81 : axis == 1 ? 9 : 1)];
-      const double param = (d0 == d1) ? 0.5 : d0 / (d0 - d1);
-      const int ga = (axis == 0 ? R.coord.x * kB + ox : axis == 1 ? R.coord.y * kB + oy : R.coord.z * kB + oz);
-      S.vparam[slot] = __dadd_rn(__dmul_rn((double)ga, l), __dmul_rn(param, l));
-      // claim: the first requester to set the slot's occupancy bit allocates
-      const uint32_t bit = 1u << (slot & 31);
-      if (!(atomicOr(S.vocc + (slot >> 5), bit) & bit)) {
-        allocs += (S.nranks <= 1 || S.bowned[owner]);   // counted by the slot's owning rank
-        S.vbirth[slot] = frame;
-        S.vnrm[3 * slot] = 0.0; S.vnrm[3 * slot + 1] = 0.0; S.vnrm[3 * slot + 2] = 0.0;
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        if (owner[j] < 0 || (old[j] & bit[j])) continue;
+        allocs += (S.nranks <= 1 || S.bowned[owner[j]]);   // counted by the slot's owning rank
+        S.vbirth[slot[j]] = frame;
+        S.vnrm[3 * slot[j]] = 0.0; S.vnrm[3 * slot[j] + 1] = 0.0; S.vnrm[3 * slot[j] + 2] = 0.0;
       }
     }
     __syncthreads();   // R, tile and the placement list are rewritten by the next item
@@ -869,7 +889,7 @@ __global__ void __launch_bounds__(kNT, 8) k_retype_place(DevState S, const Frame
                              &S.ctr->t_released, &S.ctr->t_allocated, &S.ctr->irr_delta, &S.ctr->refined};
     block_add_counters<8>(vals, red8, dst);
   }
-  if (t == 0 && live) atomicAdd(&S.ctr->nitems_live, (int)live);
+  if (t == 0 && live) S.ctr->nitems_live = 1;   // (a flag: some item was live this call)
   trace_at(S, TK_RETYPE, 31);
 }
 constexpr size_t kRetypeSmem = 0;
@@ -1045,7 +1065,24 @@ __device__ __noinline__ void consume_fallbacks(const FallbackArgs S) {
   }
 }
 
-constexpr int kGT = 64;   // threads per CTA of k_gc_normals
+constexpr int kGT = 32;   // threads per CTA of k_gc_normals (one warp per halo block)
+
+// cp.async global -> shared of 4 / 8 bytes, zero-filled when `valid` is false
+// (no register staging: the loads stay in flight while the warp goes on)
+__device__ __forceinline__ void cp_async4(void *dst, const void *src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(src), "r"(valid ? 4 : 0));
+}
+__device__ __forceinline__ void cp_async8(void *dst, const void *src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// type tile over cube locals -1..7: 81 columns (lx, ly) of 16 bytes, z = 0..7
+// at bytes 0..7 and z = -1 at byte 15 (the -z neighbour's z = 7, fetched as
+// the aligned word of its z = 4..7 into bytes 12..15)
+__device__ __forceinline__ int tt_idx(int lx, int ly, int lz) { return ((lx + 1) * 9 + (ly + 1)) * 16 + (lz & 15); }
 
 // tsdf / weight sample at block-local corner (lx, ly, lz) in [-1, 9]^3
 __device__ __forceinline__ size_t sample_index(const int *s_nbr, int lx, int ly, int lz) {
@@ -1053,24 +1090,38 @@ __device__ __forceinline__ size_t sample_index(const int *s_nbr, int lx, int ly,
   return nb < 0 ? ~(size_t)0 : (size_t)nb * kNC + ((lx & 7) * 64 + (ly & 7) * 8 + (lz & 7));
 }
 
-// Grid barrier (k_gc_normals is launched cooperatively: every CTA is
-// resident).  CTAs arrive on one per-call counter; the last arriver releases
-// 32 flags on separate lines with the call's epoch, and each CTA polls the
-// flag of its group -- polling spread over 32 lines instead of one.
-__device__ __forceinline__ void grid_barrier(int32_t *count, int32_t *flags, int stamp) {
+// Grid barrier.  k_gc_normals' grid is the occupancy limit (every CTA fits on
+// the GPU at once) and its CTAs never wait on later work, so all arrive.  CTAs
+// arrive on one per-call counter; the last arriver releases 32 flags on
+// separate lines with the launch's stamp, and each CTA polls its group's flag
+// (polling spread over 32 lines).  A wait far beyond any frame's duration
+// raises an error instead of spinning forever.
+__device__ __forceinline__ bool grid_barrier(const DevState &S, int32_t *count, int32_t *flags, int stamp) {
+  __shared__ int s_ok;
   __syncthreads();
   if (threadIdx.x == 0) {
+    int ok = 1;
     __threadfence();
     if (atomicAdd(count, 1) == (int)gridDim.x - 1) {
 #pragma unroll 1
       for (int g = 0; g < 32; g++) *(volatile int32_t *)(flags + g * 32) = stamp;
     } else {
       volatile int32_t *f = flags + (blockIdx.x & 31) * 32;
-      while (*f != stamp) __nanosleep(32);
+      long long spins = 0;
+      while (*f != stamp) {
+        __nanosleep(32);
+        if (++spins > (1LL << 25)) {   // > ~1 s
+          set_error(S, ERR_CONSISTENCY, 50);
+          ok = 0;
+          break;
+        }
+      }
     }
     __threadfence();
+    s_ok = ok;
   }
   __syncthreads();
+  return s_ok != 0;
 }
 
 // One CTA of 64 threads per listed (halo) block:
@@ -1085,7 +1136,7 @@ __device__ __forceinline__ void grid_barrier(int32_t *count, int32_t *flags, int
 //    mesher.py:456-486).
 // The per-call counters are summed per CTA; G_COMMIT: the last CTA folds the
 // deltas into the pool counters.
-__global__ void __launch_bounds__(kGT, 12) k_gc_normals(DevState S, const FrameDev F,
+__global__ void __launch_bounds__(kGT, 24) k_gc_normals(DevState S, const FrameDev F,
                                                     const int32_t *__restrict__ list,
                                                     const int32_t *__restrict__ count_ptr,
                                                     int count_const, int mode) {
@@ -1102,15 +1153,16 @@ __global__ void __launch_bounds__(kGT, 12) k_gc_normals(DevState S, const FrameD
   if (s_pro[0]) return;
   const int live_items = (mode & G_REQUIRE_ITEMS) ? s_pro[1] : 1;
   const int n_listed = count_ptr ? s_pro[2] : count_const;
-  __shared__ uint8_t tt[729];          // type_curr over cube locals -1..7
+  __shared__ __align__(16) uint8_t tt[81 * 16];   // type_curr over cube locals -1..7 (tt_idx)
   __shared__ uint8_t s_inhalo[27];     // neighbour is a halo block of this call
   __shared__ uint32_t occ[kEV / 32];   // slot occupancy bits
   __shared__ uint16_t s_vlist[kEV];    // surviving slots
+  __shared__ uint16_t s_fb[kEV];       // ... whose gradient failed
   __shared__ Resolved R;
-  __shared__ int s_nv;
+  __shared__ int s_nv, s_nfb;
   __shared__ int red[3 * 32];
   const int n = live_items > 0 ? n_listed : 0;
-  const int t = threadIdx.x, lane = t & 31;
+  const int t = threadIdx.x;
   const bool normals = (mode & G_NORMALS) != 0;
   FrameDev Fr = F;
   Fr.scope_mode = 1;   // resolve as explicit items: no slab bits
@@ -1125,7 +1177,7 @@ __global__ void __launch_bounds__(kGT, 12) k_gc_normals(DevState S, const FrameD
       const ResolveRegs rr = resolve_load(S, Fr, b, i, 0);
       resolve_store(S, Fr, rr, b, i, n, 0, R);
     }
-    if (t == 0) s_nv = 0;
+    if (t == 0) { s_nv = 0; s_nfb = 0; }
     __syncthreads();
     trace_item(S, TK_GC, nth, 1);
     if (R.mode <= 0) {
@@ -1135,18 +1187,17 @@ __global__ void __launch_bounds__(kGT, 12) k_gc_normals(DevState S, const FrameD
     const int b = R.b;
     // stage occupancy, types and halo flags (all loads in flight)
     {
-      const uint32_t ov = t < kEV / 32 ? __ldcg(S.vocc + (size_t)b * (kEV / 32) + t) : 0u;
-      constexpr int kT = (729 + kGT - 1) / kGT;   // 12
-      uint8_t tv[kT];
-#pragma unroll
-      for (int j = 0; j < kT; j++) {
-        const int q = t + j * kGT;
-        tv[j] = 0;
-        if (q < 729) {
-          int dir, src;
-          type_tile_src(q, dir, src);
-          const int nb = R.nbr[dir];
-          if (nb >= 0) tv[j] = S.tc[(size_t)nb * kNC + src];
+      for (int q = t; q < kEV / 32; q += kGT) cp_async4(&occ[q], S.vocc + (size_t)b * (kEV / 32) + q, true);
+      for (int q = t; q < 2 * 81; q += kGT) {   // per column: the z = 0..7 run, then z = -1
+        const int col = q >> 1, lx = col / 9 - 1, ly = col % 9 - 1;
+        const int dx = lx < 0 ? -1 : 0, dy = ly < 0 ? -1 : 0;
+        const size_t row = (size_t)((lx & 7) * 64 + (ly & 7) * 8);
+        if ((q & 1) == 0) {
+          const int nb = R.nbr[nbr_dir(dx, dy, 0)];
+          cp_async8(&tt[col * 16], S.tc + (size_t)(nb >= 0 ? nb : 0) * kNC + row, nb >= 0);
+        } else {
+          const int nb = R.nbr[nbr_dir(dx, dy, -1)];
+          cp_async4(&tt[col * 16 + 12], S.tc + (size_t)(nb >= 0 ? nb : 0) * kNC + row + 4, nb >= 0);
         }
       }
       int hv = 0;
@@ -1154,11 +1205,8 @@ __global__ void __launch_bounds__(kGT, 12) k_gc_normals(DevState S, const FrameD
         const int nb = R.nbr[t];
         hv = nb >= 0 && __ldcg(S.stamp_halo + nb) == F.epoch;
       }
-      if (t < kEV / 32) occ[t] = ov;
-#pragma unroll
-      for (int j = 0; j < kT; j++)
-        if (t + j * kGT < 729) tt[t + j * kGT] = tv[j];
       if (t < 27) s_inhalo[t] = (uint8_t)hv;
+      cp_async_wait_all();
     }
     __syncthreads();
     trace_item(S, TK_GC, nth, 2);
@@ -1166,7 +1214,6 @@ __global__ void __launch_bounds__(kGT, 12) k_gc_normals(DevState S, const FrameD
 #pragma unroll 1
     for (int j = 0; j < kNC / kGT; j++) {
       const int c = t + j * kGT;
-      const int x = c >> 6, y = (c >> 3) & 7, z = c & 7;
       int keep = 0;
       unsigned keep_axes = 0;
 #pragma unroll
@@ -1175,14 +1222,13 @@ __global__ void __launch_bounds__(kGT, 12) k_gc_normals(DevState S, const FrameD
         if (!((occ[sl >> 5] >> (sl & 31)) & 1)) continue;
         if (mode & G_GC) {
           // the 4 cubes around the edge: offsets -du along u, -dw along w
-          // (u, w = the two axes other than `axis`); tile strides 81, 9, 1
-          const int su = axis == 0 ? 9 : 81, sw = axis == 2 ? 9 : 1;
-          const int p0 = ((x + 1) * 9 + (y + 1)) * 9 + (z + 1);
+          // (u, w = the two axes other than `axis`)
           bool ref = false;
 #pragma unroll
           for (int q = 0; q < 4; q++) {
-            const int du = q >> 1, dw = q & 1;
-            ref = ref || ((T.edge_mask[tt[p0 - du * su - dw * sw]] >> cube_edge_of_slot(axis, du, dw)) & 1);
+            int l0, l1, l2;
+            slot_cube(c, axis, q, l0, l1, l2);
+            ref = ref || ((T.edge_mask[tt[tt_idx(l0, l1, l2)]] >> cube_edge_of_slot(axis, q >> 1, q & 1)) & 1);
           }
           if (!ref) {
             S.vbirth[(size_t)b * kEV + sl] = -1;
@@ -1202,7 +1248,8 @@ __global__ void __launch_bounds__(kGT, 12) k_gc_normals(DevState S, const FrameD
       }
     }
     __syncthreads();
-    if ((mode & G_GC) && t < kEV / 32) S.vocc[(size_t)b * (kEV / 32) + t] = occ[t];   // frees applied
+    if (mode & G_GC)   // frees applied
+      for (int q = t; q < kEV / 32; q += kGT) S.vocc[(size_t)b * (kEV / 32) + q] = occ[q];
     if (normals) {
       const int nv = s_nv;
       for (int p = t; p < nv; p += kGT) {
@@ -1251,23 +1298,30 @@ __global__ void __launch_bounds__(kGT, 12) k_gc_normals(DevState S, const FrameD
           double *dst = S.vnrm + 3 * ((size_t)b * kEV + sl);
           dst[0] = g[0] / nrm; dst[1] = g[1] / nrm; dst[2] = g[2] / nrm;
         } else {
-          // face-normal fallback: publish the slot with its 4 cube types and
-          // candidate mask (types, neighbour row and halo flags are staged here)
           fallbacks += R.owned;
-          uint32_t types4 = 0, cand = 0;
-#pragma unroll
-          for (int q = 0; q < 4; q++) {
-            int l0, l1, l2;
-            slot_cube(ci, axis, q, l0, l1, l2);
-            const uint32_t ty = tt[((l0 + 1) * 9 + (l1 + 1)) * 9 + (l2 + 1)];
-            const int dir = nbr_dir(l0 < 0 ? -1 : 0, l1 < 0 ? -1 : 0, l2 < 0 ? -1 : 0);
-            types4 |= ty << (8 * q);
-            if (((T.edge_mask[ty] >> cube_edge_of_slot(axis, q >> 1, q & 1)) & 1) && R.nbr[dir] >= 0 &&
-                s_inhalo[dir])
-              cand |= 1u << q;
-          }
-          S.fallback[atomicAdd(&ctr->nfallback, 1)] = make_int4(b, sl, (int)types4, (int)cand);
+          s_fb[atomicAdd(&s_nfb, 1)] = (uint16_t)sl;
         }
+      }
+      __syncthreads();
+      // face-normal fallback: publish each failed slot with its 4 cube types and
+      // candidate mask (types, neighbour row and halo flags are staged here)
+      const int nfb = s_nfb;
+      for (int p = t; p < nfb; p += kGT) {
+        const int sl = s_fb[p];
+        const int ci = sl / 3, axis = sl - 3 * ci;
+        uint32_t types4 = 0, cand = 0;
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          int l0, l1, l2;
+          slot_cube(ci, axis, q, l0, l1, l2);
+          const uint32_t ty = tt[tt_idx(l0, l1, l2)];
+          const int dir = nbr_dir(l0 < 0 ? -1 : 0, l1 < 0 ? -1 : 0, l2 < 0 ? -1 : 0);
+          types4 |= ty << (8 * q);
+          if (((T.edge_mask[ty] >> cube_edge_of_slot(axis, q >> 1, q & 1)) & 1) && R.nbr[dir] >= 0 &&
+              s_inhalo[dir])
+            cand |= 1u << q;
+        }
+        S.fallback[atomicAdd(&ctr->nfallback, 1)] = make_int4(b, sl, (int)types4, (int)cand);
       }
     }
     trace_item(S, TK_GC, nth, 3);
@@ -1276,9 +1330,9 @@ __global__ void __launch_bounds__(kGT, 12) k_gc_normals(DevState S, const FrameD
   trace_count(S, TK_GC, nth);
   trace_at(S, TK_GC, 28);
   if (normals) {
-    grid_barrier(&ctr->gc_bar, S.bar_flags, F.bar_stamp);
+    const bool ok = grid_barrier(S, &ctr->gc_bar, S.bar_flags, F.bar_stamp);
     trace_at(S, TK_GC, 29);
-    consume_fallbacks(FallbackArgs{S.ctr, S.fallback, S.nbr, S.bcoord, S.vparam, S.vnrm, S.cube_size});
+    if (ok) consume_fallbacks(FallbackArgs{S.ctr, S.fallback, S.nbr, S.bcoord, S.vparam, S.vnrm, S.cube_size});
     trace_at(S, TK_GC, 30);
   }
   {
