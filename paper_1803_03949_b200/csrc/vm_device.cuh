@@ -337,9 +337,13 @@ __device__ int alloc_block(const DevState &S, int x, int y, int z, int epoch) {
   if (idx >= S.block_cap) atomicOr(&S.ctr->need, NEED_BLOCKS);
   S.bcoord[idx] = make_int4(x, y, z, 0);
   S.stamp_new[idx] = epoch;
-  const bool own = block_owned(S, x, y, z);
-  S.bowned[idx] = own;
-  if (own) atomicAdd((unsigned long long *)&S.ctr->nblocks_owned, 1ull);
+  if (S.nranks > 1) {   // (single rank: every block is owned, nblocks_owned == nblocks)
+    const bool own = block_owned(S, x, y, z);
+    S.bowned[idx] = own;
+    if (own) atomicAdd((unsigned long long *)&S.ctr->nblocks_owned, 1ull);
+  } else {
+    S.bowned[idx] = 1;
+  }
   S.newlist[atomicAdd(&S.ctr->nnew, 1)] = idx;
   return idx;
 }

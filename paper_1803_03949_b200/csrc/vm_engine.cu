@@ -572,7 +572,7 @@ static void fill_stats(vm_engine *e, int64_t frame, vm_stats *out) {
   const Counters &c = *e->h_ctr;
   memset(out, 0, sizeof *out);
   out->frame = frame;
-  out->blocks_active = c.nblocks_owned;
+  out->blocks_active = e->S.nranks > 1 ? c.nblocks_owned : c.nblocks;
   out->vertices_live = c.v_live;
   out->triangles_live = c.t_live;
   out->vertices_allocated_total = c.v_count;
@@ -1017,8 +1017,8 @@ int vm_counters(vm_engine *e, vm_counter_set *out) {
   if (!e || !out) return set_err(VM_ERR_INPUT, "null argument");
   TRY(read_counters(e));
   const Counters &c = *e->h_ctr;
-  out->block_count = c.nblocks_owned;
-  out->block_allocations = c.nblocks_owned;
+  out->block_count = e->S.nranks > 1 ? c.nblocks_owned : c.nblocks;
+  out->block_allocations = out->block_count;
   out->vertex_count = c.v_count;
   out->vertex_free = c.v_count - c.v_live;
   out->vertex_recycled_total = c.v_recycled;

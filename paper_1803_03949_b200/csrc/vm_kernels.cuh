@@ -629,7 +629,7 @@ __device__ __forceinline__ uint32_t corner_bytes4(const uint32_t (&w)[4], int sh
 //    in a shared-memory bitmap (all requesters of a slot write identical bits),
 //    then each is claimed (atomicCAS on its birth word -- exactly one
 //    allocation per edge) and its coordinate written.
-__global__ void __launch_bounds__(kNT, 14) k_retype_place(DevState S, const FrameDev F) {
+__global__ void __launch_bounds__(kNT, 16) k_retype_place(DevState S, const FrameDev F) {
   cudaGridDependencySynchronize();   // PDL: wait for the previous kernel of the frame
   trace_at(S, TK_RETYPE, 0);
   __shared__ int s_pro[5];
@@ -649,7 +649,7 @@ __global__ void __launch_bounds__(kNT, 14) k_retype_place(DevState S, const Fram
   __shared__ uint32_t s_claim[3 * 81];   // requested slots: [axis][tile column], bit = owner z
   __shared__ uint16_t s_place[kTileSlots];
   __shared__ Resolved R;
-  __shared__ int red8[8 * 32];
+  __shared__ int red8[8 * 32];   // (block_add_counters indexes k * 32 + warp)
   __shared__ int s_nplace;
   const int t = threadIdx.x, lane = t & 31;
   const double l = S.cube_size;
