@@ -299,7 +299,9 @@ def run_gpu(args, spec, cfg, rank, world, local_rank):
         e2 = PartitionedEngine(RunConfig(strategy=args.strategy, **cfg, **caps), spec.intrinsics(),
                                tile_blocks=args.tile_blocks, device=dev)
     else:
-        e2 = Engine(RunConfig(strategy=args.strategy, **cfg, **caps), spec.intrinsics())
+        # pipelined submission (vm_fuse_frame_submit): the next frame's H2D copy
+        # overlaps this frame's kernels; every frame's StatsRow is still read back
+        e2 = Engine(RunConfig(strategy=args.strategy, **cfg, **caps), spec.intrinsics(), pipelined=True)
     for i in range(args.warmup):
         e2.fuse_frame(host_np[i], poses[i])
     torch.cuda.synchronize()

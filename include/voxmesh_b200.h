@@ -190,6 +190,20 @@ int vm_fuse_frame_enqueue(vm_engine *e, const double *depth, int32_t h, int32_t 
                           const vm_pose *pose, const vm_frame_config *cfg,
                           int64_t frame_index);
 int vm_fuse_frame_finish(vm_engine *e, vm_stats *out);
+/* Pipelined form of vm_fuse_frame (same results, frame for frame): submit
+ * starts this frame's host->device depth copy on a second stream, completes
+ * the previously submitted frame (host wait, arena resume), orders this
+ * frame's kernels after its copy and returns once the copy is done (the host
+ * buffer may be reused) while the kernels run.  The copy of frame t+1
+ * therefore overlaps the kernels of frame t.  vm_fuse_frame_result delivers
+ * the stats of the oldest submitted frame not yet delivered (completing it if
+ * needed); it must be called once per submitted frame, before the next
+ * submit.  An error of frame t is returned by the call that completes it.
+ * Every other entry point completes a pending submitted frame first. */
+int vm_fuse_frame_submit(vm_engine *e, const double *depth, int32_t h, int32_t w,
+                         int32_t depth_on_device, const vm_intrinsics *intr,
+                         const vm_pose *pose, const vm_frame_config *cfg, int64_t frame_index);
+int vm_fuse_frame_result(vm_engine *e, vm_stats *out);
 
 /* ---- phase-level API (tests / reference function mirrors) ------------ */
 /* fusion.collect_blocks (fusion.py:70-107): allocates the touched blocks and

@@ -81,6 +81,15 @@ struct vm_engine {
   int last_resumes = 0;
   int32_t bar_seq = 0;     // k_gc_normals grid-barrier stamps
   int frame_launches = 0;   // kernels launched by the pending / last frame
+  // pipelined submission (vm_fuse_frame_submit): the next frame's depth is
+  // copied on a second stream into the other slot while the pending frame runs
+  cudaStream_t copy_stream = nullptr;
+  double *d_slot[2] = {nullptr, nullptr};
+  size_t slot_cap = 0;
+  int slot = 0;
+  cudaEvent_t ev_copy[2] = {nullptr, nullptr};
+  vm_stats settled{};       // stats of the last settled, not yet delivered frame
+  int settled_valid = 0;
   // ray-norm bounds over the image, cached per (h, w, fx, fy, cx, cy)
   double norm_key[6] = {0, 0, 0, 0, 0, 0};
   double norm_lo = 0.0, norm_hi = 0.0;
@@ -88,6 +97,10 @@ struct vm_engine {
   double *d_rays = nullptr;   // ray tables of the cached intrinsics (k_norm_bounds)
   size_t rays_cap = 0;
 };
+
+extern "C" {
+static int settle(vm_engine *e);
+}
 
 // ------------------------------------------------------------ helpers
 template <typename T>
@@ -515,6 +528,12 @@ int vm_destroy(vm_engine *e) {
   if (e->h_frame) cudaFreeHost(e->h_frame);
   for (int i = 0; i < PH_COUNT; i++)
     if (e->ev[i]) cudaEventDestroy(e->ev[i]);
+  if (e->copy_stream) cudaStreamSynchronize(e->copy_stream);
+  for (int i = 0; i < 2; i++) {
+    if (e->d_slot[i]) cudaFree(e->d_slot[i]);
+    if (e->ev_copy[i]) cudaEventDestroy(e->ev_copy[i]);
+  }
+  if (e->copy_stream) cudaStreamDestroy(e->copy_stream);
   if (e->own_stream && e->stream) cudaStreamDestroy(e->stream);
   delete e;
   return VM_OK;
@@ -522,6 +541,7 @@ int vm_destroy(vm_engine *e) {
 
 int vm_set_stream(vm_engine *e, void *stream) {
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
+  TRY(settle(e));
   CK(cudaStreamSynchronize(e->stream));
   if (e->own_stream) CK(cudaStreamDestroy(e->stream));
   if (stream) {
@@ -550,6 +570,7 @@ int vm_set_profiling(vm_engine *e, int on) {
 // depth_stats, collect, fuse_blocks, retype_place, gc_normals
 int vm_phase_times(vm_engine *e, double *ms, int n) {
   if (!e || !ms) return set_err(VM_ERR_INPUT, "null argument");
+  TRY(settle(e));
   CK(cudaEventSynchronize(e->ev[PH_END]));
   for (int i = 0; i < n && i < PH_END; i++) {
     float f = 0.f;
@@ -562,6 +583,7 @@ int vm_phase_times(vm_engine *e, double *ms, int n) {
 
 int vm_reserve(vm_engine *e, int64_t blocks, int64_t vertices, int64_t triangles) {
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
+  TRY(settle(e));
   (void)vertices;
   (void)triangles;   // vertices live in edge slots, triangles are implicit
   if (blocks > e->S.block_cap) TRY(grow_blocks(e, std::min<int64_t>(blocks, e->S.max_blocks)));
@@ -711,11 +733,79 @@ int vm_fuse_frame(vm_engine *e, const double *depth, int32_t h, int32_t w, int32
   return vm_fuse_frame_finish(e, out);
 }
 
+// Complete a pending submitted frame (host wait, arena resume) and keep its
+// stats for vm_fuse_frame_result.  Every call that touches the engine's state
+// settles first, so a submitted frame is never observed half done.
+static int settle(vm_engine *e) {
+  if (!e->pending) return VM_OK;
+  e->pending = 0;
+  e->last_resumes = 0;
+  TRY(complete_with_resume(e, &e->last_resumes));
+  fill_stats(e, e->pending_frame, &e->settled);
+  e->settled_valid = 1;
+  return VM_OK;
+}
+
+int vm_fuse_frame_submit(vm_engine *e, const double *depth, int32_t h, int32_t w, int32_t depth_on_device,
+                         const vm_intrinsics *intr, const vm_pose *pose, const vm_frame_config *cfg,
+                         int64_t frame_index) {
+  if (!e || !intr || !pose || !cfg) return set_err(VM_ERR_INPUT, "null argument");
+  if (!depth || h <= 0 || w <= 0) return set_err(VM_ERR_INPUT, "depth must be a non-empty (H, W) array");
+  if (e->settled_valid && e->pending)   // (at most one undelivered result)
+    return set_err(VM_ERR_INPUT, "the previous frame's result was not taken");
+  const double *dd = depth;
+  int sl = -1;
+  if (!depth_on_device) {
+    // 1. this frame's depth goes up on the copy stream, into the slot the
+    //    pending frame does not read (the frame before it has settled)
+    const size_t bytes = (size_t)h * w * sizeof(double);
+    if (!e->copy_stream) {
+      CK(cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking));
+      for (int i = 0; i < 2; i++) CK(cudaEventCreateWithFlags(&e->ev_copy[i], cudaEventDisableTiming));
+    }
+    if (bytes > e->slot_cap) {
+      TRY(settle(e));   // (rare) reallocation: nothing may be reading the slots
+      CK(cudaStreamSynchronize(e->copy_stream));
+      for (int i = 0; i < 2; i++) {
+        if (e->d_slot[i]) CK(cudaFree(e->d_slot[i]));
+        CK(cudaMalloc((void **)&e->d_slot[i], bytes));
+      }
+      e->slot_cap = bytes;
+    }
+    sl = e->slot ^ 1;
+    CK(cudaMemcpyAsync(e->d_slot[sl], depth, bytes, cudaMemcpyHostToDevice, e->copy_stream));
+    CK(cudaEventRecord(e->ev_copy[sl], e->copy_stream));
+    dd = e->d_slot[sl];
+  }
+  // 2. the previous frame completes (its stats are kept for vm_fuse_frame_result)
+  TRY(settle(e));
+  // 3. this frame's kernels, ordered after its copy
+  if (sl >= 0) CK(cudaStreamWaitEvent(e->stream, e->ev_copy[sl], 0));
+  TRY(vm_fuse_frame_enqueue(e, dd, h, w, 1, intr, pose, cfg, frame_index));
+  if (sl >= 0) {
+    e->slot = sl;
+    CK(cudaEventSynchronize(e->ev_copy[sl]));   // the caller may reuse its buffer on return
+  }
+  return VM_OK;
+}
+
+int vm_fuse_frame_result(vm_engine *e, vm_stats *out) {
+  if (!e) return set_err(VM_ERR_INPUT, "null engine");
+  if (!e->settled_valid) {
+    if (!e->pending) return set_err(VM_ERR_INPUT, "no frame submitted");
+    TRY(settle(e));
+  }
+  if (out) *out = e->settled;
+  e->settled_valid = 0;
+  return VM_OK;
+}
+
 // ---- phase API ------------------------------------------------------------
 int vm_collect(vm_engine *e, const double *depth, int32_t h, int32_t w, int32_t depth_on_device,
                const vm_intrinsics *intr, const vm_pose *pose, double trunc, double max_range,
                int64_t *n_out) {
   if (!e || !intr || !pose) return set_err(VM_ERR_INPUT, "null argument");
+  TRY(settle(e));
   const double *dd;
   TRY(stage_depth(e, depth, h, w, depth_on_device, &dd));
   fill_frame_host(e, dd, h, w, intr, pose);
@@ -737,6 +827,7 @@ int vm_collect(vm_engine *e, const double *depth, int32_t h, int32_t w, int32_t 
 
 int vm_get_collected(vm_engine *e, int32_t *coords_out, int64_t n) {
   if (!e || (!coords_out && n)) return set_err(VM_ERR_INPUT, "null argument");
+  TRY(settle(e));
   if (n == 0) return VM_OK;
   std::vector<int32_t> idx(n);
   CK(cudaMemcpyAsync(idx.data(), e->S.scope, (size_t)n * sizeof(int32_t), cudaMemcpyDeviceToHost, e->stream));
@@ -756,6 +847,7 @@ int vm_integrate(vm_engine *e, const int32_t *coords, int64_t n, const double *d
                  int32_t depth_on_device, const vm_intrinsics *intr, const vm_pose *pose, double trunc,
                  double max_range, int64_t weight_cap) {
   if (!e || !intr || !pose) return set_err(VM_ERR_INPUT, "null argument");
+  TRY(settle(e));
   const double *dd;
   TRY(stage_depth(e, depth, h, w, depth_on_device, &dd));
   fill_frame_host(e, dd, h, w, intr, pose);
@@ -796,6 +888,7 @@ int vm_integrate(vm_engine *e, const int32_t *coords, int64_t n, const double *d
 int vm_scope_halo(vm_engine *e, int64_t *n_scope, int32_t *scope_coords, uint8_t *scope_masks,
                   int64_t *n_halo, int32_t *halo_coords) {
   if (!e || !n_scope || !n_halo) return set_err(VM_ERR_INPUT, "null argument");
+  TRY(settle(e));
   CK(cudaMemsetAsync(&e->S.ctr->nslab, 0, sizeof(int32_t), e->stream));
   CK(cudaMemsetAsync(&e->S.ctr->nhalo, 0, sizeof(int32_t), e->stream));
   k_fuse_blocks<<<grid_blocks(e), kFB, 0, e->stream>>>(e->S, *e->h_frame, e->S.scope,
@@ -859,6 +952,7 @@ int vm_extract(vm_engine *e, const int32_t *scope_coords, const uint8_t *scope_m
                const int32_t *halo_coords, int64_t n_halo, int64_t frame_index, int32_t strategy,
                int32_t refine, double epsilon, int64_t *out2) {
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
+  TRY(settle(e));
   if (strategy < 0 || strategy > 2) return set_err(VM_ERR_VALUE, "unknown strategy %d", strategy);
   if (out2) { out2[0] = 0; out2[1] = 0; }
   if (n_scope <= 0) return VM_OK;   // mesher.py:564-565
@@ -907,6 +1001,7 @@ int vm_extract(vm_engine *e, const int32_t *scope_coords, const uint8_t *scope_m
 
 int vm_garbage_collect(vm_engine *e, const int32_t *coords, int64_t n, int64_t *freed) {
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
+  TRY(settle(e));
   TRY(reset_call_counters(e));
   int32_t *di = nullptr;
   if (n > 0) TRY(map_coords(e, coords, n, &di, nullptr, 0, false));
@@ -920,6 +1015,7 @@ int vm_garbage_collect(vm_engine *e, const int32_t *coords, int64_t n, int64_t *
 
 int vm_compute_normals(vm_engine *e, const int32_t *coords, int64_t n) {
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
+  TRY(settle(e));
   TRY(reset_call_counters(e));
   if (n <= 0) return VM_OK;
   e->h_frame->epoch = ++e->epoch;
@@ -934,6 +1030,7 @@ int vm_compute_normals(vm_engine *e, const int32_t *coords, int64_t n) {
 int vm_refine_eval(vm_engine *e, const uint8_t *t_curr, const uint8_t *t_prev, const double *corners,
                    int64_t n, double epsilon, int32_t *out) {
   if (!e || !t_curr || !t_prev || !corners || !out) return set_err(VM_ERR_INPUT, "null argument");
+  TRY(settle(e));
   if (n <= 0) return VM_OK;
   void *buf;
   const size_t o1 = ((size_t)n + 255) & ~(size_t)255, o2 = o1 * 2, o3 = o2 + (size_t)n * 64;
@@ -954,6 +1051,7 @@ int vm_refine_eval(vm_engine *e, const uint8_t *t_curr, const uint8_t *t_prev, c
 int vm_block_in_frustum(vm_engine *e, const int32_t *coords, int64_t n, const vm_pose *pose,
                         const vm_intrinsics *intr, uint8_t *out) {
   if (!e || !coords || !pose || !intr || !out) return set_err(VM_ERR_INPUT, "null argument");
+  TRY(settle(e));
   if (n <= 0) return VM_OK;
   fill_frame_host(e, nullptr, 0, 0, intr, pose);
   void *buf;
@@ -971,6 +1069,7 @@ int vm_block_in_frustum(vm_engine *e, const int32_t *coords, int64_t n, const vm
 // ---- store access -----------------------------------------------------------
 int vm_set_blocks(vm_engine *e, const int32_t *coords, int64_t n, const double *tsdf, const int32_t *weight) {
   if (!e || (!coords && n)) return set_err(VM_ERR_INPUT, "null argument");
+  TRY(settle(e));
   if (n <= 0) return VM_OK;
   TRY(reset_call_counters(e));
   int32_t *di;
@@ -1003,6 +1102,7 @@ int vm_set_blocks(vm_engine *e, const int32_t *coords, int64_t n, const double *
 
 int vm_lookup(vm_engine *e, const int32_t *coords, int64_t n, uint8_t *out) {
   if (!e || ((!coords || !out) && n)) return set_err(VM_ERR_INPUT, "null argument");
+  TRY(settle(e));
   if (n <= 0) return VM_OK;
   int32_t *di;
   TRY(map_coords(e, coords, n, &di, nullptr, 0, false));
@@ -1015,6 +1115,7 @@ int vm_lookup(vm_engine *e, const int32_t *coords, int64_t n, uint8_t *out) {
 
 int vm_counters(vm_engine *e, vm_counter_set *out) {
   if (!e || !out) return set_err(VM_ERR_INPUT, "null argument");
+  TRY(settle(e));
   TRY(read_counters(e));
   const Counters &c = *e->h_ctr;
   out->block_count = e->S.nranks > 1 ? c.nblocks_owned : c.nblocks;
@@ -1036,6 +1137,7 @@ int vm_counters(vm_engine *e, vm_counter_set *out) {
 int vm_snapshot_blocks(vm_engine *e, int64_t n, int32_t *coords, double *tsdf, int32_t *weight, uint8_t *tp,
                        uint8_t *tc, int32_t *ev, int32_t *tri) {
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
+  TRY(settle(e));
   TRY(read_counters(e));
   if (n != e->h_ctr->nblocks)
     return set_err(VM_ERR_INPUT, "snapshot size %lld != block count %d", (long long)n, e->h_ctr->nblocks);
@@ -1067,6 +1169,7 @@ int vm_snapshot_blocks(vm_engine *e, int64_t n, int32_t *coords, double *tsdf, i
 int vm_snapshot_vertices(vm_engine *e, int64_t n, double *pos, double *nrm, int32_t *ref, int32_t *birth,
                          uint8_t *alive, int32_t *free_stack) {
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
+  TRY(settle(e));
   TRY(read_counters(e));
   const int64_t count = e->h_ctr->v_count, live = e->h_ctr->v_live;
   if (n != count) return set_err(VM_ERR_INPUT, "snapshot size mismatch");
@@ -1113,6 +1216,7 @@ int vm_snapshot_vertices(vm_engine *e, int64_t n, double *pos, double *nrm, int3
 
 int vm_snapshot_triangles(vm_engine *e, int64_t n, int32_t *verts, uint8_t *alive, int32_t *free_stack) {
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
+  TRY(settle(e));
   TRY(read_counters(e));
   const int64_t count = e->h_ctr->t_count, live = e->h_ctr->t_live;
   if (n != count) return set_err(VM_ERR_INPUT, "snapshot size mismatch");
@@ -1132,6 +1236,7 @@ int vm_snapshot_triangles(vm_engine *e, int64_t n, int32_t *verts, uint8_t *aliv
 // ---- outputs ------------------------------------------------------------------
 int vm_irregular_count(vm_engine *e, int64_t *out) {
   if (!e || !out) return set_err(VM_ERR_INPUT, "null argument");
+  TRY(settle(e));
   TRY(read_counters(e));
   void *buf;
   TRY(scratch(e, 64, &buf));
@@ -1151,6 +1256,7 @@ int vm_irregular_count(vm_engine *e, int64_t *out) {
 
 int vm_compact(vm_engine *e, int64_t current_frame, int64_t *n_vertices, int64_t *n_triangles) {
   if (!e || !n_vertices || !n_triangles) return set_err(VM_ERR_INPUT, "null argument");
+  TRY(settle(e));
   TRY(run_compaction(e, current_frame, false));
   *n_vertices = e->comp.nv;
   *n_triangles = e->comp.nt;
@@ -1172,6 +1278,7 @@ int vm_compact_fetch(vm_engine *e, double *pos, double *nrm, int64_t *ages, int3
 int vm_export_blocks(vm_engine *e, int32_t owned_only, int64_t *n_out, int32_t *coords, double *tsdf,
                      int32_t *weight, uint8_t *tp, uint8_t *tc, int32_t *birth, double *param, double *normal) {
   if (!e || !n_out) return set_err(VM_ERR_INPUT, "null argument");
+  TRY(settle(e));
   TRY(read_counters(e));
   const int nb = e->h_ctr->nblocks;
   std::vector<uint8_t> own(nb);
@@ -1202,6 +1309,7 @@ int vm_import_blocks(vm_engine *e, int64_t n, const int32_t *coords, const doubl
                      const uint8_t *tp, const uint8_t *tc, const int32_t *birth, const double *param,
                      const double *normal) {
   if (!e || (n && !coords)) return set_err(VM_ERR_INPUT, "null argument");
+  TRY(settle(e));
   if (n <= 0) return VM_OK;
   TRY(reset_call_counters(e));
   int32_t *di;
@@ -1236,6 +1344,7 @@ int vm_import_blocks(vm_engine *e, int64_t n, const int32_t *coords, const doubl
 // slot; conservation compares the pool counters with full recounts.
 int vm_audit(vm_engine *e, vm_audit_report *out) {
   if (!e || !out) return set_err(VM_ERR_INPUT, "null argument");
+  TRY(settle(e));
   TRY(read_counters(e));
   const Counters c = *e->h_ctr;
   unsigned long long *sums;

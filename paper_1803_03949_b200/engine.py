@@ -108,8 +108,41 @@ def _is_device_tensor(x) -> bool:
     return hasattr(x, "data_ptr") and getattr(x, "is_cuda", False)
 
 
+class _PendingRow(StatsRow):
+    """StatsRow of a frame submitted in pipelined mode: its fields are filled
+    when the frame completes -- at the engine's next call or on first access."""
+
+    def __init__(self, engine: "Engine", frame: int):
+        object.__setattr__(self, "_engine", engine)
+        object.__setattr__(self, "_done", False)
+        object.__setattr__(self, "frame", frame)
+
+    def _fill(self, row: StatsRow) -> None:
+        for k in StatsRow.FIELDS:
+            object.__setattr__(self, k, getattr(row, k))
+        object.__setattr__(self, "_done", True)
+
+    def __getattribute__(self, name):
+        if name in StatsRow.FIELDS and name != "frame" and not object.__getattribute__(self, "_done"):
+            object.__getattribute__(self, "_engine")._resolve_pending()
+        return object.__getattribute__(self, name)
+
+    def __repr__(self):
+        return StatsRow.__repr__(self) if self._done else f"_PendingRow(frame={self.frame})"
+
+    def __eq__(self, other):
+        self.blocks_active   # resolve
+        return StatsRow.__eq__(self, other)
+
+
 class Engine:
-    def __init__(self, config: RunConfig, intrinsics: Intrinsics, audit_every_frame: bool = False):
+    def __init__(self, config: RunConfig, intrinsics: Intrinsics, audit_every_frame: bool = False,
+                 pipelined: bool = False):
+        """pipelined=True: fuse_frame returns once the frame's work is queued
+        (its StatsRow fills in when the frame completes) and the next frame's
+        host->device depth copy overlaps this frame's kernels
+        (vm_fuse_frame_submit).  Results are identical; an error of frame t
+        surfaces at the engine's next call."""
         self.config = config.resolved()
         self.intrinsics = intrinsics
         c = self.config
@@ -128,6 +161,8 @@ class Engine:
                                       int(bool(c.frustum_only)), _lib.STRATEGY_CODES[c.strategy], 0)
         self._collected_n = 0
         self._collected_cache = None
+        self.pipelined = bool(pipelined) and not audit_every_frame
+        self._pending: Optional[_PendingRow] = None
 
     # -- per-frame pipeline ---------------------------------------------------
     def _depth_args(self, depth):
@@ -143,16 +178,56 @@ class Engine:
 
     def fuse_frame(self, depth, pose: Pose) -> StatsRow:
         ptr, h, w, on_dev, keep = self._depth_args(depth)
-        st = _lib.Stats()
         self.store._touch()
+        if self.pipelined:
+            rc = _lib.load().vm_fuse_frame_submit(self.store._h, ptr, h, w, on_dev, C.byref(self._intr_c),
+                                                  C.byref(_lib.pose_c(pose)), C.byref(self._fcfg),
+                                                  self.frame_index)
+            del keep
+            prev, self._pending = self._pending, None
+            _lib.check(rc)          # (an error of the previous frame surfaces here)
+            if prev is not None:    # completed by the submit: deliver its stats
+                self._deliver(prev)
+            row = _PendingRow(self, self.frame_index)
+            self._pending = row
+            self.stats.append(row)
+            self.frame_index += 1
+            return row
+        st = _lib.Stats()
         _lib.check(_lib.load().vm_fuse_frame(self.store._h, ptr, h, w, on_dev,
                                               C.byref(self._intr_c), C.byref(_lib.pose_c(pose)),
                                               C.byref(self._fcfg), self.frame_index, C.byref(st)))
         del keep
         return self._record(st)
 
+    def _deliver(self, row: _PendingRow) -> None:
+        st = _lib.Stats()
+        _lib.check(_lib.load().vm_fuse_frame_result(self.store._h, C.byref(st)))
+        d = st.as_dict()
+        self.device_stats.append(d)
+        self._collected_n = d["collected_blocks"]
+        self._collected_cache = None
+        row._fill(self._row_from(row.frame, d))
+
+    def _resolve_pending(self) -> None:
+        """Complete the pipelined frame in flight, if any (every engine
+        entry point settles it on the device side as well)."""
+        row, self._pending = self._pending, None
+        if row is not None:
+            self._deliver(row)
+
+    @staticmethod
+    def _row_from(frame: int, d: dict) -> StatsRow:
+        return StatsRow(frame=frame, blocks_active=d["blocks_active"],
+                        vertices_live=d["vertices_live"], triangles_live=d["triangles_live"],
+                        vertices_allocated_total=d["vertices_allocated_total"],
+                        vertices_recycled_total=d["vertices_recycled_total"],
+                        irregular_cube_count=d["irregular_cube_count"],
+                        fusion_ms=d["fusion_ms"], meshing_ms=d["meshing_ms"], compact_ms=0.0)
+
     def fuse_frame_enqueue(self, depth, pose: Pose):
         """Split form for device timing: enqueue only (see vm_fuse_frame_enqueue)."""
+        self._resolve_pending()
         ptr, h, w, on_dev, keep = self._depth_args(depth)
         self.store._touch()
         _lib.check(_lib.load().vm_fuse_frame_enqueue(self.store._h, ptr, h, w, on_dev,
@@ -187,6 +262,7 @@ class Engine:
 
     @property
     def last_collected(self) -> list:
+        self._resolve_pending()
         if self._collected_cache is None:
             n = self._collected_n
             out = np.zeros((n, 3), np.int32)
@@ -198,9 +274,11 @@ class Engine:
     # -- derived quantities -----------------------------------------------------
     def irregular_cube_count(self) -> int:
         """engine.py:169-176 as a full device scan."""
+        self._resolve_pending()
         return self.store.irregular_cube_count()
 
     def compact(self) -> CompactMesh:
+        self._resolve_pending()
         t0 = time.perf_counter()
         mesh = self.store.compact_mesh(self.frame_index)
         if self.stats:
@@ -209,6 +287,7 @@ class Engine:
 
     def audit(self) -> AuditReport:
         """engine.py:187-230 as device reductions."""
+        self._resolve_pending()
         a = _lib.AuditC()
         _lib.check(_lib.load().vm_audit(self.store._h, C.byref(a)))
         return AuditReport(vertices_live=int(a.vertices_live), triangles_live=int(a.triangles_live),
@@ -218,10 +297,12 @@ class Engine:
                            conservation_ok=bool(a.conservation_ok))
 
     def set_profiling(self, on: bool = True) -> None:
+        self._resolve_pending()
         _lib.check(_lib.load().vm_set_profiling(self.store._h, int(bool(on))))
 
     def phase_times(self) -> dict:
         """Per-kernel device ms of the last frame (requires set_profiling)."""
+        self._resolve_pending()
         ms = np.zeros(len(PHASES))
         _lib.check(_lib.load().vm_phase_times(self.store._h, _lib.ptr(ms), len(PHASES)))
         return dict(zip(PHASES, (float(v) for v in ms)))
@@ -233,6 +314,7 @@ class Engine:
         _lib.check(_lib.load().vm_set_trace(self.store._h, C.c_void_p(ptr)))
 
     def set_stream(self, stream_handle: int) -> None:
+        self._resolve_pending()
         _lib.check(_lib.load().vm_set_stream(self.store._h, C.c_void_p(stream_handle or None)))
 
 

@@ -16,13 +16,13 @@ pytestmark = pytest.mark.gpu
 NORMAL_ATOL = 1e-12
 
 
-def _engine_from_golden(g, **over):
+def _engine_from_golden(g, pipelined=False, **over):
     from paper_1803_03949_b200 import Engine, Intrinsics, RunConfig
     cfg = cfg_from_golden(g)
     cfg.update(over)
     i6 = g["intr6"]
     intr = Intrinsics(float(i6[0]), float(i6[1]), float(i6[2]), float(i6[3]), int(i6[4]), int(i6[5]))
-    return Engine(RunConfig(**cfg), intr)
+    return Engine(RunConfig(**cfg), intr, pipelined=pipelined)
 
 
 def _pose(g, i):
@@ -101,6 +101,30 @@ def test_engine_resume_after_arena_growth(name):
     if g["coords"].shape[0] > 16:
         assert resumes > 0
     _check_mesh(eng.compact(), g)
+
+
+@pytest.mark.parametrize("name", ENGINE_SCENES)
+@pytest.mark.parametrize("tiny", [False, True])
+def test_pipelined_engine_matches_reference_golden(name, tiny):
+    """Pipelined submission (vm_fuse_frame_submit: frame t+1's depth copy
+    overlaps frame t's kernels, rows fill in lazily): identical rows, blocks and
+    mesh; with tiny arenas every frame also resumes after growth, and a store
+    access between frames completes the frame in flight."""
+    g = load_golden(name)
+    over = dict(block_capacity=4, vertex_capacity=16, triangle_capacity=16) if tiny else {}
+    eng = _engine_from_golden(g, pipelined=True, **over)
+    rows = []
+    for i in range(len(g["depth"])):
+        depth = np.array(g["depth"][i])       # a fresh host buffer, overwritten after the call
+        rows.append(eng.fuse_frame(depth, _pose(g, i)))
+        depth[:] = -1.0                         # the engine must not read it after returning
+        if i == 1:
+            eng.store._counters()               # completes frame 1 on the device side
+    for i, row in enumerate(rows):
+        assert _stats_tuple(row) == tuple(g["stats"][i]), (name, i)
+    _check_blocks(eng.store, g)
+    _check_mesh(eng.compact(), g)
+    assert eng.audit().ok
 
 
 @pytest.mark.parametrize("name", FIELD_SCENES)
