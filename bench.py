@@ -44,27 +44,37 @@ sys.path.insert(0, str(ROOT))
 METRIC = "depth frames/sec (integrate+mesh) at 640x480, 8mm voxels; % of HBM roofline"
 FLUSH_BYTES = 256 << 20
 
-# Algorithmic bytes per unit, device layout v2:
+# Algorithmic bytes per unit of the current device layout:
 # a corner sample is tsdf f64 + weight i32 (12 B); cube types 2 x u8; an edge
-# slot is birth i32 (4) + coordinate f64 (8) + normal 3 x f64 (24).
+# slot is occupancy 1 bit + birth i32 + coordinate f64 + normal 3 x f64; a hash
+# probe reads one 128-B bucket.
 SAMPLE = 12
-SLOT_SCAN = 4
+OCC = 1536 // 8        # occupancy bitmap bytes per block
+BUCKET = 128
 
 
 def phase_bytes(ds: dict, h: int, w: int) -> dict:
-    """Compulsory bytes per kernel for one frame's unit counts."""
+    """Compulsory bytes per kernel for one frame's unit counts (each touched
+    byte once; re-reads that hit L2 are not counted)."""
     depth = h * w * 8
     coll, new, scope, halo = ds["collected_blocks"], ds["new_blocks"], ds["scope_blocks"], ds["halo_blocks"]
     old = coll - new
     return {
         "depth_stats": depth,
-        "collect": depth + coll * 16 + new * 40,
-        "fuse_blocks": old * 512 * SAMPLE + coll * 512 * SAMPLE + new * (512 * 2 + 1536 * SLOT_SCAN)
-        + min(coll * 512, h * w) * 8 + coll * 27 * 16,
-        "retype_place": scope * (729 * SAMPLE + 512 + 1024) + ds["edge_placements"] * (4 + 8)
-        + ds["new_vertices"] * 24,
-        "gc_normals": halo * (1536 * SLOT_SCAN + 729) + ds["normals_computed"] * (12 * SAMPLE + 24)
-        + ds["vertices_freed"] * 4 + ds["fallback_normals"] * (27 * 4 + 4 + 20 * 3 * 8 + 24),
+        # depth + one bucket probe and stamp per collected block + new-block records
+        "collect": depth + coll * (BUCKET + 8) + new * 40,
+        # old state read + new state written, init of new blocks (samples, types,
+        # births, occupancy), depth gathers, neighbour rows + stamps
+        "fuse_blocks": old * 512 * SAMPLE + coll * 512 * SAMPLE + new * (512 * (SAMPLE + 2) + 1536 * 4 + OCC)
+        + min(coll * 512, h * w) * 8 + coll * 27 * 12,
+        # (B+1)^3 sample tile, types read + written, per placement coordinate +
+        # occupancy word, new vertex birth + normal
+        "retype_place": scope * (729 * SAMPLE + 1024 + 1024) + ds["edge_placements"] * (8 + 4)
+        + ds["new_vertices"] * (4 + 24),
+        # occupancy + 9^3 type tile, 12-sample stencil + normal per vertex,
+        # freed births, fallback records and incident vertex coordinates
+        "gc_normals": halo * (OCC + 729) + ds["normals_computed"] * (12 * SAMPLE + 24)
+        + ds["vertices_freed"] * 4 + ds["fallback_normals"] * (16 + 27 * 4 + 20 * 3 * 8 + 24),
     }
 
 
