@@ -135,6 +135,7 @@ struct DevState {
   int32_t block_cap;
   double *tsdf;         // [cap*512]
   int32_t *weight;      // [cap*512]
+  uint32_t *vmask;      // [cap*16] weight > 0, one bit per cube corner sample (C order)
   uint8_t *tp, *tc;     // [cap*512]
   int32_t *vbirth;      // [cap*1536] slot occupancy: birth frame, -1 empty
   uint32_t *vocc;       // [cap*48] the same occupancy as bits (claimed with atomicOr; read by GC)
@@ -156,8 +157,9 @@ struct DevState {
 // Diagnostics only: with a trace buffer set, thread 0 of CTA c < kTraceCtas of
 // kernel k stores %globaltimer at phase p to trace[(k * kTraceCtas + c) * kTraceSlots + p].
 // Slots: 0 start, 1 prologue done, 2 + 4 * item + {0 item start, 1 resolved,
-// 2 staged, 3 computed} for the first 6 items, 27 items processed (a count),
-// 28 item loop done, 29 / 30 kernel-specific, 31 end.
+// 2 staged, 3 computed} for the first 5 items, 22..26 sub-phases of the first
+// item, 27 items processed (a count), 28 item loop done, 29 / 30
+// kernel-specific, 31 end.
 constexpr int kTraceCtas = 2048, kTraceSlots = 32;
 enum { TK_COLLECT = 0, TK_FUSE = 1, TK_RETYPE = 2, TK_GC = 3, TK_COUNT = 4 };
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -179,8 +181,20 @@ __device__ __forceinline__ void trace_at(const DevState &, int, int) {}
 __device__ __forceinline__ void trace_count(const DevState &, int, int) {}
 #endif
 __device__ __forceinline__ void trace_item(const DevState &S, int k, int nth, int phase) {
-  if (nth < 6) trace_at(S, k, 2 + 4 * nth + phase);
+  if (nth < 5) trace_at(S, k, 2 + 4 * nth + phase);
 }
+// sub-phase marks of a CTA's first item: slots 22..26
+__device__ __forceinline__ void trace_sub(const DevState &S, int k, int nth, int sub) {
+  if (nth == 0) trace_at(S, k, 22 + sub);
+}
+#ifdef VM_TRACE
+__device__ __forceinline__ void trace_val(const DevState &S, int k, int nth, int slot, long long v) {
+  if (nth == 0 && S.trace && threadIdx.x == 0 && blockIdx.x < kTraceCtas)
+    S.trace[((size_t)k * kTraceCtas + blockIdx.x) * kTraceSlots + slot] = (unsigned long long)v;
+}
+#else
+__device__ __forceinline__ void trace_val(const DevState &, int, int, int, long long) {}
+#endif
 
 // ---------------------------------------------------------------- tables
 __constant__ uint16_t c_edge_mask[256] = VM_EDGE_MASK_INIT;
@@ -193,11 +207,6 @@ __constant__ uint8_t c_e_own[12] = {0, 1, 2, 0, 4, 5, 6, 4, 0, 1, 3, 2};
 __constant__ uint8_t c_e_axis[12] = {0, 1, 0, 1, 0, 1, 0, 1, 2, 2, 2, 2};
 __constant__ uint8_t c_e_start[12] = {0, 1, 3, 0, 4, 5, 7, 4, 0, 1, 2, 3};
 __constant__ uint8_t c_e_end[12] = {1, 2, 2, 3, 5, 6, 6, 7, 4, 5, 6, 7};
-// inverse: edge index of the cube whose owner offset is `own` along `axis`
-// (-1 if no such edge); [axis][own]
-__constant__ int8_t c_edge_of[3][8] = {{0, -1, 2, -1, 4, -1, 6, -1},
-                                       {3, 1, -1, -1, 7, 5, -1, -1},
-                                       {8, 9, 11, 10, -1, -1, -1, -1}};
 __constant__ uint8_t c_regular[6] = {0x99, 0x66, 0x33, 0xCC, 0x0F, 0xF0};
 // global-memory copies, staged into shared memory by the meshing kernels
 // (coalesced loads; constant-bank reads with per-thread indices serialise)

@@ -196,6 +196,7 @@ static int grow_blocks(vm_engine *e, int64_t need) {
   cudaStream_t st = e->stream;
   TRY(dev_grow(&S.tsdf, o * kNC, n * kNC, st));
   TRY(dev_grow(&S.weight, o * kNC, n * kNC, st));
+  TRY(dev_grow(&S.vmask, o * (kNC / 32), n * (kNC / 32), st));
   TRY(dev_grow(&S.tp, o * kNC, n * kNC, st));
   TRY(dev_grow(&S.tc, o * kNC, n * kNC, st));
   TRY(dev_grow(&S.vbirth, o * kEV, n * kEV, st));
@@ -519,7 +520,7 @@ int vm_destroy(vm_engine *e) {
   DevState &S = e->S;
   void *ptrs[] = {S.slots, S.ovf_head, S.ovf_lock, S.ovf_key, S.ovf_val, S.ovf_next, S.ovf_stamp, S.bcoord,
                   S.nbr, S.stamp_collect, S.stamp_halo, S.stamp_new, S.bowned, S.slab_bits, S.scope, S.newlist,
-                  S.halo, S.tsdf, S.weight, S.tp, S.tc, S.vbirth, S.vocc, S.vparam, S.vnrm, S.item_mask, S.fallback, S.bar_flags, e->d_rays,
+                  S.halo, S.tsdf, S.weight, S.vmask, S.tp, S.tc, S.vbirth, S.vocc, S.vparam, S.vnrm, S.item_mask, S.fallback, S.bar_flags, e->d_rays,
                   S.ctr, e->d_depth, e->d_scratch};
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -1091,6 +1092,7 @@ int vm_set_blocks(vm_engine *e, const int32_t *coords, int64_t n, const double *
       TRY(copy_sync(e, dw, weight, sizeof(int32_t) * n * kNC, cudaMemcpyHostToDevice));
     }
     k_scatter_samples<<<grid_threads(e, n * kNC, 256), 256, 0, e->stream>>>(e->S, didx, (int)n, dt, dw);
+    k_rebuild_vmask<<<grid_threads(e, n * (kNC / 32), 256), 256, 0, e->stream>>>(e->S, didx, (int)n);
     TRY(check_launch());
     CK(cudaStreamSynchronize(e->stream));
     cudaFree(didx);
@@ -1322,7 +1324,13 @@ int vm_import_blocks(vm_engine *e, int64_t n, const int32_t *coords, const doubl
     const size_t i = (size_t)idx[k];
     if (idx[k] < 0) return set_err(VM_ERR_CAPACITY, "import: block table full");
     if (tsdf) TRY(copy_sync(e, S.tsdf + i * kNC, tsdf + k * kNC, 8 * kNC, cudaMemcpyHostToDevice));
-    if (weight) TRY(copy_sync(e, S.weight + i * kNC, weight + k * kNC, 4 * kNC, cudaMemcpyHostToDevice));
+    if (weight) {
+      TRY(copy_sync(e, S.weight + i * kNC, weight + k * kNC, 4 * kNC, cudaMemcpyHostToDevice));
+      uint32_t vm[kNC / 32] = {};
+      for (int q = 0; q < kNC; q++)
+        if (weight[k * kNC + q] > 0) vm[q >> 5] |= 1u << (q & 31);
+      TRY(copy_sync(e, S.vmask + i * (kNC / 32), vm, sizeof vm, cudaMemcpyHostToDevice));
+    }
     if (tp) TRY(copy_sync(e, S.tp + i * kNC, tp + k * kNC, kNC, cudaMemcpyHostToDevice));
     if (tc) TRY(copy_sync(e, S.tc + i * kNC, tc + k * kNC, kNC, cudaMemcpyHostToDevice));
     if (birth) {

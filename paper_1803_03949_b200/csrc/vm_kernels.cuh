@@ -86,6 +86,22 @@ __device__ __forceinline__ void read_prologue(const DevState &S, int *sv, const 
   __syncthreads();
 }
 
+// cp.async global -> shared of 4 / 8 bytes, zero-filled when `valid` is false
+// (no register staging: the loads stay in flight while the warp goes on)
+__device__ __forceinline__ void cp_async4(void *dst, const void *src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(src), "r"(valid ? 4 : 0));
+}
+__device__ __forceinline__ void cp_async8(void *dst, const void *src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async16(void *dst, const void *src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(valid ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
 // ------------------------------------------------------------ depth stats
 __global__ void __launch_bounds__(256) k_depth_stats(DevState S, const FrameDev F) {
   cudaGridDependencySynchronize();   // PDL: wait for the previous kernel of the frame
@@ -330,6 +346,7 @@ __global__ void __launch_bounds__(kThreadsCube) k_init_blocks(DevState S) {
   for (int i = blockIdx.x; i < nnew; i += gridDim.x) {
     const int b = S.newlist[i];
     init_block(S, b, threadIdx.x);
+    if (threadIdx.x < kNC / 32) S.vmask[(size_t)b * (kNC / 32) + threadIdx.x] = 0u;
     if (threadIdx.x < 27) {
       const int t = threadIdx.x;
       const int4 c = S.bcoord[b];
@@ -445,11 +462,17 @@ __global__ void __launch_bounds__(kFB, 6) k_fuse_blocks(DevState S, const FrameD
     if (!(flags & F_INTEGRATE)) continue;
 #pragma unroll
     for (int j = 0; j < kNC / kFB; j++) {
-      if (!ok[j]) continue;
+      bool upd = ok[j] && meas[j] > 0 && meas[j] <= F.max_range && meas[j] - zc[j] >= -F.trunc;
+      // validity bitmap: a warp's 32 lanes hold 32 consecutive corners (one word)
+      const unsigned vb = __ballot_sync(0xffffffffu, upd && (fresh || w_old[j] == 0));
+      if ((threadIdx.x & 31) == 0) {
+        uint32_t *wp = S.vmask + (size_t)b * (kNC / 32) + ((t + j * kFB) >> 5);
+        if (fresh) *wp = vb;                 // (a new block's words are written whole)
+        else if (vb) atomicOr(wp, vb);
+      }
+      if (!upd) continue;
       const double m = meas[j];
-      if (!(m > 0 && m <= F.max_range)) continue;
       const double sdf = m - zc[j];
-      if (!(sdf >= -F.trunc)) continue;
       double dn = sdf / F.trunc;
       dn = dn < -1.0 ? -1.0 : (dn > 1.0 ? 1.0 : dn);
       const size_t q = (size_t)b * kNC + t + j * kFB;
@@ -643,7 +666,8 @@ __global__ void __launch_bounds__(kNT, 16) k_retype_place(DevState S, const Fram
   int nth = 0;
   __shared__ double tile[729];
   __shared__ uint32_t s_col[81];    // tile column x*9+y: sign bits 0..7, valid 9..16, small 18..25
-  __shared__ uint8_t s_top[81];     // its z = 8 point: bit 0 sign, 1 valid, 2 small
+  __shared__ uint8_t s_top[81];     // its z = 8 point: bit 0 sign, 2 small
+  __shared__ __align__(16) uint32_t s_vm8[8 * 16];   // weight > 0 bitmaps: block + 7 plus-neighbours
   __shared__ __align__(16) uint8_t s_tc[kNC];
   __shared__ __align__(16) uint8_t s_tp[kNC];
   __shared__ uint32_t s_claim[3 * 81];   // requested slots: [axis][tile column], bit = owner z
@@ -681,29 +705,27 @@ __global__ void __launch_bounds__(kNT, 16) k_retype_place(DevState S, const Fram
       // batched gathers: all loads in flight before any shared-memory store
       constexpr int kOwn = kNC / kNT, kExt = (217 + kNT - 1) / kNT;
       double ov[kOwn], xv[kExt];
-      int ow[kOwn], xw[kExt], xp[kExt];
+      int xp[kExt];
       uint4 tcv = make_uint4(0, 0, 0, 0);
-#pragma unroll
-      for (int j = 0; j < kOwn; j++) {
-        ov[j] = S.tsdf[(size_t)b * kNC + t + j * kNT];
-        ow[j] = S.weight[(size_t)b * kNC + t + j * kNT];
+      if (t < 32) {   // weight > 0 bitmaps of the block and its 7 plus-neighbours (o = dx*4+dy*2+dz)
+        const int o = t >> 2;
+        const int nb = R.nbr[nbr_dir(o >> 2, (o >> 1) & 1, o & 1)];
+        cp_async16(&s_vm8[t * 4], S.vmask + (size_t)(nb >= 0 ? nb : 0) * (kNC / 32) + (t & 3) * 4, nb >= 0);
       }
+#pragma unroll
+      for (int j = 0; j < kOwn; j++) ov[j] = S.tsdf[(size_t)b * kNC + t + j * kNT];
       tcv = t < 32 ? reinterpret_cast<const uint4 *>(S.tc + (size_t)b * kNC)[t]
                    : reinterpret_cast<const uint4 *>(S.tp + (size_t)b * kNC)[t - 32];
 #pragma unroll
       for (int j = 0; j < kExt; j++) {
         const int q = t + j * kNT;
         xv[j] = 0.0;
-        xw[j] = 0;
         xp[j] = -1;
         if (q < 217) {
           int dir, src;
           ext_src(q, xp[j], dir, src);
           const int nb = R.nbr[dir];
-          if (nb >= 0) {
-            xv[j] = S.tsdf[(size_t)nb * kNC + src];
-            xw[j] = S.weight[(size_t)nb * kNC + src];
-          }
+          if (nb >= 0) xv[j] = S.tsdf[(size_t)nb * kNC + src];
         }
       }
       // own samples: lanes 8g..8g+7 hold z = 0..7 of one column
@@ -714,12 +736,11 @@ __global__ void __launch_bounds__(kNT, 16) k_retype_place(DevState S, const Fram
         const int col = (c >> 6) * 9 + ((c >> 3) & 7);
         tile[col * 9 + (c & 7)] = ov[j];
         const unsigned bs = __ballot_sync(0xffffffffu, ov[j] < 0.0);
-        const unsigned bv = __ballot_sync(0xffffffffu, ow[j] > 0);
         const unsigned bm = __ballot_sync(0xffffffffu, fabs(ov[j]) < eps);
-        if ((lane & 7) == 0)
-          s_col[col] = ((bs >> g8) & 0xFFu) | (((bv >> g8) & 0xFFu) << 9) | (((bm >> g8) & 0xFFu) << 18);
+        if ((lane & 7) == 0) s_col[col] = ((bs >> g8) & 0xFFu) | (((bm >> g8) & 0xFFu) << 18);
       }
       reinterpret_cast<uint4 *>(t < 32 ? s_tc : s_tp)[t & 31] = tcv;
+      cp_async_wait_all();
       // plus layer: q < 128 are the x = 8 and y = 8 faces (z = 0..7 runs of a
       // column), q = 192..199 the column (8, 8); the rest are z = 8 points
 #pragma unroll
@@ -727,16 +748,14 @@ __global__ void __launch_bounds__(kNT, 16) k_retype_place(DevState S, const Fram
         const int q = t + j * kNT;
         const bool run = q < 128 || (q >= 192 && q < 200);
         const unsigned bs = __ballot_sync(0xffffffffu, xv[j] < 0.0);
-        const unsigned bv = __ballot_sync(0xffffffffu, xw[j] > 0);
         const unsigned bm = __ballot_sync(0xffffffffu, fabs(xv[j]) < eps);
         if (xp[j] >= 0) {
           tile[xp[j]] = xv[j];
           const int col = xp[j] / 9;
           if (run) {
-            if ((lane & 7) == 0)
-              s_col[col] = ((bs >> g8) & 0xFFu) | (((bv >> g8) & 0xFFu) << 9) | (((bm >> g8) & 0xFFu) << 18);
+            if ((lane & 7) == 0) s_col[col] = ((bs >> g8) & 0xFFu) | (((bm >> g8) & 0xFFu) << 18);
           } else {
-            s_top[col] = (uint8_t)((xv[j] < 0.0) | ((xw[j] > 0) << 1) | ((fabs(xv[j]) < eps) << 2));
+            s_top[col] = (uint8_t)((xv[j] < 0.0) | ((fabs(xv[j]) < eps) << 2));
           }
         }
       }
@@ -750,10 +769,17 @@ __global__ void __launch_bounds__(kNT, 16) k_retype_place(DevState S, const Fram
       const int x = t >> 3, y = t & 7;
       uint32_t w[4];
       const int cols[4] = {x * 9 + y, (x + 1) * 9 + y, (x + 1) * 9 + y + 1, x * 9 + y + 1};
+      const int cx[4] = {x, x + 1, x + 1, x}, cy[4] = {y, y, y + 1, y + 1};
 #pragma unroll
       for (int k = 0; k < 4; k++) {
         const uint32_t tp8 = s_top[cols[k]];
-        w[k] = s_col[cols[k]] | ((tp8 & 1u) << 8) | (((tp8 >> 1) & 1u) << 17) | (((tp8 >> 2) & 1u) << 26);
+        // weight > 0 of the column's 9 points from the bitmaps: z = 0..7 are one
+        // byte of block (X>>3, Y>>3, 0), z = 8 one bit of block (X>>3, Y>>3, 1)
+        const int ob = ((cx[k] >> 3) << 2) | ((cy[k] >> 3) << 1);
+        const int c0 = (cx[k] & 7) * 64 + (cy[k] & 7) * 8;
+        const uint32_t val9 = ((s_vm8[ob * 16 + (c0 >> 5)] >> (c0 & 31)) & 0xFFu) |
+                              (((s_vm8[(ob | 1) * 16 + (c0 >> 5)] >> (c0 & 31)) & 1u) << 8);
+        w[k] = s_col[cols[k]] | ((tp8 & 1u) << 8) | (val9 << 9) | (((tp8 >> 2) & 1u) << 26);
       }
       uint32_t cxa = 0, cxb = 0, cya = 0, cyb = 0, cza = 0, czb = 0, czc = 0, czd = 0;
 #pragma unroll
@@ -899,10 +925,12 @@ constexpr size_t kRetypeSmem = 0;
 // ------------------------------------------------------------ GC + normals
 // edge index, in the neighbour cube owner - du*e_u - dw*e_w, of the edge slot
 // owned along `axis` (u, w the other two axes)
+// (register-only: [axis][du*2+dw] packed 4 bits each -- per-thread axes would
+// make a constant-bank table read serialise)
 __device__ __forceinline__ int cube_edge_of_slot(int axis, int du, int dw) {
-  const int u = axis == 0 ? 1 : 0, w = axis == 2 ? 1 : 2;
-  const int own = (du << u) | (dw << w);
-  return c_edge_of[axis][own];
+  constexpr unsigned long long kTab = 0x0ull | 4ull << 4 | 2ull << 8 | 6ull << 12 | 3ull << 16 | 7ull << 20 |
+                                      1ull << 24 | 5ull << 28 | 8ull << 32 | 11ull << 36 | 9ull << 40 | 10ull << 44;
+  return (int)((kTab >> (4 * (axis * 4 + du * 2 + dw))) & 15ull);
 }
 
 // position q of the 9^3 type tile over cube locals -1..7 -> neighbour
@@ -1066,23 +1094,21 @@ __device__ __noinline__ void consume_fallbacks(const FallbackArgs S) {
 }
 
 constexpr int kGT = 32;   // threads per CTA of k_gc_normals (one warp per halo block)
-
-// cp.async global -> shared of 4 / 8 bytes, zero-filled when `valid` is false
-// (no register staging: the loads stay in flight while the warp goes on)
-__device__ __forceinline__ void cp_async4(void *dst, const void *src, bool valid) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(src), "r"(valid ? 4 : 0));
-}
-__device__ __forceinline__ void cp_async8(void *dst, const void *src, bool valid) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(valid ? 8 : 0));
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
-
 // type tile over cube locals -1..7: 81 columns (lx, ly) of 16 bytes, z = 0..7
 // at bytes 0..7 and z = -1 at byte 15 (the -z neighbour's z = 7, fetched as
 // the aligned word of its z = 4..7 into bytes 12..15)
 __device__ __forceinline__ int tt_idx(int lx, int ly, int lz) { return ((lx + 1) * 9 + (ly + 1)) * 16 + (lz & 15); }
+
+
+
+
+
+// weight > 0 of the sample at block-local corner (lx, ly, lz) in [-1, 9]^3,
+// from the 27 neighbours' staged validity bitmaps
+__device__ __forceinline__ bool sample_valid(const uint32_t *s_vm, int lx, int ly, int lz) {
+  const int c = (lx & 7) * 64 + (ly & 7) * 8 + (lz & 7);
+  return (s_vm[nbr_dir(lx >> 3, ly >> 3, lz >> 3) * 16 + (c >> 5)] >> (c & 31)) & 1u;
+}
 
 // tsdf / weight sample at block-local corner (lx, ly, lz) in [-1, 9]^3
 __device__ __forceinline__ size_t sample_index(const int *s_nbr, int lx, int ly, int lz) {
@@ -1106,11 +1132,15 @@ __device__ __forceinline__ bool grid_barrier(const DevState &S, int32_t *count, 
 #pragma unroll 1
       for (int g = 0; g < 32; g++) *(volatile int32_t *)(flags + g * 32) = stamp;
     } else {
+      // back off exponentially: a spinning warp steals issue slots from the
+      // CTAs still working on the same SM
       volatile int32_t *f = flags + (blockIdx.x & 31) * 32;
       long long spins = 0;
+      unsigned ns = 64;
       while (*f != stamp) {
-        __nanosleep(32);
-        if (++spins > (1LL << 25)) {   // > ~1 s
+        __nanosleep(ns);
+        ns = ns < 1024 ? 2 * ns : 1024;
+        if (++spins > (1LL << 21)) {   // > ~2 s
           set_error(S, ERR_CONSISTENCY, 50);
           ok = 0;
           break;
@@ -1136,7 +1166,7 @@ __device__ __forceinline__ bool grid_barrier(const DevState &S, int32_t *count, 
 //    mesher.py:456-486).
 // The per-call counters are summed per CTA; G_COMMIT: the last CTA folds the
 // deltas into the pool counters.
-__global__ void __launch_bounds__(kGT, 24) k_gc_normals(DevState S, const FrameDev F,
+__global__ void __launch_bounds__(kGT, 20) k_gc_normals(DevState S, const FrameDev F,
                                                     const int32_t *__restrict__ list,
                                                     const int32_t *__restrict__ count_ptr,
                                                     int count_const, int mode) {
@@ -1154,6 +1184,7 @@ __global__ void __launch_bounds__(kGT, 24) k_gc_normals(DevState S, const FrameD
   const int live_items = (mode & G_REQUIRE_ITEMS) ? s_pro[1] : 1;
   const int n_listed = count_ptr ? s_pro[2] : count_const;
   __shared__ __align__(16) uint8_t tt[81 * 16];   // type_curr over cube locals -1..7 (tt_idx)
+  __shared__ __align__(16) uint32_t s_vm[27 * 16]; // weight > 0 bitmaps of the 27 neighbours
   __shared__ uint8_t s_inhalo[27];     // neighbour is a halo block of this call
   __shared__ uint32_t occ[kEV / 32];   // slot occupancy bits
   __shared__ uint16_t s_vlist[kEV];    // surviving slots
@@ -1200,6 +1231,11 @@ __global__ void __launch_bounds__(kGT, 24) k_gc_normals(DevState S, const FrameD
           cp_async4(&tt[col * 16 + 12], S.tc + (size_t)(nb >= 0 ? nb : 0) * kNC + row + 4, nb >= 0);
         }
       }
+      if (normals)   // validity bitmaps of the 27 neighbours (16 words each, 4 x 16 B)
+        for (int q = t; q < 27 * 4; q += kGT) {
+          const int nb = R.nbr[q >> 2];
+          cp_async16(&s_vm[q * 4], S.vmask + (size_t)(nb >= 0 ? nb : 0) * (kNC / 32) + (q & 3) * 4, nb >= 0);
+        }
       int hv = 0;
       if (normals && t < 27) {
         const int nb = R.nbr[t];
@@ -1210,99 +1246,120 @@ __global__ void __launch_bounds__(kGT, 24) k_gc_normals(DevState S, const FrameD
     }
     __syncthreads();
     trace_item(S, TK_GC, nth, 2);
-    // GC: a slot survives iff a cube around its edge still has the edge in its mask
-#pragma unroll 1
-    for (int j = 0; j < kNC / kGT; j++) {
-      const int c = t + j * kGT;
-      int keep = 0;
-      unsigned keep_axes = 0;
+    // GC, word-parallel over the occupancy bitmap: thread t owns words t, t+32;
+    // an occupied slot survives iff a cube around its edge still has the edge
+    // in its mask (the 4 cubes at -du along u, -dw along w; u, w = the two axes
+    // other than the slot's) -- work proportional to occupied slots, no atomics
 #pragma unroll
-      for (int axis = 0; axis < 3; axis++) {
-        const int sl = c * 3 + axis;
-        if (!((occ[sl >> 5] >> (sl & 31)) & 1)) continue;
+    for (int r = 0; r < (kEV / 32 + kGT - 1) / kGT; r++) {
+      const int wi = t + r * kGT;
+      uint32_t keep = 0;
+      if (wi < kEV / 32) {
+        const uint32_t word = occ[wi];
+        keep = word;
         if (mode & G_GC) {
-          // the 4 cubes around the edge: offsets -du along u, -dw along w
-          // (u, w = the two axes other than `axis`)
-          bool ref = false;
+          for (uint32_t m = word; m; m &= m - 1) {
+            const int bit = __ffs(m) - 1;
+            const int sl = wi * 32 + bit;
+            const int c = sl / 3, axis = sl - 3 * c;
+            // (no short-circuit: the 4 type and mask lookups issue together)
+            unsigned ty[4], ref = 0;
 #pragma unroll
-          for (int q = 0; q < 4; q++) {
-            int l0, l1, l2;
-            slot_cube(c, axis, q, l0, l1, l2);
-            ref = ref || ((T.edge_mask[tt[tt_idx(l0, l1, l2)]] >> cube_edge_of_slot(axis, q >> 1, q & 1)) & 1);
+            for (int q = 0; q < 4; q++) {
+              int l0, l1, l2;
+              slot_cube(c, axis, q, l0, l1, l2);
+              ty[q] = tt[tt_idx(l0, l1, l2)];
+            }
+#pragma unroll
+            for (int q = 0; q < 4; q++) ref |= (unsigned)T.edge_mask[ty[q]] >> cube_edge_of_slot(axis, q >> 1, q & 1);
+            if (!(ref & 1u)) {
+              keep &= ~(1u << bit);
+              S.vbirth[(size_t)b * kEV + sl] = -1;
+              frees += R.owned;
+            }
           }
-          if (!ref) {
-            S.vbirth[(size_t)b * kEV + sl] = -1;
-            atomicAnd(&occ[sl >> 5], ~(1u << (sl & 31)));
-            frees += R.owned;
-            continue;
-          }
+          occ[wi] = keep;
         }
-        keep++;
-        keep_axes |= 1u << axis;
       }
       if (normals) {
-        int pos = smem_append(keep, &s_nv);
-#pragma unroll
-        for (int axis = 0; axis < 3; axis++)
-          if ((keep_axes >> axis) & 1) s_vlist[pos++] = (uint16_t)(c * 3 + axis);
+        int pos = smem_append(__popc(keep), &s_nv);
+        for (uint32_t m = keep; m; m &= m - 1) s_vlist[pos++] = (uint16_t)(wi * 32 + __ffs(m) - 1);
       }
     }
     __syncthreads();
+    trace_sub(S, TK_GC, nth, 0);   // GC done
+    trace_val(S, TK_GC, nth, 25, s_nv);
+#ifdef VM_TRACE
+    { unsigned smid; asm volatile("mov.u32 %0, %%smid;" : "=r"(smid)); trace_val(S, TK_GC, nth, 24, smid); }
+#endif
     if (mode & G_GC)   // frees applied
       for (int q = t; q < kEV / 32; q += kGT) S.vocc[(size_t)b * (kEV / 32) + q] = occ[q];
     if (normals) {
       const int nv = s_nv;
-      for (int p = t; p < nv; p += kGT) {
-        const int sl = s_vlist[p];
-        const int ci = sl / 3, axis = sl - 3 * ci;
-        computed += R.owned;
-        const int x0 = ci >> 6, y0 = (ci >> 3) & 7, z0 = ci & 7;
-        const int x1 = x0 + (axis == 0), y1 = y0 + (axis == 1), z1 = z0 + (axis == 2);
-        // the 12 stencil samples c0 +- e_d, c1 +- e_d (c1 = c0 + e_axis), all
-        // 24 loads in flight together; absent neighbours read a dummy in-bounds
-        // sample and invalidate the stencil
-        double v0p[3], v0m[3], v1p[3], v1m[3];
-        int w0p[3], w0m[3], w1p[3], w1m[3];
-        bool inb = true;
-        const size_t dummy = (size_t)b * kNC;
+      // two vertices per thread per pass: their 24 tsdf loads in flight together
+      for (int p0 = 0; p0 < nv; p0 += 2 * kGT) {
+        double v[2][12];
+        int slv[2];
+        bool val[2];
 #pragma unroll
-        for (int d = 0; d < 3; d++) {
-          const int dx = d == 0, dy = d == 1, dz = d == 2;
-          size_t a = sample_index(R.nbr, x0 + dx, y0 + dy, z0 + dz);
-          size_t bq = sample_index(R.nbr, x0 - dx, y0 - dy, z0 - dz);
-          size_t cq = sample_index(R.nbr, x1 + dx, y1 + dy, z1 + dz);
-          size_t dq = sample_index(R.nbr, x1 - dx, y1 - dy, z1 - dz);
-          inb = inb && a != ~(size_t)0 && bq != ~(size_t)0 && cq != ~(size_t)0 && dq != ~(size_t)0;
-          a = a == ~(size_t)0 ? dummy : a;
-          bq = bq == ~(size_t)0 ? dummy : bq;
-          cq = cq == ~(size_t)0 ? dummy : cq;
-          dq = dq == ~(size_t)0 ? dummy : dq;
-          v0p[d] = S.tsdf[a]; v0m[d] = S.tsdf[bq]; v1p[d] = S.tsdf[cq]; v1m[d] = S.tsdf[dq];
-          w0p[d] = S.weight[a]; w0m[d] = S.weight[bq]; w1p[d] = S.weight[cq]; w1m[d] = S.weight[dq];
+        for (int u = 0; u < 2; u++) {
+          const int p = p0 + u * kGT + t;
+          slv[u] = p < nv ? s_vlist[p] : -1;
+          const int sl = slv[u] < 0 ? 0 : slv[u];
+          const int ci = sl / 3, axis = sl - 3 * ci;
+          const int x0 = ci >> 6, y0 = (ci >> 3) & 7, z0 = ci & 7;
+          const int x1 = x0 + (axis == 0), y1 = y0 + (axis == 1), z1 = z0 + (axis == 2);
+          // the 12 stencil samples c0 +- e_d, c1 +- e_d (c1 = c0 + e_axis), absent
+          // neighbours read a dummy in-bounds sample; weight > 0 from the staged
+          // bitmaps (absent = 0)
+          const size_t dummy = (size_t)b * kNC;
+          bool ok = slv[u] >= 0;
+#pragma unroll
+          for (int d = 0; d < 3; d++) {
+            const int dx = d == 0, dy = d == 1, dz = d == 2;
+            const size_t a = sample_index(R.nbr, x0 + dx, y0 + dy, z0 + dz);
+            const size_t bq = sample_index(R.nbr, x0 - dx, y0 - dy, z0 - dz);
+            const size_t cq = sample_index(R.nbr, x1 + dx, y1 + dy, z1 + dz);
+            const size_t dq = sample_index(R.nbr, x1 - dx, y1 - dy, z1 - dz);
+            v[u][4 * d + 0] = S.tsdf[a == ~(size_t)0 ? dummy : a];     // c0 + e_d
+            v[u][4 * d + 1] = S.tsdf[bq == ~(size_t)0 ? dummy : bq];   // c0 - e_d
+            v[u][4 * d + 2] = S.tsdf[cq == ~(size_t)0 ? dummy : cq];   // c1 + e_d
+            v[u][4 * d + 3] = S.tsdf[dq == ~(size_t)0 ? dummy : dq];   // c1 - e_d
+            ok = ok & sample_valid(s_vm, x0 + dx, y0 + dy, z0 + dz) & sample_valid(s_vm, x0 - dx, y0 - dy, z0 - dz) &
+                 sample_valid(s_vm, x1 + dx, y1 + dy, z1 + dz) & sample_valid(s_vm, x1 - dx, y1 - dy, z1 - dz);
+          }
+          val[u] = ok;
         }
-        bool valid = inb;   // (an invalid stencil's gradient is never used)
 #pragma unroll
-        for (int d = 0; d < 3; d++) valid = valid && w0p[d] > 0 && w0m[d] > 0 && w1p[d] > 0 && w1m[d] > 0;
-        const double d0 = axis == 0 ? v1m[0] : axis == 1 ? v1m[1] : v1m[2];   // samples at c0 and c1
-        const double d1 = axis == 0 ? v0p[0] : axis == 1 ? v0p[1] : v0p[2];
-        const double denom = d0 - d1;
-        const double param = (denom != 0) ? d0 / denom : 0.5;
-        double g[3];
-        const double wa = 1.0 - param;
+        for (int u = 0; u < 2; u++) {
+          if (slv[u] < 0) continue;
+          const int sl = slv[u];
+          const int axis = sl - 3 * (sl / 3);
+          computed += R.owned;
+          const double d0 = axis == 0 ? v[u][3] : axis == 1 ? v[u][7] : v[u][11];   // samples at c0 and c1
+          const double d1 = axis == 0 ? v[u][0] : axis == 1 ? v[u][4] : v[u][8];
+          const double denom = d0 - d1;
+          const double param = (denom != 0) ? d0 / denom : 0.5;
+          double g[3];
+          const double wa = 1.0 - param;
 #pragma unroll
-        for (int d = 0; d < 3; d++)
-          g[d] = __dadd_rn(__dmul_rn(wa, v0p[d] - v0m[d]), __dmul_rn(param, v1p[d] - v1m[d]));
-        const double nrm = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(g[0], g[0]), __dmul_rn(g[1], g[1])),
-                                          __dmul_rn(g[2], g[2])));
-        if (valid && nrm > 1e-12) {
-          double *dst = S.vnrm + 3 * ((size_t)b * kEV + sl);
-          dst[0] = g[0] / nrm; dst[1] = g[1] / nrm; dst[2] = g[2] / nrm;
-        } else {
-          fallbacks += R.owned;
-          s_fb[atomicAdd(&s_nfb, 1)] = (uint16_t)sl;
+          for (int d = 0; d < 3; d++)
+            g[d] = __dadd_rn(__dmul_rn(wa, v[u][4 * d] - v[u][4 * d + 1]),
+                             __dmul_rn(param, v[u][4 * d + 2] - v[u][4 * d + 3]));
+          const double nrm = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(g[0], g[0]), __dmul_rn(g[1], g[1])),
+                                            __dmul_rn(g[2], g[2])));
+          if (val[u] && nrm > 1e-12) {
+            double *dst = S.vnrm + 3 * ((size_t)b * kEV + sl);
+            dst[0] = g[0] / nrm; dst[1] = g[1] / nrm; dst[2] = g[2] / nrm;
+          } else {
+            fallbacks += R.owned;
+            s_fb[atomicAdd(&s_nfb, 1)] = (uint16_t)sl;
+          }
         }
       }
       __syncthreads();
+      trace_sub(S, TK_GC, nth, 1);   // normals done
+
       // face-normal fallback: publish each failed slot with its 4 cube types and
       // candidate mask (types, neighbour row and halo flags are staged here)
       const int nfb = s_nfb;
@@ -1462,6 +1519,19 @@ __global__ void k_scatter_samples(DevState S, const int32_t *idx, int n, const d
     const size_t dst = (size_t)b * kNC + (q % kNC);
     if (tsdf) S.tsdf[dst] = tsdf[q];
     if (weight) S.weight[dst] = weight[q];
+  }
+}
+
+// validity bitmap of listed blocks from their weights (after host writes)
+__global__ void k_rebuild_vmask(DevState S, const int32_t *idx, int n) {
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < (long long)n * (kNC / 32);
+       q += (long long)gridDim.x * blockDim.x) {
+    const int b = idx[q / (kNC / 32)];
+    if (b < 0) continue;
+    const int w = (int)(q % (kNC / 32));
+    uint32_t bits = 0;
+    for (int k = 0; k < 32; k++) bits |= (S.weight[(size_t)b * kNC + w * 32 + k] > 0 ? 1u : 0u) << k;
+    S.vmask[(size_t)b * (kNC / 32) + w] = bits;
   }
 }
 

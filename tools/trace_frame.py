@@ -64,7 +64,7 @@ for k, name in enumerate(NAMES):
     for idx in order:
         row = m[idx]
         segs = []
-        for it in range(min(int(row[27]), 6)):
+        for it in range(min(int(row[27]), 5)):
             ts = [row[2 + 4 * it + p] for p in range(4)]
             prev = ts[0]
             parts = []
@@ -73,5 +73,25 @@ for k, name in enumerate(NAMES):
                     parts.append(f"{(ts[p] - prev) / 1e3:.2f}")
                     prev = ts[p]
             segs.append(f"[{(ts[0] - t0) / 1e3:.2f}: {'/'.join(parts)}]")
-        extra = " ".join(f"s{p}={(row[p] - t0) / 1e3:.2f}" for p in (28, 29, 30) if row[p] > 0)
+        extra = " ".join(f"s{p}={(row[p] - t0) / 1e3:.2f}" for p in (22, 23, 28, 29, 30) if row[p] > 0)
+        extra += f" nv={row[25]} nfb={row[26]} sm={row[24]}" if name == "gc_normals" else ""
         print(f"  slow CTA end {(row[31] - t0) / 1e3:.2f} items {row[27]} {' '.join(segs)} {extra}")
+
+# per-SM view of gc: items and the latest item end on each SM
+m = tr[3]
+live = (m[:, 0] > 0) & (m[:, 27] > 0)
+if live.any():
+    sm = m[live, 24]
+    en = (m[live, 28] - t0) / 1e3
+    nv = m[live, 25]
+    import collections
+    per = collections.defaultdict(list)
+    for a, e, v in zip(sm, en, nv):
+        per[int(a)].append((e, int(v)))
+    worst = sorted(per.items(), key=lambda kv: -max(e for e, _ in kv[1]))[:5]
+    print("\ngc per SM (items, sum nv, latest item end):")
+    for s_, L in worst:
+        print(f"  sm {s_}: {len(L)} items, nv {sum(v for _, v in L)}, latest {max(e for e, _ in L):.2f} us")
+    allsm = [(len(L), sum(v for _, v in L)) for L in per.values()]
+    print("  SMs:", len(per), "items/SM min/max", min(a for a, _ in allsm), max(a for a, _ in allsm),
+          "nv/SM min/max", min(b for _, b in allsm), max(b for _, b in allsm))
