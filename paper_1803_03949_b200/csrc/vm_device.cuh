@@ -129,7 +129,6 @@ struct DevState {
   int32_t *stamp_new;   // epoch in which the block was allocated
   uint8_t *slab_bits;
   int32_t *scope;       // scope items: collected first, then minus slabs
-  int32_t *newlist;
   int32_t *halo;
   // heavy block storage, sized block_cap (grows)
   int32_t block_cap;
@@ -353,7 +352,7 @@ __device__ int alloc_block(const DevState &S, int x, int y, int z, int epoch) {
   } else {
     S.bowned[idx] = 1;
   }
-  S.newlist[atomicAdd(&S.ctr->nnew, 1)] = idx;
+  atomicAdd(&S.ctr->nnew, 1);   // (a statistic: result unused, no round trip)
   return idx;
 }
 
@@ -374,9 +373,10 @@ __device__ HashRef hash_insert_ref(const DevState &S, int x, int y, int z, int e
       k = (long long)atomicCAS((unsigned long long *)&kb[i].key, (unsigned long long)kEmptyKey,
                                (unsigned long long)key);
       if (k == kEmptyKey) {
+        // publish the index: readers in this kernel use only the index (the
+        // block's coordinate and stamps are read by later kernels)
         const int idx = alloc_block(S, x, y, z, epoch);
-        __threadfence();
-        atomicExch(&kb[i].val, idx);
+        *(volatile int32_t *)&kb[i].val = idx;
         return {idx, ld_vol(&kb[i].pad), &kb[i].pad};
       }
     }

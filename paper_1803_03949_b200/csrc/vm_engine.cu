@@ -342,7 +342,7 @@ static int init_new_blocks(vm_engine *e) {
     TRY(grow_blocks(e, e->h_ctr->nblocks));
     CK(cudaMemsetAsync(&e->S.ctr->need, 0, sizeof(int32_t), e->stream));
   }
-  k_init_blocks<<<grid_blocks(e), kThreadsCube, 0, e->stream>>>(e->S);
+  k_init_blocks<<<grid_blocks(e), kThreadsCube, 0, e->stream>>>(e->S, e->epoch);
   TRY(check_launch());
   TRY(read_counters(e));
   return error_from_counters(e);
@@ -482,7 +482,6 @@ int vm_create(const vm_store_config *cfg, vm_engine **out) {
   TRY(dev_alloc(&S.bowned, mb, 0));
   TRY(dev_alloc(&S.slab_bits, (mb + 4) & ~(size_t)3, 0));
   TRY(dev_alloc(&S.scope, mb));
-  TRY(dev_alloc(&S.newlist, mb));
   TRY(dev_alloc(&S.halo, mb));
   TRY(dev_alloc(&S.ctr, 1, 0));
   TRY(dev_alloc(&S.bar_flags, 32 * 32, 0));
@@ -519,7 +518,7 @@ int vm_destroy(vm_engine *e) {
   cudaStreamSynchronize(e->stream);
   DevState &S = e->S;
   void *ptrs[] = {S.slots, S.ovf_head, S.ovf_lock, S.ovf_key, S.ovf_val, S.ovf_next, S.ovf_stamp, S.bcoord,
-                  S.nbr, S.stamp_collect, S.stamp_halo, S.stamp_new, S.bowned, S.slab_bits, S.scope, S.newlist,
+                  S.nbr, S.stamp_collect, S.stamp_halo, S.stamp_new, S.bowned, S.slab_bits, S.scope,
                   S.halo, S.tsdf, S.weight, S.vmask, S.tp, S.tc, S.vbirth, S.vocc, S.vparam, S.vnrm, S.item_mask, S.fallback, S.bar_flags, e->d_rays,
                   S.ctr, e->d_depth, e->d_scratch};
   for (void *p : ptrs)

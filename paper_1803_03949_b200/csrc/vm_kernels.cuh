@@ -340,11 +340,12 @@ __device__ __forceinline__ void init_block(const DevState &S, int b, int t) {
   if (t < kEV / 32) S.vocc[(size_t)b * (kEV / 32) + t] = 0u;
 }
 
-__global__ void __launch_bounds__(kThreadsCube) k_init_blocks(DevState S) {
+__global__ void __launch_bounds__(kThreadsCube) k_init_blocks(DevState S, int epoch) {
   if (halted(S)) return;
-  const int nnew = ld_vol(&S.ctr->nnew);
-  for (int i = blockIdx.x; i < nnew; i += gridDim.x) {
-    const int b = S.newlist[i];
+  // the blocks allocated by this call (stamp_new == epoch), phase API only
+  const int nb_all = ld_vol(&S.ctr->nblocks);
+  for (int b = blockIdx.x; b < nb_all; b += gridDim.x) {
+    if (__ldcg(S.stamp_new + b) != epoch) continue;
     init_block(S, b, threadIdx.x);
     if (threadIdx.x < kNC / 32) S.vmask[(size_t)b * (kNC / 32) + threadIdx.x] = 0u;
     if (threadIdx.x < 27) {
