@@ -892,7 +892,7 @@ int vm_scope_halo(vm_engine *e, int64_t *n_scope, int32_t *scope_coords, uint8_t
   CK(cudaMemsetAsync(&e->S.ctr->nslab, 0, sizeof(int32_t), e->stream));
   CK(cudaMemsetAsync(&e->S.ctr->nhalo, 0, sizeof(int32_t), e->stream));
   k_fuse_blocks<<<grid_blocks(e), kFB, 0, e->stream>>>(e->S, *e->h_frame, e->S.scope,
-                                                                &e->S.ctr->ncollected, 0, F_SCOPE);
+                                                                &e->S.ctr->ncollected, 0, F_SCOPE | F_HALO);
   TRY(check_launch());
   TRY(read_counters(e));
   const int nc = e->h_ctr->ncollected, ns = e->h_ctr->nslab, nh = e->h_ctr->nhalo;

@@ -23,7 +23,7 @@ namespace vm {
 
 constexpr int kThreadsCube = 512;   // one thread per cube of a block
 
-enum { F_INIT = 1, F_INTEGRATE = 2, F_SCOPE = 4 };
+enum { F_INIT = 1, F_INTEGRATE = 2, F_SCOPE = 4, F_HALO = 8 };
 enum { G_GC = 1, G_NORMALS = 2, G_COMMIT = 4, G_REQUIRE_ITEMS = 8 };
 
 // error and need are adjacent: one 8-byte load
@@ -221,6 +221,12 @@ __global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, cons
     __syncthreads();
     const int ry0 = reg / rx, rx0 = reg - ry0 * rx;
     const int u = rx0 * kRegionW + (t & (kRegionW - 1));
+    for (int pass = 0; pass < 2; pass++) {   // pass 1 only if the key set overflowed
+    const bool direct = pass == 1;
+    if (direct) {
+      if (s_nover <= kCOver) break;   // (uniform: read after the barrier below)
+      __syncthreads();
+    }
     const double rxn = u < F.w ? __ldg(S.rays + u) : 0.0;
     double d[2];
     bool valid[2];
@@ -253,6 +259,13 @@ __global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, cons
           if (block_relevant(S, c[0], c[1], c[2])) key = (unsigned long long)pack_coord(c[0], c[1], c[2]);
         }
         const unsigned grp = __match_any_sync(0xffffffffu, key);
+        if (direct) {   // (rare) the set overflowed: probe the table directly
+          if (key != kNoKey && lane == __ffs(grp) - 1) {
+            const int got = collect_block(S, F, c[0], c[1], c[2]);
+            if (got >= 0) S.scope[atomicAdd(&ctr->ncollected, 1)] = got;
+          }
+          continue;
+        }
         if (key != kNoKey && lane == __ffs(grp) - 1) {
           // CTA-local set: first inserter lists the key
           unsigned h = cset_hash(key);
@@ -262,7 +275,10 @@ __global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, cons
             if (old == kNoKey) s_list[atomicAdd(&s_n, 1)] = (uint16_t)h;
             placed = old == kNoKey || old == key;
           }
-          if (!placed) s_over[atomicAdd(&s_nover, 1) & (kCOver - 1)] = key;   // set crowded
+          if (!placed) {   // set crowded: the overflow list, or (full) a direct pass
+            const int o = atomicAdd(&s_nover, 1);
+            if (o < kCOver) s_over[o] = key;
+          }
         }
       }
     }
@@ -291,6 +307,9 @@ __global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, cons
     if (t == 0 && s_nout) s_base = atomicAdd(&ctr->ncollected, s_nout);
     __syncthreads();
     for (int q = t; q < s_nout; q += kCollectThreads) S.scope[s_base + q] = s_out[q];
+    __syncthreads();
+    if (pass == 0) continue;
+    }   // pass
     __syncthreads();   // the set is reset for the next region
     trace_item(S, TK_COLLECT, nth, 3);
   }
@@ -362,7 +381,9 @@ __global__ void __launch_bounds__(kThreadsCube) k_init_blocks(DevState S, int ep
 // One CTA per collected block, one thread per corner:
 //  F_INIT      blocks allocated this call are initialised and linked;
 //  F_INTEGRATE TSDF running average (fusion.py:138-168);
-//  F_SCOPE     27-neighbour halo marking and minus-slab scope marking
+//  F_SCOPE     minus-slab scope marking (mesher.py:499-527)
+//  F_HALO      27-neighbour halo marking (mesher.py:530-543; in fuse_frame
+//              the halo is marked by k_retype_place instead)
 //              (mesher.py:499-543), with hash lookups (links of blocks
 //              created in this launch are still being written).
 constexpr int kFB = 128;   // threads per CTA of k_fuse_blocks (4 corners each)
@@ -428,8 +449,11 @@ __global__ void __launch_bounds__(kFB, 6) k_fuse_blocks(DevState S, const FrameD
     if (fresh)
 #pragma unroll
       for (int j = 0; j < kNC / kFB; j++) init_block(S, b, t + j * kFB);
-    if ((flags & (F_SCOPE | F_INIT)) && prober) {
-      const int dx = pdir / 9 - 1, dy = (pdir / 3) % 3 - 1, dz = pdir % 3 - 1;
+    const int dx = pdir / 9 - 1, dy = (pdir / 3) % 3 - 1, dz = pdir % 3 - 1;
+    const bool minus = dx <= 0 && dy <= 0 && dz <= 0 && pdir != 13;
+    // probes: all 27 to link a new block or to mark the halo (F_HALO); else
+    // only the 7 minus directions (slab scope items)
+    if (prober && ((fresh && (flags & F_INIT)) || (flags & F_HALO) || ((flags & F_SCOPE) && minus))) {
       int nb = b, nb_collected = 1;
       if (pdir != 13) {
         if (fresh) {   // its links are built here, from the table
@@ -447,17 +471,16 @@ __global__ void __launch_bounds__(kFB, 6) k_fuse_blocks(DevState S, const FrameD
         S.nbr[(size_t)b * 27 + pdir] = nb;
         if (nb >= 0 && pdir != 13) S.nbr[(size_t)nb * 27 + (26 - pdir)] = b;
       }
-      if ((flags & F_SCOPE) && nb >= 0) {
+      if ((flags & F_HALO) && nb >= 0) {
         if (ld_vol(S.stamp_halo + nb) != F.epoch && atomicExch(S.stamp_halo + nb, F.epoch) != F.epoch)
           S.halo[atomicAdd(&S.ctr->nhalo, 1)] = nb;
-        // minus neighbour n = c - o, o in {0,1}^3 \ 0, not itself collected
-        if (dx <= 0 && dy <= 0 && dz <= 0 && pdir != 13 && !nb_collected) {
-          const int o = (-dx) * 4 + (-dy) * 2 + (-dz);
-          const unsigned sh = 8 * (nb & 3);
-          const unsigned old = atomicOr((unsigned *)(S.slab_bits + (nb & ~3)), (1u << (o - 1)) << sh);
-          if (((old >> sh) & 0xFF) == 0)
-            S.scope[ld_vol(&S.ctr->ncollected) + atomicAdd(&S.ctr->nslab, 1)] = nb;
-        }
+      }
+      // minus neighbour n = c - o, o in {0,1}^3 \ 0, not itself collected
+      if ((flags & F_SCOPE) && nb >= 0 && minus && !nb_collected) {
+        const int o = (-dx) * 4 + (-dy) * 2 + (-dz);
+        const unsigned sh = 8 * (nb & 3);
+        const unsigned old = atomicOr((unsigned *)(S.slab_bits + (nb & ~3)), (1u << (o - 1)) << sh);
+        if (((old >> sh) & 0xFF) == 0) S.scope[n + atomicAdd(&S.ctr->nslab, 1)] = nb;   // (n = collected)
       }
     }
     if (!(flags & F_INTEGRATE)) continue;
@@ -695,7 +718,17 @@ __global__ void __launch_bounds__(kNT, 16) k_retype_place(DevState S, const Fram
     __syncthreads();
     trace_item(S, TK_RETYPE, nth, 1);
     const int mode = R.mode;
+    // fused_halo (mesher.py:530-543): a collected item marks its 27-neighbourhood
+    // (frustum-culled ones too); issued after the tile loads below, so the
+    // exchange round trips overlap them
+    const bool halo_item = F.scope_mode == 0 && i < nc && R.b >= 0 && t < 27;
+    auto mark_halo = [&]() {
+      if (!halo_item) return;
+      const int nb = R.nbr[t];
+      if (nb >= 0 && atomicExch(S.stamp_halo + nb, F.epoch) != F.epoch) S.halo[atomicAdd(&S.ctr->nhalo, 1)] = nb;
+    };
     if (mode <= 0) {
+      mark_halo();
       __syncthreads();
       continue;
     }
@@ -729,6 +762,7 @@ __global__ void __launch_bounds__(kNT, 16) k_retype_place(DevState S, const Fram
           if (nb >= 0) xv[j] = S.tsdf[(size_t)nb * kNC + src];
         }
       }
+      mark_halo();
       // own samples: lanes 8g..8g+7 hold z = 0..7 of one column
       const int g8 = (lane >> 3) * 8;
 #pragma unroll

@@ -237,3 +237,29 @@ def test_c5_multiroom_prefix_matches_oracle():
     spec.width, spec.height, spec.fx, spec.fy = 320, 240, 262.5, 262.5
     eng, ora = _run_oracle_and_gpu(spec, cfg, 4, pose_fn=multiroom_pose)
     _compare_final(eng, ora)
+
+
+@pytest.mark.parametrize("cube", [0.002, 0.02])
+def test_scattered_depth_overflows_collect_set_matches_oracle(cube):
+    """Uniform random depth at fine cubes and a wide band: a 64x8-pixel region
+    touches far more distinct blocks than k_collect's shared-memory key set
+    holds (its overflow list, then the direct-probe pass); at 2 cm the set does
+    not overflow.  Block set, TSDF and mesh must equal the oracle's."""
+    from oracle.oracle import OracleEngine
+    from paper_1803_03949_b200 import Engine, Intrinsics, Pose, RunConfig
+    rng = np.random.default_rng(7)
+    w, h = 64, 32
+    intr = Intrinsics(40.0, 40.0, (w - 1) / 2, (h - 1) / 2, w, h)
+    cfg = dict(cube_size=cube, trunc=max(0.03, 2 * cube), table_size=1 << 22)
+    eng = Engine(RunConfig(**cfg), intr)
+    ora = OracleEngine(cfg, (intr.fx, intr.fy, intr.cx, intr.cy, w, h))
+    for i in range(2):
+        d = rng.uniform(0.3, 3.0, size=(h, w))
+        d[rng.random((h, w)) < 0.05] = 0.0
+        pose = Pose(np.eye(3), np.array([0.01 * i, 0.0, 0.0]))
+        row = eng.fuse_frame(d, pose)
+        ref = ora.fuse_frame(d, pose.rotation, pose.translation)
+        assert _stats_tuple(row) == tuple(ref[k] for k in (
+            "frame", "blocks_active", "vertices_live", "triangles_live",
+            "vertices_allocated_total", "vertices_recycled_total", "irregular_cube_count")), i
+    _compare_final(eng, ora)
