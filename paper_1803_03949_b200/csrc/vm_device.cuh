@@ -513,21 +513,22 @@ __device__ __forceinline__ long long block_sum(long long v, long long *sh) {
 // Block-wide sums of N per-thread counters (each < 2^31 per CTA): one
 // redux.sync per counter and warp, one barrier pair, then one atomicAdd per
 // counter (thread k adds counter k to dst[k]; null = skip).  `sh` holds 32 * N.
-template <int N>
+template <int N, int NW>
 __device__ __forceinline__ void block_add_counters(int (&vals)[N], int *sh, int64_t *const (&dst)[N]) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;   // (NW = warps per CTA; sh holds N * NW)
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < N; k++) {
     const unsigned v = __reduce_add_sync(0xffffffffu, (unsigned)vals[k]);
-    if (lane == 0) sh[k * 32 + wid] = (int)v;
+    if (lane == 0) sh[k * NW + wid] = (int)v;
   }
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < N; k++)   // static indices: dst stays in registers
     if (threadIdx.x == k) {
       long long r = 0;
-      for (int w = 0; w < nw; w++) r += sh[k * 32 + w];
+#pragma unroll
+      for (int w = 0; w < NW; w++) r += sh[k * NW + w];
       if (r && dst[k]) atomicAdd((unsigned long long *)dst[k], (unsigned long long)r);
     }
 }

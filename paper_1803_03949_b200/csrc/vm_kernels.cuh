@@ -676,7 +676,7 @@ __device__ __forceinline__ uint32_t corner_bytes4(const uint32_t (&w)[4], int sh
 //    in a shared-memory bitmap (all requesters of a slot write identical bits),
 //    then each is claimed (atomicCAS on its birth word -- exactly one
 //    allocation per edge) and its coordinate written.
-__global__ void __launch_bounds__(kNT, 16) k_retype_place(DevState S, const FrameDev F) {
+__global__ void __launch_bounds__(kNT, 18) k_retype_place(DevState S, const FrameDev F) {
   cudaGridDependencySynchronize();   // PDL: wait for the previous kernel of the frame
   trace_at(S, TK_RETYPE, 0);
   __shared__ int s_pro[5];
@@ -695,9 +695,9 @@ __global__ void __launch_bounds__(kNT, 16) k_retype_place(DevState S, const Fram
   __shared__ __align__(16) uint8_t s_tc[kNC];
   __shared__ __align__(16) uint8_t s_tp[kNC];
   __shared__ uint32_t s_claim[3 * 81];   // requested slots: [axis][tile column], bit = owner z
-  __shared__ uint16_t s_place[kTileSlots];
+  __shared__ uint8_t s_wl[3 * 81];   // non-empty claim words
   __shared__ Resolved R;
-  __shared__ int red8[8 * 32];   // (block_add_counters indexes k * 32 + warp)
+  __shared__ int red8[8 * (kNT / 32)];
   __shared__ int s_nplace;
   const int t = threadIdx.x, lane = t & 31;
   const double l = S.cube_size;
@@ -887,57 +887,58 @@ __global__ void __launch_bounds__(kNT, 16) k_retype_place(DevState S, const Fram
       if (czd) atomicOr(&s_claim[2 * 81 + cols[3]], czd);
     }
     __syncthreads();
-    // compact the requested slots (each once, whichever cubes asked for it):
-    // word a * 81 + col holds owner heights z of axis a in column col
+    // list the non-empty claim words (word a * 81 + col: owner heights z of
+    // axis a in tile column col; each requested slot once, whichever cubes
+    // asked for it)
 #pragma unroll
     for (int r = 0; r < (3 * 81 + kNT - 1) / kNT; r++) {
       const int wi = t + r * kNT;
       const uint32_t word = wi < 3 * 81 ? s_claim[wi] : 0u;
-      int pos = smem_append(__popc(word), &s_nplace);
-      const int axis = wi / 81, col = wi - axis * 81;
-      for (uint32_t m = word; m; m &= m - 1) s_place[pos++] = (uint16_t)(((col * 9 + __ffs(m) - 1) * 3) + axis);
+      const int pos = smem_append(word != 0u, &s_nplace);
+      if (word) s_wl[pos] = (uint8_t)wi;
     }
     __syncthreads();
     trace_item(S, TK_RETYPE, nth, 3);
-    // placement, 4 slots per thread in flight: coordinate store and claim
-    // (the first requester to set the slot's occupancy bit allocates)
-    const int np = s_nplace;
-    for (int p0 = 0; p0 < np; p0 += 4 * kNT) {
-      size_t slot[4];
-      uint32_t bit[4], old[4];
-      int owner[4];
+    // placement, one claim word (<= 9 slots) per thread at a time, all its
+    // coordinate stores and occupancy claims in flight together (the first
+    // requester to set a slot's occupancy bit allocates)
+    const int nwl = s_nplace;
+    for (int p = t; p < nwl; p += kNT) {
+      const int wi = s_wl[p];
+      const uint32_t word = s_claim[wi];
+      const int axis = wi / 81, col = wi - 81 * axis;
+      const int ox = col / 9, oy = col - 9 * ox;
+      const int sa = axis == 0 ? 81 : axis == 1 ? 9 : 1;
+      const int ga_c = axis == 0 ? R.coord.x * kB + ox : R.coord.y * kB + oy;   // (axis 2: per z)
+      uint32_t fresh = 0;
+      uint32_t old[9];
 #pragma unroll
-      for (int j = 0; j < 4; j++) {
-        const int p = p0 + j * kNT + t;
-        owner[j] = -1;
-        old[j] = ~0u;
-        bit[j] = 0;
-        slot[j] = 0;
-        if (p >= np) continue;
-        const int u = s_place[p];
-        const int pt = u / 3, axis = u - 3 * pt;
-        const int ox = pt / 81, oy = (pt / 9) % 9, oz = pt % 9;
-        owner[j] = R.nbr[nbr_dir(ox >> 3, oy >> 3, oz >> 3)];
-        if (owner[j] < 0) {
-          set_error(S, ERR_CONSISTENCY, 10, R.coord.x * kB + ox, R.coord.y * kB + oy, R.coord.z * kB + oz);
+      for (int z = 0; z < 9; z++) {
+        old[z] = ~0u;
+        if (!((word >> z) & 1u)) continue;
+        const int owner = R.nbr[nbr_dir(ox >> 3, oy >> 3, z >> 3)];
+        if (owner < 0) {
+          set_error(S, ERR_CONSISTENCY, 10, R.coord.x * kB + ox, R.coord.y * kB + oy, R.coord.z * kB + z);
           continue;
         }
-        slot[j] = (size_t)owner[j] * kEV + (((ox & 7) * 64 + (oy & 7) * 8 + (oz & 7)) * 3 + axis);
+        const size_t slot = (size_t)owner * kEV + (((ox & 7) * 64 + (oy & 7) * 8 + (z & 7)) * 3 + axis);
         // start corner = the owner point; end corner one step along the axis
-        const double d0 = tile[pt];
-        const double d1 = tile[pt + (axis == 0 ? 81 : axis == 1 ? 9 : 1)];
+        const int pt = col * 9 + z;
+        const double d0 = tile[pt], d1 = tile[pt + sa];
         const double param = (d0 == d1) ? 0.5 : d0 / (d0 - d1);
-        const int ga = (axis == 0 ? R.coord.x * kB + ox : axis == 1 ? R.coord.y * kB + oy : R.coord.z * kB + oz);
-        S.vparam[slot[j]] = __dadd_rn(__dmul_rn((double)ga, l), __dmul_rn(param, l));
-        bit[j] = 1u << (slot[j] & 31);
-        old[j] = atomicOr(S.vocc + (slot[j] >> 5), bit[j]);
+        const int ga = axis == 2 ? R.coord.z * kB + z : ga_c;
+        S.vparam[slot] = __dadd_rn(__dmul_rn((double)ga, l), __dmul_rn(param, l));
+        old[z] = atomicOr(S.vocc + (slot >> 5), 1u << (slot & 31)) & (1u << (slot & 31));
       }
 #pragma unroll
-      for (int j = 0; j < 4; j++) {
-        if (owner[j] < 0 || (old[j] & bit[j])) continue;
-        allocs += (S.nranks <= 1 || S.bowned[owner[j]]);   // counted by the slot's owning rank
-        S.vbirth[slot[j]] = frame;
-        S.vnrm[3 * slot[j]] = 0.0; S.vnrm[3 * slot[j] + 1] = 0.0; S.vnrm[3 * slot[j] + 2] = 0.0;
+      for (int z = 0; z < 9; z++) fresh |= (old[z] == 0u ? 1u : 0u) << z;
+      for (uint32_t m = fresh; m; m &= m - 1) {
+        const int z = __ffs(m) - 1;
+        const int owner = R.nbr[nbr_dir(ox >> 3, oy >> 3, z >> 3)];
+        const size_t slot = (size_t)owner * kEV + (((ox & 7) * 64 + (oy & 7) * 8 + (z & 7)) * 3 + axis);
+        allocs += (S.nranks <= 1 || S.bowned[owner]);   // counted by the slot's owning rank
+        S.vbirth[slot] = frame;
+        S.vnrm[3 * slot] = 0.0; S.vnrm[3 * slot + 1] = 0.0; S.vnrm[3 * slot + 2] = 0.0;
       }
     }
     __syncthreads();   // R, tile and the placement list are rewritten by the next item
@@ -948,7 +949,7 @@ __global__ void __launch_bounds__(kNT, 16) k_retype_place(DevState S, const Fram
     int vals[8] = {allocs, placements, active, changed, t_rel, t_new, irr, refined};
     int64_t *const dst[8] = {&S.ctr->v_allocs, &S.ctr->placements, &S.ctr->active, &S.ctr->changed,
                              &S.ctr->t_released, &S.ctr->t_allocated, &S.ctr->irr_delta, &S.ctr->refined};
-    block_add_counters<8>(vals, red8, dst);
+    block_add_counters<8, kNT / 32>(vals, red8, dst);
   }
   if (t == 0 && live) S.ctr->nitems_live = 1;   // (a flag: some item was live this call)
   trace_at(S, TK_RETYPE, 31);
@@ -1226,7 +1227,7 @@ __global__ void __launch_bounds__(kGT, 20) k_gc_normals(DevState S, const FrameD
   __shared__ uint16_t s_fb[kEV];       // ... whose gradient failed
   __shared__ Resolved R;
   __shared__ int s_nv, s_nfb;
-  __shared__ int red[3 * 32];
+  __shared__ int red[3 * (kGT / 32)];
   const int n = live_items > 0 ? n_listed : 0;
   const int t = threadIdx.x;
   const bool normals = (mode & G_NORMALS) != 0;
@@ -1430,7 +1431,7 @@ __global__ void __launch_bounds__(kGT, 20) k_gc_normals(DevState S, const FrameD
   {
     int vals[3] = {frees, computed, fallbacks};
     int64_t *const dst[3] = {&ctr->v_frees, &ctr->normals, &ctr->fallbacks};
-    block_add_counters<3>(vals, red, dst);
+    block_add_counters<3, kGT / 32>(vals, red, dst);
   }
   if (t == 0 && (mode & G_COMMIT)) {
     __threadfence();
