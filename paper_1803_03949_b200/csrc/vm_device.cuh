@@ -51,6 +51,8 @@ struct Counters {
   int64_t irregular;     // Engine.irregular_cube_count, maintained incrementally
   int64_t nblocks_owned; // blocks this rank owns (== nblocks unless partitioned)
   int64_t err_info[4];
+  int32_t fb_pending;    // face-normal fallback records of the last frame not yet applied
+  int32_t pad0;
   // ---- per call ----------------------------------------------------------
   int32_t nvalid;
   int32_t nsteps;
@@ -62,8 +64,6 @@ struct Counters {
   int32_t nexplicit;
   int32_t nitems_live;
   int32_t done_gc;
-  int32_t nfallback;     // face-normal fallback entries reserved this call
-  int32_t gc_bar;        // k_gc_normals grid barrier arrivals
   int64_t v_allocs;
   int64_t v_frees;
   int64_t placements;
@@ -93,7 +93,7 @@ struct FrameDev {
   int32_t frame;        // frame index (vertex birth)
   int32_t scope_mode;   // 0: collected + slabs (device scope); 1: explicit items
   int32_t nsteps_fixed; // > 0: band step count fixed by the intrinsics (k_depth_stats skipped)
-  int32_t bar_stamp;    // unique per k_gc_normals launch (grid-barrier release value)
+  int32_t consume_fb;   // fuse_frame: k_collect applies the previous frame's fallback records
   int32_t pad2;
 };
 
@@ -142,7 +142,6 @@ struct DevState {
   double *vnrm;         // [cap*1536*3]
   uint32_t *item_mask;  // [cap*16] explicit scope cube masks
   int4 *fallback;       // [cap*1536] fallback worklist: block, slot, 4 cube types, candidate mask
-  int32_t *bar_flags;   // [32 * 32] grid-barrier release flags (one line each), epoch-stamped
   long long max_vertices;
   // spatial partition: blocks are owned by hashed tiles
   // of 2^tile_shift blocks per axis; a rank also computes a 1-block margin

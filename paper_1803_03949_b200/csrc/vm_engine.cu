@@ -79,7 +79,6 @@ struct vm_engine {
   int pending = 0;
   int64_t pending_frame = 0;
   int last_resumes = 0;
-  int32_t bar_seq = 0;     // k_gc_normals grid-barrier stamps
   int frame_launches = 0;   // kernels launched by the pending / last frame
   // pipelined submission (vm_fuse_frame_submit): the next frame's depth is
   // copied on a second stream into the other slot while the pending frame runs
@@ -100,6 +99,7 @@ struct vm_engine {
 
 extern "C" {
 static int settle(vm_engine *e);
+static int settle_all(vm_engine *e);
 }
 
 // ------------------------------------------------------------ helpers
@@ -169,11 +169,10 @@ static void launch_pdl(void (*kern)(KArgs...), int grid, int block, cudaStream_t
   cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
-// k_gc_normals with a fresh grid-barrier stamp; its grid is the occupancy
-// limit, so every CTA is resident once the previous kernel drains
+// k_gc_normals (its face-normal fallback records are applied by the next
+// frame's k_collect, or by flush_fallbacks)
 static void launch_gc(vm_engine *e, bool pdl, const int32_t *list, const int32_t *count_ptr, int count_const,
                       int mode) {
-  e->h_frame->bar_stamp = ++e->bar_seq;
   if (pdl)
     launch_pdl(k_gc_normals, e->grid_gc, kGT, e->stream, e->S, *e->h_frame, list, count_ptr, count_const, mode);
   else
@@ -283,6 +282,7 @@ static int complete_with_resume(vm_engine *e, int *resumes) {
 static void fill_frame_host(vm_engine *e, const double *depth_dev, int32_t h, int32_t w,
                             const vm_intrinsics *intr, const vm_pose *pose) {
   FrameDev &F = *e->h_frame;
+  F.consume_fb = 0;
   F.depth = depth_dev;
   F.h = h;
   F.w = w;
@@ -484,7 +484,6 @@ int vm_create(const vm_store_config *cfg, vm_engine **out) {
   TRY(dev_alloc(&S.scope, mb));
   TRY(dev_alloc(&S.halo, mb));
   TRY(dev_alloc(&S.ctr, 1, 0));
-  TRY(dev_alloc(&S.bar_flags, 32 * 32, 0));
   uint8_t slab_sel[8];   // mesher.py:518-525
   for (int m = 0; m < 8; m++) {
     uint8_t bits = 0;
@@ -519,7 +518,7 @@ int vm_destroy(vm_engine *e) {
   DevState &S = e->S;
   void *ptrs[] = {S.slots, S.ovf_head, S.ovf_lock, S.ovf_key, S.ovf_val, S.ovf_next, S.ovf_stamp, S.bcoord,
                   S.nbr, S.stamp_collect, S.stamp_halo, S.stamp_new, S.bowned, S.slab_bits, S.scope,
-                  S.halo, S.tsdf, S.weight, S.vmask, S.tp, S.tc, S.vbirth, S.vocc, S.vparam, S.vnrm, S.item_mask, S.fallback, S.bar_flags, e->d_rays,
+                  S.halo, S.tsdf, S.weight, S.vmask, S.tp, S.tc, S.vbirth, S.vocc, S.vparam, S.vnrm, S.item_mask, S.fallback, e->d_rays,
                   S.ctr, e->d_depth, e->d_scratch};
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -541,7 +540,7 @@ int vm_destroy(vm_engine *e) {
 
 int vm_set_stream(vm_engine *e, void *stream) {
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
-  TRY(settle(e));
+  TRY(settle_all(e));
   CK(cudaStreamSynchronize(e->stream));
   if (e->own_stream) CK(cudaStreamDestroy(e->stream));
   if (stream) {
@@ -583,7 +582,7 @@ int vm_phase_times(vm_engine *e, double *ms, int n) {
 
 int vm_reserve(vm_engine *e, int64_t blocks, int64_t vertices, int64_t triangles) {
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
-  TRY(settle(e));
+  TRY(settle_all(e));
   (void)vertices;
   (void)triangles;   // vertices live in edge slots, triangles are implicit
   if (blocks > e->S.block_cap) TRY(grow_blocks(e, std::min<int64_t>(blocks, e->S.max_blocks)));
@@ -699,6 +698,7 @@ int vm_fuse_frame_enqueue(vm_engine *e, const double *depth, int32_t h, int32_t 
   F.scope_mode = 0;
   TRY(ensure_rays(e, h, w));
   F.nsteps_fixed = fixed_nsteps(e, cfg->trunc);
+  F.consume_fb = 1;   // k_collect applies the previous frame's fallback records
   TRY(reset_call_counters(e));
   cudaStream_t st = e->stream;
   rec(e, PH_DEPTH);
@@ -744,6 +744,20 @@ static int settle(vm_engine *e) {
   fill_stats(e, e->pending_frame, &e->settled);
   e->settled_valid = 1;
   return VM_OK;
+}
+
+// Apply pending face-normal fallback records (kept between frames for the next
+// k_collect): every entry point outside the frame pipeline calls this first,
+// and the ones that run k_gc_normals themselves call it again at their end.
+static int flush_fallbacks(vm_engine *e) {
+  k_flush_fallbacks<<<e->sm_count * 4, 128, 0, e->stream>>>(e->S);
+  CK(cudaMemsetAsync(&e->S.ctr->fb_pending, 0, sizeof(int32_t), e->stream));
+  return check_launch();
+}
+
+static int settle_all(vm_engine *e) {
+  TRY(settle(e));
+  return flush_fallbacks(e);
 }
 
 int vm_fuse_frame_submit(vm_engine *e, const double *depth, int32_t h, int32_t w, int32_t depth_on_device,
@@ -805,7 +819,7 @@ int vm_collect(vm_engine *e, const double *depth, int32_t h, int32_t w, int32_t 
                const vm_intrinsics *intr, const vm_pose *pose, double trunc, double max_range,
                int64_t *n_out) {
   if (!e || !intr || !pose) return set_err(VM_ERR_INPUT, "null argument");
-  TRY(settle(e));
+  TRY(settle_all(e));
   const double *dd;
   TRY(stage_depth(e, depth, h, w, depth_on_device, &dd));
   fill_frame_host(e, dd, h, w, intr, pose);
@@ -827,7 +841,7 @@ int vm_collect(vm_engine *e, const double *depth, int32_t h, int32_t w, int32_t 
 
 int vm_get_collected(vm_engine *e, int32_t *coords_out, int64_t n) {
   if (!e || (!coords_out && n)) return set_err(VM_ERR_INPUT, "null argument");
-  TRY(settle(e));
+  TRY(settle_all(e));
   if (n == 0) return VM_OK;
   std::vector<int32_t> idx(n);
   CK(cudaMemcpyAsync(idx.data(), e->S.scope, (size_t)n * sizeof(int32_t), cudaMemcpyDeviceToHost, e->stream));
@@ -847,7 +861,7 @@ int vm_integrate(vm_engine *e, const int32_t *coords, int64_t n, const double *d
                  int32_t depth_on_device, const vm_intrinsics *intr, const vm_pose *pose, double trunc,
                  double max_range, int64_t weight_cap) {
   if (!e || !intr || !pose) return set_err(VM_ERR_INPUT, "null argument");
-  TRY(settle(e));
+  TRY(settle_all(e));
   const double *dd;
   TRY(stage_depth(e, depth, h, w, depth_on_device, &dd));
   fill_frame_host(e, dd, h, w, intr, pose);
@@ -888,7 +902,7 @@ int vm_integrate(vm_engine *e, const int32_t *coords, int64_t n, const double *d
 int vm_scope_halo(vm_engine *e, int64_t *n_scope, int32_t *scope_coords, uint8_t *scope_masks,
                   int64_t *n_halo, int32_t *halo_coords) {
   if (!e || !n_scope || !n_halo) return set_err(VM_ERR_INPUT, "null argument");
-  TRY(settle(e));
+  TRY(settle_all(e));
   CK(cudaMemsetAsync(&e->S.ctr->nslab, 0, sizeof(int32_t), e->stream));
   CK(cudaMemsetAsync(&e->S.ctr->nhalo, 0, sizeof(int32_t), e->stream));
   k_fuse_blocks<<<grid_blocks(e), kFB, 0, e->stream>>>(e->S, *e->h_frame, e->S.scope,
@@ -952,7 +966,7 @@ int vm_extract(vm_engine *e, const int32_t *scope_coords, const uint8_t *scope_m
                const int32_t *halo_coords, int64_t n_halo, int64_t frame_index, int32_t strategy,
                int32_t refine, double epsilon, int64_t *out2) {
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
-  TRY(settle(e));
+  TRY(settle_all(e));
   if (strategy < 0 || strategy > 2) return set_err(VM_ERR_VALUE, "unknown strategy %d", strategy);
   if (out2) { out2[0] = 0; out2[1] = 0; }
   if (n_scope <= 0) return VM_OK;   // mesher.py:564-565
@@ -990,6 +1004,7 @@ int vm_extract(vm_engine *e, const int32_t *scope_coords, const uint8_t *scope_m
   k_retype_place<<<e->grid_retype, kNT, kRetypeSmem, e->stream>>>(e->S, *e->h_frame);
   launch_gc(e, false, e->S.halo, &e->S.ctr->nhalo, 0, (int)(G_GC | G_NORMALS | G_COMMIT | G_REQUIRE_ITEMS));
   TRY(check_launch());
+  TRY(flush_fallbacks(e));
   TRY(read_counters(e));
   TRY(error_from_counters(e));
   if (out2) {
@@ -1001,7 +1016,7 @@ int vm_extract(vm_engine *e, const int32_t *scope_coords, const uint8_t *scope_m
 
 int vm_garbage_collect(vm_engine *e, const int32_t *coords, int64_t n, int64_t *freed) {
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
-  TRY(settle(e));
+  TRY(settle_all(e));
   TRY(reset_call_counters(e));
   int32_t *di = nullptr;
   if (n > 0) TRY(map_coords(e, coords, n, &di, nullptr, 0, false));
@@ -1015,13 +1030,14 @@ int vm_garbage_collect(vm_engine *e, const int32_t *coords, int64_t n, int64_t *
 
 int vm_compute_normals(vm_engine *e, const int32_t *coords, int64_t n) {
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
-  TRY(settle(e));
+  TRY(settle_all(e));
   TRY(reset_call_counters(e));
   if (n <= 0) return VM_OK;
   e->h_frame->epoch = ++e->epoch;
   int32_t *di;
   TRY(map_coords(e, coords, n, &di, e->S.stamp_halo, e->epoch, false));
   launch_gc(e, false, di, nullptr, (int)n, (int)G_NORMALS);
+  TRY(flush_fallbacks(e));
   TRY(check_launch());
   TRY(read_counters(e));
   return error_from_counters(e);
@@ -1030,7 +1046,7 @@ int vm_compute_normals(vm_engine *e, const int32_t *coords, int64_t n) {
 int vm_refine_eval(vm_engine *e, const uint8_t *t_curr, const uint8_t *t_prev, const double *corners,
                    int64_t n, double epsilon, int32_t *out) {
   if (!e || !t_curr || !t_prev || !corners || !out) return set_err(VM_ERR_INPUT, "null argument");
-  TRY(settle(e));
+  TRY(settle_all(e));
   if (n <= 0) return VM_OK;
   void *buf;
   const size_t o1 = ((size_t)n + 255) & ~(size_t)255, o2 = o1 * 2, o3 = o2 + (size_t)n * 64;
@@ -1051,7 +1067,7 @@ int vm_refine_eval(vm_engine *e, const uint8_t *t_curr, const uint8_t *t_prev, c
 int vm_block_in_frustum(vm_engine *e, const int32_t *coords, int64_t n, const vm_pose *pose,
                         const vm_intrinsics *intr, uint8_t *out) {
   if (!e || !coords || !pose || !intr || !out) return set_err(VM_ERR_INPUT, "null argument");
-  TRY(settle(e));
+  TRY(settle_all(e));
   if (n <= 0) return VM_OK;
   fill_frame_host(e, nullptr, 0, 0, intr, pose);
   void *buf;
@@ -1069,7 +1085,7 @@ int vm_block_in_frustum(vm_engine *e, const int32_t *coords, int64_t n, const vm
 // ---- store access -----------------------------------------------------------
 int vm_set_blocks(vm_engine *e, const int32_t *coords, int64_t n, const double *tsdf, const int32_t *weight) {
   if (!e || (!coords && n)) return set_err(VM_ERR_INPUT, "null argument");
-  TRY(settle(e));
+  TRY(settle_all(e));
   if (n <= 0) return VM_OK;
   TRY(reset_call_counters(e));
   int32_t *di;
@@ -1103,7 +1119,7 @@ int vm_set_blocks(vm_engine *e, const int32_t *coords, int64_t n, const double *
 
 int vm_lookup(vm_engine *e, const int32_t *coords, int64_t n, uint8_t *out) {
   if (!e || ((!coords || !out) && n)) return set_err(VM_ERR_INPUT, "null argument");
-  TRY(settle(e));
+  TRY(settle_all(e));
   if (n <= 0) return VM_OK;
   int32_t *di;
   TRY(map_coords(e, coords, n, &di, nullptr, 0, false));
@@ -1116,7 +1132,7 @@ int vm_lookup(vm_engine *e, const int32_t *coords, int64_t n, uint8_t *out) {
 
 int vm_counters(vm_engine *e, vm_counter_set *out) {
   if (!e || !out) return set_err(VM_ERR_INPUT, "null argument");
-  TRY(settle(e));
+  TRY(settle_all(e));
   TRY(read_counters(e));
   const Counters &c = *e->h_ctr;
   out->block_count = e->S.nranks > 1 ? c.nblocks_owned : c.nblocks;
@@ -1138,7 +1154,7 @@ int vm_counters(vm_engine *e, vm_counter_set *out) {
 int vm_snapshot_blocks(vm_engine *e, int64_t n, int32_t *coords, double *tsdf, int32_t *weight, uint8_t *tp,
                        uint8_t *tc, int32_t *ev, int32_t *tri) {
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
-  TRY(settle(e));
+  TRY(settle_all(e));
   TRY(read_counters(e));
   if (n != e->h_ctr->nblocks)
     return set_err(VM_ERR_INPUT, "snapshot size %lld != block count %d", (long long)n, e->h_ctr->nblocks);
@@ -1170,7 +1186,7 @@ int vm_snapshot_blocks(vm_engine *e, int64_t n, int32_t *coords, double *tsdf, i
 int vm_snapshot_vertices(vm_engine *e, int64_t n, double *pos, double *nrm, int32_t *ref, int32_t *birth,
                          uint8_t *alive, int32_t *free_stack) {
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
-  TRY(settle(e));
+  TRY(settle_all(e));
   TRY(read_counters(e));
   const int64_t count = e->h_ctr->v_count, live = e->h_ctr->v_live;
   if (n != count) return set_err(VM_ERR_INPUT, "snapshot size mismatch");
@@ -1217,7 +1233,7 @@ int vm_snapshot_vertices(vm_engine *e, int64_t n, double *pos, double *nrm, int3
 
 int vm_snapshot_triangles(vm_engine *e, int64_t n, int32_t *verts, uint8_t *alive, int32_t *free_stack) {
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
-  TRY(settle(e));
+  TRY(settle_all(e));
   TRY(read_counters(e));
   const int64_t count = e->h_ctr->t_count, live = e->h_ctr->t_live;
   if (n != count) return set_err(VM_ERR_INPUT, "snapshot size mismatch");
@@ -1237,7 +1253,7 @@ int vm_snapshot_triangles(vm_engine *e, int64_t n, int32_t *verts, uint8_t *aliv
 // ---- outputs ------------------------------------------------------------------
 int vm_irregular_count(vm_engine *e, int64_t *out) {
   if (!e || !out) return set_err(VM_ERR_INPUT, "null argument");
-  TRY(settle(e));
+  TRY(settle_all(e));
   TRY(read_counters(e));
   void *buf;
   TRY(scratch(e, 64, &buf));
@@ -1257,7 +1273,7 @@ int vm_irregular_count(vm_engine *e, int64_t *out) {
 
 int vm_compact(vm_engine *e, int64_t current_frame, int64_t *n_vertices, int64_t *n_triangles) {
   if (!e || !n_vertices || !n_triangles) return set_err(VM_ERR_INPUT, "null argument");
-  TRY(settle(e));
+  TRY(settle_all(e));
   TRY(run_compaction(e, current_frame, false));
   *n_vertices = e->comp.nv;
   *n_triangles = e->comp.nt;
@@ -1279,7 +1295,7 @@ int vm_compact_fetch(vm_engine *e, double *pos, double *nrm, int64_t *ages, int3
 int vm_export_blocks(vm_engine *e, int32_t owned_only, int64_t *n_out, int32_t *coords, double *tsdf,
                      int32_t *weight, uint8_t *tp, uint8_t *tc, int32_t *birth, double *param, double *normal) {
   if (!e || !n_out) return set_err(VM_ERR_INPUT, "null argument");
-  TRY(settle(e));
+  TRY(settle_all(e));
   TRY(read_counters(e));
   const int nb = e->h_ctr->nblocks;
   std::vector<uint8_t> own(nb);
@@ -1310,7 +1326,7 @@ int vm_import_blocks(vm_engine *e, int64_t n, const int32_t *coords, const doubl
                      const uint8_t *tp, const uint8_t *tc, const int32_t *birth, const double *param,
                      const double *normal) {
   if (!e || (n && !coords)) return set_err(VM_ERR_INPUT, "null argument");
-  TRY(settle(e));
+  TRY(settle_all(e));
   if (n <= 0) return VM_OK;
   TRY(reset_call_counters(e));
   int32_t *di;
@@ -1351,7 +1367,7 @@ int vm_import_blocks(vm_engine *e, int64_t n, const int32_t *coords, const doubl
 // slot; conservation compares the pool counters with full recounts.
 int vm_audit(vm_engine *e, vm_audit_report *out) {
   if (!e || !out) return set_err(VM_ERR_INPUT, "null argument");
-  TRY(settle(e));
+  TRY(settle_all(e));
   TRY(read_counters(e));
   const Counters c = *e->h_ctr;
   unsigned long long *sums;

@@ -160,6 +160,176 @@ __global__ void k_norm_bounds(const FrameDev F, unsigned long long *out, double 
   atomicMax(out + 1, hi);
 }
 
+// ------------------------------------------------------------ face-normal fallback
+// edge index, in the neighbour cube owner - du*e_u - dw*e_w, of the edge slot
+// owned along `axis` (u, w the other two axes)
+// (register-only: [axis][du*2+dw] packed 4 bits each -- per-thread axes would
+// make a constant-bank table read serialise)
+__device__ __forceinline__ int cube_edge_of_slot(int axis, int du, int dw) {
+  constexpr unsigned long long kTab = 0x0ull | 4ull << 4 | 2ull << 8 | 6ull << 12 | 3ull << 16 | 7ull << 20 |
+                                      1ull << 24 | 5ull << 28 | 8ull << 32 | 11ull << 36 | 9ull << 40 | 10ull << 44;
+  return (int)((kTab >> (4 * (axis * 4 + du * 2 + dw))) & 15ull);
+}
+
+// position q of the 9^3 type tile over cube locals -1..7 -> neighbour
+// direction and source cube (index arithmetic, no table load on the chain)
+__device__ __forceinline__ void type_tile_src(int q, int &dir, int &src) {
+  const int a = q / 81, r = q - a * 81, bb = r / 9, cc = r - bb * 9;
+  const int lx = a - 1, ly = bb - 1, lz = cc - 1;
+  dir = nbr_dir(lx < 0 ? -1 : 0, ly < 0 ? -1 : 0, lz < 0 ? -1 : 0);
+  src = (lx & 7) * 64 + (ly & 7) * 8 + (lz & 7);
+}
+
+// edge e -> owner-cube offset (x | y<<1 | z<<2) | axis << 3, 5 bits per edge (mc_tables.py:44-64)
+__host__ __device__ constexpr unsigned long long edge_own_axis(int e) {
+  constexpr int own[12] = {0, 1, 2, 0, 4, 5, 6, 4, 0, 1, 3, 2};
+  constexpr int axis[12] = {0, 1, 0, 1, 0, 1, 0, 1, 2, 2, 2, 2};
+  return (unsigned long long)(own[e] | axis[e] << 3);
+}
+constexpr unsigned long long kEdgeOwnAxis =
+    edge_own_axis(0) | edge_own_axis(1) << 5 | edge_own_axis(2) << 10 | edge_own_axis(3) << 15 |
+    edge_own_axis(4) << 20 | edge_own_axis(5) << 25 | edge_own_axis(6) << 30 | edge_own_axis(7) << 35 |
+    edge_own_axis(8) << 40 | edge_own_axis(9) << 45 | edge_own_axis(10) << 50 | edge_own_axis(11) << 55;
+
+// The 4 cubes around the edge slot (slot_ci, axis): candidate j = (du, dw) =
+// (j >> 1, j & 1) sits at -du along u and -dw along w (u, w = the other two
+// axes), i.e. at cube locals (l0, l1, l2) in [-1, 7]^3.
+__device__ __forceinline__ void slot_cube(int slot_ci, int axis, int j, int &l0, int &l1, int &l2) {
+  const int du = j >> 1, dw = j & 1;
+  l0 = (slot_ci >> 6) - (axis == 0 ? 0 : du);
+  l1 = ((slot_ci >> 3) & 7) - (axis == 0 ? du : 0) - (axis == 2 ? dw : 0);
+  l2 = (slot_ci & 7) - (axis == 2 ? 0 : dw);
+}
+
+// Face-normal fallback for one vertex, computed by one warp (mesher.py:456-486).
+// `types4` holds the types of the 4 cubes around the slot (byte j = candidate
+// j), `cand` flags the candidates whose triangles count (edge in the cube's
+// mask, cube inside a halo block of this call); lanes 0..26 hold the block's
+// neighbour row in `nbr_lane`.  Lane l handles (incident cube j = l / 5,
+// triangle slot s = l % 5); the contributions are then summed by lane 0 in the
+// reference's order: vertex position k major, then halo blocks in sorted order,
+// then cube, then triangle slot -- bit-identical to np.add.at's.
+__device__ __forceinline__ void fallback_normal_warp(const double *__restrict__ vparam, double cube_size,
+                                                     int nbr_lane, uint32_t types4, uint32_t cand, int4 bc,
+                                                     int slot_ci, int axis, double *dst) {
+  const int lane = threadIdx.x & 31;
+  // the vertex's current normal ("never set" test) is requested first
+  const double o0 = lane == 0 ? dst[0] : 0.0, o1 = lane == 0 ? dst[1] : 0.0, o2 = lane == 0 ? dst[2] : 0.0;
+  // lane l: candidate cube j = l / 5, triangle slot s = l % 5
+  const int j = lane / 5, s = lane % 5;
+  const int jj = j < 4 ? j : 0;
+  int m0, m1, m2;
+  slot_cube(slot_ci, axis, jj, m0, m1, m2);
+  const int tt = (types4 >> (8 * jj)) & 0xFF;
+  const int e = cube_edge_of_slot(axis, jj >> 1, jj & 1);
+  // rank of the candidate cube by (sorted block, cube) key among the valid ones
+  int jrank = 0;
+  {
+    auto key = [&](int q) {
+      int a0, a1, a2;
+      slot_cube(slot_ci, axis, q, a0, a1, a2);
+      const int dx = a0 < 0 ? -1 : 0, dy = a1 < 0 ? -1 : 0, dz = a2 < 0 ? -1 : 0;
+      return (((dx + 1) * 4 + (dy + 1) * 2 + (dz + 1)) << 9) | ((a0 & 7) * 64 + (a1 & 7) * 8 + (a2 & 7));
+    };
+    const int mine = key(jj);
+#pragma unroll
+    for (int q = 0; q < 4; q++) jrank += ((cand >> q) & 1) && key(q) < mine;
+  }
+  const bool my_valid = j < 4 && ((cand >> jj) & 1) && s < c_tri_count[tt];
+  const unsigned long long packed = c_tri_packed[tt];
+  int kpos = -1;
+  if (my_valid) {
+#pragma unroll
+    for (int q = 0; q < 3; q++)
+      if ((int)((packed >> (4 * (3 * s + q))) & 0xF) == e) kpos = q;
+  }
+  // owner block of each of the triangle's 3 vertices (shuffled from the row)
+  int obq[3], oxq[3], oyq[3], ozq[3], axq[3];
+#pragma unroll
+  for (int q = 0; q < 3; q++) {
+    const int eq = (int)((packed >> (4 * (3 * s + q))) & 0xF);
+    const int oa = (int)((kEdgeOwnAxis >> (5 * eq)) & 31);   // owner offset | axis << 3
+    const int own = oa & 7;
+    axq[q] = oa >> 3;
+    oxq[q] = m0 + (own & 1); oyq[q] = m1 + ((own >> 1) & 1); ozq[q] = m2 + ((own >> 2) & 1);
+    const int dir = nbr_dir(oxq[q] < 0 ? -1 : oxq[q] >> 3, oyq[q] < 0 ? -1 : oyq[q] >> 3,
+                            ozq[q] < 0 ? -1 : ozq[q] >> 3);
+    obq[q] = __shfl_sync(0xffffffffu, nbr_lane, dir);
+  }
+  double fn[3] = {0.0, 0.0, 0.0};
+  if (kpos >= 0) {
+    double p[3][3];
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+      const int ox = oxq[q], oy = oyq[q], oz = ozq[q], ax = axq[q];
+      const double pa = vparam[(size_t)obq[q] * kEV + ((ox & 7) * 64 + (oy & 7) * 8 + (oz & 7)) * 3 + ax];
+      const double gx = __dmul_rn((double)(bc.x * kB + ox), cube_size);
+      const double gy = __dmul_rn((double)(bc.y * kB + oy), cube_size);
+      const double gz = __dmul_rn((double)(bc.z * kB + oz), cube_size);
+      p[q][0] = ax == 0 ? pa : gx;
+      p[q][1] = ax == 1 ? pa : gy;
+      p[q][2] = ax == 2 ? pa : gz;
+    }
+    const double a[3] = {p[1][0] - p[0][0], p[1][1] - p[0][1], p[1][2] - p[0][2]};
+    const double bb[3] = {p[2][0] - p[0][0], p[2][1] - p[0][1], p[2][2] - p[0][2]};
+    fn[0] = __dmul_rn(a[1], bb[2]) - __dmul_rn(a[2], bb[1]);
+    fn[1] = __dmul_rn(a[2], bb[0]) - __dmul_rn(a[0], bb[2]);
+    fn[2] = __dmul_rn(a[0], bb[1]) - __dmul_rn(a[1], bb[0]);
+  }
+  // ordered accumulation: k major, then cube rank, then triangle slot
+  int mykey = kpos >= 0 ? (kpos * 4 + jrank) * 5 + s : (1 << 20);
+  double acc[3] = {0.0, 0.0, 0.0};
+  const int npend = __popc(__ballot_sync(0xffffffffu, kpos >= 0));
+  for (int it = 0; it < npend; it++) {
+    int best = mykey, bl = lane;   // pending lane with the smallest key
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const int ok = __shfl_xor_sync(0xffffffffu, best, o), ol = __shfl_xor_sync(0xffffffffu, bl, o);
+      if (ok < best || (ok == best && ol < bl)) { best = ok; bl = ol; }
+    }
+    acc[0] = __dadd_rn(acc[0], __shfl_sync(0xffffffffu, fn[0], bl));
+    acc[1] = __dadd_rn(acc[1], __shfl_sync(0xffffffffu, fn[1], bl));
+    acc[2] = __dadd_rn(acc[2], __shfl_sync(0xffffffffu, fn[2], bl));
+    if (lane == bl) mykey = 1 << 20;
+  }
+  if (lane == 0) {
+    const double nrm = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(acc[0], acc[0]), __dmul_rn(acc[1], acc[1])),
+                                      __dmul_rn(acc[2], acc[2])));
+    if (nrm > 1e-20) {
+      dst[0] = (-1.0 * acc[0]) / nrm;
+      dst[1] = (-1.0 * acc[1]) / nrm;
+      dst[2] = (-1.0 * acc[2]) / nrm;
+    } else if (o0 == 0.0 && o1 == 0.0 && o2 == 0.0) {
+      dst[2] = 1.0;
+    }
+  }
+}
+
+struct FallbackArgs {   // what the consumer touches (passed by value: no DevState copy in local memory)
+  Counters *ctr;
+  const int4 *fallback;
+  const int32_t *nbr;
+  const int4 *bcoord;
+  const double *vparam;
+  double *vnrm;
+  double cube_size;
+};
+
+// The call's face-normal fallback worklist, after the grid barrier: entries
+// are spread statically over every warp of the grid, one warp per entry.
+// Apply fallback records [0, n): warp `first` of `nwarps` takes every nwarps-th.
+__device__ __noinline__ void consume_fallbacks(const FallbackArgs S, int n, int first, int nwarps) {
+  const int lane = threadIdx.x & 31;
+  for (int f = first; f < n; f += nwarps) {
+    const int4 rec = __ldcg(S.fallback + f);
+    const int b = rec.x, sl = rec.y;
+    const int nbr_lane = lane < 27 ? (lane == 13 ? b : __ldcg(S.nbr + (size_t)b * 27 + lane)) : -1;
+    const int4 bc = __ldcg(S.bcoord + b);
+    fallback_normal_warp(S.vparam, S.cube_size, nbr_lane, (uint32_t)rec.z, (uint32_t)rec.w, bc, sl / 3, sl % 3,
+                         S.vnrm + 3 * ((size_t)b * kEV + sl));
+  }
+}
+
 // ------------------------------------------------------------ collect
 // fusion.py:95-106 + store.py:296-320.  A CTA covers a 64x8-pixel region (two
 // pixels per thread, coalesced rows).  The band samples' block keys are first
@@ -212,6 +382,17 @@ __global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, cons
   __shared__ int s_n, s_nover, s_valid, s_nout, s_base;
   const int t = threadIdx.x, lane = t & 31;
   const int rx = (F.w + kRegionW - 1) / kRegionW, ry = (F.h + kRegionH - 1) / kRegionH;
+  // The previous frame's face-normal fallback records (k_gc_normals) are
+  // applied here, by the CTAs that have no pixel region (else by every CTA
+  // after its regions): nothing in this kernel reads or writes what they use
+  // (types, vertex coordinates, neighbour rows) and the idle warps absorb them.
+  const int nreg = rx * ry, wpc = kCollectThreads / 32;
+  const bool spare = (int)gridDim.x > nreg;
+  if (F.consume_fb && spare && (int)blockIdx.x >= nreg) {
+    const int nfb = ld_vol(&ctr->fb_pending);
+    consume_fallbacks(FallbackArgs{S.ctr, S.fallback, S.nbr, S.bcoord, S.vparam, S.vnrm, S.cube_size}, nfb,
+                      (blockIdx.x - nreg) * wpc + (t >> 5), ((int)gridDim.x - nreg) * wpc);
+  }
   int nvalid = 0, nth = 0;
   if (t == 0) s_valid = 0;
   for (int reg = blockIdx.x; reg < rx * ry; reg += gridDim.x, nth++) {
@@ -313,6 +494,11 @@ __global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, cons
     __syncthreads();   // the set is reset for the next region
     trace_item(S, TK_COLLECT, nth, 3);
   }
+  if (F.consume_fb && !spare) {
+    const int nfb = ld_vol(&ctr->fb_pending);
+    consume_fallbacks(FallbackArgs{S.ctr, S.fallback, S.nbr, S.bcoord, S.vparam, S.vnrm, S.cube_size}, nfb,
+                      blockIdx.x * wpc + (t >> 5), (int)gridDim.x * wpc);
+  }
   if (F.nsteps_fixed > 0) {   // valid-pixel count (k_depth_stats did not run): one atomic per CTA
     nvalid = __reduce_add_sync(0xffffffffu, (unsigned)nvalid);
     if (lane == 0 && nvalid) atomicAdd(&s_valid, nvalid);
@@ -399,6 +585,7 @@ __global__ void __launch_bounds__(kFB, 6) k_fuse_blocks(DevState S, const FrameD
   read_prologue(S, s_pro, count_ptr, nullptr, nullptr, (int)blockIdx.x < list_cap ? list + blockIdx.x : nullptr);
   if (s_pro[0]) return;
   const int n = count_ptr ? s_pro[1] : count_const;
+  if (F.consume_fb && blockIdx.x == 0 && threadIdx.x == 0) S.ctr->fb_pending = 0;   // (k_collect applied them)
   trace_at(S, TK_FUSE, 1);
   int nth = 0;
   const int t = threadIdx.x;
@@ -959,176 +1146,6 @@ constexpr size_t kRetypeSmem = 0;
 
 
 // ------------------------------------------------------------ GC + normals
-// edge index, in the neighbour cube owner - du*e_u - dw*e_w, of the edge slot
-// owned along `axis` (u, w the other two axes)
-// (register-only: [axis][du*2+dw] packed 4 bits each -- per-thread axes would
-// make a constant-bank table read serialise)
-__device__ __forceinline__ int cube_edge_of_slot(int axis, int du, int dw) {
-  constexpr unsigned long long kTab = 0x0ull | 4ull << 4 | 2ull << 8 | 6ull << 12 | 3ull << 16 | 7ull << 20 |
-                                      1ull << 24 | 5ull << 28 | 8ull << 32 | 11ull << 36 | 9ull << 40 | 10ull << 44;
-  return (int)((kTab >> (4 * (axis * 4 + du * 2 + dw))) & 15ull);
-}
-
-// position q of the 9^3 type tile over cube locals -1..7 -> neighbour
-// direction and source cube (index arithmetic, no table load on the chain)
-__device__ __forceinline__ void type_tile_src(int q, int &dir, int &src) {
-  const int a = q / 81, r = q - a * 81, bb = r / 9, cc = r - bb * 9;
-  const int lx = a - 1, ly = bb - 1, lz = cc - 1;
-  dir = nbr_dir(lx < 0 ? -1 : 0, ly < 0 ? -1 : 0, lz < 0 ? -1 : 0);
-  src = (lx & 7) * 64 + (ly & 7) * 8 + (lz & 7);
-}
-
-// edge e -> owner-cube offset (x | y<<1 | z<<2) | axis << 3, 5 bits per edge (mc_tables.py:44-64)
-__host__ __device__ constexpr unsigned long long edge_own_axis(int e) {
-  constexpr int own[12] = {0, 1, 2, 0, 4, 5, 6, 4, 0, 1, 3, 2};
-  constexpr int axis[12] = {0, 1, 0, 1, 0, 1, 0, 1, 2, 2, 2, 2};
-  return (unsigned long long)(own[e] | axis[e] << 3);
-}
-constexpr unsigned long long kEdgeOwnAxis =
-    edge_own_axis(0) | edge_own_axis(1) << 5 | edge_own_axis(2) << 10 | edge_own_axis(3) << 15 |
-    edge_own_axis(4) << 20 | edge_own_axis(5) << 25 | edge_own_axis(6) << 30 | edge_own_axis(7) << 35 |
-    edge_own_axis(8) << 40 | edge_own_axis(9) << 45 | edge_own_axis(10) << 50 | edge_own_axis(11) << 55;
-
-// The 4 cubes around the edge slot (slot_ci, axis): candidate j = (du, dw) =
-// (j >> 1, j & 1) sits at -du along u and -dw along w (u, w = the other two
-// axes), i.e. at cube locals (l0, l1, l2) in [-1, 7]^3.
-__device__ __forceinline__ void slot_cube(int slot_ci, int axis, int j, int &l0, int &l1, int &l2) {
-  const int du = j >> 1, dw = j & 1;
-  l0 = (slot_ci >> 6) - (axis == 0 ? 0 : du);
-  l1 = ((slot_ci >> 3) & 7) - (axis == 0 ? du : 0) - (axis == 2 ? dw : 0);
-  l2 = (slot_ci & 7) - (axis == 2 ? 0 : dw);
-}
-
-// Face-normal fallback for one vertex, computed by one warp (mesher.py:456-486).
-// `types4` holds the types of the 4 cubes around the slot (byte j = candidate
-// j), `cand` flags the candidates whose triangles count (edge in the cube's
-// mask, cube inside a halo block of this call); lanes 0..26 hold the block's
-// neighbour row in `nbr_lane`.  Lane l handles (incident cube j = l / 5,
-// triangle slot s = l % 5); the contributions are then summed by lane 0 in the
-// reference's order: vertex position k major, then halo blocks in sorted order,
-// then cube, then triangle slot -- bit-identical to np.add.at's.
-__device__ __forceinline__ void fallback_normal_warp(const double *__restrict__ vparam, double cube_size,
-                                                     int nbr_lane, uint32_t types4, uint32_t cand, int4 bc,
-                                                     int slot_ci, int axis, double *dst) {
-  const int lane = threadIdx.x & 31;
-  // the vertex's current normal ("never set" test) is requested first
-  const double o0 = lane == 0 ? dst[0] : 0.0, o1 = lane == 0 ? dst[1] : 0.0, o2 = lane == 0 ? dst[2] : 0.0;
-  // lane l: candidate cube j = l / 5, triangle slot s = l % 5
-  const int j = lane / 5, s = lane % 5;
-  const int jj = j < 4 ? j : 0;
-  int m0, m1, m2;
-  slot_cube(slot_ci, axis, jj, m0, m1, m2);
-  const int tt = (types4 >> (8 * jj)) & 0xFF;
-  const int e = cube_edge_of_slot(axis, jj >> 1, jj & 1);
-  // rank of the candidate cube by (sorted block, cube) key among the valid ones
-  int jrank = 0;
-  {
-    auto key = [&](int q) {
-      int a0, a1, a2;
-      slot_cube(slot_ci, axis, q, a0, a1, a2);
-      const int dx = a0 < 0 ? -1 : 0, dy = a1 < 0 ? -1 : 0, dz = a2 < 0 ? -1 : 0;
-      return (((dx + 1) * 4 + (dy + 1) * 2 + (dz + 1)) << 9) | ((a0 & 7) * 64 + (a1 & 7) * 8 + (a2 & 7));
-    };
-    const int mine = key(jj);
-#pragma unroll
-    for (int q = 0; q < 4; q++) jrank += ((cand >> q) & 1) && key(q) < mine;
-  }
-  const bool my_valid = j < 4 && ((cand >> jj) & 1) && s < c_tri_count[tt];
-  const unsigned long long packed = c_tri_packed[tt];
-  int kpos = -1;
-  if (my_valid) {
-#pragma unroll
-    for (int q = 0; q < 3; q++)
-      if ((int)((packed >> (4 * (3 * s + q))) & 0xF) == e) kpos = q;
-  }
-  // owner block of each of the triangle's 3 vertices (shuffled from the row)
-  int obq[3], oxq[3], oyq[3], ozq[3], axq[3];
-#pragma unroll
-  for (int q = 0; q < 3; q++) {
-    const int eq = (int)((packed >> (4 * (3 * s + q))) & 0xF);
-    const int oa = (int)((kEdgeOwnAxis >> (5 * eq)) & 31);   // owner offset | axis << 3
-    const int own = oa & 7;
-    axq[q] = oa >> 3;
-    oxq[q] = m0 + (own & 1); oyq[q] = m1 + ((own >> 1) & 1); ozq[q] = m2 + ((own >> 2) & 1);
-    const int dir = nbr_dir(oxq[q] < 0 ? -1 : oxq[q] >> 3, oyq[q] < 0 ? -1 : oyq[q] >> 3,
-                            ozq[q] < 0 ? -1 : ozq[q] >> 3);
-    obq[q] = __shfl_sync(0xffffffffu, nbr_lane, dir);
-  }
-  double fn[3] = {0.0, 0.0, 0.0};
-  if (kpos >= 0) {
-    double p[3][3];
-#pragma unroll
-    for (int q = 0; q < 3; q++) {
-      const int ox = oxq[q], oy = oyq[q], oz = ozq[q], ax = axq[q];
-      const double pa = vparam[(size_t)obq[q] * kEV + ((ox & 7) * 64 + (oy & 7) * 8 + (oz & 7)) * 3 + ax];
-      const double gx = __dmul_rn((double)(bc.x * kB + ox), cube_size);
-      const double gy = __dmul_rn((double)(bc.y * kB + oy), cube_size);
-      const double gz = __dmul_rn((double)(bc.z * kB + oz), cube_size);
-      p[q][0] = ax == 0 ? pa : gx;
-      p[q][1] = ax == 1 ? pa : gy;
-      p[q][2] = ax == 2 ? pa : gz;
-    }
-    const double a[3] = {p[1][0] - p[0][0], p[1][1] - p[0][1], p[1][2] - p[0][2]};
-    const double bb[3] = {p[2][0] - p[0][0], p[2][1] - p[0][1], p[2][2] - p[0][2]};
-    fn[0] = __dmul_rn(a[1], bb[2]) - __dmul_rn(a[2], bb[1]);
-    fn[1] = __dmul_rn(a[2], bb[0]) - __dmul_rn(a[0], bb[2]);
-    fn[2] = __dmul_rn(a[0], bb[1]) - __dmul_rn(a[1], bb[0]);
-  }
-  // ordered accumulation: k major, then cube rank, then triangle slot
-  int mykey = kpos >= 0 ? (kpos * 4 + jrank) * 5 + s : (1 << 20);
-  double acc[3] = {0.0, 0.0, 0.0};
-  const int npend = __popc(__ballot_sync(0xffffffffu, kpos >= 0));
-  for (int it = 0; it < npend; it++) {
-    int best = mykey, bl = lane;   // pending lane with the smallest key
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const int ok = __shfl_xor_sync(0xffffffffu, best, o), ol = __shfl_xor_sync(0xffffffffu, bl, o);
-      if (ok < best || (ok == best && ol < bl)) { best = ok; bl = ol; }
-    }
-    acc[0] = __dadd_rn(acc[0], __shfl_sync(0xffffffffu, fn[0], bl));
-    acc[1] = __dadd_rn(acc[1], __shfl_sync(0xffffffffu, fn[1], bl));
-    acc[2] = __dadd_rn(acc[2], __shfl_sync(0xffffffffu, fn[2], bl));
-    if (lane == bl) mykey = 1 << 20;
-  }
-  if (lane == 0) {
-    const double nrm = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(acc[0], acc[0]), __dmul_rn(acc[1], acc[1])),
-                                      __dmul_rn(acc[2], acc[2])));
-    if (nrm > 1e-20) {
-      dst[0] = (-1.0 * acc[0]) / nrm;
-      dst[1] = (-1.0 * acc[1]) / nrm;
-      dst[2] = (-1.0 * acc[2]) / nrm;
-    } else if (o0 == 0.0 && o1 == 0.0 && o2 == 0.0) {
-      dst[2] = 1.0;
-    }
-  }
-}
-
-struct FallbackArgs {   // what the consumer touches (passed by value: no DevState copy in local memory)
-  Counters *ctr;
-  const int4 *fallback;
-  const int32_t *nbr;
-  const int4 *bcoord;
-  const double *vparam;
-  double *vnrm;
-  double cube_size;
-};
-
-// The call's face-normal fallback worklist, after the grid barrier: entries
-// are spread statically over every warp of the grid, one warp per entry.
-__device__ __noinline__ void consume_fallbacks(const FallbackArgs S) {
-  const int lane = threadIdx.x & 31;
-  const int nwarps = (blockDim.x >> 5) * gridDim.x;
-  const int n = __ldcg(&S.ctr->nfallback);
-  for (int f = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); f < n; f += nwarps) {
-    const int4 rec = __ldcg(S.fallback + f);
-    const int b = rec.x, sl = rec.y;
-    const int nbr_lane = lane < 27 ? (lane == 13 ? b : __ldcg(S.nbr + (size_t)b * 27 + lane)) : -1;
-    const int4 bc = __ldcg(S.bcoord + b);
-    fallback_normal_warp(S.vparam, S.cube_size, nbr_lane, (uint32_t)rec.z, (uint32_t)rec.w, bc, sl / 3, sl % 3,
-                         S.vnrm + 3 * ((size_t)b * kEV + sl));
-  }
-}
-
 constexpr int kGT = 32;   // threads per CTA of k_gc_normals (one warp per halo block)
 // type tile over cube locals -1..7: 81 columns (lx, ly) of 16 bytes, z = 0..7
 // at bytes 0..7 and z = -1 at byte 15 (the -z neighbour's z = 7, fetched as
@@ -1150,44 +1167,6 @@ __device__ __forceinline__ bool sample_valid(const uint32_t *s_vm, int lx, int l
 __device__ __forceinline__ size_t sample_index(const int *s_nbr, int lx, int ly, int lz) {
   const int nb = s_nbr[nbr_dir(lx >> 3, ly >> 3, lz >> 3)];
   return nb < 0 ? ~(size_t)0 : (size_t)nb * kNC + ((lx & 7) * 64 + (ly & 7) * 8 + (lz & 7));
-}
-
-// Grid barrier.  k_gc_normals' grid is the occupancy limit (every CTA fits on
-// the GPU at once) and its CTAs never wait on later work, so all arrive.  CTAs
-// arrive on one per-call counter; the last arriver releases 32 flags on
-// separate lines with the launch's stamp, and each CTA polls its group's flag
-// (polling spread over 32 lines).  A wait far beyond any frame's duration
-// raises an error instead of spinning forever.
-__device__ __forceinline__ bool grid_barrier(const DevState &S, int32_t *count, int32_t *flags, int stamp) {
-  __shared__ int s_ok;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int ok = 1;
-    __threadfence();
-    if (atomicAdd(count, 1) == (int)gridDim.x - 1) {
-#pragma unroll 1
-      for (int g = 0; g < 32; g++) *(volatile int32_t *)(flags + g * 32) = stamp;
-    } else {
-      // back off exponentially: a spinning warp steals issue slots from the
-      // CTAs still working on the same SM
-      volatile int32_t *f = flags + (blockIdx.x & 31) * 32;
-      long long spins = 0;
-      unsigned ns = 64;
-      while (*f != stamp) {
-        __nanosleep(ns);
-        ns = ns < 1024 ? 2 * ns : 1024;
-        if (++spins > (1LL << 21)) {   // > ~2 s
-          set_error(S, ERR_CONSISTENCY, 50);
-          ok = 0;
-          break;
-        }
-      }
-    }
-    __threadfence();
-    s_ok = ok;
-  }
-  __syncthreads();
-  return s_ok != 0;
 }
 
 // One CTA of 64 threads per listed (halo) block:
@@ -1414,7 +1393,7 @@ __global__ void __launch_bounds__(kGT, 20) k_gc_normals(DevState S, const FrameD
               s_inhalo[dir])
             cand |= 1u << q;
         }
-        S.fallback[atomicAdd(&ctr->nfallback, 1)] = make_int4(b, sl, (int)types4, (int)cand);
+        S.fallback[atomicAdd(&ctr->fb_pending, 1)] = make_int4(b, sl, (int)types4, (int)cand);
       }
     }
     trace_item(S, TK_GC, nth, 3);
@@ -1422,12 +1401,6 @@ __global__ void __launch_bounds__(kGT, 20) k_gc_normals(DevState S, const FrameD
   }
   trace_count(S, TK_GC, nth);
   trace_at(S, TK_GC, 28);
-  if (normals) {
-    const bool ok = grid_barrier(S, &ctr->gc_bar, S.bar_flags, F.bar_stamp);
-    trace_at(S, TK_GC, 29);
-    if (ok) consume_fallbacks(FallbackArgs{S.ctr, S.fallback, S.nbr, S.bcoord, S.vparam, S.vnrm, S.cube_size});
-    trace_at(S, TK_GC, 30);
-  }
   {
     int vals[3] = {frees, computed, fallbacks};
     int64_t *const dst[3] = {&ctr->v_frees, &ctr->normals, &ctr->fallbacks};
@@ -1556,6 +1529,14 @@ __global__ void k_scatter_samples(DevState S, const int32_t *idx, int n, const d
     if (tsdf) S.tsdf[dst] = tsdf[q];
     if (weight) S.weight[dst] = weight[q];
   }
+}
+
+// apply pending face-normal fallback records (before the engine state is read
+// or changed outside fuse_frame)
+__global__ void __launch_bounds__(128) k_flush_fallbacks(DevState S) {
+  const int n = ld_vol(&S.ctr->fb_pending);
+  consume_fallbacks(FallbackArgs{S.ctr, S.fallback, S.nbr, S.bcoord, S.vparam, S.vnrm, S.cube_size}, n,
+                    blockIdx.x * 4 + (threadIdx.x >> 5), (int)gridDim.x * 4);
 }
 
 // validity bitmap of listed blocks from their weights (after host writes)
