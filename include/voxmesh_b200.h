@@ -204,6 +204,15 @@ int vm_fuse_frame_submit(vm_engine *e, const double *depth, int32_t h, int32_t w
                          int32_t depth_on_device, const vm_intrinsics *intr,
                          const vm_pose *pose, const vm_frame_config *cfg, int64_t frame_index);
 int vm_fuse_frame_result(vm_engine *e, vm_stats *out);
+/* vm_fuse_frame_submit for a raw 16-bit depth image (native byte order, as
+ * decoded from the reference's PGM files): the device converts each pixel
+ * exactly as io_formats.read_depth (io_formats.py:84: raw / depth_scale in
+ * f64, 0 = invalid) inside the frame's first pixel kernel, so a quarter of the
+ * f64 frame's bytes cross PCIe.  Results equal vm_fuse_frame on the converted
+ * frame bit for bit.  raw_on_device != 0: `raw` is a device pointer. */
+int vm_fuse_frame_submit_raw(vm_engine *e, const uint16_t *raw, int32_t h, int32_t w,
+                             int32_t raw_on_device, double depth_scale, const vm_intrinsics *intr,
+                             const vm_pose *pose, const vm_frame_config *cfg, int64_t frame_index);
 
 /* ---- phase-level API (tests / reference function mirrors) ------------ */
 /* fusion.collect_blocks (fusion.py:70-107): allocates the touched blocks and

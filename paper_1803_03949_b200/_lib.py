@@ -105,6 +105,9 @@ _SIGS = {
                                        C.POINTER(Intr), C.POINTER(PoseC), C.POINTER(FrameConfig),
                                        C.c_int64]),
     "vm_fuse_frame_result": (C.c_int, [C.c_void_p, C.POINTER(Stats)]),
+    "vm_fuse_frame_submit_raw": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                           C.c_double, C.POINTER(Intr), C.POINTER(PoseC),
+                                           C.POINTER(FrameConfig), C.c_int64]),
     "vm_collect": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                              C.POINTER(Intr), C.POINTER(PoseC), C.c_double, C.c_double,
                              C.POINTER(C.c_int64)]),

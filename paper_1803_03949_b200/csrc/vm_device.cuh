@@ -81,6 +81,9 @@ struct Counters {
 // new poses / depth pointers).
 struct FrameDev {
   const double *depth;
+  const uint16_t *raw;  // non-null: the frame arrived as raw u16 (read_depth): the first pixel
+  double *depth_out;    //   pass fills depth_out[p] = raw[p] / depth_scale (io_formats.py:84)
+  double depth_scale;
   int32_t h, w;
   double fx, fy, cx, cy;
   int32_t width, height;

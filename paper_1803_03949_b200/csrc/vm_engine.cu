@@ -87,6 +87,10 @@ struct vm_engine {
   size_t slot_cap = 0;
   int slot = 0;
   cudaEvent_t ev_copy[2] = {nullptr, nullptr};
+  uint16_t *d_raw[2] = {nullptr, nullptr};   // raw u16 frames (vm_fuse_frame_submit_raw)
+  size_t raw_cap = 0;
+  const uint16_t *raw_next = nullptr;          // set while a raw frame is being enqueued
+  double raw_scale = 0.0;
   vm_stats settled{};       // stats of the last settled, not yet delivered frame
   int settled_valid = 0;
   // ray-norm bounds over the image, cached per (h, w, fx, fy, cx, cy)
@@ -283,6 +287,8 @@ static void fill_frame_host(vm_engine *e, const double *depth_dev, int32_t h, in
                             const vm_intrinsics *intr, const vm_pose *pose) {
   FrameDev &F = *e->h_frame;
   F.consume_fb = 0;
+  F.raw = nullptr;
+  F.depth_out = nullptr;
   F.depth = depth_dev;
   F.h = h;
   F.w = w;
@@ -530,6 +536,7 @@ int vm_destroy(vm_engine *e) {
   if (e->copy_stream) cudaStreamSynchronize(e->copy_stream);
   for (int i = 0; i < 2; i++) {
     if (e->d_slot[i]) cudaFree(e->d_slot[i]);
+    if (e->d_raw[i]) cudaFree(e->d_raw[i]);
     if (e->ev_copy[i]) cudaEventDestroy(e->ev_copy[i]);
   }
   if (e->copy_stream) cudaStreamDestroy(e->copy_stream);
@@ -699,16 +706,24 @@ int vm_fuse_frame_enqueue(vm_engine *e, const double *depth, int32_t h, int32_t 
   TRY(ensure_rays(e, h, w));
   F.nsteps_fixed = fixed_nsteps(e, cfg->trunc);
   F.consume_fb = 1;   // k_collect applies the previous frame's fallback records
+  if (e->raw_next) {   // raw u16 frame: the first pixel kernel fills the f64 depth from it
+    F.raw = e->raw_next;
+    F.depth_out = const_cast<double *>(dd);
+    F.depth_scale = e->raw_scale;
+  }
   TRY(reset_call_counters(e));
   cudaStream_t st = e->stream;
   rec(e, PH_DEPTH);
   e->frame_launches = 4;   // collect, fuse, retype, gc (+ depth stats)
+  FrameDev Fc = F;   // (collect's copy: a raw frame converted by k_depth_stats is f64 now)
   if (F.nsteps_fixed <= 0) {
-    k_depth_stats<<<grid_blocks(e), 256, 0, st>>>(e->S, *e->h_frame);
+    k_depth_stats<<<grid_blocks(e), 256, 0, st>>>(e->S, F);
     e->frame_launches++;
+    Fc.raw = nullptr;
   }
   rec(e, PH_COLLECT);
-  launch_pdl(k_collect, e->grid_collect, kCollectThreads, st, e->S, *e->h_frame);
+  launch_pdl(k_collect, e->grid_collect, kCollectThreads, st, e->S, Fc);
+  F.raw = nullptr;   // (the later kernels read the f64 depth)
   TRY(enqueue_after_collect(e));
   CK(cudaMemcpyAsync(e->h_ctr, e->S.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
   e->pending = 1;
@@ -800,6 +815,49 @@ int vm_fuse_frame_submit(vm_engine *e, const double *depth, int32_t h, int32_t w
     e->slot = sl;
     CK(cudaEventSynchronize(e->ev_copy[sl]));   // the caller may reuse its buffer on return
   }
+  return VM_OK;
+}
+
+int vm_fuse_frame_submit_raw(vm_engine *e, const uint16_t *raw, int32_t h, int32_t w, int32_t raw_on_device,
+                             double depth_scale, const vm_intrinsics *intr, const vm_pose *pose,
+                             const vm_frame_config *cfg, int64_t frame_index) {
+  if (!e || !intr || !pose || !cfg) return set_err(VM_ERR_INPUT, "null argument");
+  if (!raw || h <= 0 || w <= 0) return set_err(VM_ERR_INPUT, "depth must be a non-empty (H, W) array");
+  if (!(depth_scale > 0)) return set_err(VM_ERR_VALUE, "depth_scale must be positive");
+  if (e->settled_valid && e->pending) return set_err(VM_ERR_INPUT, "the previous frame's result was not taken");
+  const size_t npix = (size_t)h * w;
+  if (!e->copy_stream) {
+    CK(cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; i++) CK(cudaEventCreateWithFlags(&e->ev_copy[i], cudaEventDisableTiming));
+  }
+  if (npix * sizeof(double) > e->slot_cap || npix * sizeof(uint16_t) > e->raw_cap) {
+    TRY(settle(e));   // (rare) reallocation: nothing may be reading the slots
+    CK(cudaStreamSynchronize(e->copy_stream));
+    for (int i = 0; i < 2; i++) {
+      if (e->d_slot[i]) CK(cudaFree(e->d_slot[i]));
+      if (e->d_raw[i]) CK(cudaFree(e->d_raw[i]));
+      CK(cudaMalloc((void **)&e->d_slot[i], npix * sizeof(double)));
+      CK(cudaMalloc((void **)&e->d_raw[i], npix * sizeof(uint16_t)));
+    }
+    e->slot_cap = npix * sizeof(double);
+    e->raw_cap = npix * sizeof(uint16_t);
+  }
+  const int sl = e->slot ^ 1;
+  const uint16_t *dr = raw;
+  if (!raw_on_device) {   // a quarter of the f64 frame's bytes over PCIe
+    CK(cudaMemcpyAsync(e->d_raw[sl], raw, npix * sizeof(uint16_t), cudaMemcpyHostToDevice, e->copy_stream));
+    CK(cudaEventRecord(e->ev_copy[sl], e->copy_stream));
+    dr = e->d_raw[sl];
+  }
+  TRY(settle(e));
+  if (!raw_on_device) CK(cudaStreamWaitEvent(e->stream, e->ev_copy[sl], 0));
+  e->raw_next = dr;
+  e->raw_scale = depth_scale;
+  const int rc = vm_fuse_frame_enqueue(e, e->d_slot[sl], h, w, 1, intr, pose, cfg, frame_index);
+  e->raw_next = nullptr;
+  TRY(rc);
+  e->slot = sl;
+  if (!raw_on_device) CK(cudaEventSynchronize(e->ev_copy[sl]));   // the caller may reuse its buffer
   return VM_OK;
 }
 

@@ -112,7 +112,13 @@ __global__ void __launch_bounds__(256) k_depth_stats(DevState S, const FrameDev 
   int cnt = 0;
   for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < npix;
        p += (long long)gridDim.x * blockDim.x) {
-    const double d = F.depth[p];
+    double d;
+    if (F.raw) {   // raw u16 frame: convert exactly as read_depth and keep the f64 depth
+      d = (double)F.raw[p] / F.depth_scale;
+      F.depth_out[p] = d;
+    } else {
+      d = F.depth[p];
+    }
     if (d > 0 && d <= F.max_range) {
       const int v = (int)(p / F.w), u = (int)(p - (long long)v * F.w);
       const double rx = ((double)u - F.cx) / F.fx, ry = ((double)v - F.cy) / F.fy;
@@ -414,7 +420,13 @@ __global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, cons
 #pragma unroll
     for (int k = 0; k < 2; k++) {   // both depth loads in flight together
       const int v = ry0 * kRegionH + (t >> 6) + 4 * k;
-      d[k] = (u < F.w && v < F.h) ? F.depth[(long long)v * F.w + u] : 0.0;
+      const long long idx = (long long)v * F.w + u;
+      if (F.raw) {   // raw u16 frame: convert exactly as read_depth and keep the f64 depth
+        d[k] = (u < F.w && v < F.h) ? (double)F.raw[idx] / F.depth_scale : 0.0;
+        if (u < F.w && v < F.h) F.depth_out[idx] = d[k];
+      } else {
+        d[k] = (u < F.w && v < F.h) ? F.depth[idx] : 0.0;
+      }
     }
 #pragma unroll
     for (int k = 0; k < 2; k++) {

@@ -200,6 +200,37 @@ class Engine:
         del keep
         return self._record(st)
 
+    def fuse_frame_raw(self, raw, pose: Pose, depth_scale: float = 5000.0) -> StatsRow:
+        """fuse_frame(read_depth-style raw / depth_scale, pose) from the raw 16-bit
+        depth image (io_formats.py:41-84): the conversion runs on the device,
+        bit-identical, and only the u16 image crosses PCIe.  `raw` is a (H, W)
+        uint16 array (native byte order) or a contiguous uint16/int16 CUDA tensor."""
+        if _is_device_tensor(raw):
+            if raw.element_size() != 2 or not raw.is_contiguous() or raw.dim() != 2:
+                raise ValueError("device raw depth must be a contiguous 2-D 16-bit CUDA tensor")
+            ptr, h, w, on_dev, keep = C.c_void_p(raw.data_ptr()), raw.shape[0], raw.shape[1], 1, None
+        else:
+            a = np.ascontiguousarray(np.asarray(raw, dtype=np.uint16))
+            if a.ndim != 2:
+                raise ValueError("raw depth must be a 2-D array")
+            ptr, h, w, on_dev, keep = _lib.ptr(a), a.shape[0], a.shape[1], 0, a
+        self.store._touch()
+        rc = _lib.load().vm_fuse_frame_submit_raw(self.store._h, ptr, h, w, on_dev, float(depth_scale),
+                                                  C.byref(self._intr_c), C.byref(_lib.pose_c(pose)),
+                                                  C.byref(self._fcfg), self.frame_index)
+        del keep
+        prev, self._pending = self._pending, None
+        _lib.check(rc)
+        if prev is not None:
+            self._deliver(prev)
+        row = _PendingRow(self, self.frame_index)
+        self._pending = row
+        self.stats.append(row)
+        self.frame_index += 1
+        if not self.pipelined:
+            self._resolve_pending()
+        return row
+
     def _deliver(self, row: _PendingRow) -> None:
         st = _lib.Stats()
         _lib.check(_lib.load().vm_fuse_frame_result(self.store._h, C.byref(st)))

@@ -263,3 +263,33 @@ def test_scattered_depth_overflows_collect_set_matches_oracle(cube):
             "frame", "blocks_active", "vertices_live", "triangles_live",
             "vertices_allocated_total", "vertices_recycled_total", "irregular_cube_count")), i
     _compare_final(eng, ora)
+
+
+@pytest.mark.parametrize("config", ["C1", "C4"])
+@pytest.mark.parametrize("pipelined", [False, True])
+def test_raw_u16_depth_matches_converted_frames(config, pipelined):
+    """fuse_frame_raw (device-side read_depth conversion, io_formats.py:84) is
+    bit-identical to fuse_frame on the host-converted f64 frames; C4's band
+    step count depends on the depth, so its raw frame is converted by
+    k_depth_stats, C1's by k_collect."""
+    from paper_1803_03949_b200 import Engine, RunConfig
+    from paper_1803_03949_b200.synth import camera_pose, config_spec, render_depth
+    spec, cfg = config_spec(config)
+    spec.width, spec.height = 160, 120
+    spec.fx = spec.fy = 131.25 if config == "C4" else 65.6
+    scale = 5000.0
+    intr = spec.intrinsics()
+    a = Engine(RunConfig(**cfg), intr)
+    b = Engine(RunConfig(**cfg), intr, pipelined=pipelined)
+    rows_b = []
+    for i in range(3):
+        pose = camera_pose(spec, i)
+        raw = np.clip(np.rint(render_depth(spec, pose) * scale), 0, 65535).astype(np.uint16)
+        ra = a.fuse_frame(raw.astype(np.float64) / scale, pose)
+        rows_b.append(b.fuse_frame_raw(raw, pose, depth_scale=scale))
+        assert _stats_tuple(rows_b[-1]) == _stats_tuple(ra), i
+    ma, mb = a.compact(), b.compact()
+    assert np.array_equal(ma.indices, mb.indices) and np.array_equal(ma.positions, mb.positions)
+    assert np.array_equal(ma.normals, mb.normals)
+    ba, bb = list(a.store.blocks()), list(b.store.blocks())
+    assert np.array_equal(np.stack([x.tsdf for x in ba]), np.stack([x.tsdf for x in bb]))
