@@ -330,6 +330,27 @@ def run_gpu(args, spec, cfg, rank, world, local_rank):
     e2_local = e2.engine if part else e2
     same = eng.stats[-1].vertices_live == e2_local.stats[-1].vertices_live
     glob = e2.stats[-1]
+    # informational: the same frames as raw 16-bit depth images (read_depth's
+    # format, scale 5000, i.e. quantised to 0.2 mm) through Engine.fuse_frame_raw
+    # -- the device converts them, a quarter of the H2D bytes
+    raw_e2e = None
+    if not part:
+        raws = [torch.from_numpy(np.clip(np.rint(h * 5000.0), 0, 65535).astype(np.uint16)).pin_memory().numpy()
+                for h in host_np]
+        e3 = Engine(RunConfig(strategy=args.strategy, **cfg, **caps), spec.intrinsics(), pipelined=True)
+        for i in range(args.warmup):
+            e3.fuse_frame_raw(raws[i], poses[i])
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for k in range(args.steps):
+            e3.fuse_frame_raw(raws[args.warmup + k], poses[args.warmup + k])
+        torch.cuda.synchronize()
+        raw_s = time.perf_counter() - t0
+        e3.stats[-1].blocks_active   # (complete the last frame)
+        raw_e2e = {"value": world * args.steps / raw_s, "unit": "frames/s",
+                   "h2d_bytes_per_step": spec.width * spec.height * 2 + 256, "d2h_bytes_per_step": 512,
+                   "input": "same frames quantised to u16 at depth_scale 5000 (read_depth format)"}
+        del e3
 
     if rank != 0:
         return
@@ -359,6 +380,7 @@ def run_gpu(args, spec, cfg, rank, world, local_rank):
         "e2e": {"value": (1 if part else world) * args.steps / e2e_s, "unit": "frames/s",
                 "h2d_bytes_per_step": spec.width * spec.height * 8 + 256,
                 "d2h_bytes_per_step": 512},
+        "e2e_raw_u16": raw_e2e,
         "gpu_launches": launches * world,
         "resumes_in_timed_region": resumes,
         "clocks": clk,
