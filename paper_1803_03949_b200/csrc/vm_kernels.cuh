@@ -944,6 +944,13 @@ __global__ void __launch_bounds__(kNT, 18) k_retype_place(DevState S, const Fram
         const int o = t >> 2;
         const int nb = R.nbr[nbr_dir(o >> 2, (o >> 1) & 1, o & 1)];
         cp_async16(&s_vm8[t * 4], S.vmask + (size_t)(nb >= 0 ? nb : 0) * (kNC / 32) + (t & 3) * 4, nb >= 0);
+      } else if (t < 48) {   // the same 8 blocks' slot-occupancy words (claimed at the end): into L2 now
+        const int o = (t - 32) >> 1;
+        const int nb = R.nbr[nbr_dir(o >> 2, (o >> 1) & 1, o & 1)];
+        if (nb >= 0) {
+          const uint32_t *pw = S.vocc + (size_t)nb * (kEV / 32) + ((t - 32) & 1) * 32;
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(pw));
+        }
       }
 #pragma unroll
       for (int j = 0; j < kOwn; j++) ov[j] = S.tsdf[(size_t)b * kNC + t + j * kNT];
