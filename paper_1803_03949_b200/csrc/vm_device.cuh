@@ -140,7 +140,8 @@ struct DevState {
   uint32_t *vmask;      // [cap*16] weight > 0, one bit per cube corner sample (C order)
   uint8_t *tp, *tc;     // [cap*512]
   int32_t *vbirth;      // [cap*1536] slot occupancy: birth frame, -1 empty
-  uint32_t *vocc;       // [cap*48] the same occupancy as bits (claimed with atomicOr; read by GC)
+  uint32_t *vocc;       // [cap*48] the same occupancy as bits (read and written by k_gc_normals)
+  uint32_t *vclaim;     // [cap*48] slots requested this frame (k_retype_place ORs, k_gc_normals applies + clears)
   double *vparam;       // [cap*1536] vertex coordinate along the edge axis
   double *vnrm;         // [cap*1536*3]
   uint32_t *item_mask;  // [cap*16] explicit scope cube masks

@@ -204,6 +204,7 @@ static int grow_blocks(vm_engine *e, int64_t need) {
   TRY(dev_grow(&S.tc, o * kNC, n * kNC, st));
   TRY(dev_grow(&S.vbirth, o * kEV, n * kEV, st));
   TRY(dev_grow(&S.vocc, o * (kEV / 32), n * (kEV / 32), st));
+  TRY(dev_grow(&S.vclaim, o * (kEV / 32), n * (kEV / 32), st));
   TRY(dev_grow(&S.vparam, o * kEV, n * kEV, st));
   TRY(dev_grow(&S.vnrm, o * kEV * 3, n * kEV * 3, st));
   TRY(dev_grow(&S.item_mask, 0, n * 16, st));
@@ -524,7 +525,7 @@ int vm_destroy(vm_engine *e) {
   DevState &S = e->S;
   void *ptrs[] = {S.slots, S.ovf_head, S.ovf_lock, S.ovf_key, S.ovf_val, S.ovf_next, S.ovf_stamp, S.bcoord,
                   S.nbr, S.stamp_collect, S.stamp_halo, S.stamp_new, S.bowned, S.slab_bits, S.scope,
-                  S.halo, S.tsdf, S.weight, S.vmask, S.tp, S.tc, S.vbirth, S.vocc, S.vparam, S.vnrm, S.item_mask, S.fallback, e->d_rays,
+                  S.halo, S.tsdf, S.weight, S.vmask, S.tp, S.tc, S.vbirth, S.vocc, S.vclaim, S.vparam, S.vnrm, S.item_mask, S.fallback, e->d_rays,
                   S.ctr, e->d_depth, e->d_scratch};
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -1060,6 +1061,10 @@ int vm_extract(vm_engine *e, const int32_t *scope_coords, const uint8_t *scope_m
   }
   const int gb = grid_blocks(e);
   k_retype_place<<<e->grid_retype, kNT, kRetypeSmem, e->stream>>>(e->S, *e->h_frame);
+  // the halo given here need not hold every block a request went to: apply them all
+  TRY(read_counters(e));
+  k_apply_claims<<<grid_threads(e, (long long)e->h_ctr->nblocks * (kEV / 32), 256), 256, 0, e->stream>>>(
+      e->S, e->h_ctr->nblocks, e->h_frame->frame);
   launch_gc(e, false, e->S.halo, &e->S.ctr->nhalo, 0, (int)(G_GC | G_NORMALS | G_COMMIT | G_REQUIRE_ITEMS));
   TRY(check_launch());
   TRY(flush_fallbacks(e));

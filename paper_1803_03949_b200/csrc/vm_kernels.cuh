@@ -554,7 +554,10 @@ __device__ __forceinline__ void init_block(const DevState &S, int b, int t) {
   vb[t] = -1;
   vb[t + kNC] = -1;
   vb[t + 2 * kNC] = -1;
-  if (t < kEV / 32) S.vocc[(size_t)b * (kEV / 32) + t] = 0u;
+  if (t < kEV / 32) {
+    S.vocc[(size_t)b * (kEV / 32) + t] = 0u;
+    S.vclaim[(size_t)b * (kEV / 32) + t] = 0u;
+  }
 }
 
 __global__ void __launch_bounds__(kThreadsCube) k_init_blocks(DevState S, int epoch) {
@@ -896,15 +899,14 @@ __global__ void __launch_bounds__(kNT, 18) k_retype_place(DevState S, const Fram
   __shared__ uint32_t s_claim[3 * 81];   // requested slots: [axis][tile column], bit = owner z
   __shared__ uint8_t s_wl[3 * 81];   // non-empty claim words
   __shared__ Resolved R;
-  __shared__ int red8[8 * (kNT / 32)];
+  __shared__ int red8[7 * (kNT / 32)];
   __shared__ int s_nplace;
   const int t = threadIdx.x, lane = t & 31;
   const double l = S.cube_size;
   const int frame = F.frame;
   const int do_refine = F.refine;
   const double eps = F.epsilon;
-  int allocs = 0, placements = 0, active = 0, changed = 0, t_rel = 0, t_new = 0, irr = 0, refined = 0,
-      live = 0;
+  int placements = 0, active = 0, changed = 0, t_rel = 0, t_new = 0, irr = 0, refined = 0, live = 0;
   for (int i = blockIdx.x; i < n; i += gridDim.x, nth++) {
     trace_item(S, TK_RETYPE, nth, 0);
     if (t < 32) {
@@ -944,13 +946,6 @@ __global__ void __launch_bounds__(kNT, 18) k_retype_place(DevState S, const Fram
         const int o = t >> 2;
         const int nb = R.nbr[nbr_dir(o >> 2, (o >> 1) & 1, o & 1)];
         cp_async16(&s_vm8[t * 4], S.vmask + (size_t)(nb >= 0 ? nb : 0) * (kNC / 32) + (t & 3) * 4, nb >= 0);
-      } else if (t < 48) {   // the same 8 blocks' slot-occupancy words (claimed at the end): into L2 now
-        const int o = (t - 32) >> 1;
-        const int nb = R.nbr[nbr_dir(o >> 2, (o >> 1) & 1, o & 1)];
-        if (nb >= 0) {
-          const uint32_t *pw = S.vocc + (size_t)nb * (kEV / 32) + ((t - 32) & 1) * 32;
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(pw));
-        }
       }
 #pragma unroll
       for (int j = 0; j < kOwn; j++) ov[j] = S.tsdf[(size_t)b * kNC + t + j * kNT];
@@ -1105,9 +1100,10 @@ __global__ void __launch_bounds__(kNT, 18) k_retype_place(DevState S, const Fram
     }
     __syncthreads();
     trace_item(S, TK_RETYPE, nth, 3);
-    // placement, one claim word (<= 9 slots) per thread at a time, all its
-    // coordinate stores and occupancy claims in flight together (the first
-    // requester to set a slot's occupancy bit allocates)
+    // placement, one claim word (<= 9 slots) per thread at a time: the slot's
+    // coordinate (mesher.py:216-235; every requester writes the same bits) and
+    // a request bit in the owner block's claim bitmap (a reduction, no round
+    // trip); k_gc_normals turns first requests into allocations
     const int nwl = s_nplace;
     for (int p = t; p < nwl; p += kNT) {
       const int wi = s_wl[p];
@@ -1116,11 +1112,8 @@ __global__ void __launch_bounds__(kNT, 18) k_retype_place(DevState S, const Fram
       const int ox = col / 9, oy = col - 9 * ox;
       const int sa = axis == 0 ? 81 : axis == 1 ? 9 : 1;
       const int ga_c = axis == 0 ? R.coord.x * kB + ox : R.coord.y * kB + oy;   // (axis 2: per z)
-      uint32_t fresh = 0;
-      uint32_t old[9];
 #pragma unroll
       for (int z = 0; z < 9; z++) {
-        old[z] = ~0u;
         if (!((word >> z) & 1u)) continue;
         const int owner = R.nbr[nbr_dir(ox >> 3, oy >> 3, z >> 3)];
         if (owner < 0) {
@@ -1134,17 +1127,7 @@ __global__ void __launch_bounds__(kNT, 18) k_retype_place(DevState S, const Fram
         const double param = (d0 == d1) ? 0.5 : d0 / (d0 - d1);
         const int ga = axis == 2 ? R.coord.z * kB + z : ga_c;
         S.vparam[slot] = __dadd_rn(__dmul_rn((double)ga, l), __dmul_rn(param, l));
-        old[z] = atomicOr(S.vocc + (slot >> 5), 1u << (slot & 31)) & (1u << (slot & 31));
-      }
-#pragma unroll
-      for (int z = 0; z < 9; z++) fresh |= (old[z] == 0u ? 1u : 0u) << z;
-      for (uint32_t m = fresh; m; m &= m - 1) {
-        const int z = __ffs(m) - 1;
-        const int owner = R.nbr[nbr_dir(ox >> 3, oy >> 3, z >> 3)];
-        const size_t slot = (size_t)owner * kEV + (((ox & 7) * 64 + (oy & 7) * 8 + (z & 7)) * 3 + axis);
-        allocs += (S.nranks <= 1 || S.bowned[owner]);   // counted by the slot's owning rank
-        S.vbirth[slot] = frame;
-        S.vnrm[3 * slot] = 0.0; S.vnrm[3 * slot + 1] = 0.0; S.vnrm[3 * slot + 2] = 0.0;
+        atomicOr(S.vclaim + (slot >> 5), 1u << (slot & 31));
       }
     }
     __syncthreads();   // R, tile and the placement list are rewritten by the next item
@@ -1152,10 +1135,10 @@ __global__ void __launch_bounds__(kNT, 18) k_retype_place(DevState S, const Fram
   {
     trace_count(S, TK_RETYPE, nth);
     trace_at(S, TK_RETYPE, 28);
-    int vals[8] = {allocs, placements, active, changed, t_rel, t_new, irr, refined};
-    int64_t *const dst[8] = {&S.ctr->v_allocs, &S.ctr->placements, &S.ctr->active, &S.ctr->changed,
+    int vals[7] = {placements, active, changed, t_rel, t_new, irr, refined};
+    int64_t *const dst[7] = {&S.ctr->placements, &S.ctr->active, &S.ctr->changed,
                              &S.ctr->t_released, &S.ctr->t_allocated, &S.ctr->irr_delta, &S.ctr->refined};
-    block_add_counters<8, kNT / 32>(vals, red8, dst);
+    block_add_counters<7, kNT / 32>(vals, red8, dst);
   }
   if (t == 0 && live) S.ctr->nitems_live = 1;   // (a flag: some item was live this call)
   trace_at(S, TK_RETYPE, 31);
@@ -1221,18 +1204,19 @@ __global__ void __launch_bounds__(kGT, 20) k_gc_normals(DevState S, const FrameD
   __shared__ __align__(16) uint32_t s_vm[27 * 16]; // weight > 0 bitmaps of the 27 neighbours
   __shared__ uint8_t s_inhalo[27];     // neighbour is a halo block of this call
   __shared__ uint32_t occ[kEV / 32];   // slot occupancy bits
+  __shared__ uint32_t s_cl[kEV / 32];  // this frame's placement requests
   __shared__ uint16_t s_vlist[kEV];    // surviving slots
   __shared__ uint16_t s_fb[kEV];       // ... whose gradient failed
   __shared__ Resolved R;
   __shared__ int s_nv, s_nfb;
-  __shared__ int red[3 * (kGT / 32)];
+  __shared__ int red[4 * (kGT / 32)];
   const int n = live_items > 0 ? n_listed : 0;
   const int t = threadIdx.x;
   const bool normals = (mode & G_NORMALS) != 0;
   FrameDev Fr = F;
   Fr.scope_mode = 1;   // resolve as explicit items: no slab bits
   Fr.frustum_only = 0;
-  int frees = 0, computed = 0, fallbacks = 0;
+  int frees = 0, computed = 0, fallbacks = 0, allocs = 0;
   trace_at(S, TK_GC, 1);
   int nth = 0;
   for (int i = blockIdx.x; i < n; i += gridDim.x, nth++) {
@@ -1252,7 +1236,10 @@ __global__ void __launch_bounds__(kGT, 20) k_gc_normals(DevState S, const FrameD
     const int b = R.b;
     // stage occupancy, types and halo flags (all loads in flight)
     {
-      for (int q = t; q < kEV / 32; q += kGT) cp_async4(&occ[q], S.vocc + (size_t)b * (kEV / 32) + q, true);
+      for (int q = t; q < kEV / 32; q += kGT) {
+        cp_async4(&occ[q], S.vocc + (size_t)b * (kEV / 32) + q, true);
+        cp_async4(&s_cl[q], S.vclaim + (size_t)b * (kEV / 32) + q, true);
+      }
       for (int q = t; q < 2 * 81; q += kGT) {   // per column: the z = 0..7 run, then z = -1
         const int col = q >> 1, lx = col / 9 - 1, ly = col % 9 - 1;
         const int dx = lx < 0 ? -1 : 0, dy = ly < 0 ? -1 : 0;
@@ -1289,7 +1276,18 @@ __global__ void __launch_bounds__(kGT, 20) k_gc_normals(DevState S, const FrameD
       const int wi = t + r * kGT;
       uint32_t keep = 0;
       if (wi < kEV / 32) {
-        const uint32_t word = occ[wi];
+        // this frame's placement requests (k_retype_place): a requested empty
+        // slot is allocated here (birth = frame, normal 0, store.py:145-162)
+        const uint32_t claim = s_cl[wi], fresh = claim & ~occ[wi];
+        for (uint32_t m = fresh; m; m &= m - 1) {
+          const size_t q = (size_t)b * kEV + wi * 32 + __ffs(m) - 1;
+          S.vbirth[q] = F.frame;
+          S.vnrm[3 * q] = 0.0; S.vnrm[3 * q + 1] = 0.0; S.vnrm[3 * q + 2] = 0.0;
+        }
+        allocs += R.owned * __popc(fresh);   // counted by the slot's owning rank
+        if (claim) S.vclaim[(size_t)b * (kEV / 32) + wi] = 0u;
+        const uint32_t word = occ[wi] | claim;
+        occ[wi] = word;
         keep = word;
         if (mode & G_GC) {
           for (uint32_t m = word; m; m &= m - 1) {
@@ -1326,8 +1324,7 @@ __global__ void __launch_bounds__(kGT, 20) k_gc_normals(DevState S, const FrameD
 #ifdef VM_TRACE
     { unsigned smid; asm volatile("mov.u32 %0, %%smid;" : "=r"(smid)); trace_val(S, TK_GC, nth, 24, smid); }
 #endif
-    if (mode & G_GC)   // frees applied
-      for (int q = t; q < kEV / 32; q += kGT) S.vocc[(size_t)b * (kEV / 32) + q] = occ[q];
+    for (int q = t; q < kEV / 32; q += kGT) S.vocc[(size_t)b * (kEV / 32) + q] = occ[q];   // claims + frees
     if (normals) {
       const int nv = s_nv;
       // two vertices per thread per pass: their 24 tsdf loads in flight together
@@ -1421,9 +1418,9 @@ __global__ void __launch_bounds__(kGT, 20) k_gc_normals(DevState S, const FrameD
   trace_count(S, TK_GC, nth);
   trace_at(S, TK_GC, 28);
   {
-    int vals[3] = {frees, computed, fallbacks};
-    int64_t *const dst[3] = {&ctr->v_frees, &ctr->normals, &ctr->fallbacks};
-    block_add_counters<3, kGT / 32>(vals, red, dst);
+    int vals[4] = {frees, computed, fallbacks, allocs};
+    int64_t *const dst[4] = {&ctr->v_frees, &ctr->normals, &ctr->fallbacks, &ctr->v_allocs};
+    block_add_counters<4, kGT / 32>(vals, red, dst);
   }
   if (t == 0 && (mode & G_COMMIT)) {
     __threadfence();
@@ -1556,6 +1553,30 @@ __global__ void __launch_bounds__(128) k_flush_fallbacks(DevState S) {
   const int n = ld_vol(&S.ctr->fb_pending);
   consume_fallbacks(FallbackArgs{S.ctr, S.fallback, S.nbr, S.bcoord, S.vparam, S.vnrm, S.cube_size}, n,
                     blockIdx.x * 4 + (threadIdx.x >> 5), (int)gridDim.x * 4);
+}
+
+// phase API (mesher.extract_frame with an arbitrary halo): apply every pending
+// placement request of every block (in fuse_frame k_gc_normals does it for the
+// halo, which holds every block a scope cube can request a slot of)
+__global__ void k_apply_claims(DevState S, int nblocks, int frame) {
+  long long allocs = 0;
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < (long long)nblocks * (kEV / 32);
+       q += (long long)gridDim.x * blockDim.x) {
+    const uint32_t claim = S.vclaim[q];
+    if (!claim) continue;
+    const uint32_t old = S.vocc[q], fresh = claim & ~old;
+    const long long b = q / (kEV / 32);
+    for (uint32_t m = fresh; m; m &= m - 1) {
+      const size_t sl = (size_t)q * 32 + __ffs(m) - 1;
+      S.vbirth[sl] = frame;
+      S.vnrm[3 * sl] = 0.0; S.vnrm[3 * sl + 1] = 0.0; S.vnrm[3 * sl + 2] = 0.0;
+    }
+    if (S.nranks <= 1 || S.bowned[b]) allocs += __popc(fresh);
+    S.vocc[q] = old | claim;
+    S.vclaim[q] = 0u;
+  }
+  allocs = warp_sum(allocs);
+  if ((threadIdx.x & 31) == 0 && allocs) atomicAdd((unsigned long long *)&S.ctr->v_allocs, (unsigned long long)allocs);
 }
 
 // validity bitmap of listed blocks from their weights (after host writes)
