@@ -792,7 +792,7 @@ struct ResolveRegs {
 
 __device__ __forceinline__ ResolveRegs resolve_load(const DevState &S, const FrameDev &F, int b, int item,
                                                     int nc) {
-  const int lane = threadIdx.x;
+  const int lane = threadIdx.x & 31;
   ResolveRegs r;
   r.v = -1;
   r.coord = make_int4(0, 0, 0, 0);
@@ -806,7 +806,7 @@ __device__ __forceinline__ ResolveRegs resolve_load(const DevState &S, const Fra
 
 __device__ __forceinline__ void resolve_store(const DevState &S, const FrameDev &F, const ResolveRegs &r,
                                               int b, int item, int n, int nc, Resolved &R) {
-  const int lane = threadIdx.x;
+  const int lane = threadIdx.x & 31;
   if (lane < 27) R.nbr[lane] = r.v;
   const int slab = __shfl_sync(0xffffffffu, r.v, 27);
   int4 c;
@@ -1148,7 +1148,7 @@ constexpr size_t kRetypeSmem = 0;
 
 
 // ------------------------------------------------------------ GC + normals
-constexpr int kGT = 32;   // threads per CTA of k_gc_normals (one warp per halo block)
+constexpr int kGT = 128;  // threads per CTA of k_gc_normals (kGW warps, one halo block each)
 // type tile over cube locals -1..7: 81 columns (lx, ly) of 16 bytes, z = 0..7
 // at bytes 0..7 and z = -1 at byte 15 (the -z neighbour's z = 7, fetched as
 // the aligned word of its z = 4..7 into bytes 12..15)
@@ -1171,128 +1171,147 @@ __device__ __forceinline__ size_t sample_index(const int *s_nbr, int lx, int ly,
   return nb < 0 ? ~(size_t)0 : (size_t)nb * kNC + ((lx & 7) * 64 + (ly & 7) * 8 + (lz & 7));
 }
 
-// One CTA of 64 threads per listed (halo) block:
-//  * stage slot occupancy and the 9^3 type tile (cube locals -1..7);
+// per-item shared state of k_gc_normals (one warp stages and collects each)
+struct GcItem {
+  Resolved R;
+  uint32_t occ[kEV / 32];               // slot occupancy bits
+  uint32_t cl[kEV / 32];                // this frame's placement requests
+  __align__(16) uint32_t vm[27 * 16];   // weight > 0 bitmaps of the 27 neighbours
+  __align__(16) uint8_t tt[81 * 16];    // type_curr over cube locals -1..7 (tt_idx)
+  uint8_t inhalo[28];                   // neighbour is a halo block of this call
+  uint16_t vlist[kEV];                  // surviving slots
+  uint16_t fb[kEV];                     // ... whose gradient failed
+  int nv, nfb;
+};
+
+// kGW warps per CTA, kGW halo blocks per CTA at a time: each warp resolves,
+// stages (cp.async: occupancy and request bits, the 9^3 type tile, the 27
+// neighbours' weight bitmaps) and garbage-collects its own block; the
+// normals of the kGW blocks' surviving vertices are then computed by the whole
+// CTA over the union of their lists, so a block with many vertices shares the
+// work with lighter ones.
+//  * requests (k_retype_place) of empty slots become allocations: birth =
+//    frame, normal 0 (store.py:145-162);
 //  * G_GC clears every occupied slot that no cube references any more (the
 //    reference's refcount == 0 recycling, mesher.py:333-356: the 4 cubes
-//    around the edge from the type tile);
-//  * G_NORMALS computes each surviving vertex's central-difference normal
-//    from its 12-sample stencil, gathered directly (mesher.py:369-439);
-//    vertices whose stencil fails go to a global worklist, drained after a
-//    grid barrier by the whole grid, one warp per vertex (face-normal fallback,
-//    mesher.py:456-486).
-// The per-call counters are summed per CTA; G_COMMIT: the last CTA folds the
-// deltas into the pool counters.
-__global__ void __launch_bounds__(kGT, 20) k_gc_normals(DevState S, const FrameDev F,
-                                                    const int32_t *__restrict__ list,
-                                                    const int32_t *__restrict__ count_ptr,
-                                                    int count_const, int mode) {
+//    around the edge from the type tile), word-parallel over the bitmap;
+//  * G_NORMALS: central-difference normals from each vertex's 12-sample
+//    stencil (mesher.py:369-439), tsdf gathered directly, "observed" from the
+//    bitmaps; stencil failures are recorded with their 4 cube types and
+//    candidate mask for the face-normal fallback (mesher.py:456-486), applied
+//    by the next frame's k_collect (or k_flush_fallbacks).
+// G_COMMIT: the last CTA folds the per-call deltas into the pool counters.
+constexpr int kGW = 4;
+
+__global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDev F,
+                                                   const int32_t *__restrict__ list,
+                                                   const int32_t *__restrict__ count_ptr,
+                                                   int count_const, int mode) {
   cudaGridDependencySynchronize();   // PDL: wait for the previous kernel of the frame
   trace_at(S, TK_GC, 0);
   Counters *ctr = S.ctr;
   __shared__ int s_pro[5];
   __shared__ SmemTables T;
-  // the halt flags, the live-item count, the list length and the first list
-  // entry: one thread, one round trip (the tables are staged meanwhile)
-  const int list_cap = count_ptr ? S.max_blocks : count_const;
   read_prologue(S, s_pro, (mode & G_REQUIRE_ITEMS) ? &ctr->nitems_live : nullptr, count_ptr, nullptr,
-                (int)blockIdx.x < list_cap ? list + blockIdx.x : nullptr, &T);
+                nullptr, &T);
   if (s_pro[0]) return;
   const int live_items = (mode & G_REQUIRE_ITEMS) ? s_pro[1] : 1;
-  const int n_listed = count_ptr ? s_pro[2] : count_const;
-  __shared__ __align__(16) uint8_t tt[81 * 16];   // type_curr over cube locals -1..7 (tt_idx)
-  __shared__ __align__(16) uint32_t s_vm[27 * 16]; // weight > 0 bitmaps of the 27 neighbours
-  __shared__ uint8_t s_inhalo[27];     // neighbour is a halo block of this call
-  __shared__ uint32_t occ[kEV / 32];   // slot occupancy bits
-  __shared__ uint32_t s_cl[kEV / 32];  // this frame's placement requests
-  __shared__ uint16_t s_vlist[kEV];    // surviving slots
-  __shared__ uint16_t s_fb[kEV];       // ... whose gradient failed
-  __shared__ Resolved R;
-  __shared__ int s_nv, s_nfb;
-  __shared__ int red[4 * (kGT / 32)];
-  const int n = live_items > 0 ? n_listed : 0;
-  const int t = threadIdx.x;
+  const int n = live_items > 0 ? (count_ptr ? s_pro[2] : count_const) : 0;
+  __shared__ GcItem G[kGW];
+  __shared__ int red[4 * kGW];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  GcItem &I = G[w];
   const bool normals = (mode & G_NORMALS) != 0;
   FrameDev Fr = F;
   Fr.scope_mode = 1;   // resolve as explicit items: no slab bits
   Fr.frustum_only = 0;
   int frees = 0, computed = 0, fallbacks = 0, allocs = 0;
   trace_at(S, TK_GC, 1);
+  const int per_round = (int)gridDim.x * kGW;
   int nth = 0;
-  for (int i = blockIdx.x; i < n; i += gridDim.x, nth++) {
+  for (int base = 0; base < n; base += per_round, nth++) {
     trace_item(S, TK_GC, nth, 0);
-    if (t < 32) {
-      const int b = i == (int)blockIdx.x && s_pro[4] != -1 ? s_pro[4] : __ldcg(list + i);
-      const ResolveRegs rr = resolve_load(S, Fr, b, i, 0);
-      resolve_store(S, Fr, rr, b, i, n, 0, R);
-    }
-    if (t == 0) { s_nv = 0; s_nfb = 0; }
-    __syncthreads();
-    trace_item(S, TK_GC, nth, 1);
-    if (R.mode <= 0) {
-      __syncthreads();
-      continue;
-    }
-    const int b = R.b;
-    // stage occupancy, types and halo flags (all loads in flight)
+    // (the kGW blocks of a CTA are a grid apart in the list: neighbouring list
+    // entries are neighbouring blocks of similar surface density)
+    const int i = base + w * (int)gridDim.x + blockIdx.x;
     {
-      for (int q = t; q < kEV / 32; q += kGT) {
-        cp_async4(&occ[q], S.vocc + (size_t)b * (kEV / 32) + q, true);
-        cp_async4(&s_cl[q], S.vclaim + (size_t)b * (kEV / 32) + q, true);
+      const int bi = i < n ? __ldcg(list + i) : -1;
+      const ResolveRegs rr = resolve_load(S, Fr, bi, i, 0);
+      resolve_store(S, Fr, rr, bi, i, n, 0, I.R);
+    }
+    if (lane == 0) { I.nv = 0; I.nfb = 0; }
+    __syncwarp();
+    const bool live = I.R.mode > 0;
+    const int b = I.R.b;
+    if (live) {
+      // stage occupancy + requests, types and halo flags (all copies in flight)
+      for (int q = lane; q < kEV / 32; q += 32) {
+        cp_async4(&I.occ[q], S.vocc + (size_t)b * (kEV / 32) + q, true);
+        cp_async4(&I.cl[q], S.vclaim + (size_t)b * (kEV / 32) + q, true);
       }
-      for (int q = t; q < 2 * 81; q += kGT) {   // per column: the z = 0..7 run, then z = -1
+      for (int q = lane; q < 2 * 81; q += 32) {   // per column: the z = 0..7 run, then z = -1
         const int col = q >> 1, lx = col / 9 - 1, ly = col % 9 - 1;
         const int dx = lx < 0 ? -1 : 0, dy = ly < 0 ? -1 : 0;
         const size_t row = (size_t)((lx & 7) * 64 + (ly & 7) * 8);
         if ((q & 1) == 0) {
-          const int nb = R.nbr[nbr_dir(dx, dy, 0)];
-          cp_async8(&tt[col * 16], S.tc + (size_t)(nb >= 0 ? nb : 0) * kNC + row, nb >= 0);
+          const int nb = I.R.nbr[nbr_dir(dx, dy, 0)];
+          cp_async8(&I.tt[col * 16], S.tc + (size_t)(nb >= 0 ? nb : 0) * kNC + row, nb >= 0);
         } else {
-          const int nb = R.nbr[nbr_dir(dx, dy, -1)];
-          cp_async4(&tt[col * 16 + 12], S.tc + (size_t)(nb >= 0 ? nb : 0) * kNC + row + 4, nb >= 0);
+          const int nb = I.R.nbr[nbr_dir(dx, dy, -1)];
+          cp_async4(&I.tt[col * 16 + 12], S.tc + (size_t)(nb >= 0 ? nb : 0) * kNC + row + 4, nb >= 0);
         }
       }
-      if (normals)   // validity bitmaps of the 27 neighbours (16 words each, 4 x 16 B)
-        for (int q = t; q < 27 * 4; q += kGT) {
-          const int nb = R.nbr[q >> 2];
-          cp_async16(&s_vm[q * 4], S.vmask + (size_t)(nb >= 0 ? nb : 0) * (kNC / 32) + (q & 3) * 4, nb >= 0);
+      if (normals)   // weight > 0 bitmaps of the 27 neighbours (16 words each, 4 x 16 B)
+        for (int q = lane; q < 27 * 4; q += 32) {
+          const int nb = I.R.nbr[q >> 2];
+          cp_async16(&I.vm[q * 4], S.vmask + (size_t)(nb >= 0 ? nb : 0) * (kNC / 32) + (q & 3) * 4, nb >= 0);
         }
       int hv = 0;
-      if (normals && t < 27) {
-        const int nb = R.nbr[t];
+      if (normals && lane < 27) {
+        const int nb = I.R.nbr[lane];
         hv = nb >= 0 && __ldcg(S.stamp_halo + nb) == F.epoch;
       }
-      if (t < 27) s_inhalo[t] = (uint8_t)hv;
+      if (lane < 27) I.inhalo[lane] = (uint8_t)hv;
       cp_async_wait_all();
-    }
-    __syncthreads();
-    trace_item(S, TK_GC, nth, 2);
-    // GC, word-parallel over the occupancy bitmap: thread t owns words t, t+32;
-    // an occupied slot survives iff a cube around its edge still has the edge
-    // in its mask (the 4 cubes at -du along u, -dw along w; u, w = the two axes
-    // other than the slot's) -- work proportional to occupied slots, no atomics
+      __syncwarp();
+      trace_item(S, TK_GC, nth, 2);
+      // requests: lane owns words lane, lane + 32; a requested empty slot is
+      // allocated (birth = frame, normal 0); every occupied slot is listed
+      __shared__ int s_nocc[kGW];
+      if (lane == 0) s_nocc[w] = 0;
+      __syncwarp();
 #pragma unroll
-    for (int r = 0; r < (kEV / 32 + kGT - 1) / kGT; r++) {
-      const int wi = t + r * kGT;
-      uint32_t keep = 0;
-      if (wi < kEV / 32) {
-        // this frame's placement requests (k_retype_place): a requested empty
-        // slot is allocated here (birth = frame, normal 0, store.py:145-162)
-        const uint32_t claim = s_cl[wi], fresh = claim & ~occ[wi];
-        for (uint32_t m = fresh; m; m &= m - 1) {
-          const size_t q = (size_t)b * kEV + wi * 32 + __ffs(m) - 1;
-          S.vbirth[q] = F.frame;
-          S.vnrm[3 * q] = 0.0; S.vnrm[3 * q + 1] = 0.0; S.vnrm[3 * q + 2] = 0.0;
+      for (int r = 0; r < (kEV / 32 + 31) / 32; r++) {
+        const int wi = lane + r * 32;
+        uint32_t word = 0;
+        if (wi < kEV / 32) {
+          const uint32_t claim = I.cl[wi], fresh = claim & ~I.occ[wi];
+          for (uint32_t m = fresh; m; m &= m - 1) {
+            const size_t q = (size_t)b * kEV + wi * 32 + __ffs(m) - 1;
+            S.vbirth[q] = F.frame;
+            S.vnrm[3 * q] = 0.0; S.vnrm[3 * q + 1] = 0.0; S.vnrm[3 * q + 2] = 0.0;
+          }
+          allocs += I.R.owned * __popc(fresh);   // counted by the slot's owning rank
+          if (claim) S.vclaim[(size_t)b * (kEV / 32) + wi] = 0u;
+          word = I.occ[wi] | claim;
+          I.occ[wi] = word;
         }
-        allocs += R.owned * __popc(fresh);   // counted by the slot's owning rank
-        if (claim) S.vclaim[(size_t)b * (kEV / 32) + wi] = 0u;
-        const uint32_t word = occ[wi] | claim;
-        occ[wi] = word;
-        keep = word;
-        if (mode & G_GC) {
-          for (uint32_t m = word; m; m &= m - 1) {
-            const int bit = __ffs(m) - 1;
-            const int sl = wi * 32 + bit;
+        int pos = smem_append(__popc(word), &s_nocc[w]);
+        for (uint32_t m = word; m; m &= m - 1) I.fb[pos++] = (uint16_t)(wi * 32 + __ffs(m) - 1);
+      }
+      __syncwarp();
+      // GC over the occupied list, balanced across the lanes: a slot survives
+      // iff a cube around its edge still has the edge in its mask (the 4 cubes
+      // at -du along u, -dw along w; u, w = the two axes other than the slot's)
+      const int nocc = s_nocc[w];
+      for (int p0 = 0; p0 < nocc; p0 += 32) {
+        const int p = p0 + lane;
+        bool keep = false;
+        int sl = 0;
+        if (p < nocc) {
+          sl = I.fb[p];
+          keep = true;
+          if (mode & G_GC) {
             const int c = sl / 3, axis = sl - 3 * c;
             // (no short-circuit: the 4 type and mask lookups issue together)
             unsigned ty[4], ref = 0;
@@ -1300,42 +1319,50 @@ __global__ void __launch_bounds__(kGT, 20) k_gc_normals(DevState S, const FrameD
             for (int q = 0; q < 4; q++) {
               int l0, l1, l2;
               slot_cube(c, axis, q, l0, l1, l2);
-              ty[q] = tt[tt_idx(l0, l1, l2)];
+              ty[q] = I.tt[tt_idx(l0, l1, l2)];
             }
 #pragma unroll
             for (int q = 0; q < 4; q++) ref |= (unsigned)T.edge_mask[ty[q]] >> cube_edge_of_slot(axis, q >> 1, q & 1);
             if (!(ref & 1u)) {
-              keep &= ~(1u << bit);
+              keep = false;
               S.vbirth[(size_t)b * kEV + sl] = -1;
-              frees += R.owned;
+              atomicAnd(&I.occ[sl >> 5], ~(1u << (sl & 31)));
+              frees += I.R.owned;
             }
           }
-          occ[wi] = keep;
+        }
+        if (normals) {
+          const int pos = smem_append(keep ? 1 : 0, &I.nv);
+          if (keep) I.vlist[pos] = (uint16_t)sl;
         }
       }
-      if (normals) {
-        int pos = smem_append(__popc(keep), &s_nv);
-        for (uint32_t m = keep; m; m &= m - 1) s_vlist[pos++] = (uint16_t)(wi * 32 + __ffs(m) - 1);
-      }
+      __syncwarp();
+      for (int q = lane; q < kEV / 32; q += 32) S.vocc[(size_t)b * (kEV / 32) + q] = I.occ[q];   // requests + frees
     }
-    __syncthreads();
-    trace_sub(S, TK_GC, nth, 0);   // GC done
-    trace_val(S, TK_GC, nth, 25, s_nv);
-#ifdef VM_TRACE
-    { unsigned smid; asm volatile("mov.u32 %0, %%smid;" : "=r"(smid)); trace_val(S, TK_GC, nth, 24, smid); }
-#endif
-    for (int q = t; q < kEV / 32; q += kGT) S.vocc[(size_t)b * (kEV / 32) + q] = occ[q];   // claims + frees
+    __syncthreads();   // every warp's vertex list is complete
+    trace_sub(S, TK_GC, nth, 0);
     if (normals) {
-      const int nv = s_nv;
-      // two vertices per thread per pass: their 24 tsdf loads in flight together
+      // the kGW blocks' vertices, whole CTA, two per thread per pass (their
+      // 24 tsdf loads in flight together)
+      int pre[kGW + 1];
+      pre[0] = 0;
+#pragma unroll
+      for (int k = 0; k < kGW; k++) pre[k + 1] = pre[k] + (G[k].R.mode > 0 ? G[k].nv : 0);
+      const int nv = pre[kGW];
       for (int p0 = 0; p0 < nv; p0 += 2 * kGT) {
         double v[2][12];
-        int slv[2];
+        int slv[2], itv[2];
         bool val[2];
 #pragma unroll
         for (int u = 0; u < 2; u++) {
           const int p = p0 + u * kGT + t;
-          slv[u] = p < nv ? s_vlist[p] : -1;
+          int k = 0;
+#pragma unroll
+          for (int q = 1; q < kGW; q++) k += p >= pre[q];
+          itv[u] = k;
+          slv[u] = p < nv ? G[k].vlist[p - pre[k]] : -1;
+          const GcItem &J = G[k];
+          const int bj = J.R.b;
           const int sl = slv[u] < 0 ? 0 : slv[u];
           const int ci = sl / 3, axis = sl - 3 * ci;
           const int x0 = ci >> 6, y0 = (ci >> 3) & 7, z0 = ci & 7;
@@ -1343,30 +1370,31 @@ __global__ void __launch_bounds__(kGT, 20) k_gc_normals(DevState S, const FrameD
           // the 12 stencil samples c0 +- e_d, c1 +- e_d (c1 = c0 + e_axis), absent
           // neighbours read a dummy in-bounds sample; weight > 0 from the staged
           // bitmaps (absent = 0)
-          const size_t dummy = (size_t)b * kNC;
+          const size_t dummy = (size_t)(bj < 0 ? 0 : bj) * kNC;
           bool ok = slv[u] >= 0;
 #pragma unroll
           for (int d = 0; d < 3; d++) {
             const int dx = d == 0, dy = d == 1, dz = d == 2;
-            const size_t a = sample_index(R.nbr, x0 + dx, y0 + dy, z0 + dz);
-            const size_t bq = sample_index(R.nbr, x0 - dx, y0 - dy, z0 - dz);
-            const size_t cq = sample_index(R.nbr, x1 + dx, y1 + dy, z1 + dz);
-            const size_t dq = sample_index(R.nbr, x1 - dx, y1 - dy, z1 - dz);
+            const size_t a = sample_index(J.R.nbr, x0 + dx, y0 + dy, z0 + dz);
+            const size_t bq = sample_index(J.R.nbr, x0 - dx, y0 - dy, z0 - dz);
+            const size_t cq = sample_index(J.R.nbr, x1 + dx, y1 + dy, z1 + dz);
+            const size_t dq = sample_index(J.R.nbr, x1 - dx, y1 - dy, z1 - dz);
             v[u][4 * d + 0] = S.tsdf[a == ~(size_t)0 ? dummy : a];     // c0 + e_d
             v[u][4 * d + 1] = S.tsdf[bq == ~(size_t)0 ? dummy : bq];   // c0 - e_d
             v[u][4 * d + 2] = S.tsdf[cq == ~(size_t)0 ? dummy : cq];   // c1 + e_d
             v[u][4 * d + 3] = S.tsdf[dq == ~(size_t)0 ? dummy : dq];   // c1 - e_d
-            ok = ok & sample_valid(s_vm, x0 + dx, y0 + dy, z0 + dz) & sample_valid(s_vm, x0 - dx, y0 - dy, z0 - dz) &
-                 sample_valid(s_vm, x1 + dx, y1 + dy, z1 + dz) & sample_valid(s_vm, x1 - dx, y1 - dy, z1 - dz);
+            ok = ok & sample_valid(J.vm, x0 + dx, y0 + dy, z0 + dz) & sample_valid(J.vm, x0 - dx, y0 - dy, z0 - dz) &
+                 sample_valid(J.vm, x1 + dx, y1 + dy, z1 + dz) & sample_valid(J.vm, x1 - dx, y1 - dy, z1 - dz);
           }
           val[u] = ok;
         }
 #pragma unroll
         for (int u = 0; u < 2; u++) {
           if (slv[u] < 0) continue;
+          GcItem &J = G[itv[u]];
           const int sl = slv[u];
           const int axis = sl - 3 * (sl / 3);
-          computed += R.owned;
+          computed += J.R.owned;
           const double d0 = axis == 0 ? v[u][3] : axis == 1 ? v[u][7] : v[u][11];   // samples at c0 and c1
           const double d1 = axis == 0 ? v[u][0] : axis == 1 ? v[u][4] : v[u][8];
           const double denom = d0 - d1;
@@ -1380,60 +1408,61 @@ __global__ void __launch_bounds__(kGT, 20) k_gc_normals(DevState S, const FrameD
           const double nrm = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(g[0], g[0]), __dmul_rn(g[1], g[1])),
                                             __dmul_rn(g[2], g[2])));
           if (val[u] && nrm > 1e-12) {
-            double *dst = S.vnrm + 3 * ((size_t)b * kEV + sl);
+            double *dst = S.vnrm + 3 * ((size_t)J.R.b * kEV + sl);
             dst[0] = g[0] / nrm; dst[1] = g[1] / nrm; dst[2] = g[2] / nrm;
           } else {
-            fallbacks += R.owned;
-            s_fb[atomicAdd(&s_nfb, 1)] = (uint16_t)sl;
+            fallbacks += J.R.owned;
+            J.fb[atomicAdd(&J.nfb, 1)] = (uint16_t)sl;
           }
         }
       }
       __syncthreads();
-      trace_sub(S, TK_GC, nth, 1);   // normals done
-
-      // face-normal fallback: publish each failed slot with its 4 cube types and
-      // candidate mask (types, neighbour row and halo flags are staged here)
-      const int nfb = s_nfb;
-      for (int p = t; p < nfb; p += kGT) {
-        const int sl = s_fb[p];
-        const int ci = sl / 3, axis = sl - 3 * ci;
-        uint32_t types4 = 0, cand = 0;
+      trace_sub(S, TK_GC, nth, 1);
+      // face-normal fallback records: each warp its own block's failed slots,
+      // with their 4 cube types and candidate mask (staged tile, row, halo flags)
+      if (live) {
+        const int nfb = I.nfb;
+        for (int p = lane; p < nfb; p += 32) {
+          const int sl = I.fb[p];
+          const int ci = sl / 3, axis = sl - 3 * ci;
+          uint32_t types4 = 0, cand = 0;
 #pragma unroll
-        for (int q = 0; q < 4; q++) {
-          int l0, l1, l2;
-          slot_cube(ci, axis, q, l0, l1, l2);
-          const uint32_t ty = tt[tt_idx(l0, l1, l2)];
-          const int dir = nbr_dir(l0 < 0 ? -1 : 0, l1 < 0 ? -1 : 0, l2 < 0 ? -1 : 0);
-          types4 |= ty << (8 * q);
-          if (((T.edge_mask[ty] >> cube_edge_of_slot(axis, q >> 1, q & 1)) & 1) && R.nbr[dir] >= 0 &&
-              s_inhalo[dir])
-            cand |= 1u << q;
+          for (int q = 0; q < 4; q++) {
+            int l0, l1, l2;
+            slot_cube(ci, axis, q, l0, l1, l2);
+            const uint32_t ty = I.tt[tt_idx(l0, l1, l2)];
+            const int dir = nbr_dir(l0 < 0 ? -1 : 0, l1 < 0 ? -1 : 0, l2 < 0 ? -1 : 0);
+            types4 |= ty << (8 * q);
+            if (((T.edge_mask[ty] >> cube_edge_of_slot(axis, q >> 1, q & 1)) & 1) && I.R.nbr[dir] >= 0 &&
+                I.inhalo[dir])
+              cand |= 1u << q;
+          }
+          S.fallback[atomicAdd(&ctr->fb_pending, 1)] = make_int4(b, sl, (int)types4, (int)cand);
         }
-        S.fallback[atomicAdd(&ctr->fb_pending, 1)] = make_int4(b, sl, (int)types4, (int)cand);
       }
     }
     trace_item(S, TK_GC, nth, 3);
-    __syncthreads();   // R and the tiles are rewritten by the next item
+    __syncthreads();   // the items' shared state is rewritten by the next round
   }
   trace_count(S, TK_GC, nth);
   trace_at(S, TK_GC, 28);
   {
     int vals[4] = {frees, computed, fallbacks, allocs};
     int64_t *const dst[4] = {&ctr->v_frees, &ctr->normals, &ctr->fallbacks, &ctr->v_allocs};
-    block_add_counters<4, kGT / 32>(vals, red, dst);
+    block_add_counters<4, kGW>(vals, red, dst);
   }
   if (t == 0 && (mode & G_COMMIT)) {
     __threadfence();
     if (atomicAdd(&ctr->done_gc, 1) == (int)gridDim.x - 1) {
       __threadfence();
-      const long long allocs = ld_vol(&ctr->v_allocs), fr = ld_vol(&ctr->v_frees);
-      const long long peak = ctr->v_live + allocs;     // all allocations precede all frees
+      const long long allocs_all = ld_vol(&ctr->v_allocs), fr = ld_vol(&ctr->v_frees);
+      const long long peak = ctr->v_live + allocs_all;     // all allocations precede all frees
       if (S.max_vertices > 0 && peak > S.max_vertices)
         set_error(S, ERR_CAPACITY, peak, S.max_vertices, 3);
       if (peak > ctr->v_count) ctr->v_count = peak;
       ctr->v_live = peak - fr;
       ctr->v_recycled += fr;
-      ctr->v_events += allocs;
+      ctr->v_events += allocs_all;
       const long long rel = ld_vol(&ctr->t_released), nw = ld_vol(&ctr->t_allocated);
       ctr->t_live += nw - rel;
       ctr->t_recycled += rel;

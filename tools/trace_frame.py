@@ -95,3 +95,4 @@ if live.any():
     allsm = [(len(L), sum(v for _, v in L)) for L in per.values()]
     print("  SMs:", len(per), "items/SM min/max", min(a for a, _ in allsm), max(a for a, _ in allsm),
           "nv/SM min/max", min(b for _, b in allsm), max(b for _, b in allsm))
+    print("  SM of gc CTAs 0..39:", [int(x) for x in m[:40, 24]] if len(m) >= 40 else [])
