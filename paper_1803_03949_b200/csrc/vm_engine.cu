@@ -74,10 +74,19 @@ struct vm_engine {
   void *d_scratch = nullptr;
   size_t scratch_cap = 0;
   Compacted comp;
-  cudaEvent_t ev[PH_COUNT] = {};
+  cudaEvent_t evs[2][PH_COUNT] = {};   // per frame slot (two frames may be in flight)
+  cudaEvent_t *ev = evs[0];            // the slot being enqueued / settled
   bool profiling = false;
   int pending = 0;
   int64_t pending_frame = 0;
+  // Frame slots: each enqueued frame keeps its parameters, a pinned snapshot of
+  // the counters taken after its last kernel, and an event behind that copy, so
+  // vm_fuse_frame_submit can queue frame t+1 before frame t is settled.
+  int fslot = 0;                      // slot of the most recently enqueued frame
+  FrameDev f_saved[2];                // its parameters (as launched)
+  Counters *h_snap[2] = {nullptr, nullptr};
+  cudaEvent_t ev_done[2] = {nullptr, nullptr};
+  int64_t frame_of[2] = {0, 0};
   int last_resumes = 0;
   int frame_launches = 0;   // kernels launched by the pending / last frame
   // pipelined submission (vm_fuse_frame_submit): the next frame's depth is
@@ -449,7 +458,12 @@ int vm_create(const vm_store_config *cfg, vm_engine **out) {
   CK(cudaDeviceGetAttribute(&e->sm_count, cudaDevAttrMultiProcessorCount, dev));
   CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
   e->own_stream = true;
-  for (int i = 0; i < PH_COUNT; i++) CK(cudaEventCreate(&e->ev[i]));
+  for (int k = 0; k < 2; k++) {
+    for (int i = 0; i < PH_COUNT; i++) CK(cudaEventCreate(&e->evs[k][i]));
+    CK(cudaEventCreateWithFlags(&e->ev_done[k], cudaEventDisableTiming));
+    CK(cudaMallocHost((void **)&e->h_snap[k], sizeof(Counters)));
+    memset(e->h_snap[k], 0, sizeof(Counters));
+  }
   CK(cudaMallocHost((void **)&e->h_ctr, sizeof(Counters)));
   CK(cudaMallocHost((void **)&e->h_frame, sizeof(FrameDev)));
   memset(e->h_ctr, 0, sizeof(Counters));
@@ -532,8 +546,12 @@ int vm_destroy(vm_engine *e) {
   free_compacted(e->comp);
   if (e->h_ctr) cudaFreeHost(e->h_ctr);
   if (e->h_frame) cudaFreeHost(e->h_frame);
-  for (int i = 0; i < PH_COUNT; i++)
-    if (e->ev[i]) cudaEventDestroy(e->ev[i]);
+  for (int k = 0; k < 2; k++) {
+    for (int i = 0; i < PH_COUNT; i++)
+      if (e->evs[k][i]) cudaEventDestroy(e->evs[k][i]);
+    if (e->ev_done[k]) cudaEventDestroy(e->ev_done[k]);
+    if (e->h_snap[k]) cudaFreeHost(e->h_snap[k]);
+  }
   if (e->copy_stream) cudaStreamSynchronize(e->copy_stream);
   for (int i = 0; i < 2; i++) {
     if (e->d_slot[i]) cudaFree(e->d_slot[i]);
@@ -684,6 +702,34 @@ static int fixed_nsteps(vm_engine *e, double trunc) {
   return lo == hi ? lo : 0;
 }
 
+// Queue the kernels of the frame whose parameters are in slot `slot`; the
+// counters are snapshotted into the slot's pinned buffer after its last kernel.
+static int launch_frame(vm_engine *e, int slot) {
+  FrameDev &F = *e->h_frame;
+  F = e->f_saved[slot];
+  e->fslot = slot;
+  e->ev = e->evs[slot];
+  TRY(reset_call_counters(e));
+  cudaStream_t st = e->stream;
+  rec(e, PH_DEPTH);
+  e->frame_launches = 4;   // collect, fuse, retype, gc (+ depth stats)
+  FrameDev Fc = F;   // (collect's copy: a raw frame converted by k_depth_stats is f64 now)
+  if (F.nsteps_fixed <= 0) {
+    k_depth_stats<<<grid_blocks(e), 256, 0, st>>>(e->S, F);
+    e->frame_launches++;
+    Fc.raw = nullptr;
+  }
+  rec(e, PH_COLLECT);
+  launch_pdl(k_collect, e->grid_collect, kCollectThreads, st, e->S, Fc);
+  F.raw = nullptr;   // (the later kernels read the f64 depth)
+  TRY(enqueue_after_collect(e));
+  CK(cudaMemcpyAsync(e->h_snap[slot], e->S.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+  CK(cudaEventRecord(e->ev_done[slot], st));
+  e->pending = 1;
+  e->pending_frame = e->frame_of[slot];
+  return VM_OK;
+}
+
 int vm_fuse_frame_enqueue(vm_engine *e, const double *depth, int32_t h, int32_t w, int32_t depth_on_device,
                           const vm_intrinsics *intr, const vm_pose *pose, const vm_frame_config *cfg,
                           int64_t frame_index) {
@@ -712,24 +758,10 @@ int vm_fuse_frame_enqueue(vm_engine *e, const double *depth, int32_t h, int32_t 
     F.depth_out = const_cast<double *>(dd);
     F.depth_scale = e->raw_scale;
   }
-  TRY(reset_call_counters(e));
-  cudaStream_t st = e->stream;
-  rec(e, PH_DEPTH);
-  e->frame_launches = 4;   // collect, fuse, retype, gc (+ depth stats)
-  FrameDev Fc = F;   // (collect's copy: a raw frame converted by k_depth_stats is f64 now)
-  if (F.nsteps_fixed <= 0) {
-    k_depth_stats<<<grid_blocks(e), 256, 0, st>>>(e->S, F);
-    e->frame_launches++;
-    Fc.raw = nullptr;
-  }
-  rec(e, PH_COLLECT);
-  launch_pdl(k_collect, e->grid_collect, kCollectThreads, st, e->S, Fc);
-  F.raw = nullptr;   // (the later kernels read the f64 depth)
-  TRY(enqueue_after_collect(e));
-  CK(cudaMemcpyAsync(e->h_ctr, e->S.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
-  e->pending = 1;
-  e->pending_frame = frame_index;
-  return VM_OK;
+  const int slot = e->fslot ^ 1;
+  e->f_saved[slot] = F;
+  e->frame_of[slot] = frame_index;
+  return launch_frame(e, slot);
 }
 
 int vm_fuse_frame_finish(vm_engine *e, vm_stats *out) {
@@ -752,12 +784,53 @@ int vm_fuse_frame(vm_engine *e, const double *depth, int32_t h, int32_t w, int32
 // Complete a pending submitted frame (host wait, arena resume) and keep its
 // stats for vm_fuse_frame_result.  Every call that touches the engine's state
 // settles first, so a submitted frame is never observed half done.
+//
+// settle_slot completes the frame of slot `slot`; when `succ` the frame after it
+// is already queued behind it (vm_fuse_frame_submit).  The common case is one
+// event wait on the frame's counter snapshot -- the queued frame keeps the GPU
+// busy meanwhile.  A frame that ran out of block heap (or failed) made every
+// later kernel exit at its guard, the queued frame's included (k_collect checks
+// it before any write), so its only effect was resetting the per-call
+// counters: the device counters are restored from the snapshot, the frame is
+// resumed as in the synchronous path, and the queued frame is launched again
+// (or, when the frame failed, dropped: the engine is left as the synchronous
+// path leaves it).
+static int settle_slot(vm_engine *e, int slot, bool succ) {
+  CK(cudaEventSynchronize(e->ev_done[slot]));
+  const int launched = e->frame_launches;
+  memcpy(e->h_ctr, e->h_snap[slot], sizeof(Counters));
+  e->ev = e->evs[slot];
+  e->last_resumes = 0;
+  int rc = VM_OK;
+  if (e->h_ctr->need || e->h_ctr->error) {
+    if (succ) {
+      CK(cudaStreamSynchronize(e->stream));
+      TRY(copy_sync(e, e->S.ctr, e->h_snap[slot], sizeof(Counters), cudaMemcpyHostToDevice));
+      *e->h_frame = e->f_saved[slot];
+      e->h_frame->raw = nullptr;
+    }
+    rc = complete_with_resume(e, &e->last_resumes);
+  }
+  if (rc == VM_OK) fill_stats(e, e->frame_of[slot], &e->settled);
+  if (succ) {
+    e->pending = 0;
+    if (rc == VM_OK && e->last_resumes) {
+      TRY(launch_frame(e, slot ^ 1));   // (sets pending again)
+    } else if (rc == VM_OK) {
+      e->pending = 1;
+      e->pending_frame = e->frame_of[slot ^ 1];
+      e->ev = e->evs[slot ^ 1];
+      e->frame_launches = launched;
+    }
+    if (rc == VM_OK) e->settled.kernel_launches = 4 + (e->f_saved[slot].nsteps_fixed <= 0) + 3 * e->last_resumes;
+  }
+  return rc;
+}
+
 static int settle(vm_engine *e) {
   if (!e->pending) return VM_OK;
   e->pending = 0;
-  e->last_resumes = 0;
-  TRY(complete_with_resume(e, &e->last_resumes));
-  fill_stats(e, e->pending_frame, &e->settled);
+  TRY(settle_slot(e, e->fslot, false));
   e->settled_valid = 1;
   return VM_OK;
 }
@@ -807,11 +880,23 @@ int vm_fuse_frame_submit(vm_engine *e, const double *depth, int32_t h, int32_t w
     CK(cudaEventRecord(e->ev_copy[sl], e->copy_stream));
     dd = e->d_slot[sl];
   }
-  // 2. the previous frame completes (its stats are kept for vm_fuse_frame_result)
-  TRY(settle(e));
-  // 3. this frame's kernels, ordered after its copy
+  // 2. this frame's kernels, ordered after its copy, queued behind the pending
+  //    frame's; 3. the pending frame completes (its stats are kept for
+  //    vm_fuse_frame_result) while this one keeps the GPU busy
   if (sl >= 0) CK(cudaStreamWaitEvent(e->stream, e->ev_copy[sl], 0));
-  TRY(vm_fuse_frame_enqueue(e, dd, h, w, 1, intr, pose, cfg, frame_index));
+  const bool prev = e->pending != 0;
+  const int pslot = e->fslot;
+  e->pending = 0;
+  const int rc = vm_fuse_frame_enqueue(e, dd, h, w, 1, intr, pose, cfg, frame_index);
+  if (rc != VM_OK) {   // (argument errors: nothing was queued)
+    e->pending = prev;
+    e->fslot = pslot;
+    return rc;
+  }
+  if (prev) {
+    TRY(settle_slot(e, pslot, true));
+    e->settled_valid = 1;
+  }
   if (sl >= 0) {
     e->slot = sl;
     CK(cudaEventSynchronize(e->ev_copy[sl]));   // the caller may reuse its buffer on return
@@ -850,13 +935,23 @@ int vm_fuse_frame_submit_raw(vm_engine *e, const uint16_t *raw, int32_t h, int32
     CK(cudaEventRecord(e->ev_copy[sl], e->copy_stream));
     dr = e->d_raw[sl];
   }
-  TRY(settle(e));
   if (!raw_on_device) CK(cudaStreamWaitEvent(e->stream, e->ev_copy[sl], 0));
   e->raw_next = dr;
   e->raw_scale = depth_scale;
+  const bool prev = e->pending != 0;
+  const int pslot = e->fslot;
+  e->pending = 0;
   const int rc = vm_fuse_frame_enqueue(e, e->d_slot[sl], h, w, 1, intr, pose, cfg, frame_index);
   e->raw_next = nullptr;
-  TRY(rc);
+  if (rc != VM_OK) {
+    e->pending = prev;
+    e->fslot = pslot;
+    return rc;
+  }
+  if (prev) {
+    TRY(settle_slot(e, pslot, true));
+    e->settled_valid = 1;
+  }
   e->slot = sl;
   if (!raw_on_device) CK(cudaEventSynchronize(e->ev_copy[sl]));   // the caller may reuse its buffer
   return VM_OK;

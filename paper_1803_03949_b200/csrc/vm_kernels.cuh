@@ -385,15 +385,29 @@ __global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, cons
   __shared__ uint16_t s_list[kCSet];
   __shared__ unsigned long long s_over[kCOver];
   __shared__ int s_out[kCSet + kCOver];
-  __shared__ int s_n, s_nover, s_valid, s_nout, s_base;
+  __shared__ int s_n, s_nover, s_valid, s_nout, s_base, s_stop;
   const int t = threadIdx.x, lane = t & 31;
   const int rx = (F.w + kRegionW - 1) / kRegionW, ry = (F.h + kRegionH - 1) / kRegionH;
+  // Guard (error / heap exhausted): a frame queued behind one that stopped
+  // must not write anything -- the host resumes the stopped frame and launches
+  // this one again.  Read here, checked before the first write (the load's
+  // latency hides behind the first region's sampling).
+  int stop = 0;
+  if (t == 0) {
+    const int2 h = __ldcg(reinterpret_cast<const int2 *>(&ctr->error));
+    stop = (h.x | h.y) != 0;
+  }
   // The previous frame's face-normal fallback records (k_gc_normals) are
   // applied here, by the CTAs that have no pixel region (else by every CTA
   // after its regions): nothing in this kernel reads or writes what they use
   // (types, vertex coordinates, neighbour rows) and the idle warps absorb them.
   const int nreg = rx * ry, wpc = kCollectThreads / 32;
   const bool spare = (int)gridDim.x > nreg;
+  if (spare && (int)blockIdx.x >= nreg) {
+    if (t == 0) s_stop = stop;
+    __syncthreads();
+    if (s_stop) return;
+  }
   if (F.consume_fb && spare && (int)blockIdx.x >= nreg) {
     const int nfb = ld_vol(&ctr->fb_pending);
     consume_fallbacks(FallbackArgs{S.ctr, S.fallback, S.nbr, S.bcoord, S.vparam, S.vnrm, S.cube_size}, nfb,
@@ -476,7 +490,9 @@ __global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, cons
       }
     }
     trace_item(S, TK_COLLECT, nth, 1);
+    if (t == 0) s_stop = stop;
     __syncthreads();
+    if (s_stop) return;   // (uniform; before any table write)
     trace_item(S, TK_COLLECT, nth, 2);
     // the region's distinct blocks, one thread each (+ keys that found the set
     // crowded); the newly collected ones are appended with one atomic per CTA

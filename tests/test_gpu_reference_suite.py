@@ -160,6 +160,21 @@ def test_capacity_error_vertex_pool():                 # store.py:150-152
         eng.fuse_frame(render_depth(spec, pose), pose)
 
 
+def test_capacity_error_vertex_pool_pipelined():       # store.py:150-152, pipelined submission
+    """The failing frame's error surfaces at the next call; the frame queued
+    behind it is dropped (its kernels stop at the guard) and raises nothing twice."""
+    from paper_1803_03949_b200 import CapacityError, Engine, RunConfig
+    from paper_1803_03949_b200.synth import SceneSpec, static_pose, render_depth
+    spec = SceneSpec(scene="plane", width=48, height=48, fx=40.0, fy=40.0)
+    pose = static_pose((0, 0, 0), (0, 0, 1))
+    depth = render_depth(spec, pose)
+    eng = Engine(RunConfig(cube_size=0.02, max_vertices=50), spec.intrinsics(), pipelined=True)
+    eng.fuse_frame(depth, pose)                        # queued; fails on the device
+    with pytest.raises(CapacityError):
+        eng.fuse_frame(depth, pose)                    # queues frame 1, settles frame 0
+    eng.settle()                                       # nothing pending: frame 1 was dropped
+
+
 def test_hash_table_heavy_load_no_dropped_inserts():   # test_store.py:40-57 (load 50%)
     from paper_1803_03949_b200 import SpatialStore
     st = SpatialStore(cube_size=0.03, table_size=1 << 14)
