@@ -172,7 +172,11 @@ def test_capacity_error_vertex_pool_pipelined():       # store.py:150-152, pipel
     eng.fuse_frame(depth, pose)                        # queued; fails on the device
     with pytest.raises(CapacityError):
         eng.fuse_frame(depth, pose)                    # queues frame 1, settles frame 0
-    eng.settle()                                       # nothing pending: frame 1 was dropped
+    assert eng._pending is None                        # frame 1 was dropped, not left in flight
+    from paper_1803_03949_b200 import _lib
+    import ctypes as C
+    st = _lib.Stats()
+    assert _lib.load().vm_fuse_frame_result(eng.store._h, C.byref(st)) != 0   # nothing submitted
 
 
 def test_hash_table_heavy_load_no_dropped_inserts():   # test_store.py:40-57 (load 50%)
