@@ -36,6 +36,14 @@ enum { NEED_BLOCKS = 1 };
 
 // Device counters.  Persistent fields first; everything from `nvalid` on is
 // reset at the start of every call (one memset).
+// The frame's halo list is appended by every retype CTA at once: one counter
+// would serialise ~2.5k returning atomics (~6 us at the end of the kernel), so
+// appends go to kHaloShards sub-lists (shard = CTA index mod kHaloShards) of
+// halo_sh_cap entries each, a full shard spilling into the general list (halo,
+// nhalo), which the phase API also uses.  k_gc_normals (G_SHARDED) walks the
+// shards' prefix then the general list.
+constexpr int kHaloShards = 32;
+
 struct Counters {
   int32_t nblocks;       // SpatialStore.block_count
   int32_t ovf_count;
@@ -75,6 +83,7 @@ struct Counters {
   int64_t normals;
   int64_t fallbacks;
   int64_t refined;
+  int32_t nhalo_sh[kHaloShards];   // halo shard fill counts (may exceed halo_sh_cap: clamp)
 };
 
 // Per-call parameters in device memory (a captured frame graph replays with
@@ -133,6 +142,8 @@ struct DevState {
   uint8_t *slab_bits;
   int32_t *scope;       // scope items: collected first, then minus slabs
   int32_t *halo;
+  int32_t *halo_sh;     // kHaloShards x halo_sh_cap
+  int32_t halo_sh_cap;
   // heavy block storage, sized block_cap (grows)
   int32_t block_cap;
   double *tsdf;         // [cap*512]
@@ -178,7 +189,12 @@ __device__ __forceinline__ void trace_count(const DevState &S, int k, int n) {
   if (S.trace && threadIdx.x == 0 && blockIdx.x < kTraceCtas)
     S.trace[((size_t)k * kTraceCtas + blockIdx.x) * kTraceSlots + 27] = (unsigned long long)n;
 }
+// (any thread: per-warp marks)
+__device__ __forceinline__ void trace_at_any(const DevState &S, int k, int slot) {
+  if (S.trace && blockIdx.x < kTraceCtas) S.trace[((size_t)k * kTraceCtas + blockIdx.x) * kTraceSlots + slot] = gtimer();
+}
 #else
+__device__ __forceinline__ void trace_at_any(const DevState &, int, int) {}
 __device__ __forceinline__ void trace_at(const DevState &, int, int) {}
 __device__ __forceinline__ void trace_count(const DevState &, int, int) {}
 #endif
@@ -199,7 +215,6 @@ __device__ __forceinline__ void trace_val(const DevState &, int, int, int, long 
 #endif
 
 // ---------------------------------------------------------------- tables
-__constant__ uint16_t c_edge_mask[256] = VM_EDGE_MASK_INIT;
 __constant__ uint8_t c_tri_count[256] = VM_TRI_COUNT_INIT;
 __constant__ unsigned long long c_tri_packed[256] = VM_TRI_PACKED_INIT;
 // corner offsets (mc_tables.py:31-34) packed as x | y<<1 | z<<2
@@ -212,9 +227,17 @@ __constant__ uint8_t c_e_end[12] = {1, 2, 2, 3, 5, 6, 6, 7, 4, 5, 6, 7};
 __constant__ uint8_t c_regular[6] = {0x99, 0x66, 0x33, 0xCC, 0x0F, 0xF0};
 // global-memory copies, staged into shared memory by the meshing kernels
 // (coalesced loads; constant-bank reads with per-thread indices serialise)
-__device__ const uint16_t g_edge_mask[256] = VM_EDGE_MASK_INIT;
 __device__ const uint8_t g_tri_count[256] = VM_TRI_COUNT_INIT;
 __constant__ uint8_t c_slab_sel[8];
+
+// EDGE_MASK[t] (mc_tables.py:79-112) computed from the corner bits: edge e is
+// active iff its two corners differ (edges (i, i+1 mod 4) of each face ring,
+// then the 4 verticals (i, i + 4)); equal to the table for all 256 types
+// (tests/test_tables.py)
+__host__ __device__ __forceinline__ unsigned edge_mask_of(unsigned t) {
+  const unsigned x = t ^ (((t >> 1) & 0x77u) | ((t << 3) & 0x88u));
+  return (x & 0xFFu) | (((t ^ (t >> 4)) & 0xFu) << 8);
+}
 
 __host__ __device__ inline bool is_regular_type(unsigned t) {
   return t == 0x99 || t == 0x66 || t == 0x33 || t == 0xCC || t == 0x0F || t == 0xF0;
@@ -534,6 +557,22 @@ __device__ __forceinline__ void block_add_counters(int (&vals)[N], int *sh, int6
       for (int w = 0; w < NW; w++) r += sh[k * NW + w];
       if (r && dst[k]) atomicAdd((unsigned long long *)dst[k], (unsigned long long)r);
     }
+}
+
+// Warp sums of N per-thread counters (each < 2^31 in magnitude per warp), added
+// by lane k to dst[k] (a reduction, no round trip; null = skip): no barrier, so
+// a warp that finishes early leaves without waiting for the rest of its CTA.
+template <int N>
+__device__ __forceinline__ void warp_add_counters(const int (&vals)[N], int64_t *const (&dst)[N]) {
+  const int lane = threadIdx.x & 31;
+  int mine = 0;
+  int64_t *d = nullptr;
+#pragma unroll
+  for (int k = 0; k < N; k++) {
+    const int v = (int)__reduce_add_sync(0xffffffffu, (unsigned)vals[k]);
+    if (lane == k) { mine = v; d = dst[k]; }
+  }
+  if (mine && d) atomicAdd((unsigned long long *)d, (unsigned long long)(long long)mine);
 }
 
 // vertex position from its slot (mesher.py:216-235): every coordinate is

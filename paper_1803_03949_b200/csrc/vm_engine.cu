@@ -273,7 +273,7 @@ static int enqueue_after_collect(vm_engine *e) {
   rec(e, PH_RETYPE);
   launch_pdl(k_retype_place, e->grid_retype, kNT, st, S, F);
   rec(e, PH_GC);
-  launch_gc(e, true, S.halo, &S.ctr->nhalo, 0, (int)(G_GC | G_NORMALS | G_COMMIT | G_REQUIRE_ITEMS));
+  launch_gc(e, true, S.halo, &S.ctr->nhalo, 0, (int)(G_GC | G_NORMALS | G_COMMIT | G_REQUIRE_ITEMS | G_SHARDED));
   rec(e, PH_END);
   return check_launch();
 }
@@ -504,6 +504,8 @@ int vm_create(const vm_store_config *cfg, vm_engine **out) {
   TRY(dev_alloc(&S.slab_bits, (mb + 4) & ~(size_t)3, 0));
   TRY(dev_alloc(&S.scope, mb));
   TRY(dev_alloc(&S.halo, mb));
+  S.halo_sh_cap = (int32_t)((mb + kHaloShards - 1) / kHaloShards + 64);
+  TRY(dev_alloc(&S.halo_sh, (size_t)kHaloShards * S.halo_sh_cap));
   TRY(dev_alloc(&S.ctr, 1, 0));
   uint8_t slab_sel[8];   // mesher.py:518-525
   for (int m = 0; m < 8; m++) {
@@ -539,7 +541,7 @@ int vm_destroy(vm_engine *e) {
   DevState &S = e->S;
   void *ptrs[] = {S.slots, S.ovf_head, S.ovf_lock, S.ovf_key, S.ovf_val, S.ovf_next, S.ovf_stamp, S.bcoord,
                   S.nbr, S.stamp_collect, S.stamp_halo, S.stamp_new, S.bowned, S.slab_bits, S.scope,
-                  S.halo, S.tsdf, S.weight, S.vmask, S.tp, S.tc, S.vbirth, S.vocc, S.vclaim, S.vparam, S.vnrm, S.item_mask, S.fallback, e->d_rays,
+                  S.halo, S.halo_sh, S.tsdf, S.weight, S.vmask, S.tp, S.tc, S.vbirth, S.vocc, S.vclaim, S.vparam, S.vnrm, S.item_mask, S.fallback, e->d_rays,
                   S.ctr, e->d_depth, e->d_scratch};
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -631,6 +633,7 @@ static void fill_stats(vm_engine *e, int64_t frame, vm_stats *out) {
   out->new_blocks = c.nnew;
   out->scope_blocks = (int64_t)c.ncollected + c.nslab;
   out->halo_blocks = c.nhalo;
+  for (int k = 0; k < kHaloShards; k++) out->halo_blocks += std::min(c.nhalo_sh[k], e->S.halo_sh_cap);
   out->active_cubes = c.active;
   out->edge_placements = c.placements;
   out->new_vertices = c.v_allocs;

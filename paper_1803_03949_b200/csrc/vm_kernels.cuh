@@ -24,7 +24,7 @@ namespace vm {
 constexpr int kThreadsCube = 512;   // one thread per cube of a block
 
 enum { F_INIT = 1, F_INTEGRATE = 2, F_SCOPE = 4, F_HALO = 8 };
-enum { G_GC = 1, G_NORMALS = 2, G_COMMIT = 4, G_REQUIRE_ITEMS = 8 };
+enum { G_GC = 1, G_NORMALS = 2, G_COMMIT = 4, G_REQUIRE_ITEMS = 8, G_SHARDED = 16 };
 
 // error and need are adjacent: one 8-byte load
 __device__ __forceinline__ bool halted(const DevState &S) {
@@ -51,30 +51,16 @@ __device__ __forceinline__ int smem_append(int cnt, int *s_count) {
 }
 
 // ------------------------------------------------------------ shared helpers
-// MC tables indexed by a per-thread cube type: from the constant bank every
-// distinct index of a warp is a serialised access, so the meshing kernels copy
-// them to shared memory once per CTA.
-struct __align__(16) SmemTables {
-  uint16_t edge_mask[256];
-  uint8_t tri_count[256];
-};
-__device__ __forceinline__ void load_tables(SmemTables &T) {
-  for (int q = threadIdx.x; q < 128; q += blockDim.x)
-    reinterpret_cast<uint32_t *>(T.edge_mask)[q] = __ldg(reinterpret_cast<const uint32_t *>(g_edge_mask) + q);
-  for (int q = threadIdx.x; q < 64; q += blockDim.x)
-    reinterpret_cast<uint32_t *>(T.tri_count)[q] = __ldg(reinterpret_cast<const uint32_t *>(g_tri_count) + q);
-}
-
 // Per-call counters a kernel needs before its loop, read by ONE thread and
 // broadcast through shared memory (every CTA reading them from every warp
 // serialises thousands of requests on one L2 line).  v[0] = halted, v[1..3]
 // kernel-specific.  Ends with a barrier.
 // (null pointers read as 0).  sv[4] = the CTA's first list entry, prefetched
-// in the same round trip when `first` is non-null, and the MC tables are
-// staged into `T` (if given) meanwhile.
+// in the same round trip when `first` is non-null.  (The MC edge masks are
+// computed from the type bits, edge_mask_of, and the triangle counts read
+// through the read-only cache where a cube changed: no per-CTA table staging.)
 __device__ __forceinline__ void read_prologue(const DevState &S, int *sv, const int32_t *a, const int32_t *b,
-                                              const int32_t *c, const int32_t *first = nullptr,
-                                              SmemTables *T = nullptr) {
+                                              const int32_t *c, const int32_t *first = nullptr) {
   if (threadIdx.x == 0) {
     const int2 h = __ldcg(reinterpret_cast<const int2 *>(&S.ctr->error));
     const int va = a ? __ldcg(a) : 0, vb = b ? __ldcg(b) : 0, vc = c ? __ldcg(c) : 0;
@@ -82,7 +68,6 @@ __device__ __forceinline__ void read_prologue(const DevState &S, int *sv, const 
     sv[0] = (h.x | h.y) != 0;
     sv[1] = va; sv[2] = vb; sv[3] = vc; sv[4] = vf;
   }
-  if (T) load_tables(*T);
   __syncthreads();
 }
 
@@ -872,6 +857,14 @@ __device__ __forceinline__ void ext_src(int q, int &p, int &dir, int &src) {
 // z0 + j's 8 corner bits in CORNER_OFFSETS order (mc_tables.py:31-34:
 // (0,0,0) (1,0,0) (1,1,0) (0,1,0), then the same at z + 1).  spread4 moves
 // 4 bits to the low bit of 4 bytes (one multiply, no carries).
+// bit z (z < 9) -> bit 3 z
+__device__ __forceinline__ uint32_t part1by2_9(uint32_t x) {
+  x &= 0x1FFu;
+  x = (x | (x << 16)) & 0x030000FFu;
+  x = (x | (x << 8)) & 0x0300F00Fu;
+  x = (x | (x << 4)) & 0x030C30C3u;
+  return (x | (x << 2)) & 0x09249249u;
+}
 __device__ __forceinline__ uint32_t spread4(uint32_t v) { return ((v & 0xFu) * 0x00204081u) & 0x01010101u; }
 __device__ __forceinline__ uint32_t corner_bytes4(const uint32_t (&w)[4], int sh) {
   uint32_t r = 0;
@@ -898,9 +891,8 @@ __global__ void __launch_bounds__(kNT, 18) k_retype_place(DevState S, const Fram
   cudaGridDependencySynchronize();   // PDL: wait for the previous kernel of the frame
   trace_at(S, TK_RETYPE, 0);
   __shared__ int s_pro[5];
-  __shared__ SmemTables T;
   read_prologue(S, s_pro, &S.ctr->ncollected, &S.ctr->nslab, &S.ctr->nexplicit,
-                (int)blockIdx.x < S.max_blocks ? S.scope + blockIdx.x : nullptr, &T);
+                (int)blockIdx.x < S.max_blocks ? S.scope + blockIdx.x : nullptr);
   if (s_pro[0]) return;
   const int nc = s_pro[1];
   const int n = F.scope_mode != 0 ? s_pro[3] : nc + s_pro[2];
@@ -909,17 +901,19 @@ __global__ void __launch_bounds__(kNT, 18) k_retype_place(DevState S, const Fram
   __shared__ double tile[729];
   __shared__ uint32_t s_col[81];    // tile column x*9+y: sign bits 0..7, valid 9..16, small 18..25
   __shared__ uint8_t s_top[81];     // its z = 8 point: bit 0 sign, 2 small
-  __shared__ __align__(16) uint32_t s_vm8[8 * 16];   // weight > 0 bitmaps: block + 7 plus-neighbours
-  __shared__ __align__(16) uint8_t s_tc[kNC];
-  __shared__ __align__(16) uint8_t s_tp[kNC];
+  // typing inputs, reused by the placement as per-warp slot lists
+  __shared__ union __align__(16) {
+    struct {
+      uint32_t vm8[8 * 16];   // weight > 0 bitmaps: block + 7 plus-neighbours
+      uint8_t tc[kNC], tp[kNC];
+    } ty;
+  } U;
+  uint32_t *const s_vm8 = U.ty.vm8;
+  uint8_t *const s_tc = U.ty.tc, *const s_tp = U.ty.tp;
   __shared__ uint32_t s_claim[3 * 81];   // requested slots: [axis][tile column], bit = owner z
-  __shared__ uint8_t s_wl[3 * 81];   // non-empty claim words
   __shared__ Resolved R;
-  __shared__ int red8[7 * (kNT / 32)];
-  __shared__ int s_nplace;
   const int t = threadIdx.x, lane = t & 31;
   const double l = S.cube_size;
-  const int frame = F.frame;
   const int do_refine = F.refine;
   const double eps = F.epsilon;
   int placements = 0, active = 0, changed = 0, t_rel = 0, t_new = 0, irr = 0, refined = 0, live = 0;
@@ -931,21 +925,46 @@ __global__ void __launch_bounds__(kNT, 18) k_retype_place(DevState S, const Fram
       resolve_store(S, F, rr, b, i, n, nc, R);
     }
     for (int q = t; q < 3 * 81; q += kNT) s_claim[q] = 0;
-    if (t == 0) s_nplace = 0;
     __syncthreads();
     trace_item(S, TK_RETYPE, nth, 1);
     const int mode = R.mode;
     // fused_halo (mesher.py:530-543): a collected item marks its 27-neighbourhood
-    // (frustum-culled ones too); issued after the tile loads below, so the
-    // exchange round trips overlap them
+    // (frustum-culled ones too).  The exchanges are issued after the tile loads
+    // below and their results consumed only at the end of the item, where the
+    // first markers are appended to the halo list with one atomic per warp (a
+    // single hot counter: an append on the critical path queued behind every
+    // other CTA's)
     const bool halo_item = F.scope_mode == 0 && i < nc && R.b >= 0 && t < 27;
+    int h_nb = -1, h_old = F.epoch;
     auto mark_halo = [&]() {
       if (!halo_item) return;
-      const int nb = R.nbr[t];
-      if (nb >= 0 && atomicExch(S.stamp_halo + nb, F.epoch) != F.epoch) S.halo[atomicAdd(&S.ctr->nhalo, 1)] = nb;
+      h_nb = R.nbr[t];
+      if (h_nb >= 0) h_old = atomicExch(S.stamp_halo + h_nb, F.epoch);
+    };
+    auto append_halo = [&]() {
+      if (t >= 32) return;
+      const bool nw = h_nb >= 0 && h_old != F.epoch;
+      const unsigned bal = __ballot_sync(0xffffffffu, nw);
+      if (!bal) return;
+      const int cnt = __popc(bal), r = __popc(bal & ((1u << t) - 1));
+      const int k = blockIdx.x & (kHaloShards - 1);
+      int base = 0;
+      if (t == 0) base = atomicAdd(&S.ctr->nhalo_sh[k], cnt);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      const int room = max(0, S.halo_sh_cap - base);
+      int obase = 0;
+      if (room < cnt) {   // (uniform) the shard is full: the rest go to the general list
+        if (t == 0) obase = atomicAdd(&S.ctr->nhalo, cnt - room);
+        obase = __shfl_sync(0xffffffffu, obase, 0);
+      }
+      if (nw) {
+        if (r < room) S.halo_sh[(size_t)k * S.halo_sh_cap + base + r] = h_nb;
+        else S.halo[obase + r - room] = h_nb;
+      }
     };
     if (mode <= 0) {
       mark_halo();
+      append_halo();
       __syncthreads();
       continue;
     }
@@ -1065,12 +1084,12 @@ __global__ void __launch_bounds__(kNT, 18) k_retype_place(DevState S, const Fram
           new_tc = (new_tc & ~(0xFFu << (8 * k))) | (tc << (8 * k));
           if (tc != tp && own) {
             changed++;
-            const int nold = T.tri_count[tp], nnew = T.tri_count[tc];
+            const int nold = __ldg(g_tri_count + tp), nnew = __ldg(g_tri_count + tc);
             t_rel += nold;
             t_new += nnew;
             irr += (nnew > 0 && !is_regular_type(tc)) - (nold > 0 && !is_regular_type(tp));
           }
-          const unsigned mask = T.edge_mask[tc];
+          const unsigned mask = edge_mask_of(tc);
           if (mask && own) {
             active++;
             placements += __popc(mask);
@@ -1104,57 +1123,103 @@ __global__ void __launch_bounds__(kNT, 18) k_retype_place(DevState S, const Fram
       if (czd) atomicOr(&s_claim[2 * 81 + cols[3]], czd);
     }
     __syncthreads();
-    // list the non-empty claim words (word a * 81 + col: owner heights z of
-    // axis a in tile column col; each requested slot once, whichever cubes
-    // asked for it)
-#pragma unroll
-    for (int r = 0; r < (3 * 81 + kNT - 1) / kNT; r++) {
-      const int wi = t + r * kNT;
-      const uint32_t word = wi < 3 * 81 ? s_claim[wi] : 0u;
-      const int pos = smem_append(word != 0u, &s_nplace);
-      if (word) s_wl[pos] = (uint8_t)wi;
-    }
-    __syncthreads();
     trace_item(S, TK_RETYPE, nth, 3);
-    // placement, one claim word (<= 9 slots) per thread at a time: the slot's
-    // coordinate (mesher.py:216-235; every requester writes the same bits) and
-    // a request bit in the owner block's claim bitmap (a reduction, no round
-    // trip); k_gc_normals turns first requests into allocations
-    const int nwl = s_nplace;
-    for (int p = t; p < nwl; p += kNT) {
-      const int wi = s_wl[p];
-      const uint32_t word = s_claim[wi];
-      const int axis = wi / 81, col = wi - 81 * axis;
-      const int ox = col / 9, oy = col - 9 * ox;
-      const int sa = axis == 0 ? 81 : axis == 1 ? 9 : 1;
-      const int ga_c = axis == 0 ? R.coord.x * kB + ox : R.coord.y * kB + oy;   // (axis 2: per z)
+    // placement (mesher.py:216-235), one tile column per lane: its 3 claim words
+    // interleave into a 27-bit mask, bit 3 z + axis = the slot (z, axis) of the
+    // column's owner cubes -- consecutive slot indices of the owner block
+    // (C-order cubes, 3 slots each), so the column's requests are <= 3 OR
+    // reductions into the owner blocks' claim bitmaps (k_gc_normals turns first
+    // requests into allocations).  The requested slots are then dealt out one
+    // per lane (a warp search over the lanes' prefix counts) for their
+    // coordinate stores; every requester of a slot writes the same bits.
+    {
+      const int wq = t >> 5;
 #pragma unroll
-      for (int z = 0; z < 9; z++) {
-        if (!((word >> z) & 1u)) continue;
-        const int owner = R.nbr[nbr_dir(ox >> 3, oy >> 3, z >> 3)];
-        if (owner < 0) {
-          set_error(S, ERR_CONSISTENCY, 10, R.coord.x * kB + ox, R.coord.y * kB + oy, R.coord.z * kB + z);
-          continue;
+      for (int round = 0; round < 2; round++) {
+        // warp 0: columns 0..31, 64..72; warp 1: 32..63, 73..80
+        const int col = round == 0 ? wq * 32 + lane : 64 + wq * 9 + lane;
+        const bool has = round == 0 || lane < 9 - wq;
+        uint32_t m = 0;
+        int sA = 0, ox = 0, oy = 0;
+        if (has) {
+          m = part1by2_9(s_claim[col]) | (part1by2_9(s_claim[81 + col]) << 1) |
+              (part1by2_9(s_claim[162 + col]) << 2);
+          if (m) {
+            ox = col / 9;
+            oy = col - 9 * ox;
+            sA = ((ox & 7) * 64 + (oy & 7) * 8) * 3;   // slot of (owner cube z = 0, axis 0)
+            const int A = R.nbr[nbr_dir(ox >> 3, oy >> 3, 0)], B = R.nbr[nbr_dir(ox >> 3, oy >> 3, 1)];
+            const uint32_t mA = m & 0xFFFFFFu, mB = m >> 24;
+            const int off = sA & 31;
+            if (mA) {
+              if (A >= 0) {
+                uint32_t *wp = S.vclaim + (size_t)A * (kEV / 32) + (sA >> 5);
+                atomicOr(wp, mA << off);
+                if (off > 8) atomicOr(wp + 1, mA >> (32 - off));
+              } else {
+                set_error(S, ERR_CONSISTENCY, 10, R.coord.x * kB + ox, R.coord.y * kB + oy,
+                          R.coord.z * kB + (__ffs(mA) - 1) / 3);
+                m &= ~0xFFFFFFu;
+              }
+            }
+            if (mB) {
+              if (B >= 0) atomicOr(S.vclaim + (size_t)B * (kEV / 32) + (sA >> 5), mB << off);
+              else {
+                set_error(S, ERR_CONSISTENCY, 10, R.coord.x * kB + ox, R.coord.y * kB + oy, R.coord.z * kB + 8);
+                m &= 0xFFFFFFu;
+              }
+            }
+          }
         }
-        const size_t slot = (size_t)owner * kEV + (((ox & 7) * 64 + (oy & 7) * 8 + (z & 7)) * 3 + axis);
-        // start corner = the owner point; end corner one step along the axis
-        const int pt = col * 9 + z;
-        const double d0 = tile[pt], d1 = tile[pt + sa];
-        const double param = (d0 == d1) ? 0.5 : d0 / (d0 - d1);
-        const int ga = axis == 2 ? R.coord.z * kB + z : ga_c;
-        S.vparam[slot] = __dadd_rn(__dmul_rn((double)ga, l), __dmul_rn(param, l));
-        atomicOr(S.vclaim + (slot >> 5), 1u << (slot & 31));
+        const int cnt = __popc(m);
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int u = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += u;
+        }
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        for (int e0 = 0; e0 < total; e0 += 32) {
+          const int e = e0 + lane;
+          // the lane L whose slots hold entry e: the count of lanes with incl <= e
+          int L = 0;
+#pragma unroll
+          for (int step = 16; step > 0; step >>= 1) {
+            const int v = __shfl_sync(0xffffffffu, incl, L + step - 1);
+            if (v <= e) L += step;
+          }
+          uint32_t bm = __shfl_sync(0xffffffffu, m, L);
+          const int k = e - (__shfl_sync(0xffffffffu, incl, L) - __popc(bm));
+          if (e < total) {
+            for (int q = 0; q < k; q++) bm &= bm - 1;
+            const int bit = __ffs(bm) - 1;
+            const int z = bit / 3, axis = bit - 3 * z;
+            const int c = round == 0 ? wq * 32 + L : 64 + wq * 9 + L;
+            const int cx = c / 9, cy = c - 9 * cx;
+            const int owner = R.nbr[nbr_dir(cx >> 3, cy >> 3, z >> 3)];
+            const size_t slot = (size_t)owner * kEV + ((cx & 7) * 64 + (cy & 7) * 8 + (z & 7)) * 3 + axis;
+            // start corner = the owner point; end corner one step along the axis
+            const int pt = c * 9 + z;
+            const double d0 = tile[pt], d1 = tile[pt + (axis == 0 ? 81 : axis == 1 ? 9 : 1)];
+            const double param = (d0 == d1) ? 0.5 : d0 / (d0 - d1);
+            const int ga = axis == 0 ? R.coord.x * kB + cx : axis == 1 ? R.coord.y * kB + cy : R.coord.z * kB + z;
+            S.vparam[slot] = __dadd_rn(__dmul_rn((double)ga, l), __dmul_rn(param, l));
+          }
+        }
       }
     }
+    trace_at(S, TK_RETYPE, 30);
+    append_halo();
+    if (t == 32) trace_at_any(S, TK_RETYPE, 29);
     __syncthreads();   // R, tile and the placement list are rewritten by the next item
   }
   {
     trace_count(S, TK_RETYPE, nth);
     trace_at(S, TK_RETYPE, 28);
-    int vals[7] = {placements, active, changed, t_rel, t_new, irr, refined};
+    const int vals[7] = {placements, active, changed, t_rel, t_new, irr, refined};
     int64_t *const dst[7] = {&S.ctr->placements, &S.ctr->active, &S.ctr->changed,
                              &S.ctr->t_released, &S.ctr->t_allocated, &S.ctr->irr_delta, &S.ctr->refined};
-    block_add_counters<7, kNT / 32>(vals, red8, dst);
+    warp_add_counters<7>(vals, dst);
   }
   if (t == 0 && live) S.ctr->nitems_live = 1;   // (a flag: some item was live this call)
   trace_at(S, TK_RETYPE, 31);
@@ -1227,12 +1292,24 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
   trace_at(S, TK_GC, 0);
   Counters *ctr = S.ctr;
   __shared__ int s_pro[5];
-  __shared__ SmemTables T;
+  __shared__ int s_shp[kHaloShards + 1];   // G_SHARDED: prefix of the shard fills
+  const bool sharded = (mode & G_SHARDED) != 0;
+  if (sharded && threadIdx.x < 32) {
+    int c = min(__ldcg(ctr->nhalo_sh + threadIdx.x), S.halo_sh_cap);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, c, o);
+      if ((int)threadIdx.x >= o) c += u;
+    }
+    s_shp[threadIdx.x + 1] = c;
+    if (threadIdx.x == 0) s_shp[0] = 0;
+  }
   read_prologue(S, s_pro, (mode & G_REQUIRE_ITEMS) ? &ctr->nitems_live : nullptr, count_ptr, nullptr,
-                nullptr, &T);
+                nullptr);
   if (s_pro[0]) return;
   const int live_items = (mode & G_REQUIRE_ITEMS) ? s_pro[1] : 1;
-  const int n = live_items > 0 ? (count_ptr ? s_pro[2] : count_const) : 0;
+  const int nsh = sharded ? s_shp[kHaloShards] : 0;
+  const int n = live_items > 0 ? nsh + (count_ptr ? s_pro[2] : count_const) : 0;
   __shared__ GcItem G[kGW];
   __shared__ int red[4 * kGW];
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
@@ -1251,7 +1328,16 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
     // entries are neighbouring blocks of similar surface density)
     const int i = base + w * (int)gridDim.x + blockIdx.x;
     {
-      const int bi = i < n ? __ldcg(list + i) : -1;
+      int bi = -1;
+      if (i < nsh) {   // shard k holds flat items [s_shp[k], s_shp[k + 1])
+        int k = 0;
+#pragma unroll
+        for (int step = kHaloShards / 2; step > 0; step >>= 1)
+          if (s_shp[k + step] <= i) k += step;
+        bi = __ldcg(S.halo_sh + (size_t)k * S.halo_sh_cap + (i - s_shp[k]));
+      } else if (i < n) {
+        bi = __ldcg(list + (i - nsh));
+      }
       const ResolveRegs rr = resolve_load(S, Fr, bi, i, 0);
       resolve_store(S, Fr, rr, bi, i, n, 0, I.R);
     }
@@ -1338,7 +1424,7 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
               ty[q] = I.tt[tt_idx(l0, l1, l2)];
             }
 #pragma unroll
-            for (int q = 0; q < 4; q++) ref |= (unsigned)T.edge_mask[ty[q]] >> cube_edge_of_slot(axis, q >> 1, q & 1);
+            for (int q = 0; q < 4; q++) ref |= edge_mask_of(ty[q]) >> cube_edge_of_slot(axis, q >> 1, q & 1);
             if (!(ref & 1u)) {
               keep = false;
               S.vbirth[(size_t)b * kEV + sl] = -1;
@@ -1449,7 +1535,7 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
             const uint32_t ty = I.tt[tt_idx(l0, l1, l2)];
             const int dir = nbr_dir(l0 < 0 ? -1 : 0, l1 < 0 ? -1 : 0, l2 < 0 ? -1 : 0);
             types4 |= ty << (8 * q);
-            if (((T.edge_mask[ty] >> cube_edge_of_slot(axis, q >> 1, q & 1)) & 1) && I.R.nbr[dir] >= 0 &&
+            if (((edge_mask_of(ty) >> cube_edge_of_slot(axis, q >> 1, q & 1)) & 1) && I.R.nbr[dir] >= 0 &&
                 I.inhalo[dir])
               cand |= 1u << q;
           }
