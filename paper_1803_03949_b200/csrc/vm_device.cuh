@@ -44,7 +44,7 @@ enum { NEED_BLOCKS = 1 };
 // shards' prefix then the general list.
 constexpr int kHaloShards = 32;
 
-struct Counters {
+struct alignas(16) Counters {
   int32_t nblocks;       // SpatialStore.block_count
   int32_t ovf_count;
   int32_t error;
@@ -84,7 +84,10 @@ struct Counters {
   int64_t fallbacks;
   int64_t refined;
   int32_t nhalo_sh[kHaloShards];   // halo shard fill counts (may exceed halo_sh_cap: clamp)
+  unsigned long long t_start_ns;   // %globaltimer: k_collect start, k_gc_normals commit
+  unsigned long long t_end_ns;
 };
+static_assert(sizeof(Counters) % 16 == 0, "snapshots are copied in 16-byte words");
 
 // Per-call parameters in device memory (a captured frame graph replays with
 // new poses / depth pointers).
@@ -106,7 +109,21 @@ struct FrameDev {
   int32_t scope_mode;   // 0: collected + slabs (device scope); 1: explicit items
   int32_t nsteps_fixed; // > 0: band step count fixed by the intrinsics (k_depth_stats skipped)
   int32_t consume_fb;   // fuse_frame: k_collect applies the previous frame's fallback records
-  int32_t pad2;
+  int32_t reset_after;  // k_gc_normals' commit clears the per-call counters after its snapshot
+  Counters *snap;       // non-null: k_gc_normals' commit copies the counter block here (device)
+  // non-null: k_collect copies the previous frame's snapshot (pub_src) to the
+  // host's mapped buffer (pub_dst) and then writes pub_id to *pub_seq, the
+  // word the host waits on -- off the frame's critical path
+  const Counters *pub_src;
+  Counters *pub_dst;
+  unsigned long long *pub_seq;
+  unsigned long long pub_id;
+  // non-null: k_gc_normals' commit publishes this frame's own snapshot to the
+  // host (used when the next frame's input arrives by a host copy, so its
+  // k_collect would publish late)
+  Counters *self_dst;
+  unsigned long long *self_seq;
+  unsigned long long self_id;
 };
 
 // one hash slot: packed coordinate (-1 empty) and block index (-1 while the
@@ -189,11 +206,21 @@ __device__ __forceinline__ void trace_count(const DevState &S, int k, int n) {
   if (S.trace && threadIdx.x == 0 && blockIdx.x < kTraceCtas)
     S.trace[((size_t)k * kTraceCtas + blockIdx.x) * kTraceSlots + 27] = (unsigned long long)n;
 }
+// per-frame kernel spans (a ring of 256 frames after the per-CTA area): entry
+// [frame][2k] = kernel k's block-0 start, [2k+1] = the latest CTA end
+constexpr size_t kTraceRing = (size_t)TK_COUNT * kTraceCtas * kTraceSlots;
+__device__ __forceinline__ void trace_span(const DevState &S, int k, int frame, bool end) {
+  if (!S.trace || threadIdx.x != 0) return;
+  unsigned long long *r = S.trace + kTraceRing + (size_t)(frame & 255) * 8 + 2 * k;
+  if (end) atomicMax(r + 1, gtimer());
+  else if (blockIdx.x == 0) *r = gtimer();
+}
 // (any thread: per-warp marks)
 __device__ __forceinline__ void trace_at_any(const DevState &S, int k, int slot) {
   if (S.trace && blockIdx.x < kTraceCtas) S.trace[((size_t)k * kTraceCtas + blockIdx.x) * kTraceSlots + slot] = gtimer();
 }
 #else
+__device__ __forceinline__ void trace_span(const DevState &, int, int, bool) {}
 __device__ __forceinline__ void trace_at_any(const DevState &, int, int) {}
 __device__ __forceinline__ void trace_at(const DevState &, int, int) {}
 __device__ __forceinline__ void trace_count(const DevState &, int, int) {}

@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <array>
 #include <cstdarg>
 #include <cstdio>
@@ -84,8 +85,21 @@ struct vm_engine {
   // vm_fuse_frame_submit can queue frame t+1 before frame t is settled.
   int fslot = 0;                      // slot of the most recently enqueued frame
   FrameDev f_saved[2];                // its parameters (as launched)
+  // Frame counters: k_gc_normals' commit copies them to d_snapbuf[slot]; when
+  // the next frame is already queued its k_collect publishes that copy to the
+  // mapped pinned h_snap[slot] and then writes the sequence word h_seq[slot]
+  Counters *d_snapbuf[2] = {nullptr, nullptr};
   Counters *h_snap[2] = {nullptr, nullptr};
-  cudaEvent_t ev_done[2] = {nullptr, nullptr};
+  unsigned long long *h_seq[2] = {nullptr, nullptr};
+  Counters *d_snap[2] = {nullptr, nullptr};           // (device views of h_snap / h_seq)
+  unsigned long long *d_seq[2] = {nullptr, nullptr};
+  bool publish_prev = false;          // set by vm_fuse_frame_submit: the frame launched next publishes
+  bool host_input = false;            // set by vm_fuse_frame_submit: this frame's depth came by a host copy
+  bool self_pub[2] = {false, false};  // the slot's frame publishes its own snapshot (gc commit)
+  unsigned long long snap_ids = 0, want_id[2] = {0, 0};
+  bool ev_rec[2] = {false, false};   // the slot's frame recorded PH_DEPTH / PH_END events
+  bool ctr_clean = false;            // the per-call counters are zero (a frame's commit cleared them)
+  bool restore_calls = false;        // ... and hold nothing: a non-frame call restores the last frame's
   int64_t frame_of[2] = {0, 0};
   int last_resumes = 0;
   int frame_launches = 0;   // kernels launched by the pending / last frame
@@ -113,6 +127,7 @@ struct vm_engine {
 extern "C" {
 static int settle(vm_engine *e);
 static int settle_all(vm_engine *e);
+static int settle_slot(vm_engine *e, int slot, bool succ);
 }
 
 // ------------------------------------------------------------ helpers
@@ -258,7 +273,7 @@ static int reset_call_counters(vm_engine *e) {
 }
 
 static inline void rec(vm_engine *e, int ph) {
-  if (e->profiling || ph == PH_DEPTH || ph == PH_END) cudaEventRecord(e->ev[ph], e->stream);
+  if (e->profiling) cudaEventRecord(e->ev[ph], e->stream);   // (else the kernels' own clock: t_start/t_end_ns)
 }
 
 // frame segment after collect: fuse (init/integrate/scope), retype+place, gc+normals
@@ -460,9 +475,16 @@ int vm_create(const vm_store_config *cfg, vm_engine **out) {
   e->own_stream = true;
   for (int k = 0; k < 2; k++) {
     for (int i = 0; i < PH_COUNT; i++) CK(cudaEventCreate(&e->evs[k][i]));
-    CK(cudaEventCreateWithFlags(&e->ev_done[k], cudaEventDisableTiming));
-    CK(cudaMallocHost((void **)&e->h_snap[k], sizeof(Counters)));
-    memset(e->h_snap[k], 0, sizeof(Counters));
+    const size_t sb = (sizeof(Counters) + 63) & ~(size_t)63;
+    void *hp = nullptr, *dp = nullptr;
+    CK(cudaHostAlloc(&hp, sb + 64, cudaHostAllocMapped));
+    memset(hp, 0, sb + 64);
+    CK(cudaHostGetDevicePointer(&dp, hp, 0));
+    e->h_snap[k] = (Counters *)hp;
+    e->h_seq[k] = (unsigned long long *)((char *)hp + sb);
+    e->d_snap[k] = (Counters *)dp;
+    e->d_seq[k] = (unsigned long long *)((char *)dp + sb);
+    TRY(dev_alloc(&e->d_snapbuf[k], 1, 0));
   }
   CK(cudaMallocHost((void **)&e->h_ctr, sizeof(Counters)));
   CK(cudaMallocHost((void **)&e->h_frame, sizeof(FrameDev)));
@@ -551,8 +573,8 @@ int vm_destroy(vm_engine *e) {
   for (int k = 0; k < 2; k++) {
     for (int i = 0; i < PH_COUNT; i++)
       if (e->evs[k][i]) cudaEventDestroy(e->evs[k][i]);
-    if (e->ev_done[k]) cudaEventDestroy(e->ev_done[k]);
     if (e->h_snap[k]) cudaFreeHost(e->h_snap[k]);
+    if (e->d_snapbuf[k]) cudaFree(e->d_snapbuf[k]);
   }
   if (e->copy_stream) cudaStreamSynchronize(e->copy_stream);
   for (int i = 0; i < 2; i++) {
@@ -647,7 +669,12 @@ static void fill_stats(vm_engine *e, int64_t frame, vm_stats *out) {
   out->resumes = e->last_resumes;
   out->kernel_launches = e->frame_launches;
   float ms = 0.f;
-  if (cudaEventElapsedTime(&ms, e->ev[PH_DEPTH], e->ev[PH_END]) == cudaSuccess) out->device_ms = ms;
+  if (e->ev_rec[e->ev == e->evs[1]]) {
+    cudaEventSynchronize(e->ev[PH_END]);
+    if (cudaEventElapsedTime(&ms, e->ev[PH_DEPTH], e->ev[PH_END]) == cudaSuccess) out->device_ms = ms;
+  } else if (c.t_end_ns > c.t_start_ns && c.t_start_ns) {   // submitted frame: the kernels' own clock
+    out->device_ms = (double)(c.t_end_ns - c.t_start_ns) * 1e-6;
+  }
   if (e->profiling) {   // segment split needs the per-kernel events
     if (cudaEventElapsedTime(&ms, e->ev[PH_DEPTH], e->ev[PH_RETYPE]) == cudaSuccess) out->fusion_ms = ms;
     if (cudaEventElapsedTime(&ms, e->ev[PH_RETYPE], e->ev[PH_END]) == cudaSuccess) out->meshing_ms = ms;
@@ -710,9 +737,28 @@ static int fixed_nsteps(vm_engine *e, double trunc) {
 static int launch_frame(vm_engine *e, int slot) {
   FrameDev &F = *e->h_frame;
   F = e->f_saved[slot];
+  F.snap = e->d_snapbuf[slot];
+  F.reset_after = 1;
+  e->want_id[slot] = ++e->snap_ids;
+  // Host-copied input: the next frame's k_collect starts only after its copy,
+  // so this frame's gc commit publishes itself (a few PCIe writes at its end);
+  // else the next frame's k_collect publishes it, off the critical path.
+  e->self_pub[slot] = e->host_input;
+  if (e->host_input) {
+    F.self_dst = e->d_snap[slot];
+    F.self_seq = e->d_seq[slot];
+    F.self_id = e->want_id[slot];
+  }
+  if (e->publish_prev && !e->self_pub[slot ^ 1]) {   // the pending frame's snapshot, from this k_collect
+    F.pub_src = e->d_snapbuf[slot ^ 1];
+    F.pub_dst = e->d_snap[slot ^ 1];
+    F.pub_seq = e->d_seq[slot ^ 1];
+    F.pub_id = e->want_id[slot ^ 1];
+  }
   e->fslot = slot;
   e->ev = e->evs[slot];
-  TRY(reset_call_counters(e));
+  e->ev_rec[slot] = e->profiling;
+  if (!e->ctr_clean) TRY(reset_call_counters(e));
   cudaStream_t st = e->stream;
   rec(e, PH_DEPTH);
   e->frame_launches = 4;   // collect, fuse, retype, gc (+ depth stats)
@@ -726,8 +772,16 @@ static int launch_frame(vm_engine *e, int slot) {
   launch_pdl(k_collect, e->grid_collect, kCollectThreads, st, e->S, Fc);
   F.raw = nullptr;   // (the later kernels read the f64 depth)
   TRY(enqueue_after_collect(e));
-  CK(cudaMemcpyAsync(e->h_snap[slot], e->S.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
-  CK(cudaEventRecord(e->ev_done[slot], st));
+  // the frame's gc commit publishes its counters and clears the per-call ones:
+  // the next frame's kernels follow with no stream operation in between
+  F.snap = nullptr;
+  F.reset_after = 0;
+  F.pub_src = nullptr;
+  F.pub_dst = nullptr;
+  F.pub_seq = nullptr;
+  F.self_dst = nullptr;
+  F.self_seq = nullptr;
+  e->ctr_clean = true;
   e->pending = 1;
   e->pending_frame = e->frame_of[slot];
   return VM_OK;
@@ -771,9 +825,8 @@ int vm_fuse_frame_finish(vm_engine *e, vm_stats *out) {
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
   if (!e->pending) return set_err(VM_ERR_INPUT, "no frame pending");
   e->pending = 0;
-  e->last_resumes = 0;
-  TRY(complete_with_resume(e, &e->last_resumes));
-  if (out) fill_stats(e, e->pending_frame, out);
+  TRY(settle_slot(e, e->fslot, false));
+  if (out) *out = e->settled;
   return VM_OK;
 }
 
@@ -798,17 +851,41 @@ int vm_fuse_frame(vm_engine *e, const double *depth, int32_t h, int32_t w, int32
 // resumed as in the synchronous path, and the queued frame is launched again
 // (or, when the frame failed, dropped: the engine is left as the synchronous
 // path leaves it).
+// The frame's counters: published by the queued successor's k_collect (wait
+// on the sequence word; the GPU stays busy), else read after the stream drains.
+static int wait_snapshot(vm_engine *e, int slot, bool succ) {
+  volatile unsigned long long *seq = e->h_seq[slot];
+  const unsigned long long want = e->want_id[slot];
+  for (unsigned spins = 1; succ && *seq != want; spins++) {
+    if ((spins & 1023u) == 0) {   // (a failed launch publishes nothing: watch the stream)
+      const cudaError_t q = cudaStreamQuery(e->stream);
+      if (q != cudaSuccess && q != cudaErrorNotReady)
+        return set_err(VM_ERR_CUDA, "frame failed: %s", cudaGetErrorString(q));
+      if (q == cudaSuccess && *seq != want) succ = false;
+    }
+  }
+  if (succ) {
+    std::atomic_thread_fence(std::memory_order_acquire);
+    memcpy(e->h_ctr, e->h_snap[slot], sizeof(Counters));
+  } else {
+    TRY(copy_sync(e, e->h_ctr, e->d_snapbuf[slot], sizeof(Counters), cudaMemcpyDeviceToHost));
+  }
+  return VM_OK;
+}
+
 static int settle_slot(vm_engine *e, int slot, bool succ) {
-  CK(cudaEventSynchronize(e->ev_done[slot]));
+  TRY(wait_snapshot(e, slot, succ));
   const int launched = e->frame_launches;
-  memcpy(e->h_ctr, e->h_snap[slot], sizeof(Counters));
   e->ev = e->evs[slot];
   e->last_resumes = 0;
   int rc = VM_OK;
+  e->restore_calls = true;   // (unhalted: the commit cleared the per-call counters)
   if (e->h_ctr->need || e->h_ctr->error) {
+    e->ctr_clean = false;    // (halted: not cleared)
+    e->restore_calls = false;
     if (succ) {
       CK(cudaStreamSynchronize(e->stream));
-      TRY(copy_sync(e, e->S.ctr, e->h_snap[slot], sizeof(Counters), cudaMemcpyHostToDevice));
+      TRY(copy_sync(e, e->S.ctr, e->h_ctr, sizeof(Counters), cudaMemcpyHostToDevice));
       *e->h_frame = e->f_saved[slot];
       e->h_frame->raw = nullptr;
     }
@@ -849,6 +926,13 @@ static int flush_fallbacks(vm_engine *e) {
 
 static int settle_all(vm_engine *e) {
   TRY(settle(e));
+  if (e->restore_calls) {   // the last frame's per-call counters, as a synchronous frame leaves them
+    const size_t off = offsetof(Counters, nvalid);
+    TRY(copy_sync(e, (char *)e->S.ctr + off, (const char *)e->h_ctr + off, sizeof(Counters) - off,
+                  cudaMemcpyHostToDevice));
+    e->restore_calls = false;
+  }
+  e->ctr_clean = false;
   return flush_fallbacks(e);
 }
 
@@ -890,7 +974,11 @@ int vm_fuse_frame_submit(vm_engine *e, const double *depth, int32_t h, int32_t w
   const bool prev = e->pending != 0;
   const int pslot = e->fslot;
   e->pending = 0;
+  e->publish_prev = prev;
+  e->host_input = sl >= 0;
   const int rc = vm_fuse_frame_enqueue(e, dd, h, w, 1, intr, pose, cfg, frame_index);
+  e->publish_prev = false;
+  e->host_input = false;
   if (rc != VM_OK) {   // (argument errors: nothing was queued)
     e->pending = prev;
     e->fslot = pslot;
@@ -944,7 +1032,11 @@ int vm_fuse_frame_submit_raw(vm_engine *e, const uint16_t *raw, int32_t h, int32
   const bool prev = e->pending != 0;
   const int pslot = e->fslot;
   e->pending = 0;
+  e->publish_prev = prev;
+  e->host_input = false;   // (a quarter of the bytes: the copy is done before the kernels are)
   const int rc = vm_fuse_frame_enqueue(e, e->d_slot[sl], h, w, 1, intr, pose, cfg, frame_index);
+  e->publish_prev = false;
+  e->host_input = false;
   e->raw_next = nullptr;
   if (rc != VM_OK) {
     e->pending = prev;

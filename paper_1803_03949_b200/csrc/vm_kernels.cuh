@@ -87,9 +87,24 @@ __device__ __forceinline__ void cp_async16(void *dst, const void *src, bool vali
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
+// Publish the previous frame's counter snapshot to the host (k_collect, one CTA)
+__device__ __forceinline__ void publish_snapshot(const FrameDev &F) {
+  constexpr int kWords = (int)(sizeof(Counters) / 4);
+  const uint32_t *src = reinterpret_cast<const uint32_t *>(F.pub_src);
+  uint32_t *dst = reinterpret_cast<uint32_t *>(F.pub_dst);
+  for (int q = threadIdx.x; q < kWords; q += blockDim.x) dst[q] = __ldcg(src + q);
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    *reinterpret_cast<volatile unsigned long long *>(F.pub_seq) = F.pub_id;
+  }
+}
+
 // ------------------------------------------------------------ depth stats
 __global__ void __launch_bounds__(256) k_depth_stats(DevState S, const FrameDev F) {
   cudaGridDependencySynchronize();   // PDL: wait for the previous kernel of the frame
+  if (blockIdx.x == 0 && threadIdx.x == 0) S.ctr->t_start_ns = gtimer();
   __shared__ double smax[8];
   __shared__ int scnt[8];
   const long long npix = (long long)F.h * F.w;
@@ -354,7 +369,10 @@ __device__ __forceinline__ int collect_block(const DevState &S, const FrameDev &
 __global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, const FrameDev F) {
   cudaGridDependencySynchronize();   // PDL: wait for the previous kernel of the frame
   trace_at(S, TK_COLLECT, 0);
+  trace_span(S, 0, F.frame, false);
   Counters *ctr = S.ctr;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && F.nsteps_fixed > 0) ctr->t_start_ns = gtimer();
+  if (F.pub_src && blockIdx.x == gridDim.x - 1) publish_snapshot(F);
   int nsteps = F.nsteps_fixed;
   if (nsteps <= 0) {
     if (ld_vol(&ctr->nvalid) == 0) return;
@@ -520,6 +538,7 @@ __global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, cons
   }
   if (blockIdx.x == 0 && t == 0) ctr->nsteps = nsteps;
   trace_count(S, TK_COLLECT, nth);
+  trace_span(S, 0, F.frame, true);
   trace_at(S, TK_COLLECT, 31);
 }
 
@@ -596,6 +615,7 @@ __global__ void __launch_bounds__(kFB, 6) k_fuse_blocks(DevState S, const FrameD
                                                      int count_const, int flags) {
   cudaGridDependencySynchronize();   // PDL: wait for the previous kernel of the frame
   trace_at(S, TK_FUSE, 0);
+  trace_span(S, 1, F.frame, false);
   __shared__ int s_pro[5];
   const int list_cap = count_ptr ? S.max_blocks : count_const;
   read_prologue(S, s_pro, count_ptr, nullptr, nullptr, (int)blockIdx.x < list_cap ? list + blockIdx.x : nullptr);
@@ -711,6 +731,7 @@ __global__ void __launch_bounds__(kFB, 6) k_fuse_blocks(DevState S, const FrameD
     trace_item(S, TK_FUSE, nth, 3);
   }
   trace_count(S, TK_FUSE, nth);
+  trace_span(S, 1, F.frame, true);
   trace_at(S, TK_FUSE, 31);
 }
 
@@ -890,6 +911,7 @@ __device__ __forceinline__ uint32_t corner_bytes4(const uint32_t (&w)[4], int sh
 __global__ void __launch_bounds__(kNT, 18) k_retype_place(DevState S, const FrameDev F) {
   cudaGridDependencySynchronize();   // PDL: wait for the previous kernel of the frame
   trace_at(S, TK_RETYPE, 0);
+  trace_span(S, 2, F.frame, false);
   __shared__ int s_pro[5];
   read_prologue(S, s_pro, &S.ctr->ncollected, &S.ctr->nslab, &S.ctr->nexplicit,
                 (int)blockIdx.x < S.max_blocks ? S.scope + blockIdx.x : nullptr);
@@ -1222,6 +1244,7 @@ __global__ void __launch_bounds__(kNT, 18) k_retype_place(DevState S, const Fram
     warp_add_counters<7>(vals, dst);
   }
   if (t == 0 && live) S.ctr->nitems_live = 1;   // (a flag: some item was live this call)
+  trace_span(S, 2, F.frame, true);
   trace_at(S, TK_RETYPE, 31);
 }
 constexpr size_t kRetypeSmem = 0;
@@ -1251,6 +1274,86 @@ __device__ __forceinline__ size_t sample_index(const int *s_nbr, int lx, int ly,
   const int nb = s_nbr[nbr_dir(lx >> 3, ly >> 3, lz >> 3)];
   return nb < 0 ? ~(size_t)0 : (size_t)nb * kNC + ((lx & 7) * 64 + (ly & 7) * 8 + (lz & 7));
 }
+
+// End of k_gc_normals, every CTA (halted ones included).  G_COMMIT: the last
+// CTA to arrive folds the call's deltas into the pool counters (not for a
+// halted frame: it is resumed and committed then); then, when F.snap is set,
+// copies the counter block there (device memory; the next frame's k_collect
+// publishes it to the host) and with F.reset_after clears the per-call
+// counters for the next frame -- so consecutive frames need no stream
+// operation between their kernels.
+__device__ __forceinline__ void gc_commit(const DevState &S, const FrameDev &F, int mode) {
+  __shared__ int s_last;
+  Counters *ctr = S.ctr;
+  if (threadIdx.x == 0) {
+    int last = 0;
+    if (mode & G_COMMIT) {
+      __threadfence();
+      last = atomicAdd(&ctr->done_gc, 1) == (int)gridDim.x - 1;
+    }
+    s_last = last;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int2 h = __ldcg(reinterpret_cast<const int2 *>(&ctr->error));
+  const bool halted = (h.x | h.y) != 0;
+  if (threadIdx.x == 0) {
+    if (!halted) {
+      const long long allocs_all = ld_vol(&ctr->v_allocs), fr = ld_vol(&ctr->v_frees);
+      const long long peak = ctr->v_live + allocs_all;     // all allocations precede all frees
+      if (S.max_vertices > 0 && peak > S.max_vertices)
+        set_error(S, ERR_CAPACITY, peak, S.max_vertices, 3);
+      if (peak > ctr->v_count) ctr->v_count = peak;
+      ctr->v_live = peak - fr;
+      ctr->v_recycled += fr;
+      ctr->v_events += allocs_all;
+      const long long rel = ld_vol(&ctr->t_released), nw = ld_vol(&ctr->t_allocated);
+      ctr->t_live += nw - rel;
+      ctr->t_recycled += rel;
+      if (ctr->t_live > ctr->t_count) ctr->t_count = ctr->t_live;
+      ctr->irregular += ld_vol(&ctr->irr_delta);
+    }
+    ctr->done_gc = 0;
+    ctr->t_end_ns = gtimer();
+    __threadfence();
+  }
+  if (!F.snap) return;
+  __syncthreads();
+  constexpr int kWords = (int)(sizeof(Counters) / 4);
+  const volatile uint32_t *src = reinterpret_cast<const volatile uint32_t *>(ctr);
+  uint32_t *dst = reinterpret_cast<uint32_t *>(F.snap);
+  uint32_t keep[(kWords + 127) / 128];
+#pragma unroll
+  for (int r = 0; r < (kWords + 127) / 128; r++) {
+    const int q = threadIdx.x + 128 * r;
+    keep[r] = q < kWords ? src[q] : 0u;
+  }
+  __syncthreads();   // (every word read before any is cleared)
+#pragma unroll
+  for (int r = 0; r < (kWords + 127) / 128; r++) {
+    const int q = threadIdx.x + 128 * r;
+    if (q < kWords) {
+      dst[q] = keep[r];
+      if (F.reset_after && !halted && q >= (int)(offsetof(Counters, nvalid) / 4))
+        reinterpret_cast<uint32_t *>(ctr)[q] = 0u;
+    }
+  }
+  if (F.self_dst) {   // publish to the host now (the next frame's k_collect waits on a copy)
+    __syncthreads();   // (F.snap complete)
+    if (threadIdx.x < 32) {   // one warp, 16-byte stores, then one system fence before the flag
+      const uint4 *sv = reinterpret_cast<const uint4 *>(F.snap);
+      uint4 *hd = reinterpret_cast<uint4 *>(F.self_dst);
+      for (int q = threadIdx.x; q < (int)(sizeof(Counters) / 16); q += 32) hd[q] = sv[q];
+      __syncwarp();
+      if (threadIdx.x == 0) {
+        __threadfence_system();
+        *reinterpret_cast<volatile unsigned long long *>(F.self_seq) = F.self_id;
+      }
+    }
+  }
+}
+
 
 // per-item shared state of k_gc_normals (one warp stages and collects each)
 struct GcItem {
@@ -1290,6 +1393,7 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
                                                    int count_const, int mode) {
   cudaGridDependencySynchronize();   // PDL: wait for the previous kernel of the frame
   trace_at(S, TK_GC, 0);
+  trace_span(S, 3, F.frame, false);
   Counters *ctr = S.ctr;
   __shared__ int s_pro[5];
   __shared__ int s_shp[kHaloShards + 1];   // G_SHARDED: prefix of the shard fills
@@ -1306,7 +1410,10 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
   }
   read_prologue(S, s_pro, (mode & G_REQUIRE_ITEMS) ? &ctr->nitems_live : nullptr, count_ptr, nullptr,
                 nullptr);
-  if (s_pro[0]) return;
+  if (s_pro[0]) {   // halted frame: no work, but the commit still publishes
+    gc_commit(S, F, mode);
+    return;
+  }
   const int live_items = (mode & G_REQUIRE_ITEMS) ? s_pro[1] : 1;
   const int nsh = sharded ? s_shp[kHaloShards] : 0;
   const int n = live_items > 0 ? nsh + (count_ptr ? s_pro[2] : count_const) : 0;
@@ -1553,26 +1660,8 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
     int64_t *const dst[4] = {&ctr->v_frees, &ctr->normals, &ctr->fallbacks, &ctr->v_allocs};
     block_add_counters<4, kGW>(vals, red, dst);
   }
-  if (t == 0 && (mode & G_COMMIT)) {
-    __threadfence();
-    if (atomicAdd(&ctr->done_gc, 1) == (int)gridDim.x - 1) {
-      __threadfence();
-      const long long allocs_all = ld_vol(&ctr->v_allocs), fr = ld_vol(&ctr->v_frees);
-      const long long peak = ctr->v_live + allocs_all;     // all allocations precede all frees
-      if (S.max_vertices > 0 && peak > S.max_vertices)
-        set_error(S, ERR_CAPACITY, peak, S.max_vertices, 3);
-      if (peak > ctr->v_count) ctr->v_count = peak;
-      ctr->v_live = peak - fr;
-      ctr->v_recycled += fr;
-      ctr->v_events += allocs_all;
-      const long long rel = ld_vol(&ctr->t_released), nw = ld_vol(&ctr->t_allocated);
-      ctr->t_live += nw - rel;
-      ctr->t_recycled += rel;
-      if (ctr->t_live > ctr->t_count) ctr->t_count = ctr->t_live;
-      ctr->irregular += ld_vol(&ctr->irr_delta);
-      ctr->done_gc = 0;
-    }
-  }
+  gc_commit(S, F, mode);
+  trace_span(S, 3, F.frame, true);
   trace_at(S, TK_GC, 31);
 }
 constexpr size_t kGcSmem = 0;
