@@ -1656,9 +1656,25 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
   trace_count(S, TK_GC, nth);
   trace_at(S, TK_GC, 28);
   {
-    int vals[4] = {frees, computed, fallbacks, allocs};
-    int64_t *const dst[4] = {&ctr->v_frees, &ctr->normals, &ctr->fallbacks, &ctr->v_allocs};
-    block_add_counters<4, kGW>(vals, red, dst);
+    // warp sums, then thread 0 adds all four: its own fence in gc_commit then
+    // orders them before its arrival count (the fold reads v_frees / v_allocs)
+    const int vals[4] = {frees, computed, fallbacks, allocs};
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const int v = (int)__reduce_add_sync(0xffffffffu, (unsigned)vals[k]);
+      if (lane == 0) red[w * 4 + k] = v;
+    }
+    __syncthreads();
+    if (t == 0) {
+      int64_t *const dst[4] = {&ctr->v_frees, &ctr->normals, &ctr->fallbacks, &ctr->v_allocs};
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        long long r = 0;
+#pragma unroll
+        for (int q = 0; q < kGW; q++) r += red[q * 4 + k];
+        if (r) atomicAdd((unsigned long long *)dst[k], (unsigned long long)r);
+      }
+    }
   }
   gc_commit(S, F, mode);
   trace_span(S, 3, F.frame, true);
