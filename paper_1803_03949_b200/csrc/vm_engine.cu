@@ -15,6 +15,7 @@
 #include <array>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -527,6 +528,10 @@ int vm_create(const vm_store_config *cfg, vm_engine **out) {
   TRY(dev_alloc(&S.scope, mb));
   TRY(dev_alloc(&S.halo, mb));
   S.halo_sh_cap = (int32_t)((mb + kHaloShards - 1) / kHaloShards + 64);
+  if (const char *cap = getenv("VOXMESH_B200_HALO_SHARD_CAP")) {   // (test hook: force shard spills)
+    const long v = strtol(cap, nullptr, 10);
+    if (v > 0 && v < S.halo_sh_cap) S.halo_sh_cap = (int32_t)v;
+  }
   TRY(dev_alloc(&S.halo_sh, (size_t)kHaloShards * S.halo_sh_cap));
   TRY(dev_alloc(&S.ctr, 1, 0));
   uint8_t slab_sel[8];   // mesher.py:518-525
