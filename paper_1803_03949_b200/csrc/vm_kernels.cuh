@@ -1075,6 +1075,75 @@ __global__ void __launch_bounds__(kNT, 18) k_retype_place(DevState S, const Fram
         w[k] = s_col[cols[k]] | ((tp8 & 1u) << 8) | (val9 << 9) | (((tp8 >> 2) & 1u) << 26);
       }
       uint32_t cxa = 0, cxb = 0, cya = 0, cyb = 0, cza = 0, czb = 0, czc = 0, czd = 0;
+      if (!do_refine) {
+        // Without refinement a cube's type is its corner signs and its edge
+        // mask their sign changes (edge_mask_of), so the column's 8 cubes are
+        // typed word-parallel: bit z of every word below is cube z (or owner
+        // height z).  Selected cubes (scope rule, all 8 weights > 0):
+        uint32_t sel;
+        if (mode == 1) {
+          sel = 0xFFu;
+        } else if (mode == 2) {
+          const int sb = ((x == 7) << 2) | ((y == 7) << 1);
+          sel = ((R.slab & c_slab_sel[sb]) ? 0x7Fu : 0u) | ((R.slab & c_slab_sel[sb | 1]) ? 0x80u : 0u);
+        } else {
+          const int c0 = (x * 8 + y) * 8;
+          sel = (S.item_mask[(size_t)R.item * 16 + (c0 >> 5)] >> (c0 & 31)) & 0xFFu;
+        }
+        const uint32_t vall = ((w[0] & w[1] & w[2] & w[3]) >> 9) & 0x1FFu;   // points z with 4 weights > 0
+        sel &= vall & (vall >> 1);
+        const uint32_t sg0 = w[0] & 0x1FFu, sg1 = w[1] & 0x1FFu, sg2 = w[2] & 0x1FFu, sg3 = w[3] & 0x1FFu;
+        // sign changes along the cube edges (mc_tables.py:44-64): e0/e4 between
+        // corners 0-1 at z / z + 1, e1/e5 1-2, e2/e6 3-2, e3/e7 0-3, e8..e11 the
+        // verticals of corners 0..3
+        const uint32_t d01 = sg0 ^ sg1, d12 = sg1 ^ sg2, d32 = sg3 ^ sg2, d03 = sg0 ^ sg3;
+        const uint32_t z0m = (sg0 ^ (sg0 >> 1)) & 0xFFu, z1m = (sg1 ^ (sg1 >> 1)) & 0xFFu,
+                       z2m = (sg2 ^ (sg2 >> 1)) & 0xFFu, z3m = (sg3 ^ (sg3 >> 1)) & 0xFFu;
+        const uint32_t sel2 = sel | (sel << 1);   // owner heights of the e0..e7 slots: z and z + 1
+        cxa = d01 & sel2;   // e0, e4: (x, y)
+        cxb = d32 & sel2;   // e2, e6: (x, y+1)
+        cya = d12 & sel2;   // e1, e5: (x+1, y)
+        cyb = d03 & sel2;   // e3, e7: (x, y)
+        cza = z0m & sel;    // e8: (x, y)
+        czb = z1m & sel;    // e9: (x+1, y)
+        czc = z2m & sel;    // e10: (x+1, y+1)
+        czd = z3m & sel;    // e11: (x, y+1)
+        if (own) {
+          const uint32_t hz = d01 | d12 | d32 | d03;
+          const uint32_t nonuni = (hz | (hz >> 1) | z0m | z1m | z2m | z3m) & 0xFFu;   // type not 0 / 0xFF
+          active += __popc(nonuni & sel);
+          placements += __popc(d01 & sel) + __popc(d01 & (sel << 1)) + __popc(d32 & sel) +
+                        __popc(d32 & (sel << 1)) + __popc(d12 & sel) + __popc(d12 & (sel << 1)) +
+                        __popc(d03 & sel) + __popc(d03 & (sel << 1)) + __popc(cza) + __popc(czb) +
+                        __popc(czc) + __popc(czd);
+        }
+#pragma unroll
+        for (int half = 0; half < 2; half++) {
+          const int z0 = 4 * half;
+          const uint32_t tcw = corner_bytes4(w, z0);   // the 4 cubes' new types
+          const uint32_t m = spread4(sel >> z0) * 0xFFu;
+          const int c0 = (x * 8 + y) * 8 + z0;
+          const uint32_t old_tc = reinterpret_cast<const uint32_t *>(s_tc)[c0 >> 2];
+          const uint32_t old_tp = reinterpret_cast<const uint32_t *>(s_tp)[c0 >> 2];
+          const uint32_t new_tp = (old_tp & ~m) | (old_tc & m), new_tc = (old_tc & ~m) | (tcw & m);
+          if (own)   // changed cubes (type_curr != type_prev): their triangle deltas
+            for (uint32_t ch = __vcmpne4(tcw, old_tc) & m; ch;) {
+              const int sh = (__ffs(ch) - 1) & ~7;
+              ch &= ~(0xFFu << sh);
+              const unsigned tp = (old_tc >> sh) & 0xFFu, tc = (tcw >> sh) & 0xFFu;
+              changed++;
+              const int nold = __ldg(g_tri_count + tp), nnew = __ldg(g_tri_count + tc);
+              t_rel += nold;
+              t_new += nnew;
+              irr += (nnew > 0 && !is_regular_type(tc)) - (nold > 0 && !is_regular_type(tp));
+            }
+          if (new_tc != old_tc || new_tp != old_tp) {   // 4 cubes per 32-bit store
+            const size_t q4 = ((size_t)b * kNC + c0) >> 2;
+            reinterpret_cast<uint32_t *>(S.tp)[q4] = new_tp;
+            reinterpret_cast<uint32_t *>(S.tc)[q4] = new_tc;
+          }
+        }
+      } else
 #pragma unroll
       for (int half = 0; half < 2; half++) {
         const int z0 = 4 * half;
