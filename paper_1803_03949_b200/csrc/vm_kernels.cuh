@@ -878,6 +878,17 @@ __device__ __forceinline__ void ext_src(int q, int &p, int &dir, int &src) {
 // z0 + j's 8 corner bits in CORNER_OFFSETS order (mc_tables.py:31-34:
 // (0,0,0) (1,0,0) (1,1,0) (0,1,0), then the same at z + 1).  spread4 moves
 // 4 bits to the low bit of 4 bytes (one multiply, no carries).
+// position of the k-th (0-based) set bit of m (k < popc(m)), branch-free
+__device__ __forceinline__ int select_bit(uint32_t m, int k) {
+  int p = 0, c;
+  c = __popc(m & 0xFFFFu);         if (k >= c) { k -= c; p = 16; }
+  c = __popc((m >> p) & 0xFFu);    if (k >= c) { k -= c; p += 8; }
+  c = __popc((m >> p) & 0xFu);     if (k >= c) { k -= c; p += 4; }
+  c = __popc((m >> p) & 0x3u);     if (k >= c) { k -= c; p += 2; }
+  c = (int)((m >> p) & 1u);        if (k >= c) p += 1;
+  return p;
+}
+
 // bit z (z < 9) -> bit 3 z
 __device__ __forceinline__ uint32_t part1by2_9(uint32_t x) {
   x &= 0x1FFu;
@@ -1282,8 +1293,7 @@ __global__ void __launch_bounds__(kNT, 18) k_retype_place(DevState S, const Fram
           uint32_t bm = __shfl_sync(0xffffffffu, m, L);
           const int k = e - (__shfl_sync(0xffffffffu, incl, L) - __popc(bm));
           if (e < total) {
-            for (int q = 0; q < k; q++) bm &= bm - 1;
-            const int bit = __ffs(bm) - 1;
+            const int bit = select_bit(bm, k);
             const int z = bit / 3, axis = bit - 3 * z;
             const int c = round == 0 ? wq * 32 + L : 64 + wq * 9 + L;
             const int cx = c / 9, cy = c - 9 * cx;
