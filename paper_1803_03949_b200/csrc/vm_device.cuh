@@ -232,20 +232,10 @@ __device__ __forceinline__ void trace_item(const DevState &S, int k, int nth, in
 __device__ __forceinline__ void trace_sub(const DevState &S, int k, int nth, int sub) {
   if (nth == 0) trace_at(S, k, 22 + sub);
 }
-#ifdef VM_TRACE
-__device__ __forceinline__ void trace_val(const DevState &S, int k, int nth, int slot, long long v) {
-  if (nth == 0 && S.trace && threadIdx.x == 0 && blockIdx.x < kTraceCtas)
-    S.trace[((size_t)k * kTraceCtas + blockIdx.x) * kTraceSlots + slot] = (unsigned long long)v;
-}
-#else
-__device__ __forceinline__ void trace_val(const DevState &, int, int, int, long long) {}
-#endif
 
 // ---------------------------------------------------------------- tables
 __constant__ uint8_t c_tri_count[256] = VM_TRI_COUNT_INIT;
 __constant__ unsigned long long c_tri_packed[256] = VM_TRI_PACKED_INIT;
-// corner offsets (mc_tables.py:31-34) packed as x | y<<1 | z<<2
-__constant__ uint8_t c_corner[8] = {0, 1, 3, 2, 4, 5, 7, 6};
 // edge geometry (mc_tables.py:44-64): owner offset (packed), axis, oriented corners
 __constant__ uint8_t c_e_own[12] = {0, 1, 2, 0, 4, 5, 6, 4, 0, 1, 3, 2};
 __constant__ uint8_t c_e_axis[12] = {0, 1, 0, 1, 0, 1, 0, 1, 2, 2, 2, 2};
@@ -563,28 +553,6 @@ __device__ __forceinline__ long long block_sum(long long v, long long *sh) {
   return r;
 }
 
-// Block-wide sums of N per-thread counters (each < 2^31 per CTA): one
-// redux.sync per counter and warp, one barrier pair, then one atomicAdd per
-// counter (thread k adds counter k to dst[k]; null = skip).  `sh` holds 32 * N.
-template <int N, int NW>
-__device__ __forceinline__ void block_add_counters(int (&vals)[N], int *sh, int64_t *const (&dst)[N]) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;   // (NW = warps per CTA; sh holds N * NW)
-  __syncthreads();
-#pragma unroll
-  for (int k = 0; k < N; k++) {
-    const unsigned v = __reduce_add_sync(0xffffffffu, (unsigned)vals[k]);
-    if (lane == 0) sh[k * NW + wid] = (int)v;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int k = 0; k < N; k++)   // static indices: dst stays in registers
-    if (threadIdx.x == k) {
-      long long r = 0;
-#pragma unroll
-      for (int w = 0; w < NW; w++) r += sh[k * NW + w];
-      if (r && dst[k]) atomicAdd((unsigned long long *)dst[k], (unsigned long long)r);
-    }
-}
 
 // Warp sums of N per-thread counters (each < 2^31 in magnitude per warp), added
 // by lane k to dst[k] (a reduction, no round trip; null = skip): no barrier, so

@@ -756,47 +756,6 @@ __global__ void k_clear_slabs(DevState S, int nc, int ns) {
     S.slab_bits[S.scope[nc + i]] = 0;
 }
 
-// ------------------------------------------------------------ tile loaders
-// the block's 27-neighbour row, cached in shared memory (one round trip)
-__device__ __forceinline__ void load_nbr_row(const DevState &S, int b, int *s_nbr) {
-  if (threadIdx.x < 27) s_nbr[threadIdx.x] = threadIdx.x == 13 ? b : S.nbr[(size_t)b * 27 + threadIdx.x];
-}
-
-// (B+1)^3 tile of a block plus its 7 plus-neighbours (mesher.py:75-96):
-// tsdf and the "weight > 0" flag.
-__device__ __forceinline__ void load_ext_tile(const DevState &S, int b, const int *s_nbr, double *tile,
-                                              uint8_t *tw) {
-  const int t = threadIdx.x;
-  {
-    const int x = t >> 6, y = (t >> 3) & 7, z = t & 7;
-    const size_t q = (size_t)b * kNC + t;
-    tile[(x * 9 + y) * 9 + z] = S.tsdf[q];
-    tw[(x * 9 + y) * 9 + z] = S.weight[q] > 0;
-  }
-  if (t < 217) {
-    int x, y, z;   // the 217 tile positions with max(x, y, z) == 8
-    if (t < 64) { x = 8; y = t >> 3; z = t & 7; }
-    else if (t < 128) { x = (t - 64) >> 3; y = 8; z = t & 7; }
-    else if (t < 192) { x = (t - 128) >> 3; y = t & 7; z = 8; }
-    else if (t < 200) { x = 8; y = 8; z = t - 192; }
-    else if (t < 208) { x = 8; y = t - 200; z = 8; }
-    else if (t < 216) { x = t - 208; y = 8; z = 8; }
-    else { x = 8; y = 8; z = 8; }
-    const int nb = s_nbr[nbr_dir(x >> 3, y >> 3, z >> 3)];
-    double v = 0.0;
-    uint8_t w = 0;
-    if (nb >= 0) {
-      const size_t q = (size_t)nb * kNC + ((x & 7) * 64 + (y & 7) * 8 + (z & 7));
-      v = S.tsdf[q];
-      w = S.weight[q] > 0;
-    }
-    tile[(x * 9 + y) * 9 + z] = v;
-    tw[(x * 9 + y) * 9 + z] = w;
-  }
-}
-
-
-
 // ------------------------------------------------------------ retype + place
 // Per-item "resolved" record: the item's block, neighbour row and selection mode
 struct Resolved {
@@ -1329,16 +1288,12 @@ __global__ void __launch_bounds__(kNT, 18) k_retype_place(DevState S, const Fram
 constexpr size_t kRetypeSmem = 0;
 
 
-
 // ------------------------------------------------------------ GC + normals
 constexpr int kGT = 128;  // threads per CTA of k_gc_normals (kGW warps, one halo block each)
 // type tile over cube locals -1..7: 81 columns (lx, ly) of 16 bytes, z = 0..7
 // at bytes 0..7 and z = -1 at byte 15 (the -z neighbour's z = 7, fetched as
 // the aligned word of its z = 4..7 into bytes 12..15)
 __device__ __forceinline__ int tt_idx(int lx, int ly, int lz) { return ((lx + 1) * 9 + (ly + 1)) * 16 + (lz & 15); }
-
-
-
 
 
 // weight > 0 of the sample at block-local corner (lx, ly, lz) in [-1, 9]^3,
@@ -1760,9 +1715,6 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
   trace_at(S, TK_GC, 31);
 }
 constexpr size_t kGcSmem = 0;
-
-
-
 
 
 // ------------------------------------------------------------ full scans
