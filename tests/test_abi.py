@@ -55,9 +55,8 @@ def _cuh_array(name):
 
 
 def test_device_edge_tables_match_geometry():
-    from paper_1803_03949_b200.mc_tables import (CORNER_OFFSETS, EDGE_AXIS, EDGE_END_CORNER,
+    from paper_1803_03949_b200.mc_tables import (EDGE_AXIS, EDGE_END_CORNER,
                                                  EDGE_OWNER_OFFSET, EDGE_START_CORNER, pack_offset)
-    assert _cuh_array("c_corner") == [pack_offset(o) for o in CORNER_OFFSETS]
     assert _cuh_array("c_e_own") == [pack_offset(o) for o in EDGE_OWNER_OFFSET]
     assert _cuh_array("c_e_axis") == list(EDGE_AXIS)
     assert _cuh_array("c_e_start") == list(EDGE_START_CORNER)
