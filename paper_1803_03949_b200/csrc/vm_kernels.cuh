@@ -1397,17 +1397,15 @@ struct GcItem {
   __align__(16) uint32_t vm[27 * 16];   // weight > 0 bitmaps of the 27 neighbours
   __align__(16) uint8_t tt[81 * 16];    // type_curr over cube locals -1..7 (tt_idx)
   uint8_t inhalo[28];                   // neighbour is a halo block of this call
-  uint16_t vlist[kEV];                  // surviving slots
-  uint16_t fb[kEV];                     // ... whose gradient failed
-  int nv, nfb;
 };
+// entry of the CTA's union slot lists: item k (of kGW) << 11 | slot (< kEV = 1536)
+__device__ __forceinline__ uint16_t gc_entry(int k, int sl) { return (uint16_t)((k << 11) | sl); }
 
-// kGW warps per CTA, kGW halo blocks per CTA at a time: each warp resolves,
-// stages (cp.async: occupancy and request bits, the 9^3 type tile, the 27
-// neighbours' weight bitmaps) and garbage-collects its own block; the
-// normals of the kGW blocks' surviving vertices are then computed by the whole
-// CTA over the union of their lists, so a block with many vertices shares the
-// work with lighter ones.
+// kGW warps per CTA, kGW halo blocks per CTA at a time: each warp resolves
+// and stages its own block (cp.async: occupancy and request bits, the 9^3 type
+// tile, the 27 neighbours' weight bitmaps); requests, GC, normals and the
+// fallback records then run over the union of the kGW blocks' slots with the
+// whole CTA, so a block with many vertices shares the work with lighter ones.
 //  * requests (k_retype_place) of empty slots become allocations: birth =
 //    frame, normal 0 (store.py:145-162);
 //  * G_GC clears every occupied slot that no cube references any more (the
@@ -1452,6 +1450,9 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
   const int nsh = sharded ? s_shp[kHaloShards] : 0;
   const int n = live_items > 0 ? nsh + (count_ptr ? s_pro[2] : count_const) : 0;
   __shared__ GcItem G[kGW];
+  __shared__ uint16_t s_la[kGW * kEV];   // occupied slots, then the failed-gradient ones (gc_entry)
+  __shared__ uint16_t s_lv[kGW * kEV];   // surviving slots
+  __shared__ int s_nocc, s_nv, s_nfb;
   __shared__ int red[4 * kGW];
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   GcItem &I = G[w];
@@ -1482,7 +1483,7 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
       const ResolveRegs rr = resolve_load(S, Fr, bi, i, 0);
       resolve_store(S, Fr, rr, bi, i, n, 0, I.R);
     }
-    if (lane == 0) { I.nv = 0; I.nfb = 0; }
+    if (t == 0) { s_nocc = 0; s_nv = 0; s_nfb = 0; }
     __syncwarp();
     const bool live = I.R.mode > 0;
     const int b = I.R.b;
@@ -1518,80 +1519,80 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
       cp_async_wait_all();
       __syncwarp();
       trace_item(S, TK_GC, nth, 2);
-      // requests: lane owns words lane, lane + 32; a requested empty slot is
-      // allocated (birth = frame, normal 0); every occupied slot is listed
-      __shared__ int s_nocc[kGW];
-      if (lane == 0) s_nocc[w] = 0;
-      __syncwarp();
-#pragma unroll
-      for (int r = 0; r < (kEV / 32 + 31) / 32; r++) {
-        const int wi = lane + r * 32;
-        uint32_t word = 0;
-        if (wi < kEV / 32) {
-          const uint32_t claim = I.cl[wi], fresh = claim & ~I.occ[wi];
-          for (uint32_t m = fresh; m; m &= m - 1) {
-            const size_t q = (size_t)b * kEV + wi * 32 + __ffs(m) - 1;
-            S.vbirth[q] = F.frame;
-            S.vnrm[3 * q] = 0.0; S.vnrm[3 * q + 1] = 0.0; S.vnrm[3 * q + 2] = 0.0;
-          }
-          allocs += I.R.owned * __popc(fresh);   // counted by the slot's owning rank
-          if (claim) S.vclaim[(size_t)b * (kEV / 32) + wi] = 0u;
-          word = I.occ[wi] | claim;
-          I.occ[wi] = word;
-        }
-        int pos = smem_append(__popc(word), &s_nocc[w]);
-        for (uint32_t m = word; m; m &= m - 1) I.fb[pos++] = (uint16_t)(wi * 32 + __ffs(m) - 1);
-      }
-      __syncwarp();
-      // GC over the occupied list, balanced across the lanes: a slot survives
-      // iff a cube around its edge still has the edge in its mask (the 4 cubes
-      // at -du along u, -dw along w; u, w = the two axes other than the slot's)
-      const int nocc = s_nocc[w];
-      for (int p0 = 0; p0 < nocc; p0 += 32) {
-        const int p = p0 + lane;
-        bool keep = false;
-        int sl = 0;
-        if (p < nocc) {
-          sl = I.fb[p];
-          keep = true;
-          if (mode & G_GC) {
-            const int c = sl / 3, axis = sl - 3 * c;
-            // (no short-circuit: the 4 type and mask lookups issue together)
-            unsigned ty[4], ref = 0;
-#pragma unroll
-            for (int q = 0; q < 4; q++) {
-              int l0, l1, l2;
-              slot_cube(c, axis, q, l0, l1, l2);
-              ty[q] = I.tt[tt_idx(l0, l1, l2)];
-            }
-#pragma unroll
-            for (int q = 0; q < 4; q++) ref |= edge_mask_of(ty[q]) >> cube_edge_of_slot(axis, q >> 1, q & 1);
-            if (!(ref & 1u)) {
-              keep = false;
-              S.vbirth[(size_t)b * kEV + sl] = -1;
-              atomicAnd(&I.occ[sl >> 5], ~(1u << (sl & 31)));
-              frees += I.R.owned;
-            }
-          }
-        }
-        if (normals) {
-          const int pos = smem_append(keep ? 1 : 0, &I.nv);
-          if (keep) I.vlist[pos] = (uint16_t)sl;
-        }
-      }
-      __syncwarp();
-      for (int q = lane; q < kEV / 32; q += 32) S.vocc[(size_t)b * (kEV / 32) + q] = I.occ[q];   // requests + frees
     }
-    __syncthreads();   // every warp's vertex list is complete
+    __syncthreads();   // every block staged
+    // requests, over the kGW blocks' bitmap words: a requested empty slot is
+    // allocated (birth = frame, normal 0); every occupied slot is listed
+#pragma unroll
+    for (int r = 0; r < (kGW * (kEV / 32) + kGT - 1) / kGT; r++) {
+      const int wi = t + r * kGT;
+      const int k = wi / (kEV / 32), wd = wi - k * (kEV / 32);
+      uint32_t word = 0;
+      if (wi < kGW * (kEV / 32) && G[k].R.mode > 0) {
+        GcItem &J = G[k];
+        const size_t bk = (size_t)J.R.b;
+        const uint32_t claim = J.cl[wd], fresh = claim & ~J.occ[wd];
+        for (uint32_t m = fresh; m; m &= m - 1) {
+          const size_t q = bk * kEV + wd * 32 + __ffs(m) - 1;
+          S.vbirth[q] = F.frame;
+          S.vnrm[3 * q] = 0.0; S.vnrm[3 * q + 1] = 0.0; S.vnrm[3 * q + 2] = 0.0;
+        }
+        allocs += J.R.owned * __popc(fresh);   // counted by the slot's owning rank
+        if (claim) S.vclaim[bk * (kEV / 32) + wd] = 0u;
+        word = J.occ[wd] | claim;
+        J.occ[wd] = word;
+      }
+      int pos = smem_append(__popc(word), &s_nocc);
+      for (uint32_t m = word; m; m &= m - 1) s_la[pos++] = gc_entry(k, wd * 32 + __ffs(m) - 1);
+    }
+    __syncthreads();
+    // GC over the occupied list: a slot survives iff a cube around its edge
+    // still has the edge in its mask (the 4 cubes at -du along u, -dw along w;
+    // u, w = the two axes other than the slot's)
+    const int nocc = s_nocc;
+    for (int p0 = 0; p0 < nocc; p0 += kGT) {
+      const int p = p0 + t;
+      bool keep = false;
+      uint16_t e = 0;
+      if (p < nocc) {
+        e = s_la[p];
+        keep = true;
+        if (mode & G_GC) {
+          GcItem &J = G[e >> 11];
+          const int sl = e & 2047, c = sl / 3, axis = sl - 3 * c;
+          // (no short-circuit: the 4 type and mask lookups issue together)
+          unsigned ty[4], ref = 0;
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            int l0, l1, l2;
+            slot_cube(c, axis, q, l0, l1, l2);
+            ty[q] = J.tt[tt_idx(l0, l1, l2)];
+          }
+#pragma unroll
+          for (int q = 0; q < 4; q++) ref |= edge_mask_of(ty[q]) >> cube_edge_of_slot(axis, q >> 1, q & 1);
+          if (!(ref & 1u)) {
+            keep = false;
+            S.vbirth[(size_t)J.R.b * kEV + sl] = -1;
+            atomicAnd(&J.occ[sl >> 5], ~(1u << (sl & 31)));
+            frees += J.R.owned;
+          }
+        }
+      }
+      if (normals) {
+        const int pos = smem_append(keep ? 1 : 0, &s_nv);
+        if (keep) s_lv[pos] = e;
+      }
+    }
+    __syncthreads();
+    for (int wi = t; wi < kGW * (kEV / 32); wi += kGT) {   // occupancy after requests + frees
+      const int k = wi / (kEV / 32), wd = wi - k * (kEV / 32);
+      if (G[k].R.mode > 0) S.vocc[(size_t)G[k].R.b * (kEV / 32) + wd] = G[k].occ[wd];
+    }
     trace_sub(S, TK_GC, nth, 0);
     if (normals) {
-      // the kGW blocks' vertices, whole CTA, two per thread per pass (their
-      // 24 tsdf loads in flight together)
-      int pre[kGW + 1];
-      pre[0] = 0;
-#pragma unroll
-      for (int k = 0; k < kGW; k++) pre[k + 1] = pre[k] + (G[k].R.mode > 0 ? G[k].nv : 0);
-      const int nv = pre[kGW];
+      // the surviving vertices, whole CTA, two per thread per pass (their 24
+      // tsdf loads in flight together)
+      const int nv = s_nv;
       for (int p0 = 0; p0 < nv; p0 += 2 * kGT) {
         double v[2][12];
         int slv[2], itv[2];
@@ -1599,11 +1600,10 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
 #pragma unroll
         for (int u = 0; u < 2; u++) {
           const int p = p0 + u * kGT + t;
-          int k = 0;
-#pragma unroll
-          for (int q = 1; q < kGW; q++) k += p >= pre[q];
+          const uint16_t e = p < nv ? s_lv[p] : (uint16_t)0;
+          const int k = e >> 11;
           itv[u] = k;
-          slv[u] = p < nv ? G[k].vlist[p - pre[k]] : -1;
+          slv[u] = p < nv ? (e & 2047) : -1;
           const GcItem &J = G[k];
           const int bj = J.R.b;
           const int sl = slv[u] < 0 ? 0 : slv[u];
@@ -1634,7 +1634,7 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
 #pragma unroll
         for (int u = 0; u < 2; u++) {
           if (slv[u] < 0) continue;
-          GcItem &J = G[itv[u]];
+          const GcItem &J = G[itv[u]];
           const int sl = slv[u];
           const int axis = sl - 3 * (sl / 3);
           computed += J.R.owned;
@@ -1655,33 +1655,33 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
             dst[0] = g[0] / nrm; dst[1] = g[1] / nrm; dst[2] = g[2] / nrm;
           } else {
             fallbacks += J.R.owned;
-            J.fb[atomicAdd(&J.nfb, 1)] = (uint16_t)sl;
+            s_la[atomicAdd(&s_nfb, 1)] = gc_entry(itv[u], sl);   // (the occupied list is spent)
           }
         }
       }
       __syncthreads();
       trace_sub(S, TK_GC, nth, 1);
-      // face-normal fallback records: each warp its own block's failed slots,
-      // with their 4 cube types and candidate mask (staged tile, row, halo flags)
-      if (live) {
-        const int nfb = I.nfb;
-        for (int p = lane; p < nfb; p += 32) {
-          const int sl = I.fb[p];
-          const int ci = sl / 3, axis = sl - 3 * ci;
-          uint32_t types4 = 0, cand = 0;
+      // face-normal fallback records: the failed slots with their 4 cube types
+      // and candidate mask (staged tile, row, halo flags)
+      const int nfb = s_nfb;
+      for (int p = t; p < nfb; p += kGT) {
+        const uint16_t e = s_la[p];
+        const GcItem &J = G[e >> 11];
+        const int sl = e & 2047;
+        const int ci = sl / 3, axis = sl - 3 * ci;
+        uint32_t types4 = 0, cand = 0;
 #pragma unroll
-          for (int q = 0; q < 4; q++) {
-            int l0, l1, l2;
-            slot_cube(ci, axis, q, l0, l1, l2);
-            const uint32_t ty = I.tt[tt_idx(l0, l1, l2)];
-            const int dir = nbr_dir(l0 < 0 ? -1 : 0, l1 < 0 ? -1 : 0, l2 < 0 ? -1 : 0);
-            types4 |= ty << (8 * q);
-            if (((edge_mask_of(ty) >> cube_edge_of_slot(axis, q >> 1, q & 1)) & 1) && I.R.nbr[dir] >= 0 &&
-                I.inhalo[dir])
-              cand |= 1u << q;
-          }
-          S.fallback[atomicAdd(&ctr->fb_pending, 1)] = make_int4(b, sl, (int)types4, (int)cand);
+        for (int q = 0; q < 4; q++) {
+          int l0, l1, l2;
+          slot_cube(ci, axis, q, l0, l1, l2);
+          const uint32_t ty = J.tt[tt_idx(l0, l1, l2)];
+          const int dir = nbr_dir(l0 < 0 ? -1 : 0, l1 < 0 ? -1 : 0, l2 < 0 ? -1 : 0);
+          types4 |= ty << (8 * q);
+          if (((edge_mask_of(ty) >> cube_edge_of_slot(axis, q >> 1, q & 1)) & 1) && J.R.nbr[dir] >= 0 &&
+              J.inhalo[dir])
+            cand |= 1u << q;
         }
+        S.fallback[atomicAdd(&ctr->fb_pending, 1)] = make_int4(J.R.b, sl, (int)types4, (int)cand);
       }
     }
     trace_item(S, TK_GC, nth, 3);
