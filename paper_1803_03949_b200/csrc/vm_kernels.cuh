@@ -1521,6 +1521,7 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
       trace_item(S, TK_GC, nth, 2);
     }
     __syncthreads();   // every block staged
+    trace_sub(S, TK_GC, nth, 2);
     // requests, over the kGW blocks' bitmap words: a requested empty slot is
     // allocated (birth = frame, normal 0); every occupied slot is listed
 #pragma unroll
@@ -1532,20 +1533,25 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
         GcItem &J = G[k];
         const size_t bk = (size_t)J.R.b;
         const uint32_t claim = J.cl[wd], fresh = claim & ~J.occ[wd];
+        // (a new vertex's zero normal is written here only without the normals
+        // pass, which writes every surviving vertex's normal -- zero first
+        // where its stencil fails, for the fallback's "never set" test)
         for (uint32_t m = fresh; m; m &= m - 1) {
           const size_t q = bk * kEV + wd * 32 + __ffs(m) - 1;
           S.vbirth[q] = F.frame;
-          S.vnrm[3 * q] = 0.0; S.vnrm[3 * q + 1] = 0.0; S.vnrm[3 * q + 2] = 0.0;
+          if (!normals) { S.vnrm[3 * q] = 0.0; S.vnrm[3 * q + 1] = 0.0; S.vnrm[3 * q + 2] = 0.0; }
         }
         allocs += J.R.owned * __popc(fresh);   // counted by the slot's owning rank
         if (claim) S.vclaim[bk * (kEV / 32) + wd] = 0u;
         word = J.occ[wd] | claim;
         J.occ[wd] = word;
+        J.cl[wd] = fresh;   // (the allocations of this call, for the normals pass)
       }
       int pos = smem_append(__popc(word), &s_nocc);
       for (uint32_t m = word; m; m &= m - 1) s_la[pos++] = gc_entry(k, wd * 32 + __ffs(m) - 1);
     }
     __syncthreads();
+    trace_sub(S, TK_GC, nth, 3);
     // GC over the occupied list: a slot survives iff a cube around its edge
     // still has the edge in its mask (the 4 cubes at -du along u, -dw along w;
     // u, w = the two axes other than the slot's)
@@ -1654,6 +1660,10 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
             double *dst = S.vnrm + 3 * ((size_t)J.R.b * kEV + sl);
             dst[0] = g[0] / nrm; dst[1] = g[1] / nrm; dst[2] = g[2] / nrm;
           } else {
+            if ((J.cl[sl >> 5] >> (sl & 31)) & 1u) {   // allocated now: its normal starts at zero
+              double *dst = S.vnrm + 3 * ((size_t)J.R.b * kEV + sl);
+              dst[0] = 0.0; dst[1] = 0.0; dst[2] = 0.0;
+            }
             fallbacks += J.R.owned;
             s_la[atomicAdd(&s_nfb, 1)] = gc_entry(itv[u], sl);   // (the occupied list is spent)
           }

@@ -73,8 +73,7 @@ for k, name in enumerate(NAMES):
                     parts.append(f"{(ts[p] - prev) / 1e3:.2f}")
                     prev = ts[p]
             segs.append(f"[{(ts[0] - t0) / 1e3:.2f}: {'/'.join(parts)}]")
-        extra = " ".join(f"s{p}={(row[p] - t0) / 1e3:.2f}" for p in (22, 23, 28, 29, 30) if row[p] > 0)
-        extra += f" nv={row[25]} nfb={row[26]} sm={row[24]}" if name == "gc_normals" else ""
+        extra = " ".join(f"s{p}={(row[p] - t0) / 1e3:.2f}" for p in (22, 23, 24, 25, 26, 28, 29, 30) if row[p] > 0)
         print(f"  slow CTA end {(row[31] - t0) / 1e3:.2f} items {row[27]} {' '.join(segs)} {extra}")
 
 # per-SM view of gc: items and the latest item end on each SM
