@@ -1318,6 +1318,7 @@ __device__ __forceinline__ size_t sample_index(const int *s_nbr, int lx, int ly,
 // operation between their kernels.
 __device__ __forceinline__ void gc_commit(const DevState &S, const FrameDev &F, int mode) {
   __shared__ int s_last;
+  __shared__ __align__(16) Counters s_c;   // the last CTA's copy of the counter block
   Counters *ctr = S.ctr;
   if (threadIdx.x == 0) {
     int last = 0;
@@ -1330,60 +1331,63 @@ __device__ __forceinline__ void gc_commit(const DevState &S, const FrameDev &F, 
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  const int2 h = __ldcg(reinterpret_cast<const int2 *>(&ctr->error));
-  const bool halted = (h.x | h.y) != 0;
+  // one round trip: the whole block, a word per thread (every other CTA has
+  // arrived, so nothing changes it meanwhile)
+  constexpr int kWords = (int)(sizeof(Counters) / 4);
+  {
+    const volatile uint32_t *src = reinterpret_cast<const volatile uint32_t *>(ctr);
+    uint32_t *sw = reinterpret_cast<uint32_t *>(&s_c);
+    for (int q = threadIdx.x; q < kWords; q += blockDim.x) sw[q] = src[q];
+  }
+  __syncthreads();
+  const bool halted = (s_c.error | s_c.need) != 0;
   if (threadIdx.x == 0) {
-    if (!halted) {
-      const long long allocs_all = ld_vol(&ctr->v_allocs), fr = ld_vol(&ctr->v_frees);
-      const long long peak = ctr->v_live + allocs_all;     // all allocations precede all frees
-      if (S.max_vertices > 0 && peak > S.max_vertices)
+    Counters &c = s_c;
+    if (!halted) {   // the fold, mirrored into the global block (persistent fields only)
+      const long long allocs_all = c.v_allocs, fr = c.v_frees;
+      const long long peak = c.v_live + allocs_all;     // all allocations precede all frees
+      if (S.max_vertices > 0 && peak > S.max_vertices) {
         set_error(S, ERR_CAPACITY, peak, S.max_vertices, 3);
-      if (peak > ctr->v_count) ctr->v_count = peak;
-      ctr->v_live = peak - fr;
-      ctr->v_recycled += fr;
-      ctr->v_events += allocs_all;
-      const long long rel = ld_vol(&ctr->t_released), nw = ld_vol(&ctr->t_allocated);
-      ctr->t_live += nw - rel;
-      ctr->t_recycled += rel;
-      if (ctr->t_live > ctr->t_count) ctr->t_count = ctr->t_live;
-      ctr->irregular += ld_vol(&ctr->irr_delta);
+        if (c.error == 0) {
+          c.error = ERR_CAPACITY;
+          c.err_info[0] = peak; c.err_info[1] = S.max_vertices; c.err_info[2] = 3; c.err_info[3] = 0;
+        }
+      }
+      if (peak > c.v_count) c.v_count = peak;
+      c.v_live = peak - fr;
+      c.v_recycled += fr;
+      c.v_events += allocs_all;
+      c.t_live += c.t_allocated - c.t_released;
+      c.t_recycled += c.t_released;
+      if (c.t_live > c.t_count) c.t_count = c.t_live;
+      c.irregular += c.irr_delta;
+      ctr->v_count = c.v_count; ctr->v_live = c.v_live; ctr->v_recycled = c.v_recycled;
+      ctr->v_events = c.v_events; ctr->t_live = c.t_live; ctr->t_recycled = c.t_recycled;
+      ctr->t_count = c.t_count; ctr->irregular = c.irregular;
     }
+    c.done_gc = 0;
     ctr->done_gc = 0;
-    ctr->t_end_ns = gtimer();
-    __threadfence();
+    c.t_end_ns = gtimer();
   }
   if (!F.snap) return;
   __syncthreads();
-  constexpr int kWords = (int)(sizeof(Counters) / 4);
-  const volatile uint32_t *src = reinterpret_cast<const volatile uint32_t *>(ctr);
-  uint32_t *dst = reinterpret_cast<uint32_t *>(F.snap);
-  uint32_t keep[(kWords + 127) / 128];
-#pragma unroll
-  for (int r = 0; r < (kWords + 127) / 128; r++) {
-    const int q = threadIdx.x + 128 * r;
-    keep[r] = q < kWords ? src[q] : 0u;
-  }
-  __syncthreads();   // (every word read before any is cleared)
-#pragma unroll
-  for (int r = 0; r < (kWords + 127) / 128; r++) {
-    const int q = threadIdx.x + 128 * r;
-    if (q < kWords) {
-      dst[q] = keep[r];
+  {
+    const uint32_t *sw = reinterpret_cast<const uint32_t *>(&s_c);
+    uint32_t *dst = reinterpret_cast<uint32_t *>(F.snap);
+    for (int q = threadIdx.x; q < kWords; q += blockDim.x) {
+      dst[q] = sw[q];
       if (F.reset_after && !halted && q >= (int)(offsetof(Counters, nvalid) / 4))
         reinterpret_cast<uint32_t *>(ctr)[q] = 0u;
     }
   }
-  if (F.self_dst) {   // publish to the host now (the next frame's k_collect waits on a copy)
-    __syncthreads();   // (F.snap complete)
-    if (threadIdx.x < 32) {   // one warp, 16-byte stores, then one system fence before the flag
-      const uint4 *sv = reinterpret_cast<const uint4 *>(F.snap);
-      uint4 *hd = reinterpret_cast<uint4 *>(F.self_dst);
-      for (int q = threadIdx.x; q < (int)(sizeof(Counters) / 16); q += 32) hd[q] = sv[q];
-      __syncwarp();
-      if (threadIdx.x == 0) {
-        __threadfence_system();
-        *reinterpret_cast<volatile unsigned long long *>(F.self_seq) = F.self_id;
-      }
+  if (F.self_dst && threadIdx.x < 32) {   // publish to the host now (the next frame's k_collect waits on a copy)
+    const uint4 *sv = reinterpret_cast<const uint4 *>(&s_c);
+    uint4 *hd = reinterpret_cast<uint4 *>(F.self_dst);
+    for (int q = threadIdx.x; q < (int)(sizeof(Counters) / 16); q += 32) hd[q] = sv[q];
+    __syncwarp();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      *reinterpret_cast<volatile unsigned long long *>(F.self_seq) = F.self_id;
     }
   }
 }
