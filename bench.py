@@ -14,8 +14,11 @@ Arms
   dominant kernel's algorithmic bytes / its mean event-timed duration against
   MEASURED_PEAKS.json hbm_gbs.  ``cpu_baseline`` = the CPU oracle port
   (oracle/, serial C restatement of the reference) on a bounded prefix.
-* --impl reference: the reference CPU algorithm (the oracle port; the
-  reference itself is pure Python and cannot travel) on the same frames.
+* --impl reference: the reference CPU algorithm (the oracle port, 1 core) on
+  the same frames, and next to it the reference itself (pure-Python voxmesh
+  from baseline/_ref) at serial/1 and claim/os.cpu_count() for a bounded
+  prefix.  ``parity`` (default arm): a fresh B200 engine over the oracle
+  leg's frames, diffed against the oracle's rows and final state.
 Multi-GPU (torchrun, NCCL): default ``--mode partition`` -- one reconstruction
 spatially partitioned across the ranks (hashed tiles of --tile-blocks^3
 blocks), every rank fed the same frame; strong scaling,
@@ -145,7 +148,7 @@ def make_frames(spec, nframes, device):
     return poses, depths
 
 
-def oracle_run(spec, cfg, depths_host, poses, budget_s, warmup=0):
+def oracle_run(spec, cfg, depths_host, poses, budget_s, warmup=0, return_engine=False):
     """Time the CPU oracle (serial C port of the reference) frame by frame."""
     from oracle.oracle import OracleEngine
     intr = spec.intrinsics()
@@ -160,7 +163,64 @@ def oracle_run(spec, cfg, depths_host, poses, budget_s, warmup=0):
         n += 1
         if t_total > budget_s:
             break
-    return n, t_total
+    return (n, t_total, eng) if return_engine else (n, t_total)
+
+
+REF_PKG = ROOT / "baseline" / "_ref"
+
+
+def python_reference_run(spec, cfg, depths_host, poses, strategy, workers, budget_s):
+    """The reference itself (pure-Python ``voxmesh``, installed unmodified into
+    baseline/_ref by `pip install --target`), timed with its own StatsRow
+    fusion_ms + meshing_ms (engine.py:123-165) over frames 0.. until the budget
+    is spent.  Returns None when the install is absent."""
+    if not (REF_PKG / "voxmesh").is_dir():
+        return None
+    if str(REF_PKG) not in sys.path:
+        sys.path.insert(0, str(REF_PKG))
+    import voxmesh
+    intr = spec.intrinsics()
+    rc = voxmesh.RunConfig(strategy=strategy, workers=workers, **cfg)
+    eng = voxmesh.Engine(rc, voxmesh.Intrinsics(intr.fx, intr.fy, intr.cx, intr.cy, intr.width, intr.height))
+    ms, n = 0.0, 0
+    for i in range(len(depths_host)):
+        row = eng.fuse_frame(depths_host[i], voxmesh.Pose(poses[i].rotation, poses[i].translation))
+        ms += row.fusion_ms + row.meshing_ms
+        n += 1
+        if ms / 1e3 > budget_s:
+            break
+    cores = eng.config.workers if strategy != "serial" else 1
+    return {"value": n / (ms / 1e3), "unit": "frames/s", "cores": int(cores), "strategy": strategy,
+            "workers": int(eng.config.workers), "kind": "reference (pure-Python voxmesh, baseline/_ref)",
+            "sample": f"{n} frames (0..{n - 1}), engine's own fusion_ms + meshing_ms = {ms / 1e3:.1f} s"}
+
+
+def python_reference_legs(spec, cfg, depths_host, poses, budget_s):
+    """serial/1 (fastest, one core busy) and the default claim/os.cpu_count()
+    (SURVEY.md 8d timing)."""
+    out = []
+    for strategy, workers in (("serial", 1), ("claim", 0)):
+        r = python_reference_run(spec, cfg, depths_host, poses, strategy, workers, budget_s)
+        if r is None:
+            return [{"unavailable": "baseline/_ref/voxmesh not installed"}]
+        out.append(r)
+    return out
+
+
+def parity_vs_oracle(spec, cfg, depths_dev, poses, ora, n, strategy):
+    """A fresh B200 engine over the oracle leg's frames 0..n-1 (device depth),
+    diffed against the oracle's rows and final state (oracle/parity.py)."""
+    from oracle.parity import compare_rows, compare_state
+    from paper_1803_03949_b200 import Engine, RunConfig
+    eng = Engine(RunConfig(strategy=strategy, **cfg), spec.intrinsics())
+    for i in range(n):
+        eng.fuse_frame(depths_dev[i], poses[i])
+    rows = compare_rows(eng.stats, ora.stats)
+    st = compare_state(eng, ora)
+    return {"frames": n, "match": bool(rows["match"] and st["match"]), "rows": rows,
+            "state": {k: v for k, v in st.items() if k != "match"},
+            "checked": "StatsRow every frame; final block set, tsdf, weight, type_prev, type_curr, "
+                       "compact positions / indices / ages bit-exact, normals <= 1e-12"}
 
 
 # ---------------------------------------------------------------- arms
@@ -176,12 +236,15 @@ def run_reference(args, spec, cfg, rank, world):
     v = n / t if t > 0 else 0.0
     sample = (f"{args.config} frames {args.warmup}..{args.warmup + n - 1} after {args.warmup} "
               f"untimed warm-up frames (time cap {args.ref_budget:.0f} s)")
+    pyref = python_reference_legs(spec, cfg, host, poses, args.pyref_budget)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "frames/s", "n_gpus": world,
             "steps": n, "warmup": args.warmup, "ms_per_step": 1e3 * t / max(n, 1),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (sphere-traced analytic scene)", "config": workload(args, spec, cfg),
             "cpu_baseline": {"value": v, "unit": "frames/s", "cores": 1, "kind": "port",
                              "sample": sample},
+            # the reference itself (pure Python) next to its C port, same frames from 0
+            "python_reference": pyref,
             "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -355,12 +418,18 @@ def run_gpu(args, spec, cfg, rank, world, local_rank):
     if rank != 0:
         return
     cpu = None
+    parity = None
     if not args.no_cpu_baseline:
         hn = [d.cpu().numpy() for d in depths]
-        n, t = oracle_run(spec, cfg, hn, poses, budget_s=args.cpu_budget)
+        n, t, ora = oracle_run(spec, cfg, hn, poses, budget_s=args.cpu_budget, return_engine=True)
         cpu = {"value": n / t, "unit": "frames/s", "cores": 1, "kind": "port",
                "sample": f"{args.config} frames 0..{n - 1} through the CPU oracle (serial C "
                          f"restatement of the reference, oracle/), {t:.1f} s"}
+        # the published numbers' parity: the GPU engine on the same frames vs the oracle
+        parity = parity_vs_oracle(spec, cfg, depths, poses, ora, n, args.strategy)
+        del ora
+        if args.pyref_budget > 0:
+            cpu["python_reference"] = python_reference_legs(spec, cfg, hn, poses, args.pyref_budget)
     clk = clocks.summary()
     line = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
@@ -377,6 +446,7 @@ def run_gpu(args, spec, cfg, rank, world, local_rank):
         "phase_ms_mean": {n: tot[n] / args.steps for n in names},
         "profiled_pass_ms_per_step": sum(prof_frame_ms) / args.steps,
         "cpu_baseline": cpu,
+        "parity": parity,
         "e2e": {"value": (1 if part else world) * args.steps / e2e_s, "unit": "frames/s",
                 "h2d_bytes_per_step": spec.width * spec.height * 8 + 256,
                 "d2h_bytes_per_step": 512},
@@ -403,6 +473,8 @@ def main():
     ap.add_argument("--backend", default="nccl", help="gloo only to test N>1 on a single GPU")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--ref-budget", type=float, default=150.0)
+    ap.add_argument("--pyref-budget", type=float, default=12.0,
+                    help="seconds of the pure-Python reference per strategy (0 = skip)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

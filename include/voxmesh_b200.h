@@ -161,6 +161,10 @@ int vm_create(const vm_store_config *cfg, vm_engine **out);
 int vm_destroy(vm_engine *e);
 /* Run on a caller-owned cudaStream_t (NULL = the engine's own stream). */
 int vm_set_stream(vm_engine *e, void *cuda_stream);
+/* The cudaStream_t the engine's kernels run on (device inputs produced on
+ * another stream must be ordered before it: the binding records an event on
+ * the producer stream and makes this one wait, engine.py). */
+int vm_get_stream(vm_engine *e, void **cuda_stream);
 /* Record CUDA events between the frame's kernels (per-phase device times). */
 int vm_set_profiling(vm_engine *e, int on);
 /* Per-kernel device times (ms) of the last frame: depth_stats, collect,

@@ -15,7 +15,7 @@ DEPS = [SRC, PKG / "csrc" / "vm_kernels.cuh", PKG / "csrc" / "vm_device.cuh",
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3",
               "--fmad=false",          # no implicit FMA contraction (numeric parity)
-              "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-cudart", "static"]
+              "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-cudart", "static", "-ldl"]
 
 
 def nvcc() -> str:

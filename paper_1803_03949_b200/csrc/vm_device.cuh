@@ -32,7 +32,6 @@ constexpr int kEV = kNC * 3;   // edge-vertex slots per block
 constexpr long long kEmptyKey = -1LL;
 
 enum { ERR_NONE = 0, ERR_CAPACITY = 1, ERR_CONSISTENCY = 2 };
-enum { NEED_BLOCKS = 1 };
 
 // Device counters.  Persistent fields first; everything from `nvalid` on is
 // reset at the start of every call (one memset).
@@ -48,7 +47,7 @@ struct alignas(16) Counters {
   int32_t nblocks;       // SpatialStore.block_count
   int32_t ovf_count;
   int32_t error;
-  int32_t need;
+  int32_t need;          // heap exhausted: the epoch of the call whose allocation ran past block_cap (0 = no)
   int64_t v_live;        // VertexPool.live_count
   int64_t v_count;       // VertexPool.count (arena high-water)
   int64_t v_recycled;
@@ -86,6 +85,8 @@ struct alignas(16) Counters {
   int32_t nhalo_sh[kHaloShards];   // halo shard fill counts (may exceed halo_sh_cap: clamp)
   unsigned long long t_start_ns;   // %globaltimer: k_collect start, k_gc_normals commit
   unsigned long long t_end_ns;
+  unsigned long long t_mesh_ns;    // k_retype_place start (after integration): fusion | meshing split
+  unsigned long long pad1;
 };
 static_assert(sizeof(Counters) % 16 == 0, "snapshots are copied in 16-byte words");
 
@@ -382,10 +383,12 @@ __device__ __forceinline__ bool block_relevant(const DevState &S, int x, int y, 
 __device__ int alloc_block(const DevState &S, int x, int y, int z, int epoch) {
   int idx = atomicAdd(&S.ctr->nblocks, 1);
   if (2LL * idx >= S.table_size) {
-    set_error(S, ERR_CAPACITY, idx, S.table_size, 1);
+    set_error(S, ERR_CAPACITY, idx, S.table_size, 1, epoch);
     return -2;
   }
-  if (idx >= S.block_cap) atomicOr(&S.ctr->need, NEED_BLOCKS);
+  // (latched with the call's epoch: a k_collect CTA stops only for a flag left
+  // by an EARLIER frame, never for one a sibling CTA of its own frame just set)
+  if (idx >= S.block_cap) atomicExch(&S.ctr->need, epoch);
   S.bcoord[idx] = make_int4(x, y, z, 0);
   S.stamp_new[idx] = epoch;
   if (S.nranks > 1) {   // (single rank: every block is owned, nblocks_owned == nblocks)
@@ -436,7 +439,7 @@ __device__ HashRef hash_insert_ref(const DevState &S, int x, int y, int z, int e
       if (found == -1) {
         int e = atomicAdd(&S.ctr->ovf_count, 1);
         if (e >= S.ovf_cap) {
-          set_error(S, ERR_CAPACITY, e, S.ovf_cap, 2);
+          set_error(S, ERR_CAPACITY, e, S.ovf_cap, 2, epoch);
           found = -2;
         } else {
           found = alloc_block(S, x, y, z, epoch);

@@ -20,10 +20,20 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/voxmesh_b200.h"
 #include "vm_kernels.cuh"
 
 using namespace vm;
+
+// NVTX ranges around the host-side phases (frame enqueue, settle wait,
+// compaction, halo exchange) so an nsys / ncu timeline names them; free when
+// no tool is attached (header-only NVTX v3).
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 static thread_local std::string g_err;
 
@@ -244,7 +254,23 @@ static int read_counters(vm_engine *e) {
   return VM_OK;
 }
 
+static int recover_after_error(vm_engine *e);
+static int error_message(vm_engine *e);
+
+// Report the device error flag of the call just read back (h_ctr) and clear
+// it, so the store stays usable after the error as the reference's does
+// (compact / audit / snapshots of the partially updated store, later frames).
 static int error_from_counters(vm_engine *e) {
+  const int rc = error_message(e);
+  if (rc != VM_OK) {
+    const std::string msg = g_err;
+    recover_after_error(e);   // (best effort: the call's own error is what is reported)
+    g_err = msg;
+  }
+  return rc;
+}
+
+static int error_message(vm_engine *e) {
   const Counters &c = *e->h_ctr;
   if (c.error == ERR_CAPACITY) {
     if (c.err_info[2] == 1)
@@ -264,6 +290,30 @@ static int error_from_counters(vm_engine *e) {
       default: return set_err(VM_ERR_CONSISTENCY, "consistency error %lld", (long long)c.err_info[0]);
     }
   }
+  return VM_OK;
+}
+
+// After a reported error: clamp the block / overflow counts the failed
+// allocations ran past, give every allocated block its storage, initialise
+// (and link) the blocks a failed k_collect allocated -- its k_fuse_blocks never
+// ran, so they are empty blocks as the reference leaves them after
+// get_or_allocate_block raised (store.py:296-320) -- and clear the flags.
+static int recover_after_error(vm_engine *e) {
+  Counters &c = *e->h_ctr;
+  const bool collect_time = c.error == ERR_CAPACITY && (c.err_info[2] == 1 || c.err_info[2] == 2);
+  const int32_t epoch = (int32_t)c.err_info[3];
+  c.nblocks = std::min<int32_t>(c.nblocks, e->S.max_blocks);
+  c.ovf_count = std::min<int32_t>(c.ovf_count, e->S.ovf_cap);
+  if (c.nblocks > e->S.block_cap) TRY(grow_blocks(e, c.nblocks));
+  c.error = 0;
+  c.need = 0;
+  for (auto &v : c.err_info) v = 0;
+  const size_t persist = offsetof(Counters, nvalid);
+  TRY(copy_sync(e, e->S.ctr, e->h_ctr, persist, cudaMemcpyHostToDevice));
+  if (collect_time && epoch > 0)
+    k_init_blocks<<<grid_blocks(e), kThreadsCube, 0, e->stream>>>(e->S, epoch);
+  TRY(check_launch());
+  CK(cudaStreamSynchronize(e->stream));
   return VM_OK;
 }
 
@@ -299,7 +349,7 @@ static int complete_with_resume(vm_engine *e, int *resumes) {
   for (int guard = 0; guard < 64; guard++) {
     TRY(read_counters(e));
     TRY(error_from_counters(e));
-    if (!(e->h_ctr->need & NEED_BLOCKS)) return VM_OK;
+    if (!e->h_ctr->need) return VM_OK;
     TRY(grow_blocks(e, e->h_ctr->nblocks));
     CK(cudaMemsetAsync(&e->S.ctr->need, 0, sizeof(int32_t), e->stream));
     if (resumes) (*resumes)++;
@@ -370,7 +420,7 @@ static int map_coords(vm_engine *e, const int32_t *coords, int64_t n, int32_t **
 static int init_new_blocks(vm_engine *e) {
   TRY(read_counters(e));
   TRY(error_from_counters(e));
-  if (e->h_ctr->need & NEED_BLOCKS) {
+  if (e->h_ctr->need) {
     TRY(grow_blocks(e, e->h_ctr->nblocks));
     CK(cudaMemsetAsync(&e->S.ctr->need, 0, sizeof(int32_t), e->stream));
   }
@@ -390,6 +440,7 @@ static void free_compacted(Compacted &c) {
 // store.py:388-425 on the device; with_handles also materialises the
 // per-slot / per-triangle-slot dense handles of the snapshot views
 static int run_compaction(vm_engine *e, int64_t frame, bool with_handles) {
+  NvtxRange nvtx_("vm_compaction");
   TRY(read_counters(e));
   const int nb = e->h_ctr->nblocks;
   cudaStream_t st = e->stream;
@@ -608,6 +659,12 @@ int vm_set_stream(vm_engine *e, void *stream) {
   return VM_OK;
 }
 
+int vm_get_stream(vm_engine *e, void **stream) {
+  if (!e || !stream) return set_err(VM_ERR_INPUT, "null argument");
+  *stream = (void *)e->stream;
+  return VM_OK;
+}
+
 int vm_set_trace(vm_engine *e, void *device_buffer) {
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
   e->S.trace = (unsigned long long *)device_buffer;
@@ -683,8 +740,13 @@ static void fill_stats(vm_engine *e, int64_t frame, vm_stats *out) {
   if (e->profiling) {   // segment split needs the per-kernel events
     if (cudaEventElapsedTime(&ms, e->ev[PH_DEPTH], e->ev[PH_RETYPE]) == cudaSuccess) out->fusion_ms = ms;
     if (cudaEventElapsedTime(&ms, e->ev[PH_RETYPE], e->ev[PH_END]) == cudaSuccess) out->meshing_ms = ms;
+  } else if (c.t_mesh_ns > c.t_start_ns && c.t_end_ns >= c.t_mesh_ns && c.t_start_ns) {
+    // the kernels' own clock: collect + integrate | retype + placement + GC + normals
+    // (the reference's fusion_ms / meshing_ms segments, engine.py:127-156)
+    out->fusion_ms = (double)(c.t_mesh_ns - c.t_start_ns) * 1e-6;
+    out->meshing_ms = (double)(c.t_end_ns - c.t_mesh_ns) * 1e-6;
   } else {
-    out->fusion_ms = out->device_ms;   // whole frame; per-segment split with vm_set_profiling
+    out->fusion_ms = out->device_ms;
     out->meshing_ms = 0.0;
   }
   cudaGetLastError();
@@ -740,6 +802,7 @@ static int fixed_nsteps(vm_engine *e, double trunc) {
 // Queue the kernels of the frame whose parameters are in slot `slot`; the
 // counters are snapshotted into the slot's pinned buffer after its last kernel.
 static int launch_frame(vm_engine *e, int slot) {
+  NvtxRange nvtx_("vm_launch_frame");
   FrameDev &F = *e->h_frame;
   F = e->f_saved[slot];
   F.snap = e->d_snapbuf[slot];
@@ -879,6 +942,7 @@ static int wait_snapshot(vm_engine *e, int slot, bool succ) {
 }
 
 static int settle_slot(vm_engine *e, int slot, bool succ) {
+  NvtxRange nvtx_("vm_settle_frame");
   TRY(wait_snapshot(e, slot, succ));
   const int launched = e->frame_launches;
   e->ev = e->evs[slot];

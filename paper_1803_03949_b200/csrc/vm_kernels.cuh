@@ -395,10 +395,13 @@ __global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, cons
   // must not write anything -- the host resumes the stopped frame and launches
   // this one again.  Read here, checked before the first write (the load's
   // latency hides behind the first region's sampling).
+  // The heap flag counts only when an earlier frame set it: a sibling CTA of
+  // this k_collect may set it mid-kernel (the frame then resumes after
+  // k_collect, whose results must be complete).
   int stop = 0;
   if (t == 0) {
     const int2 h = __ldcg(reinterpret_cast<const int2 *>(&ctr->error));
-    stop = (h.x | h.y) != 0;
+    stop = h.x != 0 || (h.y != 0 && h.y != F.epoch);
   }
   // The previous frame's face-normal fallback records (k_gc_normals) are
   // applied here, by the CTAs that have no pixel region (else by every CTA
@@ -886,6 +889,8 @@ __global__ void __launch_bounds__(kNT, 18) k_retype_place(DevState S, const Fram
   read_prologue(S, s_pro, &S.ctr->ncollected, &S.ctr->nslab, &S.ctr->nexplicit,
                 (int)blockIdx.x < S.max_blocks ? S.scope + blockIdx.x : nullptr);
   if (s_pro[0]) return;
+  // meshing starts here: every k_fuse_blocks CTA has completed (engine.py:127-156's split)
+  if (blockIdx.x == 0 && threadIdx.x == 0) S.ctr->t_mesh_ns = gtimer();
   const int nc = s_pro[1];
   const int n = F.scope_mode != 0 ? s_pro[3] : nc + s_pro[2];
   trace_at(S, TK_RETYPE, 1);
@@ -1368,6 +1373,7 @@ __device__ __forceinline__ void gc_commit(const DevState &S, const FrameDev &F, 
     c.done_gc = 0;
     ctr->done_gc = 0;
     c.t_end_ns = gtimer();
+    ctr->t_end_ns = c.t_end_ns;   // (resumed frames and the phase API read the global block)
   }
   if (!F.snap) return;
   __syncthreads();

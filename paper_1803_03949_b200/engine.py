@@ -4,8 +4,10 @@
 then the whole per-frame kernel sequence on the device (collect -> integrate
 -> scope/halo -> retype(+refine) -> place -> triangulate -> GC -> normals), and
 a D2H read of the StatsRow counters.  The non-timing StatsRow columns match
-the reference exactly; ``fusion_ms`` / ``meshing_ms`` are device times (CUDA
-events) of the same two segments the reference times on the host.
+the reference exactly; ``fusion_ms`` / ``meshing_ms`` are device times (the
+kernels' own %globaltimer stamps: collect + integrate | retype + placement +
+GC + normals) of the same two segments the reference times on the host
+(engine.py:127-156).
 """
 from __future__ import annotations
 
@@ -165,11 +167,27 @@ class Engine:
         self._pending: Optional[_PendingRow] = None
 
     # -- per-frame pipeline ---------------------------------------------------
+    def _order_device_input(self, t) -> None:
+        """A CUDA tensor input is read by kernels on the engine's stream: order
+        that stream after the stream that produced it (torch's current stream)
+        and tell the caching allocator the engine's stream uses the tensor, so
+        its memory is not reused while a queued frame still reads it."""
+        import torch
+        h = C.c_void_p()
+        _lib.check(_lib.load().vm_get_stream(self.store._h, C.byref(h)))
+        producer = torch.cuda.current_stream(t.device)
+        if (h.value or 0) == producer.cuda_stream:
+            return
+        es = torch.cuda.ExternalStream(h.value, device=t.device)
+        es.wait_stream(producer)
+        t.record_stream(es)
+
     def _depth_args(self, depth):
         if _is_device_tensor(depth):
             import torch
             if depth.dtype != torch.float64 or not depth.is_contiguous() or depth.dim() != 2:
                 raise ValueError("device depth must be a contiguous 2-D float64 CUDA tensor")
+            self._order_device_input(depth)
             return C.c_void_p(depth.data_ptr()), depth.shape[0], depth.shape[1], 1, None
         d = np.ascontiguousarray(np.asarray(depth, dtype=np.float64))
         if d.ndim != 2:
@@ -184,15 +202,7 @@ class Engine:
                                                   C.byref(_lib.pose_c(pose)), C.byref(self._fcfg),
                                                   self.frame_index)
             del keep
-            prev, self._pending = self._pending, None
-            _lib.check(rc)          # (an error of the previous frame surfaces here)
-            if prev is not None:    # completed by the submit: deliver its stats
-                self._deliver(prev)
-            row = _PendingRow(self, self.frame_index)
-            self._pending = row
-            self.stats.append(row)
-            self.frame_index += 1
-            return row
+            return self._after_submit(rc)
         st = _lib.Stats()
         _lib.check(_lib.load().vm_fuse_frame(self.store._h, ptr, h, w, on_dev,
                                               C.byref(self._intr_c), C.byref(_lib.pose_c(pose)),
@@ -215,20 +225,32 @@ class Engine:
                 raise ValueError("raw depth must be a 2-D array")
             ptr, h, w, on_dev, keep = _lib.ptr(a), a.shape[0], a.shape[1], 0, a
         self.store._touch()
+        if on_dev:
+            self._order_device_input(raw)
         rc = _lib.load().vm_fuse_frame_submit_raw(self.store._h, ptr, h, w, on_dev, float(depth_scale),
                                                   C.byref(self._intr_c), C.byref(_lib.pose_c(pose)),
                                                   C.byref(self._fcfg), self.frame_index)
         del keep
+        row = self._after_submit(rc)
+        if not self.pipelined:
+            self._resolve_pending()
+        return row
+
+    def _after_submit(self, rc: int) -> StatsRow:
+        """Bookkeeping after vm_fuse_frame_submit[_raw].  An argument error
+        (empty depth, bad config) queued nothing and left the frame in flight
+        pending: its row stays pending.  Any other error completed the pending
+        frame (it is the error reported) and dropped the new one."""
+        if rc in (_lib.VM_ERR_INPUT, _lib.VM_ERR_VALUE):
+            _lib.check(rc)
         prev, self._pending = self._pending, None
-        _lib.check(rc)
-        if prev is not None:
+        _lib.check(rc)          # (an error of the previous frame surfaces here)
+        if prev is not None:    # completed by the submit: deliver its stats
             self._deliver(prev)
         row = _PendingRow(self, self.frame_index)
         self._pending = row
         self.stats.append(row)
         self.frame_index += 1
-        if not self.pipelined:
-            self._resolve_pending()
         return row
 
     def _deliver(self, row: _PendingRow) -> None:

@@ -4,7 +4,8 @@ The per-cube rule runs on the device inside ``k_retype``
 (csrc/vm_device.cuh: refine_type); this module keeps the reference's public
 names (pkg/src/voxmesh/refine.py:29-140).  ``detect_disturbance`` is the
 reference's scalar statement of Eq. 3-5 and is what the exhaustive KAT
-compares the device kernel against (tests/test_refine_gpu.py).
+compares the device kernel against
+(tests/test_gpu_reference_suite.py::test_refine_kernel_exhaustive_eq3_5).
 """
 from __future__ import annotations
 

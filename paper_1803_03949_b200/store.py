@@ -165,6 +165,21 @@ class SpatialStore:
         _lib.check(_lib.load().vm_counters(self._h, C.byref(c)))
         return {k: int(getattr(c, k)) for k in _lib.COUNTER_FIELDS}
 
+    def snapshot_arrays(self) -> dict:
+        """Dense host copies of every block, sorted by coordinate (the order of
+        ``blocks()``): coords (n, 3), tsdf / weight / type_prev / type_curr
+        (n, 8, 8, 8) -- the bulk form of the per-block views."""
+        n = self._counters()["block_count"]
+        out = dict(coords=np.zeros((n, 3), np.int32), tsdf=np.zeros((n, 8, 8, 8)),
+                   weight=np.zeros((n, 8, 8, 8), np.int32), type_prev=np.zeros((n, 8, 8, 8), np.uint8),
+                   type_curr=np.zeros((n, 8, 8, 8), np.uint8))
+        _lib.check(_lib.load().vm_snapshot_blocks(self._h, n, *[_lib.ptr(out[k]) for k in
+                                                               ("coords", "tsdf", "weight", "type_prev",
+                                                                "type_curr")], None, None))
+        c = out["coords"]
+        order = np.lexsort((c[:, 2], c[:, 1], c[:, 0])) if n else np.zeros(0, int)
+        return {k: v[order] for k, v in out.items()}
+
     def _snapshot(self):
         if self._snap_version == self._version and self._snap is not None:
             return self._snap
