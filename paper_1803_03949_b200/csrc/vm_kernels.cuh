@@ -359,6 +359,8 @@ __device__ __forceinline__ unsigned cset_hash(unsigned long long k) {
 __device__ __forceinline__ int collect_block(const DevState &S, const FrameDev &F, int x, int y, int z) {
   HashRef r = hash_find_ref(S, x, y, z);
   if (r.idx == -1) r = hash_insert_ref(S, x, y, z, F.epoch);
+  else if (r.idx == -2)   // a key whose allocation failed (table full): the reference raises again
+    set_error(S, ERR_CAPACITY, S.max_blocks, S.table_size, 1, F.epoch);
   if (r.idx >= 0 && r.stamp != F.epoch && atomicExch(r.stamp_ptr, F.epoch) != F.epoch) {
     S.stamp_collect[r.idx] = F.epoch;
     return r.idx;

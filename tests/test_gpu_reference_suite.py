@@ -505,3 +505,105 @@ def test_device_resident_depth_matches_host_depth():
         e2.fuse_frame(torch.tensor(d, device="cuda"), p)
     m1, m2 = e1.compact(), e2.compact()
     assert np.array_equal(m1.positions, m2.positions) and np.array_equal(m1.indices, m2.indices)
+
+
+def test_store_usable_after_block_table_capacity_error():   # store.py:296-320, 304-306
+    """A frame that fills the block table raises CapacityError; the device
+    flag is then cleared and the partially updated store stays usable as the
+    reference's does: the block count is the reference's (table_size / 2,
+    allocation stopped at 2n >= table_size), the blocks it allocated are empty
+    ones, compaction / audit / snapshots work, and a later frame that needs a
+    new block raises again."""
+    from oracle.oracle import OracleCapacityError, OracleEngine
+    from paper_1803_03949_b200 import CapacityError, Engine, RunConfig
+    from paper_1803_03949_b200.synth import SceneSpec, camera_pose, render_depth
+    spec = SceneSpec(scene="sphere", sphere_radius=0.3, orbit_radius=0.9, elevation_amp_deg=60.0,
+                     angular_step_deg=18.0, frames=3, width=64, height=48, fx=55.0, fy=55.0)
+    intr = spec.intrinsics()
+    cfg = dict(cube_size=0.025, table_size=64)
+    eng = Engine(RunConfig(**cfg), intr)
+    ora = OracleEngine(cfg, (intr.fx, intr.fy, intr.cx, intr.cy, intr.width, intr.height))
+    pose = camera_pose(spec, 0)
+    d = render_depth(spec, pose)
+    with pytest.raises(CapacityError):
+        eng.fuse_frame(d, pose)
+    with pytest.raises(OracleCapacityError):
+        ora.fuse_frame(d, pose.rotation, pose.translation)
+    assert eng.store.block_count == ora.store.block_count() == 32
+    m = eng.compact()                                  # no stale error re-raised
+    assert len(m.indices) == 0 and len(m.positions) == 0
+    assert eng.audit().ok
+    snap = eng.store.snapshot_arrays()
+    assert (snap["weight"] == 0).all() and (snap["tsdf"] == 0).all()
+    with pytest.raises(CapacityError):                # a block of frame 0 it could not allocate
+        eng.fuse_frame(d, pose)
+    with pytest.raises(OracleCapacityError):
+        ora.fuse_frame(d, pose.rotation, pose.translation)
+    assert eng.store.block_count == ora.store.block_count() == 32
+
+
+def test_pipelined_engine_continues_after_capacity_error():
+    """After a pipelined frame's CapacityError the engine is not wedged: the
+    dropped frame can be submitted again and compaction works."""
+    from paper_1803_03949_b200 import CapacityError, Engine, RunConfig
+    from paper_1803_03949_b200.synth import SceneSpec, static_pose, render_depth
+    spec = SceneSpec(scene="plane", width=48, height=48, fx=40.0, fy=40.0)
+    pose = static_pose((0, 0, 0), (0, 0, 1))
+    depth = render_depth(spec, pose)
+    eng = Engine(RunConfig(cube_size=0.02, max_vertices=50), spec.intrinsics(), pipelined=True)
+    eng.fuse_frame(depth, pose)
+    with pytest.raises(CapacityError):
+        eng.fuse_frame(depth, pose)
+    eng.compact()
+    far = np.zeros_like(depth)                         # no valid pixel: nothing allocated
+    row = eng.fuse_frame(far, pose)
+    assert row.vertices_live >= 0
+
+
+def test_pipelined_empty_depth_keeps_pending_frame():
+    """An argument error (empty depth) queues nothing: the frame in flight
+    keeps its row and later submissions proceed (the engine is not wedged)."""
+    from paper_1803_03949_b200 import Engine, InputError, RunConfig
+    from paper_1803_03949_b200.synth import SceneSpec, static_pose, render_depth
+    spec = SceneSpec(scene="plane", width=48, height=48, fx=40.0, fy=40.0)
+    pose = static_pose((0, 0, 0), (0, 0, 1))
+    depth = render_depth(spec, pose)
+    a = Engine(RunConfig(cube_size=0.02), spec.intrinsics(), pipelined=True)
+    b = Engine(RunConfig(cube_size=0.02), spec.intrinsics())
+    r0 = a.fuse_frame(depth, pose)
+    with pytest.raises(InputError):
+        a.fuse_frame(np.zeros((0, 48)), pose)
+    r1 = a.fuse_frame(depth, pose)
+    s0, s1 = b.fuse_frame(depth, pose), b.fuse_frame(depth, pose)
+    assert (r0.vertices_live, r1.vertices_live) == (s0.vertices_live, s1.vertices_live)
+    assert r1.frame == 1
+
+
+def test_device_depth_from_another_stream_is_ordered():
+    """A CUDA depth tensor produced on a side stream (torch's current stream
+    at the call) is ordered before the engine's kernels and kept alive for
+    them (record_stream): rows equal the host-input engine's."""
+    import torch
+    from paper_1803_03949_b200 import Engine, RunConfig
+    from paper_1803_03949_b200.synth import SceneSpec, camera_pose, render_depth
+    spec = SceneSpec(scene="sphere", sphere_radius=0.3, orbit_radius=0.9, elevation_amp_deg=60.0,
+                     angular_step_deg=18.0, frames=4, width=96, height=72, fx=80.0, fy=80.0)
+    intr = spec.intrinsics()
+    a = Engine(RunConfig(cube_size=0.025), intr, pipelined=True)
+    b = Engine(RunConfig(cube_size=0.025), intr)
+    side = torch.cuda.Stream()
+    rows = []
+    for i in range(spec.frames):
+        pose = camera_pose(spec, i)
+        d = render_depth(spec, pose)
+        with torch.cuda.stream(side):
+            big = torch.randn(4096, 4096, device="cuda")
+            for _ in range(4):
+                big = big @ big.T / 4096.0          # keep the side stream busy
+            dev = torch.from_numpy(d).to("cuda") + big[0, 0].clamp(-1.0, 1.0) * 0.0
+            rows.append(a.fuse_frame(dev, pose))
+            del dev                                     # freed while the frame may still read it
+        b.fuse_frame(d, pose)
+    for ra, rb in zip(rows, b.stats):
+        assert (ra.blocks_active, ra.vertices_live, ra.triangles_live) == \
+               (rb.blocks_active, rb.vertices_live, rb.triangles_live)
