@@ -165,22 +165,22 @@ class Engine:
         self._collected_cache = None
         self.pipelined = bool(pipelined) and not audit_every_frame
         self._pending: Optional[_PendingRow] = None
+        self._inflight = None   # CUDA tensor input of the frame in flight (kept alive until it completes)
 
     # -- per-frame pipeline ---------------------------------------------------
     def _order_device_input(self, t) -> None:
         """A CUDA tensor input is read by kernels on the engine's stream: order
-        that stream after the stream that produced it (torch's current stream)
-        and tell the caching allocator the engine's stream uses the tensor, so
-        its memory is not reused while a queued frame still reads it."""
+        that stream after the stream that produced it (torch's current stream).
+        The tensor is kept referenced until its frame has completed (the
+        pipelined paths hold it in ``_inflight``), so the caching allocator
+        cannot hand its memory out while a queued frame still reads it."""
         import torch
         h = C.c_void_p()
         _lib.check(_lib.load().vm_get_stream(self.store._h, C.byref(h)))
         producer = torch.cuda.current_stream(t.device)
         if (h.value or 0) == producer.cuda_stream:
             return
-        es = torch.cuda.ExternalStream(h.value, device=t.device)
-        es.wait_stream(producer)
-        t.record_stream(es)
+        torch.cuda.ExternalStream(h.value, device=t.device).wait_stream(producer)
 
     def _depth_args(self, depth):
         if _is_device_tensor(depth):
@@ -188,7 +188,7 @@ class Engine:
             if depth.dtype != torch.float64 or not depth.is_contiguous() or depth.dim() != 2:
                 raise ValueError("device depth must be a contiguous 2-D float64 CUDA tensor")
             self._order_device_input(depth)
-            return C.c_void_p(depth.data_ptr()), depth.shape[0], depth.shape[1], 1, None
+            return C.c_void_p(depth.data_ptr()), depth.shape[0], depth.shape[1], 1, depth
         d = np.ascontiguousarray(np.asarray(depth, dtype=np.float64))
         if d.ndim != 2:
             raise ValueError("depth must be a 2-D array")
@@ -201,8 +201,7 @@ class Engine:
             rc = _lib.load().vm_fuse_frame_submit(self.store._h, ptr, h, w, on_dev, C.byref(self._intr_c),
                                                   C.byref(_lib.pose_c(pose)), C.byref(self._fcfg),
                                                   self.frame_index)
-            del keep
-            return self._after_submit(rc)
+            return self._after_submit(rc, keep if on_dev else None)
         st = _lib.Stats()
         _lib.check(_lib.load().vm_fuse_frame(self.store._h, ptr, h, w, on_dev,
                                               C.byref(self._intr_c), C.byref(_lib.pose_c(pose)),
@@ -218,7 +217,7 @@ class Engine:
         if _is_device_tensor(raw):
             if raw.element_size() != 2 or not raw.is_contiguous() or raw.dim() != 2:
                 raise ValueError("device raw depth must be a contiguous 2-D 16-bit CUDA tensor")
-            ptr, h, w, on_dev, keep = C.c_void_p(raw.data_ptr()), raw.shape[0], raw.shape[1], 1, None
+            ptr, h, w, on_dev, keep = C.c_void_p(raw.data_ptr()), raw.shape[0], raw.shape[1], 1, raw
         else:
             a = np.ascontiguousarray(np.asarray(raw, dtype=np.uint16))
             if a.ndim != 2:
@@ -230,13 +229,12 @@ class Engine:
         rc = _lib.load().vm_fuse_frame_submit_raw(self.store._h, ptr, h, w, on_dev, float(depth_scale),
                                                   C.byref(self._intr_c), C.byref(_lib.pose_c(pose)),
                                                   C.byref(self._fcfg), self.frame_index)
-        del keep
-        row = self._after_submit(rc)
+        row = self._after_submit(rc, keep if on_dev else None)
         if not self.pipelined:
             self._resolve_pending()
         return row
 
-    def _after_submit(self, rc: int) -> StatsRow:
+    def _after_submit(self, rc: int, device_input=None) -> StatsRow:
         """Bookkeeping after vm_fuse_frame_submit[_raw].  An argument error
         (empty depth, bad config) queued nothing and left the frame in flight
         pending: its row stays pending.  Any other error completed the pending
@@ -244,7 +242,9 @@ class Engine:
         if rc in (_lib.VM_ERR_INPUT, _lib.VM_ERR_VALUE):
             _lib.check(rc)
         prev, self._pending = self._pending, None
+        self._inflight = None   # (the previous frame has completed on the device)
         _lib.check(rc)          # (an error of the previous frame surfaces here)
+        self._inflight = device_input   # read by the frame now in flight
         if prev is not None:    # completed by the submit: deliver its stats
             self._deliver(prev)
         row = _PendingRow(self, self.frame_index)
@@ -268,6 +268,7 @@ class Engine:
         row, self._pending = self._pending, None
         if row is not None:
             self._deliver(row)
+        self._inflight = None
 
     @staticmethod
     def _row_from(frame: int, d: dict) -> StatsRow:

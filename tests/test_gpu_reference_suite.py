@@ -520,7 +520,7 @@ def test_store_usable_after_block_table_capacity_error():   # store.py:296-320, 
     spec = SceneSpec(scene="sphere", sphere_radius=0.3, orbit_radius=0.9, elevation_amp_deg=60.0,
                      angular_step_deg=18.0, frames=3, width=64, height=48, fx=55.0, fy=55.0)
     intr = spec.intrinsics()
-    cfg = dict(cube_size=0.025, table_size=64)
+    cfg = dict(cube_size=0.025, table_size=48)          # frame 0 needs 32 blocks, the table holds 24
     eng = Engine(RunConfig(**cfg), intr)
     ora = OracleEngine(cfg, (intr.fx, intr.fy, intr.cx, intr.cy, intr.width, intr.height))
     pose = camera_pose(spec, 0)
@@ -529,7 +529,7 @@ def test_store_usable_after_block_table_capacity_error():   # store.py:296-320, 
         eng.fuse_frame(d, pose)
     with pytest.raises(OracleCapacityError):
         ora.fuse_frame(d, pose.rotation, pose.translation)
-    assert eng.store.block_count == ora.store.block_count() == 32
+    assert eng.store.block_count == ora.store.block_count() == 24
     m = eng.compact()                                  # no stale error re-raised
     assert len(m.indices) == 0 and len(m.positions) == 0
     assert eng.audit().ok
@@ -539,7 +539,7 @@ def test_store_usable_after_block_table_capacity_error():   # store.py:296-320, 
         eng.fuse_frame(d, pose)
     with pytest.raises(OracleCapacityError):
         ora.fuse_frame(d, pose.rotation, pose.translation)
-    assert eng.store.block_count == ora.store.block_count() == 32
+    assert eng.store.block_count == ora.store.block_count() == 24
 
 
 def test_pipelined_engine_continues_after_capacity_error():
