@@ -554,10 +554,15 @@ def test_pipelined_engine_continues_after_capacity_error():
     eng.fuse_frame(depth, pose)
     with pytest.raises(CapacityError):
         eng.fuse_frame(depth, pose)
-    eng.compact()
-    far = np.zeros_like(depth)                         # no valid pixel: nothing allocated
-    row = eng.fuse_frame(far, pose)
-    assert row.vertices_live >= 0
+    eng.compact()                                      # the partial store can be read
+    # the pool stays over its limit (the failing frame's vertices were placed),
+    # so every later frame reports CapacityError again -- never the wedge
+    # "previous frame's result was not taken"
+    for _ in range(2):
+        eng.fuse_frame(np.zeros_like(depth), pose)
+        with pytest.raises(CapacityError):
+            eng.fuse_frame(np.zeros_like(depth), pose)
+        assert eng._pending is None
 
 
 def test_pipelined_empty_depth_keeps_pending_frame():
