@@ -266,7 +266,9 @@ def workload(args, spec, cfg):
             "cube_size_m": cfg["cube_size"], "trunc_m": cfg["trunc"],
             "refine": bool(cfg.get("refine", False)), "strategy": args.strategy,
             "l2": "flushed between frames (256 MiB write, outside the timed events)",
-            "parallelism": (f"spatial partition x{args.gpus} (tiles of {args.tile_blocks}^3 blocks)"
+            "halo": args.halo if args.gpus > 1 and args.mode == "partition" else None,
+            "parallelism": (f"spatial partition x{args.gpus} (tiles of {args.tile_blocks}^3 blocks, "
+                            f"halo {args.halo})"
                             if args.gpus > 1 and args.mode == "partition" else
                             f"replicas x{args.gpus}" if args.gpus > 1 else "single GPU")}
 
@@ -277,7 +279,15 @@ def run_gpu(args, spec, cfg, rank, world, local_rank):
     from paper_1803_03949_b200 import Engine, RunConfig
     from paper_1803_03949_b200.partition import PartitionedEngine
     part = world > 1 and args.mode == "partition"
+    xchg = part and args.halo == "exchange"
     ekw = dict(rank=rank, nranks=world, tile_blocks=args.tile_blocks) if part else {}
+    gloo = world > 1 and str(dist.get_backend()).lower() != "nccl"
+
+    def reduce_(vals, op):
+        """all-reduce of a float64 vector (gloo: on the host)"""
+        t = torch.tensor(vals, dtype=torch.float64, device="cpu" if gloo else dev)
+        dist.all_reduce(t, op=op)
+        return t.cpu().tolist()
     local_rank %= torch.cuda.device_count()   # (several ranks may share a GPU in tests)
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -301,7 +311,27 @@ def run_gpu(args, spec, cfg, rank, world, local_rank):
 
     def timed_pass(profiling: bool):
         """warmup + steps frames on a fresh engine, each step timed with CUDA
-        events on the engine's stream, L2 flushed between steps"""
+        events on the engine's stream, L2 flushed between steps.  Halo
+        exchange: each step is PartitionedEngine.fuse_frame (begin, the
+        all-gather of boundary blocks, finish, the StatsRow all-reduce)."""
+        if xchg:
+            pe = PartitionedEngine(RunConfig(strategy=args.strategy, **cfg, **caps), spec.intrinsics(),
+                                   tile_blocks=args.tile_blocks, device=dev, halo="exchange")
+            pe.engine.set_stream(stream.cuda_stream)
+            for i in range(args.warmup):
+                pe.fuse_frame(depths[i], poses[i])
+            dist.barrier()
+            torch.cuda.synchronize()
+            starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+            ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+            for k in range(args.steps):
+                i = args.warmup + k
+                flush.zero_()
+                starts[k].record(stream)
+                pe.fuse_frame(depths[i], poses[i])
+                ends[k].record(stream)
+            torch.cuda.synchronize()
+            return pe.engine, [s.elapsed_time(e) for s, e in zip(starts, ends)], [], 0
         eng = Engine(RunConfig(strategy=args.strategy, **cfg, **caps, **ekw), spec.intrinsics())
         eng.set_stream(stream.cuda_stream)
         eng.set_profiling(profiling)
@@ -332,36 +362,41 @@ def run_gpu(args, spec, cfg, rank, world, local_rank):
         eng, frame_ms, _, resumes = timed_pass(False)
     # second pass on a fresh engine (same frames, same state evolution) with an
     # event before every kernel: per-kernel durations for the roofline
-    _, prof_frame_ms, phase_ms, _ = timed_pass(True)
+    _, prof_frame_ms, phase_ms, _ = timed_pass(True) if not xchg else (None, frame_ms, [], 0)
     local_s = sum(frame_ms) / 1e3
     if part:
         # frames are processed jointly: a frame ends when its slowest rank ends
-        t = torch.tensor(frame_ms, device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dev_s = float(t.sum().item()) / 1e3
+        dev_s = sum(reduce_(frame_ms, dist.ReduceOp.MAX)) / 1e3
         value = args.steps / dev_s
     else:
         dev_s = local_s
         if world > 1:
-            t = torch.tensor([dev_s], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dev_s = float(t.item())
+            dev_s = reduce_([dev_s], dist.ReduceOp.MAX)[0]
         value = world * args.steps / dev_s
     stats = eng.device_stats[args.warmup:]
     launches = sum(s["kernel_launches"] for s in stats)   # our kernels in the timed region
 
-    # roofline: dominant kernel (largest share of the timed frames)
-    names = list(phase_ms[0].keys())
-    tot = {n: sum(p[n] for p in phase_ms) for n in names}
-    dom = max(names, key=lambda n: tot[n])
-    bytes_dom = sum(phase_bytes(s, spec.height, spec.width)[dom] for s in stats)
-    achieved = bytes_dom / (tot[dom] / 1e3) / 1e9
+    # roofline: dominant kernel (largest share of the timed frames); the halo
+    # exchange frame has no per-kernel events (its two halves are separate
+    # calls around the collective): the frame as a whole
     peak, peak_kind = measured_peak_gbs()
+    frame_bytes = sum(sum(phase_bytes(s, spec.height, spec.width).values()) for s in stats)
+    if phase_ms:
+        names = list(phase_ms[0].keys())
+        tot = {n: sum(p[n] for p in phase_ms) for n in names}
+        dom = max(names, key=lambda n: tot[n])
+        bytes_dom = sum(phase_bytes(s, spec.height, spec.width)[dom] for s in stats)
+        achieved = bytes_dom / (tot[dom] / 1e3) / 1e9
+        kernel_share = tot[dom] / sum(tot.values())
+    else:
+        names, tot, dom = [], {}, "frame"
+        bytes_dom, achieved, kernel_share = frame_bytes, frame_bytes / local_s / 1e9, 1.0
     traffic = None   # dram read+write bytes per launch of that kernel, from the committed ncu capture
     tp = ROOT / "profiles" / "ncu_traffic.json"
     if tp.exists():
-        traffic = json.loads(tp.read_text()).get("dram_bytes_per_launch", {}).get(f"k_{dom}")
-    frame_bytes = sum(sum(phase_bytes(s, spec.height, spec.width).values()) for s in stats)
+        tj = json.loads(tp.read_text())
+        traffic = tj.get("by_config", {}).get(args.config, tj.get("dram_bytes_per_launch", {}) if args.config == "C2"
+                                              else {}).get(f"k_{dom}")
 
     # e2e: public API, pinned host depth, H2D + StatsRow D2H per frame, wall clock
     host = [torch.empty(d.shape, dtype=torch.float64, pin_memory=True) for d in depths]
@@ -370,7 +405,7 @@ def run_gpu(args, spec, cfg, rank, world, local_rank):
     host_np = [h.numpy() for h in host]
     if part:   # global StatsRow every frame: one NCCL all-reduce of the rank counters
         e2 = PartitionedEngine(RunConfig(strategy=args.strategy, **cfg, **caps), spec.intrinsics(),
-                               tile_blocks=args.tile_blocks, device=dev)
+                               tile_blocks=args.tile_blocks, device=dev, halo=args.halo)
     else:
         # pipelined submission (vm_fuse_frame_submit): the next frame's H2D copy
         # overlaps this frame's kernels; every frame's StatsRow is still read back
@@ -386,9 +421,7 @@ def run_gpu(args, spec, cfg, rank, world, local_rank):
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
     if world > 1:
-        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+        e2e_s = reduce_([e2e_s], dist.ReduceOp.MAX)[0]
     # parity spot check of the timed engine vs the e2e engine (same frames)
     e2_local = e2.engine if part else e2
     same = eng.stats[-1].vertices_live == e2_local.stats[-1].vertices_live
@@ -439,7 +472,7 @@ def run_gpu(args, spec, cfg, rank, world, local_rank):
         "config": workload(args, spec, cfg),
         "roofline": {"bound": "hbm", "kernel": f"k_{dom}", "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "alg_bytes_per_launch": bytes_dom / args.steps, "kernel_share": tot[dom] / sum(tot.values()),
+                     "traffic": traffic, "alg_bytes_per_launch": bytes_dom / args.steps, "kernel_share": kernel_share,
                      "frame_alg_bytes": frame_bytes / args.steps,
                      "frame_achieved_gbs": frame_bytes / local_s / 1e9,
                      "frame_frac": frame_bytes / local_s / 1e9 / peak},
@@ -470,6 +503,8 @@ def main():
     ap.add_argument("--strategy", default="claim")
     ap.add_argument("--mode", default="partition", choices=["partition", "replicas"])
     ap.add_argument("--tile-blocks", type=int, default=8)
+    ap.add_argument("--halo", default="margin", choices=["margin", "exchange"],
+                    help="partition mode: margin blocks integrated locally, or received from their owners")
     ap.add_argument("--backend", default="nccl", help="gloo only to test N>1 on a single GPU")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--ref-budget", type=float, default=150.0)

@@ -51,7 +51,9 @@ typedef struct {
   int32_t rank;
   int32_t nranks;
   int32_t tile_blocks;       /* power of two (default 8) */
-  int32_t reserved;
+  int32_t halo_exchange;     /* 0: margin blocks integrated by this rank from the broadcast
+                              * depth; 1: owned blocks only, margin blocks received from their
+                              * owners before meshing (vm_partition_frame_begin / _finish) */
 } vm_store_config;
 
 /* Intrinsics (fusion.py:20-33) */
@@ -289,6 +291,42 @@ int vm_compact_fetch(vm_engine *e, double *positions, double *normals, int64_t *
                      int32_t *indices);
 /* Engine.audit (engine.py:187-230) as device reductions */
 int vm_audit(vm_engine *e, vm_audit_report *out);
+
+/* ---- spatial partition across ranks ----
+ * The reference is single-process; these entry points are what a rank of the
+ * partitioned reconstruction calls around its collectives (the Python layer,
+ * partition.py, runs them over torch.distributed: NCCL on the GPU box).
+ *
+ * Halo-exchange frame = begin (collect + integrate the owned blocks, pack the
+ * collected boundary blocks into `send`: kVM_GHOST_RECORD bytes each), an
+ * all-gather of every rank's records (max_count per rank, padded), finish
+ * (adopt the records in this rank's margin, then meshing).  Engine.fuse_frame
+ * (engine.py:123-165) split around the exchange.  `send` / `recv` are device
+ * pointers.  If *n_send > send_cap, grow the buffer and call
+ * vm_partition_repack.  *n_owned_collected: owned blocks collected. */
+#define VM_GHOST_RECORD 6160
+int vm_partition_frame_begin(vm_engine *e, const double *depth, int32_t h, int32_t w, int32_t depth_on_device,
+                             const vm_intrinsics *intr, const vm_pose *pose, const vm_frame_config *cfg,
+                             int64_t frame_index, uint8_t *send, int64_t send_cap, int64_t *n_send,
+                             int64_t *n_owned_collected);
+int vm_partition_repack(vm_engine *e, uint8_t *send, int64_t send_cap, int64_t *n_send);
+int vm_partition_frame_finish(vm_engine *e, const uint8_t *recv, const int32_t *counts, int32_t nranks,
+                              int64_t max_count, vm_stats *out);
+/* Distributed compaction (store.py:388-425 over the union of the ranks'
+ * owned blocks).  begin: sort this rank's owned blocks; meta: their packed
+ * keys (sorted), vertex / triangle counts and 48-word slot occupancy (host
+ * arrays of *n_owned entries); fill: given the merged (k-way, by key) global
+ * block list -- keys, exclusive vertex / triangle bases, occupancy and its
+ * per-word exclusive popcount prefix (host arrays of n_global entries) and
+ * this rank's blocks' global positions -- write this rank's vertices and
+ * triangles at their global positions into zero-initialised DEVICE arrays of
+ * the global mesh (the ranks' arrays are then summed: disjoint ranges). */
+int vm_partition_compact_begin(vm_engine *e, int64_t *n_owned);
+int vm_partition_compact_meta(vm_engine *e, uint64_t *keys, int32_t *vcnt, int32_t *tcnt, uint32_t *occ);
+int vm_partition_compact_fill(vm_engine *e, const uint64_t *gkeys, const int64_t *vbase, const int64_t *tbase,
+                              const uint32_t *gocc, const int32_t *gocc_pre, int64_t n_global,
+                              const int32_t *my_global, int64_t current_frame, double *pos, double *nrm,
+                              int64_t *ages, int32_t *idx);
 
 #ifdef __cplusplus
 }

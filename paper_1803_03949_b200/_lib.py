@@ -25,13 +25,14 @@ def lib_path() -> Path:
 
 VM_OK, VM_ERR_CAPACITY, VM_ERR_CONSISTENCY, VM_ERR_VALUE, VM_ERR_CUDA, VM_ERR_INPUT = range(6)
 STRATEGY_CODES = {"serial": 0, "claim": 1, "partition": 2}
+GHOST_RECORD = 6160   # VM_GHOST_RECORD: halo-exchange record bytes (coord + 512 tsdf + 512 weights)
 
 
 class StoreConfig(C.Structure):
     _fields_ = [("cube_size", C.c_double), ("table_size", C.c_int64), ("max_vertices", C.c_int64),
                 ("initial_blocks", C.c_int64), ("initial_vertices", C.c_int64),
                 ("initial_triangles", C.c_int64), ("rank", C.c_int32), ("nranks", C.c_int32),
-                ("tile_blocks", C.c_int32), ("reserved", C.c_int32)]
+                ("tile_blocks", C.c_int32), ("halo_exchange", C.c_int32)]
 
 
 class Intr(C.Structure):
@@ -138,6 +139,17 @@ _SIGS = {
     "vm_audit": (C.c_int, [C.c_void_p, C.POINTER(AuditC)]),
     "vm_export_blocks": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_int64)] + [C.c_void_p] * 8),
     "vm_import_blocks": (C.c_int, [C.c_void_p, C.c_int64] + [C.c_void_p] * 8),
+    "vm_partition_frame_begin": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                           C.POINTER(Intr), C.POINTER(PoseC), C.POINTER(FrameConfig),
+                                           C.c_int64, C.c_void_p, C.c_int64, C.POINTER(C.c_int64),
+                                           C.POINTER(C.c_int64)]),
+    "vm_partition_repack": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]),
+    "vm_partition_frame_finish": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int64,
+                                            C.POINTER(Stats)]),
+    "vm_partition_compact_begin": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
+    "vm_partition_compact_meta": (C.c_int, [C.c_void_p] + [C.c_void_p] * 4),
+    "vm_partition_compact_fill": (C.c_int, [C.c_void_p] + [C.c_void_p] * 5 + [C.c_int64, C.c_void_p, C.c_int64]
+                                  + [C.c_void_p] * 4),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -86,7 +86,8 @@ struct alignas(16) Counters {
   unsigned long long t_start_ns;   // %globaltimer: k_collect start, k_gc_normals commit
   unsigned long long t_end_ns;
   unsigned long long t_mesh_ns;    // k_retype_place start (after integration): fusion | meshing split
-  unsigned long long pad1;
+  int32_t nsend;                   // halo exchange: boundary blocks packed for the other ranks
+  int32_t pad1;
 };
 static_assert(sizeof(Counters) % 16 == 0, "snapshots are copied in 16-byte words");
 
@@ -125,6 +126,10 @@ struct FrameDev {
   Counters *self_dst;
   unsigned long long *self_seq;
   unsigned long long self_id;
+  // halo exchange: the ranks' packed boundary blocks,
+  // rank q's k-th record at ghost_recv + (q * ghost_max + k) * kGhostRec
+  const uint8_t *ghost_recv;
+  int32_t ghost_max, ghost_nranks;
 };
 
 // one hash slot: packed coordinate (-1 empty) and block index (-1 while the
@@ -179,7 +184,13 @@ struct DevState {
   // spatial partition: blocks are owned by hashed tiles
   // of 2^tile_shift blocks per axis; a rank also computes a 1-block margin
   int32_t rank, nranks, tile_shift;
+  // 0: margin mode -- the rank integrates its margin blocks itself from the
+  //    broadcast depth; 1: halo exchange -- it integrates owned blocks only and
+  //    receives the margin blocks' samples from their owners before meshing
+  int32_t halo_exchange;
   uint8_t *bowned;      // [max_blocks] block owned by this rank
+  int32_t *ghost_src;   // [max_blocks] scope position -> received record (halo exchange)
+  const int32_t *ghost_counts;   // [nranks] records per rank of the current exchange
   Counters *ctr;
   unsigned long long *trace;   // per-CTA phase timestamps (vm_set_trace), null = off
 };
@@ -366,8 +377,27 @@ __device__ __forceinline__ int tile_owner(const DevState &S, int tx, int ty, int
 __device__ __forceinline__ bool block_owned(const DevState &S, int x, int y, int z) {
   return S.nranks <= 1 || tile_owner(S, x >> S.tile_shift, y >> S.tile_shift, z >> S.tile_shift) == S.rank;
 }
+// a block whose 27-neighbourhood reaches a tile of another rank: it lies in
+// that rank's margin, so its samples are sent in halo-exchange mode
+__device__ __forceinline__ bool block_on_boundary(const DevState &S, int x, int y, int z) {
+  const int sh = S.tile_shift;
+  for (int tx = (x - 1) >> sh; tx <= (x + 1) >> sh; tx++)
+    for (int ty = (y - 1) >> sh; ty <= (y + 1) >> sh; ty++)
+      for (int tz = (z - 1) >> sh; tz <= (z + 1) >> sh; tz++)
+        if (tile_owner(S, tx, ty, tz) != S.rank) return true;
+  return false;
+}
+
 // owned, or within one block of an owned tile (the margin this rank computes)
+__device__ __forceinline__ bool block_in_margin(const DevState &S, int x, int y, int z);
+// the blocks this rank's band walk collects: owned + margin (margin mode) or
+// owned only (halo exchange: the margin arrives from the owners)
 __device__ __forceinline__ bool block_relevant(const DevState &S, int x, int y, int z) {
+  if (S.nranks <= 1) return true;
+  if (S.halo_exchange) return block_owned(S, x, y, z);
+  return block_in_margin(S, x, y, z);
+}
+__device__ __forceinline__ bool block_in_margin(const DevState &S, int x, int y, int z) {
   if (S.nranks <= 1) return true;
   const int sh = S.tile_shift;
   const int x0 = (x - 1) >> sh, x1 = (x + 1) >> sh, y0 = (y - 1) >> sh, y1 = (y + 1) >> sh;

@@ -24,6 +24,7 @@
 
 #include "../../include/voxmesh_b200.h"
 #include "vm_kernels.cuh"
+#include "vm_partition.cuh"
 
 using namespace vm;
 
@@ -133,7 +134,22 @@ struct vm_engine {
   bool norm_valid = false;
   double *d_rays = nullptr;   // ray tables of the cached intrinsics (k_norm_bounds)
   size_t rays_cap = 0;
+  // spatial partition: a halo-exchange frame between begin and finish, and
+  // the owned-block arrays of a distributed compaction
+  bool part_active = false;
+  int32_t part_nc_own = 0;
+  int64_t part_frame = 0;
+  int32_t *d_ghost_counts = nullptr;   // [kMaxRanks]
+  struct {
+    unsigned long long *keys_in = nullptr, *keys_out = nullptr;
+    int32_t *vals = nullptr, *order = nullptr, *vcnt = nullptr, *tcnt = nullptr;
+    uint32_t *occ_bits = nullptr;
+    uint16_t *occ_pre = nullptr;
+    void *tmp = nullptr;
+    int nb = 0, nown = 0;
+  } pc;
 };
+constexpr int kMaxRanks = 256;
 
 extern "C" {
 static int settle(vm_engine *e);
@@ -335,7 +351,7 @@ static int enqueue_after_collect(vm_engine *e) {
   const FrameDev F = *e->h_frame;
   rec(e, PH_FUSE);
   launch_pdl(k_fuse_blocks, e->grid_fuse, kFB, st, S, F, (const int32_t *)S.scope,
-             (const int32_t *)&S.ctr->ncollected, 0, (int)(F_INIT | F_INTEGRATE | F_SCOPE));
+             (const int32_t *)&S.ctr->ncollected, 0, (int)(F_INIT | F_INTEGRATE | F_SCOPE), 0);
   rec(e, PH_RETYPE);
   launch_pdl(k_retype_place, e->grid_retype, kNT, st, S, F);
   rec(e, PH_GC);
@@ -428,6 +444,14 @@ static int init_new_blocks(vm_engine *e) {
   TRY(check_launch());
   TRY(read_counters(e));
   return error_from_counters(e);
+}
+
+static void free_pcompact(vm_engine *e) {
+  auto &p = e->pc;
+  for (void *q : {(void *)p.keys_in, (void *)p.keys_out, (void *)p.vals, (void *)p.order, (void *)p.vcnt,
+                  (void *)p.tcnt, (void *)p.occ_bits, (void *)p.occ_pre, p.tmp})
+    if (q) cudaFree(q);
+  e->pc = {};
 }
 
 static void free_compacted(Compacted &c) {
@@ -575,6 +599,10 @@ int vm_create(const vm_store_config *cfg, vm_engine **out) {
   TRY(dev_alloc(&S.stamp_halo, mb, 0xFF));
   TRY(dev_alloc(&S.stamp_new, mb, 0xFF));
   TRY(dev_alloc(&S.bowned, mb, 0));
+  TRY(dev_alloc(&S.ghost_src, mb));
+  TRY(dev_alloc(&e->d_ghost_counts, kMaxRanks, 0));
+  S.ghost_counts = e->d_ghost_counts;
+  S.halo_exchange = (cfg->nranks > 1 && cfg->halo_exchange) ? 1 : 0;
   TRY(dev_alloc(&S.slab_bits, (mb + 4) & ~(size_t)3, 0));
   TRY(dev_alloc(&S.scope, mb));
   TRY(dev_alloc(&S.halo, mb));
@@ -620,10 +648,11 @@ int vm_destroy(vm_engine *e) {
   void *ptrs[] = {S.slots, S.ovf_head, S.ovf_lock, S.ovf_key, S.ovf_val, S.ovf_next, S.ovf_stamp, S.bcoord,
                   S.nbr, S.stamp_collect, S.stamp_halo, S.stamp_new, S.bowned, S.slab_bits, S.scope,
                   S.halo, S.halo_sh, S.tsdf, S.weight, S.vmask, S.tp, S.tc, S.vbirth, S.vocc, S.vclaim, S.vparam, S.vnrm, S.item_mask, S.fallback, e->d_rays,
-                  S.ctr, e->d_depth, e->d_scratch};
+                  S.ctr, e->d_depth, e->d_scratch, S.ghost_src, e->d_ghost_counts};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   free_compacted(e->comp);
+  free_pcompact(e);
   if (e->h_ctr) cudaFreeHost(e->h_ctr);
   if (e->h_frame) cudaFreeHost(e->h_frame);
   for (int k = 0; k < 2; k++) {
@@ -1681,6 +1710,248 @@ int vm_import_blocks(vm_engine *e, int64_t n, const int32_t *coords, const doubl
     if (normal) TRY(copy_sync(e, S.vnrm + i * kEV * 3, normal + k * kEV * 3, 24 * kEV, cudaMemcpyHostToDevice));
   }
   return VM_OK;
+}
+
+// ---- spatial partition ------------------------------------------------------
+// Halo-exchange frame, first half: collect + integrate the owned blocks and
+// pack the collected boundary blocks (k_pack_boundary).  Synchronous: the
+// caller needs the record count for the all-gather; a heap shortfall is
+// handled here (grow, integrate again -- k_fuse_blocks stopped at its guard,
+// so nothing was integrated twice).
+int vm_partition_frame_begin(vm_engine *e, const double *depth, int32_t h, int32_t w, int32_t depth_on_device,
+                             const vm_intrinsics *intr, const vm_pose *pose, const vm_frame_config *cfg,
+                             int64_t frame_index, uint8_t *send, int64_t send_cap, int64_t *n_send,
+                             int64_t *n_owned_collected) {
+  if (!e || !intr || !pose || !cfg || !n_send || !n_owned_collected) return set_err(VM_ERR_INPUT, "null argument");
+  if (!e->S.halo_exchange) return set_err(VM_ERR_INPUT, "engine not created in halo-exchange mode");
+  if (cfg->strategy < 0 || cfg->strategy > 2) return set_err(VM_ERR_VALUE, "unknown strategy %d", cfg->strategy);
+  if (cfg->trunc < e->S.cube_size) return set_err(VM_ERR_VALUE, "truncation band must be at least one cube");
+  NvtxRange nvtx_("vm_partition_frame_begin");
+  TRY(settle_all(e));
+  e->part_active = false;
+  const double *dd;
+  TRY(stage_depth(e, depth, h, w, depth_on_device, &dd));
+  fill_frame_host(e, dd, h, w, intr, pose);
+  FrameDev &F = *e->h_frame;
+  F.trunc = cfg->trunc;
+  F.max_range = cfg->max_range;
+  F.epsilon = cfg->epsilon;
+  F.weight_cap = cfg->weight_cap;
+  F.refine = cfg->refine;
+  F.frustum_only = cfg->frustum_only;
+  F.epoch = ++e->epoch;
+  F.frame = (int32_t)frame_index;
+  F.scope_mode = 0;
+  F.consume_fb = 0;   // (settle_all applied the pending records)
+  F.snap = nullptr;
+  F.reset_after = 0;
+  F.pub_src = nullptr; F.pub_dst = nullptr; F.pub_seq = nullptr;
+  F.self_dst = nullptr; F.self_seq = nullptr;
+  F.ghost_recv = nullptr;
+  F.ghost_max = 0;
+  F.ghost_nranks = 0;
+  TRY(ensure_rays(e, h, w));
+  F.nsteps_fixed = fixed_nsteps(e, cfg->trunc);
+  TRY(reset_call_counters(e));
+  e->ctr_clean = false;
+  e->restore_calls = false;
+  cudaStream_t st = e->stream;
+  e->frame_launches = 4;
+  if (F.nsteps_fixed <= 0) {
+    k_depth_stats<<<grid_blocks(e), 256, 0, st>>>(e->S, F);
+    e->frame_launches++;
+  }
+  launch_pdl(k_collect, e->grid_collect, kCollectThreads, st, e->S, F);
+  launch_pdl(k_fuse_blocks, e->grid_fuse, kFB, st, e->S, F, (const int32_t *)e->S.scope,
+             (const int32_t *)&e->S.ctr->ncollected, 0, (int)(F_INIT | F_INTEGRATE), 0);
+  launch_pdl(k_pack_boundary, e->grid_fuse, kFB, st, e->S, F, send, (int)std::min<int64_t>(send_cap, INT32_MAX));
+  TRY(check_launch());
+  for (int guard = 0; guard < 64; guard++) {
+    TRY(read_counters(e));
+    TRY(error_from_counters(e));
+    if (!e->h_ctr->need) break;
+    TRY(grow_blocks(e, e->h_ctr->nblocks));
+    CK(cudaMemsetAsync(&e->S.ctr->need, 0, sizeof(int32_t), st));
+    e->last_resumes++;
+    k_fuse_blocks<<<e->grid_fuse, kFB, 0, st>>>(e->S, F, (const int32_t *)e->S.scope,
+                                                (const int32_t *)&e->S.ctr->ncollected, 0, (int)(F_INIT | F_INTEGRATE), 0);
+    k_pack_boundary<<<e->grid_fuse, kFB, 0, st>>>(e->S, F, send, (int)std::min<int64_t>(send_cap, INT32_MAX));
+    e->frame_launches += 2;
+    TRY(check_launch());
+  }
+  *n_send = e->h_ctr->nsend;
+  *n_owned_collected = e->h_ctr->ncollected;
+  e->part_nc_own = e->h_ctr->ncollected;
+  e->part_frame = frame_index;
+  e->part_active = true;
+  return VM_OK;
+}
+
+int vm_partition_repack(vm_engine *e, uint8_t *send, int64_t send_cap, int64_t *n_send) {
+  if (!e || !n_send) return set_err(VM_ERR_INPUT, "null argument");
+  if (!e->part_active) return set_err(VM_ERR_INPUT, "no partition frame begun");
+  CK(cudaMemsetAsync(&e->S.ctr->nsend, 0, sizeof(int32_t), e->stream));
+  k_pack_boundary<<<e->grid_fuse, kFB, 0, e->stream>>>(e->S, *e->h_frame, send,
+                                                       (int)std::min<int64_t>(send_cap, INT32_MAX));
+  e->frame_launches++;
+  TRY(check_launch());
+  TRY(read_counters(e));
+  *n_send = e->h_ctr->nsend;
+  return VM_OK;
+}
+
+// Second half: adopt the margin records, then scope + meshing as in a fused
+// frame (k_retype_place, k_gc_normals with the counter commit).
+int vm_partition_frame_finish(vm_engine *e, const uint8_t *recv, const int32_t *counts, int32_t nranks,
+                              int64_t max_count, vm_stats *out) {
+  if (!e || !counts || (max_count > 0 && !recv)) return set_err(VM_ERR_INPUT, "null argument");
+  if (!e->part_active) return set_err(VM_ERR_INPUT, "no partition frame begun");
+  if (nranks != e->S.nranks || nranks > kMaxRanks) return set_err(VM_ERR_INPUT, "rank count mismatch");
+  NvtxRange nvtx_("vm_partition_frame_finish");
+  e->part_active = false;
+  cudaStream_t st = e->stream;
+  int64_t total = 0;
+  for (int q = 0; q < nranks; q++) {
+    if (counts[q] < 0 || counts[q] > max_count) return set_err(VM_ERR_INPUT, "bad record count");
+    if (q != e->S.rank) total += counts[q];
+  }
+  // every received record may become a new block: size the heap for all of
+  // them now, so the rest of the frame never stops for growth
+  const int64_t need = (int64_t)e->h_ctr->nblocks + total;
+  if (need > e->S.block_cap) TRY(grow_blocks(e, std::min<int64_t>(need, e->S.max_blocks)));
+  CK(cudaMemcpyAsync(e->d_ghost_counts, counts, sizeof(int32_t) * nranks, cudaMemcpyHostToDevice, st));
+  FrameDev &F = *e->h_frame;
+  F.ghost_recv = recv;
+  F.ghost_max = (int32_t)max_count;
+  F.ghost_nranks = nranks;
+  const DevState &S = e->S;
+  const long long nrec = (long long)nranks * max_count;
+  k_unpack_ghosts<<<grid_threads(e, std::max<long long>(nrec, 1), 128), 128, 0, st>>>(S, F);
+  launch_pdl(k_fuse_blocks, e->grid_fuse, kFB, st, S, F, (const int32_t *)S.scope, (const int32_t *)&S.ctr->ncollected,
+             0, (int)(F_INIT | F_GHOST), (int)e->part_nc_own);
+  launch_pdl(k_fuse_blocks, e->grid_fuse, kFB, st, S, F, (const int32_t *)S.scope, (const int32_t *)&S.ctr->ncollected,
+             0, (int)F_SCOPE, 0);
+  launch_pdl(k_retype_place, e->grid_retype, kNT, st, S, F);
+  launch_gc(e, true, S.halo, &S.ctr->nhalo, 0, (int)(G_GC | G_NORMALS | G_COMMIT | G_REQUIRE_ITEMS | G_SHARDED));
+  e->frame_launches += 5;
+  TRY(check_launch());
+  TRY(read_counters(e));
+  TRY(error_from_counters(e));
+  if (e->h_ctr->need) return set_err(VM_ERR_CUDA, "halo exchange: block heap not pre-sized");
+  e->ev_rec[e->ev == e->evs[1]] = false;
+  fill_stats(e, e->part_frame, out ? out : &e->settled);
+  if (out) out->kernel_launches = e->frame_launches;
+  F.ghost_recv = nullptr;
+  return VM_OK;
+}
+
+// Distributed compaction, per rank: sort the owned blocks, count their
+// vertices / triangles and slot occupancy (k_compact_count over the owned list).
+int vm_partition_compact_begin(vm_engine *e, int64_t *n_owned) {
+  if (!e || !n_owned) return set_err(VM_ERR_INPUT, "null argument");
+  NvtxRange nvtx_("vm_partition_compact_begin");
+  TRY(settle_all(e));
+  TRY(read_counters(e));
+  free_pcompact(e);
+  auto &p = e->pc;
+  const int nb = e->h_ctr->nblocks;
+  const int nown = (int)(e->S.nranks > 1 ? e->h_ctr->nblocks_owned : nb);
+  p.nb = nb;
+  p.nown = nown;
+  *n_owned = nown;
+  if (nb == 0) return VM_OK;
+  cudaStream_t st = e->stream;
+  CK(cudaMalloc(&p.keys_in, 8ull * nb));
+  CK(cudaMalloc(&p.keys_out, 8ull * nb));
+  CK(cudaMalloc(&p.vals, 4ull * nb));
+  CK(cudaMalloc(&p.order, 4ull * nb));
+  CK(cudaMalloc(&p.vcnt, 4ull * (nb + 1)));
+  CK(cudaMalloc(&p.tcnt, 4ull * (nb + 1)));
+  CK(cudaMalloc(&p.occ_bits, 4ull * 48 * nb));
+  CK(cudaMalloc(&p.occ_pre, 2ull * 48 * nb));
+  k_owned_block_keys<<<grid_threads(e, nb, 256), 256, 0, st>>>(e->S, nb, p.keys_in, p.vals);
+  size_t tmp_bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, p.keys_in, p.keys_out, p.vals, p.order, nb, 0, 64, st);
+  CK(cudaMalloc(&p.tmp, tmp_bytes + 16));
+  cub::DeviceRadixSort::SortPairs(p.tmp, tmp_bytes, p.keys_in, p.keys_out, p.vals, p.order, nb, 0, 64, st);
+  if (nown) k_compact_count<<<grid_blocks(e), kThreadsCube, 0, st>>>(e->S, p.order, nown, p.vcnt, p.tcnt, p.occ_bits, p.occ_pre);
+  TRY(check_launch());
+  CK(cudaStreamSynchronize(st));
+  return VM_OK;
+}
+
+// the owned blocks' occupancy words in sorted order (k_compact_count wrote
+// them by block index)
+__global__ static void k_gather_occ(const int32_t *order, int n, const uint32_t *occ_by_blk, uint32_t *out) {
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < (long long)n * 48;
+       q += (long long)gridDim.x * blockDim.x)
+    out[q] = occ_by_blk[(size_t)order[q / 48] * 48 + q % 48];
+}
+
+int vm_partition_compact_meta(vm_engine *e, uint64_t *keys, int32_t *vcnt, int32_t *tcnt, uint32_t *occ) {
+  if (!e) return set_err(VM_ERR_INPUT, "null engine");
+  auto &p = e->pc;
+  if (p.nown == 0) return VM_OK;
+  if (keys) TRY(copy_sync(e, keys, p.keys_out, 8ull * p.nown, cudaMemcpyDeviceToHost));
+  if (vcnt) TRY(copy_sync(e, vcnt, p.vcnt, 4ull * p.nown, cudaMemcpyDeviceToHost));
+  if (tcnt) TRY(copy_sync(e, tcnt, p.tcnt, 4ull * p.nown, cudaMemcpyDeviceToHost));
+  if (occ) {
+    uint32_t *tmp;
+    CK(cudaMalloc(&tmp, 4ull * 48 * p.nown));
+    k_gather_occ<<<grid_threads(e, (long long)p.nown * 48, 256), 256, 0, e->stream>>>(p.order, p.nown, p.occ_bits, tmp);
+    TRY(check_launch());
+    const int rc = copy_sync(e, occ, tmp, 4ull * 48 * p.nown, cudaMemcpyDeviceToHost);
+    cudaFree(tmp);
+    TRY(rc);
+  }
+  return VM_OK;
+}
+
+__global__ static void k_pbase(const int32_t *order, int n, const int32_t *my_global, const int64_t *vbase,
+                               int32_t *vbase_by_blk) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    vbase_by_blk[order[i]] = (int32_t)vbase[my_global[i]];
+}
+
+int vm_partition_compact_fill(vm_engine *e, const uint64_t *gkeys, const int64_t *vbase, const int64_t *tbase,
+                              const uint32_t *gocc, const int32_t *gocc_pre, int64_t n_global,
+                              const int32_t *my_global, int64_t current_frame, double *pos, double *nrm,
+                              int64_t *ages, int32_t *idx) {
+  if (!e) return set_err(VM_ERR_INPUT, "null engine");
+  NvtxRange nvtx_("vm_partition_compact_fill");
+  auto &p = e->pc;
+  if (p.nown == 0 || n_global == 0) return VM_OK;
+  if (!gkeys || !vbase || !tbase || !gocc || !gocc_pre || !my_global) return set_err(VM_ERR_INPUT, "null argument");
+  cudaStream_t st = e->stream;
+  const size_t ng = (size_t)n_global;
+  char *buf;
+  const size_t o_keys = 0, o_vb = o_keys + 8 * ng, o_tb = o_vb + 8 * ng, o_occ = o_tb + 8 * ng,
+               o_pre = o_occ + 4 * 48 * ng, o_my = o_pre + 4 * 48 * ng, o_vbb = o_my + 4 * (size_t)p.nown,
+               total = o_vbb + 4 * (size_t)p.nb + 64;
+  CK(cudaMalloc(&buf, total));
+  CK(cudaMemcpyAsync(buf + o_keys, gkeys, 8 * ng, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(buf + o_vb, vbase, 8 * ng, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(buf + o_tb, tbase, 8 * ng, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(buf + o_occ, gocc, 4 * 48 * ng, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(buf + o_pre, gocc_pre, 4 * 48 * ng, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(buf + o_my, my_global, 4 * (size_t)p.nown, cudaMemcpyHostToDevice, st));
+  int32_t *vbb = (int32_t *)(buf + o_vbb);
+  k_pbase<<<grid_threads(e, p.nown, 256), 256, 0, st>>>(p.order, p.nown, (const int32_t *)(buf + o_my),
+                                                        (const int64_t *)(buf + o_vb), vbb);
+  TRY(reset_call_counters(e));
+  k_compact_vertices<<<grid_blocks(e), kThreadsCube, 0, st>>>(e->S, p.order, p.nown, p.occ_bits, p.occ_pre, vbb, pos,
+                                                              nrm, (long long *)ages, (long long)current_frame,
+                                                              nullptr);
+  k_pcompact_triangles<<<grid_blocks(e), kThreadsCube, 0, st>>>(
+      e->S, p.order, p.nown, (const int32_t *)(buf + o_my), (const unsigned long long *)(buf + o_keys),
+      (int)n_global, (const int64_t *)(buf + o_vb), (const int64_t *)(buf + o_tb), (const uint32_t *)(buf + o_occ),
+      (const int32_t *)(buf + o_pre), idx);
+  const int lrc = check_launch();
+  CK(cudaStreamSynchronize(st));
+  cudaFree(buf);
+  TRY(lrc);
+  TRY(read_counters(e));
+  return error_from_counters(e);
 }
 
 // Engine.audit (engine.py:187-230).  With slot-resident vertices and

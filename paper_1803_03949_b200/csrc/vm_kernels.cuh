@@ -23,7 +23,9 @@ namespace vm {
 
 constexpr int kThreadsCube = 512;   // one thread per cube of a block
 
-enum { F_INIT = 1, F_INTEGRATE = 2, F_SCOPE = 4, F_HALO = 8 };
+enum { F_INIT = 1, F_INTEGRATE = 2, F_SCOPE = 4, F_HALO = 8, F_GHOST = 16 };
+// halo-exchange record: coordinate, then the block's 512 tsdf and 512 weights
+constexpr size_t kGhostRec = 16 + 8 * 512 + 4 * 512;
 enum { G_GC = 1, G_NORMALS = 2, G_COMMIT = 4, G_REQUIRE_ITEMS = 8, G_SHARDED = 16 };
 
 // error and need are adjacent: one 8-byte load
@@ -614,16 +616,19 @@ __global__ void __launch_bounds__(kThreadsCube) k_init_blocks(DevState S, int ep
 //              created in this launch are still being written).
 constexpr int kFB = 128;   // threads per CTA of k_fuse_blocks (4 corners each)
 
+// F_GHOST (halo exchange): items [base, n) are margin blocks received from
+// their owners; their samples are copied from the records instead of integrated.
 __global__ void __launch_bounds__(kFB, 6) k_fuse_blocks(DevState S, const FrameDev F,
                                                      const int32_t *__restrict__ list,
                                                      const int32_t *__restrict__ count_ptr,
-                                                     int count_const, int flags) {
+                                                     int count_const, int flags, int base = 0) {
   cudaGridDependencySynchronize();   // PDL: wait for the previous kernel of the frame
   trace_at(S, TK_FUSE, 0);
   trace_span(S, 1, F.frame, false);
   __shared__ int s_pro[5];
   const int list_cap = count_ptr ? S.max_blocks : count_const;
-  read_prologue(S, s_pro, count_ptr, nullptr, nullptr, (int)blockIdx.x < list_cap ? list + blockIdx.x : nullptr);
+  read_prologue(S, s_pro, count_ptr, nullptr, nullptr,
+                base + (int)blockIdx.x < list_cap ? list + base + blockIdx.x : nullptr);
   if (s_pro[0]) return;
   const int n = count_ptr ? s_pro[1] : count_const;
   if (F.consume_fb && blockIdx.x == 0 && threadIdx.x == 0) S.ctr->fb_pending = 0;   // (k_collect applied them)
@@ -633,9 +638,9 @@ __global__ void __launch_bounds__(kFB, 6) k_fuse_blocks(DevState S, const FrameD
   // neighbour probe of this thread: 7 lanes of each warp, directions 0..26
   const int pl = t & 31, pdir = (t >> 5) * 7 + pl;
   const bool prober = pl < 7 && pdir < 27;
-  for (int i = blockIdx.x; i < n; i += gridDim.x, nth++) {
+  for (int i = base + blockIdx.x; i < n; i += gridDim.x, nth++) {
     trace_item(S, TK_FUSE, nth, 0);
-    const int b = i == (int)blockIdx.x && s_pro[4] != -1 ? s_pro[4] : __ldcg(list + i);
+    const int b = i == base + (int)blockIdx.x && s_pro[4] != -1 ? s_pro[4] : __ldcg(list + i);
     if (b < 0) continue;
     const int4 c = __ldcg(S.bcoord + b);
     const bool fresh = (flags & F_INIT) && __ldcg(S.stamp_new + b) == F.epoch;
@@ -710,6 +715,22 @@ __global__ void __launch_bounds__(kFB, 6) k_fuse_blocks(DevState S, const FrameD
         const unsigned old = atomicOr((unsigned *)(S.slab_bits + (nb & ~3)), (1u << (o - 1)) << sh);
         if (((old >> sh) & 0xFF) == 0) S.scope[n + atomicAdd(&S.ctr->nslab, 1)] = nb;   // (n = collected)
       }
+    }
+    if (flags & F_GHOST) {   // the owner's samples, as integrated there (bit-identical)
+      const uint8_t *rec = F.ghost_recv + (size_t)__ldcg(S.ghost_src + i) * kGhostRec;
+      const double *gt = reinterpret_cast<const double *>(rec + 16);
+      const int32_t *gw = reinterpret_cast<const int32_t *>(rec + 16 + 8 * kNC);
+#pragma unroll
+      for (int j = 0; j < kNC / kFB; j++) {
+        const int ci = t + j * kFB;
+        const double tv = __ldcg(gt + ci);
+        const int32_t wv = __ldcg(gw + ci);
+        S.tsdf[(size_t)b * kNC + ci] = tv;
+        S.weight[(size_t)b * kNC + ci] = wv;
+        const unsigned vb = __ballot_sync(0xffffffffu, wv > 0);
+        if ((threadIdx.x & 31) == 0) S.vmask[(size_t)b * (kNC / 32) + (ci >> 5)] = vb;
+      }
+      continue;
     }
     if (!(flags & F_INTEGRATE)) continue;
 #pragma unroll

@@ -50,6 +50,7 @@ class RunConfig:
     rank: int = 0
     nranks: int = 1
     tile_blocks: int = 8
+    halo_exchange: bool = False          # margin blocks received from their owners (partition.py)
 
     def resolved(self) -> "RunConfig":
         cfg = replace(self)
@@ -152,7 +153,8 @@ class Engine:
                                   max_vertices=c.max_vertices, initial_blocks=c.block_capacity,
                                   initial_vertices=c.vertex_capacity,
                                   initial_triangles=c.triangle_capacity, rank=c.rank,
-                                  nranks=c.nranks, tile_blocks=c.tile_blocks)
+                                  nranks=c.nranks, tile_blocks=c.tile_blocks,
+                                  halo_exchange=c.halo_exchange)
         self.frame_index = 0
         self.stats: list[StatsRow] = []
         self.device_stats: list[dict] = []

@@ -130,7 +130,7 @@ class SpatialStore:
     def __init__(self, cube_size: float, table_size: int = DEFAULT_TABLE_SIZE,
                  max_vertices: Optional[int] = None, initial_blocks: int = 0,
                  initial_vertices: int = 0, initial_triangles: int = 0, rank: int = 0,
-                 nranks: int = 1, tile_blocks: int = 8):
+                 nranks: int = 1, tile_blocks: int = 8, halo_exchange: bool = False):
         if cube_size <= 0:
             raise ValueError("cube_size must be positive")
         self.cube_size = float(cube_size)
@@ -141,7 +141,7 @@ class SpatialStore:
         self.rank, self.nranks = int(rank), int(nranks)
         cfg = _lib.StoreConfig(self.cube_size, self.table_size, int(max_vertices or 0),
                                int(initial_blocks), int(initial_vertices), int(initial_triangles),
-                               self.rank, self.nranks, int(tile_blocks), 0)
+                               self.rank, self.nranks, int(tile_blocks), int(bool(halo_exchange)))
         h = C.c_void_p()
         _lib.check(L.vm_create(C.byref(cfg), C.byref(h)))
         self._h = h

@@ -81,3 +81,101 @@ def test_partitioned_room_prefix_matches_single_engine():
         assert np.array_equal(mesh.positions, ref.positions)
         assert np.array_equal(mesh.ages, ref.ages)
         assert np.allclose(mesh.normals, ref.normals, rtol=0, atol=NORMAL_ATOL)
+
+
+# ---- halo exchange + distributed compaction (in-process ranks) -------------
+from partition_sim import fuse_all, rank_engines  # noqa: E402
+
+
+def _intr_of(g):
+    from paper_1803_03949_b200 import Intrinsics
+    i6 = g["intr6"]
+    return Intrinsics(float(i6[0]), float(i6[1]), float(i6[2]), float(i6[3]), int(i6[4]), int(i6[5]))
+
+
+@pytest.mark.parametrize("name", ENGINE_SCENES)
+@pytest.mark.parametrize("halo", ["margin", "exchange"])
+@pytest.mark.parametrize("nranks,tile_blocks", [(2, 1), (3, 2), (4, 8)])
+def test_distributed_compaction_and_halo_exchange_match_reference_golden(name, halo, nranks, tile_blocks):
+    """Halo exchange (owners integrate; boundary blocks all-gathered and
+    adopted by the ranks whose margin they are in, before meshing) and the
+    distributed compaction (owned-block metadata merged by key, each rank
+    fills its global ranges, ranges summed): rows and mesh equal the
+    reference's golden output bit for bit."""
+    from paper_1803_03949_b200.partition import StatsCombiner, compact_local, sum_stats
+    g = load_golden(name)
+    engines = rank_engines(cfg_from_golden(g), _intr_of(g), nranks, tile_blocks, halo)
+    comb = StatsCombiner()
+    log = []
+    for i in range(len(g["depth"])):
+        rows = fuse_all(engines, g["depth"][i], _pose(g, i), halo, log)
+        c = comb.combine(sum_stats(rows))
+        got = (i, c["blocks_active"], c["vertices_live"], c["triangles_live"],
+               c["vertices_allocated_total"], c["vertices_recycled_total"], c["irregular_cube_count"])
+        assert got == tuple(g["stats"][i]), (name, i)
+    if halo == "exchange" and tile_blocks == 1:
+        assert sum(map(sum, log)) > 0                  # records actually crossed ranks
+    _check_mesh(compact_local([e.store for e in engines], engines[0].frame_index), g)
+
+
+def test_halo_exchange_integrates_owned_blocks_only():
+    """In exchange mode a rank's band walk collects only its owned blocks and
+    the margin arrives by the exchange: the collected set (owned + adopted
+    margin) equals margin mode's, rows and the mesh are identical, and
+    records did cross ranks."""
+    from paper_1803_03949_b200.synth import camera_pose, config_spec, render_depth
+    spec, cfg = config_spec("C2")
+    spec.width, spec.height, spec.fx, spec.fy = 320, 240, 262.5, 262.5
+    intr = spec.intrinsics()
+    m = rank_engines(cfg, intr, 2, 8, "margin")
+    x = rank_engines(cfg, intr, 2, 8, "exchange")
+    log = []
+    for i in range(0, 12, 3):
+        pose = camera_pose(spec, i)
+        d = render_depth(spec, pose)
+        rm = fuse_all(m, d, pose, "margin")
+        rx = fuse_all(x, d, pose, "exchange", log)
+        for a, b in zip(rm, rx):
+            assert b["collected_blocks"] == a["collected_blocks"]      # owned + adopted margin
+            for k in ("blocks_active", "vertices_live", "triangles_live", "irregular_cube_count"):
+                assert a[k] == b[k], k
+    assert all(sum(c) > 0 for c in log)
+    from paper_1803_03949_b200.partition import compact_local
+    ma = compact_local([e.store for e in m], m[0].frame_index)
+    mb = compact_local([e.store for e in x], x[0].frame_index)
+    assert np.array_equal(ma.indices, mb.indices) and np.array_equal(ma.positions, mb.positions)
+    assert np.array_equal(ma.normals, mb.normals)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("halo", ["margin", "exchange"])
+def test_c2_halo_modes_full_resolution_match_oracle(halo):
+    """C2 (640x480, 8 mm), 2 and 4 ranks, 16 frames: rows every frame and the
+    distributed compaction against the CPU oracle."""
+    import torch
+    from oracle.oracle import OracleEngine
+    from oracle.parity import NORMAL_ATOL, stats_tuple_oracle
+    from paper_1803_03949_b200.partition import StatsCombiner, compact_local, sum_stats
+    from paper_1803_03949_b200.synth import camera_pose, config_spec, render_depth_torch
+    spec, cfg = config_spec("C2")
+    intr = spec.intrinsics()
+    groups = {n: rank_engines(cfg, intr, n, 8, halo) for n in (2, 4)}
+    combs = {n: StatsCombiner() for n in groups}
+    ora = OracleEngine(cfg, (intr.fx, intr.fy, intr.cx, intr.cy, intr.width, intr.height))
+    for i in range(16):
+        pose = camera_pose(spec, i)
+        d = render_depth_torch(spec, pose)
+        torch.cuda.synchronize()
+        ref = stats_tuple_oracle(ora.fuse_frame(d.cpu().numpy(), pose.rotation, pose.translation))
+        for n, engines in groups.items():
+            c = combs[n].combine(sum_stats(fuse_all(engines, d, pose, halo)))
+            got = (i, c["blocks_active"], c["vertices_live"], c["triangles_live"],
+                   c["vertices_allocated_total"], c["vertices_recycled_total"], c["irregular_cube_count"])
+            assert got == ref, (n, i)
+    pos, nrm, ages, idx = ora.compact()
+    for n, engines in groups.items():
+        mesh = compact_local([e.store for e in engines], 16)
+        assert np.array_equal(mesh.indices, idx), n
+        assert np.array_equal(mesh.positions, pos), n
+        assert np.array_equal(mesh.ages, ages), n
+        assert np.allclose(mesh.normals, nrm, rtol=0, atol=NORMAL_ATOL), n
