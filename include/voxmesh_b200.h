@@ -77,7 +77,11 @@ typedef struct {
   int32_t refine;        /* RefineParams.enabled (refine.py:55-60) */
   int32_t frustum_only;  /* engine.py:135-138 */
   int32_t strategy;      /* VM_STRATEGY_* */
-  int32_t reserved;
+  int32_t block_gc_age;  /* > 0: opt-in block GC -- every block_gc_age frames, evict the blocks
+                          * not collected for block_gc_age frames that hold no vertex and no
+                          * observed sample (all weights 0); the mesh is unchanged, only
+                          * blocks_active drops.  0 = off (the reference never frees a block,
+                          * store.py:14) */
 } vm_frame_config;
 
 /* StatsRow non-timing columns (engine.py:71-86) + per-frame unit counts used
@@ -109,6 +113,7 @@ typedef struct {
   int64_t refined_cubes;
   int64_t resumes;        /* arena growths that required a resume this frame */
   int64_t kernel_launches;/* kernels this library launched for the frame */
+  int64_t blocks_evicted; /* block GC: blocks evicted so far (0 with block GC off) */
   double device_ms;       /* device time of the frame (CUDA events) */
   double fusion_ms;       /* collect + integrate (engine.py:127-132 split) */
   double meshing_ms;      /* scope .. normals (engine.py:134-144 split) */

@@ -47,7 +47,7 @@ class PoseC(C.Structure):
 class FrameConfig(C.Structure):
     _fields_ = [("trunc", C.c_double), ("max_range", C.c_double), ("epsilon", C.c_double),
                 ("weight_cap", C.c_int64), ("refine", C.c_int32), ("frustum_only", C.c_int32),
-                ("strategy", C.c_int32), ("reserved", C.c_int32)]
+                ("strategy", C.c_int32), ("block_gc_age", C.c_int32)]
 
 
 STATS_FIELDS = ("frame", "blocks_active", "vertices_live", "triangles_live",
@@ -55,7 +55,7 @@ STATS_FIELDS = ("frame", "blocks_active", "vertices_live", "triangles_live",
                 "valid_pixels", "nsteps", "collected_blocks", "new_blocks", "scope_blocks",
                 "halo_blocks", "active_cubes", "edge_placements", "new_vertices", "changed_cubes",
                 "triangles_freed", "triangles_allocated", "vertices_freed", "normals_computed",
-                "fallback_normals", "refined_cubes", "resumes", "kernel_launches")
+                "fallback_normals", "refined_cubes", "resumes", "kernel_launches", "blocks_evicted")
 
 
 class Stats(C.Structure):

@@ -30,6 +30,7 @@ constexpr int kNC = 512;       // cubes per block
 constexpr int kSlotsPerBucket = 8;
 constexpr int kEV = kNC * 3;   // edge-vertex slots per block
 constexpr long long kEmptyKey = -1LL;
+constexpr int kEvicted = -3;   // hash value of a key whose block the block GC evicted (key kept)
 
 enum { ERR_NONE = 0, ERR_CAPACITY = 1, ERR_CONSISTENCY = 2 };
 
@@ -59,7 +60,8 @@ struct alignas(16) Counters {
   int64_t nblocks_owned; // blocks this rank owns (== nblocks unless partitioned)
   int64_t err_info[4];
   int32_t fb_pending;    // face-normal fallback records of the last frame not yet applied
-  int32_t pad0;
+  int32_t nfree;         // block GC: evicted block indices on the free list
+  int64_t evicted_total; // block GC: blocks evicted so far
   // ---- per call ----------------------------------------------------------
   int32_t nvalid;
   int32_t nsteps;
@@ -110,6 +112,7 @@ struct FrameDev {
   int32_t frame;        // frame index (vertex birth)
   int32_t scope_mode;   // 0: collected + slabs (device scope); 1: explicit items
   int32_t nsteps_fixed; // > 0: band step count fixed by the intrinsics (k_depth_stats skipped)
+  int32_t block_gc_age; // > 0: opt-in block GC (k_block_gc before this frame when frame % age == 0)
   int32_t consume_fb;   // fuse_frame: k_collect applies the previous frame's fallback records
   int32_t reset_after;  // k_gc_normals' commit clears the per-call counters after its snapshot
   Counters *snap;       // non-null: k_gc_normals' commit copies the counter block here (device)
@@ -190,6 +193,8 @@ struct DevState {
   int32_t halo_exchange;
   uint8_t *bowned;      // [max_blocks] block owned by this rank
   int32_t *ghost_src;   // [max_blocks] scope position -> received record (halo exchange)
+  int32_t *last_frame;  // [max_blocks] frame in which the block was last collected (block GC)
+  int32_t *free_list;   // [max_blocks] evicted block indices (block GC)
   const int32_t *ghost_counts;   // [nranks] records per rank of the current exchange
   Counters *ctr;
   unsigned long long *trace;   // per-CTA phase timestamps (vm_set_trace), null = off
@@ -341,11 +346,16 @@ __device__ HashRef hash_find_ref(const DevState &S, int x, int y, int z) {
   }
   if (hit >= 0) {
     if (idx == -1) idx = wait_val(&kb[hit].val);
+    if (idx == kEvicted) return {-1, -1, nullptr};   // (an evicted block reads as absent)
     return {idx, stamp, &kb[hit].pad};
   }
   if (stop) return {-1, -1, nullptr};
   for (int e = ld_vol(S.ovf_head + b); e >= 0; e = ld_vol(S.ovf_next + e))
-    if (ld_vol(S.ovf_key + e) == key) return {ld_vol(S.ovf_val + e), ld_vol(S.ovf_stamp + e), S.ovf_stamp + e};
+    if (ld_vol(S.ovf_key + e) == key) {
+      const int v = ld_vol(S.ovf_val + e);
+      if (v == kEvicted) return {-1, -1, nullptr};
+      return {v, ld_vol(S.ovf_stamp + e), S.ovf_stamp + e};
+    }
   return {-1, -1, nullptr};
 }
 
@@ -358,13 +368,17 @@ __device__ int hash_find(const DevState &S, int x, int y, int z) {
   for (int i = 0; i < kSlotsPerBucket; i++) {
     const long long k = ld_vol(&kb[i].key);
     if (k == key) {
-      const int v = ld_vol(&kb[i].val);
-      return v != -1 ? v : wait_val(&kb[i].val);
+      int v = ld_vol(&kb[i].val);
+      if (v == -1) v = wait_val(&kb[i].val);
+      return v == kEvicted ? -1 : v;
     }
     if (k == kEmptyKey) return -1;  // slots fill in prefix order
   }
   for (int e = ld_vol(S.ovf_head + b); e >= 0; e = ld_vol(S.ovf_next + e))
-    if (ld_vol(S.ovf_key + e) == key) return ld_vol(S.ovf_val + e);
+    if (ld_vol(S.ovf_key + e) == key) {
+      const int v = ld_vol(S.ovf_val + e);
+      return v == kEvicted ? -1 : v;
+    }
   return -1;
 }
 
@@ -411,10 +425,21 @@ __device__ __forceinline__ bool block_in_margin(const DevState &S, int x, int y,
 
 // allocate the next block index; CapacityError at 2*n >= table_size (store.py:304-306)
 __device__ int alloc_block(const DevState &S, int x, int y, int z, int epoch) {
-  int idx = atomicAdd(&S.ctr->nblocks, 1);
-  if (2LL * idx >= S.table_size) {
-    set_error(S, ERR_CAPACITY, idx, S.table_size, 1, epoch);
-    return -2;
+  // block GC: reuse an evicted block's index first (its storage is initialised
+  // as a fresh block's by k_fuse_blocks).  Pops only race with pops (pushes
+  // happen in k_block_gc alone): a pop that finds the list empty undoes itself.
+  int idx = -1;
+  if (ld_vol(&S.ctr->nfree) > 0) {
+    const int k = atomicSub(&S.ctr->nfree, 1);
+    if (k > 0) idx = __ldcg(S.free_list + (k - 1));
+    else atomicAdd(&S.ctr->nfree, 1);
+  }
+  if (idx < 0) {
+    idx = atomicAdd(&S.ctr->nblocks, 1);
+    if (2LL * idx >= S.table_size) {
+      set_error(S, ERR_CAPACITY, idx, S.table_size, 1, epoch);
+      return -2;
+    }
   }
   // (latched with the call's epoch: a k_collect CTA stops only for a flag left
   // by an EARLIER frame, never for one a sibling CTA of its own frame just set)
@@ -456,7 +481,15 @@ __device__ HashRef hash_insert_ref(const DevState &S, int x, int y, int z, int e
         return {idx, ld_vol(&kb[i].pad), &kb[i].pad};
       }
     }
-    if (k == key) return {wait_val(&kb[i].val), ld_vol(&kb[i].pad), &kb[i].pad};
+    if (k == key) {
+      // an evicted block's key: the first re-inserter allocates a new block
+      if (ld_vol(&kb[i].val) == kEvicted && atomicCAS(&kb[i].val, kEvicted, -1) == kEvicted) {
+        const int idx = alloc_block(S, x, y, z, epoch);
+        *(volatile int32_t *)&kb[i].val = idx;
+        return {idx, ld_vol(&kb[i].pad), &kb[i].pad};
+      }
+      return {wait_val(&kb[i].val), ld_vol(&kb[i].pad), &kb[i].pad};
+    }
   }
   int32_t *sp = nullptr;
   int found = -1;
@@ -465,7 +498,15 @@ __device__ HashRef hash_insert_ref(const DevState &S, int x, int y, int z, int e
     if (atomicCAS(S.ovf_lock + b, 0, 1) == 0) {
       __threadfence();
       for (int e = ld_vol(S.ovf_head + b); e >= 0; e = ld_vol(S.ovf_next + e))
-        if (ld_vol(S.ovf_key + e) == key) { found = ld_vol(S.ovf_val + e); sp = S.ovf_stamp + e; break; }
+        if (ld_vol(S.ovf_key + e) == key) {
+          sp = S.ovf_stamp + e;
+          found = ld_vol(S.ovf_val + e);
+          if (found == kEvicted) {   // (under the bucket's lock)
+            found = alloc_block(S, x, y, z, epoch);
+            S.ovf_val[e] = found;
+          }
+          break;
+        }
       if (found == -1) {
         int e = atomicAdd(&S.ctr->ovf_count, 1);
         if (e >= S.ovf_cap) {

@@ -600,6 +600,8 @@ int vm_create(const vm_store_config *cfg, vm_engine **out) {
   TRY(dev_alloc(&S.stamp_new, mb, 0xFF));
   TRY(dev_alloc(&S.bowned, mb, 0));
   TRY(dev_alloc(&S.ghost_src, mb));
+  TRY(dev_alloc(&S.last_frame, mb, 0));
+  TRY(dev_alloc(&S.free_list, mb));
   TRY(dev_alloc(&e->d_ghost_counts, kMaxRanks, 0));
   S.ghost_counts = e->d_ghost_counts;
   S.halo_exchange = (cfg->nranks > 1 && cfg->halo_exchange) ? 1 : 0;
@@ -648,7 +650,7 @@ int vm_destroy(vm_engine *e) {
   void *ptrs[] = {S.slots, S.ovf_head, S.ovf_lock, S.ovf_key, S.ovf_val, S.ovf_next, S.ovf_stamp, S.bcoord,
                   S.nbr, S.stamp_collect, S.stamp_halo, S.stamp_new, S.bowned, S.slab_bits, S.scope,
                   S.halo, S.halo_sh, S.tsdf, S.weight, S.vmask, S.tp, S.tc, S.vbirth, S.vocc, S.vclaim, S.vparam, S.vnrm, S.item_mask, S.fallback, e->d_rays,
-                  S.ctr, e->d_depth, e->d_scratch, S.ghost_src, e->d_ghost_counts};
+                  S.ctr, e->d_depth, e->d_scratch, S.ghost_src, e->d_ghost_counts, S.last_frame, S.free_list};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   free_compacted(e->comp);
@@ -734,7 +736,8 @@ static void fill_stats(vm_engine *e, int64_t frame, vm_stats *out) {
   const Counters &c = *e->h_ctr;
   memset(out, 0, sizeof *out);
   out->frame = frame;
-  out->blocks_active = e->S.nranks > 1 ? c.nblocks_owned : c.nblocks;
+  out->blocks_active = e->S.nranks > 1 ? c.nblocks_owned : c.nblocks - c.nfree;
+  out->blocks_evicted = c.evicted_total;
   out->vertices_live = c.v_live;
   out->triangles_live = c.t_live;
   out->vertices_allocated_total = c.v_count;
@@ -859,6 +862,11 @@ static int launch_frame(vm_engine *e, int slot) {
   cudaStream_t st = e->stream;
   rec(e, PH_DEPTH);
   e->frame_launches = 4;   // collect, fuse, retype, gc (+ depth stats)
+  if (F.block_gc_age > 0 && F.frame > 0 && F.frame % F.block_gc_age == 0) {
+    // opt-in block GC, before the frame allocates (its pops reuse the indices)
+    k_block_gc<<<e->sm_count * 8, 256, 0, st>>>(e->S, F.frame, F.block_gc_age);
+    e->frame_launches++;
+  }
   FrameDev Fc = F;   // (collect's copy: a raw frame converted by k_depth_stats is f64 now)
   if (F.nsteps_fixed <= 0) {
     k_depth_stats<<<grid_blocks(e), 256, 0, st>>>(e->S, F);
@@ -906,6 +914,7 @@ int vm_fuse_frame_enqueue(vm_engine *e, const double *depth, int32_t h, int32_t 
   F.scope_mode = 0;
   TRY(ensure_rays(e, h, w));
   F.nsteps_fixed = fixed_nsteps(e, cfg->trunc);
+  F.block_gc_age = cfg->block_gc_age > 0 ? cfg->block_gc_age : 0;
   F.consume_fb = 1;   // k_collect applies the previous frame's fallback records
   if (e->raw_next) {   // raw u16 frame: the first pixel kernel fills the f64 depth from it
     F.raw = e->raw_next;
@@ -1000,7 +1009,11 @@ static int settle_slot(vm_engine *e, int slot, bool succ) {
       e->ev = e->evs[slot ^ 1];
       e->frame_launches = launched;
     }
-    if (rc == VM_OK) e->settled.kernel_launches = 4 + (e->f_saved[slot].nsteps_fixed <= 0) + 3 * e->last_resumes;
+    if (rc == VM_OK) {
+      const FrameDev &Fs = e->f_saved[slot];
+      e->settled.kernel_launches = 4 + (Fs.nsteps_fixed <= 0) + 3 * e->last_resumes +
+                                   (Fs.block_gc_age > 0 && Fs.frame > 0 && Fs.frame % Fs.block_gc_age == 0);
+    }
   }
   return rc;
 }
@@ -1486,7 +1499,7 @@ int vm_counters(vm_engine *e, vm_counter_set *out) {
   TRY(settle_all(e));
   TRY(read_counters(e));
   const Counters &c = *e->h_ctr;
-  out->block_count = e->S.nranks > 1 ? c.nblocks_owned : c.nblocks;
+  out->block_count = e->S.nranks > 1 ? c.nblocks_owned : c.nblocks - c.nfree;
   out->block_allocations = out->block_count;
   out->vertex_count = c.v_count;
   out->vertex_free = c.v_count - c.v_live;
@@ -1502,15 +1515,49 @@ int vm_counters(vm_engine *e, vm_counter_set *out) {
   return VM_OK;
 }
 
+// host copy of `count` rows of `row_bytes` each from a device array, keeping
+// only the rows in `sel` (block GC: evicted blocks are not part of the store)
+static int copy_rows(vm_engine *e, void *dst, const void *src, size_t row_bytes, int64_t count,
+                     const std::vector<int> &sel) {
+  if ((int64_t)sel.size() == count) return copy_sync(e, dst, src, row_bytes * count, cudaMemcpyDeviceToHost);
+  std::vector<char> tmp(row_bytes * count);
+  TRY(copy_sync(e, tmp.data(), src, row_bytes * count, cudaMemcpyDeviceToHost));
+  for (size_t k = 0; k < sel.size(); k++) memcpy((char *)dst + k * row_bytes, tmp.data() + sel[k] * row_bytes, row_bytes);
+  return VM_OK;
+}
+
 int vm_snapshot_blocks(vm_engine *e, int64_t n, int32_t *coords, double *tsdf, int32_t *weight, uint8_t *tp,
                        uint8_t *tc, int32_t *ev, int32_t *tri) {
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
   TRY(settle_all(e));
   TRY(read_counters(e));
-  if (n != e->h_ctr->nblocks)
-    return set_err(VM_ERR_INPUT, "snapshot size %lld != block count %d", (long long)n, e->h_ctr->nblocks);
+  const int64_t nb = e->h_ctr->nblocks, live = nb - e->h_ctr->nfree;
+  if (n != live)
+    return set_err(VM_ERR_INPUT, "snapshot size %lld != block count %lld", (long long)n, (long long)live);
   if (n == 0) return VM_OK;
   const DevState &S = e->S;
+  if (live != nb) {   // evicted blocks (block GC) are skipped
+    std::vector<int4> bc(nb);
+    TRY(copy_sync(e, bc.data(), S.bcoord, sizeof(int4) * nb, cudaMemcpyDeviceToHost));
+    std::vector<int> sel;
+    for (int64_t i = 0; i < nb; i++)
+      if (bc[i].w == 0) sel.push_back((int)i);
+    if ((int64_t)sel.size() != live) return set_err(VM_ERR_CONSISTENCY, "evicted block count mismatch");
+    if (coords)
+      for (size_t k = 0; k < sel.size(); k++) {
+        coords[3 * k] = bc[sel[k]].x; coords[3 * k + 1] = bc[sel[k]].y; coords[3 * k + 2] = bc[sel[k]].z;
+      }
+    if (tsdf) TRY(copy_rows(e, tsdf, S.tsdf, 8 * kNC, nb, sel));
+    if (weight) TRY(copy_rows(e, weight, S.weight, 4 * kNC, nb, sel));
+    if (tp) TRY(copy_rows(e, tp, S.tp, kNC, nb, sel));
+    if (tc) TRY(copy_rows(e, tc, S.tc, kNC, nb, sel));
+    if (ev || tri) {
+      TRY(run_compaction(e, 0, true));
+      if (ev) TRY(copy_rows(e, ev, e->comp.ev_handles, 4 * kEV, nb, sel));
+      if (tri) TRY(copy_rows(e, tri, e->comp.tri_handles, 4 * kNC * 5, nb, sel));
+    }
+    return VM_OK;
+  }
   if (coords) {
     std::vector<int4> bc(n);
     TRY(copy_sync(e, bc.data(), S.bcoord, sizeof(int4) * n, cudaMemcpyDeviceToHost));
@@ -1651,14 +1698,14 @@ int vm_export_blocks(vm_engine *e, int32_t owned_only, int64_t *n_out, int32_t *
   const int nb = e->h_ctr->nblocks;
   std::vector<uint8_t> own(nb);
   if (nb) TRY(copy_sync(e, own.data(), e->S.bowned, nb, cudaMemcpyDeviceToHost));
-  std::vector<int> sel;
-  for (int i = 0; i < nb; i++)
-    if (!owned_only || own[i] || e->S.nranks <= 1) sel.push_back(i);
-  *n_out = (int64_t)sel.size();
-  if (!coords || sel.empty()) return VM_OK;
   const DevState &S = e->S;
   std::vector<int4> bc(nb);
-  TRY(copy_sync(e, bc.data(), S.bcoord, sizeof(int4) * nb, cudaMemcpyDeviceToHost));
+  if (nb) TRY(copy_sync(e, bc.data(), S.bcoord, sizeof(int4) * nb, cudaMemcpyDeviceToHost));
+  std::vector<int> sel;
+  for (int i = 0; i < nb; i++)
+    if ((!owned_only || own[i] || e->S.nranks <= 1) && bc[i].w == 0) sel.push_back(i);
+  *n_out = (int64_t)sel.size();
+  if (!coords || sel.empty()) return VM_OK;
   for (size_t k = 0; k < sel.size(); k++) {
     const int i = sel[k];
     coords[3 * k] = bc[i].x; coords[3 * k + 1] = bc[i].y; coords[3 * k + 2] = bc[i].z;
@@ -1752,6 +1799,7 @@ int vm_partition_frame_begin(vm_engine *e, const double *depth, int32_t h, int32
   F.ghost_nranks = 0;
   TRY(ensure_rays(e, h, w));
   F.nsteps_fixed = fixed_nsteps(e, cfg->trunc);
+  F.block_gc_age = cfg->block_gc_age > 0 ? cfg->block_gc_age : 0;
   TRY(reset_call_counters(e));
   e->ctr_clean = false;
   e->restore_calls = false;

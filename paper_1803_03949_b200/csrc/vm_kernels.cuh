@@ -644,6 +644,7 @@ __global__ void __launch_bounds__(kFB, 6) k_fuse_blocks(DevState S, const FrameD
     if (b < 0) continue;
     const int4 c = __ldcg(S.bcoord + b);
     const bool fresh = (flags & F_INIT) && __ldcg(S.stamp_new + b) == F.epoch;
+    if ((flags & (F_INTEGRATE | F_GHOST)) && threadIdx.x == 0) S.last_frame[b] = F.frame;   // (block GC)
     // fusion.py:138-168, four corners per thread.  The old state of the corners
     // is requested first, so its round trip overlaps the projections and the
     // depth gathers.
@@ -1760,6 +1761,59 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
 constexpr size_t kGcSmem = 0;
 
 
+// ------------------------------------------------------------ block GC
+// Opt-in block eviction (north star item 5; the reference never frees a
+// block, store.py:14, so this is off in parity mode).  A block is evicted when
+// it was last collected at least `age` frames ago and holds nothing: no
+// occupied edge slot, no pending request and no observed sample (every
+// weight 0; weights never decrease).  Every cube with a corner in it is then
+// undefined and every normal stencil touching it unobserved, exactly as for
+// an absent block, so the mesh is unchanged -- only blocks_active differs.
+// (A free-space block -- tsdf +1 with weight > 0 -- is kept: a neighbour's
+// boundary cube can be defined through its samples.)
+// Its hash entry keeps the key with value kEvicted (a re-observation
+// allocates a fresh block there), its neighbours' rows are unlinked and its
+// index goes to the free list, which allocations pop first.  One warp per
+// block; runs before a frame's k_collect.
+__global__ void __launch_bounds__(256) k_block_gc(DevState S, int frame, int age) {
+  const int lane = threadIdx.x & 31;
+  const int nb = ld_vol(&S.ctr->nblocks);
+  const int warps = (int)(gridDim.x * blockDim.x) >> 5;
+  long long evicted = 0;
+  for (int b = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); b < nb; b += warps) {
+    const int4 c = S.bcoord[b];
+    if (c.w != 0 || S.last_frame[b] > frame - age) continue;   // (dead, or seen recently)
+    bool busy = false;
+    for (int q = lane; q < kEV / 32; q += 32)
+      busy |= (S.vocc[(size_t)b * (kEV / 32) + q] | S.vclaim[(size_t)b * (kEV / 32) + q]) != 0u;
+    if (lane < kNC / 32) busy |= S.vmask[(size_t)b * (kNC / 32) + lane] != 0u;   // a sample with weight > 0
+    if (__any_sync(0xffffffffu, busy)) continue;
+    // unlink: neighbours forget the block, its own row is cleared
+    if (lane < 27 && lane != 13) {
+      const int n = S.nbr[(size_t)b * 27 + lane];
+      if (n >= 0) S.nbr[(size_t)n * 27 + (26 - lane)] = -1;
+    }
+    if (lane < 27) S.nbr[(size_t)b * 27 + lane] = -1;
+    if (lane == 0) {
+      // the hash entry keeps its key, value kEvicted
+      const long long key = pack_coord(c.x, c.y, c.z);
+      const unsigned bk = bucket_of(S, key);
+      HashSlot *kb = S.slots + (size_t)bk * kSlotsPerBucket;
+      bool done = false;
+      for (int i = 0; i < kSlotsPerBucket && !done; i++)
+        if (kb[i].key == key) { kb[i].val = kEvicted; done = true; }
+      for (int e = S.ovf_head[bk]; e >= 0 && !done; e = S.ovf_next[e])
+        if (S.ovf_key[e] == key) { S.ovf_val[e] = kEvicted; done = true; }
+      S.bcoord[b] = make_int4(c.x, c.y, c.z, 1);   // dead
+      S.free_list[atomicAdd(&S.ctr->nfree, 1)] = b;
+      if (S.nranks > 1 && S.bowned[b]) atomicAdd((unsigned long long *)&S.ctr->nblocks_owned, ~0ull);
+      evicted++;
+    }
+  }
+  evicted = warp_sum(evicted);
+  if (lane == 0 && evicted) atomicAdd((unsigned long long *)&S.ctr->evicted_total, (unsigned long long)evicted);
+}
+
 // ------------------------------------------------------------ full scans
 __global__ void k_irregular_full(DevState S, int nblocks, unsigned long long *out) {
   long long cnt = 0;
@@ -1908,7 +1962,7 @@ __global__ void k_rebuild_vmask(DevState S, const int32_t *idx, int n) {
 __global__ void k_block_keys(DevState S, int nblocks, unsigned long long *keys, int32_t *vals) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nblocks; i += gridDim.x * blockDim.x) {
     const int4 c = S.bcoord[i];
-    keys[i] = (unsigned long long)pack_coord(c.x, c.y, c.z);
+    keys[i] = c.w ? ~0ull : (unsigned long long)pack_coord(c.x, c.y, c.z);   // (evicted blocks last)
     vals[i] = i;
   }
 }

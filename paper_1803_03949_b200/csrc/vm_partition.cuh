@@ -78,7 +78,7 @@ __global__ void k_unpack_ghosts(DevState S, const FrameDev F) {
 __global__ void k_owned_block_keys(DevState S, int nblocks, unsigned long long *keys, int32_t *vals) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nblocks; i += gridDim.x * blockDim.x) {
     const int4 c = S.bcoord[i];
-    const bool own = S.nranks <= 1 || S.bowned[i];
+    const bool own = (S.nranks <= 1 || S.bowned[i]) && c.w == 0;
     keys[i] = own ? (unsigned long long)pack_coord(c.x, c.y, c.z) : ~0ull;
     vals[i] = i;
   }

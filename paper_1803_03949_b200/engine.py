@@ -51,6 +51,10 @@ class RunConfig:
     nranks: int = 1
     tile_blocks: int = 8
     halo_exchange: bool = False          # margin blocks received from their owners (partition.py)
+    # opt-in block GC (north star item 5; off = the reference's never-evict
+    # store, store.py:14): every block_gc_age frames, evict blocks not
+    # collected for that long that hold no vertex and no observed sample
+    block_gc_age: int = 0
 
     def resolved(self) -> "RunConfig":
         cfg = replace(self)
@@ -62,6 +66,8 @@ class RunConfig:
             cfg.workers = os.cpu_count() or 1
         if cfg.strategy not in STRATEGIES:
             raise ValueError(f"unknown strategy {cfg.strategy!r}")
+        if cfg.block_gc_age < 0:
+            raise ValueError("block_gc_age must be >= 0")
         return cfg
 
     def to_dict(self) -> dict:
@@ -162,7 +168,8 @@ class Engine:
         self._intr_c = _lib.intr_c(intrinsics)
         self._fcfg = _lib.FrameConfig(float(c.trunc), float(c.max_range), float(c.epsilon),
                                       int(c.weight_cap), int(bool(c.refine)),
-                                      int(bool(c.frustum_only)), _lib.STRATEGY_CODES[c.strategy], 0)
+                                      int(bool(c.frustum_only)), _lib.STRATEGY_CODES[c.strategy],
+                                      int(max(0, c.block_gc_age)))
         self._collected_n = 0
         self._collected_cache = None
         self.pipelined = bool(pipelined) and not audit_every_frame
