@@ -115,6 +115,7 @@ struct FrameDev {
   int32_t block_gc_age; // > 0: opt-in block GC (k_block_gc before this frame when frame % age == 0)
   int32_t consume_fb;   // fuse_frame: k_collect applies the previous frame's fallback records
   int32_t reset_after;  // k_gc_normals' commit clears the per-call counters after its snapshot
+  int32_t strategy;     // VM_STRATEGY_*: 2 = partition (8 parity passes of plain stores, k_place_parity)
   Counters *snap;       // non-null: k_gc_normals' commit copies the counter block here (device)
   // non-null: k_collect copies the previous frame's snapshot (pub_src) to the
   // host's mapped buffer (pub_dst) and then writes pub_id to *pub_seq, the
@@ -182,6 +183,11 @@ struct DevState {
   double *vparam;       // [cap*1536] vertex coordinate along the edge axis
   double *vnrm;         // [cap*1536*3]
   uint32_t *item_mask;  // [cap*16] explicit scope cube masks
+  // strategy "partition" only (allocated on first use): per-slot request bytes
+  // written by the parity passes with plain stores, and the retype's selection
+  // (one byte per tile column, bit z) of each scope item
+  uint8_t *vreq;        // [cap*1536]
+  uint8_t *psel;        // [cap*64]
   int4 *fallback;       // [cap*1536] fallback worklist: block, slot, 4 cube types, candidate mask
   long long max_vertices;
   // spatial partition: blocks are owned by hashed tiles

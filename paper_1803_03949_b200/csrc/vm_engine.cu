@@ -83,7 +83,7 @@ struct vm_engine {
   bool own_stream = false;
   int32_t epoch = 0;
   int sm_count = 148;
-  int grid_retype = 296, grid_gc = 296, grid_fuse = 296, grid_collect = 296;
+  int grid_retype = 296, grid_gc = 296, grid_fuse = 296, grid_collect = 296, grid_parity = 296;
   void *d_scratch = nullptr;
   size_t scratch_cap = 0;
   Compacted comp;
@@ -259,6 +259,11 @@ static int grow_blocks(vm_engine *e, int64_t need) {
   TRY(dev_grow(&S.vparam, o * kEV, n * kEV, st));
   TRY(dev_grow(&S.vnrm, o * kEV * 3, n * kEV * 3, st));
   TRY(dev_grow(&S.item_mask, 0, n * 16, st));
+  if (S.vreq) {   // strategy "partition" buffers (zero request bytes for the new blocks)
+    TRY(dev_grow(&S.vreq, o * kEV, n * kEV, st));
+    CK(cudaMemsetAsync(S.vreq + o * kEV, 0, (n - o) * kEV, st));
+    TRY(dev_grow(&S.psel, 0, n * 64, st));
+  }
   TRY(dev_grow(&S.fallback, 0, n * kEV, st));
   S.block_cap = (int32_t)cap;
   return VM_OK;
@@ -343,6 +348,28 @@ static inline void rec(vm_engine *e, int ph) {
   if (e->profiling) cudaEventRecord(e->ev[ph], e->stream);   // (else the kernels' own clock: t_start/t_end_ns)
 }
 
+// strategy "partition" buffers, allocated on first use (block storage size)
+static int ensure_partition_bufs(vm_engine *e, int strategy) {
+  DevState &S = e->S;
+  if (strategy != VM_STRATEGY_PARTITION || S.vreq) return VM_OK;
+  TRY(dev_alloc(&S.vreq, (size_t)S.block_cap * kEV, 0));
+  TRY(dev_alloc(&S.psel, (size_t)S.block_cap * 64));
+  return VM_OK;
+}
+
+// kernels of the meshing segment before k_gc_normals: k_retype_place, then for
+// strategy "partition" the eight parity passes of the placement
+static int meshing_launches(const FrameDev &F) { return F.strategy == VM_STRATEGY_PARTITION ? 9 : 1; }
+static void launch_retype(vm_engine *e, bool pdl, const FrameDev &F) {
+  const DevState &S = e->S;
+  cudaStream_t st = e->stream;
+  if (pdl) launch_pdl(k_retype_place, e->grid_retype, kNT, st, S, F);
+  else k_retype_place<<<e->grid_retype, kNT, kRetypeSmem, st>>>(S, F);
+  if (F.strategy == VM_STRATEGY_PARTITION)
+    for (int p = 0; p < 8; p++) launch_pdl(k_place_parity, e->grid_parity, kNT, st, S, F, p);
+}
+static int gc_strategy_flag(const FrameDev &F) { return F.strategy == VM_STRATEGY_PARTITION ? G_PARTITION : 0; }
+
 // frame segment after collect: fuse (init/integrate/scope), retype+place, gc+normals
 static int enqueue_after_collect(vm_engine *e) {
   DevState &S = e->S;
@@ -353,9 +380,10 @@ static int enqueue_after_collect(vm_engine *e) {
   launch_pdl(k_fuse_blocks, e->grid_fuse, kFB, st, S, F, (const int32_t *)S.scope,
              (const int32_t *)&S.ctr->ncollected, 0, (int)(F_INIT | F_INTEGRATE | F_SCOPE), 0);
   rec(e, PH_RETYPE);
-  launch_pdl(k_retype_place, e->grid_retype, kNT, st, S, F);
+  launch_retype(e, true, F);
   rec(e, PH_GC);
-  launch_gc(e, true, S.halo, &S.ctr->nhalo, 0, (int)(G_GC | G_NORMALS | G_COMMIT | G_REQUIRE_ITEMS | G_SHARDED));
+  launch_gc(e, true, S.halo, &S.ctr->nhalo, 0,
+            (int)(G_GC | G_NORMALS | G_COMMIT | G_REQUIRE_ITEMS | G_SHARDED) | gc_strategy_flag(F));
   rec(e, PH_END);
   return check_launch();
 }
@@ -370,7 +398,7 @@ static int complete_with_resume(vm_engine *e, int *resumes) {
     CK(cudaMemsetAsync(&e->S.ctr->need, 0, sizeof(int32_t), e->stream));
     if (resumes) (*resumes)++;
     TRY(enqueue_after_collect(e));
-    e->frame_launches += 3;
+    e->frame_launches += 2 + meshing_launches(*e->h_frame);
   }
   return set_err(VM_ERR_CUDA, "resume loop did not converge");
 }
@@ -634,6 +662,8 @@ int vm_create(const vm_store_config *cfg, vm_engine **out) {
     e->grid_fuse = std::max(1, occ) * e->sm_count;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_collect, kCollectThreads, 0));
     e->grid_collect = std::max(1, occ) * e->sm_count;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_place_parity, kNT, 0));
+    e->grid_parity = std::max(1, occ) * e->sm_count;
   }
   S.block_cap = 0;
   const int64_t ib = cfg->initial_blocks > 0 ? cfg->initial_blocks : 1024;
@@ -649,7 +679,7 @@ int vm_destroy(vm_engine *e) {
   DevState &S = e->S;
   void *ptrs[] = {S.slots, S.ovf_head, S.ovf_lock, S.ovf_key, S.ovf_val, S.ovf_next, S.ovf_stamp, S.bcoord,
                   S.nbr, S.stamp_collect, S.stamp_halo, S.stamp_new, S.bowned, S.slab_bits, S.scope,
-                  S.halo, S.halo_sh, S.tsdf, S.weight, S.vmask, S.tp, S.tc, S.vbirth, S.vocc, S.vclaim, S.vparam, S.vnrm, S.item_mask, S.fallback, e->d_rays,
+                  S.halo, S.halo_sh, S.tsdf, S.weight, S.vmask, S.tp, S.tc, S.vbirth, S.vocc, S.vclaim, S.vparam, S.vnrm, S.item_mask, S.vreq, S.psel, S.fallback, e->d_rays,
                   S.ctr, e->d_depth, e->d_scratch, S.ghost_src, e->d_ghost_counts, S.last_frame, S.free_list};
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -861,7 +891,7 @@ static int launch_frame(vm_engine *e, int slot) {
   if (!e->ctr_clean) TRY(reset_call_counters(e));
   cudaStream_t st = e->stream;
   rec(e, PH_DEPTH);
-  e->frame_launches = 4;   // collect, fuse, retype, gc (+ depth stats)
+  e->frame_launches = 3 + meshing_launches(F);   // collect, fuse, retype (+ parity passes), gc (+ depth stats)
   if (F.block_gc_age > 0 && F.frame > 0 && F.frame % F.block_gc_age == 0) {
     // opt-in block GC, before the frame allocates (its pops reuse the indices)
     k_block_gc<<<e->sm_count * 8, 256, 0, st>>>(e->S, F.frame, F.block_gc_age);
@@ -912,6 +942,8 @@ int vm_fuse_frame_enqueue(vm_engine *e, const double *depth, int32_t h, int32_t 
   F.epoch = ++e->epoch;
   F.frame = (int32_t)frame_index;
   F.scope_mode = 0;
+  F.strategy = cfg->strategy;
+  TRY(ensure_partition_bufs(e, cfg->strategy));
   TRY(ensure_rays(e, h, w));
   F.nsteps_fixed = fixed_nsteps(e, cfg->trunc);
   F.block_gc_age = cfg->block_gc_age > 0 ? cfg->block_gc_age : 0;
@@ -1011,7 +1043,8 @@ static int settle_slot(vm_engine *e, int slot, bool succ) {
     }
     if (rc == VM_OK) {
       const FrameDev &Fs = e->f_saved[slot];
-      e->settled.kernel_launches = 4 + (Fs.nsteps_fixed <= 0) + 3 * e->last_resumes +
+      e->settled.kernel_launches = 3 + meshing_launches(Fs) + (Fs.nsteps_fixed <= 0) +
+                                   (2 + meshing_launches(Fs)) * e->last_resumes +
                                    (Fs.block_gc_age > 0 && Fs.frame > 0 && Fs.frame % Fs.block_gc_age == 0);
     }
   }
@@ -1339,6 +1372,8 @@ int vm_extract(vm_engine *e, const int32_t *scope_coords, const uint8_t *scope_m
   F.epoch = ++e->epoch;
   F.frame = (int32_t)frame_index;
   F.scope_mode = 1;
+  F.strategy = strategy;
+  TRY(ensure_partition_bufs(e, strategy));
   TRY(reset_call_counters(e));
   int32_t *di;
   TRY(map_coords(e, scope_coords, n_scope, &di, nullptr, 0, false));
@@ -1360,12 +1395,11 @@ int vm_extract(vm_engine *e, const int32_t *scope_coords, const uint8_t *scope_m
     k_halo_from_items<<<grid_threads(e, n_scope * 27, 256), 256, 0, e->stream>>>(e->S, *e->h_frame);
     TRY(check_launch());
   }
-  const int gb = grid_blocks(e);
-  k_retype_place<<<e->grid_retype, kNT, kRetypeSmem, e->stream>>>(e->S, *e->h_frame);
+  launch_retype(e, false, *e->h_frame);
   // the halo given here need not hold every block a request went to: apply them all
   TRY(read_counters(e));
   k_apply_claims<<<grid_threads(e, (long long)e->h_ctr->nblocks * (kEV / 32), 256), 256, 0, e->stream>>>(
-      e->S, e->h_ctr->nblocks, e->h_frame->frame);
+      e->S, e->h_ctr->nblocks, e->h_frame->frame, (int)(e->h_frame->strategy == VM_STRATEGY_PARTITION));
   launch_gc(e, false, e->S.halo, &e->S.ctr->nhalo, 0, (int)(G_GC | G_NORMALS | G_COMMIT | G_REQUIRE_ITEMS));
   TRY(check_launch());
   TRY(flush_fallbacks(e));
@@ -1789,6 +1823,8 @@ int vm_partition_frame_begin(vm_engine *e, const double *depth, int32_t h, int32
   F.epoch = ++e->epoch;
   F.frame = (int32_t)frame_index;
   F.scope_mode = 0;
+  F.strategy = cfg->strategy;
+  TRY(ensure_partition_bufs(e, cfg->strategy));
   F.consume_fb = 0;   // (settle_all applied the pending records)
   F.snap = nullptr;
   F.reset_after = 0;
@@ -1879,9 +1915,10 @@ int vm_partition_frame_finish(vm_engine *e, const uint8_t *recv, const int32_t *
              0, (int)(F_INIT | F_GHOST), (int)e->part_nc_own);
   launch_pdl(k_fuse_blocks, e->grid_fuse, kFB, st, S, F, (const int32_t *)S.scope, (const int32_t *)&S.ctr->ncollected,
              0, (int)F_SCOPE, 0);
-  launch_pdl(k_retype_place, e->grid_retype, kNT, st, S, F);
-  launch_gc(e, true, S.halo, &S.ctr->nhalo, 0, (int)(G_GC | G_NORMALS | G_COMMIT | G_REQUIRE_ITEMS | G_SHARDED));
-  e->frame_launches += 5;
+  launch_retype(e, true, F);
+  launch_gc(e, true, S.halo, &S.ctr->nhalo, 0,
+            (int)(G_GC | G_NORMALS | G_COMMIT | G_REQUIRE_ITEMS | G_SHARDED) | gc_strategy_flag(F));
+  e->frame_launches += 4 + meshing_launches(F);
   TRY(check_launch());
   TRY(read_counters(e));
   TRY(error_from_counters(e));

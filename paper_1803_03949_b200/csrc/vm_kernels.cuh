@@ -26,7 +26,8 @@ constexpr int kThreadsCube = 512;   // one thread per cube of a block
 enum { F_INIT = 1, F_INTEGRATE = 2, F_SCOPE = 4, F_HALO = 8, F_GHOST = 16 };
 // halo-exchange record: coordinate, then the block's 512 tsdf and 512 weights
 constexpr size_t kGhostRec = 16 + 8 * 512 + 4 * 512;
-enum { G_GC = 1, G_NORMALS = 2, G_COMMIT = 4, G_REQUIRE_ITEMS = 8, G_SHARDED = 16 };
+enum { G_GC = 1, G_NORMALS = 2, G_COMMIT = 4, G_REQUIRE_ITEMS = 8, G_SHARDED = 16,
+       G_PARTITION = 32 };   // G_PARTITION: requests are k_place_parity's bytes (S.vreq)
 
 // error and need are adjacent: one 8-byte load
 __device__ __forceinline__ bool halted(const DevState &S) {
@@ -937,6 +938,7 @@ __global__ void __launch_bounds__(kNT, 18) k_retype_place(DevState S, const Fram
   const double l = S.cube_size;
   const int do_refine = F.refine;
   const double eps = F.epsilon;
+  const bool part = F.strategy == 2;   // placement by k_place_parity: record the selection instead
   int placements = 0, active = 0, changed = 0, t_rel = 0, t_new = 0, irr = 0, refined = 0, live = 0;
   for (int i = blockIdx.x; i < n; i += gridDim.x, nth++) {
     trace_item(S, TK_RETYPE, nth, 0);
@@ -984,6 +986,7 @@ __global__ void __launch_bounds__(kNT, 18) k_retype_place(DevState S, const Fram
       }
     };
     if (mode <= 0) {
+      if (part) S.psel[(size_t)i * 64 + t] = 0;
       mark_halo();
       append_halo();
       __syncthreads();
@@ -1091,6 +1094,7 @@ __global__ void __launch_bounds__(kNT, 18) k_retype_place(DevState S, const Fram
         }
         const uint32_t vall = ((w[0] & w[1] & w[2] & w[3]) >> 9) & 0x1FFu;   // points z with 4 weights > 0
         sel &= vall & (vall >> 1);
+        if (part) S.psel[(size_t)i * 64 + t] = (uint8_t)sel;
         const uint32_t sg0 = w[0] & 0x1FFu, sg1 = w[1] & 0x1FFu, sg2 = w[2] & 0x1FFu, sg3 = w[3] & 0x1FFu;
         // sign changes along the cube edges (mc_tables.py:44-64): e0/e4 between
         // corners 0-1 at z / z + 1, e1/e5 1-2, e2/e6 3-2, e3/e7 0-3, e8..e11 the
@@ -1142,7 +1146,8 @@ __global__ void __launch_bounds__(kNT, 18) k_retype_place(DevState S, const Fram
             reinterpret_cast<uint32_t *>(S.tc)[q4] = new_tc;
           }
         }
-      } else
+      } else {
+      uint32_t selb = 0;   // (partition: the column's selected cubes)
 #pragma unroll
       for (int half = 0; half < 2; half++) {
         const int z0 = 4 * half;
@@ -1162,6 +1167,7 @@ __global__ void __launch_bounds__(kNT, 18) k_retype_place(DevState S, const Fram
           else sel = (S.item_mask[(size_t)R.item * 16 + (c >> 5)] >> (c & 31)) & 1;
           sel = sel && ((val >> (8 * k)) & 0xFFu) == 0xFFu;   // all 8 weights > 0
           if (!sel) continue;
+          selb |= 1u << z;
           const unsigned bits = (sgn >> (8 * k)) & 0xFFu;
           const unsigned tp = (old_tc >> (8 * k)) & 0xFFu;
           unsigned tc = bits;
@@ -1202,6 +1208,9 @@ __global__ void __launch_bounds__(kNT, 18) k_retype_place(DevState S, const Fram
           reinterpret_cast<uint32_t *>(S.tc)[q4] = new_tc;
         }
       }
+      if (part) S.psel[(size_t)i * 64 + t] = (uint8_t)selb;
+      }
+      if (part) cxa = cxb = cya = cyb = cza = czb = czc = czd = 0u;   // (no claims)
       // one shared-memory OR per (axis, column) word this thread touched
       if (cxa) atomicOr(&s_claim[0 * 81 + cols[0]], cxa);
       if (cxb) atomicOr(&s_claim[0 * 81 + cols[3]], cxb);
@@ -1222,7 +1231,7 @@ __global__ void __launch_bounds__(kNT, 18) k_retype_place(DevState S, const Fram
     // requests into allocations).  The requested slots are then dealt out one
     // per lane (a warp search over the lanes' prefix counts) for their
     // coordinate stores; every requester of a slot writes the same bits.
-    {
+    if (!part) {
       const int wq = t >> 5;
 #pragma unroll
       for (int round = 0; round < 2; round++) {
@@ -1315,6 +1324,84 @@ __global__ void __launch_bounds__(kNT, 18) k_retype_place(DevState S, const Fram
   trace_at(S, TK_RETYPE, 31);
 }
 constexpr size_t kRetypeSmem = 0;
+
+// Strategy "partition" (mesher.py:250-254, 606-614): vertex placement in eight
+// passes, one per 2x2x2 parity class of the cubes (one launch each, so the
+// passes are separated by grid-wide completion).  Inside a pass no two cubes
+// share an edge slot (cubes of one class are >= 2 apart along some axis, and
+// the 4 cubes around an edge all differ in parity), so every request and
+// coordinate is a PLAIN store: a request byte per slot (no atomic on a shared
+// bitmap word, whose 32 slots span cubes of one class) and the slot's
+// coordinate along its axis.  k_gc_normals (G_PARTITION) then reads the bytes
+// as the claim bitmap.  Results are identical to the claim strategy's.
+// One CTA of 64 threads per scope item: thread t = one of the item's 64 cubes
+// of the class -- tile column (2 (t >> 4 & 3) + px, 2 (t >> 2 & 3) + py),
+// z = 2 (t & 3) + pz.
+__global__ void __launch_bounds__(kNT) k_place_parity(DevState S, const FrameDev F, int parity) {
+  cudaGridDependencySynchronize();   // PDL: the previous pass (or the retype) has completed
+  __shared__ int s_pro[5];
+  read_prologue(S, s_pro, &S.ctr->ncollected, &S.ctr->nslab, &S.ctr->nexplicit, nullptr);
+  if (s_pro[0]) return;
+  const int nc = s_pro[1];
+  const int n = F.scope_mode != 0 ? s_pro[3] : nc + s_pro[2];
+  __shared__ int s_row[27];
+  __shared__ int4 s_coord;
+  const int t = threadIdx.x;
+  const int x = 2 * ((t >> 4) & 3) + (parity & 1), y = 2 * ((t >> 2) & 3) + ((parity >> 1) & 1),
+            z = 2 * (t & 3) + ((parity >> 2) & 1);
+  const int c = (x * 8 + y) * 8 + z;
+  const double l = S.cube_size;
+  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+    const int b = __ldcg(S.scope + i);
+    if (b < 0) continue;   // (uniform)
+    if (t < 27) s_row[t] = t == 13 ? b : __ldcg(S.nbr + (size_t)b * 27 + t);
+    if (t == 27) s_coord = __ldcg(S.bcoord + b);
+    const bool sel = (__ldcg(S.psel + (size_t)i * 64 + x * 8 + y) >> z) & 1u;
+    const unsigned mask = sel ? edge_mask_of(__ldcg(S.tc + (size_t)b * kNC + c)) : 0u;
+    __syncthreads();
+    const int4 bc = s_coord;
+    for (unsigned m = mask; m; m &= m - 1) {
+      const int e = __ffs(m) - 1;
+      const int oa = (int)((kEdgeOwnAxis >> (5 * e)) & 31);   // owner offset | axis << 3
+      const int axis = oa >> 3;
+      const int ox = x + (oa & 1), oy = y + ((oa >> 1) & 1), oz = z + ((oa >> 2) & 1);
+      const int ob = s_row[nbr_dir(ox >> 3, oy >> 3, oz >> 3)];
+      if (ob < 0) {   // mesher.py:200-203
+        set_error(S, ERR_CONSISTENCY, 10, bc.x * kB + ox, bc.y * kB + oy, bc.z * kB + oz);
+        continue;
+      }
+      const size_t slot = (size_t)ob * kEV + ((ox & 7) * 64 + (oy & 7) * 8 + (oz & 7)) * 3 + axis;
+      // start corner = the owner point, end corner one step along the axis
+      const int ex = ox + (axis == 0), ey = oy + (axis == 1), ez = oz + (axis == 2);
+      const int eb = s_row[nbr_dir(ex >> 3, ey >> 3, ez >> 3)];
+      const double d0 = S.tsdf[(size_t)ob * kNC + (ox & 7) * 64 + (oy & 7) * 8 + (oz & 7)];
+      const double d1 = eb >= 0 ? S.tsdf[(size_t)eb * kNC + (ex & 7) * 64 + (ey & 7) * 8 + (ez & 7)] : 0.0;
+      const double param = (d0 == d1) ? 0.5 : d0 / (d0 - d1);
+      const int ga = axis == 0 ? bc.x * kB + ox : axis == 1 ? bc.y * kB + oy : bc.z * kB + oz;
+      S.vreq[slot] = 1;
+      S.vparam[slot] = __dadd_rn(__dmul_rn((double)ga, l), __dmul_rn(param, l));
+    }
+    __syncthreads();   // s_row is rewritten by the next item
+  }
+}
+
+// the 32 request bytes of one slot word as bits (strategy "partition")
+__device__ __forceinline__ uint32_t pack_requests(const uint8_t *p) {
+  const uint4 a = __ldcg(reinterpret_cast<const uint4 *>(p)), b = __ldcg(reinterpret_cast<const uint4 *>(p + 16));
+  const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+  uint32_t r = 0;
+#pragma unroll
+  for (int k = 0; k < 8; k++) {   // byte j of word k -> bit 4 k + j
+    const uint32_t v = w[k];
+    r |= (((v & 0xFFu) != 0) | (((v >> 8) & 0xFFu) != 0) << 1 | (((v >> 16) & 0xFFu) != 0) << 2 |
+          ((v >> 24) != 0) << 3) << (4 * k);
+  }
+  return r;
+}
+__device__ __forceinline__ void clear_requests(uint8_t *p) {
+  reinterpret_cast<uint4 *>(p)[0] = make_uint4(0, 0, 0, 0);
+  reinterpret_cast<uint4 *>(p)[1] = make_uint4(0, 0, 0, 0);
+}
 
 
 // ------------------------------------------------------------ GC + normals
@@ -1525,7 +1612,8 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
       // stage occupancy + requests, types and halo flags (all copies in flight)
       for (int q = lane; q < kEV / 32; q += 32) {
         cp_async4(&I.occ[q], S.vocc + (size_t)b * (kEV / 32) + q, true);
-        cp_async4(&I.cl[q], S.vclaim + (size_t)b * (kEV / 32) + q, true);
+        if (mode & G_PARTITION) I.cl[q] = pack_requests(S.vreq + (size_t)b * kEV + q * 32);
+        else cp_async4(&I.cl[q], S.vclaim + (size_t)b * (kEV / 32) + q, true);
       }
       for (int q = lane; q < 2 * 81; q += 32) {   // per column: the z = 0..7 run, then z = -1
         const int col = q >> 1, lx = col / 9 - 1, ly = col % 9 - 1;
@@ -1576,7 +1664,10 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
           if (!normals) { S.vnrm[3 * q] = 0.0; S.vnrm[3 * q + 1] = 0.0; S.vnrm[3 * q + 2] = 0.0; }
         }
         allocs += J.R.owned * __popc(fresh);   // counted by the slot's owning rank
-        if (claim) S.vclaim[bk * (kEV / 32) + wd] = 0u;
+        if (claim) {
+          if (mode & G_PARTITION) clear_requests(S.vreq + bk * kEV + wd * 32);
+          else S.vclaim[bk * (kEV / 32) + wd] = 0u;
+        }
         word = J.occ[wd] | claim;
         J.occ[wd] = word;
         J.cl[wd] = fresh;   // (the allocations of this call, for the normals pass)
@@ -1922,11 +2013,15 @@ __global__ void __launch_bounds__(128) k_flush_fallbacks(DevState S) {
 // phase API (mesher.extract_frame with an arbitrary halo): apply every pending
 // placement request of every block (in fuse_frame k_gc_normals does it for the
 // halo, which holds every block a scope cube can request a slot of)
-__global__ void k_apply_claims(DevState S, int nblocks, int frame) {
+__global__ void k_apply_claims(DevState S, int nblocks, int frame, int from_bytes) {
   long long allocs = 0;
   for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < (long long)nblocks * (kEV / 32);
        q += (long long)gridDim.x * blockDim.x) {
-    const uint32_t claim = S.vclaim[q];
+    uint32_t claim = S.vclaim[q];
+    if (from_bytes) {   // strategy "partition": k_place_parity's request bytes
+      claim |= pack_requests(S.vreq + (size_t)q * 32);
+      if (claim) clear_requests(S.vreq + (size_t)q * 32);
+    }
     if (!claim) continue;
     const uint32_t old = S.vocc[q], fresh = claim & ~old;
     const long long b = q / (kEV / 32);
