@@ -1,7 +1,8 @@
 """Summarise an ncu --set full capture and a launch-list CSV into profiles/.
-usage: python tools/ncu_summary.py TAG report.ncu-rep launches.csv bench.json
+usage: python tools/ncu_summary.py TAG report.ncu-rep launches.csv bench.json [CONFIG]
 writes profiles/TAG_summary.md and refreshes profiles/ncu_traffic.json (the
-per-launch DRAM bytes bench.py reports as roofline.traffic)."""
+per-launch DRAM bytes bench.py reports as roofline.traffic, per BASELINE config;
+CONFIG defaults to C2)."""
 import csv
 import io
 import json
@@ -11,6 +12,7 @@ import sys
 from pathlib import Path
 
 tag, rep, launches, bench = sys.argv[1:5]
+config = sys.argv[5] if len(sys.argv) > 5 else "C2"
 ROOT = Path(__file__).resolve().parents[1]
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
            "lts__t_sector_hit_rate.pct", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
@@ -26,7 +28,7 @@ per = {}
 for r in data:
     k = r[ki].split("(")[0]
     per.setdefault(k, []).append({m: float((r[hdr.index(m)] or "0").replace(",", "")) for m in METRICS})
-lines = [f"# {tag}: ncu --set full (cold cache, serialised replay), C2 frames", "",
+lines = [f"# {tag}: ncu --set full (cold cache, serialised replay), {config} frames", "",
          "| kernel | launches | time us | DRAM read MB | DRAM write MB | L2 hit % | SM thru % | warps active % | regs | grid x block | warp-inst | SM active/elapsed |",
          "|---|---|---|---|---|---|---|---|---|---|---|---|"]
 traffic = {}
@@ -58,7 +60,12 @@ lines += ["", f"bench (same code): value {b['value']:.0f} frames/s ({b['ms_per_s
               f"{b['roofline']['achieved']:.0f} GB/s = {100 * b['roofline']['frac']:.1f}% of {b['roofline']['peak']:.0f} GB/s, "
               f"frame {100 * b['roofline']['frame_frac']:.1f}%; phases (profiled pass, ms) {json.dumps({k: round(v, 4) for k, v in b['phase_ms_mean'].items()})}"]
 (ROOT / "profiles" / f"{tag}_summary.md").write_text("\n".join(lines) + "\n")
-(ROOT / "profiles" / "ncu_traffic.json").write_text(json.dumps(
-    {"source": f"profiles/{tag}_summary.md (ncu --set full, C2 frames, per launch)",
-     "dram_bytes_per_launch": traffic}, indent=1))
+tp = ROOT / "profiles" / "ncu_traffic.json"
+tj = json.loads(tp.read_text()) if tp.exists() else {}
+tj.setdefault("by_config", {})[config] = traffic
+tj.setdefault("sources", {})[config] = f"profiles/{tag}_summary.md (ncu --set full, {config} frames, per launch)"
+if config == "C2":
+    tj["source"] = tj["sources"]["C2"]
+    tj["dram_bytes_per_launch"] = traffic
+tp.write_text(json.dumps(tj, indent=1))
 print("\n".join(lines))
