@@ -29,6 +29,7 @@ per-frame global StatsRow is one NCCL int64 all-reduce (inside e2e).
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import math
 import os
@@ -258,6 +259,19 @@ CONFIG_TEXT = {
 }
 
 
+class PausedGC:
+    """Python's cyclic collector is run once and paused for a timed loop: a
+    generation-2 pass over torch's objects takes milliseconds and lands at a
+    random frame (profiles/r2_v3_raw_e2e_probe.txt: one 12 ms call)."""
+
+    def __enter__(self):
+        gc.collect()
+        gc.disable()
+
+    def __exit__(self, *exc):
+        gc.enable()
+
+
 def workload(args, spec, cfg):
     return {"workload": f"{args.config}: {CONFIG_TEXT.get(args.config, args.config)}, "
                         f"{spec.width}x{spec.height} depth, {cfg['cube_size'] * 1e3:.0f} mm voxels, "
@@ -266,6 +280,7 @@ def workload(args, spec, cfg):
             "cube_size_m": cfg["cube_size"], "trunc_m": cfg["trunc"],
             "refine": bool(cfg.get("refine", False)), "strategy": args.strategy,
             "l2": "flushed between frames (256 MiB write, outside the timed events)",
+            "python_gc": "collected, then paused during each timed loop",
             "halo": args.halo if args.gpus > 1 and args.mode == "partition" else None,
             "parallelism": (f"spatial partition x{args.gpus} (tiles of {args.tile_blocks}^3 blocks, "
                             f"halo {args.halo})"
@@ -304,7 +319,12 @@ def run_gpu(args, spec, cfg, rank, world, local_rank):
     probe = Engine(RunConfig(strategy=args.strategy, **cfg, **ekw), spec.intrinsics())
     for i in range(nframes):
         probe.fuse_frame(depths[i], poses[i])
-    caps = dict(block_capacity=probe.store._counters()["block_count"] + 64)
+    pc = probe.store._counters()
+    # vertex records: what the scene ends with + k_retype_place's per-frame bound
+    # (2187 per scope item) + the gc CTAs' chunk runs
+    max_items = max(d["scope_blocks"] for d in probe.device_stats)
+    caps = dict(block_capacity=pc["block_count"] + 64,
+                vertex_capacity=pc["vertex_records"] + 2187 * max_items + 2 * 64 * 2048 + 4096)
     del probe
 
     flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
@@ -324,13 +344,14 @@ def run_gpu(args, spec, cfg, rank, world, local_rank):
             torch.cuda.synchronize()
             starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
             ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-            for k in range(args.steps):
-                i = args.warmup + k
-                flush.zero_()
-                starts[k].record(stream)
-                pe.fuse_frame(depths[i], poses[i])
-                ends[k].record(stream)
-            torch.cuda.synchronize()
+            with PausedGC():
+                for k in range(args.steps):
+                    i = args.warmup + k
+                    flush.zero_()
+                    starts[k].record(stream)
+                    pe.fuse_frame(depths[i], poses[i])
+                    ends[k].record(stream)
+                torch.cuda.synchronize()
             return pe.engine, [s.elapsed_time(e) for s, e in zip(starts, ends)], [], 0
         eng = Engine(RunConfig(strategy=args.strategy, **cfg, **caps, **ekw), spec.intrinsics())
         eng.set_stream(stream.cuda_stream)
@@ -343,17 +364,18 @@ def run_gpu(args, spec, cfg, rank, world, local_rank):
         starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
         ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
         phases, resumes = [], 0
-        for k in range(args.steps):
-            i = args.warmup + k
-            flush.zero_()
-            starts[k].record(stream)
-            eng.fuse_frame_enqueue(depths[i], poses[i])
-            ends[k].record(stream)
-            eng.fuse_frame_finish()
-            resumes += eng.device_stats[-1]["resumes"]
-            if profiling:
-                phases.append(eng.phase_times())
-        torch.cuda.synchronize()
+        with PausedGC():
+            for k in range(args.steps):
+                i = args.warmup + k
+                flush.zero_()
+                starts[k].record(stream)
+                eng.fuse_frame_enqueue(depths[i], poses[i])
+                ends[k].record(stream)
+                eng.fuse_frame_finish()
+                resumes += eng.device_stats[-1]["resumes"]
+                if profiling:
+                    phases.append(eng.phase_times())
+            torch.cuda.synchronize()
         return eng, [s.elapsed_time(e) for s, e in zip(starts, ends)], phases, resumes
 
     # timed region for `value`: no per-kernel events (an event between two
@@ -374,6 +396,11 @@ def run_gpu(args, spec, cfg, rank, world, local_rank):
             dev_s = reduce_([dev_s], dist.ReduceOp.MAX)[0]
         value = world * args.steps / dev_s
     stats = eng.device_stats[args.warmup:]
+    mc = eng.store._counters()   # HBM footprint of the final store
+    memory = {"store_bytes": mc["store_bytes"], "blocks": mc["block_count"], "vertex_records": mc["vertex_records"],
+              "bytes_per_cube": mc["store_bytes"] / max(1, 512 * mc["block_count"]),
+              "bytes_per_block": mc["store_bytes"] / max(1, mc["block_count"]),
+              "device_bytes_allocated": mc["device_bytes"], "paper_bytes_per_cube": 56}
     launches = sum(s["kernel_launches"] for s in stats)   # our kernels in the timed region
 
     # roofline: dominant kernel (largest share of the timed frames); the halo
@@ -415,11 +442,12 @@ def run_gpu(args, spec, cfg, rank, world, local_rank):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    t0 = time.perf_counter()
-    for k in range(args.steps):
-        e2.fuse_frame(host_np[args.warmup + k], poses[args.warmup + k])
-    torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - t0
+    with PausedGC():
+        t0 = time.perf_counter()
+        for k in range(args.steps):
+            e2.fuse_frame(host_np[args.warmup + k], poses[args.warmup + k])
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - t0
     if world > 1:
         e2e_s = reduce_([e2e_s], dist.ReduceOp.MAX)[0]
     # parity spot check of the timed engine vs the e2e engine (same frames)
@@ -437,11 +465,12 @@ def run_gpu(args, spec, cfg, rank, world, local_rank):
         for i in range(args.warmup):
             e3.fuse_frame_raw(raws[i], poses[i])
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for k in range(args.steps):
-            e3.fuse_frame_raw(raws[args.warmup + k], poses[args.warmup + k])
-        torch.cuda.synchronize()
-        raw_s = time.perf_counter() - t0
+        with PausedGC():
+            t0 = time.perf_counter()
+            for k in range(args.steps):
+                e3.fuse_frame_raw(raws[args.warmup + k], poses[args.warmup + k])
+            torch.cuda.synchronize()
+            raw_s = time.perf_counter() - t0
         e3.stats[-1].blocks_active   # (complete the last frame)
         raw_e2e = {"value": world * args.steps / raw_s, "unit": "frames/s",
                    "h2d_bytes_per_step": spec.width * spec.height * 2 + 256, "d2h_bytes_per_step": 512,
@@ -487,6 +516,7 @@ def run_gpu(args, spec, cfg, rank, world, local_rank):
         "gpu_launches": launches * world,
         "resumes_in_timed_region": resumes,
         "clocks": clk,
+        "memory": memory,
         "final_state": {"blocks": glob.blocks_active, "vertices": glob.vertices_live,
                         "triangles": glob.triangles_live, "e2e_state_match": bool(same)},
     }

@@ -158,6 +158,9 @@ typedef struct {
   int64_t block_capacity;        /* current device arena capacities */
   int64_t vertex_capacity;
   int64_t triangle_capacity;
+  int64_t vertex_records;        /* device vertex records in use (slots ever occupied) */
+  int64_t store_bytes;           /* HBM held by the stored blocks + their vertex records */
+  int64_t device_bytes;          /* HBM allocated by the engine (capacities, tables, lists) */
 } vm_counter_set;
 
 /* ---- lifecycle ------------------------------------------------------- */

@@ -77,7 +77,8 @@ class AuditC(C.Structure):
 COUNTER_FIELDS = ("block_count", "block_allocations", "vertex_count", "vertex_free",
                   "vertex_recycled_total", "vertex_allocation_events", "triangle_count",
                   "triangle_free", "triangle_recycled_total", "irregular_cube_count",
-                  "block_capacity", "vertex_capacity", "triangle_capacity")
+                  "block_capacity", "vertex_capacity", "triangle_capacity", "vertex_records",
+                  "store_bytes", "device_bytes")
 
 
 class CountersC(C.Structure):

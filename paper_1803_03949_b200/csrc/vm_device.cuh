@@ -5,10 +5,14 @@
 //   * block table: bucketed hash (8 CAS slots per bucket + locked overflow
 //     chains) mapping packed block coordinates to a dense block index;
 //   * per block (SoA, 8x8x8 cubes, C order x,y,z): tsdf f64, weight i32,
-//     type_prev/type_curr u8, and per owned edge slot (3 per cube): vertex
-//     birth frame i32 (-1 = empty slot), position along the edge axis f64,
-//     normal f64x3.  A vertex lives IN its edge slot (the paper's "cube owns
-//     its 3 edges"): allocation = claiming the slot, recycling = clearing it.
+//     type_prev/type_curr u8, and per owned edge slot (3 per cube): an
+//     occupancy bit, the position along the edge axis f64 and the slot's
+//     vertex-record handle i32.  A vertex lives IN its edge slot (the paper's
+//     "cube owns its 3 edges"): allocation = setting the occupancy bit,
+//     recycling = clearing it.  Birth frame and normal live in a compact
+//     vertex-record arena: a slot gets a record the first time it is occupied
+//     and keeps it (re-occupation reuses it), so the arena holds the slots
+//     ever used, not 1536 per block.
 //   * triangles are not stored: a cube's live triangles are always
 //     TRI_TABLE[type_curr] (the reference retriangulates exactly when the type
 //     changes, mesher.py:283-320), so triangle lists and vertex reference
@@ -62,6 +66,9 @@ struct alignas(16) Counters {
   int32_t fb_pending;    // face-normal fallback records of the last frame not yet applied
   int32_t nfree;         // block GC: evicted block indices on the free list
   int64_t evicted_total; // block GC: blocks evicted so far
+  int64_t a_hw;          // vertex records assigned: handles [0, a_hw) (slots keep theirs)
+  int32_t need_stage;    // where a halted frame resumes: 0 k_fuse_blocks (block heap), 1 k_retype_place (records)
+  int32_t pad0;
   // ---- per call ----------------------------------------------------------
   int32_t nvalid;
   int32_t nsteps;
@@ -138,6 +145,17 @@ struct FrameDev {
 
 // one hash slot: packed coordinate (-1 empty) and block index (-1 while the
 // inserting thread has not published it yet)
+// per-vertex record (the slot's handle indexes it): normal, birth frame
+struct alignas(32) VertexRec {
+  double nrm[3];
+  int32_t birth;
+  int32_t pad;
+};
+// vertex records one scope item can assign in a frame: its cubes own the
+// edges of the 9^3 points of its tile, 3 per point
+constexpr long long kRecsPerItem = 729 * 3;
+constexpr long long kRecChunk = 64;
+
 struct alignas(16) HashSlot {
   long long key;
   int32_t val;
@@ -177,18 +195,26 @@ struct DevState {
   int32_t *weight;      // [cap*512]
   uint32_t *vmask;      // [cap*16] weight > 0, one bit per cube corner sample (C order)
   uint8_t *tp, *tc;     // [cap*512]
-  int32_t *vbirth;      // [cap*1536] slot occupancy: birth frame, -1 empty
-  uint32_t *vocc;       // [cap*48] the same occupancy as bits (read and written by k_gc_normals)
+  int32_t *vh;          // [cap*1536] the slot's vertex record (-1: never occupied); kept when the slot empties
+  uint32_t *vrb;        // [cap*48] the slot has a record (vh >= 0), as bits (staged by k_gc_normals)
+  uint32_t *vocc;       // [cap*48] slot occupancy bits (read and written by k_gc_normals)
   uint32_t *vclaim;     // [cap*48] slots requested this frame (k_retype_place ORs, k_gc_normals applies + clears)
   double *vparam;       // [cap*1536] vertex coordinate along the edge axis
-  double *vnrm;         // [cap*1536*3]
+  VertexRec *vrec;      // [vrec_cap] vertex records (normal, birth)
+  long long vrec_cap;
+  // k_gc_normals hands out records from per-CTA chunks of kRecChunk (one
+  // atomic on a_hw per chunk, not per CTA and frame): CTA c's next free record
+  // and the end of its chunk at rec_chunk[2 c], [2 c + 1]
+  long long *rec_chunk;
+  int32_t rec_chunk_ctas;
   uint32_t *item_mask;  // [cap*16] explicit scope cube masks
   // strategy "partition" only (allocated on first use): per-slot request bytes
   // written by the parity passes with plain stores, and the retype's selection
   // (one byte per tile column, bit z) of each scope item
   uint8_t *vreq;        // [cap*1536]
   uint8_t *psel;        // [cap*64]
-  int4 *fallback;       // [cap*1536] fallback worklist: block, slot, 4 cube types, candidate mask
+  int4 *fallback;       // [fb_cap] fallback records of the last frame: block, slot, 4 cube types, candidate mask
+  int32_t fb_cap;       //   (a bounded ring: records past it are applied inline by k_gc_normals)
   long long max_vertices;
   // spatial partition: blocks are owned by hashed tiles
   // of 2^tile_shift blocks per axis; a rank also computes a 1-block margin

@@ -114,6 +114,7 @@ struct vm_engine {
   bool restore_calls = false;        // ... and hold nothing: a non-frame call restores the last frame's
   int64_t frame_of[2] = {0, 0};
   int last_resumes = 0;
+  int resume_launches = 0;   // kernels the resumes of the last settled frame launched
   int frame_launches = 0;   // kernels launched by the pending / last frame
   // pipelined submission (vm_fuse_frame_submit): the next frame's depth is
   // copied on a second stream into the other slot while the pending frame runs
@@ -253,21 +254,44 @@ static int grow_blocks(vm_engine *e, int64_t need) {
   TRY(dev_grow(&S.vmask, o * (kNC / 32), n * (kNC / 32), st));
   TRY(dev_grow(&S.tp, o * kNC, n * kNC, st));
   TRY(dev_grow(&S.tc, o * kNC, n * kNC, st));
-  TRY(dev_grow(&S.vbirth, o * kEV, n * kEV, st));
+  TRY(dev_grow(&S.vh, o * kEV, n * kEV, st));
+  CK(cudaMemsetAsync(S.vh + o * kEV, 0xFF, (n - o) * kEV * sizeof(int32_t), st));   // (no record yet)
+  TRY(dev_grow(&S.vrb, o * (kEV / 32), n * (kEV / 32), st));
+  CK(cudaMemsetAsync(S.vrb + o * (kEV / 32), 0, (n - o) * (kEV / 32) * sizeof(uint32_t), st));
   TRY(dev_grow(&S.vocc, o * (kEV / 32), n * (kEV / 32), st));
   TRY(dev_grow(&S.vclaim, o * (kEV / 32), n * (kEV / 32), st));
   TRY(dev_grow(&S.vparam, o * kEV, n * kEV, st));
-  TRY(dev_grow(&S.vnrm, o * kEV * 3, n * kEV * 3, st));
   TRY(dev_grow(&S.item_mask, 0, n * 16, st));
   if (S.vreq) {   // strategy "partition" buffers (zero request bytes for the new blocks)
     TRY(dev_grow(&S.vreq, o * kEV, n * kEV, st));
     CK(cudaMemsetAsync(S.vreq + o * kEV, 0, (n - o) * kEV, st));
     TRY(dev_grow(&S.psel, 0, n * 64, st));
   }
-  TRY(dev_grow(&S.fallback, 0, n * kEV, st));
   S.block_cap = (int32_t)cap;
   return VM_OK;
 }
+
+// Vertex-record arena: at least `need` records (grows geometrically; the
+// records are addressed by handle, so a copy keeps them valid)
+static int grow_records(vm_engine *e, int64_t need) {
+  DevState &S = e->S;
+  if (need <= S.vrec_cap) return VM_OK;
+  const int64_t cap = std::max<int64_t>(need + need / 4, (int64_t)S.vrec_cap * 2);
+  if (cap > INT32_MAX) return set_err(VM_ERR_CAPACITY, "vertex record arena exhausted (%lld)", (long long)need);
+  TRY(dev_grow(&S.vrec, (size_t)S.vrec_cap, (size_t)cap, e->stream));
+  S.vrec_cap = cap;
+  return VM_OK;
+}
+
+// HBM per stored block: tsdf f64, weight i32, weight > 0
+// bits, type_prev / type_curr u8 per cube; per edge slot: position f64, record
+// handle i32, occupancy / request / has-record bits; the explicit-scope mask
+constexpr size_t kBlockBytes = 8 * kNC + 4 * kNC + 4 * (kNC / 32) + 2 * kNC + 8 * kEV + 4 * kEV +
+                               3 * 4 * (kEV / 32) + 4 * 16;
+// per-block metadata, sized for the table's block limit: coordinate, neighbour
+// row, epoch stamps, slab / owner bytes, ghost / GC / free-list entries, scope
+// and halo list entries
+constexpr size_t kBlockMetaBytes = 16 + 27 * 4 + 3 * 4 + 1 + 1 + 4 + 4 + 4 + 4 + 4;
 
 static int read_counters(vm_engine *e) {
   CK(cudaMemcpyAsync(e->h_ctr, e->S.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, e->stream));
@@ -370,6 +394,33 @@ static void launch_retype(vm_engine *e, bool pdl, const FrameDev &F) {
 }
 static int gc_strategy_flag(const FrameDev &F) { return F.strategy == VM_STRATEGY_PARTITION ? G_PARTITION : 0; }
 
+static int clear_need(vm_engine *e) {
+  CK(cudaMemsetAsync(&e->S.ctr->need_stage, 0, sizeof(int32_t), e->stream));
+  CK(cudaMemsetAsync(&e->S.ctr->need, 0, sizeof(int32_t), e->stream));
+  return VM_OK;
+}
+
+// records a halted meshing segment may need (k_retype_place's bound, with the
+// counters just read back)
+static int64_t record_bound(vm_engine *e) {
+  const Counters &c = *e->h_ctr;
+  const int64_t items = (int64_t)c.ncollected + c.nslab + c.nexplicit;
+  return c.a_hw + std::min<int64_t>(kRecsPerItem * items, (int64_t)kEV * c.nblocks) +
+         2 * kRecChunk * e->S.rec_chunk_ctas + 1024;
+}
+
+// meshing segment: retype+place, gc+normals (a frame resumed for records)
+static int enqueue_meshing(vm_engine *e) {
+  const FrameDev F = *e->h_frame;
+  rec(e, PH_RETYPE);
+  launch_retype(e, true, F);
+  rec(e, PH_GC);
+  launch_gc(e, true, e->S.halo, &e->S.ctr->nhalo, 0,
+            (int)(G_GC | G_NORMALS | G_COMMIT | G_REQUIRE_ITEMS | G_SHARDED) | gc_strategy_flag(F));
+  rec(e, PH_END);
+  return check_launch();
+}
+
 // frame segment after collect: fuse (init/integrate/scope), retype+place, gc+normals
 static int enqueue_after_collect(vm_engine *e) {
   DevState &S = e->S;
@@ -394,11 +445,20 @@ static int complete_with_resume(vm_engine *e, int *resumes) {
     TRY(read_counters(e));
     TRY(error_from_counters(e));
     if (!e->h_ctr->need) return VM_OK;
-    TRY(grow_blocks(e, e->h_ctr->nblocks));
-    CK(cudaMemsetAsync(&e->S.ctr->need, 0, sizeof(int32_t), e->stream));
     if (resumes) (*resumes)++;
+    if (e->h_ctr->need_stage == 1) {   // vertex records: grow, resume at k_retype_place
+      TRY(grow_records(e, record_bound(e)));
+      TRY(clear_need(e));
+      TRY(enqueue_meshing(e));
+      e->frame_launches += 1 + meshing_launches(*e->h_frame);
+      e->resume_launches += 1 + meshing_launches(*e->h_frame);
+      continue;
+    }
+    TRY(grow_blocks(e, e->h_ctr->nblocks));
+    TRY(clear_need(e));
     TRY(enqueue_after_collect(e));
     e->frame_launches += 2 + meshing_launches(*e->h_frame);
+    e->resume_launches += 2 + meshing_launches(*e->h_frame);
   }
   return set_err(VM_ERR_CUDA, "resume loop did not converge");
 }
@@ -466,7 +526,7 @@ static int init_new_blocks(vm_engine *e) {
   TRY(error_from_counters(e));
   if (e->h_ctr->need) {
     TRY(grow_blocks(e, e->h_ctr->nblocks));
-    CK(cudaMemsetAsync(&e->S.ctr->need, 0, sizeof(int32_t), e->stream));
+    TRY(clear_need(e));
   }
   k_init_blocks<<<grid_blocks(e), kThreadsCube, 0, e->stream>>>(e->S, e->epoch);
   TRY(check_launch());
@@ -643,6 +703,12 @@ int vm_create(const vm_store_config *cfg, vm_engine **out) {
   }
   TRY(dev_alloc(&S.halo_sh, (size_t)kHaloShards * S.halo_sh_cap));
   TRY(dev_alloc(&S.ctr, 1, 0));
+  S.fb_cap = 1 << 16;   // fallback records kept for the next frame (~0.6 k per C2 frame; more are applied inline)
+  if (const char *cap = getenv("VOXMESH_B200_FALLBACK_CAP")) {   // (test hook: force inline fallbacks)
+    const long v = strtol(cap, nullptr, 10);
+    if (v >= 0 && v < S.fb_cap) S.fb_cap = (int32_t)v;
+  }
+  TRY(dev_alloc(&S.fallback, (size_t)std::max(S.fb_cap, 1)));
   uint8_t slab_sel[8];   // mesher.py:518-525
   for (int m = 0; m < 8; m++) {
     uint8_t bits = 0;
@@ -658,6 +724,8 @@ int vm_create(const vm_store_config *cfg, vm_engine **out) {
     e->grid_retype = std::max(1, occ) * e->sm_count;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gc_normals, kGT, kGcSmem));
     e->grid_gc = std::max(1, occ) * e->sm_count;
+    S.rec_chunk_ctas = e->grid_gc;
+    TRY(dev_alloc(&S.rec_chunk, 2 * (size_t)S.rec_chunk_ctas, 0));   // (empty chunks: next = end = 0)
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fuse_blocks, kFB, 0));
     e->grid_fuse = std::max(1, occ) * e->sm_count;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_collect, kCollectThreads, 0));
@@ -665,6 +733,9 @@ int vm_create(const vm_store_config *cfg, vm_engine **out) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_place_parity, kNT, 0));
     e->grid_parity = std::max(1, occ) * e->sm_count;
   }
+  // vertex records (grow on demand; a frame short of them resumes at k_retype_place)
+  S.vrec_cap = cfg->initial_vertices > 0 ? cfg->initial_vertices : (int64_t)1 << 20;
+  TRY(dev_alloc(&S.vrec, (size_t)S.vrec_cap));
   S.block_cap = 0;
   const int64_t ib = cfg->initial_blocks > 0 ? cfg->initial_blocks : 1024;
   TRY(grow_blocks(e, std::min<int64_t>(ib, S.max_blocks)));
@@ -679,7 +750,7 @@ int vm_destroy(vm_engine *e) {
   DevState &S = e->S;
   void *ptrs[] = {S.slots, S.ovf_head, S.ovf_lock, S.ovf_key, S.ovf_val, S.ovf_next, S.ovf_stamp, S.bcoord,
                   S.nbr, S.stamp_collect, S.stamp_halo, S.stamp_new, S.bowned, S.slab_bits, S.scope,
-                  S.halo, S.halo_sh, S.tsdf, S.weight, S.vmask, S.tp, S.tc, S.vbirth, S.vocc, S.vclaim, S.vparam, S.vnrm, S.item_mask, S.vreq, S.psel, S.fallback, e->d_rays,
+                  S.halo, S.halo_sh, S.tsdf, S.weight, S.vmask, S.tp, S.tc, S.vh, S.vrb, S.rec_chunk, S.vocc, S.vclaim, S.vparam, S.vrec, S.item_mask, S.vreq, S.psel, S.fallback, e->d_rays,
                   S.ctr, e->d_depth, e->d_scratch, S.ghost_src, e->d_ghost_counts, S.last_frame, S.free_list};
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -756,9 +827,9 @@ int vm_phase_times(vm_engine *e, double *ms, int n) {
 int vm_reserve(vm_engine *e, int64_t blocks, int64_t vertices, int64_t triangles) {
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
   TRY(settle_all(e));
-  (void)vertices;
-  (void)triangles;   // vertices live in edge slots, triangles are implicit
+  (void)triangles;   // triangles are implicit (derived from the cube types)
   if (blocks > e->S.block_cap) TRY(grow_blocks(e, std::min<int64_t>(blocks, e->S.max_blocks)));
+  if (vertices > 0) TRY(grow_records(e, vertices));
   return VM_OK;
 }
 
@@ -1017,6 +1088,7 @@ static int settle_slot(vm_engine *e, int slot, bool succ) {
   const int launched = e->frame_launches;
   e->ev = e->evs[slot];
   e->last_resumes = 0;
+  e->resume_launches = 0;
   int rc = VM_OK;
   e->restore_calls = true;   // (unhalted: the commit cleared the per-call counters)
   if (e->h_ctr->need || e->h_ctr->error) {
@@ -1044,7 +1116,7 @@ static int settle_slot(vm_engine *e, int slot, bool succ) {
     if (rc == VM_OK) {
       const FrameDev &Fs = e->f_saved[slot];
       e->settled.kernel_launches = 3 + meshing_launches(Fs) + (Fs.nsteps_fixed <= 0) +
-                                   (2 + meshing_launches(Fs)) * e->last_resumes +
+                                   e->resume_launches +
                                    (Fs.block_gc_age > 0 && Fs.frame > 0 && Fs.frame % Fs.block_gc_age == 0);
     }
   }
@@ -1396,8 +1468,14 @@ int vm_extract(vm_engine *e, const int32_t *scope_coords, const uint8_t *scope_m
     TRY(check_launch());
   }
   launch_retype(e, false, *e->h_frame);
-  // the halo given here need not hold every block a request went to: apply them all
   TRY(read_counters(e));
+  for (int guard = 0; e->h_ctr->need && e->h_ctr->need_stage == 1 && guard < 8; guard++) {
+    TRY(grow_records(e, record_bound(e)));   // (the retype stopped before any write)
+    TRY(clear_need(e));
+    launch_retype(e, false, *e->h_frame);
+    TRY(read_counters(e));
+  }
+  // the halo given here need not hold every block a request went to: apply them all
   k_apply_claims<<<grid_threads(e, (long long)e->h_ctr->nblocks * (kEV / 32), 256), 256, 0, e->stream>>>(
       e->S, e->h_ctr->nblocks, e->h_frame->frame, (int)(e->h_frame->strategy == VM_STRATEGY_PARTITION));
   launch_gc(e, false, e->S.halo, &e->S.ctr->nhalo, 0, (int)(G_GC | G_NORMALS | G_COMMIT | G_REQUIRE_ITEMS));
@@ -1544,8 +1622,17 @@ int vm_counters(vm_engine *e, vm_counter_set *out) {
   out->triangle_recycled_total = c.t_recycled;
   out->irregular_cube_count = c.irregular;
   out->block_capacity = e->S.block_cap;
-  out->vertex_capacity = (int64_t)e->S.block_cap * kEV;
+  out->vertex_capacity = e->S.vrec_cap;
   out->triangle_capacity = (int64_t)e->S.block_cap * kNC * 5;
+  out->vertex_records = c.a_hw;
+  const DevState &S = e->S;
+  out->store_bytes = (int64_t)(c.nblocks - c.nfree) * (int64_t)kBlockBytes + c.a_hw * (int64_t)sizeof(VertexRec);
+  out->device_bytes = (int64_t)S.block_cap * (int64_t)kBlockBytes + S.vrec_cap * (int64_t)sizeof(VertexRec) +
+                      (int64_t)S.max_blocks * (int64_t)kBlockMetaBytes +
+                      (int64_t)S.nbuckets * kSlotsPerBucket * (int64_t)sizeof(HashSlot) +
+                      (int64_t)S.nbuckets * 8 + (int64_t)S.ovf_cap * 20 +
+                      (int64_t)kHaloShards * S.halo_sh_cap * 4 + (int64_t)S.fb_cap * 16 +
+                      (S.vreq ? (int64_t)S.block_cap * (kEV + 64) : 0);
   return VM_OK;
 }
 
@@ -1747,9 +1834,21 @@ int vm_export_blocks(vm_engine *e, int32_t owned_only, int64_t *n_out, int32_t *
     if (weight) TRY(copy_sync(e, weight + k * kNC, S.weight + (size_t)i * kNC, 4 * kNC, cudaMemcpyDeviceToHost));
     if (tp) TRY(copy_sync(e, tp + k * kNC, S.tp + (size_t)i * kNC, kNC, cudaMemcpyDeviceToHost));
     if (tc) TRY(copy_sync(e, tc + k * kNC, S.tc + (size_t)i * kNC, kNC, cudaMemcpyDeviceToHost));
-    if (birth) TRY(copy_sync(e, birth + k * kEV, S.vbirth + (size_t)i * kEV, 4 * kEV, cudaMemcpyDeviceToHost));
     if (param) TRY(copy_sync(e, param + k * kEV, S.vparam + (size_t)i * kEV, 8 * kEV, cudaMemcpyDeviceToHost));
-    if (normal) TRY(copy_sync(e, normal + k * kEV * 3, S.vnrm + (size_t)i * kEV * 3, 24 * kEV, cudaMemcpyDeviceToHost));
+  }
+  if (birth || normal) {   // per-slot views of the vertex records
+    const size_t ns = sel.size();
+    void *buf;
+    TRY(scratch(e, ns * 4 + ns * kEV * (4 + 24) + 512, &buf));
+    int32_t *d_idx = (int32_t *)buf;
+    int32_t *d_birth = (int32_t *)((char *)buf + ((ns * 4 + 255) & ~(size_t)255));
+    double *d_nrm = (double *)((char *)d_birth + ((ns * kEV * 4 + 255) & ~(size_t)255));
+    CK(cudaMemcpyAsync(d_idx, sel.data(), ns * 4, cudaMemcpyHostToDevice, e->stream));
+    k_gather_slots<<<grid_threads(e, (long long)ns * kEV, 256), 256, 0, e->stream>>>(
+        S, d_idx, (int)ns, birth ? d_birth : nullptr, normal ? d_nrm : nullptr);
+    TRY(check_launch());
+    if (birth) TRY(copy_sync(e, birth, d_birth, ns * kEV * 4, cudaMemcpyDeviceToHost));
+    if (normal) TRY(copy_sync(e, normal, d_nrm, ns * kEV * 24, cudaMemcpyDeviceToHost));
   }
   return VM_OK;
 }
@@ -1781,14 +1880,30 @@ int vm_import_blocks(vm_engine *e, int64_t n, const int32_t *coords, const doubl
     if (tp) TRY(copy_sync(e, S.tp + i * kNC, tp + k * kNC, kNC, cudaMemcpyHostToDevice));
     if (tc) TRY(copy_sync(e, S.tc + i * kNC, tc + k * kNC, kNC, cudaMemcpyHostToDevice));
     if (birth) {
-      TRY(copy_sync(e, S.vbirth + i * kEV, birth + k * kEV, 4 * kEV, cudaMemcpyHostToDevice));
       uint32_t occ[kEV / 32] = {};
       for (int q = 0; q < kEV; q++)
         if (birth[k * kEV + q] >= 0) occ[q >> 5] |= 1u << (q & 31);
       TRY(copy_sync(e, S.vocc + i * (kEV / 32), occ, sizeof occ, cudaMemcpyHostToDevice));
     }
     if (param) TRY(copy_sync(e, S.vparam + i * kEV, param + k * kEV, 8 * kEV, cudaMemcpyHostToDevice));
-    if (normal) TRY(copy_sync(e, S.vnrm + i * kEV * 3, normal + k * kEV * 3, 24 * kEV, cudaMemcpyHostToDevice));
+  }
+  if (birth) {   // vertex records of the occupied slots
+    int64_t occupied = 0;
+    for (int64_t q = 0; q < n * kEV; q++) occupied += birth[q] >= 0;
+    TRY(read_counters(e));
+    TRY(grow_records(e, e->h_ctr->a_hw + occupied));
+    void *buf;
+    TRY(scratch(e, n * 4 + n * kEV * (4 + 24) + 512, &buf));
+    int32_t *d_idx = (int32_t *)buf;
+    int32_t *d_birth = (int32_t *)((char *)buf + ((n * 4 + 255) & ~(size_t)255));
+    double *d_nrm = (double *)((char *)d_birth + ((n * kEV * 4 + 255) & ~(size_t)255));
+    CK(cudaMemcpyAsync(d_idx, idx.data(), n * 4, cudaMemcpyHostToDevice, e->stream));
+    CK(cudaMemcpyAsync(d_birth, birth, n * kEV * 4, cudaMemcpyHostToDevice, e->stream));
+    if (normal) CK(cudaMemcpyAsync(d_nrm, normal, n * kEV * 24, cudaMemcpyHostToDevice, e->stream));
+    k_scatter_slots<<<grid_threads(e, (long long)n * kEV, 256), 256, 0, e->stream>>>(
+        e->S, d_idx, (int)n, d_birth, normal ? d_nrm : nullptr);
+    TRY(check_launch());
+    CK(cudaStreamSynchronize(e->stream));
   }
   return VM_OK;
 }
@@ -1922,6 +2037,14 @@ int vm_partition_frame_finish(vm_engine *e, const uint8_t *recv, const int32_t *
   TRY(check_launch());
   TRY(read_counters(e));
   TRY(error_from_counters(e));
+  for (int guard = 0; e->h_ctr->need && e->h_ctr->need_stage == 1 && guard < 8; guard++) {
+    TRY(grow_records(e, record_bound(e)));   // vertex records: resume at k_retype_place
+    TRY(clear_need(e));
+    TRY(enqueue_meshing(e));
+    e->frame_launches += 1 + meshing_launches(F);
+    TRY(read_counters(e));
+    TRY(error_from_counters(e));
+  }
   if (e->h_ctr->need) return set_err(VM_ERR_CUDA, "halo exchange: block heap not pre-sized");
   e->ev_rec[e->ev == e->evs[1]] = false;
   fill_stats(e, e->part_frame, out ? out : &e->settled);

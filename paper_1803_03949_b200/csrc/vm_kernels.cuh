@@ -314,13 +314,20 @@ __device__ __forceinline__ void fallback_normal_warp(const double *__restrict__ 
   }
 }
 
+// (the rare inline path of k_gc_normals: out of line, off its register budget)
+__device__ __noinline__ void fallback_normal_inline(const double *vparam, double cube_size, int nbr_lane,
+                                                    uint32_t types4, uint32_t cand, int4 bc, int slot_ci, int axis,
+                                                    double *dst) {
+  fallback_normal_warp(vparam, cube_size, nbr_lane, types4, cand, bc, slot_ci, axis, dst);
+}
+
 struct FallbackArgs {   // what the consumer touches (passed by value: no DevState copy in local memory)
   Counters *ctr;
   const int4 *fallback;
   const int32_t *nbr;
   const int4 *bcoord;
   const double *vparam;
-  double *vnrm;
+  VertexRec *vrec;
   double cube_size;
 };
 
@@ -330,12 +337,13 @@ struct FallbackArgs {   // what the consumer touches (passed by value: no DevSta
 __device__ __noinline__ void consume_fallbacks(const FallbackArgs S, int n, int first, int nwarps) {
   const int lane = threadIdx.x & 31;
   for (int f = first; f < n; f += nwarps) {
+    // record: block, slot | candidate mask << 11, the 4 cube types, the vertex record
     const int4 rec = __ldcg(S.fallback + f);
-    const int b = rec.x, sl = rec.y;
+    const int b = rec.x, sl = rec.y & 2047;
     const int nbr_lane = lane < 27 ? (lane == 13 ? b : __ldcg(S.nbr + (size_t)b * 27 + lane)) : -1;
     const int4 bc = __ldcg(S.bcoord + b);
-    fallback_normal_warp(S.vparam, S.cube_size, nbr_lane, (uint32_t)rec.z, (uint32_t)rec.w, bc, sl / 3, sl % 3,
-                         S.vnrm + 3 * ((size_t)b * kEV + sl));
+    fallback_normal_warp(S.vparam, S.cube_size, nbr_lane, (uint32_t)rec.z, (uint32_t)rec.y >> 11, bc, sl / 3,
+                         sl % 3, S.vrec[rec.w].nrm);
   }
 }
 
@@ -420,8 +428,8 @@ __global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, cons
     if (s_stop) return;
   }
   if (F.consume_fb && spare && (int)blockIdx.x >= nreg) {
-    const int nfb = ld_vol(&ctr->fb_pending);
-    consume_fallbacks(FallbackArgs{S.ctr, S.fallback, S.nbr, S.bcoord, S.vparam, S.vnrm, S.cube_size}, nfb,
+    const int nfb = min(ld_vol(&ctr->fb_pending), S.fb_cap);   // (records past the ring were applied inline)
+    consume_fallbacks(FallbackArgs{S.ctr, S.fallback, S.nbr, S.bcoord, S.vparam, S.vrec, S.cube_size}, nfb,
                       (blockIdx.x - nreg) * wpc + (t >> 5), ((int)gridDim.x - nreg) * wpc);
   }
   int nvalid = 0, nth = 0;
@@ -534,8 +542,8 @@ __global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, cons
     trace_item(S, TK_COLLECT, nth, 3);
   }
   if (F.consume_fb && !spare) {
-    const int nfb = ld_vol(&ctr->fb_pending);
-    consume_fallbacks(FallbackArgs{S.ctr, S.fallback, S.nbr, S.bcoord, S.vparam, S.vnrm, S.cube_size}, nfb,
+    const int nfb = min(ld_vol(&ctr->fb_pending), S.fb_cap);   // (records past the ring were applied inline)
+    consume_fallbacks(FallbackArgs{S.ctr, S.fallback, S.nbr, S.bcoord, S.vparam, S.vrec, S.cube_size}, nfb,
                       blockIdx.x * wpc + (t >> 5), (int)gridDim.x * wpc);
   }
   if (F.nsteps_fixed > 0) {   // valid-pixel count (k_depth_stats did not run): one atomic per CTA
@@ -578,10 +586,7 @@ __device__ __forceinline__ void init_block(const DevState &S, int b, int t) {
   S.weight[(size_t)b * kNC + t] = 0;
   S.tp[(size_t)b * kNC + t] = 0;
   S.tc[(size_t)b * kNC + t] = 0;
-  int32_t *vb = S.vbirth + (size_t)b * kEV;
-  vb[t] = -1;
-  vb[t + kNC] = -1;
-  vb[t + 2 * kNC] = -1;
+  // (the slots' vertex records stay: a reused block index keeps its handles)
   if (t < kEV / 32) {
     S.vocc[(size_t)b * (kEV / 32) + t] = 0u;
     S.vclaim[(size_t)b * (kEV / 32) + t] = 0u;
@@ -913,7 +918,28 @@ __global__ void __launch_bounds__(kNT, 18) k_retype_place(DevState S, const Fram
   __shared__ int s_pro[5];
   read_prologue(S, s_pro, &S.ctr->ncollected, &S.ctr->nslab, &S.ctr->nexplicit,
                 (int)blockIdx.x < S.max_blocks ? S.scope + blockIdx.x : nullptr);
-  if (s_pro[0]) return;
+  // Vertex-record capacity, before anything is written: this frame can give
+  // at most kRecsPerItem records per scope item (and never more than the
+  // stored blocks have slots).  Every CTA reads the same counters and takes
+  // the same decision; on a shortfall the frame stops here and the host grows
+  // the record arena and resumes it at this kernel (need_stage 1).
+  __shared__ int s_halt;
+  if (threadIdx.x == 0) {
+    int halt = s_pro[0];
+    if (!halt) {
+      const long long items = F.scope_mode != 0 ? s_pro[3] : (long long)s_pro[1] + s_pro[2];
+      const long long hw = (long long)__ldcg(reinterpret_cast<const unsigned long long *>(&S.ctr->a_hw));
+      const long long bound = min(kRecsPerItem * items, (long long)kEV * __ldcg(&S.ctr->nblocks));
+      if (hw + bound + 2 * kRecChunk * S.rec_chunk_ctas > S.vrec_cap) {   // (+ the gc CTAs' chunk runs)
+        halt = 1;
+        S.ctr->need_stage = 1;
+        atomicExch(&S.ctr->need, F.epoch);
+      }
+    }
+    s_halt = halt;
+  }
+  __syncthreads();
+  if (s_halt) return;
   // meshing starts here: every k_fuse_blocks CTA has completed (engine.py:127-156's split)
   if (blockIdx.x == 0 && threadIdx.x == 0) S.ctr->t_mesh_ns = gtimer();
   const int nc = s_pro[1];
@@ -1515,6 +1541,7 @@ struct GcItem {
   Resolved R;
   uint32_t occ[kEV / 32];               // slot occupancy bits
   uint32_t cl[kEV / 32];                // this frame's placement requests
+  uint32_t rb[kEV / 32];                // the slot has a vertex record
   __align__(16) uint32_t vm[27 * 16];   // weight > 0 bitmaps of the 27 neighbours
   __align__(16) uint8_t tt[81 * 16];    // type_curr over cube locals -1..7 (tt_idx)
   uint8_t inhalo[28];                   // neighbour is a halo block of this call
@@ -1573,7 +1600,8 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
   __shared__ GcItem G[kGW];
   __shared__ uint16_t s_la[kGW * kEV];   // occupied slots, then the failed-gradient ones (gc_entry)
   __shared__ uint16_t s_lv[kGW * kEV];   // surviving slots
-  __shared__ int s_nocc, s_nv, s_nfb;
+  __shared__ int s_nocc, s_nv, s_nfb, s_nin;
+  __shared__ long long s_recbase[3];   // this CTA's record run: chunk rest start, its length, new chunk start
   __shared__ int red[4 * kGW];
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   GcItem &I = G[w];
@@ -1604,7 +1632,7 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
       const ResolveRegs rr = resolve_load(S, Fr, bi, i, 0);
       resolve_store(S, Fr, rr, bi, i, n, 0, I.R);
     }
-    if (t == 0) { s_nocc = 0; s_nv = 0; s_nfb = 0; }
+    if (t == 0) { s_nocc = 0; s_nv = 0; s_nfb = 0; s_nin = 0; }
     __syncwarp();
     const bool live = I.R.mode > 0;
     const int b = I.R.b;
@@ -1612,6 +1640,7 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
       // stage occupancy + requests, types and halo flags (all copies in flight)
       for (int q = lane; q < kEV / 32; q += 32) {
         cp_async4(&I.occ[q], S.vocc + (size_t)b * (kEV / 32) + q, true);
+        cp_async4(&I.rb[q], S.vrb + (size_t)b * (kEV / 32) + q, true);
         if (mode & G_PARTITION) I.cl[q] = pack_requests(S.vreq + (size_t)b * kEV + q * 32);
         else cp_async4(&I.cl[q], S.vclaim + (size_t)b * (kEV / 32) + q, true);
       }
@@ -1646,23 +1675,31 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
     trace_sub(S, TK_GC, nth, 2);
     // requests, over the kGW blocks' bitmap words: a requested empty slot is
     // allocated (birth = frame, normal 0); every occupied slot is listed
+    constexpr int kReqRounds = (kGW * (kEV / 32) + kGT - 1) / kGT;
+    uint32_t rec_new[kReqRounds];   // allocated slots that have no vertex record yet
+    int n_rec = 0;
 #pragma unroll
-    for (int r = 0; r < (kGW * (kEV / 32) + kGT - 1) / kGT; r++) {
+    for (int r = 0; r < kReqRounds; r++) {
       const int wi = t + r * kGT;
       const int k = wi / (kEV / 32), wd = wi - k * (kEV / 32);
       uint32_t word = 0;
+      rec_new[r] = 0;
       if (wi < kGW * (kEV / 32) && G[k].R.mode > 0) {
         GcItem &J = G[k];
         const size_t bk = (size_t)J.R.b;
         const uint32_t claim = J.cl[wd], fresh = claim & ~J.occ[wd];
-        // (a new vertex's zero normal is written here only without the normals
-        // pass, which writes every surviving vertex's normal -- zero first
-        // where its stencil fails, for the fallback's "never set" test)
-        for (uint32_t m = fresh; m; m &= m - 1) {
-          const size_t q = bk * kEV + wd * 32 + __ffs(m) - 1;
-          S.vbirth[q] = F.frame;
-          if (!normals) { S.vnrm[3 * q] = 0.0; S.vnrm[3 * q + 1] = 0.0; S.vnrm[3 * q + 2] = 0.0; }
-        }
+        rec_new[r] = fresh & ~J.rb[wd];   // first occupation: a record is handed out below
+        n_rec += __popc(rec_new[r]);
+        // Birth and zero normal go into the slot's record: with the normals
+        // pass they are written there (it reads every surviving slot's record
+        // handle anyway, and writes every surviving vertex's normal -- zero
+        // first where its stencil fails, for the fallback's "never set" test)
+        if (!normals)
+          for (uint32_t m = fresh & J.rb[wd]; m; m &= m - 1) {
+            VertexRec &vr = S.vrec[S.vh[bk * kEV + wd * 32 + __ffs(m) - 1]];
+            vr.birth = F.frame;
+            vr.nrm[0] = 0.0; vr.nrm[1] = 0.0; vr.nrm[2] = 0.0;
+          }
         allocs += J.R.owned * __popc(fresh);   // counted by the slot's owning rank
         if (claim) {
           if (mode & G_PARTITION) clear_requests(S.vreq + bk * kEV + wd * 32);
@@ -1675,7 +1712,58 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
       int pos = smem_append(__popc(word), &s_nocc);
       for (uint32_t m = word; m; m &= m - 1) s_la[pos++] = gc_entry(k, wd * 32 + __ffs(m) - 1);
     }
-    __syncthreads();
+    // vertex records for first-time slots, from this CTA's chunk (capacity was
+    // checked by k_retype_place's prologue)
+    if (__syncthreads_or(n_rec)) {
+      int incl = n_rec;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+      }
+      if (lane == 31) red[w] = incl;
+      __syncthreads();
+      if (t == 0) {
+        int acc = 0;
+        for (int q = 0; q < kGW; q++) { const int c = red[q]; red[q] = acc; acc += c; }
+        long long *ch = S.rec_chunk + 2 * (blockIdx.x % S.rec_chunk_ctas);
+        const long long cur = ch[0], end = ch[1];
+        const long long rem = end - cur < acc ? end - cur : acc;   // the chunk's rest first,
+        long long nbase = 0;
+        if (rem < acc) {   // then a new chunk run
+          const long long want = (acc - rem + kRecChunk - 1) / kRecChunk * kRecChunk;
+          nbase = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(&ctr->a_hw), (unsigned long long)want);
+          ch[0] = nbase + (acc - rem);
+          ch[1] = nbase + want;
+        } else {
+          ch[0] = cur + acc;
+        }
+        s_recbase[0] = cur;
+        s_recbase[1] = rem;
+        s_recbase[2] = nbase;
+      }
+      __syncthreads();
+      const long long r_cur = s_recbase[0], r_rem = s_recbase[1], r_new = s_recbase[2];
+      long long j = red[w] + incl - n_rec;   // this thread's first record, as an index into the CTA's run
+#pragma unroll
+      for (int r = 0; r < kReqRounds; r++) {
+        if (!rec_new[r]) continue;
+        const int wi = t + r * kGT;
+        const int k = wi / (kEV / 32), wd = wi - k * (kEV / 32);
+        GcItem &J = G[k];
+        J.rb[wd] |= rec_new[r];   // (this thread's word only)
+        for (uint32_t m = rec_new[r]; m; m &= m - 1, j++) {
+          const long long h = j < r_rem ? r_cur + j : r_new + (j - r_rem);
+          S.vh[(size_t)J.R.b * kEV + wd * 32 + __ffs(m) - 1] = (int32_t)h;
+          if (!normals) {
+            S.vrec[h].birth = F.frame;
+            S.vrec[h].nrm[0] = 0.0; S.vrec[h].nrm[1] = 0.0; S.vrec[h].nrm[2] = 0.0;
+          }
+        }
+        S.vrb[(size_t)J.R.b * (kEV / 32) + wd] = J.rb[wd];
+      }
+      __syncthreads();   // (the handles are read by the normals pass; red is reused)
+    }
     trace_sub(S, TK_GC, nth, 3);
     // GC over the occupied list: a slot survives iff a cube around its edge
     // still has the edge in its mask (the 4 cubes at -du along u, -dw along w;
@@ -1702,8 +1790,7 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
 #pragma unroll
           for (int q = 0; q < 4; q++) ref |= edge_mask_of(ty[q]) >> cube_edge_of_slot(axis, q >> 1, q & 1);
           if (!(ref & 1u)) {
-            keep = false;
-            S.vbirth[(size_t)J.R.b * kEV + sl] = -1;
+            keep = false;   // (the slot keeps its vertex record for a later occupation)
             atomicAnd(&J.occ[sl >> 5], ~(1u << (sl & 31)));
             frees += J.R.owned;
           }
@@ -1726,7 +1813,7 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
       const int nv = s_nv;
       for (int p0 = 0; p0 < nv; p0 += 2 * kGT) {
         double v[2][12];
-        int slv[2], itv[2];
+        int slv[2], itv[2], hv[2];
         bool val[2];
 #pragma unroll
         for (int u = 0; u < 2; u++) {
@@ -1745,6 +1832,7 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
           // neighbours read a dummy in-bounds sample; weight > 0 from the staged
           // bitmaps (absent = 0)
           const size_t dummy = (size_t)(bj < 0 ? 0 : bj) * kNC;
+          hv[u] = slv[u] >= 0 ? S.vh[(size_t)bj * kEV + sl] : 0;   // the vertex record (requested with the samples)
           bool ok = slv[u] >= 0;
 #pragma unroll
           for (int d = 0; d < 3; d++) {
@@ -1781,12 +1869,14 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
                              __dmul_rn(param, v[u][4 * d + 2] - v[u][4 * d + 3]));
           const double nrm = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(g[0], g[0]), __dmul_rn(g[1], g[1])),
                                             __dmul_rn(g[2], g[2])));
+          const bool fresh = (J.cl[sl >> 5] >> (sl & 31)) & 1u;   // allocated by this call
+          if (fresh) S.vrec[hv[u]].birth = F.frame;
           if (val[u] && nrm > 1e-12) {
-            double *dst = S.vnrm + 3 * ((size_t)J.R.b * kEV + sl);
+            double *dst = S.vrec[hv[u]].nrm;
             dst[0] = g[0] / nrm; dst[1] = g[1] / nrm; dst[2] = g[2] / nrm;
           } else {
-            if ((J.cl[sl >> 5] >> (sl & 31)) & 1u) {   // allocated now: its normal starts at zero
-              double *dst = S.vnrm + 3 * ((size_t)J.R.b * kEV + sl);
+            if (fresh) {   // its normal starts at zero
+              double *dst = S.vrec[hv[u]].nrm;
               dst[0] = 0.0; dst[1] = 0.0; dst[2] = 0.0;
             }
             fallbacks += J.R.owned;
@@ -1797,14 +1887,17 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
       __syncthreads();
       trace_sub(S, TK_GC, nth, 1);
       // face-normal fallback records: the failed slots with their 4 cube types
-      // and candidate mask (staged tile, row, halo flags)
-      const int nfb = s_nfb;
-      for (int p = t; p < nfb; p += kGT) {
-        const uint16_t e = s_la[p];
+      // and candidate mask (staged tile, row, halo flags).  The record list is
+      // a bounded ring (fb_cap); records past it are applied right here, one
+      // warp each -- everything a fallback reads (types, vertex coordinates,
+      // neighbour rows, the vertex's own normal just written) is final once
+      // the frame's k_retype_place has completed.
+      auto fb_record = [&](uint16_t e, uint32_t &types4, uint32_t &cand) {
         const GcItem &J = G[e >> 11];
         const int sl = e & 2047;
         const int ci = sl / 3, axis = sl - 3 * ci;
-        uint32_t types4 = 0, cand = 0;
+        types4 = 0;
+        cand = 0;
 #pragma unroll
         for (int q = 0; q < 4; q++) {
           int l0, l1, l2;
@@ -1816,7 +1909,27 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
               J.inhalo[dir])
             cand |= 1u << q;
         }
-        S.fallback[atomicAdd(&ctr->fb_pending, 1)] = make_int4(J.R.b, sl, (int)types4, (int)cand);
+      };
+      const int nfb = s_nfb;
+      for (int p = t; p < nfb; p += kGT) {
+        const uint16_t e = s_la[p];
+        uint32_t types4, cand;
+        fb_record(e, types4, cand);
+        const int at = atomicAdd(&ctr->fb_pending, 1);
+        const int bb = G[e >> 11].R.b, sl = e & 2047;
+        if (at < S.fb_cap)
+          S.fallback[at] = make_int4(bb, sl | (int)(cand << 11), (int)types4, S.vh[(size_t)bb * kEV + sl]);
+        else s_lv[atomicAdd(&s_nin, 1)] = e;   // (the surviving list is spent)
+      }
+      __syncthreads();
+      for (int q = w; q < s_nin; q += kGW) {   // ring full: inline, one warp per record
+        const uint16_t e = s_lv[q];
+        const GcItem &J = G[e >> 11];
+        const int sl = e & 2047;
+        uint32_t types4, cand;
+        fb_record(e, types4, cand);
+        fallback_normal_inline(S.vparam, S.cube_size, lane < 27 ? J.R.nbr[lane] : -1, types4, cand, J.R.coord,
+                             sl / 3, sl % 3, S.vrec[S.vh[(size_t)J.R.b * kEV + sl]].nrm);
       }
     }
     trace_item(S, TK_GC, nth, 3);
@@ -1948,7 +2061,7 @@ __global__ void k_audit(DevState S, int nblocks, unsigned long long *sums) {
   for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < (long long)nblocks * kEV;
        q += (long long)gridDim.x * blockDim.x) {
     const int b = (int)(q / kEV), slot = (int)(q % kEV);
-    const bool o = S.vbirth[q] >= 0;
+    const bool o = (S.vocc[q >> 5] >> (q & 31)) & 1u;
     const bool r = slot_refcount(S, b, slot) > 0;
     occ += o;
     missing += r && !o;
@@ -2005,8 +2118,8 @@ __global__ void k_scatter_samples(DevState S, const int32_t *idx, int n, const d
 // apply pending face-normal fallback records (before the engine state is read
 // or changed outside fuse_frame)
 __global__ void __launch_bounds__(128) k_flush_fallbacks(DevState S) {
-  const int n = ld_vol(&S.ctr->fb_pending);
-  consume_fallbacks(FallbackArgs{S.ctr, S.fallback, S.nbr, S.bcoord, S.vparam, S.vnrm, S.cube_size}, n,
+  const int n = min(ld_vol(&S.ctr->fb_pending), S.fb_cap);
+  consume_fallbacks(FallbackArgs{S.ctr, S.fallback, S.nbr, S.bcoord, S.vparam, S.vrec, S.cube_size}, n,
                     blockIdx.x * 4 + (threadIdx.x >> 5), (int)gridDim.x * 4);
 }
 
@@ -2027,8 +2140,14 @@ __global__ void k_apply_claims(DevState S, int nblocks, int frame, int from_byte
     const long long b = q / (kEV / 32);
     for (uint32_t m = fresh; m; m &= m - 1) {
       const size_t sl = (size_t)q * 32 + __ffs(m) - 1;
-      S.vbirth[sl] = frame;
-      S.vnrm[3 * sl] = 0.0; S.vnrm[3 * sl + 1] = 0.0; S.vnrm[3 * sl + 2] = 0.0;
+      int h = S.vh[sl];
+      if (h < 0) {   // (first occupation: a new record; the caller's retype checked the capacity)
+        h = (int)atomicAdd((unsigned long long *)&S.ctr->a_hw, 1ull);
+        S.vh[sl] = h;
+        atomicOr(S.vrb + (sl >> 5), 1u << (sl & 31));
+      }
+      S.vrec[h].birth = frame;
+      S.vrec[h].nrm[0] = 0.0; S.vrec[h].nrm[1] = 0.0; S.vrec[h].nrm[2] = 0.0;
     }
     if (S.nranks <= 1 || S.bowned[b]) allocs += __popc(fresh);
     S.vocc[q] = old | claim;
@@ -2036,6 +2155,38 @@ __global__ void k_apply_claims(DevState S, int nblocks, int frame, int from_byte
   }
   allocs = warp_sum(allocs);
   if ((threadIdx.x & 31) == 0 && allocs) atomicAdd((unsigned long long *)&S.ctr->v_allocs, (unsigned long long)allocs);
+}
+
+// per-slot views of the vertex records of listed blocks (export): birth (-1
+// empty) and normal (0 when empty)
+__global__ void k_gather_slots(DevState S, const int32_t *idx, int n, int32_t *birth, double *normal) {
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < (long long)n * kEV;
+       q += (long long)gridDim.x * blockDim.x) {
+    const size_t sq = (size_t)idx[q / kEV] * kEV + (size_t)(q % kEV);
+    const bool occ = (S.vocc[sq >> 5] >> (sq & 31)) & 1u;
+    const int h = occ ? S.vh[sq] : -1;
+    if (birth) birth[q] = h >= 0 ? S.vrec[h].birth : -1;
+    if (normal)
+      for (int d = 0; d < 3; d++) normal[3 * q + d] = h >= 0 ? S.vrec[h].nrm[d] : 0.0;
+  }
+}
+
+// ... and back (import): every slot with birth >= 0 gets a record (the host
+// sized the arena and writes the occupancy bits)
+__global__ void k_scatter_slots(DevState S, const int32_t *idx, int n, const int32_t *birth, const double *normal) {
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < (long long)n * kEV;
+       q += (long long)gridDim.x * blockDim.x) {
+    if (birth[q] < 0) continue;
+    const size_t sq = (size_t)idx[q / kEV] * kEV + (size_t)(q % kEV);
+    int h = S.vh[sq];
+    if (h < 0) {
+      h = (int)atomicAdd((unsigned long long *)&S.ctr->a_hw, 1ull);
+      S.vh[sq] = h;
+      atomicOr(S.vrb + (sq >> 5), 1u << (sq & 31));
+    }
+    S.vrec[h].birth = birth[q];
+    for (int d = 0; d < 3; d++) S.vrec[h].nrm[d] = normal ? normal[3 * q + d] : 0.0;
+  }
 }
 
 // validity bitmap of listed blocks from their weights (after host writes)
@@ -2071,11 +2222,11 @@ __global__ void __launch_bounds__(kThreadsCube) k_compact_count(DevState S, cons
   __shared__ int wc[48];
   for (int i = blockIdx.x; i < nblocks; i += gridDim.x) {
     const int b = order[i];
-    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
-    for (int r = 0; r < 3; r++) {
-      const int s = r * kThreadsCube + t;
-      const unsigned ball = __ballot_sync(0xffffffffu, S.vbirth[(size_t)b * kEV + s] >= 0);
-      if (lane == 0) { occ_bits[(size_t)b * 48 + r * 16 + wid] = ball; wc[r * 16 + wid] = __popc(ball); }
+    const int t = threadIdx.x;
+    if (t < 48) {   // the occupancy words as they are
+      const uint32_t ball = S.vocc[(size_t)b * 48 + t];
+      occ_bits[(size_t)b * 48 + t] = ball;
+      wc[t] = __popc(ball);
     }
     __syncthreads();
     if (t == 0) {
@@ -2110,13 +2261,13 @@ __global__ void __launch_bounds__(kThreadsCube) k_compact_vertices(DevState S, c
     const int b = order[i];
     for (int s = threadIdx.x; s < kEV; s += blockDim.x) {
       const size_t q = (size_t)b * kEV + s;
-      const int birth = S.vbirth[q];
       int o = -1;
-      if (birth >= 0) {
+      if ((occ_bits[(size_t)b * 48 + (s >> 5)] >> (s & 31)) & 1u) {
+        const VertexRec &vr = S.vrec[S.vh[q]];
         o = slot_index(occ_bits, occ_pre, vbase_by_blk, b, s);
         slot_position(S, b, s, pos + 3 * (size_t)o);
-        for (int d = 0; d < 3; d++) nrm[3 * (size_t)o + d] = S.vnrm[3 * q + d];
-        ages[o] = frame - (long long)birth;
+        for (int d = 0; d < 3; d++) nrm[3 * (size_t)o + d] = vr.nrm[d];
+        ages[o] = frame - (long long)vr.birth;
       }
       if (ev_handles) ev_handles[q] = o;
     }
@@ -2170,7 +2321,8 @@ __global__ void __launch_bounds__(kThreadsCube) k_compact_triangles(DevState S, 
         const int ob = (dir == 13) ? b : S.nbr[(size_t)b * 27 + dir];
         const int s = ((ox & 7) * 64 + (oy & 7) * 8 + (oz & 7)) * 3 + c_e_axis[e];
         int m = -1;
-        if (ob >= 0 && S.vbirth[(size_t)ob * kEV + s] >= 0) m = slot_index(occ_bits, occ_pre, vbase_by_blk, ob, s);
+        if (ob >= 0 && ((S.vocc[(size_t)ob * 48 + (s >> 5)] >> (s & 31)) & 1u))
+          m = slot_index(occ_bits, occ_pre, vbase_by_blk, ob, s);
         else set_error(S, ERR_CONSISTENCY, 40, b);
         idx[3 * (size_t)o + k] = m;
       }

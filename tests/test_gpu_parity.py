@@ -129,12 +129,15 @@ def test_pipelined_engine_matches_reference_golden(name, tiny):
 
 @pytest.mark.parametrize("name", FIELD_SCENES)
 @pytest.mark.parametrize("strategy", ["serial", "claim", "partition"])
-def test_extract_fields_match_reference(name, strategy):
+@pytest.mark.parametrize("tiny", [False, True])
+def test_extract_fields_match_reference(name, strategy, tiny):
+    """extract_frame through the phase API; with a 16-record vertex arena the
+    retype stops at its capacity check and resumes after growth."""
     from paper_1803_03949_b200 import RefineParams, SpatialStore
     from paper_1803_03949_b200.mesher import extract_frame
     g = load_golden(name)
     cfg = cfg_from_golden(g)
-    st = SpatialStore(cfg["cube_size"])
+    st = SpatialStore(cfg["cube_size"], initial_vertices=16 if tiny else 0)
     coords = [tuple(c) for c in g["in_coords"].tolist()]
     st.set_block_samples(coords, g["in_tsdf"], g["in_weight"])
     scope = [(c, None) for c in sorted(coords)]
@@ -310,3 +313,40 @@ def test_halo_shard_spill_matches_reference_golden(name, monkeypatch):
     assert all(d["device_ms"] > 0 for d in eng.device_stats)
     _check_blocks(eng.store, g)
     _check_mesh(eng.compact(), g)
+
+
+@pytest.mark.parametrize("cap", ["0", "5"])
+@pytest.mark.parametrize("name", ["sphere_orbit", "room_noise_refine", "gc_carve"])
+def test_fallback_ring_overflow_applied_inline_matches_reference_golden(name, cap, monkeypatch):
+    """Face-normal fallback records live in a bounded ring until the next
+    frame applies them; records past it are applied inline by k_gc_normals.
+    With a 0- or 5-record ring (all or nearly all inline) every row, block and
+    the mesh, normals included, stay identical -- pipelined and synchronous."""
+    monkeypatch.setenv("VOXMESH_B200_FALLBACK_CAP", cap)
+    g = load_golden(name)
+    for pipelined in (False, True):
+        eng = _engine_from_golden(g, pipelined=pipelined)
+        rows = [eng.fuse_frame(g["depth"][i], _pose(g, i)) for i in range(len(g["depth"]))]
+        for i, row in enumerate(rows):
+            assert _stats_tuple(row) == tuple(g["stats"][i]), (name, i)
+        assert sum(d["fallback_normals"] for d in eng.device_stats) > int(cap)   # (the inline path ran)
+        _check_blocks(eng.store, g)
+        _check_mesh(eng.compact(), g)
+
+
+def test_vertex_records_are_compact_and_accounted():
+    """Birth and normal live in a vertex-record arena indexed by a per-slot
+    handle: a slot gets a record when first occupied and keeps it.  Records in
+    use cover the live vertices and stay far below 1536 per block; the store's
+    HBM accounting is blocks x per-block bytes + records x 32 B."""
+    g = load_golden("gc_carve")
+    eng = _engine_from_golden(g)
+    for i in range(len(g["depth"])):
+        eng.fuse_frame(g["depth"][i], _pose(g, i))
+    c = eng.store._counters()
+    live = eng.stats[-1].vertices_live
+    assert live <= c["vertex_records"] <= c["vertex_allocation_events"] + 2 * 64 * 148 * 8   # (+ chunk runs)
+    assert c["vertex_records"] < 0.25 * 1536 * c["block_count"]
+    per_block = 8 * 512 + 4 * 512 + 64 + 2 * 512 + 8 * 1536 + 4 * 1536 + 3 * 192 + 64
+    assert c["store_bytes"] == c["block_count"] * per_block + 32 * c["vertex_records"]
+    assert c["device_bytes"] >= c["store_bytes"]
