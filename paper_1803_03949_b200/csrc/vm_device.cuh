@@ -202,9 +202,10 @@ struct DevState {
   double *vparam;       // [cap*1536] vertex coordinate along the edge axis
   VertexRec *vrec;      // [vrec_cap] vertex records (normal, birth)
   long long vrec_cap;
-  // k_gc_normals hands out records from per-CTA chunks of kRecChunk (one
-  // atomic on a_hw per chunk, not per CTA and frame): CTA c's next free record
-  // and the end of its chunk at rec_chunk[2 c], [2 c + 1]
+  // k_gc_normals hands out records from per-CTA ranges, topped up 2 kRecChunk
+  // at a time (one atomic on a_hw every few frames per CTA, issued in its
+  // prologue): CTA c's two free ranges [rec_chunk[4 c], rec_chunk[4 c + 1]),
+  // [rec_chunk[4 c + 2], rec_chunk[4 c + 3])
   long long *rec_chunk;
   int32_t rec_chunk_ctas;
   uint32_t *item_mask;  // [cap*16] explicit scope cube masks

@@ -406,7 +406,7 @@ static int64_t record_bound(vm_engine *e) {
   const Counters &c = *e->h_ctr;
   const int64_t items = (int64_t)c.ncollected + c.nslab + c.nexplicit;
   return c.a_hw + std::min<int64_t>(kRecsPerItem * items, (int64_t)kEV * c.nblocks) +
-         2 * kRecChunk * e->S.rec_chunk_ctas + 1024;
+         4 * kRecChunk * e->S.rec_chunk_ctas + 1024;
 }
 
 // meshing segment: retype+place, gc+normals (a frame resumed for records)
@@ -725,7 +725,7 @@ int vm_create(const vm_store_config *cfg, vm_engine **out) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gc_normals, kGT, kGcSmem));
     e->grid_gc = std::max(1, occ) * e->sm_count;
     S.rec_chunk_ctas = e->grid_gc;
-    TRY(dev_alloc(&S.rec_chunk, 2 * (size_t)S.rec_chunk_ctas, 0));   // (empty chunks: next = end = 0)
+    TRY(dev_alloc(&S.rec_chunk, 4 * (size_t)S.rec_chunk_ctas, 0));   // (two empty record ranges per CTA)
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fuse_blocks, kFB, 0));
     e->grid_fuse = std::max(1, occ) * e->sm_count;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_collect, kCollectThreads, 0));
@@ -1624,9 +1624,14 @@ int vm_counters(vm_engine *e, vm_counter_set *out) {
   out->block_capacity = e->S.block_cap;
   out->vertex_capacity = e->S.vrec_cap;
   out->triangle_capacity = (int64_t)e->S.block_cap * kNC * 5;
-  out->vertex_records = c.a_hw;
   const DevState &S = e->S;
-  out->store_bytes = (int64_t)(c.nblocks - c.nfree) * (int64_t)kBlockBytes + c.a_hw * (int64_t)sizeof(VertexRec);
+  // records in use: handed out minus the gc CTAs' unused ranges
+  std::vector<long long> rr(4 * (size_t)S.rec_chunk_ctas);
+  TRY(copy_sync(e, rr.data(), S.rec_chunk, rr.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+  long long spare = 0;
+  for (size_t q = 0; q < rr.size(); q += 2) spare += rr[q + 1] > rr[q] ? rr[q + 1] - rr[q] : 0;
+  out->vertex_records = c.a_hw - spare;
+  out->store_bytes = (int64_t)(c.nblocks - c.nfree) * (int64_t)kBlockBytes + out->vertex_records * (int64_t)sizeof(VertexRec);
   out->device_bytes = (int64_t)S.block_cap * (int64_t)kBlockBytes + S.vrec_cap * (int64_t)sizeof(VertexRec) +
                       (int64_t)S.max_blocks * (int64_t)kBlockMetaBytes +
                       (int64_t)S.nbuckets * kSlotsPerBucket * (int64_t)sizeof(HashSlot) +

@@ -347,6 +347,26 @@ __device__ __noinline__ void consume_fallbacks(const FallbackArgs S, int n, int 
   }
 }
 
+// Top up k_gc_normals' per-CTA vertex-record ranges (kept >= kRecChunk, a run
+// of 2 kRecChunk appended when short): one thread per gc CTA index, run by the
+// next frame's k_collect off its critical path, so the gc never waits for the
+// record counter in the common case.
+__device__ __noinline__ void top_up_record_ranges(long long *ranges, int nctas, int64_t *a_hw, int first,
+                                                  int stride) {
+  for (int c = first; c < nctas; c += stride) {
+    long long *rr = ranges + 4 * c;
+    const longlong2 r0 = *reinterpret_cast<const longlong2 *>(rr), r1 = *reinterpret_cast<const longlong2 *>(rr + 2);
+    long long a0 = r0.x, e0 = r0.y;
+    if ((e0 - a0) + (r1.y - r1.x) >= kRecChunk) continue;
+    const long long nb = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(a_hw),
+                                              (unsigned long long)(2 * kRecChunk));
+    if (e0 <= a0) { a0 = r1.x; e0 = r1.y; }   // (range 1 moves up; both short cannot happen: range 1 is
+                                               //  consumed only after range 0)
+    *reinterpret_cast<longlong2 *>(rr) = make_longlong2(a0, e0);
+    *reinterpret_cast<longlong2 *>(rr + 2) = make_longlong2(nb, nb + 2 * kRecChunk);
+  }
+}
+
 // ------------------------------------------------------------ collect
 // fusion.py:95-106 + store.py:296-320.  A CTA covers a 64x8-pixel region (two
 // pixels per thread, coalesced rows).  The band samples' block keys are first
@@ -427,6 +447,9 @@ __global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, cons
     __syncthreads();
     if (s_stop) return;
   }
+  if (spare && (int)blockIdx.x >= nreg)
+    top_up_record_ranges(S.rec_chunk, S.rec_chunk_ctas, &ctr->a_hw, (blockIdx.x - nreg) * kCollectThreads + t,
+                         ((int)gridDim.x - nreg) * kCollectThreads);
   if (F.consume_fb && spare && (int)blockIdx.x >= nreg) {
     const int nfb = min(ld_vol(&ctr->fb_pending), S.fb_cap);   // (records past the ring were applied inline)
     consume_fallbacks(FallbackArgs{S.ctr, S.fallback, S.nbr, S.bcoord, S.vparam, S.vrec, S.cube_size}, nfb,
@@ -541,6 +564,9 @@ __global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, cons
     __syncthreads();   // the set is reset for the next region
     trace_item(S, TK_COLLECT, nth, 3);
   }
+  if (!spare)
+    top_up_record_ranges(S.rec_chunk, S.rec_chunk_ctas, &ctr->a_hw, blockIdx.x * kCollectThreads + t,
+                         (int)gridDim.x * kCollectThreads);
   if (F.consume_fb && !spare) {
     const int nfb = min(ld_vol(&ctr->fb_pending), S.fb_cap);   // (records past the ring were applied inline)
     consume_fallbacks(FallbackArgs{S.ctr, S.fallback, S.nbr, S.bcoord, S.vparam, S.vrec, S.cube_size}, nfb,
@@ -930,7 +956,7 @@ __global__ void __launch_bounds__(kNT, 18) k_retype_place(DevState S, const Fram
       const long long items = F.scope_mode != 0 ? s_pro[3] : (long long)s_pro[1] + s_pro[2];
       const long long hw = (long long)__ldcg(reinterpret_cast<const unsigned long long *>(&S.ctr->a_hw));
       const long long bound = min(kRecsPerItem * items, (long long)kEV * __ldcg(&S.ctr->nblocks));
-      if (hw + bound + 2 * kRecChunk * S.rec_chunk_ctas > S.vrec_cap) {   // (+ the gc CTAs' chunk runs)
+      if (hw + bound + 4 * kRecChunk * S.rec_chunk_ctas > S.vrec_cap) {   // (+ the gc CTAs' record ranges)
         halt = 1;
         S.ctr->need_stage = 1;
         atomicExch(&S.ctr->need, F.epoch);
@@ -1597,11 +1623,23 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
   const int live_items = (mode & G_REQUIRE_ITEMS) ? s_pro[1] : 1;
   const int nsh = sharded ? s_shp[kHaloShards] : 0;
   const int n = live_items > 0 ? nsh + (count_ptr ? s_pro[2] : count_const) : 0;
+  __shared__ long long s_rr[4];   // this CTA's free vertex records: ranges [s_rr[0], s_rr[1]), [s_rr[2], s_rr[3])
+  // a round's records: j < s_asg[1] -> s_asg[0] + j; j < s_asg3[0] -> s_asg[2] + j - s_asg[1];
+  // else s_asg3[1] + j - s_asg3[0]
+  __shared__ long long s_asg[3], s_asg3[2];
+  __shared__ int s_rr_dirty;
+  if (threadIdx.x == 0) s_rr_dirty = 0;
+  // this CTA's free vertex records (two ranges kept between calls), staged
+  // asynchronously; topped up at the CTA's end when short
+  long long *const rec_ranges = S.rec_chunk + 4 * (blockIdx.x % S.rec_chunk_ctas);
+  if (threadIdx.x == 0 && n > 0) {
+    cp_async16(&s_rr[0], rec_ranges, true);
+    cp_async16(&s_rr[2], rec_ranges + 2, true);
+  }
   __shared__ GcItem G[kGW];
   __shared__ uint16_t s_la[kGW * kEV];   // occupied slots, then the failed-gradient ones (gc_entry)
   __shared__ uint16_t s_lv[kGW * kEV];   // surviving slots
   __shared__ int s_nocc, s_nv, s_nfb, s_nin;
-  __shared__ long long s_recbase[3];   // this CTA's record run: chunk rest start, its length, new chunk start
   __shared__ int red[4 * kGW];
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   GcItem &I = G[w];
@@ -1726,24 +1764,40 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
       if (t == 0) {
         int acc = 0;
         for (int q = 0; q < kGW; q++) { const int c = red[q]; red[q] = acc; acc += c; }
-        long long *ch = S.rec_chunk + 2 * (blockIdx.x % S.rec_chunk_ctas);
-        const long long cur = ch[0], end = ch[1];
-        const long long rem = end - cur < acc ? end - cur : acc;   // the chunk's rest first,
-        long long nbase = 0;
-        if (rem < acc) {   // then a new chunk run
-          const long long want = (acc - rem + kRecChunk - 1) / kRecChunk * kRecChunk;
-          nbase = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(&ctr->a_hw), (unsigned long long)want);
-          ch[0] = nbase + (acc - rem);
-          ch[1] = nbase + want;
+        cp_async_wait_all();   // (s_rr)
+        long long a0 = s_rr[0], e0 = s_rr[1], a1 = s_rr[2], e1 = s_rr[3];
+        if ((e0 - a0) + (e1 - a1) < acc) {   // more than the CTA holds: merge its ranges' use with a new run
+          // (range 0 is used first: move range 1 behind it only when range 0 is empty)
+          if (e0 <= a0) { a0 = a1; e0 = e1; a1 = e1 = 0; }
+          const long long short_by = acc - (e0 - a0) - (e1 - a1);
+          const long long want = (short_by + 2 * kRecChunk - 1) / kRecChunk * kRecChunk;
+          const long long nb =
+              (long long)atomicAdd(reinterpret_cast<unsigned long long *>(&ctr->a_hw), (unsigned long long)want);
+          if (e1 > a1) {   // both ranges in use: they are consumed whole, the new run follows range 1
+            s_asg[0] = a0; s_asg[1] = e0 - a0; s_asg[2] = a1;
+            s_asg3[0] = (e0 - a0) + (e1 - a1); s_asg3[1] = nb;
+            a0 = nb + short_by; e0 = nb + want; a1 = e1 = 0;
+          } else {
+            s_asg[0] = a0; s_asg[1] = e0 - a0; s_asg[2] = nb;
+            s_asg3[0] = 1LL << 62;
+            a0 = nb + short_by; e0 = nb + want; a1 = e1 = 0;
+          }
         } else {
-          ch[0] = cur + acc;
+          s_asg[0] = a0; s_asg[1] = e0 - a0; s_asg[2] = a1;   // range 0 first, then range 1
+          s_asg3[0] = 1LL << 62;
+          // consume acc records; the rest stays for later rounds and calls
+          if (acc <= e0 - a0) {
+            a0 += acc;
+          } else {
+            a1 += acc - (e0 - a0);
+            a0 = a1; e0 = e1; a1 = e1 = 0;
+          }
         }
-        s_recbase[0] = cur;
-        s_recbase[1] = rem;
-        s_recbase[2] = nbase;
+        s_rr[0] = a0; s_rr[1] = e0; s_rr[2] = a1; s_rr[3] = e1;
+        s_rr_dirty = 1;
       }
       __syncthreads();
-      const long long r_cur = s_recbase[0], r_rem = s_recbase[1], r_new = s_recbase[2];
+      const long long r_cur = s_asg[0], r_rem = s_asg[1], r_new = s_asg[2], r_lim = s_asg3[0], r_ext = s_asg3[1];
       long long j = red[w] + incl - n_rec;   // this thread's first record, as an index into the CTA's run
 #pragma unroll
       for (int r = 0; r < kReqRounds; r++) {
@@ -1753,7 +1807,7 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
         GcItem &J = G[k];
         J.rb[wd] |= rec_new[r];   // (this thread's word only)
         for (uint32_t m = rec_new[r]; m; m &= m - 1, j++) {
-          const long long h = j < r_rem ? r_cur + j : r_new + (j - r_rem);
+          const long long h = j < r_rem ? r_cur + j : j < r_lim ? r_new + (j - r_rem) : r_ext + (j - r_lim);
           S.vh[(size_t)J.R.b * kEV + wd * 32 + __ffs(m) - 1] = (int32_t)h;
           if (!normals) {
             S.vrec[h].birth = F.frame;
@@ -1911,14 +1965,21 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
         }
       };
       const int nfb = s_nfb;
-      for (int p = t; p < nfb; p += kGT) {
-        const uint16_t e = s_la[p];
+      for (int p0 = 0; p0 < nfb; p0 += kGT) {   // (warp-uniform: one ring slot reservation per warp)
+        const int p = p0 + t;
+        const bool has = p < nfb;
+        const uint16_t e = has ? s_la[p] : (uint16_t)0;
+        const int bb = G[e >> 11].R.b, sl = e & 2047;
+        const int h = has ? S.vh[(size_t)bb * kEV + sl] : 0;   // (requested before the reservation)
+        const unsigned bal = __ballot_sync(0xffffffffu, has);
+        if (!bal) continue;
+        int at = 0;
+        if (lane == __ffs(bal) - 1) at = atomicAdd(&ctr->fb_pending, __popc(bal));
+        at = __shfl_sync(0xffffffffu, at, __ffs(bal) - 1) + __popc(bal & ((1u << lane) - 1));
+        if (!has) continue;
         uint32_t types4, cand;
         fb_record(e, types4, cand);
-        const int at = atomicAdd(&ctr->fb_pending, 1);
-        const int bb = G[e >> 11].R.b, sl = e & 2047;
-        if (at < S.fb_cap)
-          S.fallback[at] = make_int4(bb, sl | (int)(cand << 11), (int)types4, S.vh[(size_t)bb * kEV + sl]);
+        if (at < S.fb_cap) S.fallback[at] = make_int4(bb, sl | (int)(cand << 11), (int)types4, h);
         else s_lv[atomicAdd(&s_nin, 1)] = e;   // (the surviving list is spent)
       }
       __syncthreads();
@@ -1934,6 +1995,10 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
     }
     trace_item(S, TK_GC, nth, 3);
     __syncthreads();   // the items' shared state is rewritten by the next round
+  }
+  if (threadIdx.x == 0 && s_rr_dirty) {   // the ranges' rest (the next frame's k_collect tops them up)
+    *reinterpret_cast<longlong2 *>(rec_ranges) = make_longlong2(s_rr[0], s_rr[1]);
+    *reinterpret_cast<longlong2 *>(rec_ranges + 2) = make_longlong2(s_rr[2], s_rr[3]);
   }
   trace_count(S, TK_GC, nth);
   trace_at(S, TK_GC, 28);
