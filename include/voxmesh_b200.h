@@ -114,6 +114,8 @@ typedef struct {
   int64_t resumes;        /* arena growths that required a resume this frame */
   int64_t kernel_launches;/* kernels this library launched for the frame */
   int64_t blocks_evicted; /* block GC: blocks evicted so far (0 with block GC off) */
+  int64_t overlapped;     /* 1: this frame's k_collect ran under the previous frame's k_gc_normals
+                             (frame overlap, pipelined submission back to back) */
   double device_ms;       /* device time of the frame (CUDA events) */
   double fusion_ms;       /* collect + integrate (engine.py:127-132 split) */
   double meshing_ms;      /* scope .. normals (engine.py:134-144 split) */

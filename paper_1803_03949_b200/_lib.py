@@ -55,7 +55,8 @@ STATS_FIELDS = ("frame", "blocks_active", "vertices_live", "triangles_live",
                 "valid_pixels", "nsteps", "collected_blocks", "new_blocks", "scope_blocks",
                 "halo_blocks", "active_cubes", "edge_placements", "new_vertices", "changed_cubes",
                 "triangles_freed", "triangles_allocated", "vertices_freed", "normals_computed",
-                "fallback_normals", "refined_cubes", "resumes", "kernel_launches", "blocks_evicted")
+                "fallback_normals", "refined_cubes", "resumes", "kernel_launches", "blocks_evicted",
+                "overlapped")
 
 
 class Stats(C.Structure):

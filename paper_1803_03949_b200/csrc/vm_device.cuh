@@ -22,6 +22,7 @@
 // Numeric contract: compiled with --fmad=false; the only FMAs are explicit
 // __fma_rn chains restating numpy/OpenBLAS 3x3 products (SURVEY.md appx A).
 #pragma once
+#include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -68,18 +69,28 @@ struct alignas(16) Counters {
   int64_t evicted_total; // block GC: blocks evicted so far
   int64_t a_hw;          // vertex records assigned: handles [0, a_hw) (slots keep theirs)
   int32_t need_stage;    // where a halted frame resumes: 0 k_fuse_blocks (block heap), 1 k_retype_place (records)
-  int32_t pad0;
+  int32_t pad0[3];
   // ---- per call ----------------------------------------------------------
+  // The collect counters (written by k_collect / k_depth_stats and the block
+  // allocations).  The next frame's k_collect may run under this frame's
+  // k_gc_normals (frame overlap): so k_gc_normals saves
+  // them (sv_*) and clears them at its START, before it lets the next frame
+  // launch, and its commit snapshots the saved values and clears only the
+  // fields from `nslab` on.
   int32_t nvalid;
   int32_t nsteps;
-  unsigned long long maxnorm_bits;
   int32_t ncollected;
   int32_t nnew;
+  unsigned long long maxnorm_bits;
+  unsigned long long t_start_ns;   // %globaltimer: k_collect (or k_depth_stats) start
+  // ---- per call, cleared by k_gc_normals' commit ----------------------------
+  // (one 16-byte word: the meshing kernels' prologues read it with one load)
   int32_t nslab;
-  int32_t nhalo;
   int32_t nexplicit;
   int32_t nitems_live;
+  int32_t nhalo;
   int32_t done_gc;
+  int32_t nsend;                   // halo exchange: boundary blocks packed for the other ranks
   int64_t v_allocs;
   int64_t v_frees;
   int64_t placements;
@@ -92,13 +103,21 @@ struct alignas(16) Counters {
   int64_t fallbacks;
   int64_t refined;
   int32_t nhalo_sh[kHaloShards];   // halo shard fill counts (may exceed halo_sh_cap: clamp)
-  unsigned long long t_start_ns;   // %globaltimer: k_collect start, k_gc_normals commit
-  unsigned long long t_end_ns;
+  unsigned long long t_end_ns;     // k_gc_normals commit
   unsigned long long t_mesh_ns;    // k_retype_place start (after integration): fusion | meshing split
-  int32_t nsend;                   // halo exchange: boundary blocks packed for the other ranks
-  int32_t pad1;
+  // the frame's collect counters and block counts, saved by k_gc_normals at its start
+  int32_t sv_nvalid, sv_nsteps, sv_ncollected, sv_nnew;
+  unsigned long long sv_maxnorm_bits, sv_t_start_ns;
+  int32_t sv_nblocks, sv_nfree;
+  int64_t sv_nblocks_owned;
 };
 static_assert(sizeof(Counters) % 16 == 0, "snapshots are copied in 16-byte words");
+static_assert(offsetof(Counters, nvalid) % 16 == 0 && offsetof(Counters, ncollected) == offsetof(Counters, nvalid) + 8 &&
+              offsetof(Counters, t_start_ns) == offsetof(Counters, nvalid) + 24, "collect region: 2 words");
+static_assert(offsetof(Counters, nslab) % 16 == 0 && offsetof(Counters, nitems_live) == offsetof(Counters, nslab) + 8,
+              "prologue word: nslab, nexplicit, nitems_live, nhalo");
+static_assert(offsetof(Counters, sv_nvalid) % 16 == 0, "saved collect region: 16-byte words");
+static_assert(offsetof(Counters, error) == 8 && offsetof(Counters, need) == 12, "head word: nblocks, ovf, error, need");
 
 // Per-call parameters in device memory (a captured frame graph replays with
 // new poses / depth pointers).
@@ -123,6 +142,14 @@ struct FrameDev {
   int32_t consume_fb;   // fuse_frame: k_collect applies the previous frame's fallback records
   int32_t reset_after;  // k_gc_normals' commit clears the per-call counters after its snapshot
   int32_t strategy;     // VM_STRATEGY_*: 2 = partition (8 parity passes of plain stores, k_place_parity)
+  // Frame overlap: overlap != 0 -- this k_collect was
+  // launched right behind the previous frame's k_gc_normals, which lets it
+  // start once every gc CTA is running: it skips cudaGridDependencySynchronize
+  // (it touches nothing the gc reads or writes) and runs the work that does
+  // depend on the previous frame (fallback records, record ranges, the
+  // snapshot publish) only after *S.gc_done reaches wait_epoch.
+  int32_t overlap;
+  int32_t wait_epoch;
   Counters *snap;       // non-null: k_gc_normals' commit copies the counter block here (device)
   // non-null: k_collect copies the previous frame's snapshot (pub_src) to the
   // host's mapped buffer (pub_dst) and then writes pub_id to *pub_seq, the
@@ -230,6 +257,7 @@ struct DevState {
   int32_t *free_list;   // [max_blocks] evicted block indices (block GC)
   const int32_t *ghost_counts;   // [nranks] records per rank of the current exchange
   Counters *ctr;
+  int32_t *gc_done;     // epoch of the last k_gc_normals commit (outside Counters: host restores leave it)
   unsigned long long *trace;   // per-CTA phase timestamps (vm_set_trace), null = off
 };
 

@@ -113,6 +113,13 @@ struct vm_engine {
   bool ctr_clean = false;            // the per-call counters are zero (a frame's commit cleared them)
   bool restore_calls = false;        // ... and hold nothing: a non-frame call restores the last frame's
   int64_t frame_of[2] = {0, 0};
+  // Frame overlap: the stream's last operation is the k_gc_normals (epoch
+  // ov_epoch) of a frame launch_frame queued -- the next frame's k_collect may
+  // then start under it (FrameDev::overlap).  Every other entry point clears it.
+  bool ov_ready = false;
+  int32_t ov_epoch = 0;
+  bool ov_of[2] = {false, false};   // the slot's frame was launched overlapped
+  bool no_overlap = getenv("VOXMESH_B200_NO_OVERLAP") != nullptr;   // (A/B switch)
   int last_resumes = 0;
   int resume_launches = 0;   // kernels the resumes of the last settled frame launched
   int frame_launches = 0;   // kernels launched by the pending / last frame
@@ -434,7 +441,8 @@ static int enqueue_after_collect(vm_engine *e) {
   launch_retype(e, true, F);
   rec(e, PH_GC);
   launch_gc(e, true, S.halo, &S.ctr->nhalo, 0,
-            (int)(G_GC | G_NORMALS | G_COMMIT | G_REQUIRE_ITEMS | G_SHARDED) | gc_strategy_flag(F));
+            (int)(G_GC | G_NORMALS | G_COMMIT | G_REQUIRE_ITEMS | G_SHARDED | (F.reset_after ? G_OVERLAP : 0)) |
+                gc_strategy_flag(F));
   rec(e, PH_END);
   return check_launch();
 }
@@ -703,6 +711,7 @@ int vm_create(const vm_store_config *cfg, vm_engine **out) {
   }
   TRY(dev_alloc(&S.halo_sh, (size_t)kHaloShards * S.halo_sh_cap));
   TRY(dev_alloc(&S.ctr, 1, 0));
+  TRY(dev_alloc(&S.gc_done, 4, 0));
   S.fb_cap = 1 << 16;   // fallback records kept for the next frame (~0.6 k per C2 frame; more are applied inline)
   if (const char *cap = getenv("VOXMESH_B200_FALLBACK_CAP")) {   // (test hook: force inline fallbacks)
     const long v = strtol(cap, nullptr, 10);
@@ -745,13 +754,14 @@ int vm_create(const vm_store_config *cfg, vm_engine **out) {
 }
 
 int vm_destroy(vm_engine *e) {
+  if (e) e->ov_ready = false;   // (frame overlap: only a frame right behind a frame)
   if (!e) return VM_OK;
   cudaStreamSynchronize(e->stream);
   DevState &S = e->S;
   void *ptrs[] = {S.slots, S.ovf_head, S.ovf_lock, S.ovf_key, S.ovf_val, S.ovf_next, S.ovf_stamp, S.bcoord,
                   S.nbr, S.stamp_collect, S.stamp_halo, S.stamp_new, S.bowned, S.slab_bits, S.scope,
                   S.halo, S.halo_sh, S.tsdf, S.weight, S.vmask, S.tp, S.tc, S.vh, S.vrb, S.rec_chunk, S.vocc, S.vclaim, S.vparam, S.vrec, S.item_mask, S.vreq, S.psel, S.fallback, e->d_rays,
-                  S.ctr, e->d_depth, e->d_scratch, S.ghost_src, e->d_ghost_counts, S.last_frame, S.free_list};
+                  S.ctr, S.gc_done, e->d_depth, e->d_scratch, S.ghost_src, e->d_ghost_counts, S.last_frame, S.free_list};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   free_compacted(e->comp);
@@ -777,6 +787,7 @@ int vm_destroy(vm_engine *e) {
 }
 
 int vm_set_stream(vm_engine *e, void *stream) {
+  if (e) e->ov_ready = false;   // (frame overlap: only a frame right behind a frame)
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
   TRY(settle_all(e));
   CK(cudaStreamSynchronize(e->stream));
@@ -804,6 +815,7 @@ int vm_set_trace(vm_engine *e, void *device_buffer) {
 }
 
 int vm_set_profiling(vm_engine *e, int on) {
+  if (e) e->ov_ready = false;   // (frame overlap: only a frame right behind a frame)
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
   e->profiling = on != 0;
   return VM_OK;
@@ -812,6 +824,7 @@ int vm_set_profiling(vm_engine *e, int on) {
 // per-kernel device times of the last frame (profiling mode), ms:
 // depth_stats, collect, fuse_blocks, retype_place, gc_normals
 int vm_phase_times(vm_engine *e, double *ms, int n) {
+  if (e) e->ov_ready = false;   // (frame overlap: only a frame right behind a frame)
   if (!e || !ms) return set_err(VM_ERR_INPUT, "null argument");
   TRY(settle(e));
   CK(cudaEventSynchronize(e->ev[PH_END]));
@@ -825,6 +838,7 @@ int vm_phase_times(vm_engine *e, double *ms, int n) {
 }
 
 int vm_reserve(vm_engine *e, int64_t blocks, int64_t vertices, int64_t triangles) {
+  if (e) e->ov_ready = false;   // (frame overlap: only a frame right behind a frame)
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
   TRY(settle_all(e));
   (void)triangles;   // triangles are implicit (derived from the cube types)
@@ -959,16 +973,32 @@ static int launch_frame(vm_engine *e, int slot) {
   e->fslot = slot;
   e->ev = e->evs[slot];
   e->ev_rec[slot] = e->profiling;
+  // Frame overlap: this frame's k_collect may run under the previous frame's
+  // k_gc_normals when that kernel is the stream's last operation and nothing
+  // else runs first (no counter reset, block GC or depth-stats pass, no
+  // per-kernel events); a vertex-pool limit makes the gc commit raise, so it
+  // keeps the frames apart too
+  const bool gc_frame = F.block_gc_age > 0 && F.frame > 0 && F.frame % F.block_gc_age == 0;
+  // (and only on the engine's own stream: a caller's kernel queued on a shared
+  // stream between the frames could write what this k_collect reads, and it
+  // skips the grid-dependency wait)
+  const bool overlap = e->ov_ready && e->own_stream && e->ctr_clean && !e->profiling && F.nsteps_fixed > 0 &&
+                       !gc_frame && e->S.max_vertices <= 0 && !e->no_overlap;
+  const int32_t wait_epoch = overlap ? e->ov_epoch : 0;
+  e->ov_ready = false;
   if (!e->ctr_clean) TRY(reset_call_counters(e));
   cudaStream_t st = e->stream;
   rec(e, PH_DEPTH);
   e->frame_launches = 3 + meshing_launches(F);   // collect, fuse, retype (+ parity passes), gc (+ depth stats)
-  if (F.block_gc_age > 0 && F.frame > 0 && F.frame % F.block_gc_age == 0) {
+  if (gc_frame) {
     // opt-in block GC, before the frame allocates (its pops reuse the indices)
     k_block_gc<<<e->sm_count * 8, 256, 0, st>>>(e->S, F.frame, F.block_gc_age);
     e->frame_launches++;
   }
   FrameDev Fc = F;   // (collect's copy: a raw frame converted by k_depth_stats is f64 now)
+  Fc.overlap = overlap ? 1 : 0;
+  e->ov_of[slot] = overlap;
+  Fc.wait_epoch = wait_epoch;
   if (F.nsteps_fixed <= 0) {
     k_depth_stats<<<grid_blocks(e), 256, 0, st>>>(e->S, F);
     e->frame_launches++;
@@ -990,6 +1020,8 @@ static int launch_frame(vm_engine *e, int slot) {
   e->ctr_clean = true;
   e->pending = 1;
   e->pending_frame = e->frame_of[slot];
+  e->ov_ready = !e->profiling;   // (the stream ends with this frame's k_gc_normals)
+  e->ov_epoch = F.epoch;
   return VM_OK;
 }
 
@@ -1001,6 +1033,7 @@ int vm_fuse_frame_enqueue(vm_engine *e, const double *depth, int32_t h, int32_t 
   if (cfg->strategy < 0 || cfg->strategy > 2) return set_err(VM_ERR_VALUE, "unknown strategy %d", cfg->strategy);
   if (cfg->trunc < e->S.cube_size) return set_err(VM_ERR_VALUE, "truncation band must be at least one cube");
   const double *dd;
+  if (!depth_on_device) e->ov_ready = false;   // (a host copy goes first)
   TRY(stage_depth(e, depth, h, w, depth_on_device, &dd));
   fill_frame_host(e, dd, h, w, intr, pose);
   FrameDev &F = *e->h_frame;
@@ -1015,6 +1048,7 @@ int vm_fuse_frame_enqueue(vm_engine *e, const double *depth, int32_t h, int32_t 
   F.scope_mode = 0;
   F.strategy = cfg->strategy;
   TRY(ensure_partition_bufs(e, cfg->strategy));
+  if (!e->norm_valid) e->ov_ready = false;   // (ensure_rays launches its own kernel)
   TRY(ensure_rays(e, h, w));
   F.nsteps_fixed = fixed_nsteps(e, cfg->trunc);
   F.block_gc_age = cfg->block_gc_age > 0 ? cfg->block_gc_age : 0;
@@ -1031,6 +1065,7 @@ int vm_fuse_frame_enqueue(vm_engine *e, const double *depth, int32_t h, int32_t 
 }
 
 int vm_fuse_frame_finish(vm_engine *e, vm_stats *out) {
+  if (e) e->ov_ready = false;   // (frame overlap: only a frame right behind a frame)
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
   if (!e->pending) return set_err(VM_ERR_INPUT, "no frame pending");
   e->pending = 0;
@@ -1042,6 +1077,7 @@ int vm_fuse_frame_finish(vm_engine *e, vm_stats *out) {
 int vm_fuse_frame(vm_engine *e, const double *depth, int32_t h, int32_t w, int32_t depth_on_device,
                   const vm_intrinsics *intr, const vm_pose *pose, const vm_frame_config *cfg,
                   int64_t frame_index, vm_stats *out) {
+  if (e) e->ov_ready = false;   // (frame overlap: only a frame right behind a frame)
   TRY(vm_fuse_frame_enqueue(e, depth, h, w, depth_on_device, intr, pose, cfg, frame_index));
   return vm_fuse_frame_finish(e, out);
 }
@@ -1092,6 +1128,7 @@ static int settle_slot(vm_engine *e, int slot, bool succ) {
   int rc = VM_OK;
   e->restore_calls = true;   // (unhalted: the commit cleared the per-call counters)
   if (e->h_ctr->need || e->h_ctr->error) {
+    e->ov_ready = false;     // (the resume queues stream operations)
     e->ctr_clean = false;    // (halted: not cleared)
     e->restore_calls = false;
     if (succ) {
@@ -1102,7 +1139,10 @@ static int settle_slot(vm_engine *e, int slot, bool succ) {
     }
     rc = complete_with_resume(e, &e->last_resumes);
   }
-  if (rc == VM_OK) fill_stats(e, e->frame_of[slot], &e->settled);
+  if (rc == VM_OK) {
+    fill_stats(e, e->frame_of[slot], &e->settled);
+    e->settled.overlapped = e->ov_of[slot] && !e->last_resumes;
+  }
   if (succ) {
     e->pending = 0;
     if (rc == VM_OK && e->last_resumes) {
@@ -1170,6 +1210,7 @@ int vm_fuse_frame_submit(vm_engine *e, const double *depth, int32_t h, int32_t w
       for (int i = 0; i < 2; i++) CK(cudaEventCreateWithFlags(&e->ev_copy[i], cudaEventDisableTiming));
     }
     if (bytes > e->slot_cap) {
+      e->ov_ready = false;
       TRY(settle(e));   // (rare) reallocation: nothing may be reading the slots
       CK(cudaStreamSynchronize(e->copy_stream));
       for (int i = 0; i < 2; i++) {
@@ -1186,7 +1227,10 @@ int vm_fuse_frame_submit(vm_engine *e, const double *depth, int32_t h, int32_t w
   // 2. this frame's kernels, ordered after its copy, queued behind the pending
   //    frame's; 3. the pending frame completes (its stats are kept for
   //    vm_fuse_frame_result) while this one keeps the GPU busy
-  if (sl >= 0) CK(cudaStreamWaitEvent(e->stream, e->ev_copy[sl], 0));
+  if (sl >= 0) {
+    e->ov_ready = false;   // (an event wait on the stream: the frames stay apart)
+    CK(cudaStreamWaitEvent(e->stream, e->ev_copy[sl], 0));
+  }
   const bool prev = e->pending != 0;
   const int pslot = e->fslot;
   e->pending = 0;
@@ -1224,6 +1268,7 @@ int vm_fuse_frame_submit_raw(vm_engine *e, const uint16_t *raw, int32_t h, int32
     for (int i = 0; i < 2; i++) CK(cudaEventCreateWithFlags(&e->ev_copy[i], cudaEventDisableTiming));
   }
   if (npix * sizeof(double) > e->slot_cap || npix * sizeof(uint16_t) > e->raw_cap) {
+    e->ov_ready = false;
     TRY(settle(e));   // (rare) reallocation: nothing may be reading the slots
     CK(cudaStreamSynchronize(e->copy_stream));
     for (int i = 0; i < 2; i++) {
@@ -1242,7 +1287,10 @@ int vm_fuse_frame_submit_raw(vm_engine *e, const uint16_t *raw, int32_t h, int32
     CK(cudaEventRecord(e->ev_copy[sl], e->copy_stream));
     dr = e->d_raw[sl];
   }
-  if (!raw_on_device) CK(cudaStreamWaitEvent(e->stream, e->ev_copy[sl], 0));
+  if (!raw_on_device) {
+    e->ov_ready = false;   // (an event wait on the stream: the frames stay apart)
+    CK(cudaStreamWaitEvent(e->stream, e->ev_copy[sl], 0));
+  }
   e->raw_next = dr;
   e->raw_scale = depth_scale;
   const bool prev = e->pending != 0;
@@ -1272,6 +1320,7 @@ int vm_fuse_frame_result(vm_engine *e, vm_stats *out) {
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
   if (!e->settled_valid) {
     if (!e->pending) return set_err(VM_ERR_INPUT, "no frame submitted");
+    e->ov_ready = false;   // (settling queues stream operations)
     TRY(settle(e));
   }
   if (out) *out = e->settled;
@@ -1283,6 +1332,7 @@ int vm_fuse_frame_result(vm_engine *e, vm_stats *out) {
 int vm_collect(vm_engine *e, const double *depth, int32_t h, int32_t w, int32_t depth_on_device,
                const vm_intrinsics *intr, const vm_pose *pose, double trunc, double max_range,
                int64_t *n_out) {
+  if (e) e->ov_ready = false;   // (frame overlap: only a frame right behind a frame)
   if (!e || !intr || !pose) return set_err(VM_ERR_INPUT, "null argument");
   TRY(settle_all(e));
   const double *dd;
@@ -1305,6 +1355,7 @@ int vm_collect(vm_engine *e, const double *depth, int32_t h, int32_t w, int32_t 
 }
 
 int vm_get_collected(vm_engine *e, int32_t *coords_out, int64_t n) {
+  if (e) e->ov_ready = false;   // (frame overlap: only a frame right behind a frame)
   if (!e || (!coords_out && n)) return set_err(VM_ERR_INPUT, "null argument");
   TRY(settle_all(e));
   if (n == 0) return VM_OK;
@@ -1325,6 +1376,7 @@ int vm_get_collected(vm_engine *e, int32_t *coords_out, int64_t n) {
 int vm_integrate(vm_engine *e, const int32_t *coords, int64_t n, const double *depth, int32_t h, int32_t w,
                  int32_t depth_on_device, const vm_intrinsics *intr, const vm_pose *pose, double trunc,
                  double max_range, int64_t weight_cap) {
+  if (e) e->ov_ready = false;   // (frame overlap: only a frame right behind a frame)
   if (!e || !intr || !pose) return set_err(VM_ERR_INPUT, "null argument");
   TRY(settle_all(e));
   const double *dd;
@@ -1366,6 +1418,7 @@ int vm_integrate(vm_engine *e, const int32_t *coords, int64_t n, const double *d
 
 int vm_scope_halo(vm_engine *e, int64_t *n_scope, int32_t *scope_coords, uint8_t *scope_masks,
                   int64_t *n_halo, int32_t *halo_coords) {
+  if (e) e->ov_ready = false;   // (frame overlap: only a frame right behind a frame)
   if (!e || !n_scope || !n_halo) return set_err(VM_ERR_INPUT, "null argument");
   TRY(settle_all(e));
   CK(cudaMemsetAsync(&e->S.ctr->nslab, 0, sizeof(int32_t), e->stream));
@@ -1430,6 +1483,7 @@ int vm_scope_halo(vm_engine *e, int64_t *n_scope, int32_t *scope_coords, uint8_t
 int vm_extract(vm_engine *e, const int32_t *scope_coords, const uint8_t *scope_masks, int64_t n_scope,
                const int32_t *halo_coords, int64_t n_halo, int64_t frame_index, int32_t strategy,
                int32_t refine, double epsilon, int64_t *out2) {
+  if (e) e->ov_ready = false;   // (frame overlap: only a frame right behind a frame)
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
   TRY(settle_all(e));
   if (strategy < 0 || strategy > 2) return set_err(VM_ERR_VALUE, "unknown strategy %d", strategy);
@@ -1491,6 +1545,7 @@ int vm_extract(vm_engine *e, const int32_t *scope_coords, const uint8_t *scope_m
 }
 
 int vm_garbage_collect(vm_engine *e, const int32_t *coords, int64_t n, int64_t *freed) {
+  if (e) e->ov_ready = false;   // (frame overlap: only a frame right behind a frame)
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
   TRY(settle_all(e));
   TRY(reset_call_counters(e));
@@ -1505,6 +1560,7 @@ int vm_garbage_collect(vm_engine *e, const int32_t *coords, int64_t n, int64_t *
 }
 
 int vm_compute_normals(vm_engine *e, const int32_t *coords, int64_t n) {
+  if (e) e->ov_ready = false;   // (frame overlap: only a frame right behind a frame)
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
   TRY(settle_all(e));
   TRY(reset_call_counters(e));
@@ -1521,6 +1577,7 @@ int vm_compute_normals(vm_engine *e, const int32_t *coords, int64_t n) {
 
 int vm_refine_eval(vm_engine *e, const uint8_t *t_curr, const uint8_t *t_prev, const double *corners,
                    int64_t n, double epsilon, int32_t *out) {
+  if (e) e->ov_ready = false;   // (frame overlap: only a frame right behind a frame)
   if (!e || !t_curr || !t_prev || !corners || !out) return set_err(VM_ERR_INPUT, "null argument");
   TRY(settle_all(e));
   if (n <= 0) return VM_OK;
@@ -1542,6 +1599,7 @@ int vm_refine_eval(vm_engine *e, const uint8_t *t_curr, const uint8_t *t_prev, c
 
 int vm_block_in_frustum(vm_engine *e, const int32_t *coords, int64_t n, const vm_pose *pose,
                         const vm_intrinsics *intr, uint8_t *out) {
+  if (e) e->ov_ready = false;   // (frame overlap: only a frame right behind a frame)
   if (!e || !coords || !pose || !intr || !out) return set_err(VM_ERR_INPUT, "null argument");
   TRY(settle_all(e));
   if (n <= 0) return VM_OK;
@@ -1560,6 +1618,7 @@ int vm_block_in_frustum(vm_engine *e, const int32_t *coords, int64_t n, const vm
 
 // ---- store access -----------------------------------------------------------
 int vm_set_blocks(vm_engine *e, const int32_t *coords, int64_t n, const double *tsdf, const int32_t *weight) {
+  if (e) e->ov_ready = false;   // (frame overlap: only a frame right behind a frame)
   if (!e || (!coords && n)) return set_err(VM_ERR_INPUT, "null argument");
   TRY(settle_all(e));
   if (n <= 0) return VM_OK;
@@ -1594,6 +1653,7 @@ int vm_set_blocks(vm_engine *e, const int32_t *coords, int64_t n, const double *
 }
 
 int vm_lookup(vm_engine *e, const int32_t *coords, int64_t n, uint8_t *out) {
+  if (e) e->ov_ready = false;   // (frame overlap: only a frame right behind a frame)
   if (!e || ((!coords || !out) && n)) return set_err(VM_ERR_INPUT, "null argument");
   TRY(settle_all(e));
   if (n <= 0) return VM_OK;
@@ -1607,6 +1667,7 @@ int vm_lookup(vm_engine *e, const int32_t *coords, int64_t n, uint8_t *out) {
 }
 
 int vm_counters(vm_engine *e, vm_counter_set *out) {
+  if (e) e->ov_ready = false;   // (frame overlap: only a frame right behind a frame)
   if (!e || !out) return set_err(VM_ERR_INPUT, "null argument");
   TRY(settle_all(e));
   TRY(read_counters(e));
@@ -1654,6 +1715,7 @@ static int copy_rows(vm_engine *e, void *dst, const void *src, size_t row_bytes,
 
 int vm_snapshot_blocks(vm_engine *e, int64_t n, int32_t *coords, double *tsdf, int32_t *weight, uint8_t *tp,
                        uint8_t *tc, int32_t *ev, int32_t *tri) {
+  if (e) e->ov_ready = false;   // (frame overlap: only a frame right behind a frame)
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
   TRY(settle_all(e));
   TRY(read_counters(e));
@@ -1709,6 +1771,7 @@ int vm_snapshot_blocks(vm_engine *e, int64_t n, int32_t *coords, double *tsdf, i
 // order, live..count-1 the free entries of the reference's arena accounting
 int vm_snapshot_vertices(vm_engine *e, int64_t n, double *pos, double *nrm, int32_t *ref, int32_t *birth,
                          uint8_t *alive, int32_t *free_stack) {
+  if (e) e->ov_ready = false;   // (frame overlap: only a frame right behind a frame)
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
   TRY(settle_all(e));
   TRY(read_counters(e));
@@ -1756,6 +1819,7 @@ int vm_snapshot_vertices(vm_engine *e, int64_t n, double *pos, double *nrm, int3
 }
 
 int vm_snapshot_triangles(vm_engine *e, int64_t n, int32_t *verts, uint8_t *alive, int32_t *free_stack) {
+  if (e) e->ov_ready = false;   // (frame overlap: only a frame right behind a frame)
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
   TRY(settle_all(e));
   TRY(read_counters(e));
@@ -1776,6 +1840,7 @@ int vm_snapshot_triangles(vm_engine *e, int64_t n, int32_t *verts, uint8_t *aliv
 
 // ---- outputs ------------------------------------------------------------------
 int vm_irregular_count(vm_engine *e, int64_t *out) {
+  if (e) e->ov_ready = false;   // (frame overlap: only a frame right behind a frame)
   if (!e || !out) return set_err(VM_ERR_INPUT, "null argument");
   TRY(settle_all(e));
   TRY(read_counters(e));
@@ -1796,6 +1861,7 @@ int vm_irregular_count(vm_engine *e, int64_t *out) {
 }
 
 int vm_compact(vm_engine *e, int64_t current_frame, int64_t *n_vertices, int64_t *n_triangles) {
+  if (e) e->ov_ready = false;   // (frame overlap: only a frame right behind a frame)
   if (!e || !n_vertices || !n_triangles) return set_err(VM_ERR_INPUT, "null argument");
   TRY(settle_all(e));
   TRY(run_compaction(e, current_frame, false));
@@ -1805,6 +1871,7 @@ int vm_compact(vm_engine *e, int64_t current_frame, int64_t *n_vertices, int64_t
 }
 
 int vm_compact_fetch(vm_engine *e, double *pos, double *nrm, int64_t *ages, int32_t *idx) {
+  if (e) e->ov_ready = false;   // (frame overlap: only a frame right behind a frame)
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
   const Compacted &c = e->comp;
   if (c.nv) {
@@ -1818,6 +1885,7 @@ int vm_compact_fetch(vm_engine *e, double *pos, double *nrm, int64_t *ages, int3
 
 int vm_export_blocks(vm_engine *e, int32_t owned_only, int64_t *n_out, int32_t *coords, double *tsdf,
                      int32_t *weight, uint8_t *tp, uint8_t *tc, int32_t *birth, double *param, double *normal) {
+  if (e) e->ov_ready = false;   // (frame overlap: only a frame right behind a frame)
   if (!e || !n_out) return set_err(VM_ERR_INPUT, "null argument");
   TRY(settle_all(e));
   TRY(read_counters(e));
@@ -1861,6 +1929,7 @@ int vm_export_blocks(vm_engine *e, int32_t owned_only, int64_t *n_out, int32_t *
 int vm_import_blocks(vm_engine *e, int64_t n, const int32_t *coords, const double *tsdf, const int32_t *weight,
                      const uint8_t *tp, const uint8_t *tc, const int32_t *birth, const double *param,
                      const double *normal) {
+  if (e) e->ov_ready = false;   // (frame overlap: only a frame right behind a frame)
   if (!e || (n && !coords)) return set_err(VM_ERR_INPUT, "null argument");
   TRY(settle_all(e));
   if (n <= 0) return VM_OK;
@@ -1923,6 +1992,7 @@ int vm_partition_frame_begin(vm_engine *e, const double *depth, int32_t h, int32
                              const vm_intrinsics *intr, const vm_pose *pose, const vm_frame_config *cfg,
                              int64_t frame_index, uint8_t *send, int64_t send_cap, int64_t *n_send,
                              int64_t *n_owned_collected) {
+  if (e) e->ov_ready = false;   // (frame overlap: only a frame right behind a frame)
   if (!e || !intr || !pose || !cfg || !n_send || !n_owned_collected) return set_err(VM_ERR_INPUT, "null argument");
   if (!e->S.halo_exchange) return set_err(VM_ERR_INPUT, "engine not created in halo-exchange mode");
   if (cfg->strategy < 0 || cfg->strategy > 2) return set_err(VM_ERR_VALUE, "unknown strategy %d", cfg->strategy);
@@ -1992,6 +2062,7 @@ int vm_partition_frame_begin(vm_engine *e, const double *depth, int32_t h, int32
 }
 
 int vm_partition_repack(vm_engine *e, uint8_t *send, int64_t send_cap, int64_t *n_send) {
+  if (e) e->ov_ready = false;   // (frame overlap: only a frame right behind a frame)
   if (!e || !n_send) return set_err(VM_ERR_INPUT, "null argument");
   if (!e->part_active) return set_err(VM_ERR_INPUT, "no partition frame begun");
   CK(cudaMemsetAsync(&e->S.ctr->nsend, 0, sizeof(int32_t), e->stream));
@@ -2008,6 +2079,7 @@ int vm_partition_repack(vm_engine *e, uint8_t *send, int64_t send_cap, int64_t *
 // frame (k_retype_place, k_gc_normals with the counter commit).
 int vm_partition_frame_finish(vm_engine *e, const uint8_t *recv, const int32_t *counts, int32_t nranks,
                               int64_t max_count, vm_stats *out) {
+  if (e) e->ov_ready = false;   // (frame overlap: only a frame right behind a frame)
   if (!e || !counts || (max_count > 0 && !recv)) return set_err(VM_ERR_INPUT, "null argument");
   if (!e->part_active) return set_err(VM_ERR_INPUT, "no partition frame begun");
   if (nranks != e->S.nranks || nranks > kMaxRanks) return set_err(VM_ERR_INPUT, "rank count mismatch");
@@ -2061,6 +2133,7 @@ int vm_partition_frame_finish(vm_engine *e, const uint8_t *recv, const int32_t *
 // Distributed compaction, per rank: sort the owned blocks, count their
 // vertices / triangles and slot occupancy (k_compact_count over the owned list).
 int vm_partition_compact_begin(vm_engine *e, int64_t *n_owned) {
+  if (e) e->ov_ready = false;   // (frame overlap: only a frame right behind a frame)
   if (!e || !n_owned) return set_err(VM_ERR_INPUT, "null argument");
   NvtxRange nvtx_("vm_partition_compact_begin");
   TRY(settle_all(e));
@@ -2102,6 +2175,7 @@ __global__ static void k_gather_occ(const int32_t *order, int n, const uint32_t 
 }
 
 int vm_partition_compact_meta(vm_engine *e, uint64_t *keys, int32_t *vcnt, int32_t *tcnt, uint32_t *occ) {
+  if (e) e->ov_ready = false;   // (frame overlap: only a frame right behind a frame)
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
   auto &p = e->pc;
   if (p.nown == 0) return VM_OK;
@@ -2130,6 +2204,7 @@ int vm_partition_compact_fill(vm_engine *e, const uint64_t *gkeys, const int64_t
                               const uint32_t *gocc, const int32_t *gocc_pre, int64_t n_global,
                               const int32_t *my_global, int64_t current_frame, double *pos, double *nrm,
                               int64_t *ages, int32_t *idx) {
+  if (e) e->ov_ready = false;   // (frame overlap: only a frame right behind a frame)
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
   NvtxRange nvtx_("vm_partition_compact_fill");
   auto &p = e->pc;
@@ -2172,6 +2247,7 @@ int vm_partition_compact_fill(vm_engine *e, const uint64_t *gkeys, const int64_t
 // but empty slot and a zero-ref live vertex as an occupied but unreferenced
 // slot; conservation compares the pool counters with full recounts.
 int vm_audit(vm_engine *e, vm_audit_report *out) {
+  if (e) e->ov_ready = false;   // (frame overlap: only a frame right behind a frame)
   if (!e || !out) return set_err(VM_ERR_INPUT, "null argument");
   TRY(settle_all(e));
   TRY(read_counters(e));

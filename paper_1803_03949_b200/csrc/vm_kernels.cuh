@@ -27,7 +27,9 @@ enum { F_INIT = 1, F_INTEGRATE = 2, F_SCOPE = 4, F_HALO = 8, F_GHOST = 16 };
 // halo-exchange record: coordinate, then the block's 512 tsdf and 512 weights
 constexpr size_t kGhostRec = 16 + 8 * 512 + 4 * 512;
 enum { G_GC = 1, G_NORMALS = 2, G_COMMIT = 4, G_REQUIRE_ITEMS = 8, G_SHARDED = 16,
-       G_PARTITION = 32 };   // G_PARTITION: requests are k_place_parity's bytes (S.vreq)
+       G_PARTITION = 32,     // G_PARTITION: requests are k_place_parity's bytes (S.vreq)
+       G_OVERLAP = 64 };     // frame path: save + clear the collect counters, then let the next frame's
+                             // k_collect launch (cudaTriggerProgrammaticLaunchCompletion)
 
 // error and need are adjacent: one 8-byte load
 __device__ __forceinline__ bool halted(const DevState &S) {
@@ -89,6 +91,21 @@ __device__ __forceinline__ void cp_async16(void *dst, const void *src, bool vali
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(valid ? 16 : 0));
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+__device__ __forceinline__ int ld_acquire(const int32_t *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Frame overlap: the CTA waits until the previous frame's k_gc_normals has
+// committed (its epoch in *S.gc_done; every commit writes it, halted or not)
+__device__ __forceinline__ void wait_prev_gc(const DevState &S, const FrameDev &F) {
+  if (F.wait_epoch <= 0) return;
+  if (threadIdx.x == 0)
+    while (ld_acquire(S.gc_done) < F.wait_epoch) __nanosleep(200);
+  __syncthreads();
+}
 
 // Publish the previous frame's counter snapshot to the host (k_collect, one CTA)
 __device__ __forceinline__ void publish_snapshot(const FrameDev &F) {
@@ -400,12 +417,21 @@ __device__ __forceinline__ int collect_block(const DevState &S, const FrameDev &
 }
 
 __global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, const FrameDev F) {
-  cudaGridDependencySynchronize();   // PDL: wait for the previous kernel of the frame
+  // PDL: wait for the previous kernel -- except behind the previous frame's
+  // k_gc_normals (F.overlap): nothing below reads or writes what that kernel
+  // does, save the parts that first wait for its commit (wait_prev_gc)
+  if (!F.overlap) cudaGridDependencySynchronize();
   trace_at(S, TK_COLLECT, 0);
   trace_span(S, 0, F.frame, false);
   Counters *ctr = S.ctr;
-  if (blockIdx.x == 0 && threadIdx.x == 0 && F.nsteps_fixed > 0) ctr->t_start_ns = gtimer();
-  if (F.pub_src && blockIdx.x == gridDim.x - 1) publish_snapshot(F);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && F.nsteps_fixed > 0) {   // (not when it stops at the guard)
+    const int2 h = __ldcg(reinterpret_cast<const int2 *>(&ctr->error));
+    if (!(h.x != 0 || (h.y != 0 && h.y != F.epoch))) ctr->t_start_ns = gtimer();
+  }
+  if (F.pub_src && blockIdx.x == gridDim.x - 1) {   // (the last CTA to be dispatched)
+    wait_prev_gc(S, F);
+    publish_snapshot(F);
+  }
   int nsteps = F.nsteps_fixed;
   if (nsteps <= 0) {
     if (ld_vol(&ctr->nvalid) == 0) return;
@@ -447,6 +473,7 @@ __global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, cons
     __syncthreads();
     if (s_stop) return;
   }
+  if (spare && (int)blockIdx.x >= nreg) wait_prev_gc(S, F);
   if (spare && (int)blockIdx.x >= nreg)
     top_up_record_ranges(S.rec_chunk, S.rec_chunk_ctas, &ctr->a_hw, (blockIdx.x - nreg) * kCollectThreads + t,
                          ((int)gridDim.x - nreg) * kCollectThreads);
@@ -564,6 +591,7 @@ __global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, cons
     __syncthreads();   // the set is reset for the next region
     trace_item(S, TK_COLLECT, nth, 3);
   }
+  if (!spare) wait_prev_gc(S, F);
   if (!spare)
     top_up_record_ranges(S.rec_chunk, S.rec_chunk_ctas, &ctr->a_hw, blockIdx.x * kCollectThreads + t,
                          (int)gridDim.x * kCollectThreads);
@@ -941,21 +969,29 @@ __global__ void __launch_bounds__(kNT, 18) k_retype_place(DevState S, const Fram
   cudaGridDependencySynchronize();   // PDL: wait for the previous kernel of the frame
   trace_at(S, TK_RETYPE, 0);
   trace_span(S, 2, F.frame, false);
+  // Prologue, one thread, every load in one round trip: the halt flags, the
+  // item counts, the CTA's first scope entry, and the vertex-record capacity
+  // check -- this frame can give at most kRecsPerItem records per scope item
+  // (and never more than the stored blocks have slots).  Every CTA reads the
+  // same counters and takes the same decision; on a shortfall the frame stops
+  // here and the host grows the record arena and resumes it at this kernel
+  // (need_stage 1) -- before anything is written.
   __shared__ int s_pro[5];
-  read_prologue(S, s_pro, &S.ctr->ncollected, &S.ctr->nslab, &S.ctr->nexplicit,
-                (int)blockIdx.x < S.max_blocks ? S.scope + blockIdx.x : nullptr);
-  // Vertex-record capacity, before anything is written: this frame can give
-  // at most kRecsPerItem records per scope item (and never more than the
-  // stored blocks have slots).  Every CTA reads the same counters and takes
-  // the same decision; on a shortfall the frame stops here and the host grows
-  // the record arena and resumes it at this kernel (need_stage 1).
   __shared__ int s_halt;
   if (threadIdx.x == 0) {
-    int halt = s_pro[0];
+    // (4 requests on the counter block's lines: every CTA of the grid makes them)
+    const Counters *c = S.ctr;
+    const int4 hd = __ldcg(reinterpret_cast<const int4 *>(c));             // nblocks, ovf, error, need
+    const int4 cw = __ldcg(reinterpret_cast<const int4 *>(&c->nvalid));    // nvalid, nsteps, ncollected, nnew
+    const int4 it = __ldcg(reinterpret_cast<const int4 *>(&c->nslab));     // nslab, nexplicit, nitems_live, nhalo
+    const int first = (int)blockIdx.x < S.max_blocks ? __ldcg(S.scope + blockIdx.x) : -1;
+    const long long hw = (long long)__ldcg(reinterpret_cast<const unsigned long long *>(&c->a_hw));
+    const int nbl = hd.x, nc0 = cw.z, ns0 = it.x, ne0 = it.y;
+    int halt = (hd.z | hd.w) != 0;
+    s_pro[0] = halt; s_pro[1] = nc0; s_pro[2] = ns0; s_pro[3] = ne0; s_pro[4] = first;
     if (!halt) {
-      const long long items = F.scope_mode != 0 ? s_pro[3] : (long long)s_pro[1] + s_pro[2];
-      const long long hw = (long long)__ldcg(reinterpret_cast<const unsigned long long *>(&S.ctr->a_hw));
-      const long long bound = min(kRecsPerItem * items, (long long)kEV * __ldcg(&S.ctr->nblocks));
+      const long long items = F.scope_mode != 0 ? ne0 : (long long)nc0 + ns0;
+      const long long bound = min(kRecsPerItem * items, (long long)kEV * nbl);
       if (hw + bound + 4 * kRecChunk * S.rec_chunk_ctas > S.vrec_cap) {   // (+ the gc CTAs' record ranges)
         halt = 1;
         S.ctr->need_stage = 1;
@@ -1484,7 +1520,7 @@ __device__ __forceinline__ size_t sample_index(const int *s_nbr, int lx, int ly,
 // publishes it to the host) and with F.reset_after clears the per-call
 // counters for the next frame -- so consecutive frames need no stream
 // operation between their kernels.
-__device__ __forceinline__ void gc_commit(const DevState &S, const FrameDev &F, int mode) {
+__device__ __forceinline__ void gc_commit(const DevState &S, const FrameDev &F, int mode, bool halted) {
   __shared__ int s_last;
   __shared__ __align__(16) Counters s_c;   // the last CTA's copy of the counter block
   Counters *ctr = S.ctr;
@@ -1508,9 +1544,17 @@ __device__ __forceinline__ void gc_commit(const DevState &S, const FrameDev &F, 
     for (int q = threadIdx.x; q < kWords; q += blockDim.x) sw[q] = src[q];
   }
   __syncthreads();
-  const bool halted = (s_c.error | s_c.need) != 0;
+  // `halted` is this frame's own state, read in the prologue: with frame
+  // overlap the next frame's k_collect may have raised need / error since
   if (threadIdx.x == 0) {
     Counters &c = s_c;
+    if ((mode & G_OVERLAP) && !halted) {   // the snapshot shows this frame's collect counters and block counts
+      c.nvalid = c.sv_nvalid; c.nsteps = c.sv_nsteps; c.ncollected = c.sv_ncollected; c.nnew = c.sv_nnew;
+      c.maxnorm_bits = c.sv_maxnorm_bits; c.t_start_ns = c.sv_t_start_ns;
+      c.nblocks = c.sv_nblocks; c.nfree = c.sv_nfree; c.nblocks_owned = c.sv_nblocks_owned;
+      c.error = 0; c.need = 0;
+      c.err_info[0] = c.err_info[1] = c.err_info[2] = c.err_info[3] = 0;
+    }
     if (!halted) {   // the fold, mirrored into the global block (persistent fields only)
       const long long allocs_all = c.v_allocs, fr = c.v_frees;
       const long long peak = c.v_live + allocs_all;     // all allocations precede all frees
@@ -1538,15 +1582,17 @@ __device__ __forceinline__ void gc_commit(const DevState &S, const FrameDev &F, 
     c.t_end_ns = gtimer();
     ctr->t_end_ns = c.t_end_ns;   // (resumed frames and the phase API read the global block)
   }
-  if (!F.snap) return;
+  if (F.snap) {
   __syncthreads();
   {
+    // (with G_OVERLAP the collect counters were cleared at the kernel's start)
+    const int reset_from = (int)((mode & G_OVERLAP) ? offsetof(Counters, nslab) : offsetof(Counters, nvalid)) / 4;
+    // (halted: nothing is cleared -- see below)
     const uint32_t *sw = reinterpret_cast<const uint32_t *>(&s_c);
     uint32_t *dst = reinterpret_cast<uint32_t *>(F.snap);
     for (int q = threadIdx.x; q < kWords; q += blockDim.x) {
       dst[q] = sw[q];
-      if (F.reset_after && !halted && q >= (int)(offsetof(Counters, nvalid) / 4))
-        reinterpret_cast<uint32_t *>(ctr)[q] = 0u;
+      if (F.reset_after && !halted && q >= reset_from) reinterpret_cast<uint32_t *>(ctr)[q] = 0u;
     }
   }
   if (F.self_dst && threadIdx.x < 32) {   // publish to the host now (the next frame's k_collect waits on a copy)
@@ -1558,6 +1604,13 @@ __device__ __forceinline__ void gc_commit(const DevState &S, const FrameDev &F, 
       __threadfence_system();
       *reinterpret_cast<volatile unsigned long long *>(F.self_seq) = F.self_id;
     }
+  }
+  }
+  // the commit is complete: a next frame's k_collect waiting on it may go on
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    asm volatile("st.release.gpu.global.s32 [%0], %1;\n" ::"l"(S.gc_done), "r"(F.epoch) : "memory");
   }
 }
 
@@ -1604,20 +1657,59 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
   __shared__ int s_pro[5];
   __shared__ int s_shp[kHaloShards + 1];   // G_SHARDED: prefix of the shard fills
   const bool sharded = (mode & G_SHARDED) != 0;
-  if (sharded && threadIdx.x < 32) {
-    int c = min(__ldcg(ctr->nhalo_sh + threadIdx.x), S.halo_sh_cap);
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int u = __shfl_up_sync(0xffffffffu, c, o);
-      if ((int)threadIdx.x >= o) c += u;
+  // prologue: warp 0 issues every load at once (halt flags and counts on
+  // lane 0, the halo shard fills on all lanes), one round trip
+  if (threadIdx.x < 32) {
+    int4 hd = make_int4(0, 0, 0, 0), it = make_int4(0, 0, 0, 0);
+    int vb = 0;
+    if (threadIdx.x == 0) {
+      hd = __ldcg(reinterpret_cast<const int4 *>(ctr));                  // nblocks, ovf, error, need
+      if (mode & G_REQUIRE_ITEMS) it = __ldcg(reinterpret_cast<const int4 *>(&ctr->nslab));   // .z nitems_live
+      vb = count_ptr ? __ldcg(count_ptr) : 0;
     }
-    s_shp[threadIdx.x + 1] = c;
-    if (threadIdx.x == 0) s_shp[0] = 0;
+    const int2 h = make_int2(hd.z, hd.w);
+    const int va = it.z;
+    int c = sharded ? min(__ldcg(ctr->nhalo_sh + threadIdx.x), S.halo_sh_cap) : 0;
+    if (threadIdx.x == 0) {
+      s_pro[0] = (h.x | h.y) != 0;
+      s_pro[1] = va; s_pro[2] = vb; s_pro[3] = 0; s_pro[4] = -1;
+    }
+    if (sharded) {
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, c, o);
+        if ((int)threadIdx.x >= o) c += u;
+      }
+      s_shp[threadIdx.x + 1] = c;
+      if (threadIdx.x == 0) s_shp[0] = 0;
+    }
   }
-  read_prologue(S, s_pro, (mode & G_REQUIRE_ITEMS) ? &ctr->nitems_live : nullptr, count_ptr, nullptr,
-                nullptr);
+  __syncthreads();
+  if (mode & G_OVERLAP) {
+    // the frame's collect counters and block counts are saved for the commit's
+    // snapshot and the collect counters cleared -- then the next frame's
+    // k_collect may launch: once every CTA of this grid has triggered.  (A
+    // halted frame keeps them: the host resumes it from them; the next
+    // frame's k_collect stops at its guard and writes none of them.)
+    if (blockIdx.x == 0 && !s_pro[0]) {
+      if (threadIdx.x == 0) {
+        const int4 a = __ldcg(reinterpret_cast<const int4 *>(&ctr->nvalid));          // nvalid, nsteps, ncollected, nnew
+        const ulonglong2 m = __ldcg(reinterpret_cast<const ulonglong2 *>(&ctr->maxnorm_bits));   // maxnorm, t_start
+        const int nb = __ldcg(&ctr->nblocks), nf = __ldcg(&ctr->nfree);
+        const long long no = (long long)__ldcg(reinterpret_cast<const unsigned long long *>(&ctr->nblocks_owned));
+        *reinterpret_cast<int4 *>(&ctr->sv_nvalid) = a;
+        *reinterpret_cast<ulonglong2 *>(&ctr->sv_maxnorm_bits) = m;
+        ctr->sv_nblocks = nb; ctr->sv_nfree = nf; ctr->sv_nblocks_owned = no;
+        *reinterpret_cast<int4 *>(&ctr->nvalid) = make_int4(0, 0, 0, 0);
+        *reinterpret_cast<ulonglong2 *>(&ctr->maxnorm_bits) = make_ulonglong2(0ull, 0ull);
+        __threadfence();
+      }
+      __syncthreads();
+    }
+    cudaTriggerProgrammaticLaunchCompletion();
+  }
   if (s_pro[0]) {   // halted frame: no work, but the commit still publishes
-    gc_commit(S, F, mode);
+    gc_commit(S, F, mode, true);
     return;
   }
   const int live_items = (mode & G_REQUIRE_ITEMS) ? s_pro[1] : 1;
@@ -2023,7 +2115,7 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
       }
     }
   }
-  gc_commit(S, F, mode);
+  gc_commit(S, F, mode, false);
   trace_span(S, 3, F.frame, true);
   trace_at(S, TK_GC, 31);
 }

@@ -189,7 +189,11 @@ class Engine:
         producer = torch.cuda.current_stream(t.device)
         if (h.value or 0) == producer.cuda_stream:
             return
-        torch.cuda.ExternalStream(h.value, device=t.device).wait_stream(producer)
+        ev = torch.cuda.Event()
+        ev.record(producer)
+        if ev.query():   # (nothing pending on the producer: no wait on the engine's stream, which
+            return       #  would keep the frame from overlapping the previous one)
+        torch.cuda.ExternalStream(h.value, device=t.device).wait_event(ev)
 
     def _depth_args(self, depth):
         if _is_device_tensor(depth):
@@ -376,7 +380,15 @@ class Engine:
         ptr = None if buffer is None else buffer.data_ptr()
         _lib.check(_lib.load().vm_set_trace(self.store._h, C.c_void_p(ptr)))
 
+    def stream_handle(self) -> int:
+        """The CUDA stream the engine queues its work on (cudaStream_t as int)."""
+        h = C.c_void_p()
+        _lib.check(_lib.load().vm_get_stream(self.store._h, C.byref(h)))
+        return h.value or 0
+
     def set_stream(self, stream_handle: int) -> None:
+        """Queue the engine's work on a caller's stream (0 / None: its own).
+        Frame overlap needs the engine's own stream."""
         self._resolve_pending()
         _lib.check(_lib.load().vm_set_stream(self.store._h, C.c_void_p(stream_handle or None)))
 
