@@ -64,9 +64,12 @@ class Stats(C.Structure):
         ("device_ms", C.c_double), ("fusion_ms", C.c_double), ("meshing_ms", C.c_double)]
 
     def as_dict(self) -> dict:
-        d = {k: int(getattr(self, k)) for k in STATS_FIELDS}
-        for k in ("device_ms", "fusion_ms", "meshing_ms"):
-            d[k] = float(getattr(self, k))
+        # (one numpy view of the struct instead of a getattr per field: this
+        # runs once per frame on the submission path)
+        n = len(STATS_FIELDS)
+        d = dict(zip(STATS_FIELDS, np.frombuffer(self, dtype=np.int64, count=n).tolist()))
+        d.update(zip(("device_ms", "fusion_ms", "meshing_ms"),
+                     np.frombuffer(self, dtype=np.float64, count=3, offset=8 * n).tolist()))
         return d
 
 
@@ -202,14 +205,11 @@ def intr_c(intr) -> Intr:
                 int(intr.width), int(intr.height))
 
 
-def pose_c(pose) -> PoseC:
-    p = PoseC()
-    r = np.ascontiguousarray(np.asarray(pose.rotation, np.float64).reshape(9))
-    t = np.ascontiguousarray(np.asarray(pose.translation, np.float64).reshape(3))
-    for i in range(9):
-        p.rotation[i] = float(r[i])
-    for i in range(3):
-        p.translation[i] = float(t[i])
+def pose_c(pose, out: "PoseC | None" = None) -> PoseC:
+    p = PoseC() if out is None else out
+    v = np.frombuffer(p, dtype=np.float64, count=12)
+    v[:9] = np.asarray(pose.rotation, np.float64).reshape(9)
+    v[9:] = np.asarray(pose.translation, np.float64).reshape(3)
     return p
 
 

@@ -138,6 +138,7 @@ struct FrameDev {
   int32_t frame;        // frame index (vertex birth)
   int32_t scope_mode;   // 0: collected + slabs (device scope); 1: explicit items
   int32_t nsteps_fixed; // > 0: band step count fixed by the intrinsics (k_depth_stats skipped)
+  double band_step;     // 2 / (nsteps_fixed - 1) (fusion.py:96, np.linspace's step), when fixed
   int32_t block_gc_age; // > 0: opt-in block GC (k_block_gc before this frame when frame % age == 0)
   int32_t consume_fb;   // fuse_frame: k_collect applies the previous frame's fallback records
   int32_t reset_after;  // k_gc_normals' commit clears the per-call counters after its snapshot

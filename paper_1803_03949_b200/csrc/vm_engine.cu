@@ -107,6 +107,7 @@ struct vm_engine {
   unsigned long long *d_seq[2] = {nullptr, nullptr};
   bool publish_prev = false;          // set by vm_fuse_frame_submit: the frame launched next publishes
   bool host_input = false;            // set by vm_fuse_frame_submit: this frame's depth came by a host copy
+  bool in_submit = false;             // set by vm_fuse_frame_submit[_raw] around the enqueue
   bool self_pub[2] = {false, false};  // the slot's frame publishes its own snapshot (gc commit)
   unsigned long long snap_ids = 0, want_id[2] = {0, 0};
   bool ev_rec[2] = {false, false};   // the slot's frame recorded PH_DEPTH / PH_END events
@@ -120,6 +121,9 @@ struct vm_engine {
   int32_t ov_epoch = 0;
   bool ov_of[2] = {false, false};   // the slot's frame was launched overlapped
   bool no_overlap = getenv("VOXMESH_B200_NO_OVERLAP") != nullptr;   // (A/B switch)
+  bool host_prof = getenv("VOXMESH_B200_HOST_PROF") != nullptr;   // (diagnostics: host time per submit)
+  std::vector<std::array<double, 3>> hp;   // per submit: enqueue, settle, wall since the previous submit's end
+  double hp_last = 0;
   int last_resumes = 0;
   int resume_launches = 0;   // kernels the resumes of the last settled frame launched
   int frame_launches = 0;   // kernels launched by the pending / last frame
@@ -753,9 +757,26 @@ int vm_create(const vm_store_config *cfg, vm_engine **out) {
   return VM_OK;
 }
 
+static double now_us() {
+  timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return ts.tv_sec * 1e6 + ts.tv_nsec * 1e-3;
+}
+
 int vm_destroy(vm_engine *e) {
   if (e) e->ov_ready = false;   // (frame overlap: only a frame right behind a frame)
   if (!e) return VM_OK;
+  if (e->host_prof && e->hp.size() > 8) {
+    double med[3];
+    for (int k = 0; k < 3; k++) {
+      std::vector<double> v;
+      for (size_t i = 5; i < e->hp.size(); i++) v.push_back(e->hp[i][k]);
+      std::nth_element(v.begin(), v.begin() + v.size() / 2, v.end());
+      med[k] = v[v.size() / 2];
+    }
+    fprintf(stderr, "[host] %zu submits, medians: enqueue %.1f us, settle %.1f us, outside the call %.1f us\n",
+            e->hp.size(), med[0], med[1], med[2]);
+  }
   cudaStreamSynchronize(e->stream);
   DevState &S = e->S;
   void *ptrs[] = {S.slots, S.ovf_head, S.ovf_lock, S.ovf_key, S.ovf_val, S.ovf_next, S.ovf_stamp, S.bcoord,
@@ -956,10 +977,13 @@ static int launch_frame(vm_engine *e, int slot) {
   F.reset_after = 1;
   e->want_id[slot] = ++e->snap_ids;
   // Host-copied input: the next frame's k_collect starts only after its copy,
-  // so this frame's gc commit publishes itself (a few PCIe writes at its end);
-  // else the next frame's k_collect publishes it, off the critical path.
-  e->self_pub[slot] = e->host_input;
-  if (e->host_input) {
+  // so this frame's gc commit publishes itself (a few PCIe writes at its end).
+  // So does a submitted frame the next one may overlap: the gc's completion
+  // is then off the critical path, while a publishing k_collect's is not
+  // (its system-scope writes drain before the next kernel starts: ~1.3 us,
+  // trace v11).  Else the next frame's k_collect publishes it.
+  e->self_pub[slot] = e->host_input || (e->in_submit && e->own_stream && !e->profiling && !e->no_overlap);
+  if (e->self_pub[slot]) {
     F.self_dst = e->d_snap[slot];
     F.self_seq = e->d_seq[slot];
     F.self_id = e->want_id[slot];
@@ -1051,6 +1075,7 @@ int vm_fuse_frame_enqueue(vm_engine *e, const double *depth, int32_t h, int32_t 
   if (!e->norm_valid) e->ov_ready = false;   // (ensure_rays launches its own kernel)
   TRY(ensure_rays(e, h, w));
   F.nsteps_fixed = fixed_nsteps(e, cfg->trunc);
+  F.band_step = F.nsteps_fixed > 1 ? 2.0 / (double)(F.nsteps_fixed - 1) : 0.0;
   F.block_gc_age = cfg->block_gc_age > 0 ? cfg->block_gc_age : 0;
   F.consume_fb = 1;   // k_collect applies the previous frame's fallback records
   if (e->raw_next) {   // raw u16 frame: the first pixel kernel fills the f64 depth from it
@@ -1236,9 +1261,13 @@ int vm_fuse_frame_submit(vm_engine *e, const double *depth, int32_t h, int32_t w
   e->pending = 0;
   e->publish_prev = prev;
   e->host_input = sl >= 0;
+  e->in_submit = true;
+  const double hp0 = e->host_prof ? now_us() : 0.0;
   const int rc = vm_fuse_frame_enqueue(e, dd, h, w, 1, intr, pose, cfg, frame_index);
+  const double hp1 = e->host_prof ? now_us() : 0.0;
   e->publish_prev = false;
   e->host_input = false;
+  e->in_submit = false;
   if (rc != VM_OK) {   // (argument errors: nothing was queued)
     e->pending = prev;
     e->fslot = pslot;
@@ -1251,6 +1280,11 @@ int vm_fuse_frame_submit(vm_engine *e, const double *depth, int32_t h, int32_t w
   if (sl >= 0) {
     e->slot = sl;
     CK(cudaEventSynchronize(e->ev_copy[sl]));   // the caller may reuse its buffer on return
+  }
+  if (e->host_prof) {
+    const double hp2 = now_us();
+    e->hp.push_back({hp1 - hp0, hp2 - hp1, e->hp_last > 0 ? hp0 - e->hp_last : 0.0});
+    e->hp_last = hp2;
   }
   return VM_OK;
 }
@@ -1298,9 +1332,11 @@ int vm_fuse_frame_submit_raw(vm_engine *e, const uint16_t *raw, int32_t h, int32
   e->pending = 0;
   e->publish_prev = prev;
   e->host_input = false;   // (a quarter of the bytes: the copy is done before the kernels are)
+  e->in_submit = true;
   const int rc = vm_fuse_frame_enqueue(e, e->d_slot[sl], h, w, 1, intr, pose, cfg, frame_index);
   e->publish_prev = false;
   e->host_input = false;
+  e->in_submit = false;
   e->raw_next = nullptr;
   if (rc != VM_OK) {
     e->pending = prev;
@@ -2025,6 +2061,7 @@ int vm_partition_frame_begin(vm_engine *e, const double *depth, int32_t h, int32
   F.ghost_nranks = 0;
   TRY(ensure_rays(e, h, w));
   F.nsteps_fixed = fixed_nsteps(e, cfg->trunc);
+  F.band_step = F.nsteps_fixed > 1 ? 2.0 / (double)(F.nsteps_fixed - 1) : 0.0;
   F.block_gc_age = cfg->block_gc_age > 0 ? cfg->block_gc_age : 0;
   TRY(reset_call_counters(e));
   e->ctr_clean = false;

@@ -64,11 +64,15 @@ __device__ __forceinline__ int smem_append(int cnt, int *s_count) {
 // in the same round trip when `first` is non-null.  (The MC edge masks are
 // computed from the type bits, edge_mask_of, and the triangle counts read
 // through the read-only cache where a cube changed: no per-CTA table staging.)
+// The counters are read through the L1 / read-only path (__ldg): none of the
+// fields read here changes while the kernel runs, and a grid's CTAs on one SM
+// then share one L2 request instead of each queueing on the same line (2048
+// CTAs x 4 requests took ~2.5 us, trace v8).
 __device__ __forceinline__ void read_prologue(const DevState &S, int *sv, const int32_t *a, const int32_t *b,
                                               const int32_t *c, const int32_t *first = nullptr) {
   if (threadIdx.x == 0) {
-    const int2 h = __ldcg(reinterpret_cast<const int2 *>(&S.ctr->error));
-    const int va = a ? __ldcg(a) : 0, vb = b ? __ldcg(b) : 0, vc = c ? __ldcg(c) : 0;
+    const int2 h = __ldg(reinterpret_cast<const int2 *>(&S.ctr->error));
+    const int va = a ? __ldg(a) : 0, vb = b ? __ldg(b) : 0, vc = c ? __ldg(c) : 0;
     const int vf = first ? __ldcg(first) : -1;
     sv[0] = (h.x | h.y) != 0;
     sv[1] = va; sv[2] = vb; sv[3] = vc; sv[4] = vf;
@@ -441,7 +445,8 @@ __global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, cons
     nsteps = (int)ceil(band / half_block) + 1;
     if (nsteps < 2) nsteps = 2;
   }
-  const double step = 2.0 / (double)(nsteps - 1);
+  const double step = F.nsteps_fixed > 0 ? F.band_step : 2.0 / (double)(nsteps - 1);
+  const bool multi = S.nranks > 1;
   trace_at(S, TK_COLLECT, 1);
   __shared__ unsigned long long s_key[kCSet];
   __shared__ uint16_t s_list[kCSet];
@@ -498,6 +503,11 @@ __global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, cons
       __syncthreads();
     }
     const double rxn = u < F.w ? __ldg(S.rays + u) : 0.0;
+    // the last 4 distinct keys this lane produced in this pass: a repeat was
+    // already listed (by its match group's leader) and is dropped before the
+    // warp match -- consecutive band steps and the lane's two pixel rows mostly
+    // fall in the same blocks
+    unsigned long long h0 = kNoKey, h1 = kNoKey, h2 = kNoKey, h3 = kNoKey;
     double d[2];
     bool valid[2];
 #pragma unroll
@@ -532,8 +542,14 @@ __global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, cons
           const double f = __dadd_rn(1.0, __dmul_rn(sv, delta));
           for (int j = 0; j < 3; j++)
             c[j] = floor_div_exact(__dadd_rn(F.t[j], __dmul_rn(qs[j], f)), S.extent, S.inv_extent);
-          if (block_relevant(S, c[0], c[1], c[2])) key = (unsigned long long)pack_coord(c[0], c[1], c[2]);
+          if (!multi || block_relevant(S, c[0], c[1], c[2])) key = (unsigned long long)pack_coord(c[0], c[1], c[2]);
+          if (key == h0 || key == h1 || key == h2 || key == h3) {
+            key = kNoKey;
+          } else {
+            h3 = h2; h2 = h1; h1 = h0; h0 = key;
+          }
         }
+        if (!__any_sync(0xffffffffu, key != kNoKey)) continue;
         const unsigned grp = __match_any_sync(0xffffffffu, key);
         if (direct) {   // (rare) the set overflowed: probe the table directly
           if (key != kNoKey && lane == __ffs(grp) - 1) {
@@ -980,12 +996,14 @@ __global__ void __launch_bounds__(kNT, 18) k_retype_place(DevState S, const Fram
   __shared__ int s_halt;
   if (threadIdx.x == 0) {
     // (4 requests on the counter block's lines: every CTA of the grid makes them)
+    // (through L1, see read_prologue: nothing read here changes during the kernel --
+    // a CTA that raises need below makes every CTA take the same decision)
     const Counters *c = S.ctr;
-    const int4 hd = __ldcg(reinterpret_cast<const int4 *>(c));             // nblocks, ovf, error, need
-    const int4 cw = __ldcg(reinterpret_cast<const int4 *>(&c->nvalid));    // nvalid, nsteps, ncollected, nnew
-    const int4 it = __ldcg(reinterpret_cast<const int4 *>(&c->nslab));     // nslab, nexplicit, nitems_live, nhalo
+    const int4 hd = __ldg(reinterpret_cast<const int4 *>(c));             // nblocks, ovf, error, need
+    const int4 cw = __ldg(reinterpret_cast<const int4 *>(&c->nvalid));    // nvalid, nsteps, ncollected, nnew
+    const int4 it = __ldg(reinterpret_cast<const int4 *>(&c->nslab));     // nslab, nexplicit, nitems_live, nhalo
     const int first = (int)blockIdx.x < S.max_blocks ? __ldcg(S.scope + blockIdx.x) : -1;
-    const long long hw = (long long)__ldcg(reinterpret_cast<const unsigned long long *>(&c->a_hw));
+    const long long hw = (long long)__ldg(reinterpret_cast<const unsigned long long *>(&c->a_hw));
     const int nbl = hd.x, nc0 = cw.z, ns0 = it.x, ne0 = it.y;
     int halt = (hd.z | hd.w) != 0;
     s_pro[0] = halt; s_pro[1] = nc0; s_pro[2] = ns0; s_pro[3] = ne0; s_pro[4] = first;
@@ -1663,13 +1681,15 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
     int4 hd = make_int4(0, 0, 0, 0), it = make_int4(0, 0, 0, 0);
     int vb = 0;
     if (threadIdx.x == 0) {
-      hd = __ldcg(reinterpret_cast<const int4 *>(ctr));                  // nblocks, ovf, error, need
-      if (mode & G_REQUIRE_ITEMS) it = __ldcg(reinterpret_cast<const int4 *>(&ctr->nslab));   // .z nitems_live
-      vb = count_ptr ? __ldcg(count_ptr) : 0;
+      // (through L1, see read_prologue; the next frame's k_collect, which may
+      // raise need / error, launches only after every CTA has passed here)
+      hd = __ldg(reinterpret_cast<const int4 *>(ctr));                  // nblocks, ovf, error, need
+      if (mode & G_REQUIRE_ITEMS) it = __ldg(reinterpret_cast<const int4 *>(&ctr->nslab));   // .z nitems_live
+      vb = count_ptr ? __ldg(count_ptr) : 0;
     }
     const int2 h = make_int2(hd.z, hd.w);
     const int va = it.z;
-    int c = sharded ? min(__ldcg(ctr->nhalo_sh + threadIdx.x), S.halo_sh_cap) : 0;
+    int c = sharded ? min(__ldg(ctr->nhalo_sh + threadIdx.x), S.halo_sh_cap) : 0;
     if (threadIdx.x == 0) {
       s_pro[0] = (h.x | h.y) != 0;
       s_pro[1] = va; s_pro[2] = vb; s_pro[3] = 0; s_pro[4] = -1;

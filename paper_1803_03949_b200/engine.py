@@ -166,6 +166,9 @@ class Engine:
         self.device_stats: list[dict] = []
         self.audit_every_frame = audit_every_frame
         self._intr_c = _lib.intr_c(intrinsics)
+        self._pose_c = _lib.PoseC()   # (reused: the C side copies the pose during the call)
+        self._stream_h = None         # the engine's CUDA stream handle (cached; set_stream resets it)
+        self._order_ev = None
         self._fcfg = _lib.FrameConfig(float(c.trunc), float(c.max_range), float(c.epsilon),
                                       int(c.weight_cap), int(bool(c.refine)),
                                       int(bool(c.frustum_only)), _lib.STRATEGY_CODES[c.strategy],
@@ -184,16 +187,18 @@ class Engine:
         pipelined paths hold it in ``_inflight``), so the caching allocator
         cannot hand its memory out while a queued frame still reads it."""
         import torch
-        h = C.c_void_p()
-        _lib.check(_lib.load().vm_get_stream(self.store._h, C.byref(h)))
+        if self._stream_h is None:
+            self._stream_h = self.stream_handle()
         producer = torch.cuda.current_stream(t.device)
-        if (h.value or 0) == producer.cuda_stream:
+        if self._stream_h == producer.cuda_stream:
             return
-        ev = torch.cuda.Event()
+        if self._order_ev is None:
+            self._order_ev = torch.cuda.Event()
+        ev = self._order_ev
         ev.record(producer)
         if ev.query():   # (nothing pending on the producer: no wait on the engine's stream, which
             return       #  would keep the frame from overlapping the previous one)
-        torch.cuda.ExternalStream(h.value, device=t.device).wait_event(ev)
+        torch.cuda.ExternalStream(self._stream_h, device=t.device).wait_event(ev)
 
     def _depth_args(self, depth):
         if _is_device_tensor(depth):
@@ -212,12 +217,12 @@ class Engine:
         self.store._touch()
         if self.pipelined:
             rc = _lib.load().vm_fuse_frame_submit(self.store._h, ptr, h, w, on_dev, C.byref(self._intr_c),
-                                                  C.byref(_lib.pose_c(pose)), C.byref(self._fcfg),
+                                                  C.byref(_lib.pose_c(pose, self._pose_c)), C.byref(self._fcfg),
                                                   self.frame_index)
             return self._after_submit(rc, keep if on_dev else None)
         st = _lib.Stats()
         _lib.check(_lib.load().vm_fuse_frame(self.store._h, ptr, h, w, on_dev,
-                                              C.byref(self._intr_c), C.byref(_lib.pose_c(pose)),
+                                              C.byref(self._intr_c), C.byref(_lib.pose_c(pose, self._pose_c)),
                                               C.byref(self._fcfg), self.frame_index, C.byref(st)))
         del keep
         return self._record(st)
@@ -240,7 +245,7 @@ class Engine:
         if on_dev:
             self._order_device_input(raw)
         rc = _lib.load().vm_fuse_frame_submit_raw(self.store._h, ptr, h, w, on_dev, float(depth_scale),
-                                                  C.byref(self._intr_c), C.byref(_lib.pose_c(pose)),
+                                                  C.byref(self._intr_c), C.byref(_lib.pose_c(pose, self._pose_c)),
                                                   C.byref(self._fcfg), self.frame_index)
         row = self._after_submit(rc, keep if on_dev else None)
         if not self.pipelined:
@@ -299,7 +304,7 @@ class Engine:
         self.store._touch()
         _lib.check(_lib.load().vm_fuse_frame_enqueue(self.store._h, ptr, h, w, on_dev,
                                                       C.byref(self._intr_c),
-                                                      C.byref(_lib.pose_c(pose)),
+                                                      C.byref(_lib.pose_c(pose, self._pose_c)),
                                                       C.byref(self._fcfg), self.frame_index))
         return keep
 
@@ -391,6 +396,7 @@ class Engine:
         Frame overlap needs the engine's own stream."""
         self._resolve_pending()
         _lib.check(_lib.load().vm_set_stream(self.store._h, C.c_void_p(stream_handle or None)))
+        self._stream_h = None
 
 
 PHASES = ("depth_stats", "collect", "fuse_blocks", "retype_place", "gc_normals")
