@@ -177,6 +177,11 @@ int vm_set_stream(vm_engine *e, void *cuda_stream);
  * another stream must be ordered before it: the binding records an event on
  * the producer stream and makes this one wait, engine.py). */
 int vm_get_stream(vm_engine *e, void **cuda_stream);
+/* Order the engine's stream after the work queued so far on `producer` (a
+ * cudaStream_t that wrote a device input): nothing is queued when that work
+ * has already completed (so a frame can still overlap the previous one),
+ * else the engine's stream waits on an event recorded there. */
+int vm_order_after(vm_engine *e, void *producer);
 /* Record CUDA events between the frame's kernels (per-phase device times). */
 int vm_set_profiling(vm_engine *e, int on);
 /* Per-kernel device times (ms) of the last frame: depth_stats, collect,

@@ -134,6 +134,7 @@ struct vm_engine {
   size_t slot_cap = 0;
   int slot = 0;
   cudaEvent_t ev_copy[2] = {nullptr, nullptr};
+  cudaEvent_t ev_order = nullptr;   // vm_order_after
   uint16_t *d_raw[2] = {nullptr, nullptr};   // raw u16 frames (vm_fuse_frame_submit_raw)
   size_t raw_cap = 0;
   const uint16_t *raw_next = nullptr;          // set while a raw frame is being enqueued
@@ -826,6 +827,20 @@ int vm_set_stream(vm_engine *e, void *stream) {
 int vm_get_stream(vm_engine *e, void **stream) {
   if (!e || !stream) return set_err(VM_ERR_INPUT, "null argument");
   *stream = (void *)e->stream;
+  return VM_OK;
+}
+
+int vm_order_after(vm_engine *e, void *producer) {
+  if (!e) return set_err(VM_ERR_INPUT, "null engine");
+  cudaStream_t p = (cudaStream_t)producer;
+  if (p == e->stream) return VM_OK;
+  const cudaError_t q = cudaStreamQuery(p);
+  if (q == cudaSuccess) return VM_OK;   // (its work is done: nothing to order)
+  if (q != cudaErrorNotReady) return set_err(VM_ERR_CUDA, "producer stream: %s", cudaGetErrorString(q));
+  if (!e->ev_order) CK(cudaEventCreateWithFlags(&e->ev_order, cudaEventDisableTiming));
+  CK(cudaEventRecord(e->ev_order, p));
+  e->ov_ready = false;   // (an event wait on the stream: the frames stay apart)
+  CK(cudaStreamWaitEvent(e->stream, e->ev_order, 0));
   return VM_OK;
 }
 

@@ -398,7 +398,7 @@ __device__ __noinline__ void top_up_record_ranges(long long *ranges, int nctas, 
 constexpr int kCollectThreads = 256;
 constexpr int kRegionW = 64, kRegionH = 8;
 constexpr int kCSet = 1024;   // CTA-local key set (open addressing)
-constexpr int kCOver = 512;   // keys that found no free set slot within 32 probes
+constexpr int kCOver = 256;   // keys that found no free set slot within 32 probes
 constexpr unsigned long long kNoKey = ~0ull;
 
 __device__ __forceinline__ unsigned cset_hash(unsigned long long k) {

@@ -117,6 +117,10 @@ def _is_device_tensor(x) -> bool:
     return hasattr(x, "data_ptr") and getattr(x, "is_cuda", False)
 
 
+_ROW_KEYS = ("blocks_active", "vertices_live", "triangles_live", "vertices_allocated_total",
+             "vertices_recycled_total", "irregular_cube_count", "fusion_ms", "meshing_ms")
+
+
 class _PendingRow(StatsRow):
     """StatsRow of a frame submitted in pipelined mode: its fields are filled
     when the frame completes -- at the engine's next call or on first access."""
@@ -130,6 +134,14 @@ class _PendingRow(StatsRow):
         for k in StatsRow.FIELDS:
             object.__setattr__(self, k, getattr(row, k))
         object.__setattr__(self, "_done", True)
+
+    def _fill_from(self, d: dict) -> None:
+        """The row's columns from the frame's device stats (Engine._row_from's mapping)."""
+        sa = object.__setattr__
+        for k in _ROW_KEYS:
+            sa(self, k, d[k])
+        sa(self, "compact_ms", 0.0)
+        sa(self, "_done", True)
 
     def __getattribute__(self, name):
         if name in StatsRow.FIELDS and name != "frame" and not object.__getattribute__(self, "_done"):
@@ -167,6 +179,7 @@ class Engine:
         self.audit_every_frame = audit_every_frame
         self._intr_c = _lib.intr_c(intrinsics)
         self._pose_c = _lib.PoseC()   # (reused: the C side copies the pose during the call)
+        self._pose_v = np.frombuffer(self._pose_c, dtype=np.float64, count=12)
         self._stream_h = None         # the engine's CUDA stream handle (cached; set_stream resets it)
         self._order_ev = None
         self._fcfg = _lib.FrameConfig(float(c.trunc), float(c.max_range), float(c.epsilon),
@@ -189,16 +202,17 @@ class Engine:
         import torch
         if self._stream_h is None:
             self._stream_h = self.stream_handle()
-        producer = torch.cuda.current_stream(t.device)
-        if self._stream_h == producer.cuda_stream:
-            return
-        if self._order_ev is None:
-            self._order_ev = torch.cuda.Event()
-        ev = self._order_ev
-        ev.record(producer)
-        if ev.query():   # (nothing pending on the producer: no wait on the engine's stream, which
-            return       #  would keep the frame from overlapping the previous one)
-        torch.cuda.ExternalStream(self._stream_h, device=t.device).wait_event(ev)
+        raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+        producer = raw(t.device.index) if raw is not None else torch.cuda.current_stream(t.device).cuda_stream
+        if producer != self._stream_h:   # (C side: a wait only if the producer's work is pending --
+            _lib.check(_lib.load().vm_order_after(self.store._h, C.c_void_p(producer or None)))   # no overlap then)
+
+    def _pose_arg(self, pose) -> "_lib.PoseC":
+        v = self._pose_v
+        v[:9] = pose.rotation.reshape(9) if isinstance(pose.rotation, np.ndarray) else np.asarray(pose.rotation,
+                                                                                                    np.float64).reshape(9)
+        v[9:] = pose.translation
+        return self._pose_c
 
     def _depth_args(self, depth):
         if _is_device_tensor(depth):
@@ -217,12 +231,12 @@ class Engine:
         self.store._touch()
         if self.pipelined:
             rc = _lib.load().vm_fuse_frame_submit(self.store._h, ptr, h, w, on_dev, C.byref(self._intr_c),
-                                                  C.byref(_lib.pose_c(pose, self._pose_c)), C.byref(self._fcfg),
+                                                  C.byref(self._pose_arg(pose)), C.byref(self._fcfg),
                                                   self.frame_index)
             return self._after_submit(rc, keep if on_dev else None)
         st = _lib.Stats()
         _lib.check(_lib.load().vm_fuse_frame(self.store._h, ptr, h, w, on_dev,
-                                              C.byref(self._intr_c), C.byref(_lib.pose_c(pose, self._pose_c)),
+                                              C.byref(self._intr_c), C.byref(self._pose_arg(pose)),
                                               C.byref(self._fcfg), self.frame_index, C.byref(st)))
         del keep
         return self._record(st)
@@ -245,7 +259,7 @@ class Engine:
         if on_dev:
             self._order_device_input(raw)
         rc = _lib.load().vm_fuse_frame_submit_raw(self.store._h, ptr, h, w, on_dev, float(depth_scale),
-                                                  C.byref(self._intr_c), C.byref(_lib.pose_c(pose, self._pose_c)),
+                                                  C.byref(self._intr_c), C.byref(self._pose_arg(pose)),
                                                   C.byref(self._fcfg), self.frame_index)
         row = self._after_submit(rc, keep if on_dev else None)
         if not self.pipelined:
@@ -278,7 +292,7 @@ class Engine:
         self.device_stats.append(d)
         self._collected_n = d["collected_blocks"]
         self._collected_cache = None
-        row._fill(self._row_from(row.frame, d))
+        row._fill_from(d)
 
     def _resolve_pending(self) -> None:
         """Complete the pipelined frame in flight, if any (every engine
@@ -304,7 +318,7 @@ class Engine:
         self.store._touch()
         _lib.check(_lib.load().vm_fuse_frame_enqueue(self.store._h, ptr, h, w, on_dev,
                                                       C.byref(self._intr_c),
-                                                      C.byref(_lib.pose_c(pose, self._pose_c)),
+                                                      C.byref(self._pose_arg(pose)),
                                                       C.byref(self._fcfg), self.frame_index))
         return keep
 
