@@ -256,6 +256,7 @@ struct DevState {
   int32_t *ghost_src;   // [max_blocks] scope position -> received record (halo exchange)
   int32_t *last_frame;  // [max_blocks] frame in which the block was last collected (block GC)
   int32_t *free_list;   // [max_blocks] evicted block indices (block GC)
+  int32_t free_list_on; // block GC has run: allocations check the free list first
   const int32_t *ghost_counts;   // [nranks] records per rank of the current exchange
   Counters *ctr;
   int32_t *gc_done;     // epoch of the last k_gc_normals commit (outside Counters: host restores leave it)
@@ -385,6 +386,7 @@ struct HashRef {
   int idx;
   int stamp;
   int32_t *stamp_ptr;
+  int free_slot;   // (find, key absent) the bucket's first empty slot, -1 if full
 };
 
 // get_block with the slot's stamp: every bucket slot is one 16-byte load
@@ -398,27 +400,31 @@ __device__ HashRef hash_find_ref(const DevState &S, int x, int y, int z) {
   for (int i = 0; i < kSlotsPerBucket; i++) v[i] = __ldcg(reinterpret_cast<const int4 *>(kb + i));
   // first slot holding the key or empty (slots fill in prefix order), with
   // register selects only (no dynamically indexed local array)
-  int hit = -1, idx = -1, stamp = -1;
+  int hit = -1, idx = -1, stamp = -1, fs = -1;
   bool stop = false;
 #pragma unroll
   for (int i = 0; i < kSlotsPerBucket; i++) {
     const long long k = (long long)(((unsigned long long)(unsigned)v[i].y << 32) | (unsigned)v[i].x);
     if (!stop && k == key) { hit = i; idx = v[i].z; stamp = v[i].w; }
+    if (!stop && k == kEmptyKey) fs = i;   // (slots fill in prefix order: the first empty one)
     stop = stop || k == key || k == kEmptyKey;
   }
   if (hit >= 0) {
-    if (idx == -1) idx = wait_val(&kb[hit].val);
-    if (idx == kEvicted) return {-1, -1, nullptr};   // (an evicted block reads as absent)
-    return {idx, stamp, &kb[hit].pad};
+    if (idx == -1) {   // (being inserted: the stamp is written before the index is published)
+      idx = wait_val(&kb[hit].val);
+      stamp = ld_vol(&kb[hit].pad);
+    }
+    if (idx == kEvicted) return {-1, -1, nullptr, -1};   // (an evicted block reads as absent)
+    return {idx, stamp, &kb[hit].pad, -1};
   }
-  if (stop) return {-1, -1, nullptr};
+  if (stop) return {-1, -1, nullptr, fs};
   for (int e = ld_vol(S.ovf_head + b); e >= 0; e = ld_vol(S.ovf_next + e))
     if (ld_vol(S.ovf_key + e) == key) {
       const int v = ld_vol(S.ovf_val + e);
-      if (v == kEvicted) return {-1, -1, nullptr};
-      return {v, ld_vol(S.ovf_stamp + e), S.ovf_stamp + e};
+      if (v == kEvicted) return {-1, -1, nullptr, -1};
+      return {v, ld_vol(S.ovf_stamp + e), S.ovf_stamp + e, -1};
     }
-  return {-1, -1, nullptr};
+  return {-1, -1, nullptr, -1};
 }
 
 // SpatialStore.get_block (store.py:280-294)
@@ -491,7 +497,7 @@ __device__ int alloc_block(const DevState &S, int x, int y, int z, int epoch) {
   // as a fresh block's by k_fuse_blocks).  Pops only race with pops (pushes
   // happen in k_block_gc alone): a pop that finds the list empty undoes itself.
   int idx = -1;
-  if (ld_vol(&S.ctr->nfree) > 0) {
+  if (S.free_list_on && ld_vol(&S.ctr->nfree) > 0) {   // (no round trip unless block GC ever ran)
     const int k = atomicSub(&S.ctr->nfree, 1);
     if (k > 0) idx = __ldcg(S.free_list + (k - 1));
     else atomicAdd(&S.ctr->nfree, 1);
@@ -540,7 +546,7 @@ __device__ HashRef hash_insert_ref(const DevState &S, int x, int y, int z, int e
         // block's coordinate and stamps are read by later kernels)
         const int idx = alloc_block(S, x, y, z, epoch);
         *(volatile int32_t *)&kb[i].val = idx;
-        return {idx, ld_vol(&kb[i].pad), &kb[i].pad};
+        return {idx, ld_vol(&kb[i].pad), &kb[i].pad, -1};
       }
     }
     if (k == key) {
@@ -548,9 +554,10 @@ __device__ HashRef hash_insert_ref(const DevState &S, int x, int y, int z, int e
       if (ld_vol(&kb[i].val) == kEvicted && atomicCAS(&kb[i].val, kEvicted, -1) == kEvicted) {
         const int idx = alloc_block(S, x, y, z, epoch);
         *(volatile int32_t *)&kb[i].val = idx;
-        return {idx, ld_vol(&kb[i].pad), &kb[i].pad};
+        return {idx, ld_vol(&kb[i].pad), &kb[i].pad, -1};
       }
-      return {wait_val(&kb[i].val), ld_vol(&kb[i].pad), &kb[i].pad};
+      const int v = wait_val(&kb[i].val);
+      return {v, ld_vol(&kb[i].pad), &kb[i].pad, -1};
     }
   }
   int32_t *sp = nullptr;
@@ -592,7 +599,37 @@ __device__ HashRef hash_insert_ref(const DevState &S, int x, int y, int z, int e
       __nanosleep(64);
     }
   }
-  return {found, sp ? ld_vol(sp) : -1, sp};
+  return {found, sp ? ld_vol(sp) : -1, sp, -1};
+}
+
+// k_collect's insert of a key its find did not see, at the bucket slot the
+// find saw empty (no second read of the bucket): the thread that creates the
+// block marks it collected by this call itself -- stamp first, then the index
+// published with release semantics, so a concurrent finder that waits for the
+// index sees the stamp and does not collect it twice.  Returns the index and
+// whether this thread collected it (else it falls back to the general insert
+// and the caller's stamp exchange).
+__device__ __forceinline__ HashRef hash_insert_collect(const DevState &S, int x, int y, int z, int epoch,
+                                                       int free_slot, bool *created) {
+  *created = false;
+  if (free_slot >= 0) {
+    const long long key = pack_coord(x, y, z);
+    HashSlot *ks = S.slots + (size_t)bucket_of(S, key) * kSlotsPerBucket + free_slot;
+    const long long k = (long long)atomicCAS((unsigned long long *)&ks->key, (unsigned long long)kEmptyKey,
+                                             (unsigned long long)key);
+    if (k == kEmptyKey) {
+      const int idx = alloc_block(S, x, y, z, epoch);
+      ks->pad = epoch;
+      asm volatile("st.release.gpu.global.s32 [%0], %1;\n" ::"l"(&ks->val), "r"(idx) : "memory");
+      *created = idx >= 0;
+      return {idx, epoch, &ks->pad, -1};
+    }
+    if (k == key) {   // (someone else inserted it just now)
+      const int v = wait_val(&ks->val);
+      if (v != kEvicted) return {v, ld_vol(&ks->pad), &ks->pad, -1};
+    }
+  }
+  return hash_insert_ref(S, x, y, z, epoch);
 }
 
 // ---------------------------------------------------------------- misc

@@ -1031,6 +1031,7 @@ static int launch_frame(vm_engine *e, int slot) {
   e->frame_launches = 3 + meshing_launches(F);   // collect, fuse, retype (+ parity passes), gc (+ depth stats)
   if (gc_frame) {
     // opt-in block GC, before the frame allocates (its pops reuse the indices)
+    e->S.free_list_on = 1;   // (allocations check the free list from now on)
     k_block_gc<<<e->sm_count * 8, 256, 0, st>>>(e->S, F.frame, F.block_gc_age);
     e->frame_launches++;
   }

@@ -410,9 +410,14 @@ __device__ __forceinline__ unsigned cset_hash(unsigned long long k) {
 // (first to stamp it this call), else -1
 __device__ __forceinline__ int collect_block(const DevState &S, const FrameDev &F, int x, int y, int z) {
   HashRef r = hash_find_ref(S, x, y, z);
-  if (r.idx == -1) r = hash_insert_ref(S, x, y, z, F.epoch);
+  bool created = false;
+  if (r.idx == -1) r = hash_insert_collect(S, x, y, z, F.epoch, r.free_slot, &created);
   else if (r.idx == -2)   // a key whose allocation failed (table full): the reference raises again
     set_error(S, ERR_CAPACITY, S.max_blocks, S.table_size, 1, F.epoch);
+  if (created) {
+    S.stamp_collect[r.idx] = F.epoch;
+    return r.idx;
+  }
   if (r.idx >= 0 && r.stamp != F.epoch && atomicExch(r.stamp_ptr, F.epoch) != F.epoch) {
     S.stamp_collect[r.idx] = F.epoch;
     return r.idx;
@@ -503,11 +508,6 @@ __global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, cons
       __syncthreads();
     }
     const double rxn = u < F.w ? __ldg(S.rays + u) : 0.0;
-    // the last 4 distinct keys this lane produced in this pass: a repeat was
-    // already listed (by its match group's leader) and is dropped before the
-    // warp match -- consecutive band steps and the lane's two pixel rows mostly
-    // fall in the same blocks
-    unsigned long long h0 = kNoKey, h1 = kNoKey, h2 = kNoKey, h3 = kNoKey;
     double d[2];
     bool valid[2];
 #pragma unroll
@@ -543,11 +543,6 @@ __global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, cons
           for (int j = 0; j < 3; j++)
             c[j] = floor_div_exact(__dadd_rn(F.t[j], __dmul_rn(qs[j], f)), S.extent, S.inv_extent);
           if (!multi || block_relevant(S, c[0], c[1], c[2])) key = (unsigned long long)pack_coord(c[0], c[1], c[2]);
-          if (key == h0 || key == h1 || key == h2 || key == h3) {
-            key = kNoKey;
-          } else {
-            h3 = h2; h2 = h1; h1 = h0; h0 = key;
-          }
         }
         if (!__any_sync(0xffffffffu, key != kNoKey)) continue;
         const unsigned grp = __match_any_sync(0xffffffffu, key);
