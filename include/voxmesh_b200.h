@@ -225,6 +225,13 @@ int vm_fuse_frame_submit(vm_engine *e, const double *depth, int32_t h, int32_t w
                          int32_t depth_on_device, const vm_intrinsics *intr,
                          const vm_pose *pose, const vm_frame_config *cfg, int64_t frame_index);
 int vm_fuse_frame_result(vm_engine *e, vm_stats *out);
+/* Deferred input wait (on != 0): vm_fuse_frame_submit[_raw] returns once the
+ * host->device copy of the host buffer is queued, not done; the caller calls
+ * vm_input_wait before it reuses the buffer.  The Python binding delivers the
+ * previous frame's row in between, so that work overlaps the copy. */
+int vm_set_deferred_input_wait(vm_engine *e, int on);
+/* Block until the last submitted frame's host buffer has been read. */
+int vm_input_wait(vm_engine *e);
 /* vm_fuse_frame_submit for a raw 16-bit depth image (native byte order, as
  * decoded from the reference's PGM files): the device converts each pixel
  * exactly as io_formats.read_depth (io_formats.py:84: raw / depth_scale in

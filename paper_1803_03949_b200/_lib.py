@@ -98,6 +98,8 @@ _SIGS = {
     "vm_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
     "vm_get_stream": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "vm_order_after": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "vm_set_deferred_input_wait": (C.c_int, [C.c_void_p, C.c_int]),
+    "vm_input_wait": (C.c_int, [C.c_void_p]),
     "vm_set_profiling": (C.c_int, [C.c_void_p, C.c_int]),
     "vm_phase_times": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
     "vm_set_trace": (C.c_int, [C.c_void_p, C.c_void_p]),

@@ -135,6 +135,8 @@ struct vm_engine {
   int slot = 0;
   cudaEvent_t ev_copy[2] = {nullptr, nullptr};
   cudaEvent_t ev_order = nullptr;   // vm_order_after
+  bool defer_wait = false;          // vm_set_deferred_input_wait
+  int copy_pending = -1;            // slot whose host copy the caller has not waited for yet
   uint16_t *d_raw[2] = {nullptr, nullptr};   // raw u16 frames (vm_fuse_frame_submit_raw)
   size_t raw_cap = 0;
   const uint16_t *raw_next = nullptr;          // set while a raw frame is being enqueued
@@ -830,6 +832,32 @@ int vm_get_stream(vm_engine *e, void **stream) {
   return VM_OK;
 }
 
+// Returning from a submit: unless the caller defers it, wait until the host
+// buffer has been read (every return path, errors included)
+struct InputWait {
+  vm_engine *e;
+  ~InputWait() {
+    if (!e->defer_wait) vm_input_wait(e);
+  }
+};
+
+int vm_set_deferred_input_wait(vm_engine *e, int on) {
+  if (!e) return set_err(VM_ERR_INPUT, "null engine");
+  TRY(vm_input_wait(e));
+  e->defer_wait = on != 0;
+  return VM_OK;
+}
+
+int vm_input_wait(vm_engine *e) {
+  if (!e) return set_err(VM_ERR_INPUT, "null engine");
+  if (e->copy_pending >= 0) {
+    const int sl = e->copy_pending;
+    e->copy_pending = -1;
+    CK(cudaEventSynchronize(e->ev_copy[sl]));
+  }
+  return VM_OK;
+}
+
 int vm_order_after(vm_engine *e, void *producer) {
   if (!e) return set_err(VM_ERR_INPUT, "null engine");
   cudaStream_t p = (cudaStream_t)producer;
@@ -1263,8 +1291,10 @@ int vm_fuse_frame_submit(vm_engine *e, const double *depth, int32_t h, int32_t w
     sl = e->slot ^ 1;
     CK(cudaMemcpyAsync(e->d_slot[sl], depth, bytes, cudaMemcpyHostToDevice, e->copy_stream));
     CK(cudaEventRecord(e->ev_copy[sl], e->copy_stream));
+    e->copy_pending = sl;   // (waited for on every return below, or by the caller in deferred mode)
     dd = e->d_slot[sl];
   }
+  InputWait iw_{e};
   // 2. this frame's kernels, ordered after its copy, queued behind the pending
   //    frame's; 3. the pending frame completes (its stats are kept for
   //    vm_fuse_frame_result) while this one keeps the GPU busy
@@ -1293,10 +1323,7 @@ int vm_fuse_frame_submit(vm_engine *e, const double *depth, int32_t h, int32_t w
     TRY(settle_slot(e, pslot, true));
     e->settled_valid = 1;
   }
-  if (sl >= 0) {
-    e->slot = sl;
-    CK(cudaEventSynchronize(e->ev_copy[sl]));   // the caller may reuse its buffer on return
-  }
+  if (sl >= 0) e->slot = sl;   // (the caller may reuse its buffer once the copy is done: iw_)
   if (e->host_prof) {
     const double hp2 = now_us();
     e->hp.push_back({hp1 - hp0, hp2 - hp1, e->hp_last > 0 ? hp0 - e->hp_last : 0.0});
@@ -1335,8 +1362,10 @@ int vm_fuse_frame_submit_raw(vm_engine *e, const uint16_t *raw, int32_t h, int32
   if (!raw_on_device) {   // a quarter of the f64 frame's bytes over PCIe
     CK(cudaMemcpyAsync(e->d_raw[sl], raw, npix * sizeof(uint16_t), cudaMemcpyHostToDevice, e->copy_stream));
     CK(cudaEventRecord(e->ev_copy[sl], e->copy_stream));
+    e->copy_pending = sl;
     dr = e->d_raw[sl];
   }
+  InputWait iw_{e};
   if (!raw_on_device) {
     e->ov_ready = false;   // (an event wait on the stream: the frames stay apart)
     CK(cudaStreamWaitEvent(e->stream, e->ev_copy[sl], 0));
@@ -1363,8 +1392,7 @@ int vm_fuse_frame_submit_raw(vm_engine *e, const uint16_t *raw, int32_t h, int32
     TRY(settle_slot(e, pslot, true));
     e->settled_valid = 1;
   }
-  e->slot = sl;
-  if (!raw_on_device) CK(cudaEventSynchronize(e->ev_copy[sl]));   // the caller may reuse its buffer
+  e->slot = sl;   // (the caller may reuse its buffer once the copy is done: iw_)
   return VM_OK;
 }
 

@@ -709,9 +709,13 @@ __global__ void __launch_bounds__(kFB, 6) k_fuse_blocks(DevState S, const FrameD
   // neighbour probe of this thread: 7 lanes of each warp, directions 0..26
   const int pl = t & 31, pdir = (t >> 5) * 7 + pl;
   const bool prober = pl < 7 && pdir < 27;
+  // the item list entry of the CTA's next item is requested one item ahead
+  int b_next = (base + (int)blockIdx.x < n) ? s_pro[4] : -1;
+  if (b_next == -1 && base + (int)blockIdx.x < n) b_next = __ldcg(list + base + blockIdx.x);
   for (int i = base + blockIdx.x; i < n; i += gridDim.x, nth++) {
     trace_item(S, TK_FUSE, nth, 0);
-    const int b = i == base + (int)blockIdx.x && s_pro[4] != -1 ? s_pro[4] : __ldcg(list + i);
+    const int b = b_next;
+    b_next = i + (int)gridDim.x < n ? __ldcg(list + i + gridDim.x) : -1;
     if (b < 0) continue;
     const int4 c = __ldcg(S.bcoord + b);
     const bool fresh = (flags & F_INIT) && __ldcg(S.stamp_new + b) == F.epoch;
@@ -725,9 +729,13 @@ __global__ void __launch_bounds__(kFB, 6) k_fuse_blocks(DevState S, const FrameD
     if (flags & F_INTEGRATE) {
 #pragma unroll
       for (int j = 0; j < kNC / kFB; j++) {
+        // (requested before `fresh` is known: a new block's storage is read and
+        // ignored, so the loads need not wait for its stamp)
         const size_t q = (size_t)b * kNC + t + j * kFB;
-        t_old[j] = fresh ? 0.0 : S.tsdf[q];
-        w_old[j] = fresh ? 0 : S.weight[q];
+        const double tv = S.tsdf[q];
+        const int wv = S.weight[q];
+        t_old[j] = fresh ? 0.0 : tv;
+        w_old[j] = fresh ? 0 : wv;
       }
       const double bx = __dmul_rn((double)c.x, S.extent), by = __dmul_rn((double)c.y, S.extent),
                    bz = __dmul_rn((double)c.z, S.extent);

@@ -191,6 +191,9 @@ class Engine:
         self.pipelined = bool(pipelined) and not audit_every_frame
         self._pending: Optional[_PendingRow] = None
         self._inflight = None   # CUDA tensor input of the frame in flight (kept alive until it completes)
+        # the submit returns with the host copy in flight; fuse_frame waits for
+        # it (vm_input_wait) after delivering the previous frame's row
+        _lib.check(_lib.load().vm_set_deferred_input_wait(self.store._h, 1))
 
     # -- per-frame pipeline ---------------------------------------------------
     def _order_device_input(self, t) -> None:
@@ -230,10 +233,14 @@ class Engine:
         ptr, h, w, on_dev, keep = self._depth_args(depth)
         self.store._touch()
         if self.pipelined:
-            rc = _lib.load().vm_fuse_frame_submit(self.store._h, ptr, h, w, on_dev, C.byref(self._intr_c),
-                                                  C.byref(self._pose_arg(pose)), C.byref(self._fcfg),
-                                                  self.frame_index)
-            return self._after_submit(rc, keep if on_dev else None)
+            L = _lib.load()
+            rc = L.vm_fuse_frame_submit(self.store._h, ptr, h, w, on_dev, C.byref(self._intr_c),
+                                        C.byref(self._pose_arg(pose)), C.byref(self._fcfg), self.frame_index)
+            try:   # (the previous frame's row is delivered while this frame's host buffer is copied)
+                return self._after_submit(rc, keep if on_dev else None)
+            finally:
+                if not on_dev:
+                    L.vm_input_wait(self.store._h)   # the caller may reuse its buffer on return
         st = _lib.Stats()
         _lib.check(_lib.load().vm_fuse_frame(self.store._h, ptr, h, w, on_dev,
                                               C.byref(self._intr_c), C.byref(self._pose_arg(pose)),
@@ -258,10 +265,15 @@ class Engine:
         self.store._touch()
         if on_dev:
             self._order_device_input(raw)
-        rc = _lib.load().vm_fuse_frame_submit_raw(self.store._h, ptr, h, w, on_dev, float(depth_scale),
-                                                  C.byref(self._intr_c), C.byref(self._pose_arg(pose)),
-                                                  C.byref(self._fcfg), self.frame_index)
-        row = self._after_submit(rc, keep if on_dev else None)
+        L = _lib.load()
+        rc = L.vm_fuse_frame_submit_raw(self.store._h, ptr, h, w, on_dev, float(depth_scale),
+                                        C.byref(self._intr_c), C.byref(self._pose_arg(pose)),
+                                        C.byref(self._fcfg), self.frame_index)
+        try:
+            row = self._after_submit(rc, keep if on_dev else None)
+        finally:
+            if not on_dev:
+                L.vm_input_wait(self.store._h)
         if not self.pipelined:
             self._resolve_pending()
         return row
