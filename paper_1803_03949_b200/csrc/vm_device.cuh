@@ -151,6 +151,11 @@ struct FrameDev {
   // snapshot publish) only after *S.gc_done reaches wait_epoch.
   int32_t overlap;
   int32_t wait_epoch;
+  // host-copied input (pipelined submission): the copy stream writes in_id to
+  // *in_flag after the depth; k_collect waits for it before reading the depth
+  // (no event wait on the engine's stream, which would keep the frames apart)
+  const unsigned long long *in_flag;
+  unsigned long long in_id;
   Counters *snap;       // non-null: k_gc_normals' commit copies the counter block here (device)
   // non-null: k_collect copies the previous frame's snapshot (pub_src) to the
   // host's mapped buffer (pub_dst) and then writes pub_id to *pub_seq, the

@@ -136,6 +136,10 @@ struct vm_engine {
   cudaEvent_t ev_copy[2] = {nullptr, nullptr};
   cudaEvent_t ev_order = nullptr;   // vm_order_after
   bool defer_wait = false;          // vm_set_deferred_input_wait
+  // device-side input flags (FrameDev::in_flag): per slot, written by the copy
+  // stream after the frame's host copy
+  unsigned long long *d_inseq = nullptr, *h_inseq = nullptr, in_id = 0;
+  int in_slot = -1;                 // the slot the frame being enqueued waits on
   int copy_pending = -1;            // slot whose host copy the caller has not waited for yet
   uint16_t *d_raw[2] = {nullptr, nullptr};   // raw u16 frames (vm_fuse_frame_submit_raw)
   size_t raw_cap = 0;
@@ -346,6 +350,7 @@ static int error_message(vm_engine *e) {
                        (long long)c.err_info[1], (long long)c.err_info[2], (long long)c.err_info[3]);
       case 40: return set_err(VM_ERR_CONSISTENCY, "triangle references a vertex bound to no edge");
       case 50: return set_err(VM_ERR_CUDA, "k_gc_normals grid barrier timed out (CTAs not co-resident)");
+      case 60: return set_err(VM_ERR_CUDA, "the frame's host->device depth copy did not arrive");
       default: return set_err(VM_ERR_CONSISTENCY, "consistency error %lld", (long long)c.err_info[0]);
     }
   }
@@ -484,6 +489,10 @@ static void fill_frame_host(vm_engine *e, const double *depth_dev, int32_t h, in
   F.consume_fb = 0;
   F.raw = nullptr;
   F.depth_out = nullptr;
+  F.overlap = 0;
+  F.wait_epoch = 0;
+  F.in_flag = nullptr;
+  F.in_id = 0;
   F.depth = depth_dev;
   F.h = h;
   F.w = w;
@@ -785,12 +794,13 @@ int vm_destroy(vm_engine *e) {
   void *ptrs[] = {S.slots, S.ovf_head, S.ovf_lock, S.ovf_key, S.ovf_val, S.ovf_next, S.ovf_stamp, S.bcoord,
                   S.nbr, S.stamp_collect, S.stamp_halo, S.stamp_new, S.bowned, S.slab_bits, S.scope,
                   S.halo, S.halo_sh, S.tsdf, S.weight, S.vmask, S.tp, S.tc, S.vh, S.vrb, S.rec_chunk, S.vocc, S.vclaim, S.vparam, S.vrec, S.item_mask, S.vreq, S.psel, S.fallback, e->d_rays,
-                  S.ctr, S.gc_done, e->d_depth, e->d_scratch, S.ghost_src, e->d_ghost_counts, S.last_frame, S.free_list};
+                  S.ctr, S.gc_done, e->d_inseq, e->d_depth, e->d_scratch, S.ghost_src, e->d_ghost_counts, S.last_frame, S.free_list};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   free_compacted(e->comp);
   free_pcompact(e);
   if (e->h_ctr) cudaFreeHost(e->h_ctr);
+  if (e->h_inseq) cudaFreeHost(e->h_inseq);
   if (e->h_frame) cudaFreeHost(e->h_frame);
   for (int k = 0; k < 2; k++) {
     for (int i = 0; i < PH_COUNT; i++)
@@ -829,6 +839,22 @@ int vm_set_stream(vm_engine *e, void *stream) {
 int vm_get_stream(vm_engine *e, void **stream) {
   if (!e || !stream) return set_err(VM_ERR_INPUT, "null argument");
   *stream = (void *)e->stream;
+  return VM_OK;
+}
+
+// After a frame's host copy on the copy stream: the flag its k_collect waits
+// for (the copy of a per-slot sequence value, behind the depth in stream order)
+static int post_input_flag(vm_engine *e, int sl) {
+  if (!e->d_inseq) {
+    CK(cudaMalloc((void **)&e->d_inseq, 2 * sizeof(unsigned long long)));
+    CK(cudaMemset(e->d_inseq, 0, 2 * sizeof(unsigned long long)));
+    CK(cudaMallocHost((void **)&e->h_inseq, 2 * sizeof(unsigned long long)));
+    e->h_inseq[0] = e->h_inseq[1] = 0;
+  }
+  e->h_inseq[sl] = ++e->in_id;   // (its previous copy completed: vm_input_wait ran since)
+  CK(cudaMemcpyAsync(e->d_inseq + sl, e->h_inseq + sl, sizeof(unsigned long long), cudaMemcpyHostToDevice,
+                     e->copy_stream));
+  e->in_slot = sl;
   return VM_OK;
 }
 
@@ -1068,6 +1094,12 @@ static int launch_frame(vm_engine *e, int slot) {
   e->ov_of[slot] = overlap;
   Fc.wait_epoch = wait_epoch;
   if (F.nsteps_fixed <= 0) {
+    if (F.in_flag) {   // (k_depth_stats reads the depth first: order it after the copy on the stream)
+      Fc.overlap = 0;
+      Fc.wait_epoch = 0;
+      e->ov_of[slot] = false;
+      CK(cudaStreamWaitEvent(st, e->ev_copy[(int)(F.in_flag - e->d_inseq)], 0));
+    }
     k_depth_stats<<<grid_blocks(e), 256, 0, st>>>(e->S, F);
     e->frame_launches++;
     Fc.raw = nullptr;
@@ -1126,6 +1158,13 @@ int vm_fuse_frame_enqueue(vm_engine *e, const double *depth, int32_t h, int32_t 
     F.raw = e->raw_next;
     F.depth_out = const_cast<double *>(dd);
     F.depth_scale = e->raw_scale;
+  }
+  F.in_flag = nullptr;
+  F.in_id = 0;
+  if (e->in_slot >= 0) {   // (a submitted host copy: k_collect waits for its flag)
+    F.in_flag = e->d_inseq + e->in_slot;
+    F.in_id = e->h_inseq[e->in_slot];
+    e->in_slot = -1;
   }
   const int slot = e->fslot ^ 1;
   e->f_saved[slot] = F;
@@ -1292,16 +1331,14 @@ int vm_fuse_frame_submit(vm_engine *e, const double *depth, int32_t h, int32_t w
     CK(cudaMemcpyAsync(e->d_slot[sl], depth, bytes, cudaMemcpyHostToDevice, e->copy_stream));
     CK(cudaEventRecord(e->ev_copy[sl], e->copy_stream));
     e->copy_pending = sl;   // (waited for on every return below, or by the caller in deferred mode)
+    TRY(post_input_flag(e, sl));
     dd = e->d_slot[sl];
   }
   InputWait iw_{e};
-  // 2. this frame's kernels, ordered after its copy, queued behind the pending
-  //    frame's; 3. the pending frame completes (its stats are kept for
-  //    vm_fuse_frame_result) while this one keeps the GPU busy
-  if (sl >= 0) {
-    e->ov_ready = false;   // (an event wait on the stream: the frames stay apart)
-    CK(cudaStreamWaitEvent(e->stream, e->ev_copy[sl], 0));
-  }
+  // 2. this frame's kernels, ordered after its copy by the device-side flag
+  //    (k_collect waits for it), queued behind the pending frame's; 3. the
+  //    pending frame completes (its stats are kept for vm_fuse_frame_result)
+  //    while this one keeps the GPU busy
   const bool prev = e->pending != 0;
   const int pslot = e->fslot;
   e->pending = 0;
@@ -1363,13 +1400,10 @@ int vm_fuse_frame_submit_raw(vm_engine *e, const uint16_t *raw, int32_t h, int32
     CK(cudaMemcpyAsync(e->d_raw[sl], raw, npix * sizeof(uint16_t), cudaMemcpyHostToDevice, e->copy_stream));
     CK(cudaEventRecord(e->ev_copy[sl], e->copy_stream));
     e->copy_pending = sl;
+    TRY(post_input_flag(e, sl));
     dr = e->d_raw[sl];
   }
   InputWait iw_{e};
-  if (!raw_on_device) {
-    e->ov_ready = false;   // (an event wait on the stream: the frames stay apart)
-    CK(cudaStreamWaitEvent(e->stream, e->ev_copy[sl], 0));
-  }
   e->raw_next = dr;
   e->raw_scale = depth_scale;
   const bool prev = e->pending != 0;

@@ -494,6 +494,22 @@ __global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, cons
   }
   int nvalid = 0, nth = 0;
   if (t == 0) s_valid = 0;
+  if (F.in_flag && (int)blockIdx.x < nreg) {   // the frame's host copy has landed (copy-stream flag)
+    if (t == 0) {
+      const unsigned long long t0 = gtimer();
+      for (;;) {
+        unsigned long long v;
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(v) : "l"(F.in_flag) : "memory");
+        if (v >= F.in_id) break;
+        if (gtimer() - t0 > 2000000000ull) {   // (2 s: the copy failed -- raise, never hang)
+          set_error(S, ERR_CONSISTENCY, 60);
+          break;
+        }
+        __nanosleep(256);
+      }
+    }
+    __syncthreads();
+  }
   for (int reg = blockIdx.x; reg < rx * ry; reg += gridDim.x, nth++) {
     trace_item(S, TK_COLLECT, nth, 0);
     for (int q = t; q < kCSet; q += kCollectThreads) s_key[q] = kNoKey;
