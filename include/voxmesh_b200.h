@@ -331,6 +331,19 @@ int vm_partition_frame_begin(vm_engine *e, const double *depth, int32_t h, int32
                              const vm_intrinsics *intr, const vm_pose *pose, const vm_frame_config *cfg,
                              int64_t frame_index, uint8_t *send, int64_t send_cap, int64_t *n_send,
                              int64_t *n_owned_collected);
+/* Sharded band walk (spatial partition): walk only pixel rows [row0, row1)
+ * (row0 a multiple of 8) of the broadcast frame and list, into the device
+ * buffer keys_dev (capacity cap), the packed keys of every block the band
+ * samples there meet -- owned or not.  The ranks all-gather their lists;
+ * vm_partition_frame_begin_keys then collects each rank's relevant blocks
+ * from the union (in place of walking every pixel) and continues as
+ * vm_partition_frame_begin.  The collected set equals the unsharded one. */
+int vm_partition_collect_keys(vm_engine *e, const double *depth, int32_t h, int32_t w, int32_t depth_on_device,
+                              const vm_intrinsics *intr, const vm_pose *pose, const vm_frame_config *cfg,
+                              int64_t frame_index, int32_t row0, int32_t row1, uint64_t *keys_dev, int64_t cap,
+                              int64_t *n_keys);
+int vm_partition_frame_begin_keys(vm_engine *e, const uint64_t *keys_dev, int64_t n_keys, uint8_t *send,
+                                  int64_t send_cap, int64_t *n_send, int64_t *n_owned_collected);
 int vm_partition_repack(vm_engine *e, uint8_t *send, int64_t send_cap, int64_t *n_send);
 int vm_partition_frame_finish(vm_engine *e, const uint8_t *recv, const int32_t *counts, int32_t nranks,
                               int64_t max_count, vm_stats *out);

@@ -98,6 +98,11 @@ _SIGS = {
     "vm_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
     "vm_get_stream": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "vm_order_after": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "vm_partition_collect_keys": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                                            C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p,
+                                            C.c_int64, C.POINTER(C.c_int64)]),
+    "vm_partition_frame_begin_keys": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                                                C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "vm_set_deferred_input_wait": (C.c_int, [C.c_void_p, C.c_int]),
     "vm_input_wait": (C.c_int, [C.c_void_p]),
     "vm_set_profiling": (C.c_int, [C.c_void_p, C.c_int]),

@@ -156,6 +156,15 @@ struct FrameDev {
   // (no event wait on the engine's stream, which would keep the frames apart)
   const unsigned long long *in_flag;
   unsigned long long in_id;
+  // spatial partition, sharded band walk: k_collect walks pixel rows
+  // [row0, row1) only (row1 <= 0: all) and, with key_out set, lists the
+  // distinct block keys it meets there (every block, owned or not) instead of
+  // collecting them; the ranks all-gather the lists and each collects its
+  // relevant blocks from the union (k_collect_keys_apply)
+  int32_t row0, row1;
+  unsigned long long *key_out;
+  int32_t *key_count;
+  int32_t key_cap;
   Counters *snap;       // non-null: k_gc_normals' commit copies the counter block here (device)
   // non-null: k_collect copies the previous frame's snapshot (pub_src) to the
   // host's mapped buffer (pub_dst) and then writes pub_id to *pub_seq, the

@@ -2102,16 +2102,13 @@ int vm_import_blocks(vm_engine *e, int64_t n, const int32_t *coords, const doubl
 // caller needs the record count for the all-gather; a heap shortfall is
 // handled here (grow, integrate again -- k_fuse_blocks stopped at its guard,
 // so nothing was integrated twice).
-int vm_partition_frame_begin(vm_engine *e, const double *depth, int32_t h, int32_t w, int32_t depth_on_device,
-                             const vm_intrinsics *intr, const vm_pose *pose, const vm_frame_config *cfg,
-                             int64_t frame_index, uint8_t *send, int64_t send_cap, int64_t *n_send,
-                             int64_t *n_owned_collected) {
-  if (e) e->ov_ready = false;   // (frame overlap: only a frame right behind a frame)
-  if (!e || !intr || !pose || !cfg || !n_send || !n_owned_collected) return set_err(VM_ERR_INPUT, "null argument");
+// the frame's parameters of a partitioned frame (begin, or its key pass)
+static int partition_frame_setup(vm_engine *e, const double *depth, int32_t h, int32_t w, int32_t depth_on_device,
+                                 const vm_intrinsics *intr, const vm_pose *pose, const vm_frame_config *cfg,
+                                 int64_t frame_index, bool new_epoch) {
   if (!e->S.halo_exchange) return set_err(VM_ERR_INPUT, "engine not created in halo-exchange mode");
   if (cfg->strategy < 0 || cfg->strategy > 2) return set_err(VM_ERR_VALUE, "unknown strategy %d", cfg->strategy);
   if (cfg->trunc < e->S.cube_size) return set_err(VM_ERR_VALUE, "truncation band must be at least one cube");
-  NvtxRange nvtx_("vm_partition_frame_begin");
   TRY(settle_all(e));
   e->part_active = false;
   const double *dd;
@@ -2124,7 +2121,7 @@ int vm_partition_frame_begin(vm_engine *e, const double *depth, int32_t h, int32
   F.weight_cap = cfg->weight_cap;
   F.refine = cfg->refine;
   F.frustum_only = cfg->frustum_only;
-  F.epoch = ++e->epoch;
+  if (new_epoch) F.epoch = ++e->epoch;
   F.frame = (int32_t)frame_index;
   F.scope_mode = 0;
   F.strategy = cfg->strategy;
@@ -2137,20 +2134,42 @@ int vm_partition_frame_begin(vm_engine *e, const double *depth, int32_t h, int32
   F.ghost_recv = nullptr;
   F.ghost_max = 0;
   F.ghost_nranks = 0;
+  F.row0 = F.row1 = 0;
+  F.key_out = nullptr;
+  F.key_count = nullptr;
+  F.key_cap = 0;
   TRY(ensure_rays(e, h, w));
   F.nsteps_fixed = fixed_nsteps(e, cfg->trunc);
   F.band_step = F.nsteps_fixed > 1 ? 2.0 / (double)(F.nsteps_fixed - 1) : 0.0;
   F.block_gc_age = cfg->block_gc_age > 0 ? cfg->block_gc_age : 0;
-  TRY(reset_call_counters(e));
+  return VM_OK;
+}
+
+// collect (pixels, or the all-gathered key lists) + integrate owned blocks +
+// pack the boundary blocks for the exchange
+static int partition_frame_begin(vm_engine *e, const uint64_t *keys, int64_t n_keys, uint8_t *send,
+                                 int64_t send_cap, int64_t *n_send, int64_t *n_owned_collected) {
+  FrameDev &F = *e->h_frame;
+  if (keys) {   // (the key pass left the frame's collect counters: clear the rest only)
+    const size_t off = offsetof(Counters, nslab);
+    CK(cudaMemsetAsync((char *)e->S.ctr + off, 0, sizeof(Counters) - off, e->stream));
+  } else {
+    TRY(reset_call_counters(e));
+  }
   e->ctr_clean = false;
   e->restore_calls = false;
   cudaStream_t st = e->stream;
   e->frame_launches = 4;
-  if (F.nsteps_fixed <= 0) {
-    k_depth_stats<<<grid_blocks(e), 256, 0, st>>>(e->S, F);
-    e->frame_launches++;
+  if (keys) {
+    const int g = std::max(1, std::min(grid_threads(e, n_keys, 256), e->sm_count * 8));
+    k_collect_keys_apply<<<g, 256, 0, st>>>(e->S, F, (const unsigned long long *)keys, (int)n_keys);
+  } else {
+    if (F.nsteps_fixed <= 0) {
+      k_depth_stats<<<grid_blocks(e), 256, 0, st>>>(e->S, F);
+      e->frame_launches++;
+    }
+    launch_pdl(k_collect, e->grid_collect, kCollectThreads, st, e->S, F);
   }
-  launch_pdl(k_collect, e->grid_collect, kCollectThreads, st, e->S, F);
   launch_pdl(k_fuse_blocks, e->grid_fuse, kFB, st, e->S, F, (const int32_t *)e->S.scope,
              (const int32_t *)&e->S.ctr->ncollected, 0, (int)(F_INIT | F_INTEGRATE), 0);
   launch_pdl(k_pack_boundary, e->grid_fuse, kFB, st, e->S, F, send, (int)std::min<int64_t>(send_cap, INT32_MAX));
@@ -2171,9 +2190,65 @@ int vm_partition_frame_begin(vm_engine *e, const double *depth, int32_t h, int32
   *n_send = e->h_ctr->nsend;
   *n_owned_collected = e->h_ctr->ncollected;
   e->part_nc_own = e->h_ctr->ncollected;
-  e->part_frame = frame_index;
+  e->part_frame = F.frame;
   e->part_active = true;
   return VM_OK;
+}
+
+int vm_partition_frame_begin(vm_engine *e, const double *depth, int32_t h, int32_t w, int32_t depth_on_device,
+                             const vm_intrinsics *intr, const vm_pose *pose, const vm_frame_config *cfg,
+                             int64_t frame_index, uint8_t *send, int64_t send_cap, int64_t *n_send,
+                             int64_t *n_owned_collected) {
+  if (e) e->ov_ready = false;   // (frame overlap: only a frame right behind a frame)
+  if (!e || !intr || !pose || !cfg || !n_send || !n_owned_collected) return set_err(VM_ERR_INPUT, "null argument");
+  NvtxRange nvtx_("vm_partition_frame_begin");
+  TRY(partition_frame_setup(e, depth, h, w, depth_on_device, intr, pose, cfg, frame_index, true));
+  return partition_frame_begin(e, nullptr, 0, send, send_cap, n_send, n_owned_collected);
+}
+
+int vm_partition_collect_keys(vm_engine *e, const double *depth, int32_t h, int32_t w, int32_t depth_on_device,
+                              const vm_intrinsics *intr, const vm_pose *pose, const vm_frame_config *cfg,
+                              int64_t frame_index, int32_t row0, int32_t row1, uint64_t *keys_dev, int64_t cap,
+                              int64_t *n_keys) {
+  if (e) e->ov_ready = false;
+  if (!e || !intr || !pose || !cfg || !keys_dev || !n_keys) return set_err(VM_ERR_INPUT, "null argument");
+  if (row0 < 0 || row1 < row0 || row0 % 8) return set_err(VM_ERR_VALUE, "row slice must start at a multiple of 8");
+  NvtxRange nvtx_("vm_partition_collect_keys");
+  TRY(partition_frame_setup(e, depth, h, w, depth_on_device, intr, pose, cfg, frame_index, true));
+  FrameDev &F = *e->h_frame;
+  TRY(reset_call_counters(e));
+  e->ctr_clean = false;
+  e->restore_calls = false;
+  int32_t *d_count;
+  TRY(scratch(e, 16, (void **)&d_count));
+  CK(cudaMemsetAsync(d_count, 0, sizeof(int32_t), e->stream));
+  FrameDev Fk = F;
+  Fk.row0 = row0;
+  Fk.row1 = row1;
+  Fk.key_out = (unsigned long long *)keys_dev;
+  Fk.key_count = d_count;
+  Fk.key_cap = (int32_t)std::min<int64_t>(cap, INT32_MAX);
+  if (row1 > row0) {   // (an empty slice only sets the frame up)
+    if (F.nsteps_fixed <= 0) k_depth_stats<<<grid_blocks(e), 256, 0, e->stream>>>(e->S, F);   // (whole image)
+    launch_pdl(k_collect, e->grid_collect, kCollectThreads, e->stream, e->S, Fk);
+    TRY(check_launch());
+  }
+  int32_t cnt = 0;
+  TRY(copy_sync(e, &cnt, d_count, sizeof cnt, cudaMemcpyDeviceToHost));
+  TRY(read_counters(e));
+  TRY(error_from_counters(e));
+  if (cnt > Fk.key_cap) return set_err(VM_ERR_CAPACITY, "key list needs %d entries (capacity %d)", cnt, Fk.key_cap);
+  *n_keys = cnt;
+  return VM_OK;
+}
+
+int vm_partition_frame_begin_keys(vm_engine *e, const uint64_t *keys_dev, int64_t n_keys, uint8_t *send,
+                                  int64_t send_cap, int64_t *n_send, int64_t *n_owned_collected) {
+  if (e) e->ov_ready = false;
+  if (!e || (!keys_dev && n_keys) || !n_send || !n_owned_collected) return set_err(VM_ERR_INPUT, "null argument");
+  NvtxRange nvtx_("vm_partition_frame_begin_keys");
+  static const uint64_t none = 0;
+  return partition_frame_begin(e, keys_dev ? keys_dev : &none, n_keys, send, send_cap, n_send, n_owned_collected);
 }
 
 int vm_partition_repack(vm_engine *e, uint8_t *send, int64_t send_cap, int64_t *n_send) {

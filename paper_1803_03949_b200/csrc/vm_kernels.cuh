@@ -451,7 +451,7 @@ __global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, cons
     if (nsteps < 2) nsteps = 2;
   }
   const double step = F.nsteps_fixed > 0 ? F.band_step : 2.0 / (double)(nsteps - 1);
-  const bool multi = S.nranks > 1;
+  const bool multi = S.nranks > 1 && F.key_out == nullptr;   // (a key list keeps every block)
   trace_at(S, TK_COLLECT, 1);
   __shared__ unsigned long long s_key[kCSet];
   __shared__ uint16_t s_list[kCSet];
@@ -459,7 +459,11 @@ __global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, cons
   __shared__ int s_out[kCSet + kCOver];
   __shared__ int s_n, s_nover, s_valid, s_nout, s_base, s_stop;
   const int t = threadIdx.x, lane = t & 31;
-  const int rx = (F.w + kRegionW - 1) / kRegionW, ry = (F.h + kRegionH - 1) / kRegionH;
+  const int rx = (F.w + kRegionW - 1) / kRegionW;
+  // (the row slice of a sharded band walk: region rows [ry_begin, ry_begin + ry))
+  const int ry_begin = F.row1 > 0 ? F.row0 / kRegionH : 0;
+  const int ry = (F.row1 > 0 ? (min(F.row1, F.h) + kRegionH - 1) / kRegionH : (F.h + kRegionH - 1) / kRegionH) - ry_begin;
+  const bool emit = F.key_out != nullptr;   // list the keys, do not collect
   // Guard (error / heap exhausted): a frame queued behind one that stopped
   // must not write anything -- the host resumes the stopped frame and launches
   // this one again.  Read here, checked before the first write (the load's
@@ -515,7 +519,7 @@ __global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, cons
     for (int q = t; q < kCSet; q += kCollectThreads) s_key[q] = kNoKey;
     if (t == 0) { s_n = 0; s_nover = 0; }
     __syncthreads();
-    const int ry0 = reg / rx, rx0 = reg - ry0 * rx;
+    const int ryl = reg / rx, rx0 = reg - ryl * rx, ry0 = ry_begin + ryl;
     const int u = rx0 * kRegionW + (t & (kRegionW - 1));
     for (int pass = 0; pass < 2; pass++) {   // pass 1 only if the key set overflowed
     const bool direct = pass == 1;
@@ -564,8 +568,13 @@ __global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, cons
         const unsigned grp = __match_any_sync(0xffffffffu, key);
         if (direct) {   // (rare) the set overflowed: probe the table directly
           if (key != kNoKey && lane == __ffs(grp) - 1) {
-            const int got = collect_block(S, F, c[0], c[1], c[2]);
-            if (got >= 0) S.scope[atomicAdd(&ctr->ncollected, 1)] = got;
+            if (emit) {
+              const int at = atomicAdd(F.key_count, 1);
+              if (at < F.key_cap) F.key_out[at] = key;
+            } else {
+              const int got = collect_block(S, F, c[0], c[1], c[2]);
+              if (got >= 0) S.scope[atomicAdd(&ctr->ncollected, 1)] = got;
+            }
           }
           continue;
         }
@@ -593,6 +602,15 @@ __global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, cons
     // the region's distinct blocks, one thread each (+ keys that found the set
     // crowded); the newly collected ones are appended with one atomic per CTA
     const int nk = s_n, no = min(s_nover, kCOver);
+    if (emit) {   // sharded band walk: list the region's distinct keys (one atomic per CTA)
+      if (t == 0) s_base = atomicAdd(F.key_count, nk + no);
+      __syncthreads();
+      for (int q = t; q < nk + no; q += kCollectThreads)
+        if (s_base + q < F.key_cap) F.key_out[s_base + q] = q < nk ? s_key[s_list[q]] : s_over[q - nk];
+      __syncthreads();
+      if (pass == 0) continue;
+      break;
+    }
     if (t == 0) s_nout = 0;
     __syncthreads();
     for (int q0 = 0; q0 < nk + no; q0 += kCollectThreads) {
@@ -637,6 +655,35 @@ __global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, cons
   trace_count(S, TK_COLLECT, nth);
   trace_span(S, 0, F.frame, true);
   trace_at(S, TK_COLLECT, 31);
+}
+
+// Sharded band walk (spatial partition): collect this rank's relevant blocks
+// from the union of the ranks' key lists (k_collect with F.key_out), one key
+// per thread; a block listed by several ranks / regions is collected once
+// (collect_block's stamp exchange).  Appends to the scope list like k_collect.
+__global__ void __launch_bounds__(256) k_collect_keys_apply(DevState S, const FrameDev F,
+                                                            const unsigned long long *__restrict__ keys, int n) {
+  cudaGridDependencySynchronize();
+  if (halted(S)) return;
+  const int lane = threadIdx.x & 31;
+  for (int i0 = blockIdx.x * blockDim.x; i0 < n; i0 += gridDim.x * blockDim.x) {
+    const int i = i0 + threadIdx.x;
+    int got = -1;
+    if (i < n) {
+      const unsigned long long key = __ldg(keys + i);
+      const long long off = 1LL << 20;
+      const int x = (int)((long long)(key >> 42) - off), y = (int)((long long)((key >> 21) & 0x1FFFFF) - off),
+                z = (int)((long long)(key & 0x1FFFFF) - off);
+      // (a word that is not a packed coordinate -- the empty-slot key, say -- is never probed)
+      if (!(key >> 63) && block_relevant(S, x, y, z)) got = collect_block(S, F, x, y, z);
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, got >= 0);
+    if (!bal) continue;
+    int base = 0;
+    if (lane == __ffs(bal) - 1) base = atomicAdd(&S.ctr->ncollected, __popc(bal));
+    base = __shfl_sync(0xffffffffu, base, __ffs(bal) - 1);
+    if (got >= 0) S.scope[base + __popc(bal & ((1u << lane) - 1))] = got;
+  }
 }
 
 // ------------------------------------------------------------ explicit lists
@@ -1058,6 +1105,8 @@ __global__ void __launch_bounds__(kNT, 18) k_retype_place(DevState S, const Fram
   uint32_t *const s_vm8 = U.ty.vm8;
   uint8_t *const s_tc = U.ty.tc, *const s_tp = U.ty.tp;
   __shared__ uint32_t s_claim[3 * 81];   // requested slots: [axis][tile column], bit = owner z
+  __shared__ uint32_t s_mcol[81];        // placement: a column's requested slots (bit 3 z + axis)
+  __shared__ int s_pre[82];              //   and the exclusive prefix of their counts
   __shared__ Resolved R;
   const int t = threadIdx.x, lane = t & 31;
   const double l = S.cube_size;
@@ -1348,86 +1397,96 @@ __global__ void __launch_bounds__(kNT, 18) k_retype_place(DevState S, const Fram
     }
     __syncthreads();
     trace_item(S, TK_RETYPE, nth, 3);
-    // placement (mesher.py:216-235), one tile column per lane: its 3 claim words
-    // interleave into a 27-bit mask, bit 3 z + axis = the slot (z, axis) of the
-    // column's owner cubes -- consecutive slot indices of the owner block
-    // (C-order cubes, 3 slots each), so the column's requests are <= 3 OR
-    // reductions into the owner blocks' claim bitmaps (k_gc_normals turns first
-    // requests into allocations).  The requested slots are then dealt out one
-    // per lane (a warp search over the lanes' prefix counts) for their
-    // coordinate stores; every requester of a slot writes the same bits.
+    // placement (mesher.py:216-235).  Claims, one tile column per lane: its 3
+    // claim words interleave into a 27-bit mask, bit 3 z + axis = the slot
+    // (z, axis) of the column's owner cubes -- consecutive slot indices of the
+    // owner block (C-order cubes, 3 slots each), so the column's requests are
+    // <= 3 OR reductions into the owner blocks' claim bitmaps (k_gc_normals
+    // turns first requests into allocations).  Coordinates: the item's
+    // requested slots in column order are split into 64 equal runs, one per
+    // thread (both warps get the same share whatever the surface's position
+    // in the block); every requester of a slot writes the same bits.
     if (!part) {
       const int wq = t >> 5;
 #pragma unroll
       for (int round = 0; round < 2; round++) {
         // warp 0: columns 0..31, 64..72; warp 1: 32..63, 73..80
         const int col = round == 0 ? wq * 32 + lane : 64 + wq * 9 + lane;
-        const bool has = round == 0 || lane < 9 - wq;
-        uint32_t m = 0;
-        int sA = 0, ox = 0, oy = 0;
-        if (has) {
-          m = part1by2_9(s_claim[col]) | (part1by2_9(s_claim[81 + col]) << 1) |
-              (part1by2_9(s_claim[162 + col]) << 2);
-          if (m) {
-            ox = col / 9;
-            oy = col - 9 * ox;
-            sA = ((ox & 7) * 64 + (oy & 7) * 8) * 3;   // slot of (owner cube z = 0, axis 0)
-            const int A = R.nbr[nbr_dir(ox >> 3, oy >> 3, 0)], B = R.nbr[nbr_dir(ox >> 3, oy >> 3, 1)];
-            const uint32_t mA = m & 0xFFFFFFu, mB = m >> 24;
-            const int off = sA & 31;
-            if (mA) {
-              if (A >= 0) {
-                uint32_t *wp = S.vclaim + (size_t)A * (kEV / 32) + (sA >> 5);
-                atomicOr(wp, mA << off);
-                if (off > 8) atomicOr(wp + 1, mA >> (32 - off));
-              } else {
-                set_error(S, ERR_CONSISTENCY, 10, R.coord.x * kB + ox, R.coord.y * kB + oy,
-                          R.coord.z * kB + (__ffs(mA) - 1) / 3);
-                m &= ~0xFFFFFFu;
-              }
+        if (round == 1 && lane >= 9 - wq) continue;
+        uint32_t m = part1by2_9(s_claim[col]) | (part1by2_9(s_claim[81 + col]) << 1) |
+                     (part1by2_9(s_claim[162 + col]) << 2);
+        if (m) {
+          const int ox = col / 9, oy = col - 9 * ox;
+          const int sA = ((ox & 7) * 64 + (oy & 7) * 8) * 3;   // slot of (owner cube z = 0, axis 0)
+          const int A = R.nbr[nbr_dir(ox >> 3, oy >> 3, 0)], B = R.nbr[nbr_dir(ox >> 3, oy >> 3, 1)];
+          const uint32_t mA = m & 0xFFFFFFu, mB = m >> 24;
+          const int off = sA & 31;
+          if (mA) {
+            if (A >= 0) {
+              uint32_t *wp = S.vclaim + (size_t)A * (kEV / 32) + (sA >> 5);
+              atomicOr(wp, mA << off);
+              if (off > 8) atomicOr(wp + 1, mA >> (32 - off));
+            } else {
+              set_error(S, ERR_CONSISTENCY, 10, R.coord.x * kB + ox, R.coord.y * kB + oy,
+                        R.coord.z * kB + (__ffs(mA) - 1) / 3);
+              m &= ~0xFFFFFFu;
             }
-            if (mB) {
-              if (B >= 0) atomicOr(S.vclaim + (size_t)B * (kEV / 32) + (sA >> 5), mB << off);
-              else {
-                set_error(S, ERR_CONSISTENCY, 10, R.coord.x * kB + ox, R.coord.y * kB + oy, R.coord.z * kB + 8);
-                m &= 0xFFFFFFu;
-              }
+          }
+          if (mB) {
+            if (B >= 0) atomicOr(S.vclaim + (size_t)B * (kEV / 32) + (sA >> 5), mB << off);
+            else {
+              set_error(S, ERR_CONSISTENCY, 10, R.coord.x * kB + ox, R.coord.y * kB + oy, R.coord.z * kB + 8);
+              m &= 0xFFFFFFu;
             }
           }
         }
-        const int cnt = __popc(m);
-        int incl = cnt;
+        s_mcol[col] = m;
+      }
+      __syncthreads();
+      if (t < 32) {   // exclusive prefix of the 81 columns' counts (3 columns per lane)
+        const int c0 = 3 * lane;
+        const int n0 = lane < 27 ? __popc(s_mcol[c0]) : 0, n1 = lane < 27 ? __popc(s_mcol[c0 + 1]) : 0,
+                  n2 = lane < 27 ? __popc(s_mcol[c0 + 2]) : 0;
+        int incl = n0 + n1 + n2;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const int u = __shfl_up_sync(0xffffffffu, incl, o);
           if (lane >= o) incl += u;
         }
-        const int total = __shfl_sync(0xffffffffu, incl, 31);
-        for (int e0 = 0; e0 < total; e0 += 32) {
-          const int e = e0 + lane;
-          // the lane L whose slots hold entry e: the count of lanes with incl <= e
-          int L = 0;
+        const int excl = incl - n0 - n1 - n2;
+        if (lane < 27) {
+          s_pre[c0] = excl;
+          s_pre[c0 + 1] = excl + n0;
+          s_pre[c0 + 2] = excl + n0 + n1;
+        }
+        if (lane == 31) s_pre[81] = incl;
+      }
+      __syncthreads();
+      const int total = s_pre[81];
+      const int per = (total + kNT - 1) / kNT;
+      int e = t * per;
+      const int e_end = min(total, e + per);
+      if (e < e_end) {
+        int c = 0;   // the column holding entry e: the last one with s_pre[c] <= e
 #pragma unroll
-          for (int step = 16; step > 0; step >>= 1) {
-            const int v = __shfl_sync(0xffffffffu, incl, L + step - 1);
-            if (v <= e) L += step;
-          }
-          uint32_t bm = __shfl_sync(0xffffffffu, m, L);
-          const int k = e - (__shfl_sync(0xffffffffu, incl, L) - __popc(bm));
-          if (e < total) {
-            const int bit = select_bit(bm, k);
-            const int z = bit / 3, axis = bit - 3 * z;
-            const int c = round == 0 ? wq * 32 + L : 64 + wq * 9 + L;
-            const int cx = c / 9, cy = c - 9 * cx;
-            const int owner = R.nbr[nbr_dir(cx >> 3, cy >> 3, z >> 3)];
-            const size_t slot = (size_t)owner * kEV + ((cx & 7) * 64 + (cy & 7) * 8 + (z & 7)) * 3 + axis;
-            // start corner = the owner point; end corner one step along the axis
-            const int pt = c * 9 + z;
-            const double d0 = tile[pt], d1 = tile[pt + (axis == 0 ? 81 : axis == 1 ? 9 : 1)];
-            const double param = (d0 == d1) ? 0.5 : d0 / (d0 - d1);
-            const int ga = axis == 0 ? R.coord.x * kB + cx : axis == 1 ? R.coord.y * kB + cy : R.coord.z * kB + z;
-            S.vparam[slot] = __dadd_rn(__dmul_rn((double)ga, l), __dmul_rn(param, l));
-          }
+        for (int step = 64; step > 0; step >>= 1)
+          if (c + step < 81 && s_pre[c + step] <= e) c += step;
+        uint32_t m = s_mcol[c];
+        for (int k = e - s_pre[c]; k > 0; k--) m &= m - 1;   // (skip the column's first entries)
+        for (; e < e_end; e++) {
+          while (!m) m = s_mcol[++c];
+          const int bit = __ffs(m) - 1;
+          m &= m - 1;
+          const int z = bit / 3, axis = bit - 3 * z;
+          const int cx = c / 9, cy = c - 9 * cx;
+          const int owner = R.nbr[nbr_dir(cx >> 3, cy >> 3, z >> 3)];
+          const size_t slot = (size_t)owner * kEV + ((cx & 7) * 64 + (cy & 7) * 8 + (z & 7)) * 3 + axis;
+          // start corner = the owner point; end corner one step along the axis
+          const int pt = c * 9 + z;
+          const double d0 = tile[pt], d1 = tile[pt + (axis == 0 ? 81 : axis == 1 ? 9 : 1)];
+          const double param = (d0 == d1) ? 0.5 : d0 / (d0 - d1);
+          const int ga = axis == 0 ? R.coord.x * kB + cx : axis == 1 ? R.coord.y * kB + cy : R.coord.z * kB + z;
+          S.vparam[slot] = __dadd_rn(__dmul_rn((double)ga, l), __dmul_rn(param, l));
         }
       }
     }

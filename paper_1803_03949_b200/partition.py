@@ -285,7 +285,7 @@ class PartitionedEngine:
     """
 
     def __init__(self, config, intrinsics, group=None, tile_blocks: int = 8, device=None,
-                 halo: str = "margin"):
+                 halo: str = "margin", shard_band: bool = True):
         import dataclasses
 
         import torch
@@ -297,6 +297,10 @@ class PartitionedEngine:
         self.rank = dist.get_rank(group)
         self.nranks = dist.get_world_size(group)
         self.halo = halo
+        # halo exchange: each rank walks 1/N of the pixel rows and the ranks
+        # all-gather the block keys they met (vm_partition_collect_keys)
+        self.shard_band = bool(shard_band) and halo == "exchange" and self.nranks > 1
+        self._keys = None
         self.nccl = _is_nccl(group)
         self.device = torch.device(device) if device is not None else torch.device(
             "cuda", torch.cuda.current_device())
@@ -307,6 +311,7 @@ class PartitionedEngine:
         self.stats = []
         self._send = None
         self.exchange_log = []   # per frame: records sent by each rank (halo exchange)
+        self.key_log = []        # per frame: block keys listed by each rank (sharded band walk)
 
     # -- collectives ---------------------------------------------------------
     def _stream_ctx(self):
@@ -372,11 +377,37 @@ class PartitionedEngine:
         torch.cuda.synchronize(self.device)
         n_send, n_own = C.c_int64(), C.c_int64()
         e.store._touch()
-        _lib.check(L.vm_partition_frame_begin(e.store._h, ptr, h, w, on_dev, C.byref(e._intr_c),
-                                              C.byref(_lib.pose_c(pose)), C.byref(e._fcfg),
-                                              e.frame_index, C.c_void_p(self._send.data_ptr()),
-                                              self._send.numel() // rec, C.byref(n_send),
-                                              C.byref(n_own)))
+        if self.shard_band:
+            # this rank's pixel-row slice (multiples of 8 rows), its block keys,
+            # all-gathered: every rank then collects its relevant blocks from the union
+            rows = [(h * r // self.nranks) // 8 * 8 for r in range(self.nranks)] + [h]
+            r0, r1 = rows[self.rank], rows[self.rank + 1]
+            if self._keys is None:
+                self._keys = torch.empty(1 << 20, dtype=torch.int64, device=self.device)
+            nk = C.c_int64(0)
+            _lib.check(L.vm_partition_collect_keys(e.store._h, ptr, h, w, on_dev, C.byref(e._intr_c),
+                                                   C.byref(_lib.pose_c(pose)), C.byref(e._fcfg), e.frame_index,
+                                                   r0, r1, C.c_void_p(self._keys.data_ptr()),
+                                                   self._keys.numel(), C.byref(nk)))
+            kc = self._all_gather_ints([nk.value]).reshape(-1)
+            kmax = int(kc.max())
+            allk = None
+            if kmax:
+                g = self._all_gather_bytes(self._keys.view(torch.uint8), kmax * 8).view(torch.int64)
+                allk = torch.cat([g[q * kmax:q * kmax + int(kc[q])] for q in range(self.nranks)])
+                torch.cuda.synchronize(self.device)   # (the engine's stream reads the union next)
+            self.key_log.append(kc.tolist())
+            _lib.check(L.vm_partition_frame_begin_keys(
+                e.store._h, C.c_void_p(allk.data_ptr()) if allk is not None else None,
+                int(allk.numel()) if allk is not None else 0, C.c_void_p(self._send.data_ptr()),
+                self._send.numel() // rec, C.byref(n_send), C.byref(n_own)))
+            del allk
+        else:
+            _lib.check(L.vm_partition_frame_begin(e.store._h, ptr, h, w, on_dev, C.byref(e._intr_c),
+                                                  C.byref(_lib.pose_c(pose)), C.byref(e._fcfg),
+                                                  e.frame_index, C.c_void_p(self._send.data_ptr()),
+                                                  self._send.numel() // rec, C.byref(n_send),
+                                                  C.byref(n_own)))
         if n_send.value > self._send.numel() // rec:
             self._send = torch.empty(int(n_send.value * 1.25 + 64) * rec, dtype=torch.uint8,
                                      device=self.device)

@@ -23,6 +23,8 @@ def main():
     ap.add_argument("--backend", default="gloo")
     ap.add_argument("--out", required=True)
     a = ap.parse_args()
+    import faulthandler
+    faulthandler.dump_traceback_later(120, exit=True)   # (a hung rank reports where, then exits)
     import torch
     import torch.distributed as dist
     from paper_1803_03949_b200 import Intrinsics, Pose, RunConfig
@@ -43,7 +45,9 @@ def main():
         i6 = g["intr6"]
         intr = Intrinsics(float(i6[0]), float(i6[1]), float(i6[2]), float(i6[3]), int(i6[4]), int(i6[5]))
         frames = [(g["depth"][i], Pose(g["rot"][i], g["trans"][i])) for i in range(len(g["depth"]))]
-    pe = PartitionedEngine(RunConfig(**cfg), intr, tile_blocks=a.tile_blocks, halo=a.halo)
+    halo = "exchange" if a.halo.startswith("exchange") else a.halo
+    pe = PartitionedEngine(RunConfig(**cfg), intr, tile_blocks=a.tile_blocks, halo=halo,
+                           shard_band=a.halo == "exchange-shard")
     rows = []
     for d, p in frames:
         r = pe.fuse_frame(d, p)

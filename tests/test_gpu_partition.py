@@ -94,7 +94,7 @@ def _intr_of(g):
 
 
 @pytest.mark.parametrize("name", ENGINE_SCENES)
-@pytest.mark.parametrize("halo", ["margin", "exchange"])
+@pytest.mark.parametrize("halo", ["margin", "exchange", "exchange-shard"])
 @pytest.mark.parametrize("nranks,tile_blocks", [(2, 1), (3, 2), (4, 8)])
 def test_distributed_compaction_and_halo_exchange_match_reference_golden(name, halo, nranks, tile_blocks):
     """Halo exchange (owners integrate; boundary blocks all-gathered and
@@ -113,7 +113,7 @@ def test_distributed_compaction_and_halo_exchange_match_reference_golden(name, h
         got = (i, c["blocks_active"], c["vertices_live"], c["triangles_live"],
                c["vertices_allocated_total"], c["vertices_recycled_total"], c["irregular_cube_count"])
         assert got == tuple(g["stats"][i]), (name, i)
-    if halo == "exchange" and tile_blocks == 1:
+    if halo != "margin" and tile_blocks == 1:
         assert sum(map(sum, log)) > 0                  # records actually crossed ranks
     _check_mesh(compact_local([e.store for e in engines], engines[0].frame_index), g)
 
@@ -129,12 +129,18 @@ def test_halo_exchange_integrates_owned_blocks_only():
     intr = spec.intrinsics()
     m = rank_engines(cfg, intr, 2, 8, "margin")
     x = rank_engines(cfg, intr, 2, 8, "exchange")
+    xs = rank_engines(cfg, intr, 2, 8, "exchange-shard")
     log = []
     for i in range(0, 12, 3):
         pose = camera_pose(spec, i)
         d = render_depth(spec, pose)
         rm = fuse_all(m, d, pose, "margin")
         rx = fuse_all(x, d, pose, "exchange", log)
+        rs = fuse_all(xs, d, pose, "exchange-shard")
+        for a, b in zip(rx, rs):   # (the sharded band walk collects the same blocks)
+            assert a["collected_blocks"] == b["collected_blocks"]
+            for k in ("blocks_active", "vertices_live", "triangles_live", "irregular_cube_count"):
+                assert a[k] == b[k], k
         for a, b in zip(rm, rx):
             assert b["collected_blocks"] == a["collected_blocks"]      # owned + adopted margin
             for k in ("blocks_active", "vertices_live", "triangles_live", "irregular_cube_count"):
@@ -148,7 +154,7 @@ def test_halo_exchange_integrates_owned_blocks_only():
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("halo", ["margin", "exchange"])
+@pytest.mark.parametrize("halo", ["margin", "exchange", "exchange-shard"])
 def test_c2_halo_modes_full_resolution_match_oracle(halo):
     """C2 (640x480, 8 mm), 2 and 4 ranks, 16 frames: rows every frame and the
     distributed compaction against the CPU oracle."""
