@@ -83,6 +83,8 @@ struct alignas(16) Counters {
   int32_t nnew;
   unsigned long long maxnorm_bits;
   unsigned long long t_start_ns;   // %globaltimer: k_collect (or k_depth_stats) start
+  int32_t fb_next;                 // k_collect: the previous frame's fallback records handed out so far
+  int32_t pad3[3];
   // ---- per call, cleared by k_gc_normals' commit ----------------------------
   // (one 16-byte word: the meshing kernels' prologues read it with one load)
   int32_t nslab;
@@ -113,7 +115,8 @@ struct alignas(16) Counters {
 };
 static_assert(sizeof(Counters) % 16 == 0, "snapshots are copied in 16-byte words");
 static_assert(offsetof(Counters, nvalid) % 16 == 0 && offsetof(Counters, ncollected) == offsetof(Counters, nvalid) + 8 &&
-              offsetof(Counters, t_start_ns) == offsetof(Counters, nvalid) + 24, "collect region: 2 words");
+              offsetof(Counters, t_start_ns) == offsetof(Counters, nvalid) + 24 &&
+              offsetof(Counters, fb_next) == offsetof(Counters, nvalid) + 32, "collect region: 3 words");
 static_assert(offsetof(Counters, nslab) % 16 == 0 && offsetof(Counters, nitems_live) == offsetof(Counters, nslab) + 8,
               "prologue word: nslab, nexplicit, nitems_live, nhalo");
 static_assert(offsetof(Counters, sv_nvalid) % 16 == 0, "saved collect region: 16-byte words");

@@ -306,21 +306,23 @@ __device__ __forceinline__ void fallback_normal_warp(const double *__restrict__ 
     fn[1] = __dmul_rn(a[2], bb[0]) - __dmul_rn(a[0], bb[2]);
     fn[2] = __dmul_rn(a[0], bb[1]) - __dmul_rn(a[1], bb[0]);
   }
-  // ordered accumulation: k major, then cube rank, then triangle slot
-  int mykey = kpos >= 0 ? (kpos * 4 + jrank) * 5 + s : (1 << 20);
+  // ordered accumulation: k major, then cube rank, then triangle slot.  The
+  // pending lanes' keys are distinct and < 60: their ranks come from one
+  // 64-bit presence mask, then the contributions are added in rank order
+  const bool pend = kpos >= 0;
+  const int mykey = pend ? (kpos * 4 + jrank) * 5 + s : 0;
+  const unsigned klo = __reduce_or_sync(0xffffffffu, pend && mykey < 32 ? 1u << mykey : 0u);
+  const unsigned khi = __reduce_or_sync(0xffffffffu, pend && mykey >= 32 ? 1u << (mykey - 32) : 0u);
+  const int myrank = !pend ? -1
+                     : mykey < 32 ? __popc(klo & ((1u << mykey) - 1u))
+                                  : __popc(klo) + __popc(khi & ((1u << (mykey - 32)) - 1u));
   double acc[3] = {0.0, 0.0, 0.0};
-  const int npend = __popc(__ballot_sync(0xffffffffu, kpos >= 0));
+  const int npend = __popc(klo) + __popc(khi);
   for (int it = 0; it < npend; it++) {
-    int best = mykey, bl = lane;   // pending lane with the smallest key
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const int ok = __shfl_xor_sync(0xffffffffu, best, o), ol = __shfl_xor_sync(0xffffffffu, bl, o);
-      if (ok < best || (ok == best && ol < bl)) { best = ok; bl = ol; }
-    }
+    const int bl = __ffs(__ballot_sync(0xffffffffu, myrank == it)) - 1;
     acc[0] = __dadd_rn(acc[0], __shfl_sync(0xffffffffu, fn[0], bl));
     acc[1] = __dadd_rn(acc[1], __shfl_sync(0xffffffffu, fn[1], bl));
     acc[2] = __dadd_rn(acc[2], __shfl_sync(0xffffffffu, fn[2], bl));
-    if (lane == bl) mykey = 1 << 20;
   }
   if (lane == 0) {
     const double nrm = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(acc[0], acc[0]), __dmul_rn(acc[1], acc[1])),
@@ -352,12 +354,30 @@ struct FallbackArgs {   // what the consumer touches (passed by value: no DevSta
   double cube_size;
 };
 
-// The call's face-normal fallback worklist, after the grid barrier: entries
-// are spread statically over every warp of the grid, one warp per entry.
-// Apply fallback records [0, n): warp `first` of `nwarps` takes every nwarps-th.
-__device__ __noinline__ void consume_fallbacks(const FallbackArgs S, int n, int first, int nwarps) {
+__device__ __noinline__ void consume_fallback(const FallbackArgs S, int f);
+
+// Apply fallback records [0, n), one warp per record: warp `first` of
+// `nwarps` takes record `first`, and when there are more records than warps
+// (C5: ~7.6 k records for ~1.1 k warps) the warps that finish first take the
+// rest one at a time from a counter (*next, requested while the current
+// record is processed) -- the spare CTAs are dispatched last and a few at a
+// time under the previous frame's gc, so a static share would leave the last
+// ones with the longest chains.
+__device__ __noinline__ void consume_fallbacks(const FallbackArgs S, int n, int first, int nwarps, int32_t *next) {
   const int lane = threadIdx.x & 31;
-  for (int f = first; f < n; f += nwarps) {
+  int f = first;
+  while (f < n) {
+    int fn = n;
+    if (n > nwarps && lane == 0) fn = nwarps + atomicAdd(next, 1);
+    consume_fallback(S, f);
+    f = __shfl_sync(0xffffffffu, fn, 0);
+  }
+}
+
+// one record (its warp)
+__device__ __noinline__ void consume_fallback(const FallbackArgs S, int f) {
+  const int lane = threadIdx.x & 31;
+  {
     // record: block, slot | candidate mask << 11, the 4 cube types, the vertex record
     const int4 rec = __ldcg(S.fallback + f);
     const int b = rec.x, sl = rec.y & 2047;
@@ -494,7 +514,7 @@ __global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, cons
   if (F.consume_fb && spare && (int)blockIdx.x >= nreg) {
     const int nfb = min(ld_vol(&ctr->fb_pending), S.fb_cap);   // (records past the ring were applied inline)
     consume_fallbacks(FallbackArgs{S.ctr, S.fallback, S.nbr, S.bcoord, S.vparam, S.vrec, S.cube_size}, nfb,
-                      (blockIdx.x - nreg) * wpc + (t >> 5), ((int)gridDim.x - nreg) * wpc);
+                      (blockIdx.x - nreg) * wpc + (t >> 5), ((int)gridDim.x - nreg) * wpc, &ctr->fb_next);
   }
   int nvalid = 0, nth = 0;
   if (t == 0) s_valid = 0;
@@ -643,8 +663,9 @@ __global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, cons
   if (F.consume_fb && !spare) {
     const int nfb = min(ld_vol(&ctr->fb_pending), S.fb_cap);   // (records past the ring were applied inline)
     consume_fallbacks(FallbackArgs{S.ctr, S.fallback, S.nbr, S.bcoord, S.vparam, S.vrec, S.cube_size}, nfb,
-                      blockIdx.x * wpc + (t >> 5), (int)gridDim.x * wpc);
+                      blockIdx.x * wpc + (t >> 5), (int)gridDim.x * wpc, &ctr->fb_next);
   }
+
   if (F.nsteps_fixed > 0) {   // valid-pixel count (k_depth_stats did not run): one atomic per CTA
     nvalid = __reduce_add_sync(0xffffffffu, (unsigned)nvalid);
     if (lane == 0 && nvalid) atomicAdd(&s_valid, nvalid);
@@ -1800,6 +1821,7 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
         ctr->sv_nblocks = nb; ctr->sv_nfree = nf; ctr->sv_nblocks_owned = no;
         *reinterpret_cast<int4 *>(&ctr->nvalid) = make_int4(0, 0, 0, 0);
         *reinterpret_cast<ulonglong2 *>(&ctr->maxnorm_bits) = make_ulonglong2(0ull, 0ull);
+        *reinterpret_cast<int4 *>(&ctr->fb_next) = make_int4(0, 0, 0, 0);
         __threadfence();
       }
       __syncthreads();
@@ -2374,8 +2396,8 @@ __global__ void k_scatter_samples(DevState S, const int32_t *idx, int n, const d
 // or changed outside fuse_frame)
 __global__ void __launch_bounds__(128) k_flush_fallbacks(DevState S) {
   const int n = min(ld_vol(&S.ctr->fb_pending), S.fb_cap);
-  consume_fallbacks(FallbackArgs{S.ctr, S.fallback, S.nbr, S.bcoord, S.vparam, S.vrec, S.cube_size}, n,
-                    blockIdx.x * 4 + (threadIdx.x >> 5), (int)gridDim.x * 4);
+  const FallbackArgs A{S.ctr, S.fallback, S.nbr, S.bcoord, S.vparam, S.vrec, S.cube_size};
+  for (int f = blockIdx.x * 4 + (threadIdx.x >> 5); f < n; f += (int)gridDim.x * 4) consume_fallback(A, f);
 }
 
 // phase API (mesher.extract_frame with an arbitrary halo): apply every pending
