@@ -133,3 +133,29 @@ def test_collect_capacity_error_raised_for_its_own_frame():
     assert raised_at == k + 1, (raised_at, k)
     assert [tuple(d[q] for q in ROW_KEYS) for d in ov.device_stats[:k]] == _rows(sync)[:k]
     assert ov.store.block_count == sync.store.block_count
+
+
+@pytest.mark.parametrize("raw", [False, True])
+def test_host_copied_frames_overlap_and_match(raw):
+    """Host frames (pinned f64, or raw u16 as read_depth would decode them):
+    the copy stream posts a per-slot flag that k_collect waits for, so these
+    frames overlap too; rows and mesh equal the synchronous engine's."""
+    import torch
+    from paper_1803_03949_b200 import Engine, RunConfig
+    spec, cfg, poses, depths = _frames("C2", 24)
+    caps = dict(block_capacity=30_000, vertex_capacity=12_000_000)
+    host = [d.cpu().numpy() for d in depths]
+    if raw:
+        host = [np.clip(np.rint(h * 5000.0), 0, 65535).astype(np.uint16) for h in host]
+        conv = [torch.from_numpy(h.astype(np.float64) / 5000.0).cuda() for h in host]
+    ov = Engine(RunConfig(**cfg, **caps), spec.intrinsics(), pipelined=True)
+    for h, p in zip(host, poses):
+        buf = h.copy()
+        (ov.fuse_frame_raw if raw else ov.fuse_frame)(buf, p)
+        buf[...] = 0   # (the engine must be done reading it on return)
+    ov.stats[-1].blocks_active
+    sync = _run(spec, cfg, poses, conv if raw else depths, pipelined=False)
+    flags = [d["overlapped"] for d in ov.device_stats]
+    assert flags[0] == 0 and sum(flags[1:]) >= len(flags) - 2, flags
+    assert _rows(ov) == _rows(sync)
+    _same_mesh(ov, sync)
