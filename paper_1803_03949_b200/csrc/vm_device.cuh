@@ -84,7 +84,8 @@ struct alignas(16) Counters {
   unsigned long long maxnorm_bits;
   unsigned long long t_start_ns;   // %globaltimer: k_collect (or k_depth_stats) start
   int32_t fb_next;                 // k_collect: the previous frame's fallback records handed out so far
-  int32_t pad3[3];
+  int32_t ds_done;                 // k_depth_stats CTAs done (an overlapped k_collect waits for all)
+  int32_t pad3[2];
   // ---- per call, cleared by k_gc_normals' commit ----------------------------
   // (one 16-byte word: the meshing kernels' prologues read it with one load)
   int32_t nslab;
@@ -159,6 +160,8 @@ struct FrameDev {
   // (no event wait on the engine's stream, which would keep the frames apart)
   const unsigned long long *in_flag;
   unsigned long long in_id;
+  int32_t ds_wait;      // > 0: k_collect waits until that many k_depth_stats CTAs are done (overlap)
+  int32_t pad_ds;
   // spatial partition, sharded band walk: k_collect walks pixel rows
   // [row0, row1) only (row1 <= 0: all) and, with key_out set, lists the
   // distinct block keys it meets there (every block, owned or not) instead of

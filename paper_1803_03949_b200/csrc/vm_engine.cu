@@ -493,6 +493,7 @@ static void fill_frame_host(vm_engine *e, const double *depth_dev, int32_t h, in
   F.wait_epoch = 0;
   F.in_flag = nullptr;
   F.in_id = 0;
+  F.ds_wait = 0;
   F.depth = depth_dev;
   F.h = h;
   F.w = w;
@@ -1075,8 +1076,8 @@ static int launch_frame(vm_engine *e, int slot) {
   // (and only on the engine's own stream: a caller's kernel queued on a shared
   // stream between the frames could write what this k_collect reads, and it
   // skips the grid-dependency wait)
-  const bool overlap = e->ov_ready && e->own_stream && e->ctr_clean && !e->profiling && F.nsteps_fixed > 0 &&
-                       !gc_frame && e->S.max_vertices <= 0 && !e->no_overlap;
+  const bool overlap = e->ov_ready && e->own_stream && e->ctr_clean && !e->profiling && !gc_frame &&
+                       e->S.max_vertices <= 0 && !e->no_overlap;
   const int32_t wait_epoch = overlap ? e->ov_epoch : 0;
   e->ov_ready = false;
   if (!e->ctr_clean) TRY(reset_call_counters(e));
@@ -1094,15 +1095,18 @@ static int launch_frame(vm_engine *e, int slot) {
   e->ov_of[slot] = overlap;
   Fc.wait_epoch = wait_epoch;
   if (F.nsteps_fixed <= 0) {
-    if (F.in_flag) {   // (k_depth_stats reads the depth first: order it after the copy on the stream)
-      Fc.overlap = 0;
-      Fc.wait_epoch = 0;
-      e->ov_of[slot] = false;
-      CK(cudaStreamWaitEvent(st, e->ev_copy[(int)(F.in_flag - e->d_inseq)], 0));
-    }
-    k_depth_stats<<<grid_blocks(e), 256, 0, st>>>(e->S, F);
+    // the band step count needs the frame's max ray norm first: under overlap
+    // this pass also starts under the previous gc (PDL, no grid-dependency
+    // wait; it waits for the host copy's flag itself) and the collect waits
+    // for its CTAs on a counter
+    FrameDev Fd = F;
+    Fd.overlap = overlap ? 1 : 0;
+    if (overlap) launch_pdl(k_depth_stats, grid_blocks(e), 256, st, e->S, Fd);
+    else k_depth_stats<<<grid_blocks(e), 256, 0, st>>>(e->S, Fd);
     e->frame_launches++;
     Fc.raw = nullptr;
+    Fc.in_flag = nullptr;   // (k_depth_stats waited for the copy)
+    Fc.ds_wait = overlap ? grid_blocks(e) : 0;
   }
   rec(e, PH_COLLECT);
   launch_pdl(k_collect, e->grid_collect, kCollectThreads, st, e->S, Fc);

@@ -125,9 +125,36 @@ __device__ __forceinline__ void publish_snapshot(const FrameDev &F) {
   }
 }
 
+// The frame's host copy has landed (copy-stream flag, FrameDev::in_flag): one
+// thread polls, the CTA waits
+__device__ __forceinline__ void wait_input_flag(const DevState &S, const FrameDev &F) {
+  if (!F.in_flag) return;
+  if (threadIdx.x == 0) {
+    const unsigned long long t0 = gtimer();
+    for (;;) {
+      unsigned long long v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(v) : "l"(F.in_flag) : "memory");
+      if (v >= F.in_id) break;
+      if (gtimer() - t0 > 2000000000ull) {   // (2 s: the copy failed -- raise, never hang)
+        set_error(S, ERR_CONSISTENCY, 60);
+        break;
+      }
+      __nanosleep(256);
+    }
+  }
+  __syncthreads();
+}
+
 // ------------------------------------------------------------ depth stats
+__device__ __forceinline__ void wait_input_flag(const DevState &S, const FrameDev &F);
+
 __global__ void __launch_bounds__(256) k_depth_stats(DevState S, const FrameDev F) {
-  cudaGridDependencySynchronize();   // PDL: wait for the previous kernel of the frame
+  // PDL: wait for the previous kernel -- except behind the previous frame's
+  // k_gc_normals (F.overlap): this pass reads only the frame's depth (after
+  // its host copy, when there is one) and writes collect counters the gc
+  // cleared before it let this frame launch
+  if (!F.overlap) cudaGridDependencySynchronize();
+  wait_input_flag(S, F);
   if (blockIdx.x == 0 && threadIdx.x == 0) S.ctr->t_start_ns = gtimer();
   __shared__ double smax[8];
   __shared__ int scnt[8];
@@ -155,6 +182,7 @@ __global__ void __launch_bounds__(256) k_depth_stats(DevState S, const FrameDev 
   cnt = warp_sum(cnt);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (lane == 0) { smax[wid] = best; scnt[wid] = cnt; }
+  if (F.raw) __threadfence();   // (the f64 depth written here is read by an overlapped k_collect)
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int w = 1; w < (int)(blockDim.x >> 5); w++) { best = fmax(best, smax[w]); cnt += scnt[w]; }
@@ -162,6 +190,8 @@ __global__ void __launch_bounds__(256) k_depth_stats(DevState S, const FrameDev 
       atomicAdd(&S.ctr->nvalid, cnt);
       atomicMax(&S.ctr->maxnorm_bits, (unsigned long long)__double_as_longlong(best));
     }
+    __threadfence();
+    atomicAdd(&S.ctr->ds_done, 1);   // (an overlapped k_collect counts the CTAs done)
   }
 }
 
@@ -462,8 +492,14 @@ __global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, cons
     publish_snapshot(F);
   }
   int nsteps = F.nsteps_fixed;
-  if (nsteps <= 0) {
-    if (ld_vol(&ctr->nvalid) == 0) return;
+  if (nsteps <= 0 && F.ds_wait > 0) {   // (overlapped: no grid-dependency wait covers k_depth_stats)
+    if (threadIdx.x == 0)
+      while (ld_acquire(&ctr->ds_done) < F.ds_wait) __nanosleep(128);
+    __syncthreads();
+  }
+  if (nsteps <= 0 && ld_vol(&ctr->nvalid) == 0) {
+    nsteps = 0;   // (no valid pixel: no band samples; the spare CTAs' work still runs)
+  } else if (nsteps <= 0) {
     const double maxnorm = __longlong_as_double((long long)ld_vol(&ctr->maxnorm_bits));
     const double half_block = S.extent * 0.5;
     const double band = __dmul_rn(__dmul_rn(2.0, F.trunc), maxnorm);
@@ -518,22 +554,7 @@ __global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, cons
   }
   int nvalid = 0, nth = 0;
   if (t == 0) s_valid = 0;
-  if (F.in_flag && (int)blockIdx.x < nreg) {   // the frame's host copy has landed (copy-stream flag)
-    if (t == 0) {
-      const unsigned long long t0 = gtimer();
-      for (;;) {
-        unsigned long long v;
-        asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(v) : "l"(F.in_flag) : "memory");
-        if (v >= F.in_id) break;
-        if (gtimer() - t0 > 2000000000ull) {   // (2 s: the copy failed -- raise, never hang)
-          set_error(S, ERR_CONSISTENCY, 60);
-          break;
-        }
-        __nanosleep(256);
-      }
-    }
-    __syncthreads();
-  }
+  if ((int)blockIdx.x < nreg) wait_input_flag(S, F);   // the frame's host copy has landed
   for (int reg = blockIdx.x; reg < rx * ry; reg += gridDim.x, nth++) {
     trace_item(S, TK_COLLECT, nth, 0);
     for (int q = t; q < kCSet; q += kCollectThreads) s_key[q] = kNoKey;

@@ -159,3 +159,17 @@ def test_host_copied_frames_overlap_and_match(raw):
     assert flags[0] == 0 and sum(flags[1:]) >= len(flags) - 2, flags
     assert _rows(ov) == _rows(sync)
     _same_mesh(ov, sync)
+
+
+def test_overlap_with_depth_stats_pass_c4():
+    """C4 (4 mm, 40 mm band): the band step count depends on the frame's
+    valid pixels, so k_depth_stats runs first -- it too starts under the
+    previous gc, and the collect waits for its CTAs on a counter."""
+    spec, cfg, poses, depths = _frames("C4", 12)
+    caps = dict(block_capacity=80_000, vertex_capacity=24_000_000)
+    ov = _run(spec, cfg, poses, depths, pipelined=True, **caps)
+    sync = _run(spec, cfg, poses, depths, pipelined=False)
+    flags = [d["overlapped"] for d in ov.device_stats]
+    assert flags[0] == 0 and all(flags[1:]), flags
+    assert _rows(ov) == _rows(sync)
+    _same_mesh(ov, sync)
