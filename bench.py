@@ -413,12 +413,15 @@ def run_gpu(args, spec, cfg, rank, world, local_rank):
 
     # timed region for `value`: no per-kernel events (an event between two
     # kernels would serialise their programmatic-dependent launch)
+    # (every mode but the halo exchange, whose frames are synchronous around
+    # their collectives, streams its frames: a partition rank's engine walks
+    # the broadcast frames back to back like a single GPU's)
     stream_ms = None
     with ClockSampler(local_rank) as clocks:
-        if not part:
+        if not xchg:
             eng, stream_ms, resumes = timed_stream()
         eng_f, frame_ms, _, flushed_resumes = timed_pass(False)
-        if part:
+        if xchg:
             eng, resumes = eng_f, flushed_resumes
         del eng_f
     # second pass on a fresh engine (same frames, same state evolution) with an
@@ -426,15 +429,20 @@ def run_gpu(args, spec, cfg, rank, world, local_rank):
     _, prof_frame_ms, phase_ms, _ = timed_pass(True) if not xchg else (None, frame_ms, [], 0)
     flushed_s = sum(frame_ms) / 1e3   # per-frame, L2 flushed before each frame (no overlap)
     local_s = stream_ms / 1e3 if stream_ms is not None else flushed_s
+    # partition: the ranks process the same frames jointly (strong scaling),
+    # the job's time is the slowest rank's; replicas: N independent streams
     if part:
-        # frames are processed jointly: a frame ends when its slowest rank ends
-        dev_s = sum(reduce_(frame_ms, dist.ReduceOp.MAX)) / 1e3
-        value = args.steps / dev_s
+        # flushed per frame: a frame ends when its slowest rank ends
+        flushed_dev_s = sum(reduce_(frame_ms, dist.ReduceOp.MAX)) / 1e3
+        flushed_value = args.steps / flushed_dev_s
     else:
-        dev_s = local_s
-        if world > 1:
-            dev_s = reduce_([dev_s], dist.ReduceOp.MAX)[0]
-        value = world * args.steps / dev_s
+        flushed_dev_s = reduce_([flushed_s], dist.ReduceOp.MAX)[0] if world > 1 else flushed_s
+        flushed_value = world * args.steps / flushed_dev_s
+    if stream_ms is None:
+        dev_s, value = flushed_dev_s, flushed_value
+    else:
+        dev_s = reduce_([local_s], dist.ReduceOp.MAX)[0] if world > 1 else local_s
+        value = (1 if part else world) * args.steps / dev_s
     stats = eng.device_stats[args.warmup:]
     mc = eng.store._counters()   # HBM footprint of the final store
     memory = {"store_bytes": mc["store_bytes"], "blocks": mc["block_count"], "vertex_records": mc["vertex_records"],
@@ -546,8 +554,7 @@ def run_gpu(args, spec, cfg, rank, world, local_rank):
                      "frame_achieved_gbs": frame_bytes / local_s / 1e9,
                      "frame_frac": frame_bytes / local_s / 1e9 / peak},
         "phase_ms_mean": {n: tot[n] / args.steps for n in names},
-        "value_l2_flushed": {"value": world * args.steps / (reduce_([flushed_s], dist.ReduceOp.MAX)[0]
-                                                            if world > 1 and not part else flushed_s),
+        "value_l2_flushed": {"value": flushed_value,
                              "unit": "frames/s",
                              "how": "each frame timed alone (enqueue, events around it, L2 flushed by a 256 MiB "
                                     "write before it): no frame overlap, cold L2"},
