@@ -323,10 +323,10 @@ def run_gpu(args, spec, cfg, rank, world, local_rank):
         probe.fuse_frame(depths[i], poses[i])
     pc = probe.store._counters()
     # vertex records: what the scene ends with + k_retype_place's per-frame bound
-    # (2187 per scope item) + the gc CTAs' chunk runs
+    # (2187 per scope item) + the gc CTAs' record ranges (4 chunks per CTA, <= 4096 CTAs)
     max_items = max(d["scope_blocks"] for d in probe.device_stats)
     caps = dict(block_capacity=pc["block_count"] + 64,
-                vertex_capacity=pc["vertex_records"] + 2187 * max_items + 2 * 64 * 2048 + 4096)
+                vertex_capacity=pc["vertex_records"] + 2187 * max_items + 4 * 64 * 4096 + 4096)
     del probe
 
     flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.int32, device=dev)

@@ -1658,9 +1658,9 @@ __device__ __forceinline__ size_t sample_index(const int *s_nbr, int lx, int ly,
 // publishes it to the host) and with F.reset_after clears the per-call
 // counters for the next frame -- so consecutive frames need no stream
 // operation between their kernels.
-__device__ __forceinline__ void gc_commit(const DevState &S, const FrameDev &F, int mode, bool halted) {
+__device__ __forceinline__ void gc_commit(const DevState &S, const FrameDev &F, int mode, bool halted,
+                                          Counters &s_c /* shared scratch: the last CTA's copy of the counter block */) {
   __shared__ int s_last;
-  __shared__ __align__(16) Counters s_c;   // the last CTA's copy of the counter block
   Counters *ctr = S.ctr;
   if (threadIdx.x == 0) {
     int last = 0;
@@ -1783,8 +1783,9 @@ __device__ __forceinline__ uint16_t gc_entry(int k, int sl) { return (uint16_t)(
 //    by the next frame's k_collect (or k_flush_fallbacks).
 // G_COMMIT: the last CTA folds the per-call deltas into the pool counters.
 constexpr int kGW = 4;
+constexpr int kGV = 1;   // surviving vertices per thread per normals pass
 
-__global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDev F,
+__global__ void __launch_bounds__(kGT, 8) k_gc_normals(DevState S, const FrameDev F,
                                                    const int32_t *__restrict__ list,
                                                    const int32_t *__restrict__ count_ptr,
                                                    int count_const, int mode) {
@@ -1794,6 +1795,13 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
   Counters *ctr = S.ctr;
   __shared__ int s_pro[5];
   __shared__ int s_shp[kHaloShards + 1];   // G_SHARDED: prefix of the shard fills
+  // the CTA's slot list (gc_entry): occupied slots, compacted in place to the
+  // surviving ones, then the failed-gradient ones, then the records applied
+  // inline -- each pass reads a chunk, syncs, and only then appends (an append
+  // never passes the entries read so far), so one list serves all four and the
+  // CTA fits 8 per SM
+  __shared__ __align__(16) uint16_t s_la[kGW * kEV];
+  static_assert(sizeof(s_la) >= sizeof(Counters), "gc_commit's scratch");
   const bool sharded = (mode & G_SHARDED) != 0;
   // prologue: warp 0 issues every load at once (halt flags and counts on
   // lane 0, the halo shard fills on all lanes), one round trip
@@ -1850,7 +1858,7 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
     cudaTriggerProgrammaticLaunchCompletion();
   }
   if (s_pro[0]) {   // halted frame: no work, but the commit still publishes
-    gc_commit(S, F, mode, true);
+    gc_commit(S, F, mode, true, *reinterpret_cast<Counters *>(s_la));
     return;
   }
   const int live_items = (mode & G_REQUIRE_ITEMS) ? s_pro[1] : 1;
@@ -1870,8 +1878,6 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
     cp_async16(&s_rr[2], rec_ranges + 2, true);
   }
   __shared__ GcItem G[kGW];
-  __shared__ uint16_t s_la[kGW * kEV];   // occupied slots, then the failed-gradient ones (gc_entry)
-  __shared__ uint16_t s_lv[kGW * kEV];   // surviving slots
   __shared__ int s_nocc, s_nv, s_nfb, s_nin;
   __shared__ int red[4 * kGW];
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
@@ -2084,8 +2090,9 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
         }
       }
       if (normals) {
+        __syncthreads();   // (the chunk is read: appends stay below it)
         const int pos = smem_append(keep ? 1 : 0, &s_nv);
-        if (keep) s_lv[pos] = e;
+        if (keep) s_la[pos] = e;
       }
     }
     __syncthreads();
@@ -2098,14 +2105,14 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
       // the surviving vertices, whole CTA, two per thread per pass (their 24
       // tsdf loads in flight together)
       const int nv = s_nv;
-      for (int p0 = 0; p0 < nv; p0 += 2 * kGT) {
-        double v[2][12];
-        int slv[2], itv[2], hv[2];
-        bool val[2];
+      for (int p0 = 0; p0 < nv; p0 += kGV * kGT) {
+        double v[kGV][12];
+        int slv[kGV], itv[kGV], hv[kGV];
+        bool val[kGV];
 #pragma unroll
-        for (int u = 0; u < 2; u++) {
+        for (int u = 0; u < kGV; u++) {
           const int p = p0 + u * kGT + t;
-          const uint16_t e = p < nv ? s_lv[p] : (uint16_t)0;
+          const uint16_t e = p < nv ? s_la[p] : (uint16_t)0;
           const int k = e >> 11;
           itv[u] = k;
           slv[u] = p < nv ? (e & 2047) : -1;
@@ -2137,8 +2144,9 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
           }
           val[u] = ok;
         }
+        __syncthreads();   // (the chunk's entries are read: failure appends stay below them)
 #pragma unroll
-        for (int u = 0; u < 2; u++) {
+        for (int u = 0; u < kGV; u++) {
           if (slv[u] < 0) continue;
           const GcItem &J = G[itv[u]];
           const int sl = slv[u];
@@ -2167,7 +2175,7 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
               dst[0] = 0.0; dst[1] = 0.0; dst[2] = 0.0;
             }
             fallbacks += J.R.owned;
-            s_la[atomicAdd(&s_nfb, 1)] = gc_entry(itv[u], sl);   // (the occupied list is spent)
+            s_la[atomicAdd(&s_nfb, 1)] = gc_entry(itv[u], sl);
           }
         }
       }
@@ -2202,6 +2210,7 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
         const int p = p0 + t;
         const bool has = p < nfb;
         const uint16_t e = has ? s_la[p] : (uint16_t)0;
+        __syncthreads();   // (the chunk is read: inline appends stay below it)
         const int bb = G[e >> 11].R.b, sl = e & 2047;
         const int h = has ? S.vh[(size_t)bb * kEV + sl] : 0;   // (requested before the reservation)
         const unsigned bal = __ballot_sync(0xffffffffu, has);
@@ -2213,11 +2222,11 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
         uint32_t types4, cand;
         fb_record(e, types4, cand);
         if (at < S.fb_cap) S.fallback[at] = make_int4(bb, sl | (int)(cand << 11), (int)types4, h);
-        else s_lv[atomicAdd(&s_nin, 1)] = e;   // (the surviving list is spent)
+        else s_la[atomicAdd(&s_nin, 1)] = e;
       }
       __syncthreads();
       for (int q = w; q < s_nin; q += kGW) {   // ring full: inline, one warp per record
-        const uint16_t e = s_lv[q];
+        const uint16_t e = s_la[q];
         const GcItem &J = G[e >> 11];
         const int sl = e & 2047;
         uint32_t types4, cand;
@@ -2256,7 +2265,7 @@ __global__ void __launch_bounds__(kGT, 5) k_gc_normals(DevState S, const FrameDe
       }
     }
   }
-  gc_commit(S, F, mode, false);
+  gc_commit(S, F, mode, false, *reinterpret_cast<Counters *>(s_la));   // (the lists are spent)
   trace_span(S, 3, F.frame, true);
   trace_at(S, TK_GC, 31);
 }
