@@ -668,6 +668,15 @@ __device__ __forceinline__ int floor_div_exact(double p, double e, double inv_e)
   if (r > 1e-7 && r < 1.0 - 1e-7) return (int)f;
   return (int)floor(p / e);
 }
+// its common case alone: floor(RN(p * RN(1/e))); `near` is set when q lies
+// within 1e-7 of an integer (the caller then takes floor(p / e))
+__device__ __forceinline__ int floor_div_fast(double p, double inv_e, bool &near) {
+  const double q = __dmul_rn(p, inv_e);
+  const double f = floor(q);
+  const double r = q - f;   // exact
+  near |= !(r > 1e-7 && r < 1.0 - 1e-7);
+  return (int)f;
+}
 
 // out_j = fma(a2, B[2][j], fma(a1, B[1][j], a0*B[0][j])) -- numpy `a @ B`
 __device__ __forceinline__ double matvec_col(const double *a, const double *B, int j) {

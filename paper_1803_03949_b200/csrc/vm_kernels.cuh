@@ -598,13 +598,24 @@ __global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, cons
       for (int i = 0; i < nsteps; i++) {
         unsigned long long key = kNoKey;
         int c[3] = {0, 0, 0};
+        double pw[3];
+        bool near = false;   // a coordinate within 1e-7 blocks of a block face: divide exactly
         if (valid[k]) {
           const double sv = (i == nsteps - 1) ? 1.0 : __dadd_rn(__dmul_rn((double)i, step), -1.0);
           const double f = __dadd_rn(1.0, __dmul_rn(sv, delta));
-          for (int j = 0; j < 3; j++)
-            c[j] = floor_div_exact(__dadd_rn(F.t[j], __dmul_rn(qs[j], f)), S.extent, S.inv_extent);
-          if (!multi || block_relevant(S, c[0], c[1], c[2])) key = (unsigned long long)pack_coord(c[0], c[1], c[2]);
+#pragma unroll
+          for (int j = 0; j < 3; j++) {
+            pw[j] = __dadd_rn(F.t[j], __dmul_rn(qs[j], f));
+            c[j] = floor_div_fast(pw[j], S.inv_extent, near);
+          }
         }
+        // (warp-uniform branch: the correctly rounded divisions run only in the
+        // rare warps that need them instead of predicated in every sample)
+        if (__any_sync(0xffffffffu, near) && near)
+#pragma unroll
+          for (int j = 0; j < 3; j++) c[j] = (int)floor(pw[j] / S.extent);
+        if (valid[k] && (!multi || block_relevant(S, c[0], c[1], c[2])))
+          key = (unsigned long long)pack_coord(c[0], c[1], c[2]);
         if (!__any_sync(0xffffffffu, key != kNoKey)) continue;
         const unsigned grp = __match_any_sync(0xffffffffu, key);
         if (direct) {   // (rare) the set overflowed: probe the table directly
@@ -624,7 +635,9 @@ __global__ void __launch_bounds__(kCollectThreads, 5) k_collect(DevState S, cons
           unsigned h = cset_hash(key);
           bool placed = false;
           for (int probe = 0; probe < 32 && !placed; probe++, h = (h + 1) & (kCSet - 1)) {
-            const unsigned long long old = atomicCAS(&s_key[h], kNoKey, key);
+            // (a plain read first: most probes meet the key already listed)
+            unsigned long long old = *reinterpret_cast<volatile unsigned long long *>(&s_key[h]);
+            if (old == kNoKey) old = atomicCAS(&s_key[h], kNoKey, key);
             if (old == kNoKey) s_list[atomicAdd(&s_n, 1)] = (uint16_t)h;
             placed = old == kNoKey || old == key;
           }
@@ -1631,7 +1644,7 @@ __device__ __forceinline__ void clear_requests(uint8_t *p) {
 
 
 // ------------------------------------------------------------ GC + normals
-constexpr int kGT = 128;  // threads per CTA of k_gc_normals (kGW warps, one halo block each)
+constexpr int kGT = 128;  // threads per CTA of k_gc_normals (warps 0..kGW-1 stage a halo block each)
 // type tile over cube locals -1..7: 81 columns (lx, ly) of 16 bytes, z = 0..7
 // at bytes 0..7 and z = -1 at byte 15 (the -z neighbour's z = 7, fetched as
 // the aligned word of its z = 4..7 into bytes 12..15)
@@ -1783,6 +1796,7 @@ __device__ __forceinline__ uint16_t gc_entry(int k, int sl) { return (uint16_t)(
 //    by the next frame's k_collect (or k_flush_fallbacks).
 // G_COMMIT: the last CTA folds the per-call deltas into the pool counters.
 constexpr int kGW = 4;
+constexpr int kGWarps = kGT / 32;   // (the CTA's warps: all share the slot work)
 constexpr int kGV = 1;   // surviving vertices per thread per normals pass
 
 __global__ void __launch_bounds__(kGT, 8) k_gc_normals(DevState S, const FrameDev F,
@@ -1879,9 +1893,9 @@ __global__ void __launch_bounds__(kGT, 8) k_gc_normals(DevState S, const FrameDe
   }
   __shared__ GcItem G[kGW];
   __shared__ int s_nocc, s_nv, s_nfb, s_nin;
-  __shared__ int red[4 * kGW];
+  __shared__ int red[4 * kGWarps];
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  GcItem &I = G[w];
+  GcItem &I = G[w < kGW ? w : 0];   // (warps past kGW stage nothing)
   const bool normals = (mode & G_NORMALS) != 0;
   FrameDev Fr = F;
   Fr.scope_mode = 1;   // resolve as explicit items: no slab bits
@@ -1895,7 +1909,7 @@ __global__ void __launch_bounds__(kGT, 8) k_gc_normals(DevState S, const FrameDe
     // (the kGW blocks of a CTA are a grid apart in the list: neighbouring list
     // entries are neighbouring blocks of similar surface density)
     const int i = base + w * (int)gridDim.x + blockIdx.x;
-    {
+    if (w < kGW) {
       int bi = -1;
       if (i < nsh) {   // shard k holds flat items [s_shp[k], s_shp[k + 1])
         int k = 0;
@@ -1911,7 +1925,7 @@ __global__ void __launch_bounds__(kGT, 8) k_gc_normals(DevState S, const FrameDe
     }
     if (t == 0) { s_nocc = 0; s_nv = 0; s_nfb = 0; s_nin = 0; }
     __syncwarp();
-    const bool live = I.R.mode > 0;
+    const bool live = w < kGW && I.R.mode > 0;
     const int b = I.R.b;
     if (live) {
       // stage occupancy + requests, types and halo flags (all copies in flight)
@@ -2002,7 +2016,7 @@ __global__ void __launch_bounds__(kGT, 8) k_gc_normals(DevState S, const FrameDe
       __syncthreads();
       if (t == 0) {
         int acc = 0;
-        for (int q = 0; q < kGW; q++) { const int c = red[q]; red[q] = acc; acc += c; }
+        for (int q = 0; q < kGWarps; q++) { const int c = red[q]; red[q] = acc; acc += c; }
         cp_async_wait_all();   // (s_rr)
         long long a0 = s_rr[0], e0 = s_rr[1], a1 = s_rr[2], e1 = s_rr[3];
         if ((e0 - a0) + (e1 - a1) < acc) {   // more than the CTA holds: merge its ranges' use with a new run
@@ -2225,7 +2239,7 @@ __global__ void __launch_bounds__(kGT, 8) k_gc_normals(DevState S, const FrameDe
         else s_la[atomicAdd(&s_nin, 1)] = e;
       }
       __syncthreads();
-      for (int q = w; q < s_nin; q += kGW) {   // ring full: inline, one warp per record
+      for (int q = w; q < s_nin; q += kGWarps) {   // ring full: inline, one warp per record
         const uint16_t e = s_la[q];
         const GcItem &J = G[e >> 11];
         const int sl = e & 2047;
@@ -2260,7 +2274,7 @@ __global__ void __launch_bounds__(kGT, 8) k_gc_normals(DevState S, const FrameDe
       for (int k = 0; k < 4; k++) {
         long long r = 0;
 #pragma unroll
-        for (int q = 0; q < kGW; q++) r += red[q * 4 + k];
+        for (int q = 0; q < kGWarps; q++) r += red[q * 4 + k];
         if (r) atomicAdd((unsigned long long *)dst[k], (unsigned long long)r);
       }
     }
