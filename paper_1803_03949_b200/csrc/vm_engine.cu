@@ -749,12 +749,14 @@ int vm_create(const vm_store_config *cfg, vm_engine **out) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_retype_place, kNT, kRetypeSmem));
     e->grid_retype = std::max(1, occ) * e->sm_count;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gc_normals, kGT, kGcSmem));
+    if (const char *g = getenv("VOXMESH_B200_GC_CTAS_PER_SM")) occ = std::min(occ, atoi(g));   // (A/B knob)
     e->grid_gc = std::max(1, occ) * e->sm_count;
     S.rec_chunk_ctas = e->grid_gc;
     TRY(dev_alloc(&S.rec_chunk, 4 * (size_t)S.rec_chunk_ctas, 0));   // (two empty record ranges per CTA)
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fuse_blocks, kFB, 0));
     e->grid_fuse = std::max(1, occ) * e->sm_count;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_collect, kCollectThreads, 0));
+    if (const char *g = getenv("VOXMESH_B200_COLLECT_CTAS_PER_SM")) occ = std::min(occ, atoi(g));   // (A/B knob)
     e->grid_collect = std::max(1, occ) * e->sm_count;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_place_parity, kNT, 0));
     e->grid_parity = std::max(1, occ) * e->sm_count;
