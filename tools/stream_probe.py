@@ -20,10 +20,10 @@ from paper_1803_03949_b200 import Engine, RunConfig, _lib  # noqa: E402
 from paper_1803_03949_b200.synth import config_spec  # noqa: E402
 
 W, N = 5, 295
-spec, cfg = config_spec("C2")
+spec, cfg = config_spec(os.environ.get("VM_CONFIG", "C2"))
 dev = torch.device("cuda", 0)
 poses, depths = bench.make_frames(spec, W + N, dev)
-caps = dict(block_capacity=30_000, vertex_capacity=12_000_000)
+caps = dict(block_capacity=int(os.environ.get("VM_BLOCKS", 30_000)), vertex_capacity=int(os.environ.get("VM_RECORDS", 12_000_000)))
 
 
 def run(label, bare):
