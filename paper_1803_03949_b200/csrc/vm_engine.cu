@@ -2455,14 +2455,23 @@ int vm_audit(vm_engine *e, vm_audit_report *out) {
     k_audit<<<grid_threads(e, (long long)c.nblocks * kEV, 256), 256, 0, e->stream>>>(e->S, c.nblocks, sums);
     TRY(check_launch());
   }
+  int32_t *claims = nullptr;   // vertex-record ownership: one holder per record handed out
+  if (c.a_hw > 0) {
+    CK(cudaMalloc(&claims, (size_t)c.a_hw * sizeof(int32_t)));
+    CK(cudaMemsetAsync(claims, 0, (size_t)c.a_hw * sizeof(int32_t), e->stream));
+    k_audit_records<<<grid_threads(e, std::max<long long>((long long)c.nblocks * kEV, 2LL * e->S.rec_chunk_ctas), 256),
+                      256, 0, e->stream>>>(e->S, c.nblocks, c.a_hw, claims, sums + 4);
+    TRY(check_launch());
+  }
   unsigned long long h[8];
   CK(cudaMemcpyAsync(h, sums, 64, cudaMemcpyDeviceToHost, e->stream));
   CK(cudaStreamSynchronize(e->stream));
   cudaFree(sums);
+  if (claims) cudaFree(claims);
   out->vertices_live = c.v_live;
   out->triangles_live = c.t_live;
   out->refcount_mismatches = (int64_t)h[1];
-  out->duplicate_handles = 0;   // one vertex per slot by construction
+  out->duplicate_handles = (int64_t)h[4];   // (a vertex is its slot; its record has one holder)
   out->zero_ref_live = (int64_t)h[2];
   out->conservation_ok = ((int64_t)h[0] == c.v_live) && ((int64_t)h[3] == c.t_live) &&
                          (c.v_count >= c.v_live) && (c.t_count >= c.t_live);

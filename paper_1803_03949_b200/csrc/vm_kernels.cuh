@@ -2398,6 +2398,32 @@ __global__ void k_audit(DevState S, int nblocks, unsigned long long *sums) {
   }
 }
 
+// Vertex-record ownership (audit): every record handed out (< a_hw) belongs
+// to at most one holder -- a slot with its has-record bit, or a gc CTA's free
+// range.  claims[h] counts the holders; every claim past the first, and every
+// record-holding slot whose handle lies outside [0, a_hw), is counted in
+// out[0] (the report's duplicate_handles).
+__global__ void k_audit_records(DevState S, int nblocks, long long a_hw, int32_t *claims, unsigned long long *out) {
+  long long dup = 0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < (long long)nblocks * kEV; q += stride) {
+    if (!((S.vrb[q >> 5] >> (q & 31)) & 1u)) continue;
+    const long long h = S.vh[q];
+    if (h < 0 || h >= a_hw) { dup++; continue; }
+    dup += atomicAdd(claims + h, 1) > 0;
+  }
+  // the gc CTAs' free ranges [s_rr[0], s_rr[1]), [s_rr[2], s_rr[3])
+  for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < 2LL * S.rec_chunk_ctas; c += stride) {
+    const long long a = S.rec_chunk[2 * c], e = S.rec_chunk[2 * c + 1];
+    for (long long h = a; h < e; h++) {
+      if (h < 0 || h >= a_hw) { dup++; continue; }
+      dup += atomicAdd(claims + h, 1) > 0;
+    }
+  }
+  dup = warp_sum(dup);
+  if ((threadIdx.x & 31) == 0 && dup) atomicAdd(out, (unsigned long long)dup);
+}
+
 __global__ void k_refine_eval(const uint8_t *tc, const uint8_t *tp, const double *corners, int n,
                               double eps, int32_t *out) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
